@@ -1,0 +1,153 @@
+"""ctypes wrapper for the CPU oracle (oracle/masoracle.c).
+
+TEST INFRASTRUCTURE ONLY.  Only tests/, ``__graft_entry__.smoke()`` and
+bench.py's ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product package ``paper_2303_03398_b200`` never imports it.
+
+The oracle is a plain, slow, single-threaded C implementation of the PCG solve
+described in SURVEY.md section 8(c) (readings R1-R18):
+global grid, host arrays, no ranks, no blocking or fusion.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "masoracle.c")
+LIB = os.path.join(HERE, "libmasoracle.so")
+
+OK, NOT_CONVERGED, E_INVALID, E_SINGULAR, E_BREAKDOWN, E_NOMEM = 0, 1, -1, -3, -4, -7
+BC_DIRICHLET, BC_NEUMANN0 = 0, 1
+
+CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared", "-std=c99"]
+
+
+def build(force: bool = False) -> str:
+    """Compile libmasoracle.so with gcc (plain C99, no contraction, no fast-math)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        d, i = ctypes.c_void_p, ctypes.c_int
+        for name, args in {
+            "masoracle_check_grid": [i, i, i, d, d, d],
+            "masoracle_volumes": [i, i, i, d, d, d, d],
+            "masoracle_assemble": [i, i, i, d, d, d, d, d, d, d, i, i, d, d, d, d],
+            "masoracle_apply": [i, i, i, d, d, d, d, d, d],
+            "masoracle_rhs": [i, i, i, d, d, d, d, d, i, d, i, d, d],
+            "masoracle_pcg": [i, i, i, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
+        }.items():
+            fn = getattr(_lib, name)
+            fn.argtypes = args
+            fn.restype = i
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, what):
+        super().__init__(f"{what}: status {status}")
+        self.status = status
+
+
+def check_grid(rf, tf, pf) -> int:
+    rf, tf, pf = _c(rf), _c(tf), _c(pf)
+    return lib().masoracle_check_grid(rf.size - 1, tf.size - 1, pf.size - 1, _p(rf), _p(tf), _p(pf))
+
+
+def volumes(rf, tf, pf) -> np.ndarray:
+    rf, tf, pf = _c(rf), _c(tf), _c(pf)
+    nr, nt, np_ = rf.size - 1, tf.size - 1, pf.size - 1
+    V = np.empty((np_, nt, nr))
+    st = lib().masoracle_volumes(nr, nt, np_, _p(rf), _p(tf), _p(pf), _p(V))
+    if st:
+        raise OracleError(st, "volumes")
+    return V
+
+
+class Operator:
+    """Assembled oracle operator: Tr [np][nt][nr+1], Tt [np][nt+1][nr], Tp [np][nt][nr], D."""
+
+    def __init__(self, rf, tf, pf, kr, kt, kp, s, bc_in, bc_out):
+        self.rf, self.tf, self.pf = _c(rf), _c(tf), _c(pf)
+        self.nr, self.nt, self.np = self.rf.size - 1, self.tf.size - 1, self.pf.size - 1
+        nr, nt, np_ = self.nr, self.nt, self.np
+        self.bc_in, self.bc_out = int(bc_in), int(bc_out)
+        kr, kt, kp, s = _c(kr), _c(kt), _c(kp), _c(s)
+        assert kr.shape == (np_, nt, nr + 1) and kt.shape == (np_, nt + 1, nr)
+        assert kp.shape == (np_, nt, nr) and s.shape == (np_, nt, nr)
+        self.Tr = np.empty((np_, nt, nr + 1))
+        self.Tt = np.empty((np_, nt + 1, nr))
+        self.Tp = np.empty((np_, nt, nr))
+        self.D = np.empty((np_, nt, nr))
+        self.status = lib().masoracle_assemble(
+            nr, nt, np_, _p(self.rf), _p(self.tf), _p(self.pf), _p(kr), _p(kt), _p(kp), _p(s),
+            self.bc_in, self.bc_out, _p(self.Tr), _p(self.Tt), _p(self.Tp), _p(self.D))
+        if self.status:
+            raise OracleError(self.status, "assemble")
+
+    @property
+    def shape(self):
+        return (self.np, self.nt, self.nr)
+
+    def apply(self, u) -> np.ndarray:
+        u = _c(u)
+        assert u.shape == self.shape
+        y = np.empty(self.shape)
+        lib().masoracle_apply(self.nr, self.nt, self.np, _p(self.Tr), _p(self.Tt), _p(self.Tp),
+                              _p(self.D), _p(u), _p(y))
+        return y
+
+    def rhs(self, f, g_in=None, g_out=None) -> np.ndarray:
+        f = _c(f)
+        b = np.empty(self.shape)
+        st = lib().masoracle_rhs(self.nr, self.nt, self.np, _p(self.rf), _p(self.tf), _p(self.pf),
+                                 _p(self.Tr), _p(f), self.bc_in, _p(_c(g_in)), self.bc_out,
+                                 _p(_c(g_out)), _p(b))
+        if st:
+            raise OracleError(st, "rhs")
+        return b
+
+    def pcg(self, b, x0, tol, maxit):
+        """Returns (status, x, iters, hist[0..iters], bnorm, rnorm)."""
+        b = _c(b)
+        x = np.array(_c(x0), copy=True)
+        hist = np.zeros(maxit + 1)
+        iters = ctypes.c_int(0)
+        bn, rn = ctypes.c_double(0), ctypes.c_double(0)
+        st = lib().masoracle_pcg(self.nr, self.nt, self.np, _p(self.Tr), _p(self.Tt), _p(self.Tp),
+                                 _p(self.D), _p(b), _p(x), float(tol), int(maxit), _p(hist),
+                                 ctypes.byref(iters), ctypes.byref(bn), ctypes.byref(rn))
+        return st, x, iters.value, hist[: iters.value + 1].copy(), bn.value, rn.value
+
+
+def solve_problem(prob, tol=None, maxit=None, x0=None):
+    """Solve an ``inputs.Problem`` covering the whole global grid (k0 = 0, nloc = np)."""
+    assert prob.k0 == 0 and prob.nloc == prob.np, "the oracle works on the global grid"
+    op = Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
+    b = op.rhs(prob.f, prob.g_in, prob.g_out)
+    st, x, iters, hist, bn, rn = op.pcg(b, prob.x0 if x0 is None else x0,
+                                        prob.tol if tol is None else tol,
+                                        prob.maxit if maxit is None else maxit)
+    return dict(status=st, x=x, iters=iters, hist=hist, bnorm=bn, rnorm=rn, op=op, b=b)

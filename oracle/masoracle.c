@@ -1,0 +1,400 @@
+/*
+ * masoracle.c -- plain, slow, sequential CPU ORACLE for the MAS implicit
+ * parabolic PCG solve (arXiv 2303.03398).  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * "--impl reference" legs may load this library.  The product path
+ * (paper_2303_03398_b200/, libmaspcg.so) never includes, links or calls it,
+ * and this file includes nothing from the product tree.
+ *
+ * What it follows.  PAPER.md gives no solver mathematics.  It fixes only:
+ *   - "a logically rectangular non-uniform staggered spherical grid and
+ *     finite-difference discretizations with a combination of explicit and
+ *     implicit time-stepping methods"; "highly memory-bound"
+ *     (Sec. III "The MAS Solar MHD Model");
+ *   - a "stretched grid" test case of 36 M cells (Sec. V-A);
+ *   - "viscosity solver iterations" with MPI halo exchanges
+ *     (Sec. V-C, Fig. 4);
+ *   - validation "to within solver tolerances".
+ * BASELINE.json north_star fixes the rest: a symmetric 7-point spherical-metric
+ * diffusion operator, point-Jacobi preconditioned CG, fp64.  Every formula
+ * below is therefore a READING, numbered R1..R18 exactly as in SURVEY.md
+ * section 8(c) and restated in DESIGN.md section 3; each function cites the
+ * reading(s) it writes out.
+ *
+ * Style: triple loops in [k][j][i] order (phi outermost, r contiguous,
+ * PAPER.md:128-139 Listing 1 with i fastest), left-to-right sums, no blocking,
+ * no fusion, no reordering.  Built with -O2 -fno-fast-math -ffp-contract=off so
+ * every product and sum is one IEEE fp64 rounding, in the order written.
+ *
+ * Pins (tests/test_oracle_pins.py, -m "not gpu"): sum of V closed form; sphere
+ * r-face areas; K*1 = 0 (annihilates constants); x.Ay = y.Ax; telescoping
+ * flux sum; dense LU on tiny grids; manufactured solution second order;
+ * spherical-capacitor closed form; Dirichlet-constant and shift-only exact
+ * cases; circulant phi ring vs FFT with the CG iteration bound; a hand-worked
+ * two-cell golden fixture (tests/golden/).  Parity status: every function is
+ * pinned; the residual HISTORY beyond ~800-1000 iterations on high-contrast
+ * inputs is "parity unpinned" (SURVEY.md 8(c) contract (iii)).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define MO_OK 0
+#define MO_NOT_CONVERGED 1
+#define MO_E_INVALID (-1)
+#define MO_E_SINGULAR (-3)
+#define MO_E_BREAKDOWN (-4)
+#define MO_E_NOMEM (-7)
+
+#define MO_BC_DIRICHLET 0
+#define MO_BC_NEUMANN0 1
+
+/* R9: periodic phi, full 2*pi span.  The period used in h^phi is this literal. */
+static const double MO_TWO_PI = 6.283185307179586476925286766559;
+
+#define IDX(k, j, i, nt_, nr_) ((((size_t)(k)) * (size_t)(nt_) + (size_t)(j)) * (size_t)(nr_) + (size_t)(i))
+
+/* ---------------------------------------------------------------- grid (R1,R2,R3) */
+
+/* Grid validity (R1, R9): r_f[0] > 0, all faces strictly increasing,
+ * t_f within [0, pi], p_f span equal to 2*pi to 1e-12 relative. */
+int masoracle_check_grid(int nr, int nt, int np, const double *rf, const double *tf,
+                         const double *pf) {
+    if (nr < 1 || nt < 1 || np < 1) return MO_E_INVALID;
+    if (!(rf[0] > 0.0)) return MO_E_INVALID;
+    for (int i = 0; i < nr; i++) if (!(rf[i + 1] > rf[i])) return MO_E_INVALID;
+    for (int j = 0; j < nt; j++) if (!(tf[j + 1] > tf[j])) return MO_E_INVALID;
+    for (int k = 0; k < np; k++) if (!(pf[k + 1] > pf[k])) return MO_E_INVALID;
+    if (!(tf[0] >= 0.0) || !(tf[nt] <= 3.14159265358979323846)) return MO_E_INVALID;
+    if (!(fabs((pf[np] - pf[0]) - MO_TWO_PI) <= 1e-12 * MO_TWO_PI)) return MO_E_INVALID;
+    return MO_OK;
+}
+
+/* One-dimensional grid quantities (readings R1-R3):
+ *   centres are arithmetic midpoints of the faces (R2);
+ *   h^r_0 = rc_0 - r_f[0], h^r_i = rc_i - rc_{i-1}, h^r_nr = r_f[nr] - rc_{nr-1};
+ *   h^t_j = tc_j - tc_{j-1} (j = 1..nt-1);
+ *   h^p_k = pc_{k+1} - pc_k, h^p_{np-1} = pc_0 + 2pi - pc_{np-1} (R9);
+ *   R3_i = (r_f[i+1]^3 - r_f[i]^3)/3 = dr_i (r_f[i+1]^2 + r_f[i+1] r_f[i] + r_f[i]^2)/3,
+ *   C_j = 2 sin(tc_j) sin(dt_j/2)
+ *   (= cos t_f[j] - cos t_f[j+1], the exact integral of sin, written in its
+ *   product form, R3).                                                       */
+typedef struct {
+    double *rc, *dr, *hr, *R3;       /* nr, nr, nr+1, nr */
+    double *tc, *dt, *ht, *C, *sinf_, *sinc; /* nt, nt, nt+1, nt, nt+1, nt */
+    double *pc, *dp, *hp;            /* np, np, np */
+} mo_grid;
+
+static void mo_grid_free(mo_grid *g) {
+    free(g->rc); free(g->dr); free(g->hr); free(g->R3);
+    free(g->tc); free(g->dt); free(g->ht); free(g->C); free(g->sinf_); free(g->sinc);
+    free(g->pc); free(g->dp); free(g->hp);
+}
+
+static int mo_grid_build(int nr, int nt, int np, const double *rf, const double *tf,
+                         const double *pf, mo_grid *g) {
+    memset(g, 0, sizeof(*g));
+    g->rc = malloc(sizeof(double) * nr); g->dr = malloc(sizeof(double) * nr);
+    g->hr = malloc(sizeof(double) * (nr + 1)); g->R3 = malloc(sizeof(double) * nr);
+    g->tc = malloc(sizeof(double) * nt); g->dt = malloc(sizeof(double) * nt);
+    g->ht = malloc(sizeof(double) * (nt + 1)); g->C = malloc(sizeof(double) * nt);
+    g->sinf_ = malloc(sizeof(double) * (nt + 1)); g->sinc = malloc(sizeof(double) * nt);
+    g->pc = malloc(sizeof(double) * np); g->dp = malloc(sizeof(double) * np);
+    g->hp = malloc(sizeof(double) * np);
+    if (!g->rc || !g->dr || !g->hr || !g->R3 || !g->tc || !g->dt || !g->ht || !g->C ||
+        !g->sinf_ || !g->sinc || !g->pc || !g->dp || !g->hp) {
+        mo_grid_free(g);
+        return MO_E_NOMEM;
+    }
+    for (int i = 0; i < nr; i++) {
+        g->rc[i] = 0.5 * (rf[i] + rf[i + 1]);
+        g->dr[i] = rf[i + 1] - rf[i];
+        /* (r1^3 - r0^3)/3 written as dr (r1^2 + r1 r0 + r0^2)/3: no cancellation */
+        g->R3[i] = g->dr[i] * (rf[i + 1] * rf[i + 1] + rf[i + 1] * rf[i] + rf[i] * rf[i]) / 3.0;
+    }
+    g->hr[0] = g->rc[0] - rf[0];
+    for (int i = 1; i < nr; i++) g->hr[i] = g->rc[i] - g->rc[i - 1];
+    g->hr[nr] = rf[nr] - g->rc[nr - 1];
+
+    for (int j = 0; j < nt; j++) {
+        g->tc[j] = 0.5 * (tf[j] + tf[j + 1]);
+        g->dt[j] = tf[j + 1] - tf[j];
+        g->C[j] = 2.0 * sin(g->tc[j]) * sin(0.5 * g->dt[j]);
+        g->sinc[j] = sin(g->tc[j]);
+    }
+    g->ht[0] = 0.0; g->ht[nt] = 0.0; /* boundary theta faces carry no flux (R8) */
+    for (int j = 1; j < nt; j++) g->ht[j] = g->tc[j] - g->tc[j - 1];
+    for (int j = 0; j <= nt; j++) g->sinf_[j] = sin(tf[j]);
+
+    for (int k = 0; k < np; k++) {
+        g->pc[k] = 0.5 * (pf[k] + pf[k + 1]);
+        g->dp[k] = pf[k + 1] - pf[k];
+    }
+    for (int k = 0; k + 1 < np; k++) g->hp[k] = g->pc[k + 1] - g->pc[k];
+    g->hp[np - 1] = (g->pc[0] + MO_TWO_PI) - g->pc[np - 1];
+    return MO_OK;
+}
+
+/* Cell volumes V_kji = R3_i * C_j * dphi_k (R3: exact finite-volume integral
+ * of r^2 sin(theta) dr dtheta dphi).                                        */
+int masoracle_volumes(int nr, int nt, int np, const double *rf, const double *tf,
+                      const double *pf, double *V) {
+    int st = masoracle_check_grid(nr, nt, np, rf, tf, pf);
+    if (st) return st;
+    mo_grid g;
+    if (mo_grid_build(nr, nt, np, rf, tf, pf, &g)) return MO_E_NOMEM;
+    for (int k = 0; k < np; k++)
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i < nr; i++)
+                V[IDX(k, j, i, nt, nr)] = g.R3[i] * g.C[j] * g.dp[k];
+    mo_grid_free(&g);
+    return MO_OK;
+}
+
+/* ------------------------------------------------------- operator assembly (R3-R10) */
+
+/* Face transmissibilities and diagonal:
+ *   Tr[k][j][i], i = 0..nr   : kr * r_f[i]^2 * C_j * dphi_k / h^r_i
+ *   Tt[k][j][i], j = 0..nt   : kt * sin(t_f[j]) * dr_i * dphi_k / h^t_j for
+ *                              j = 1..nt-1; 0 on the two theta-boundary faces (R8)
+ *   Tp[k][j][i], face k+1/2  : kp * dr_i * dtheta_j / (sin(tc_j) * h^p_k)
+ *   D = s*V + Tr_lo + Tr_hi + Tt_lo + Tt_hi + Tp_lo + Tp_hi   (left to right)
+ * where the r-boundary faces enter D only when that side is Dirichlet (R7),
+ * and Tp_lo of plane k is the face (k-1 mod np)+1/2 (R9).  Input face
+ * coefficients kr [np][nt][nr+1], kt [np][nt+1][nr], kp [np][nt][nr] and the
+ * shift s [np][nt][nr] are taken as given (R4, R5).  Returns E_INVALID for a
+ * negative or non-finite coefficient, E_SINGULAR when s == 0 everywhere and
+ * neither r boundary is Dirichlet (R10 / operator definiteness).            */
+int masoracle_assemble(int nr, int nt, int np, const double *rf, const double *tf,
+                       const double *pf, const double *kr, const double *kt,
+                       const double *kp, const double *s, int bc_in, int bc_out,
+                       double *Tr, double *Tt, double *Tp, double *D) {
+    int st = masoracle_check_grid(nr, nt, np, rf, tf, pf);
+    if (st) return st;
+    if ((bc_in != MO_BC_DIRICHLET && bc_in != MO_BC_NEUMANN0) ||
+        (bc_out != MO_BC_DIRICHLET && bc_out != MO_BC_NEUMANN0))
+        return MO_E_INVALID;
+    size_t ncell = (size_t)nr * nt * np;
+    size_t nkr = (size_t)(nr + 1) * nt * np, nkt = (size_t)nr * (nt + 1) * np;
+    for (size_t c = 0; c < nkr; c++) if (!(kr[c] >= 0.0) || !isfinite(kr[c])) return MO_E_INVALID;
+    for (size_t c = 0; c < nkt; c++) if (!(kt[c] >= 0.0) || !isfinite(kt[c])) return MO_E_INVALID;
+    for (size_t c = 0; c < ncell; c++) {
+        if (!(kp[c] >= 0.0) || !isfinite(kp[c])) return MO_E_INVALID;
+        if (!(s[c] >= 0.0) || !isfinite(s[c])) return MO_E_INVALID;
+    }
+    int any_shift = 0;
+    for (size_t c = 0; c < ncell; c++) if (s[c] > 0.0) any_shift = 1;
+    if (!any_shift && bc_in != MO_BC_DIRICHLET && bc_out != MO_BC_DIRICHLET)
+        return MO_E_SINGULAR;
+
+    mo_grid g;
+    if (mo_grid_build(nr, nt, np, rf, tf, pf, &g)) return MO_E_NOMEM;
+
+    for (int k = 0; k < np; k++)
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i <= nr; i++) {
+                size_t f = IDX(k, j, i, nt, nr + 1);
+                Tr[f] = kr[f] * (rf[i] * rf[i]) * g.C[j] * g.dp[k] / g.hr[i];
+            }
+    for (int k = 0; k < np; k++)
+        for (int j = 0; j <= nt; j++)
+            for (int i = 0; i < nr; i++) {
+                size_t f = IDX(k, j, i, nt + 1, nr);
+                if (j == 0 || j == nt)
+                    Tt[f] = 0.0;
+                else
+                    Tt[f] = kt[f] * g.sinf_[j] * g.dr[i] * g.dp[k] / g.ht[j];
+            }
+    for (int k = 0; k < np; k++)
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i < nr; i++) {
+                size_t c = IDX(k, j, i, nt, nr);
+                Tp[c] = kp[c] * g.dr[i] * g.dt[j] / (g.sinc[j] * g.hp[k]);
+            }
+    for (int k = 0; k < np; k++) {
+        int km = (k + np - 1) % np;
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i < nr; i++) {
+                size_t c = IDX(k, j, i, nt, nr);
+                double V = g.R3[i] * g.C[j] * g.dp[k];
+                double trlo = Tr[IDX(k, j, i, nt, nr + 1)];
+                double trhi = Tr[IDX(k, j, i + 1, nt, nr + 1)];
+                if (i == 0 && bc_in != MO_BC_DIRICHLET) trlo = 0.0;
+                if (i == nr - 1 && bc_out != MO_BC_DIRICHLET) trhi = 0.0;
+                double ttlo = Tt[IDX(k, j, i, nt + 1, nr)];
+                double tthi = Tt[IDX(k, j + 1, i, nt + 1, nr)];
+                double tplo = Tp[IDX(km, j, i, nt, nr)];
+                double tphi = Tp[c];
+                double d = s[c] * V;
+                d = d + trlo;
+                d = d + trhi;
+                d = d + ttlo;
+                d = d + tthi;
+                d = d + tplo;
+                d = d + tphi;
+                D[c] = d;
+            }
+    }
+    mo_grid_free(&g);
+    return MO_OK;
+}
+
+/* ------------------------------------------------------------------ apply (R4) */
+
+/* y = A u with (A u)_c = D_c u_c - sum over the interior faces f of c of
+ * T_f u_nb(f), summed in the reference order
+ *   r_lo, r_hi, theta_lo, theta_hi, phi_lo, phi_hi.
+ * r-boundary faces have no neighbour (their Dirichlet part lives in D);
+ * theta-boundary faces carry no flux; phi wraps periodically (R9).          */
+int masoracle_apply(int nr, int nt, int np, const double *Tr, const double *Tt,
+                    const double *Tp, const double *D, const double *u, double *y) {
+    for (int k = 0; k < np; k++) {
+        int km = (k + np - 1) % np, kp1 = (k + 1) % np;
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i < nr; i++) {
+                size_t c = IDX(k, j, i, nt, nr);
+                double sum = 0.0;
+                if (i > 0) sum = sum + Tr[IDX(k, j, i, nt, nr + 1)] * u[IDX(k, j, i - 1, nt, nr)];
+                if (i < nr - 1) sum = sum + Tr[IDX(k, j, i + 1, nt, nr + 1)] * u[IDX(k, j, i + 1, nt, nr)];
+                if (j > 0) sum = sum + Tt[IDX(k, j, i, nt + 1, nr)] * u[IDX(k, j - 1, i, nt, nr)];
+                if (j < nt - 1) sum = sum + Tt[IDX(k, j + 1, i, nt + 1, nr)] * u[IDX(k, j + 1, i, nt, nr)];
+                sum = sum + Tp[IDX(km, j, i, nt, nr)] * u[IDX(km, j, i, nt, nr)];
+                sum = sum + Tp[c] * u[IDX(kp1, j, i, nt, nr)];
+                y[c] = D[c] * u[c] - sum;
+            }
+    }
+    return MO_OK;
+}
+
+/* -------------------------------------------------------------------- rhs (R5, R7) */
+
+/* b = V f + [i = 0, Dirichlet] Tr_0 g_in + [i = nr-1, Dirichlet] Tr_nr g_out
+ * (the boundary value sits on the face).  f is the
+ * per-unit-volume right-hand side [np][nt][nr]; g_in, g_out are [np][nt] or
+ * NULL for zero.                                                            */
+int masoracle_rhs(int nr, int nt, int np, const double *rf, const double *tf,
+                  const double *pf, const double *Tr, const double *f, int bc_in,
+                  const double *g_in, int bc_out, const double *g_out, double *b) {
+    int st = masoracle_check_grid(nr, nt, np, rf, tf, pf);
+    if (st) return st;
+    mo_grid g;
+    if (mo_grid_build(nr, nt, np, rf, tf, pf, &g)) return MO_E_NOMEM;
+    for (int k = 0; k < np; k++)
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i < nr; i++) {
+                size_t c = IDX(k, j, i, nt, nr);
+                double V = g.R3[i] * g.C[j] * g.dp[k];
+                double v = V * f[c];
+                if (i == 0 && bc_in == MO_BC_DIRICHLET && g_in)
+                    v = v + Tr[IDX(k, j, 0, nt, nr + 1)] * g_in[(size_t)k * nt + j];
+                if (i == nr - 1 && bc_out == MO_BC_DIRICHLET && g_out)
+                    v = v + Tr[IDX(k, j, nr, nt, nr + 1)] * g_out[(size_t)k * nt + j];
+                b[c] = v;
+            }
+    mo_grid_free(&g);
+    return MO_OK;
+}
+
+/* --------------------------------------------------------------- PCG (R6, R11-R14) */
+
+static double mo_dot(size_t n, const double *a, const double *b) {
+    double s = 0.0;
+    for (size_t c = 0; c < n; c++) s = s + a[c] * b[c];
+    return s;
+}
+
+/* Point-Jacobi PCG, Hestenes-Stiefel form with Fletcher-Reeves beta
+ * (R6, R11-R14):
+ *   r0 = b - A x0; z0 = r0/D; p0 = z0; rho0 = r0.z0; bn = ||b||; hist[0] = ||r0||
+ *   bn == 0 -> x = 0, OK, iters 0;   hist[0] <= tol*bn -> OK, iters 0
+ *   for k = 1..maxit:
+ *     q = A p; pi = p.q; pi <= 0 or non-finite -> E_BREAKDOWN
+ *     alpha = rho/pi; x += alpha p; r -= alpha q; hist[k] = ||r||
+ *     hist[k] <= tol*bn -> OK, iters k
+ *     z = r/D; rho' = r.z; beta = rho'/rho; rho = rho'; p = z + beta p
+ *   NOT_CONVERGED, iters = maxit.
+ * Norms are unweighted Euclidean norms of the volume-weighted system; hist is
+ * the recurrence residual.  Non-finite ||b|| or hist -> E_BREAKDOWN.
+ * hist must hold maxit+1 doubles (or be NULL).                               */
+int masoracle_pcg(int nr, int nt, int np, const double *Tr, const double *Tt,
+                  const double *Tp, const double *D, const double *b, double *x,
+                  double tol, int maxit, double *hist, int *iters, double *bnorm,
+                  double *rnorm) {
+    size_t n = (size_t)nr * nt * np;
+    if (maxit < 0 || !(tol >= 0.0)) return MO_E_INVALID;
+    *iters = 0;
+    double bn = sqrt(mo_dot(n, b, b));
+    *bnorm = bn;
+    if (!isfinite(bn)) { *rnorm = bn; return MO_E_BREAKDOWN; }
+    if (bn == 0.0) {
+        for (size_t c = 0; c < n; c++) x[c] = 0.0;
+        if (hist) hist[0] = 0.0;
+        *rnorm = 0.0;
+        return MO_OK;
+    }
+    double *r = malloc(sizeof(double) * n), *z = malloc(sizeof(double) * n);
+    double *p = malloc(sizeof(double) * n), *q = malloc(sizeof(double) * n);
+    if (!r || !z || !p || !q) { free(r); free(z); free(p); free(q); return MO_E_NOMEM; }
+    int status = MO_NOT_CONVERGED;
+
+    masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, x, q);
+    for (size_t c = 0; c < n; c++) r[c] = b[c] - q[c];
+    for (size_t c = 0; c < n; c++) z[c] = r[c] / D[c];
+    for (size_t c = 0; c < n; c++) p[c] = z[c];
+    double rho = mo_dot(n, r, z);
+    double rn = sqrt(mo_dot(n, r, r));
+    if (hist) hist[0] = rn;
+    *rnorm = rn;
+    if (!isfinite(rn) || !isfinite(rho)) { status = MO_E_BREAKDOWN; goto done; }
+    if (rn <= tol * bn) { status = MO_OK; goto done; }
+
+    for (int k = 1; k <= maxit; k++) {
+        masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, p, q);
+        double pi = mo_dot(n, p, q);
+        if (!(pi > 0.0) || !isfinite(pi)) { status = MO_E_BREAKDOWN; break; }
+        double alpha = rho / pi;
+        for (size_t c = 0; c < n; c++) x[c] = x[c] + alpha * p[c];
+        for (size_t c = 0; c < n; c++) r[c] = r[c] - alpha * q[c];
+        rn = sqrt(mo_dot(n, r, r));
+        if (hist) hist[k] = rn;
+        *iters = k;
+        *rnorm = rn;
+        if (!isfinite(rn)) { status = MO_E_BREAKDOWN; break; }
+        if (rn <= tol * bn) { status = MO_OK; break; }
+        for (size_t c = 0; c < n; c++) z[c] = r[c] / D[c];
+        double rho_new = mo_dot(n, r, z);
+        double beta = rho_new / rho;
+        rho = rho_new;
+        for (size_t c = 0; c < n; c++) p[c] = z[c] + beta * p[c];
+    }
+done:
+    free(r); free(z); free(p); free(q);
+    return status;
+}
+
+/* Whole pipeline on the global grid: assemble (R3-R10), rhs (R5), PCG (R6,
+ * R11-R14).  x holds x0 on entry and the iterate on exit.                  */
+int masoracle_solve(int nr, int nt, int np, const double *rf, const double *tf,
+                    const double *pf, const double *kr, const double *kt, const double *kp,
+                    const double *s, int bc_in, const double *g_in, int bc_out,
+                    const double *g_out, const double *f, double *x, double tol, int maxit,
+                    double *hist, int *iters, double *bnorm, double *rnorm) {
+    size_t n = (size_t)nr * nt * np;
+    double *Tr = malloc(sizeof(double) * (size_t)(nr + 1) * nt * np);
+    double *Tt = malloc(sizeof(double) * (size_t)nr * (nt + 1) * np);
+    double *Tp = malloc(sizeof(double) * n), *D = malloc(sizeof(double) * n);
+    double *b = malloc(sizeof(double) * n);
+    int st = MO_E_NOMEM;
+    *iters = 0;
+    if (!Tr || !Tt || !Tp || !D || !b) goto out;
+    st = masoracle_assemble(nr, nt, np, rf, tf, pf, kr, kt, kp, s, bc_in, bc_out, Tr, Tt, Tp, D);
+    if (st) goto out;
+    st = masoracle_rhs(nr, nt, np, rf, tf, pf, Tr, f, bc_in, g_in, bc_out, g_out, b);
+    if (st) goto out;
+    st = masoracle_pcg(nr, nt, np, Tr, Tt, Tp, D, b, x, tol, maxit, hist, iters, bnorm, rnorm);
+out:
+    free(Tr); free(Tt); free(Tp); free(D); free(b);
+    return st;
+}
