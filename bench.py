@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the fp64 spherical-grid Jacobi-PCG parabolic solve (MAS, arXiv 2303.03398) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+    torchrun --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 --master-port P bench.py --gpus N
+
+Metric (BASELINE.json): "PCG iterations/s & matvec HBM GB/s (% of peak) at 1/2/4/8 B200".
+Workload (BASELINE.json configs[2]): the coronal-relaxation-shaped viscosity
+solve on a 150 x 300 x 600 stretched spherical grid (27.0 M cells), tol 1e-10, strong scaling over
+phi-slabs.  One STEP = the whole hot path of SURVEY.md 8(a) for one synthetic input: grid/metric
+setup (a1), coefficient assembly (a2), boundary conditions, and the PCG solve to 1e-10 (a3-a11).
+``value`` = PCG iterations of the global solve per second (one solve spans all ranks).
+
+Rank 0 prints ONE JSON line.  Timing: W untimed steps, then K steps bracketed by barrier +
+cuda.synchronize, CUDA events on the launching stream, max over ranks.  The working set
+(~2.2 GB) is far larger than the 126 MB L2, so no explicit flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG iterations/s & matvec HBM GB/s (% of peak) at 1/2/4/8 B200"
+UNIT = "PCG iterations/s"
+MATVEC_BYTES_PER_CELL = 48      # p, T_r, T_theta, T_phi, D read + q written
+ITER_BYTES_PER_CELL = 136       # a5 + a7 (56) + a10 (32)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({n for s in self.samples for n, v in zip(self.NAMES, s[2:]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def ncu_traffic_per_launch():
+    """dram__bytes_read.sum + dram__bytes_write.sum of the stencil kernel from the committed
+    `ncu --set full` summary (profiles/ncu_matvec.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_matvec.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"]), d.get("source", path)
+    except Exception:
+        return None, None
+
+
+def oracle_sample(prob, iters: int):
+    """Time the CPU oracle (as it stands, single-threaded) on the full c3 grid: setup once, then
+    `iters` PCG iterations (tol = 0).  Returns (iterations/s, seconds of CPU work, description)."""
+    import oracle
+    t0 = time.perf_counter()
+    op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
+    b = op.rhs(prob.f, prob.g_in, prob.g_out)
+    t1 = time.perf_counter()
+    op.pcg(b, prob.x0, 0.0, 0)
+    t2 = time.perf_counter()
+    op.pcg(b, prob.x0, 0.0, iters)
+    t3 = time.perf_counter()
+    per_iter = ((t3 - t2) - (t2 - t1)) / iters
+    return 1.0 / per_iter, t3 - t0, per_iter
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands on the box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2303_03398_b200 import inputs
+    oracle.build()
+    prob = inputs.make_problem(args.config)
+    op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
+    b = op.rhs(prob.f, prob.g_in, prob.g_out)
+    m = args.ref_iters
+    for _ in range(args.warmup):
+        op.pcg(b, prob.x0, 0.0, 1)
+    t0 = time.perf_counter()
+    t_setup = 0.0
+    for _ in range(args.steps):
+        ts = time.perf_counter()
+        op.pcg(b, prob.x0, 0.0, 0)
+        t_setup += time.perf_counter() - ts
+        op.pcg(b, prob.x0, 0.0, m)
+    dt = time.perf_counter() - t0
+    # each pcg(m) call repeats the r0 = b - A x0 setup, timed separately and removed
+    value = args.steps * m / (dt - 2 * t_setup) if dt > 2 * t_setup else args.steps * m / dt
+    cores = 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, paper_2303_03398_b200/inputs.py)",
+        "config": {"workload": f"{args.config} {prob.nr}x{prob.nt}x{prob.np} coronal viscosity solve (BASELINE.json configs[2])",
+                   "global_cells": prob.ncell_global, "parallelism": "none (CPU oracle, 1 thread)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"oracle/masoracle.c PCG on the full c3 grid, {m} iterations per step "
+                                   f"(tol=0), operator assembled once before timing"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--chunk", type=int, default=16)
+    ap.add_argument("--maxit", type=int, default=None, help="fixed-iteration mode (tol=0), e.g. for ncu")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-iters", type=int, default=8)
+    ap.add_argument("--stencil", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.maxit is None:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2303_03398_b200 import inputs, maspcg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+
+    # ---- synthetic input of this rank's slab (decomposition-independent generator)
+    nr, nt, np_ = inputs.CONFIGS[args.config]
+    if args.config == "c4":
+        np_ *= world
+    k0, nloc = inputs.slab_extent(np_, rank, world)
+    prob = inputs.make_problem(args.config, k0, nloc, nranks=world)
+    tol = 0.0 if args.maxit else prob.tol
+    maxit = args.maxit if args.maxit else prob.maxit
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    kr, kt, kp, s, f, x0 = (T(a) for a in (prob.kr, prob.kt, prob.kp, prob.s, prob.f, prob.x0))
+
+    S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk)
+    S.set_option(maspcg.OPT_STENCIL, args.stencil)
+    x = torch.empty_like(x0)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        S.set_grid(prob.rf, prob.tf, prob.pf)                         # a1
+        S.set_coefficients(kr, kt, kp, s)                             # a2
+        S.set_bc_r(prob.bc_in, None, prob.bc_out, None)
+        x.copy_(x0)
+        st, info, hist = S.solve(f, x, tol, maxit)                    # a3-a11
+        if st < 0:
+            raise RuntimeError(f"solve failed: {st}")
+        return info["iters"]
+
+    for _ in range(args.warmup):
+        step()
+    S.set_option(maspcg.OPT_TIMING, 1)
+    S.reset_stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            iters += step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    stats = S.stats()
+    S.set_option(maspcg.OPT_TIMING, 0)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sec = ms / 1e3
+    value = iters / sec                                 # global solve iterations (strong scaling)
+    ncell_local = prob.ncell_local
+
+    # ---- roofline of the dominant kernel (stencil_matvec_dot), CUDA events on the launching stream
+    peak, peak_src = peaks()
+    mv_ms = stats["matvec_ms"] / max(stats["matvec_launches"], 1)
+    achieved = MATVEC_BYTES_PER_CELL * ncell_local / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
+    traffic, traffic_src = ncu_traffic_per_launch()
+    kern_ms = stats["matvec_ms"] + stats["update_ms"] + stats["pupdate_ms"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "stencil_matvec_dot (k_matvec_flat)",
+                "algorithmic_bytes_per_launch": MATVEC_BYTES_PER_CELL * ncell_local,
+                "avg_launch_ms": mv_ms, "peak_source": peak_src,
+                "share_of_step": stats["matvec_ms"] / ms if ms > 0 else None,
+                "traffic_source": traffic_src}
+    per_kernel = {
+        "update_jacobi_dots_GBps": 56 * ncell_local / (stats["update_ms"] / max(stats["update_launches"], 1) * 1e-3) / 1e9
+        if stats["update_ms"] > 0 else None,
+        "p_update_GBps": 32 * ncell_local / (stats["pupdate_ms"] / max(stats["pupdate_launches"], 1) * 1e-3) / 1e9
+        if stats["pupdate_ms"] > 0 else None,
+        "iteration_GBps": ITER_BYTES_PER_CELL * ncell_local * iters / sec / 1e9 / 1.0,
+        "kernels_share_of_step": kern_ms / ms if ms > 0 else None,
+    }
+
+    # ---- end to end through the C ABI with HOST buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        hkr, hkt, hkp, hs, hf, hx0 = (pin(a) for a in (prob.kr, prob.kt, prob.kp, prob.s, prob.f, prob.x0))
+        hx = pin(prob.x0)
+        h2d = sum(a.nbytes for a in (hkr, hkt, hkp, hs, hf, hx0))
+        d2h = hx.nbytes
+
+        def step_host():
+            S.set_grid(prob.rf, prob.tf, prob.pf)
+            S.set_coefficients(hkr, hkt, hkp, hs)                    # maspcg_set_coefficients_host
+            S.set_bc_r(prob.bc_in, None, prob.bc_out, None)
+            hx[...] = hx0
+            st, info, hist = S.solve(hf, hx, tol, maxit)              # maspcg_solve_host
+            return info["iters"]
+
+        step_host()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        it_h = sum(step_host() for _ in range(args.steps))
+        torch.cuda.synchronize()
+        th = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([th], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            th = float(t.item())
+        e2e = {"value": it_h / th, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": 1e3 * th / args.steps, "api": "maspcg_set_coefficients_host + maspcg_solve_host"}
+
+    # ---- CPU baseline: the oracle as it stands on this box's host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ips, cpu_s, per_it = oracle_sample(inputs.make_problem(args.config), args.ref_iters)
+        cpu = {"value": ips, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle/masoracle.c (single-threaded C, -O2) on the full {args.config} grid: operator "
+                         f"assembly + rhs + r0 once, then {args.ref_iters} PCG iterations (tol=0); "
+                         f"{cpu_s:.1f} s of CPU work, {per_it * 1e3:.0f} ms/iteration"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, paper_2303_03398_b200/inputs.py; SURVEY 8(d) recipe)",
+            "config": {"workload": f"{args.config} {nr}x{nt}x{np_} coronal viscosity solve "
+                                   f"(BASELINE.json configs[2]), tol={tol:g}, Jacobi-PCG fp64",
+                       "global_cells": nr * nt * np_, "parallelism": f"phi-slab x{world}",
+                       "iters_per_solve": iters / args.steps, "chunk": args.chunk,
+                       "l2": "no flush: working set ~2.2 GB >> 126 MB L2",
+                       "step": "set_grid + set_coefficients + set_bc_r + solve to tol"},
+            "cell_updates_per_s": nr * nt * np_ * value,
+            "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,237 @@
+/*
+ * maspcg.h -- C ABI of the B200-native fp64 PCG solve of the implicit
+ * parabolic (viscosity / thermal-conduction) terms of the MAS solar MHD code,
+ * the hot path of arXiv 2303.03398 (Caplan, Stulajter, Linker, "Acceleration
+ * of a production Solar MHD code with Fortran standard parallelism").
+ *
+ * What the paper fixes (PAPER.md, the only source text):
+ *   PAPER.md:56  (Sec. III)   "logically rectangular non-uniform staggered
+ *                              spherical grid", "finite-difference
+ *                              discretizations", "explicit and implicit
+ *                              time-stepping", "highly memory-bound";
+ *   PAPER.md:240-246 (V-A)    36 M-cell coronal test on a stretched grid,
+ *                              validated "to within solver tolerances";
+ *   PAPER.md:282, 290-292 (V-C, Figs. 3-4)  "viscosity solver iterations"
+ *                              with GPU peer-to-peer MPI halo exchanges.
+ * Everything else -- the operator, boundary conditions, preconditioner,
+ * stopping rule -- is a READING (R1..R18 of SURVEY.md section 8(c), restated
+ * in DESIGN.md section 3); each entry point below names the readings it
+ * implements.
+ *
+ * Model.  One process per GPU; every rank calls every function in the same
+ * order (like MPI).  The global grid has nr x nt x np cells (r, theta, phi);
+ * rank p owns the phi-slab k in [p*np/P, (p+1)*np/P)  (np % P == 0).  Cell
+ * arrays are fp64, C order [k][j][i]: phi outermost, r contiguous (the
+ * Fortran array(i,j,k) of PAPER.md:128-139, Listing 1).  "nloc" below is the
+ * local number of phi planes.
+ *
+ * Operator (R1-R10).  (A u)_c = D_c u_c - sum_{interior faces f} T_f u_nb(f),
+ * the volume-weighted form of (s - div kappa grad) u = f on the spherical grid:
+ * exact finite-volume metric, face transmissibilities T = kappa * area /
+ * centre distance, zero flux through theta-boundary (pole) faces, periodic
+ * phi, Dirichlet (value on the face) or zero-flux Neumann r boundaries, and
+ * D = s V + sum of the cell's face T (Dirichlet faces included).  A is
+ * symmetric positive definite unless s == 0 and no r boundary is Dirichlet.
+ *
+ * Solver (R6, R11-R14).  Point-Jacobi preconditioned CG (M = D), Fletcher-
+ * Reeves beta, stop when ||r_k||_2 <= tol * ||b||_2 (unweighted norms of the
+ * volume-weighted system; r is the recurrence residual).  tol == 0 runs
+ * exactly maxit iterations (benchmark mode).
+ *
+ * Memory and streams.  All device memory is caller-owned: the library never
+ * calls cudaMalloc (NCCL may allocate internally).  The caller supplies a
+ * workspace of maspcg_workspace_bytes() bytes (e.g. a torch uint8 tensor).
+ * Device-pointer entry points enqueue work on the caller's stream (plus an
+ * internal communication stream joined by events) and are ordered with other
+ * work on that stream; maspcg_solve() returns after the solve has finished.
+ * "_host" entry points take host pointers (pageable or pinned) and perform the
+ * host<->device copies themselves, through workspace staging buffers.
+ *
+ * Errors.  Return codes >= 0 mean the output is valid (NOT_CONVERGED: x is
+ * the maxit-th iterate).  Codes < 0 leave outputs unspecified.  Argument
+ * errors are detected on every rank before any collective; data-dependent
+ * errors (E_SINGULAR, E_BREAKDOWN, non-finite or negative coefficients) are
+ * agreed across ranks, so all ranks return the same code.  A call made out of
+ * order returns E_STATE.  maspcg_last_error() describes the last failure.  A
+ * context is not thread-safe.  There is no CPU fallback: without an sm_100a
+ * GPU every call that touches the device returns E_CUDA.
+ */
+#ifndef MASPCG_H
+#define MASPCG_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MASPCG_API __attribute__((visibility("default")))
+#define MASPCG_NCCL_UNIQUE_ID_BYTES 128
+
+typedef struct maspcg_ctx maspcg_ctx; /* opaque, one per rank */
+
+typedef enum {
+    MASPCG_OK = 0,
+    MASPCG_NOT_CONVERGED = 1,
+    MASPCG_E_INVALID = -1,   /* bad argument, bad grid, negative / non-finite coefficient */
+    MASPCG_E_STATE = -2,     /* call out of order (e.g. solve before set_coefficients) */
+    MASPCG_E_SINGULAR = -3,  /* s == 0 everywhere and no Dirichlet r boundary */
+    MASPCG_E_BREAKDOWN = -4, /* p.Ap <= 0 or a non-finite residual during PCG */
+    MASPCG_E_CUDA = -5,
+    MASPCG_E_NCCL = -6,
+    MASPCG_E_NOMEM = -7      /* workspace too small / not set */
+} maspcg_status;
+
+typedef enum { MASPCG_BC_DIRICHLET = 0, MASPCG_BC_NEUMANN0 = 1 } maspcg_bc;
+
+typedef struct {
+    int iters;          /* PCG iterations (matvecs inside the loop; R13) */
+    double bnorm;       /* ||b||_2, global */
+    double rnorm;       /* ||r_iters||_2 (recurrence residual), global */
+    double rel_resid;   /* rnorm / bnorm (0 when bnorm == 0) */
+} maspcg_info;
+
+/* Per-context counters, accumulated since creation or the last reset. */
+typedef struct {
+    long long kernel_launches;     /* kernels of this library enqueued (graph nodes count per replay) */
+    long long solves;
+    long long iterations;          /* PCG iterations executed (sum over solves) */
+    double matvec_ms;              /* summed CUDA-event time of stencil_matvec_dot launches (timing mode) */
+    long long matvec_launches;     /* launches covered by matvec_ms */
+    double update_ms;              /* update_jacobi_dots */
+    long long update_launches;
+    double pupdate_ms;             /* p_update */
+    long long pupdate_launches;
+    double comm_ms;                /* halo + all-reduce time on the comm path (timing mode, P > 1) */
+} maspcg_stats;
+
+/* Options for maspcg_set_option(). */
+typedef enum {
+    MASPCG_OPT_CHUNK = 1,        /* PCG iterations per CUDA-graph launch (1..256, default 16) */
+    MASPCG_OPT_USE_GRAPHS = 2,   /* 1 (default): replay captured graphs; 0: eager launches */
+    MASPCG_OPT_TIMING = 3,       /* 1: CUDA events around every hot kernel (forces eager launches) */
+    MASPCG_OPT_STENCIL = 4       /* stencil kernel variant: 0 = auto (default), 1 = flat, 2 = phi-marching tiles */
+} maspcg_option;
+
+/* ---- lifetime ----------------------------------------------------------- */
+
+/* Fill `out` (MASPCG_NCCL_UNIQUE_ID_BYTES bytes, host) with a fresh NCCL
+ * unique id.  Rank 0 calls it and the caller broadcasts the bytes (e.g. with
+ * torch.distributed) before every rank calls maspcg_create. */
+MASPCG_API maspcg_status maspcg_get_unique_id(void *out);
+
+/* Create a context for rank `rank` of `nranks` on CUDA device `cuda_device`.
+ * nr, nt, np: GLOBAL cell counts (>= 1; np % nranks == 0; the local slab must
+ * hold < 2^31 cells including two halo planes).  nccl_unique_id: the 128
+ * bytes from maspcg_get_unique_id, or NULL iff nranks == 1.  Collective over
+ * all ranks when nranks > 1 (ncclCommInitRank).  *out receives the context. */
+MASPCG_API maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks,
+                                       const void *nccl_unique_id, int cuda_device,
+                                       maspcg_ctx **out);
+
+/* Release the context (and its NCCL communicator).  NULL is a no-op. */
+MASPCG_API maspcg_status maspcg_destroy(maspcg_ctx *ctx);
+
+/* Human-readable description of the last failure on this context (owned by
+ * ctx; valid until the next call).  ctx == NULL: the last create failure. */
+MASPCG_API const char *maspcg_last_error(const maspcg_ctx *ctx);
+
+/* ---- grid and memory (R1-R3, R9) --------------------------- */
+
+/* Face coordinates, HOST arrays, copied: r_faces[nr+1] (r_faces[0] > 0),
+ * t_faces[nt+1] within [0, pi], p_faces[np+1] spanning exactly 2*pi (to 1e-12
+ * relative); all strictly increasing.  Precomputes the 1-D metric on the
+ * host (centres = face midpoints, centre distances, exact FV volume and area
+ * factors).  E_INVALID on a bad grid.  May be called again (marks the
+ * coefficients stale: set_coefficients must follow). */
+MASPCG_API maspcg_status maspcg_set_grid(maspcg_ctx *ctx, const double *r_faces,
+                                         const double *t_faces, const double *p_faces);
+
+/* This rank's slab: global first plane *k0 and plane count *nloc. */
+MASPCG_API maspcg_status maspcg_local_extent(const maspcg_ctx *ctx, int *k0, int *nloc);
+
+/* Bytes of device workspace this rank needs (depends only on the sizes). */
+MASPCG_API size_t maspcg_workspace_bytes(const maspcg_ctx *ctx);
+
+/* Hand the library a device buffer of >= maspcg_workspace_bytes() bytes,
+ * 256-byte aligned, owned by the caller and kept alive until destroy (or the
+ * next set_workspace).  Operator state lives here: setting a new workspace
+ * invalidates coefficients and boundary conditions. */
+MASPCG_API maspcg_status maspcg_set_workspace(maspcg_ctx *ctx, void *dev_ptr, size_t bytes);
+
+/* ---- coefficients and boundary conditions (R3-R10) -------- */
+
+/* Face diffusion coefficients and shift of the local slab, DEVICE pointers,
+ * consumed (the caller may free them afterwards):
+ *   kr    [nloc][nt][nr+1]  r-faces i = 0..nr            (kappa >= 0)
+ *   kt    [nloc][nt+1][nr]  theta-faces j = 0..nt        (the two boundary rows are ignored)
+ *   kp    [nloc][nt][nr]    phi-face k+1/2 of each local plane k
+ *   shift [nloc][nt][nr]    s >= 0 (e.g. rho/dt for backward Euler, R5)
+ * Assembles the face transmissibilities T and s*V in library memory and
+ * fetches the phi-face below the slab from the previous rank.  Returns
+ * E_INVALID (agreed across ranks) if any value is negative or non-finite.
+ * Synchronises `cuda_stream` (the validation result is read back). */
+MASPCG_API maspcg_status maspcg_set_coefficients(maspcg_ctx *ctx, const double *kr,
+                                                 const double *kt, const double *kp,
+                                                 const double *shift, void *cuda_stream);
+/* Same, HOST pointers (copied through workspace staging; timed as e2e). */
+MASPCG_API maspcg_status maspcg_set_coefficients_host(maspcg_ctx *ctx, const double *kr,
+                                                      const double *kt, const double *kp,
+                                                      const double *shift, void *cuda_stream);
+
+/* Radial boundary conditions (R7): inner (r = r_faces[0]) and outer
+ * (r = r_faces[nr]) each DIRICHLET (value on the face; g [nloc][nt], DEVICE,
+ * copied; NULL means 0) or NEUMANN0 (zero flux; g ignored).  May precede or
+ * follow set_coefficients; D is (re)assembled lazily at the next solve/apply. */
+MASPCG_API maspcg_status maspcg_set_bc_r(maspcg_ctx *ctx, maspcg_bc inner, const double *g_inner,
+                                         maspcg_bc outer, const double *g_outer, void *cuda_stream);
+MASPCG_API maspcg_status maspcg_set_bc_r_host(maspcg_ctx *ctx, maspcg_bc inner,
+                                              const double *g_inner, maspcg_bc outer,
+                                              const double *g_outer, void *cuda_stream);
+
+/* ---- the hot path -------------------------------------- */
+
+/* Solve A x = b with b = V rhs + Dirichlet face terms (R5), by point-Jacobi
+ * PCG from the initial guess in x.
+ *   rhs  DEVICE [nloc][nt][nr], per-unit-volume source f (not modified)
+ *   x    DEVICE [nloc][nt][nr], in: x0, out: the iterate; must not alias rhs
+ *   tol  >= 0 (0: run exactly maxit iterations);  maxit >= 0
+ *   resid_hist  HOST, >= maxit+1 doubles, receives ||r_k||_2 for
+ *        k = 0..info->iters, or NULL
+ *   info HOST, or NULL
+ * Returns OK, NOT_CONVERGED, E_SINGULAR, E_BREAKDOWN (p.Ap <= 0 or non-finite
+ * data), E_STATE, E_INVALID, E_CUDA or E_NCCL; the same code on all ranks.
+ * Blocks the host until the result is known (the host polls a device flag
+ * once per CUDA-graph chunk of MASPCG_OPT_CHUNK iterations). */
+MASPCG_API maspcg_status maspcg_solve(maspcg_ctx *ctx, const double *rhs, double *x, double tol,
+                                      int maxit, double *resid_hist, maspcg_info *info,
+                                      void *cuda_stream);
+/* Same, HOST rhs and x (copied in and out through workspace staging). */
+MASPCG_API maspcg_status maspcg_solve_host(maspcg_ctx *ctx, const double *rhs, double *x,
+                                           double tol, int maxit, double *resid_hist,
+                                           maspcg_info *info, void *cuda_stream);
+
+/* y = A x on the local slab (DEVICE [nloc][nt][nr] each; halo exchanged
+ * internally; x and y must not alias).  For tests and operator checks. */
+MASPCG_API maspcg_status maspcg_apply(maspcg_ctx *ctx, const double *x, double *y,
+                                      void *cuda_stream);
+
+/* ---- introspection ------------------------------------------------------------ */
+
+/* Copy the assembled local operator to HOST arrays in the oracle's face
+ * layout (NULL skips an array): Tr [nloc][nt][nr+1], Tt [nloc][nt+1][nr],
+ * Tp [nloc][nt][nr] (face k+1/2), D [nloc][nt][nr].  Finalises D first. */
+MASPCG_API maspcg_status maspcg_get_operator(maspcg_ctx *ctx, double *Tr, double *Tt, double *Tp,
+                                             double *D, void *cuda_stream);
+
+MASPCG_API maspcg_status maspcg_set_option(maspcg_ctx *ctx, maspcg_option opt, long long value);
+MASPCG_API maspcg_status maspcg_get_stats(const maspcg_ctx *ctx, maspcg_stats *out);
+MASPCG_API maspcg_status maspcg_reset_stats(maspcg_ctx *ctx);
+
+/* Library version string, e.g. "maspcg 0.1 sm_100a". */
+MASPCG_API const char *maspcg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MASPCG_H */

@@ -1,0 +1,126 @@
+// common.cuh -- shared definitions of libmaspcg (product path only; never
+// included by oracle/).  See include/maspcg.h for the model and DESIGN.md for
+// the data layout in HBM.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace maspcg {
+
+// Status codes mirrored from include/maspcg.h for device code.
+enum : int {
+    ST_OK = 0,
+    ST_NOT_CONVERGED = 1,
+    ST_E_INVALID = -1,
+    ST_E_STATE = -2,
+    ST_E_SINGULAR = -3,
+    ST_E_BREAKDOWN = -4,
+    ST_E_CUDA = -5,
+    ST_E_NCCL = -6,
+    ST_E_NOMEM = -7,
+};
+
+enum : int { BC_DIRICHLET = 0, BC_NEUMANN0 = 1 };
+
+constexpr int kMaxChunk = 256;          // PCG iterations per graph launch (upper bound)
+constexpr int kRedBlocks = 1184;        // fixed grid of the streaming kernels (8 x 148)
+constexpr int kThreads = 256;           // threads per block of the streaming kernels
+
+// Division by a runtime constant for 0 <= n < 2^31 (round-up multiplier
+// method): q = (n * m) >> p with p = 31 + ceil(log2 d), m = ceil(2^p / d).
+struct FastDiv {
+    uint32_t d;
+    uint32_t p;
+    uint64_t m;
+#ifdef __CUDACC__
+    __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return d == 1 ? n : static_cast<uint32_t>((static_cast<uint64_t>(n) * m) >> p);
+    }
+#endif
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{};
+    f.d = d;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    f.p = 31 + l;
+    f.m = ((1ull << f.p) + d - 1) / d;
+    return f;
+}
+
+// Device-resident solver scalars (one struct in the workspace).  Written only
+// by single threads (a kernel's last-arriving block or a 1-thread kernel);
+// read by every block at kernel entry.  A snapshot is copied to pinned host
+// memory once per graph chunk.
+struct Scalars {
+    double red1[2];          // [0] = p.Ap (local partial, then global after all-reduce)
+    double red2[2];          // [0] = r.z, [1] = r.r
+    double red3[4];          // setup: r.z, r.r, b.b
+    double rho;              // r.z of the current iterate
+    double bn;               // ||b||
+    double tolbn;            // tol * ||b||
+    double tol;
+    double hist0;            // ||r_0||
+    double rn;               // ||r_iter||
+    int iter;                // completed PCG iterations
+    int maxit;
+    int done;                // 1: every loop kernel returns at entry
+    int status;              // provisional / final status
+    int zero_x;              // b == 0: x := 0 at the end
+    int vinvalid;            // set_coefficients: 1 if any input is negative or non-finite
+    int vshift;              // set_coefficients: 1 if any s > 0
+    int pad_;
+    unsigned int ticket[8];  // last-block tickets (reset by the last block)
+    double hist_ring[kMaxChunk];   // ||r_k|| at slot (k-1) % chunk
+};
+
+// Geometry handed to kernels by value.
+struct Dims {
+    int nr, nt, nloc;       // local slab shape
+    int k0;                 // global index of local plane 0
+    uint32_t n;             // nloc * nt * nr
+    uint32_t plane;         // nt * nr
+    FastDiv div_r;          // / nr
+    FastDiv div_t;          // / nt
+    int periodic_local;     // 1: single rank, halo planes are written by the kernels
+};
+
+// Device pointers into the workspace.
+struct DevArrays {
+    // operator
+    double *Tr;     // [nloc][nt][nr]  lower r-face of each cell; slot i = 0 holds the inner-boundary face
+    double *TrB;    // [nloc][nt]      outer-boundary r-face (i = nr)
+    double *Tt;     // [nloc][nt][nr]  lower theta-face; slot j = 0 is 0 (pole / boundary: no flux)
+    double *Tp;     // [nloc+1][nt][nr] plane kk = phi face (k0 + kk - 1) + 1/2
+    double *D;      // [nloc][nt][nr]
+    double *sV;     // [nloc][nt][nr]  s * V
+    double *gin;    // [nloc][nt]
+    double *gout;   // [nloc][nt]
+    // PCG vectors
+    double *p;      // [nloc+2][nt][nr] plane 0 / nloc+1 are halos
+    double *q;      // [nloc][nt][nr]
+    double *r;      // [nloc][nt][nr]
+    double *xs;     // [nloc][nt][nr]  x staging (host entry points)
+    double *fs;     // [nloc][nt][nr]  rhs staging (host entry points)
+    // staging for host coefficients
+    double *skr, *skt, *skp, *ss;
+    // 1-D metric (local where noted)
+    double *rf2;    // [nr+1]  r_f^2
+    double *hr;     // [nr+1]
+    double *dr;     // [nr]
+    double *R3;     // [nr]
+    double *C;      // [nt]
+    double *sinf;   // [nt+1]
+    double *ht;     // [nt+1]
+    double *dt;     // [nt]
+    double *sinc;   // [nt]
+    double *dp;     // [nloc]  local
+    double *hp;     // [nloc]  local: h^phi of face (k0 + k) + 1/2
+    // reductions
+    double *partials;   // [4][kRedBlocks]
+    Scalars *sc;
+};
+
+}  // namespace maspcg

@@ -1,0 +1,478 @@
+// kernels.cu -- sm_100a fp64 kernels of the MAS implicit parabolic PCG solve.
+//
+// Hot path per PCG iteration (BASELINE.json north_star):
+//   stencil_matvec_dot  q = A p, partial p.q          48 B/cell algorithmic
+//   update_jacobi_dots  x += a p, r -= a q, z = r/D,  56 B/cell
+//                       partials r.z and r.r
+//   p_update            p = r/D + b p                 32 B/cell
+// All three are HBM-bandwidth bound (~0.2 flop/B, "highly
+// memory-bound"): no tensor cores.  Reductions are warp shuffles + one
+// partial per block + a last-block (atomic ticket) fixed-order final sum, so
+// results are bitwise deterministic run to run and independent of block
+// scheduling.  Scalars (alpha, beta, rho, convergence) live in device memory
+// (Scalars) and are consumed at kernel entry: no host round trip per
+// iteration (the "gaps between kernel launches" of PAPER.md:292).
+//
+// Setup kernels (assembly, D, rhs) use __dmul_rn/__dadd_rn/__ddiv_rn so the
+// operator is computed with exactly one IEEE rounding per operation in the
+// order of the formulas of SURVEY.md 8(c) items 3-5 (no FMA contraction).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace maspcg {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// Reduce N values over the block (fixed tree), thread 0 gets the totals.
+template <int N>
+__device__ __forceinline__ void block_sum(double (&v)[N]) {
+    __shared__ double sm[N][kThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < N; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) sm[k][warp] = v[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            double x = lane < (int)(blockDim.x >> 5) ? sm[k][lane] : 0.0;
+            v[k] = warp_sum(x);
+        }
+    }
+    __syncthreads();
+}
+
+// Block partials -> partials[k * kRedBlocks + slot]; returns true in the last
+// block to arrive (all partials of all `total` blocks visible), which then
+// holds the fixed-order totals in out[] (thread 0) and has reset the ticket.
+template <int N>
+__device__ __forceinline__ bool reduce_and_last(double (&v)[N], double *partials, unsigned *ticket,
+                                                unsigned slot, unsigned total, double (&out)[N]) {
+    __shared__ bool am_last;
+    block_sum<N>(v);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) partials[k * kRedBlocks + slot] = v[k];
+        __threadfence();
+        unsigned t = atomicAdd(ticket, 1u);
+        am_last = (t == total - 1);
+    }
+    __syncthreads();
+    if (!am_last) return false;
+    __threadfence();
+    double acc[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        acc[k] = 0.0;
+        for (unsigned b = threadIdx.x; b < total; b += blockDim.x)
+            acc[k] += __ldcg(partials + k * kRedBlocks + b);
+    }
+    block_sum<N>(acc);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) out[k] = acc[k];
+        *ticket = 0u;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void decompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
+    uint32_t row = d.div_r.div(c);
+    i = (int)(c - row * (uint32_t)d.nr);
+    uint32_t kk = d.div_t.div(row);
+    j = (int)(row - kk * (uint32_t)d.nt);
+    k = (int)kk;
+}
+
+// Write a freshly computed p value of local cell c (plane k) into the padded
+// p array and, on a single rank, into the periodic halo copies.
+__device__ __forceinline__ void store_p(const Dims &d, double *p, uint32_t c, int k, double v) {
+    p[(size_t)c + d.plane] = v;
+    if (d.periodic_local) {
+        if (k == 0) p[(size_t)c + (size_t)(d.nloc + 1) * d.plane] = v;          // hi halo <- first plane
+        if (k == d.nloc - 1) p[(size_t)c - (size_t)(d.nloc - 1) * d.plane] = v; // lo halo <- last plane
+    }
+}
+
+// ---------------------------------------------------------------- assembly
+// SURVEY 8(c) item 3 (R3-R5, R8): face transmissibilities, s*V, validation.
+__global__ void __launch_bounds__(kThreads) k_assemble(Dims d, DevArrays a, const double *__restrict__ kr,
+                                                       const double *__restrict__ kt,
+                                                       const double *__restrict__ kp,
+                                                       const double *__restrict__ s) {
+    int bad = 0, pos = 0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        const uint32_t row = (uint32_t)k * d.nt + j;
+        const double dpk = a.dp[k];
+        // r-face i (lower face of the cell; i = 0 is the inner boundary face)
+        const double kri = kr[(size_t)row * (d.nr + 1) + i];
+        bad |= !(kri >= 0.0) | !isfinite(kri);
+        a.Tr[c] = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(kri, a.rf2[i]), a.C[j]), dpk), a.hr[i]);
+        if (i == d.nr - 1) {
+            const double kro = kr[(size_t)row * (d.nr + 1) + d.nr];
+            bad |= !(kro >= 0.0) | !isfinite(kro);
+            a.TrB[row] = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(kro, a.rf2[d.nr]), a.C[j]), dpk), a.hr[d.nr]);
+        }
+        // theta-face j (lower); boundary faces j = 0, nt carry no flux (R8)
+        const size_t tbase = ((size_t)k * (d.nt + 1) + j) * d.nr + i;
+        const double ktj = kt[tbase];
+        bad |= !(ktj >= 0.0) | !isfinite(ktj);
+        a.Tt[c] = (j == 0) ? 0.0
+                           : __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(ktj, a.sinf[j]), a.dr[i]), dpk), a.ht[j]);
+        if (j == d.nt - 1) {
+            const double kte = kt[tbase + d.nr];
+            bad |= !(kte >= 0.0) | !isfinite(kte);
+        }
+        // phi-face k+1/2 -> Tp plane k+1
+        const double kpc = kp[c];
+        bad |= !(kpc >= 0.0) | !isfinite(kpc);
+        a.Tp[(size_t)c + d.plane] =
+            __ddiv_rn(__dmul_rn(__dmul_rn(kpc, a.dr[i]), a.dt[j]), __dmul_rn(a.sinc[j], a.hp[k]));
+        // s * V, V = R3_i C_j dphi_k
+        const double sc = s[c];
+        bad |= !(sc >= 0.0) | !isfinite(sc);
+        pos |= (sc > 0.0);
+        const double V = __dmul_rn(__dmul_rn(a.R3[i], a.C[j]), dpk);
+        a.sV[c] = __dmul_rn(sc, V);
+    }
+    bad = __syncthreads_or(bad);
+    pos = __syncthreads_or(pos);
+    if (threadIdx.x == 0) {
+        if (bad) atomicOr(&a.sc->vinvalid, 1);
+        if (pos) atomicOr(&a.sc->vshift, 1);
+    }
+}
+
+// D = sV + Tr_lo + Tr_hi + Tt_lo + Tt_hi + Tp_lo + Tp_hi  (R7, R10)
+__global__ void __launch_bounds__(kThreads) k_finalize_D(Dims d, DevArrays a, int bc_in, int bc_out) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        const uint32_t row = (uint32_t)k * d.nt + j;
+        const double trlo = (i > 0 || bc_in == BC_DIRICHLET) ? a.Tr[c] : 0.0;
+        const double trhi = (i < d.nr - 1) ? a.Tr[c + 1] : (bc_out == BC_DIRICHLET ? a.TrB[row] : 0.0);
+        const double ttlo = a.Tt[c];
+        const double tthi = (j < d.nt - 1) ? a.Tt[c + d.nr] : 0.0;
+        const double tplo = a.Tp[c];
+        const double tphi = a.Tp[(size_t)c + d.plane];
+        double v = a.sV[c];
+        v = __dadd_rn(v, trlo);
+        v = __dadd_rn(v, trhi);
+        v = __dadd_rn(v, ttlo);
+        v = __dadd_rn(v, tthi);
+        v = __dadd_rn(v, tplo);
+        v = __dadd_rn(v, tphi);
+        a.D[c] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_fill_p(Dims d, DevArrays a, const double *__restrict__ x) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        const int k = (int)(c / d.plane);
+        store_p(d, a.p, c, k, x[c]);
+    }
+}
+
+// ---------------------------------------------------------------- stencil
+// y = A p over a virtual range: c = v + off0 + (v >= split ? off1 : 0).
+// WITH_DOT: block partials of p.y -> last block writes sc->red1[0].
+// LOOP: returns at entry once sc->done is set.
+struct Range {
+    uint32_t vend, off0, split, off1;
+};
+
+template <bool WITH_DOT, bool LOOP>
+__global__ void __launch_bounds__(kThreads) k_matvec_flat(Dims d, DevArrays a, double *__restrict__ y, Range rg,
+                                                          unsigned red_slot0, unsigned red_total) {
+    if (LOOP && *(volatile int *)&a.sc->done) return;
+    const double *__restrict__ p = a.p;
+    const double *__restrict__ Tr = a.Tr;
+    const double *__restrict__ Tt = a.Tt;
+    const double *__restrict__ Tp = a.Tp;
+    const double *__restrict__ D = a.D;
+    const size_t plane = d.plane;
+    double acc = 0.0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < rg.vend; v += stride) {
+        const uint32_t c = v + rg.off0 + (v >= rg.split ? rg.off1 : 0u);
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        const size_t cp = (size_t)c + plane;
+        const double pc = __ldg(p + cp);
+        double s = 0.0;
+        if (i > 0) s = fma(__ldg(Tr + c), __ldg(p + cp - 1), s);
+        if (i < d.nr - 1) s = fma(__ldg(Tr + c + 1), __ldg(p + cp + 1), s);
+        if (j > 0) s = fma(__ldg(Tt + c), __ldg(p + cp - d.nr), s);
+        if (j < d.nt - 1) s = fma(__ldg(Tt + c + d.nr), __ldg(p + cp + d.nr), s);
+        s = fma(__ldg(Tp + c), __ldg(p + cp - plane), s);
+        s = fma(__ldg(Tp + c + plane), __ldg(p + cp + plane), s);
+        const double q = fma(__ldg(D + c), pc, -s);
+        y[c] = q;
+        if (WITH_DOT) acc = fma(pc, q, acc);
+    }
+    if (WITH_DOT) {
+        double v1[1] = {acc}, out[1];
+        if (reduce_and_last<1>(v1, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total, out)) {
+            if (threadIdx.x == 0) a.sc->red1[0] = out[0];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- setup of a solve
+// b = V f + Dirichlet face terms (R5); r0 = b - q (q = A x0); z0 = r0/D; p0 = z0;
+// partials r.z, r.r, b.b -> sc->red3.
+__global__ void __launch_bounds__(kThreads) k_setup_residual(Dims d, DevArrays a, const double *__restrict__ f,
+                                                             int din, int dout, unsigned total) {
+    double rz = 0.0, rr = 0.0, bb = 0.0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        const uint32_t row = (uint32_t)k * d.nt + j;
+        const double V = __dmul_rn(__dmul_rn(a.R3[i], a.C[j]), a.dp[k]);
+        double b = __dmul_rn(V, f[c]);
+        if (din && i == 0) b = __dadd_rn(b, __dmul_rn(a.Tr[c], a.gin[row]));
+        if (dout && i == d.nr - 1) b = __dadd_rn(b, __dmul_rn(a.TrB[row], a.gout[row]));
+        const double r = b - a.q[c];
+        const double z = r / a.D[c];
+        a.r[c] = r;
+        store_p(d, a.p, c, k, z);
+        rz = fma(r, z, rz);
+        rr = fma(r, r, rr);
+        bb = fma(b, b, bb);
+    }
+    double v3[3] = {rz, rr, bb}, out[3];
+    if (reduce_and_last<3>(v3, a.partials, &a.sc->ticket[3], blockIdx.x, total, out)) {
+        if (threadIdx.x == 0) {
+            a.sc->red3[0] = out[0];
+            a.sc->red3[1] = out[1];
+            a.sc->red3[2] = out[2];
+        }
+    }
+}
+
+// PCG start, after red3 holds global sums.
+__global__ void k_setup_scalars(DevArrays a, double tol, int maxit) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    Scalars *sc = a.sc;
+    sc->tol = tol;
+    sc->maxit = maxit;
+    const double rz = sc->red3[0], rr = sc->red3[1], bb = sc->red3[2];
+    const double bn = sqrt(bb), h0 = sqrt(rr);
+    sc->bn = bn;
+    sc->tolbn = sc->tol * bn;
+    sc->iter = 0;
+    sc->rho = rz;
+    sc->zero_x = 0;
+    sc->done = 1;
+    if (!isfinite(bn)) {
+        sc->hist0 = bn;
+        sc->rn = bn;
+        sc->status = ST_E_BREAKDOWN;
+    } else if (bn == 0.0) {
+        sc->hist0 = 0.0;
+        sc->rn = 0.0;
+        sc->zero_x = 1;
+        sc->status = ST_OK;
+    } else {
+        sc->hist0 = h0;
+        sc->rn = h0;
+        if (!isfinite(h0) || !isfinite(rz)) sc->status = ST_E_BREAKDOWN;
+        else if (h0 <= sc->tolbn) sc->status = ST_OK;
+        else if (sc->maxit == 0) sc->status = ST_NOT_CONVERGED;
+        else {
+            sc->status = ST_NOT_CONVERGED;
+            sc->done = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- PCG loop
+// alpha = rho / p.Ap; x += alpha p; r -= alpha q; z = r / D; partials r.z, r.r.
+__global__ void __launch_bounds__(kThreads) k_update(Dims d, DevArrays a, double *__restrict__ x, unsigned total) {
+    Scalars *sc = a.sc;
+    if (*(volatile int *)&sc->done) return;
+    const double pi = sc->red1[0];
+    if (!(pi > 0.0) || !isfinite(pi)) {        // breakdown: uniform decision in every block
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->status = ST_E_BREAKDOWN;
+            sc->done = 1;
+        }
+        return;
+    }
+    const double alpha = sc->rho / pi;
+    const double *__restrict__ p = a.p + d.plane;
+    const double *__restrict__ q = a.q;
+    const double *__restrict__ D = a.D;
+    double *__restrict__ r = a.r;
+    double rz = 0.0, rr = 0.0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        const double pc = __ldg(p + c);
+        x[c] = fma(alpha, pc, x[c]);
+        const double rc = fma(-alpha, __ldg(q + c), r[c]);
+        r[c] = rc;
+        const double z = rc / __ldg(D + c);
+        rz = fma(rc, z, rz);
+        rr = fma(rc, rc, rr);
+    }
+    double v2[2] = {rz, rr}, out[2];
+    if (reduce_and_last<2>(v2, a.partials, &sc->ticket[1], blockIdx.x, total, out)) {
+        if (threadIdx.x == 0) {
+            sc->red2[0] = out[0];
+            sc->red2[1] = out[1];
+        }
+    }
+}
+
+// Convergence test on ||r|| (R12); beta = r.z / rho (R11); p = r/D + beta p.
+// The last block advances the iteration counter and the scalars.
+__global__ void __launch_bounds__(kThreads) k_pupdate(Dims d, DevArrays a, int chunk, unsigned total) {
+    Scalars *sc = a.sc;
+    if (*(volatile int *)&sc->done) return;
+    const double rz = sc->red2[0], rr = sc->red2[1];
+    const double rn = sqrt(rr);
+    const bool conv = rn <= sc->tolbn;
+    const bool bad = !isfinite(rn) || !isfinite(rz);
+    if (!conv && !bad) {
+        const double beta = rz / sc->rho;
+        const double *__restrict__ r = a.r;
+        const double *__restrict__ D = a.D;
+        const uint32_t stride = gridDim.x * blockDim.x;
+        for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+            const double pold = a.p[(size_t)c + d.plane];
+            const double pn = fma(beta, pold, __ldg(r + c) / __ldg(D + c));
+            store_p(d, a.p, c, (int)(c / d.plane), pn);
+        }
+    }
+    __shared__ bool am_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
+    }
+    __syncthreads();
+    if (am_last && threadIdx.x == 0) {
+        __threadfence();
+        const int it = sc->iter + 1;
+        sc->iter = it;
+        sc->rn = rn;
+        sc->hist_ring[(it - 1) % chunk] = rn;
+        if (conv) {
+            sc->status = ST_OK;
+            sc->done = 1;
+        } else if (bad) {
+            sc->status = ST_E_BREAKDOWN;
+            sc->done = 1;
+        } else if (it >= sc->maxit) {
+            sc->status = ST_NOT_CONVERGED;
+            sc->done = 1;
+        }
+        sc->rho = rz;
+        sc->ticket[2] = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_zero_x_if(Dims d, DevArrays a, double *__restrict__ x) {
+    if (!a.sc->zero_x) return;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) x[c] = 0.0;
+}
+
+inline unsigned grid_for(uint32_t n) {
+    uint64_t g = (n + kThreads - 1) / kThreads;
+    if (g < 1) g = 1;
+    if (g > (uint64_t)kRedBlocks) g = kRedBlocks;
+    return (unsigned)g;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+void launch_assemble(const Dims &d, const DevArrays &a, const double *kr, const double *kt, const double *kp,
+                     const double *s, cudaStream_t st) {
+    k_assemble<<<grid_for(d.n), kThreads, 0, st>>>(d, a, kr, kt, kp, s);
+}
+
+void launch_finalize_D(const Dims &d, const DevArrays &a, int bc_in, int bc_out, cudaStream_t st) {
+    k_finalize_D<<<grid_for(d.n), kThreads, 0, st>>>(d, a, bc_in, bc_out);
+}
+
+void launch_fill_p(const Dims &d, const DevArrays &a, const double *x, cudaStream_t st) {
+    k_fill_p<<<grid_for(d.n), kThreads, 0, st>>>(d, a, x);
+}
+
+static Range make_range(const Dims &d, StencilPart part) {
+    Range rg{};
+    const uint32_t pl = d.plane;
+    switch (part) {
+        case StencilPart::Full: rg = {d.n, 0u, 0xffffffffu, 0u}; break;
+        case StencilPart::Interior:
+            rg = {d.nloc > 2 ? (uint32_t)(d.nloc - 2) * pl : 0u, pl, 0xffffffffu, 0u};
+            break;
+        case StencilPart::Boundary:
+            if (d.nloc == 1) rg = {pl, 0u, 0xffffffffu, 0u};
+            else rg = {2u * pl, 0u, pl, (uint32_t)(d.nloc - 2) * pl};
+            break;
+    }
+    return rg;
+}
+
+unsigned stencil_blocks(const Dims &d, StencilPart part) {
+    Range rg = make_range(d, part);
+    return rg.vend ? grid_for(rg.vend) : 0u;
+}
+
+void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart part, bool with_dot, bool loop,
+                   unsigned red_slot0, unsigned red_total, cudaStream_t st) {
+    Range rg = make_range(d, part);
+    if (rg.vend == 0) return;
+    const unsigned g = grid_for(rg.vend);
+    if (with_dot) {
+        if (loop) k_matvec_flat<true, true><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);
+        else k_matvec_flat<true, false><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);
+    } else {
+        k_matvec_flat<false, false><<<g, kThreads, 0, st>>>(d, a, y, rg, 0, 0);
+    }
+}
+
+void launch_setup_residual(const Dims &d, const DevArrays &a, const double *f, int din, int dout, cudaStream_t st) {
+    const unsigned g = grid_for(d.n);
+    k_setup_residual<<<g, kThreads, 0, st>>>(d, a, f, din, dout, g);
+}
+
+void launch_setup_scalars(const DevArrays &a, double tol, int maxit, cudaStream_t st) {
+    k_setup_scalars<<<1, 32, 0, st>>>(a, tol, maxit);
+}
+
+void launch_update(const Dims &d, const DevArrays &a, double *x, cudaStream_t st) {
+    const unsigned g = grid_for(d.n);
+    k_update<<<g, kThreads, 0, st>>>(d, a, x, g);
+}
+
+void launch_pupdate(const Dims &d, const DevArrays &a, int chunk, cudaStream_t st) {
+    const unsigned g = grid_for(d.n);
+    k_pupdate<<<g, kThreads, 0, st>>>(d, a, chunk, g);
+}
+
+void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st) {
+    k_zero_x_if<<<grid_for(d.n), kThreads, 0, st>>>(d, a, x);
+}
+
+}  // namespace maspcg

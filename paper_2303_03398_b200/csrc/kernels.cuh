@@ -1,0 +1,31 @@
+// kernels.cuh -- launchers of the sm_100a kernels (kernels.cu, stencil_tiled.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace maspcg {
+
+enum class StencilPart { Full, Interior, Boundary };
+
+void launch_assemble(const Dims &d, const DevArrays &a, const double *kr, const double *kt, const double *kp,
+                     const double *s, cudaStream_t st);
+void launch_finalize_D(const Dims &d, const DevArrays &a, int bc_in, int bc_out, cudaStream_t st);
+void launch_fill_p(const Dims &d, const DevArrays &a, const double *x, cudaStream_t st);
+
+// Number of blocks launch_matvec uses for `part` (0: nothing to do).
+unsigned stencil_blocks(const Dims &d, StencilPart part);
+// y = A p over `part` of the slab.  with_dot: partial p.y into partial slots
+// [red_slot0, red_slot0 + blocks); the last of red_total blocks writes
+// sc->red1[0].  loop: early exit when sc->done.
+void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart part, bool with_dot, bool loop,
+                   unsigned red_slot0, unsigned red_total, cudaStream_t st);
+
+void launch_setup_residual(const Dims &d, const DevArrays &a, const double *f, int din, int dout, cudaStream_t st);
+void launch_setup_scalars(const DevArrays &a, double tol, int maxit, cudaStream_t st);
+void launch_update(const Dims &d, const DevArrays &a, double *x, cudaStream_t st);
+void launch_pupdate(const Dims &d, const DevArrays &a, int chunk, cudaStream_t st);
+void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st);
+
+}  // namespace maspcg

@@ -1,0 +1,796 @@
+// maspcg.cu -- host driver and C ABI of libmaspcg (include/maspcg.h).
+//
+// Layers (new-build table): L1 grid/metric precompute on
+// the host, L3 NCCL communication (phi-slab halos + scalar all-reduces), L4
+// the PCG driver (device-resident scalars, CUDA-graph chunks of iterations,
+// host polls a device flag once per chunk), L5 this C ABI.  The kernels are in
+// kernels.cu.  Nothing here computes on the host what the hot path computes:
+// the host only precomputes O(nr + nt + np) 1-D metric factors (SURVEY 8(a)
+// a1, "negligible (setup)").
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/maspcg.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace maspcg;
+
+namespace {
+
+// Period of phi (R9).  Same literal value as the definition of 2*pi.
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+constexpr double kPi = 3.14159265358979323846;
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+struct maspcg_ctx {
+    int nr = 0, nt = 0, np = 0, rank = 0, nranks = 1, device = 0;
+    int k0 = 0, nloc = 0;
+    ncclComm_t comm = nullptr;
+    std::string err;
+
+    // grid (host copies of the 1-D metric)
+    bool grid_set = false;
+    std::vector<double> rf2, hr, dr, R3, C, sinf, ht, dt, sinc, dp_loc, hp_loc;
+    bool metric_dirty = true;
+
+    // workspace
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    DevArrays a{};
+    Dims d{};
+
+    // operator state
+    bool coef_set = false, bc_set = false, D_dirty = true;
+    int any_shift = 0;
+    int bc_in = BC_DIRICHLET, bc_out = BC_NEUMANN0;
+    int has_gin = 0, has_gout = 0;
+
+    // streams, events, host snapshots
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_p = nullptr, ev_halo = nullptr, ev_chunk[2] = {nullptr, nullptr};
+    Scalars *snap[2] = {nullptr, nullptr};
+    int *vflags_host = nullptr;
+
+    // graph cache (one captured chunk of `chunk` iterations)
+    cudaGraphExec_t gexec = nullptr;
+    const void *g_x = nullptr;
+    cudaStream_t g_stream = nullptr;
+    int g_chunk = 0, g_variant = -1;
+
+    // options
+    int chunk = 16, use_graphs = 1, timing = 0, stencil_variant = 0;
+    maspcg_stats stats{};
+    std::vector<cudaEvent_t> tev;   // timing events [3 kernels][2][chunk]
+};
+
+#define SET_ERR(ctx, code, ...)                                              \
+    do {                                                                     \
+        char _b[512];                                                        \
+        snprintf(_b, sizeof(_b), __VA_ARGS__);                               \
+        (ctx)->err = _b;                                                     \
+        return (maspcg_status)(code);                                        \
+    } while (0)
+
+#define CK(ctx, call)                                                                                \
+    do {                                                                                             \
+        cudaError_t _e = (call);                                                                     \
+        if (_e != cudaSuccess)                                                                       \
+            SET_ERR(ctx, MASPCG_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, \
+                    __LINE__);                                                                       \
+    } while (0)
+
+#define NK(ctx, call)                                                                                  \
+    do {                                                                                               \
+        ncclResult_t _r = (call);                                                                      \
+        if (_r != ncclSuccess)                                                                         \
+            SET_ERR(ctx, MASPCG_E_NCCL, "%s failed: %s (%s:%d)", #call, ncclGetErrorString(_r), __FILE__, \
+                    __LINE__);                                                                         \
+    } while (0)
+
+#define RET_IF(st)                       \
+    do {                                 \
+        maspcg_status _s = (st);         \
+        if (_s != MASPCG_OK) return _s;  \
+    } while (0)
+
+namespace {
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Workspace layout.  base == nullptr: only computes the size.
+size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
+    const size_t n = (size_t)c->nloc * c->nt * c->nr, plane = (size_t)c->nt * c->nr;
+    const size_t rows = (size_t)c->nloc * c->nt;
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char * {
+        char *p = base ? base + off : nullptr;
+        off = align_up(off + bytes, 256);
+        return p;
+    };
+    DevArrays t{};
+    t.sc = (Scalars *)take(sizeof(Scalars));
+    t.partials = (double *)take(sizeof(double) * 4 * kRedBlocks);
+    t.Tr = (double *)take(8 * n);
+    t.TrB = (double *)take(8 * rows);
+    t.Tt = (double *)take(8 * n);
+    t.Tp = (double *)take(8 * (n + plane));
+    t.D = (double *)take(8 * n);
+    t.sV = (double *)take(8 * n);
+    t.gin = (double *)take(8 * rows);
+    t.gout = (double *)take(8 * rows);
+    t.p = (double *)take(8 * (n + 2 * plane));
+    t.q = (double *)take(8 * n);
+    t.r = (double *)take(8 * n);
+    t.xs = (double *)take(8 * n);
+    t.fs = (double *)take(8 * n);
+    t.skr = (double *)take(8 * (rows * (c->nr + 1)));
+    t.skt = (double *)take(8 * ((size_t)c->nloc * (c->nt + 1) * c->nr));
+    t.skp = (double *)take(8 * n);
+    t.ss = (double *)take(8 * n);
+    t.rf2 = (double *)take(8 * (c->nr + 1));
+    t.hr = (double *)take(8 * (c->nr + 1));
+    t.dr = (double *)take(8 * c->nr);
+    t.R3 = (double *)take(8 * c->nr);
+    t.C = (double *)take(8 * c->nt);
+    t.sinf = (double *)take(8 * (c->nt + 1));
+    t.ht = (double *)take(8 * (c->nt + 1));
+    t.dt = (double *)take(8 * c->nt);
+    t.sinc = (double *)take(8 * c->nt);
+    t.dp = (double *)take(8 * c->nloc);
+    t.hp = (double *)take(8 * c->nloc);
+    if (a) *a = t;
+    return off;
+}
+
+maspcg_status bind_device(maspcg_ctx *c) {
+    CK(c, cudaSetDevice(c->device));
+    return MASPCG_OK;
+}
+
+maspcg_status ensure_metric(maspcg_ctx *c, cudaStream_t st) {
+    if (!c->metric_dirty) return MASPCG_OK;
+    auto up = [&](double *dst, const std::vector<double> &v) {
+        return cudaMemcpyAsync(dst, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, st);
+    };
+    CK(c, up(c->a.rf2, c->rf2));
+    CK(c, up(c->a.hr, c->hr));
+    CK(c, up(c->a.dr, c->dr));
+    CK(c, up(c->a.R3, c->R3));
+    CK(c, up(c->a.C, c->C));
+    CK(c, up(c->a.sinf, c->sinf));
+    CK(c, up(c->a.ht, c->ht));
+    CK(c, up(c->a.dt, c->dt));
+    CK(c, up(c->a.sinc, c->sinc));
+    CK(c, up(c->a.dp, c->dp_loc));
+    CK(c, up(c->a.hp, c->hp_loc));
+    CK(c, cudaStreamSynchronize(st));   // host vectors may change with the next set_grid
+    c->metric_dirty = false;
+    return MASPCG_OK;
+}
+
+int left_of(const maspcg_ctx *c) { return (c->rank + c->nranks - 1) % c->nranks; }
+int right_of(const maspcg_ctx *c) { return (c->rank + 1) % c->nranks; }
+
+// Exchange the boundary planes of a padded [nloc+2][nt][nr] array (plane 0 and
+// nloc+1 are halos).  Ops to the same peer are matched in issue order, so the
+// order below is also correct when left == right (P = 2): the first send and
+// the first receive between a pair carry "first plane -> hi halo".
+maspcg_status halo_padded(maspcg_ctx *c, double *buf, cudaStream_t st) {
+    const size_t pl = (size_t)c->nt * c->nr;
+    const int L = left_of(c), R = right_of(c);
+    NK(c, ncclGroupStart());
+    NK(c, ncclSend(buf + pl, pl, ncclDouble, L, c->comm, st));                       // my first plane
+    NK(c, ncclRecv(buf + (size_t)(c->nloc + 1) * pl, pl, ncclDouble, R, c->comm, st)); // right's first -> hi halo
+    NK(c, ncclSend(buf + (size_t)c->nloc * pl, pl, ncclDouble, R, c->comm, st));      // my last plane
+    NK(c, ncclRecv(buf, pl, ncclDouble, L, c->comm, st));                            // left's last -> lo halo
+    NK(c, ncclGroupEnd());
+    return MASPCG_OK;
+}
+
+maspcg_status allreduce_sum(maspcg_ctx *c, double *dev, size_t count, cudaStream_t st) {
+    if (c->nranks == 1) return MASPCG_OK;
+    NK(c, ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, c->comm, st));
+    return MASPCG_OK;
+}
+
+// Halo exchange of p (P > 1) overlapped with the interior of the stencil on
+// the caller's stream; joins before the boundary planes.
+maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st) {
+    if (c->nranks == 1) {
+        launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
+                      stencil_blocks(c->d, StencilPart::Full), st);
+        return MASPCG_OK;
+    }
+    CK(c, cudaEventRecord(c->ev_p, st));
+    CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
+    RET_IF(halo_padded(c, c->a.p, c->comm_stream));
+    CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+    const unsigned gi = stencil_blocks(c->d, StencilPart::Interior);
+    const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary);
+    launch_matvec(c->d, c->a, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, st);
+    CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+    launch_matvec(c->d, c->a, y, StencilPart::Boundary, with_dot, loop, gi, gi + gb, st);
+    return MASPCG_OK;
+}
+
+maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
+    if (!c->coef_set || !c->bc_set)
+        SET_ERR(c, MASPCG_E_STATE, "set_coefficients and set_bc_r must precede solve/apply");
+    if (!c->D_dirty) return MASPCG_OK;
+    if (!c->any_shift && c->bc_in != BC_DIRICHLET && c->bc_out != BC_DIRICHLET)
+        SET_ERR(c, MASPCG_E_SINGULAR, "shift is zero everywhere and no r boundary is Dirichlet: A is singular");
+    launch_finalize_D(c->d, c->a, c->bc_in, c->bc_out, st);
+    CK(c, cudaGetLastError());
+    c->D_dirty = false;
+    return MASPCG_OK;
+}
+
+int timing_ev_index(int kern, int which, int it, int chunk) { return (kern * 2 + which) * chunk + it; }
+
+// One PCG iteration.  it: index within the chunk (timing).
+maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int it) {
+    const bool tm = c->timing != 0;
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 0, it, c->chunk)], st));
+    RET_IF(stencil_with_halo(c, c->a.q, true, true, st));
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 1, it, c->chunk)], st));
+    RET_IF(allreduce_sum(c, c->a.sc->red1, 1, st));
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 0, it, c->chunk)], st));
+    launch_update(c->d, c->a, x, st);
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 1, it, c->chunk)], st));
+    RET_IF(allreduce_sum(c, c->a.sc->red2, 2, st));
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 0, it, c->chunk)], st));
+    launch_pupdate(c->d, c->a, c->chunk, st);
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 1, it, c->chunk)], st));
+    return MASPCG_OK;
+}
+
+maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st) {
+    const bool graphs = c->use_graphs && !c->timing;
+    if (!graphs) {
+        for (int it = 0; it < c->chunk; ++it) RET_IF(enqueue_iteration(c, x, st, it));
+        CK(c, cudaGetLastError());
+        return MASPCG_OK;
+    }
+    if (!c->gexec || c->g_x != x || c->g_stream != st || c->g_chunk != c->chunk ||
+        c->g_variant != c->stencil_variant) {
+        if (c->gexec) {
+            cudaGraphExecDestroy(c->gexec);
+            c->gexec = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        CK(c, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        maspcg_status s = MASPCG_OK;
+        for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_iteration(c, x, st, it);
+        cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (s != MASPCG_OK) {
+            if (g) cudaGraphDestroy(g);
+            return s;
+        }
+        CK(c, e);
+        cudaError_t ei = cudaGraphInstantiate(&c->gexec, g, 0);
+        cudaGraphDestroy(g);
+        CK(c, ei);
+        c->g_x = x;
+        c->g_stream = st;
+        c->g_chunk = c->chunk;
+        c->g_variant = c->stencil_variant;
+    }
+    CK(c, cudaGraphLaunch(c->gexec, st));
+    return MASPCG_OK;
+}
+
+void accumulate_timing(maspcg_ctx *c, int iters_in_chunk) {
+    for (int it = 0; it < iters_in_chunk; ++it) {
+        float ms[3];
+        for (int k = 0; k < 3; ++k) {
+            ms[k] = 0.f;
+            cudaEventElapsedTime(&ms[k], c->tev[timing_ev_index(k, 0, it, c->chunk)],
+                                 c->tev[timing_ev_index(k, 1, it, c->chunk)]);
+        }
+        c->stats.matvec_ms += ms[0];
+        c->stats.matvec_launches += 1;
+        c->stats.update_ms += ms[1];
+        c->stats.update_launches += 1;
+        c->stats.pupdate_ms += ms[2];
+        c->stats.pupdate_launches += 1;
+    }
+}
+
+long long kernels_per_iteration(const maspcg_ctx *c) {
+    if (c->nranks == 1) return 3;
+    return 2 + (stencil_blocks(c->d, StencilPart::Interior) ? 1 : 0) + 1;
+}
+
+bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
+    const char *pa = (const char *)a, *pb = (const char *)b;
+    return pa < pb + nb && pb < pa + na;
+}
+
+maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol, int maxit, double *hist,
+                         maspcg_info *info, cudaStream_t st) {
+    const size_t n = (size_t)c->nloc * c->nt * c->nr;
+    if (!rhs || !x) SET_ERR(c, MASPCG_E_INVALID, "rhs and x must be non-NULL");
+    if (overlaps(rhs, 8 * n, x, 8 * n)) SET_ERR(c, MASPCG_E_INVALID, "x must not alias rhs");
+    if (!(tol >= 0.0) || !std::isfinite(tol)) SET_ERR(c, MASPCG_E_INVALID, "tol must be finite and >= 0");
+    if (maxit < 0) SET_ERR(c, MASPCG_E_INVALID, "maxit must be >= 0");
+    if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
+    RET_IF(ensure_D(c, st));
+    if (c->timing) RET_IF(maspcg_set_option(c, MASPCG_OPT_TIMING, 1));   // events for this chunk size
+
+    // a3: r0 = b - A x0, z0 = r0/D, p0 = z0, dots; then PCG start scalars
+    launch_fill_p(c->d, c->a, x, st);
+    RET_IF(stencil_with_halo(c, c->a.q, false, false, st));
+    launch_setup_residual(c->d, c->a, rhs, c->bc_in == BC_DIRICHLET && c->has_gin,
+                          c->bc_out == BC_DIRICHLET && c->has_gout, st);
+    RET_IF(allreduce_sum(c, c->a.sc->red3, 3, st));
+    launch_setup_scalars(c->a, tol, maxit, st);
+    CK(c, cudaGetLastError());
+    long long launched = 4 + (c->nranks > 1 ? 1 : 0);
+
+    // PCG loop: chunks of `chunk` iterations, one speculative chunk in flight.
+    CK(c, cudaMemcpyAsync(c->snap[0], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaEventRecord(c->ev_chunk[0], st));
+    CK(c, cudaEventSynchronize(c->ev_chunk[0]));   // start scalars (also orders the pinned writes above)
+    Scalars s0 = *c->snap[0];
+    if (hist) hist[0] = s0.hist0;
+    int status = s0.status, iters = 0;
+    double rn = s0.rn, bn = s0.bn;
+    bool done = s0.done != 0;
+    const bool pipelined = !c->timing;
+    int issued = 0, cur = 0;
+    auto issue = [&](int b) -> maspcg_status {
+        RET_IF(enqueue_chunk(c, x, st));
+        CK(c, cudaMemcpyAsync(c->snap[b], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+        CK(c, cudaEventRecord(c->ev_chunk[b], st));
+        issued += c->chunk;
+        launched += (long long)c->chunk * kernels_per_iteration(c);
+        return MASPCG_OK;
+    };
+    if (!done) {
+        RET_IF(issue(cur));
+        while (true) {
+            bool next_issued = false;
+            if (pipelined && issued < maxit) {
+                RET_IF(issue(cur ^ 1));
+                next_issued = true;
+            }
+            CK(c, cudaEventSynchronize(c->ev_chunk[cur]));
+            const Scalars &s = *c->snap[cur];
+            if (c->timing) accumulate_timing(c, s.iter - iters);
+            if (hist)
+                for (int k = iters + 1; k <= s.iter; ++k) hist[k] = s.hist_ring[(k - 1) % c->chunk];
+            iters = s.iter;
+            status = s.status;
+            rn = s.rn;
+            if (s.done) {
+                if (next_issued) CK(c, cudaEventSynchronize(c->ev_chunk[cur ^ 1]));
+                break;
+            }
+            if (!next_issued) {
+                if (issued >= maxit + c->chunk) SET_ERR(c, MASPCG_E_CUDA, "PCG loop did not terminate");
+                RET_IF(issue(cur ^ 1));
+            }
+            cur ^= 1;
+        }
+    }
+    launch_zero_x_if(c->d, c->a, x, st);
+    launched += 1;
+    CK(c, cudaGetLastError());
+    CK(c, cudaStreamSynchronize(st));
+    if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
+    c->stats.kernel_launches += launched;
+    c->stats.solves += 1;
+    c->stats.iterations += iters;
+    if (info) {
+        info->iters = iters;
+        info->bnorm = bn;
+        info->rnorm = (bn == 0.0) ? 0.0 : rn;
+        info->rel_resid = (bn == 0.0 || !std::isfinite(bn)) ? 0.0 : rn / bn;
+    }
+    if (status == MASPCG_E_BREAKDOWN) c->err = "PCG breakdown: p.Ap <= 0 or a non-finite residual";
+    return (maspcg_status)status;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+const char *maspcg_version(void) { return "maspcg 0.1 sm_100a fp64"; }
+
+maspcg_status maspcg_get_unique_id(void *out) {
+    if (!out) return MASPCG_E_INVALID;
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        g_create_error = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+        return MASPCG_E_NCCL;
+    }
+    static_assert(sizeof(ncclUniqueId) == MASPCG_NCCL_UNIQUE_ID_BYTES, "unique id size");
+    memcpy(out, &id, sizeof(id));
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const void *nccl_unique_id,
+                            int cuda_device, maspcg_ctx **out) {
+    if (!out) return MASPCG_E_INVALID;
+    *out = nullptr;
+    auto fail = [](maspcg_status s, const char *m) {
+        g_create_error = m;
+        return s;
+    };
+    if (nr < 1 || nt < 1 || np < 1) return fail(MASPCG_E_INVALID, "nr, nt, np must be >= 1");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(MASPCG_E_INVALID, "bad rank / nranks");
+    if (np % nranks != 0) return fail(MASPCG_E_INVALID, "np must be divisible by nranks");
+    if ((nranks > 1) != (nccl_unique_id != nullptr))
+        return fail(MASPCG_E_INVALID, "nccl_unique_id must be given iff nranks > 1");
+    const long long nloc = np / nranks;
+    if ((nloc + 2) * (long long)nt * nr >= (1ll << 31))
+        return fail(MASPCG_E_INVALID, "local slab too large (>= 2^31 cells with halos)");
+    maspcg_ctx *c = new maspcg_ctx();
+    c->nr = nr;
+    c->nt = nt;
+    c->np = np;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = cuda_device;
+    c->nloc = (int)nloc;
+    c->k0 = rank * (int)nloc;
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_chunk[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_chunk[1], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->snap[0], sizeof(Scalars));
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->snap[1], sizeof(Scalars));
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&c->vflags_host, 4 * sizeof(int));
+    if (e != cudaSuccess) {
+        g_create_error = std::string("CUDA initialisation failed: ") + cudaGetErrorString(e);
+        maspcg_destroy(c);
+        return MASPCG_E_CUDA;
+    }
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            g_create_error = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+            c->comm = nullptr;
+            maspcg_destroy(c);
+            return MASPCG_E_NCCL;
+        }
+    }
+    c->d.nr = nr;
+    c->d.nt = nt;
+    c->d.nloc = c->nloc;
+    c->d.k0 = c->k0;
+    c->d.plane = (uint32_t)((size_t)nt * nr);
+    c->d.n = (uint32_t)((size_t)c->nloc * nt * nr);
+    c->d.div_r = make_fastdiv((uint32_t)nr);
+    c->d.div_t = make_fastdiv((uint32_t)nt);
+    c->d.periodic_local = nranks == 1 ? 1 : 0;
+    *out = c;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_destroy(maspcg_ctx *c) {
+    if (!c) return MASPCG_OK;
+    cudaSetDevice(c->device);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
+    if (c->ev_p) cudaEventDestroy(c->ev_p);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    for (int b = 0; b < 2; ++b) {
+        if (c->ev_chunk[b]) cudaEventDestroy(c->ev_chunk[b]);
+        if (c->snap[b]) cudaFreeHost(c->snap[b]);
+    }
+    if (c->vflags_host) cudaFreeHost(c->vflags_host);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    delete c;
+    return MASPCG_OK;
+}
+
+const char *maspcg_last_error(const maspcg_ctx *c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+maspcg_status maspcg_set_grid(maspcg_ctx *c, const double *rf, const double *tf, const double *pf) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!rf || !tf || !pf) SET_ERR(c, MASPCG_E_INVALID, "face arrays must be non-NULL");
+    const int nr = c->nr, nt = c->nt, np = c->np;
+    // R1, R9: validity of the grid
+    if (!(rf[0] > 0.0)) SET_ERR(c, MASPCG_E_INVALID, "r_faces[0] must be > 0");
+    for (int i = 0; i < nr; ++i)
+        if (!(rf[i + 1] > rf[i])) SET_ERR(c, MASPCG_E_INVALID, "r_faces must increase strictly");
+    for (int j = 0; j < nt; ++j)
+        if (!(tf[j + 1] > tf[j])) SET_ERR(c, MASPCG_E_INVALID, "t_faces must increase strictly");
+    for (int k = 0; k < np; ++k)
+        if (!(pf[k + 1] > pf[k])) SET_ERR(c, MASPCG_E_INVALID, "p_faces must increase strictly");
+    if (!(tf[0] >= 0.0) || !(tf[nt] <= kPi)) SET_ERR(c, MASPCG_E_INVALID, "t_faces must lie in [0, pi]");
+    if (!(std::fabs((pf[np] - pf[0]) - kTwoPi) <= 1e-12 * kTwoPi))
+        SET_ERR(c, MASPCG_E_INVALID, "p_faces must span exactly 2*pi (periodic phi)");
+
+    // a1: 1-D metric (R2, R3).  Centres are face midpoints; distances between
+    // centres (half cells at the r walls, periodic wrap in phi).
+    std::vector<double> rc(nr), tc(nt), pc(np), dpg(np), hpg(np);
+    c->rf2.assign(nr + 1, 0.0);
+    c->hr.assign(nr + 1, 0.0);
+    c->dr.assign(nr, 0.0);
+    c->R3.assign(nr, 0.0);
+    for (int i = 0; i <= nr; ++i) c->rf2[i] = rf[i] * rf[i];
+    for (int i = 0; i < nr; ++i) {
+        rc[i] = 0.5 * (rf[i] + rf[i + 1]);
+        c->dr[i] = rf[i + 1] - rf[i];
+        // (r1^3 - r0^3)/3 = dr (r1^2 + r1 r0 + r0^2)/3
+        c->R3[i] = c->dr[i] * (rf[i + 1] * rf[i + 1] + rf[i + 1] * rf[i] + rf[i] * rf[i]) / 3.0;
+    }
+    c->hr[0] = rc[0] - rf[0];
+    for (int i = 1; i < nr; ++i) c->hr[i] = rc[i] - rc[i - 1];
+    c->hr[nr] = rf[nr] - rc[nr - 1];
+
+    c->C.assign(nt, 0.0);
+    c->dt.assign(nt, 0.0);
+    c->sinc.assign(nt, 0.0);
+    c->sinf.assign(nt + 1, 0.0);
+    c->ht.assign(nt + 1, 0.0);
+    for (int j = 0; j < nt; ++j) {
+        tc[j] = 0.5 * (tf[j] + tf[j + 1]);
+        c->dt[j] = tf[j + 1] - tf[j];
+        // C_j = cos t_j - cos t_{j+1} = 2 sin(tc_j) sin(dt_j / 2)
+        c->C[j] = 2.0 * std::sin(tc[j]) * std::sin(0.5 * c->dt[j]);
+        c->sinc[j] = std::sin(tc[j]);
+    }
+    for (int j = 1; j < nt; ++j) c->ht[j] = tc[j] - tc[j - 1];
+    for (int j = 0; j <= nt; ++j) c->sinf[j] = std::sin(tf[j]);
+
+    for (int k = 0; k < np; ++k) {
+        pc[k] = 0.5 * (pf[k] + pf[k + 1]);
+        dpg[k] = pf[k + 1] - pf[k];
+    }
+    for (int k = 0; k + 1 < np; ++k) hpg[k] = pc[k + 1] - pc[k];
+    hpg[np - 1] = (pc[0] + kTwoPi) - pc[np - 1];
+    c->dp_loc.assign(dpg.begin() + c->k0, dpg.begin() + c->k0 + c->nloc);
+    c->hp_loc.assign(hpg.begin() + c->k0, hpg.begin() + c->k0 + c->nloc);
+
+    c->grid_set = true;
+    c->metric_dirty = true;
+    c->coef_set = false;
+    c->D_dirty = true;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_local_extent(const maspcg_ctx *c, int *k0, int *nloc) {
+    if (!c) return MASPCG_E_INVALID;
+    if (k0) *k0 = c->k0;
+    if (nloc) *nloc = c->nloc;
+    return MASPCG_OK;
+}
+
+size_t maspcg_workspace_bytes(const maspcg_ctx *c) { return c ? layout(c, nullptr, nullptr) : 0; }
+
+maspcg_status maspcg_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!dev_ptr || ((uintptr_t)dev_ptr & 255)) SET_ERR(c, MASPCG_E_INVALID, "workspace must be 256-byte aligned");
+    const size_t need = layout(c, nullptr, nullptr);
+    if (bytes < need) SET_ERR(c, MASPCG_E_NOMEM, "workspace too small: %zu < %zu bytes", bytes, need);
+    RET_IF(bind_device(c));
+    c->ws = dev_ptr;
+    c->ws_bytes = bytes;
+    layout(c, (char *)dev_ptr, &c->a);
+    CK(c, cudaMemset(c->a.sc, 0, sizeof(Scalars)));
+    CK(c, cudaMemset(c->a.partials, 0, sizeof(double) * 4 * kRedBlocks));
+    CK(c, cudaDeviceSynchronize());
+    c->metric_dirty = true;
+    c->coef_set = false;
+    c->bc_set = false;
+    c->D_dirty = true;
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_set_coefficients(maspcg_ctx *c, const double *kr, const double *kt, const double *kp,
+                                      const double *shift, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!kr || !kt || !kp || !shift) SET_ERR(c, MASPCG_E_INVALID, "coefficient arrays must be non-NULL");
+    if (!c->grid_set || !c->ws) SET_ERR(c, MASPCG_E_STATE, "set_grid and set_workspace must precede set_coefficients");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_metric(c, st));
+    CK(c, cudaMemsetAsync(&c->a.sc->vinvalid, 0, 2 * sizeof(int), st));
+    launch_assemble(c->d, c->a, kr, kt, kp, shift, st);
+    CK(c, cudaGetLastError());
+    const size_t pl = c->d.plane;
+    if (c->nranks == 1) {
+        // face (np-1)+1/2 is the lower phi face of plane 0 (periodic, R9)
+        CK(c, cudaMemcpyAsync(c->a.Tp, c->a.Tp + (size_t)c->nloc * pl, 8 * pl, cudaMemcpyDeviceToDevice, st));
+    } else {
+        NK(c, ncclGroupStart());
+        NK(c, ncclSend(c->a.Tp + (size_t)c->nloc * pl, pl, ncclDouble, right_of(c), c->comm, st));
+        NK(c, ncclRecv(c->a.Tp, pl, ncclDouble, left_of(c), c->comm, st));
+        NK(c, ncclGroupEnd());
+        NK(c, ncclAllReduce(&c->a.sc->vinvalid, &c->a.sc->vinvalid, 2, ncclInt32, ncclMax, c->comm, st));
+    }
+    CK(c, cudaMemcpyAsync(c->vflags_host, &c->a.sc->vinvalid, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    c->stats.kernel_launches += 1;
+    c->D_dirty = true;
+    if (c->vflags_host[0]) {
+        c->coef_set = false;
+        SET_ERR(c, MASPCG_E_INVALID, "a diffusion coefficient or the shift is negative or non-finite");
+    }
+    c->any_shift = c->vflags_host[1];
+    c->coef_set = true;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_set_coefficients_host(maspcg_ctx *c, const double *kr, const double *kt, const double *kp,
+                                           const double *shift, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!kr || !kt || !kp || !shift) SET_ERR(c, MASPCG_E_INVALID, "coefficient arrays must be non-NULL");
+    if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "set_workspace must precede set_coefficients_host");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)c->nloc * c->nt * c->nr;
+    CK(c, cudaMemcpyAsync(c->a.skr, kr, 8 * (size_t)c->nloc * c->nt * (c->nr + 1), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->a.skt, kt, 8 * (size_t)c->nloc * (c->nt + 1) * c->nr, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->a.skp, kp, 8 * n, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->a.ss, shift, 8 * n, cudaMemcpyHostToDevice, st));
+    return maspcg_set_coefficients(c, c->a.skr, c->a.skt, c->a.skp, c->a.ss, stream);
+}
+
+static maspcg_status set_bc_common(maspcg_ctx *c, maspcg_bc inner, const double *gi, maspcg_bc outer,
+                                   const double *go, void *stream, cudaMemcpyKind kind) {
+    if (!c) return MASPCG_E_INVALID;
+    if ((inner != MASPCG_BC_DIRICHLET && inner != MASPCG_BC_NEUMANN0) ||
+        (outer != MASPCG_BC_DIRICHLET && outer != MASPCG_BC_NEUMANN0))
+        SET_ERR(c, MASPCG_E_INVALID, "boundary type must be DIRICHLET or NEUMANN0");
+    if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "set_workspace must precede set_bc_r");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t rows = (size_t)c->nloc * c->nt;
+    c->has_gin = (inner == MASPCG_BC_DIRICHLET && gi) ? 1 : 0;
+    c->has_gout = (outer == MASPCG_BC_DIRICHLET && go) ? 1 : 0;
+    if (c->has_gin) CK(c, cudaMemcpyAsync(c->a.gin, gi, 8 * rows, kind, st));
+    if (c->has_gout) CK(c, cudaMemcpyAsync(c->a.gout, go, 8 * rows, kind, st));
+    if (kind == cudaMemcpyHostToDevice) CK(c, cudaStreamSynchronize(st));
+    c->bc_in = inner;
+    c->bc_out = outer;
+    c->bc_set = true;
+    c->D_dirty = true;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_set_bc_r(maspcg_ctx *c, maspcg_bc inner, const double *gi, maspcg_bc outer,
+                              const double *go, void *stream) {
+    return set_bc_common(c, inner, gi, outer, go, stream, cudaMemcpyDeviceToDevice);
+}
+
+maspcg_status maspcg_set_bc_r_host(maspcg_ctx *c, maspcg_bc inner, const double *gi, maspcg_bc outer,
+                                   const double *go, void *stream) {
+    return set_bc_common(c, inner, gi, outer, go, stream, cudaMemcpyHostToDevice);
+}
+
+maspcg_status maspcg_solve(maspcg_ctx *c, const double *rhs, double *x, double tol, int maxit, double *hist,
+                           maspcg_info *info, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    RET_IF(bind_device(c));
+    return solve_impl(c, rhs, x, tol, maxit, hist, info, (cudaStream_t)stream);
+}
+
+maspcg_status maspcg_solve_host(maspcg_ctx *c, const double *rhs, double *x, double tol, int maxit, double *hist,
+                                maspcg_info *info, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!rhs || !x) SET_ERR(c, MASPCG_E_INVALID, "rhs and x must be non-NULL");
+    if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)c->nloc * c->nt * c->nr;
+    CK(c, cudaMemcpyAsync(c->a.fs, rhs, 8 * n, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->a.xs, x, 8 * n, cudaMemcpyHostToDevice, st));
+    maspcg_status s = solve_impl(c, c->a.fs, c->a.xs, tol, maxit, hist, info, st);
+    if (s < 0) return s;
+    CK(c, cudaMemcpyAsync(x, c->a.xs, 8 * n, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    return s;
+}
+
+maspcg_status maspcg_apply(maspcg_ctx *c, const double *x, double *y, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!x || !y) SET_ERR(c, MASPCG_E_INVALID, "x and y must be non-NULL");
+    const size_t n = (size_t)c->nloc * c->nt * c->nr;
+    if (overlaps(x, 8 * n, y, 8 * n)) SET_ERR(c, MASPCG_E_INVALID, "x and y must not alias");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_D(c, st));
+    launch_fill_p(c->d, c->a, x, st);
+    RET_IF(stencil_with_halo(c, y, false, false, st));
+    CK(c, cudaGetLastError());
+    c->stats.kernel_launches += 2 + (c->nranks > 1 ? 1 : 0);
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_get_operator(maspcg_ctx *c, double *Tr, double *Tt, double *Tp, double *D, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_D(c, st));
+    const int nr = c->nr, nt = c->nt, nloc = c->nloc;
+    const size_t n = (size_t)nloc * nt * nr, pl = (size_t)nt * nr, rows = (size_t)nloc * nt;
+    std::vector<double> tr(n), trb(rows), tt(n), tp(n + pl), dd(n);
+    CK(c, cudaMemcpyAsync(tr.data(), c->a.Tr, 8 * n, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaMemcpyAsync(trb.data(), c->a.TrB, 8 * rows, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaMemcpyAsync(tt.data(), c->a.Tt, 8 * n, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaMemcpyAsync(tp.data(), c->a.Tp, 8 * (n + pl), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaMemcpyAsync(dd.data(), c->a.D, 8 * n, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    for (size_t row = 0; row < rows; ++row) {
+        if (Tr) {
+            for (int i = 0; i < nr; ++i) Tr[row * (nr + 1) + i] = tr[row * nr + i];
+            Tr[row * (nr + 1) + nr] = trb[row];
+        }
+    }
+    if (Tt)
+        for (int k = 0; k < nloc; ++k) {
+            for (int j = 0; j < nt; ++j)
+                for (int i = 0; i < nr; ++i)
+                    Tt[((size_t)k * (nt + 1) + j) * nr + i] = tt[((size_t)k * nt + j) * nr + i];
+            for (int i = 0; i < nr; ++i) Tt[((size_t)k * (nt + 1) + nt) * nr + i] = 0.0;
+        }
+    if (Tp) memcpy(Tp, tp.data() + pl, 8 * n);
+    if (D) memcpy(D, dd.data(), 8 * n);
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
+    if (!c) return MASPCG_E_INVALID;
+    switch (opt) {
+        case MASPCG_OPT_CHUNK:
+            if (v < 1 || v > kMaxChunk) SET_ERR(c, MASPCG_E_INVALID, "chunk must be in [1, %d]", kMaxChunk);
+            c->chunk = (int)v;
+            break;
+        case MASPCG_OPT_USE_GRAPHS: c->use_graphs = v ? 1 : 0; break;
+        case MASPCG_OPT_TIMING: c->timing = v ? 1 : 0; break;
+        case MASPCG_OPT_STENCIL:
+            if (v < 0 || v > 2) SET_ERR(c, MASPCG_E_INVALID, "stencil variant must be 0, 1 or 2");
+            c->stencil_variant = (int)v;
+            break;
+        default: SET_ERR(c, MASPCG_E_INVALID, "unknown option %d", (int)opt);
+    }
+    if (c->timing) {
+        const size_t need = (size_t)3 * 2 * c->chunk;
+        RET_IF(bind_device(c));
+        while (c->tev.size() < need) {
+            cudaEvent_t e;
+            CK(c, cudaEventCreate(&e));
+            c->tev.push_back(e);
+        }
+    }
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_get_stats(const maspcg_ctx *c, maspcg_stats *out) {
+    if (!c || !out) return MASPCG_E_INVALID;
+    *out = c->stats;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_reset_stats(maspcg_ctx *c) {
+    if (!c) return MASPCG_E_INVALID;
+    c->stats = maspcg_stats{};
+    return MASPCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,276 @@
+"""GPU parity of libmaspcg (through the C ABI) against the CPU oracle (-m gpu).
+
+Contract (BASELINE.json north_star; SURVEY.md 8(c) "Proposed parity contract";
+DESIGN.md section 6):
+  * operator (face transmissibilities T and diagonal D): bit-identical -- both
+    sides evaluate the same formulas with one IEEE rounding per operation;
+  * y = A x: per cell |y_gpu - y_orc| <= 1e-14 * (D|x| + sum T|x_nb|) (the
+    stencil is summed in a different order with FMA);
+  * solve: solution relative L2 <= 1e-10, iteration count equal +-1, residual
+    history max_k |h_gpu - h_orc| / h_orc <= 1e-10 (all k; every case here
+    needs < 1000 iterations, the regime where the history is pinned).
+Inputs are the seeded generators of paper_2303_03398_b200/inputs.py.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2303_03398_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+SOL_TOL = 1e-10
+HIST_TOL = 1e-10
+APPLY_TOL = 1e-14
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("-m gpu tests need a CUDA device")
+    from paper_2303_03398_b200 import build
+    build.build()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def M(torch_cuda):
+    from paper_2303_03398_b200 import maspcg
+    return maspcg
+
+
+def dev(torch, a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_solve(torch, M, prob, tol=None, maxit=None, chunk=16, x0=None, opts=None):
+    S = M.solver_for_problem(prob, chunk=chunk)
+    for k, v in (opts or {}).items():
+        S.set_option(k, v)
+    x = dev(torch, prob.x0 if x0 is None else x0)
+    st, info, hist = S.solve(dev(torch, prob.f), x, prob.tol if tol is None else tol,
+                             prob.maxit if maxit is None else maxit, raise_on_error=False)
+    torch.cuda.synchronize()
+    return st, info, hist, x.cpu().numpy(), S
+
+
+def assert_solve_parity(g, o):
+    st, info, hist, x, _ = g
+    assert st == o["status"], (st, o["status"])
+    assert abs(info["iters"] - o["iters"]) <= 1, (info["iters"], o["iters"])
+    nx = np.linalg.norm(o["x"])
+    assert np.linalg.norm(x - o["x"]) <= SOL_TOL * max(nx, 1e-300), np.linalg.norm(x - o["x"]) / nx
+    k = min(hist.size, o["hist"].size)
+    rel = np.abs(hist[:k] - o["hist"][:k]) / np.maximum(o["hist"][:k], 1e-300)
+    assert rel.max() <= HIST_TOL, (rel.max(), int(rel.argmax()))
+    assert info["bnorm"] == pytest.approx(o["bnorm"], rel=1e-13)
+
+
+RANDOM_SHAPES = [(13, 7, 5), (33, 17, 9), (1, 5, 6), (6, 1, 4), (5, 4, 1), (1, 1, 7), (40, 3, 2), (64, 32, 8)]
+
+
+@pytest.mark.parametrize("shape", RANDOM_SHAPES)
+@pytest.mark.parametrize("bc", [(0, 1), (0, 0), (1, 0)])
+def test_operator_bitwise_identical(torch_cuda, M, oracle_mod, shape, bc):
+    nr, nt, np_ = shape
+    p = inputs.random_problem(nr, nt, np_, 100 + nr + nt + np_, bc_in=bc[0], bc_out=bc[1])
+    S = M.solver_for_problem(p)
+    Tr, Tt, Tp, D = S.get_operator()
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, *bc)
+    assert np.array_equal(Tr, op.Tr)
+    assert np.array_equal(Tt, op.Tt)
+    assert np.array_equal(Tp, op.Tp)
+    assert np.array_equal(D, op.D)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_operator_bitwise_configs(torch_cuda, M, oracle_mod, name):
+    p = inputs.make_problem(name)
+    S = M.solver_for_problem(p)
+    got = S.get_operator()
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, p.bc_in, p.bc_out)
+    for g, o in zip(got, (op.Tr, op.Tt, op.Tp, op.D)):
+        assert np.array_equal(g, o)
+
+
+def apply_err(op, x, y):
+    mag = 2.0 * op.D * np.abs(x) - op.apply(np.abs(x))     # D|x| + sum T|x_nb| (T, D >= 0)
+    return np.abs(y - op.apply(x)) / np.maximum(mag, 1e-300)
+
+
+@pytest.mark.parametrize("shape", RANDOM_SHAPES + [(150, 30, 12)])
+def test_apply_parity(torch_cuda, M, oracle_mod, shape):
+    torch = torch_cuda
+    nr, nt, np_ = shape
+    p = inputs.random_problem(nr, nt, np_, 7 + nr, bc_in=0, bc_out=1)
+    S = M.solver_for_problem(p)
+    x = np.random.default_rng(nr * nt).standard_normal((np_, nt, nr))
+    y = S.apply(dev(torch, x)).cpu().numpy()
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, 0, 1)
+    assert apply_err(op, x, y).max() <= APPLY_TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_solve_parity_configs(torch_cuda, M, oracle_mod, name):
+    p = inputs.make_problem(name)
+    o = oracle_mod.solve_problem(p)
+    assert o["status"] == 0
+    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+
+
+@pytest.mark.parametrize("seed,shape,bc", [(1, (13, 7, 5), (0, 1)), (2, (33, 17, 9), (0, 0)),
+                                          (3, (8, 12, 16), (1, 0)), (4, (5, 4, 1), (0, 1)),
+                                          (5, (1, 9, 6), (1, 1)), (6, (20, 1, 3), (0, 0))])
+def test_solve_parity_random(torch_cuda, M, oracle_mod, seed, shape, bc):
+    nr, nt, np_ = shape
+    p = inputs.random_problem(nr, nt, np_, seed, bc_in=bc[0], bc_out=bc[1])
+    o = oracle_mod.solve_problem(p)
+    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+
+
+def test_solve_parity_warm_start(torch_cuda, M, oracle_mod):
+    p = inputs.make_problem("c2", x0_seed=9)
+    o = oracle_mod.solve_problem(p)
+    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+
+
+@pytest.mark.parametrize("chunk,graphs,timing", [(1, 1, 0), (3, 1, 0), (16, 0, 0), (64, 1, 0), (7, 1, 1)])
+def test_solve_loop_modes_identical(torch_cuda, M, oracle_mod, chunk, graphs, timing):
+    """Chunking, graph replay and timing mode change how kernels are issued, never the bits."""
+    p = inputs.make_problem("c1")
+    ref = gpu_solve(torch_cuda, M, p, chunk=16)
+    g = gpu_solve(torch_cuda, M, p, chunk=chunk, opts={M.OPT_USE_GRAPHS: graphs, M.OPT_TIMING: timing})
+    assert g[0] == ref[0] and g[1]["iters"] == ref[1]["iters"]
+    assert np.array_equal(g[2], ref[2]) and np.array_equal(g[3], ref[3])
+    if timing:
+        st = g[4].stats()
+        assert st["matvec_launches"] == g[1]["iters"]
+        assert st["matvec_ms"] > 0 and st["update_ms"] > 0 and st["pupdate_ms"] > 0
+
+
+def test_deterministic_run_to_run(torch_cuda, M):
+    p = inputs.make_problem("c2")
+    a = gpu_solve(torch_cuda, M, p)
+    b = gpu_solve(torch_cuda, M, p)
+    assert np.array_equal(a[3], b[3]) and np.array_equal(a[2], b[2])
+
+
+def test_edge_cases(torch_cuda, M, oracle_mod):
+    torch = torch_cuda
+    p = inputs.random_problem(9, 6, 8, 77)
+    o = oracle_mod.solve_problem(p)
+    S = M.solver_for_problem(p)
+    f = dev(torch, p.f)
+    # tol = 0: exactly maxit iterations
+    x = dev(torch, p.x0)
+    st, info, hist = S.solve(f, x, 0.0, 5)
+    oo = oracle_mod.solve_problem(p, tol=0.0, maxit=5)
+    assert st == M.NOT_CONVERGED == oo["status"] and info["iters"] == 5 and hist.size == 6
+    np.testing.assert_allclose(hist, oo["hist"], rtol=1e-12)
+    np.testing.assert_allclose(x.cpu().numpy(), oo["x"], rtol=0, atol=1e-12 * np.abs(oo["x"]).max())
+    # maxit = 0: only hist[0]
+    x = dev(torch, p.x0)
+    st, info, hist = S.solve(f, x, 1e-10, 0)
+    assert st == M.NOT_CONVERGED and info["iters"] == 0 and hist[0] == pytest.approx(o["hist"][0], rel=1e-13)
+    # b = 0 (f = 0, g = 0): x = 0, OK, 0 iterations
+    S0 = M.solver_for_problem(inputs.random_problem(9, 6, 8, 77, bc_in=1, bc_out=1))
+    x = dev(torch, np.ones((8, 6, 9)))
+    st, info, hist = S0.solve(dev(torch, np.zeros((8, 6, 9))), x, 1e-10, 50)
+    assert st == M.OK and info["iters"] == 0 and not x.cpu().numpy().any()
+    # converged initial guess: 0 iterations, x untouched
+    x = dev(torch, o["x"])
+    st, info, hist = S.solve(f, x, 1e-6, 50)
+    assert st == M.OK and info["iters"] == 0 and np.array_equal(x.cpu().numpy(), o["x"])
+    # non-finite rhs -> breakdown
+    fb = p.f.copy()
+    fb[3, 2, 1] = np.nan
+    x = dev(torch, p.x0)
+    st, info, hist = S.solve(dev(torch, fb), x, 1e-10, 50, raise_on_error=False)
+    assert st == M.E_BREAKDOWN
+    # aliasing and bad arguments
+    with pytest.raises(M.MaspcgError) as e:
+        S.solve(f, f, 1e-10, 5)
+    assert e.value.status == M.E_INVALID
+    with pytest.raises(M.MaspcgError):
+        S.solve(f, dev(torch, p.x0), -1.0, 5)
+
+
+def test_error_paths(torch_cuda, M):
+    torch = torch_cuda
+    p = inputs.random_problem(6, 5, 4, 5, shift=False, bc_in=1, bc_out=1)
+    S = M.Solver(p.nr, p.nt, p.np, p.rf, p.tf, p.pf)
+    x = dev(torch, p.x0)
+    with pytest.raises(M.MaspcgError) as e:       # solve before coefficients
+        S.solve(dev(torch, p.f), x, 1e-10, 5)
+    assert e.value.status == M.E_STATE
+    S.set_coefficients(dev(torch, p.kr), dev(torch, p.kt), dev(torch, p.kp), dev(torch, p.s))
+    S.set_bc_r(1, None, 1, None)
+    with pytest.raises(M.MaspcgError) as e:       # s == 0 and Neumann on both sides
+        S.solve(dev(torch, p.f), x, 1e-10, 5)
+    assert e.value.status == M.E_SINGULAR
+    S.set_bc_r(0, None, 1, None)                   # a Dirichlet side makes it definite
+    st, info, hist = S.solve(dev(torch, p.f), x, 1e-10, 500)
+    assert st == M.OK
+    kr = p.kr.copy()
+    kr[1, 2, 3] = -1.0
+    with pytest.raises(M.MaspcgError) as e:
+        S.set_coefficients(dev(torch, kr), dev(torch, p.kt), dev(torch, p.kp), dev(torch, p.s))
+    assert e.value.status == M.E_INVALID
+    bad = p.pf.copy()
+    bad[-1] = 6.0
+    with pytest.raises(M.MaspcgError) as e:
+        S.set_grid(p.rf, p.tf, bad)
+    assert e.value.status == M.E_INVALID
+
+
+def test_host_entry_points(torch_cuda, M, oracle_mod):
+    """maspcg_set_coefficients_host / maspcg_solve_host: identical bits to the device entry points."""
+    p = inputs.make_problem("c1")
+    ref = gpu_solve(torch_cuda, M, p)
+    S = M.Solver(p.nr, p.nt, p.np, p.rf, p.tf, p.pf)
+    S.set_coefficients(p.kr, p.kt, p.kp, p.s)
+    S.set_bc_r(p.bc_in, None, p.bc_out, None)
+    x = p.x0.copy()
+    st, info, hist = S.solve(p.f, x, p.tol, p.maxit)
+    assert st == ref[0] and info["iters"] == ref[1]["iters"]
+    assert np.array_equal(x, ref[3]) and np.array_equal(hist, ref[2])
+
+
+@pytest.mark.slow
+def test_solve_parity_c3_half_resolution(torch_cuda, M, oracle_mod):
+    """c3 recipe (coronal viscosity, stretched grid) at 75 x 150 x 300 = 3.4 M cells."""
+    p = inputs.make_problem("c3", shape=(75, 150, 300))
+    o = oracle_mod.solve_problem(p)
+    assert o["status"] == 0 and o["iters"] < 1000
+    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+
+
+@pytest.mark.slow
+def test_c3_full_size(torch_cuda, M, oracle_mod):
+    """The bench workload (c3, 150 x 300 x 600 = 27 M cells) in the bench's launch configuration:
+    20 fixed iterations against the oracle, then the full solve checked by its true residual."""
+    torch = torch_cuda
+    p = inputs.make_problem("c3")
+    S = M.solver_for_problem(p)
+    f = dev(torch, p.f)
+    # (1) 20 iterations, tol = 0
+    x = dev(torch, p.x0)
+    st, info, hist = S.solve(f, x, 0.0, 20)
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, p.bc_in, p.bc_out)
+    b = op.rhs(p.f, p.g_in, p.g_out)
+    ost, ox, oit, ohist, obn, orn = op.pcg(b, p.x0, 0.0, 20)
+    xg = x.cpu().numpy()
+    assert info["iters"] == oit == 20
+    assert np.linalg.norm(xg - ox) <= SOL_TOL * np.linalg.norm(ox)
+    assert (np.abs(hist - ohist) / ohist).max() <= HIST_TOL
+    # (2) apply at full size, sampled cells vs the oracle's full apply
+    y = S.apply(x).cpu().numpy()
+    assert apply_err(op, xg, y).max() <= APPLY_TOL
+    # (3) full solve to 1e-10: converged, and the true residual b - A x agrees with the recurrence
+    x = dev(torch, p.x0)
+    st, info, hist = S.solve(f, x, p.tol, p.maxit)
+    assert st == M.OK and hist[-1] <= p.tol * info["bnorm"]
+    true_r = np.linalg.norm(b - op.apply(x.cpu().numpy())) / np.linalg.norm(b)
+    assert true_r <= 2 * p.tol
