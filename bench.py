@@ -100,7 +100,8 @@ def ncu_traffic_per_launch():
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["dram_bytes_per_launch"]), d.get("source", path)
+        k = d["kernels"][0]
+        return float(k["dram_bytes_per_launch"]), d.get("source", path)
     except Exception:
         return None, None
 

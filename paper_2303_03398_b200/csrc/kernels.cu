@@ -25,6 +25,8 @@ namespace maspcg {
 
 namespace {
 
+constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -97,17 +99,17 @@ __device__ __forceinline__ void decompose(const Dims &d, uint32_t c, int &i, int
 
 // Write a freshly computed p value of local cell c (plane k) into the padded
 // p array and, on a single rank, into the periodic halo copies.
-__device__ __forceinline__ void store_p(const Dims &d, double *p, uint32_t c, int k, double v) {
+__device__ __forceinline__ void store_p(const Dims &d, double *p, uint32_t c, double v) {
     p[(size_t)c + d.plane] = v;
     if (d.periodic_local) {
-        if (k == 0) p[(size_t)c + (size_t)(d.nloc + 1) * d.plane] = v;          // hi halo <- first plane
-        if (k == d.nloc - 1) p[(size_t)c - (size_t)(d.nloc - 1) * d.plane] = v; // lo halo <- last plane
+        if (c < d.plane) p[(size_t)c + (size_t)(d.nloc + 1) * d.plane] = v;    // hi halo <- first plane
+        if (c >= d.n - d.plane) p[(size_t)c - (size_t)(d.nloc - 1) * d.plane] = v; // lo halo <- last plane
     }
 }
 
 // ---------------------------------------------------------------- assembly
 // SURVEY 8(c) item 3 (R3-R5, R8): face transmissibilities, s*V, validation.
-__global__ void __launch_bounds__(kThreads) k_assemble(Dims d, DevArrays a, const double *__restrict__ kr,
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_assemble(Dims d, DevArrays a, const double *__restrict__ kr,
                                                        const double *__restrict__ kt,
                                                        const double *__restrict__ kp,
                                                        const double *__restrict__ s) {
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Dims d, DevArrays a, cons
 }
 
 // D = sV + Tr_lo + Tr_hi + Tt_lo + Tt_hi + Tp_lo + Tp_hi  (R7, R10)
-__global__ void __launch_bounds__(kThreads) k_finalize_D(Dims d, DevArrays a, int bc_in, int bc_out) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_finalize_D(Dims d, DevArrays a, int bc_in, int bc_out) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
         int i, j, k;
@@ -181,11 +183,10 @@ __global__ void __launch_bounds__(kThreads) k_finalize_D(Dims d, DevArrays a, in
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_fill_p(Dims d, DevArrays a, const double *__restrict__ x) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_fill_p(Dims d, DevArrays a, const double *__restrict__ x) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
-        const int k = (int)(c / d.plane);
-        store_p(d, a.p, c, k, x[c]);
+        store_p(d, a.p, c, x[c]);
     }
 }
 
@@ -198,7 +199,7 @@ struct Range {
 };
 
 template <bool WITH_DOT, bool LOOP>
-__global__ void __launch_bounds__(kThreads) k_matvec_flat(Dims d, DevArrays a, double *__restrict__ y, Range rg,
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_matvec_flat(Dims d, DevArrays a, double *__restrict__ y, Range rg,
                                                           unsigned red_slot0, unsigned red_total) {
     if (LOOP && *(volatile int *)&a.sc->done) return;
     const double *__restrict__ p = a.p;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kThreads) k_matvec_flat(Dims d, DevArrays a, d
 // ---------------------------------------------------------------- setup of a solve
 // b = V f + Dirichlet face terms (R5); r0 = b - q (q = A x0); z0 = r0/D; p0 = z0;
 // partials r.z, r.r, b.b -> sc->red3.
-__global__ void __launch_bounds__(kThreads) k_setup_residual(Dims d, DevArrays a, const double *__restrict__ f,
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_setup_residual(Dims d, DevArrays a, const double *__restrict__ f,
                                                              int din, int dout, unsigned total) {
     double rz = 0.0, rr = 0.0, bb = 0.0;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(kThreads) k_setup_residual(Dims d, DevArrays a
         const double r = b - a.q[c];
         const double z = r / a.D[c];
         a.r[c] = r;
-        store_p(d, a.p, c, k, z);
+        store_p(d, a.p, c, z);
         rz = fma(r, z, rz);
         rr = fma(r, r, rr);
         bb = fma(b, b, bb);
@@ -305,7 +306,7 @@ __global__ void k_setup_scalars(DevArrays a, double tol, int maxit) {
 
 // ---------------------------------------------------------------- PCG loop
 // alpha = rho / p.Ap; x += alpha p; r -= alpha q; z = r / D; partials r.z, r.r.
-__global__ void __launch_bounds__(kThreads) k_update(Dims d, DevArrays a, double *__restrict__ x, unsigned total) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_update(Dims d, DevArrays a, double *__restrict__ x, unsigned total) {
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
     const double pi = sc->red1[0];
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kThreads) k_update(Dims d, DevArrays a, double
 
 // Convergence test on ||r|| (R12); beta = r.z / rho (R11); p = r/D + beta p.
 // The last block advances the iteration counter and the scalars.
-__global__ void __launch_bounds__(kThreads) k_pupdate(Dims d, DevArrays a, int chunk, unsigned total) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArrays a, int chunk, unsigned total) {
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
     const double rz = sc->red2[0], rr = sc->red2[1];
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_pupdate(Dims d, DevArrays a, int c
         for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
             const double pold = a.p[(size_t)c + d.plane];
             const double pn = fma(beta, pold, __ldg(r + c) / __ldg(D + c));
-            store_p(d, a.p, c, (int)(c / d.plane), pn);
+            store_p(d, a.p, c, pn);
         }
     }
     __shared__ bool am_last;
@@ -389,7 +390,7 @@ __global__ void __launch_bounds__(kThreads) k_pupdate(Dims d, DevArrays a, int c
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_zero_x_if(Dims d, DevArrays a, double *__restrict__ x) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_zero_x_if(Dims d, DevArrays a, double *__restrict__ x) {
     if (!a.sc->zero_x) return;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) x[c] = 0.0;

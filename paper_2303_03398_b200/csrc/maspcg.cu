@@ -57,6 +57,7 @@ struct maspcg_ctx {
 
     // streams, events, host snapshots
     cudaStream_t comm_stream = nullptr;
+    cudaStream_t cap_stream = nullptr;   // graphs are captured here (the caller's may be the legacy stream)
     cudaEvent_t ev_p = nullptr, ev_halo = nullptr, ev_chunk[2] = {nullptr, nullptr};
     Scalars *snap[2] = {nullptr, nullptr};
     int *vflags_host = nullptr;
@@ -64,7 +65,6 @@ struct maspcg_ctx {
     // graph cache (one captured chunk of `chunk` iterations)
     cudaGraphExec_t gexec = nullptr;
     const void *g_x = nullptr;
-    cudaStream_t g_stream = nullptr;
     int g_chunk = 0, g_variant = -1;
 
     // options
@@ -261,17 +261,17 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st) {
         CK(c, cudaGetLastError());
         return MASPCG_OK;
     }
-    if (!c->gexec || c->g_x != x || c->g_stream != st || c->g_chunk != c->chunk ||
-        c->g_variant != c->stencil_variant) {
+    if (!c->gexec || c->g_x != x || c->g_chunk != c->chunk || c->g_variant != c->stencil_variant) {
         if (c->gexec) {
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
         }
         cudaGraph_t g = nullptr;
-        CK(c, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t cs = c->cap_stream;
+        CK(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         maspcg_status s = MASPCG_OK;
-        for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_iteration(c, x, st, it);
-        cudaError_t e = cudaStreamEndCapture(st, &g);
+        for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_iteration(c, x, cs, it);
+        cudaError_t e = cudaStreamEndCapture(cs, &g);
         if (s != MASPCG_OK) {
             if (g) cudaGraphDestroy(g);
             return s;
@@ -281,7 +281,6 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st) {
         cudaGraphDestroy(g);
         CK(c, ei);
         c->g_x = x;
-        c->g_stream = st;
         c->g_chunk = c->chunk;
         c->g_variant = c->stencil_variant;
     }
@@ -448,6 +447,7 @@ maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const 
     c->k0 = rank * (int)nloc;
     cudaError_t e = cudaSetDevice(cuda_device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_chunk[0], cudaEventDisableTiming);
@@ -498,6 +498,7 @@ maspcg_status maspcg_destroy(maspcg_ctx *c) {
     }
     if (c->vflags_host) cudaFreeHost(c->vflags_host);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     delete c;
     return MASPCG_OK;
 }
