@@ -216,6 +216,22 @@ MASPCG_API maspcg_status maspcg_solve_host(maspcg_ctx *ctx, const double *rhs, d
 MASPCG_API maspcg_status maspcg_apply(maspcg_ctx *ctx, const double *x, double *y,
                                       void *cuda_stream);
 
+/* ---- in-process multi-rank emulation (TEST ONLY) ------------------------------ */
+
+/* A loopback group lets `nranks` contexts live in ONE process on ONE device, one
+ * host thread per rank, exchanging halos and all-reduce operands by device-to-
+ * device copies and fixed-order sums instead of NCCL.  It exists so the phi-slab
+ * decomposition (halo planes, split interior/boundary stencil, all-reduced
+ * scalars) can be verified against the oracle on a single GPU.
+ * Every rank must call every function concurrently from its own thread, as with
+ * MPI.  Loopback contexts never use CUDA graphs.  The group must outlive its
+ * contexts.  nranks in [1, 16]. */
+MASPCG_API maspcg_status maspcg_loopback_group_create(int nranks, void **group);
+MASPCG_API maspcg_status maspcg_loopback_group_destroy(void *group);
+/* As maspcg_create, but joined to a loopback group instead of an NCCL communicator. */
+MASPCG_API maspcg_status maspcg_create_loopback(int nr, int nt, int np, int rank, int nranks, void *group,
+                                                int cuda_device, maspcg_ctx **out);
+
 /* ---- introspection ------------------------------------------------------------ */
 
 /* Copy the assembled local operator to HOST arrays in the oracle's face

@@ -1,0 +1,44 @@
+// comm.cuh -- communication layer of libmaspcg: the phi-slab halo exchange
+// and the scalar all-reduces of the PCG, behind one interface with two implementations:
+//   * NcclComm      -- production: grouped ncclSend/ncclRecv and ncclAllReduce over NVLink /
+//                      NVSwitch, one process per GPU (the CUDA-aware MPI halo exchange of
+//                      PAPER.md:282, 290-292 re-done B200-first);
+//   * LoopbackComm  -- test-only: several ranks in ONE process on ONE device (one host thread
+//                      per rank), exchanging through device-to-device copies and fixed-order
+//                      sums.  It lets the multi-rank decomposition (slabs, halos, split stencil,
+//                      all-reduced scalars) be checked against the oracle on a single GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+namespace maspcg {
+
+class Comm {
+   public:
+    virtual ~Comm() = default;
+    int rank = 0, nranks = 1;
+    int left() const { return (rank + nranks - 1) % nranks; }
+    int right() const { return (rank + 1) % nranks; }
+    // May the calls be captured into a CUDA graph?
+    virtual bool capturable() const = 0;
+    // Padded array buf[nloc+2][plane]: buf[0] <- left's plane nloc (its last local plane),
+    // buf[nloc+1] <- right's plane 1 (its first local plane).
+    virtual int halo_padded(double *buf, size_t plane, int nloc, cudaStream_t st, std::string &err) = 0;
+    // recv[count] <- left's send[count] (ring shift towards higher ranks).
+    virtual int shift_right(const double *send, double *recv, size_t count, cudaStream_t st, std::string &err) = 0;
+    // In-place sum / max over ranks; every rank receives identical bits.
+    virtual int allreduce_sum(double *dev, int count, cudaStream_t st, std::string &err) = 0;
+    virtual int allreduce_max(int *dev, int count, cudaStream_t st, std::string &err) = 0;
+};
+
+// Returns nullptr and sets *status / err on failure.
+Comm *make_nccl_comm(const void *unique_id, int rank, int nranks, int *status, std::string &err);
+
+struct LoopbackGroup;
+LoopbackGroup *loopback_group_create(int nranks);
+void loopback_group_destroy(LoopbackGroup *g);
+Comm *make_loopback_comm(LoopbackGroup *g, int rank, int nranks, int *status, std::string &err);
+
+}  // namespace maspcg

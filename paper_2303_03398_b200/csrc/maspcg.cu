@@ -8,7 +8,7 @@
 // the host only precomputes O(nr + nt + np) 1-D metric factors (SURVEY 8(a)
 // a1, "negligible (setup)").
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include <nccl.h>   // ncclGetUniqueId only; the communicator lives in comm.cu
 
 #include <cmath>
 #include <cstdio>
@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/maspcg.h"
+#include "comm.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -35,7 +36,7 @@ thread_local std::string g_create_error;
 struct maspcg_ctx {
     int nr = 0, nt = 0, np = 0, rank = 0, nranks = 1, device = 0;
     int k0 = 0, nloc = 0;
-    ncclComm_t comm = nullptr;
+    Comm *comm = nullptr;            // nullptr when nranks == 1
     std::string err;
 
     // grid (host copies of the 1-D metric)
@@ -87,14 +88,6 @@ struct maspcg_ctx {
         if (_e != cudaSuccess)                                                                       \
             SET_ERR(ctx, MASPCG_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, \
                     __LINE__);                                                                       \
-    } while (0)
-
-#define NK(ctx, call)                                                                                  \
-    do {                                                                                               \
-        ncclResult_t _r = (call);                                                                      \
-        if (_r != ncclSuccess)                                                                         \
-            SET_ERR(ctx, MASPCG_E_NCCL, "%s failed: %s (%s:%d)", #call, ncclGetErrorString(_r), __FILE__, \
-                    __LINE__);                                                                         \
     } while (0)
 
 #define RET_IF(st)                       \
@@ -178,28 +171,20 @@ maspcg_status ensure_metric(maspcg_ctx *c, cudaStream_t st) {
     return MASPCG_OK;
 }
 
-int left_of(const maspcg_ctx *c) { return (c->rank + c->nranks - 1) % c->nranks; }
-int right_of(const maspcg_ctx *c) { return (c->rank + 1) % c->nranks; }
+#define COMM(ctx, call)                                        \
+    do {                                                       \
+        int _s = (call);                                       \
+        if (_s != ST_OK) return (maspcg_status)_s;             \
+    } while (0)
 
-// Exchange the boundary planes of a padded [nloc+2][nt][nr] array (plane 0 and
-// nloc+1 are halos).  Ops to the same peer are matched in issue order, so the
-// order below is also correct when left == right (P = 2): the first send and
-// the first receive between a pair carry "first plane -> hi halo".
 maspcg_status halo_padded(maspcg_ctx *c, double *buf, cudaStream_t st) {
-    const size_t pl = (size_t)c->nt * c->nr;
-    const int L = left_of(c), R = right_of(c);
-    NK(c, ncclGroupStart());
-    NK(c, ncclSend(buf + pl, pl, ncclDouble, L, c->comm, st));                       // my first plane
-    NK(c, ncclRecv(buf + (size_t)(c->nloc + 1) * pl, pl, ncclDouble, R, c->comm, st)); // right's first -> hi halo
-    NK(c, ncclSend(buf + (size_t)c->nloc * pl, pl, ncclDouble, R, c->comm, st));      // my last plane
-    NK(c, ncclRecv(buf, pl, ncclDouble, L, c->comm, st));                            // left's last -> lo halo
-    NK(c, ncclGroupEnd());
+    COMM(c, c->comm->halo_padded(buf, (size_t)c->nt * c->nr, c->nloc, st, c->err));
     return MASPCG_OK;
 }
 
-maspcg_status allreduce_sum(maspcg_ctx *c, double *dev, size_t count, cudaStream_t st) {
+maspcg_status allreduce_sum(maspcg_ctx *c, double *dev, int count, cudaStream_t st) {
     if (c->nranks == 1) return MASPCG_OK;
-    NK(c, ncclAllReduce(dev, dev, count, ncclDouble, ncclSum, c->comm, st));
+    COMM(c, c->comm->allreduce_sum(dev, count, st, c->err));
     return MASPCG_OK;
 }
 
@@ -420,8 +405,8 @@ maspcg_status maspcg_get_unique_id(void *out) {
     return MASPCG_OK;
 }
 
-maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const void *nccl_unique_id,
-                            int cuda_device, maspcg_ctx **out) {
+static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, const void *nccl_unique_id,
+                                 void *group, int cuda_device, maspcg_ctx **out) {
     if (!out) return MASPCG_E_INVALID;
     *out = nullptr;
     auto fail = [](maspcg_status s, const char *m) {
@@ -431,7 +416,7 @@ maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const 
     if (nr < 1 || nt < 1 || np < 1) return fail(MASPCG_E_INVALID, "nr, nt, np must be >= 1");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(MASPCG_E_INVALID, "bad rank / nranks");
     if (np % nranks != 0) return fail(MASPCG_E_INVALID, "np must be divisible by nranks");
-    if ((nranks > 1) != (nccl_unique_id != nullptr))
+    if (!group && (nranks > 1) != (nccl_unique_id != nullptr))
         return fail(MASPCG_E_INVALID, "nccl_unique_id must be given iff nranks > 1");
     const long long nloc = np / nranks;
     if ((nloc + 2) * (long long)nt * nr >= (1ll << 31))
@@ -461,15 +446,14 @@ maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const 
         return MASPCG_E_CUDA;
     }
     if (nranks > 1) {
-        ncclUniqueId id;
-        memcpy(&id, nccl_unique_id, sizeof(id));
-        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
-        if (r != ncclSuccess) {
-            g_create_error = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
-            c->comm = nullptr;
+        int st = ST_OK;
+        c->comm = group ? make_loopback_comm((LoopbackGroup *)group, rank, nranks, &st, g_create_error)
+                        : make_nccl_comm(nccl_unique_id, rank, nranks, &st, g_create_error);
+        if (!c->comm) {
             maspcg_destroy(c);
-            return MASPCG_E_NCCL;
+            return (maspcg_status)st;
         }
+        if (!c->comm->capturable()) c->use_graphs = 0;
     }
     c->d.nr = nr;
     c->d.nt = nt;
@@ -484,10 +468,39 @@ maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const 
     return MASPCG_OK;
 }
 
+maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const void *nccl_unique_id,
+                            int cuda_device, maspcg_ctx **out) {
+    return create_impl(nr, nt, np, rank, nranks, nccl_unique_id, nullptr, cuda_device, out);
+}
+
+maspcg_status maspcg_loopback_group_create(int nranks, void **group) {
+    if (!group) return MASPCG_E_INVALID;
+    *group = loopback_group_create(nranks);
+    if (!*group) {
+        g_create_error = "loopback group size must be in [1, 16]";
+        return MASPCG_E_INVALID;
+    }
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_loopback_group_destroy(void *group) {
+    loopback_group_destroy((LoopbackGroup *)group);
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_create_loopback(int nr, int nt, int np, int rank, int nranks, void *group, int cuda_device,
+                                     maspcg_ctx **out) {
+    if (!group) {
+        g_create_error = "loopback group must be non-NULL";
+        return MASPCG_E_INVALID;
+    }
+    return create_impl(nr, nt, np, rank, nranks, nullptr, group, cuda_device, out);
+}
+
 maspcg_status maspcg_destroy(maspcg_ctx *c) {
     if (!c) return MASPCG_OK;
     cudaSetDevice(c->device);
-    if (c->comm) ncclCommDestroy(c->comm);
+    delete c->comm;
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
     if (c->ev_p) cudaEventDestroy(c->ev_p);
@@ -618,11 +631,9 @@ maspcg_status maspcg_set_coefficients(maspcg_ctx *c, const double *kr, const dou
         // face (np-1)+1/2 is the lower phi face of plane 0 (periodic, R9)
         CK(c, cudaMemcpyAsync(c->a.Tp, c->a.Tp + (size_t)c->nloc * pl, 8 * pl, cudaMemcpyDeviceToDevice, st));
     } else {
-        NK(c, ncclGroupStart());
-        NK(c, ncclSend(c->a.Tp + (size_t)c->nloc * pl, pl, ncclDouble, right_of(c), c->comm, st));
-        NK(c, ncclRecv(c->a.Tp, pl, ncclDouble, left_of(c), c->comm, st));
-        NK(c, ncclGroupEnd());
-        NK(c, ncclAllReduce(&c->a.sc->vinvalid, &c->a.sc->vinvalid, 2, ncclInt32, ncclMax, c->comm, st));
+        // the face below plane 0 is the last face of the left neighbour's slab
+        COMM(c, c->comm->shift_right(c->a.Tp + (size_t)c->nloc * pl, c->a.Tp, pl, st, c->err));
+        COMM(c, c->comm->allreduce_max(&c->a.sc->vinvalid, 2, st, c->err));
     }
     CK(c, cudaMemcpyAsync(c->vflags_host, &c->a.sc->vinvalid, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(c, cudaStreamSynchronize(st));

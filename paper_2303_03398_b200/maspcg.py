@@ -74,6 +74,9 @@ SIGNATURES = {
     "maspcg_get_stats": ([_V, ctypes.POINTER(Stats)], _I),
     "maspcg_reset_stats": ([_V], _I),
     "maspcg_version": ([], ctypes.c_char_p),
+    "maspcg_loopback_group_create": ([_I, ctypes.POINTER(_V)], _I),
+    "maspcg_loopback_group_destroy": ([_V], _I),
+    "maspcg_create_loopback": ([_I, _I, _I, _I, _I, _V, _I, ctypes.POINTER(_V)], _I),
 }
 
 _lib = None
@@ -127,18 +130,30 @@ class Solver:
     torch's current device)."""
 
     def __init__(self, nr: int, nt: int, np_: int, rf, tf, pf, *, group=None, device: int | None = None,
-                 chunk: int = 16):
+                 chunk: int = 16, loopback: "tuple[LoopbackGroup, int] | None" = None):
         import torch
         import torch.distributed as dist
         self._L = lib()
+        self.ctx = None
         if not torch.cuda.is_available():
             raise MaspcgError(E_CUDA, "no CUDA device visible (libmaspcg has no CPU fallback)")
-        if dist.is_available() and dist.is_initialized() and (group is not None or dist.get_world_size() > 1):
+        if loopback is not None:
+            lgroup, self.rank = loopback
+            self.nranks = lgroup.nranks
+        elif dist.is_available() and dist.is_initialized() and (group is not None or dist.get_world_size() > 1):
             self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
         else:
             self.rank, self.nranks = 0, 1
         self.device = torch.cuda.current_device() if device is None else int(device)
         uid = None
+        if loopback is not None:
+            ctx = ctypes.c_void_p()
+            st = self._L.maspcg_create_loopback(nr, nt, np_, self.rank, self.nranks, lgroup.handle, self.device,
+                                                ctypes.byref(ctx))
+            if st != OK:
+                raise MaspcgError(st, self._L.maspcg_last_error(None).decode())
+            self._init_after_create(ctx, nr, nt, np_, rf, tf, pf, chunk)
+            return
         if self.nranks > 1:
             buf = ctypes.create_string_buffer(128)
             if self.rank == 0:
@@ -151,6 +166,10 @@ class Solver:
         st = self._L.maspcg_create(nr, nt, np_, self.rank, self.nranks, uid, self.device, ctypes.byref(ctx))
         if st != OK:
             raise MaspcgError(st, self._L.maspcg_last_error(None).decode())
+        self._init_after_create(ctx, nr, nt, np_, rf, tf, pf, chunk)
+
+    def _init_after_create(self, ctx, nr, nt, np_, rf, tf, pf, chunk):
+        import torch
         self.ctx = ctx
         self.nr, self.nt, self.np = nr, nt, np_
         k0, nloc = ctypes.c_int(), ctypes.c_int()
@@ -246,11 +265,30 @@ class Solver:
         self._check(self._L.maspcg_reset_stats(self.ctx))
 
 
-def solver_for_problem(prob, *, group=None, device=None, chunk=16, stream=None):
+class LoopbackGroup:
+    """In-process multi-rank emulation on one device (maspcg_loopback_group_create; TEST ONLY):
+    one Solver(..., loopback=(group, rank)) per rank, each driven from its own host thread."""
+
+    def __init__(self, nranks: int):
+        self._L = lib()
+        h = ctypes.c_void_p()
+        st = self._L.maspcg_loopback_group_create(nranks, ctypes.byref(h))
+        if st != OK:
+            raise MaspcgError(st, self._L.maspcg_last_error(None).decode())
+        self.handle, self.nranks = h, nranks
+
+    def close(self):
+        if self.handle:
+            self._L.maspcg_loopback_group_destroy(self.handle)
+            self.handle = None
+
+
+def solver_for_problem(prob, *, group=None, device=None, chunk=16, stream=None, loopback=None):
     """Create a Solver for an inputs.Problem slab and upload its coefficients and BCs (device copies)."""
     import torch
     dev = f"cuda:{torch.cuda.current_device() if device is None else device}"
-    S = Solver(prob.nr, prob.nt, prob.np, prob.rf, prob.tf, prob.pf, group=group, device=device, chunk=chunk)
+    S = Solver(prob.nr, prob.nt, prob.np, prob.rf, prob.tf, prob.pf, group=group, device=device, chunk=chunk,
+               loopback=loopback)
     assert (S.k0, S.nloc) == (prob.k0, prob.nloc), "problem slab does not match the library's decomposition"
     T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     S.set_coefficients(T(prob.kr), T(prob.kt), T(prob.kp), T(prob.s), stream)
