@@ -32,8 +32,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "PCG iterations/s & matvec HBM GB/s (% of peak) at 1/2/4/8 B200"
 UNIT = "PCG iterations/s"
-MATVEC_BYTES_PER_CELL = 48      # p, T_r, T_theta, T_phi, D read + q written
-ITER_BYTES_PER_CELL = 136       # a5 + a7 (56) + a10 (32)
+# algorithmic bytes per cell of each kernel
+PATHS = {
+    1: {"name": "three kernels", "stencil": ("stencil_matvec_dot (k_matvec_flat)", 48),
+        "update": ("update_jacobi_dots (k_update)", 56), "pupdate": ("p_update (k_pupdate)", 32), "iter": 136},
+    2: {"name": "fused two passes", "stencil": ("pass A: p-update + x-update + stencil + p.q (k_pass_a)", 80),
+        "update": ("pass B: r-update + Jacobi + r.z, r.r (k_pass_b)", 32), "pupdate": None, "iter": 112},
+}
 
 
 def peaks():
@@ -93,10 +98,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def ncu_traffic_per_launch():
+def ncu_traffic_per_launch(path_id: int):
     """dram__bytes_read.sum + dram__bytes_write.sum of the stencil kernel from the committed
-    `ncu --set full` summary (profiles/ncu_matvec.json), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_matvec.json")
+    `ncu --set full` summary of that path (profiles/ncu_stencil_path{1,2}.json), or None."""
+    path = os.path.join(ROOT, "profiles", f"ncu_stencil_path{path_id}.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -174,7 +179,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
-    ap.add_argument("--stencil", type=int, default=0)
+    ap.add_argument("--path", type=int, default=0, help="0 auto (fused), 1 three kernels, 2 fused")
+    ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     args = ap.parse_args()
     if args.warmup < 3 and args.maxit is None:
         args.warmup = 3
@@ -207,7 +213,8 @@ def main():
     kr, kt, kp, s, f, x0 = (T(a) for a in (prob.kr, prob.kt, prob.kp, prob.s, prob.f, prob.x0))
 
     S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk)
-    S.set_option(maspcg.OPT_STENCIL, args.stencil)
+    S.set_option(maspcg.OPT_PATH, args.path)
+    S.set_option(maspcg.OPT_ARITH, args.arith)
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
 
@@ -249,25 +256,32 @@ def main():
     value = iters / sec                                 # global solve iterations (strong scaling)
     ncell_local = prob.ncell_local
 
-    # ---- roofline of the dominant kernel (stencil_matvec_dot), CUDA events on the launching stream
+    # ---- roofline of the dominant kernel (the stencil pass), CUDA events on the launching stream
     peak, peak_src = peaks()
+    path = PATHS[stats["path"]]
+    st_name, st_bpc = path["stencil"]
     mv_ms = stats["matvec_ms"] / max(stats["matvec_launches"], 1)
-    achieved = MATVEC_BYTES_PER_CELL * ncell_local / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
-    traffic, traffic_src = ncu_traffic_per_launch()
+    achieved = st_bpc * ncell_local / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
+    traffic, traffic_src = ncu_traffic_per_launch(stats["path"])
     kern_ms = stats["matvec_ms"] + stats["update_ms"] + stats["pupdate_ms"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "stencil_matvec_dot (k_matvec_flat)",
-                "algorithmic_bytes_per_launch": MATVEC_BYTES_PER_CELL * ncell_local,
+                "kernel": st_name, "path": path["name"],
+                "algorithmic_bytes_per_launch": st_bpc * ncell_local,
                 "avg_launch_ms": mv_ms, "peak_source": peak_src,
                 "share_of_step": stats["matvec_ms"] / ms if ms > 0 else None,
                 "traffic_source": traffic_src}
+
+    def gbps(key, bpc):
+        n = stats[key + "_launches"]
+        return bpc * ncell_local / (stats[key + "_ms"] / n * 1e-3) / 1e9 if n and stats[key + "_ms"] > 0 else None
+
     per_kernel = {
-        "update_jacobi_dots_GBps": 56 * ncell_local / (stats["update_ms"] / max(stats["update_launches"], 1) * 1e-3) / 1e9
-        if stats["update_ms"] > 0 else None,
-        "p_update_GBps": 32 * ncell_local / (stats["pupdate_ms"] / max(stats["pupdate_launches"], 1) * 1e-3) / 1e9
-        if stats["pupdate_ms"] > 0 else None,
-        "iteration_GBps": ITER_BYTES_PER_CELL * ncell_local * iters / sec / 1e9 / 1.0,
+        "path": path["name"],
+        "update_kernel": path["update"][0], "update_GBps": gbps("update", path["update"][1]),
+        "p_update_GBps": gbps("pupdate", path["pupdate"][1]) if path["pupdate"] else None,
+        "iteration_bytes_per_cell": path["iter"],
+        "iteration_GBps": path["iter"] * ncell_local * iters / sec / 1e9,
         "kernels_share_of_step": kern_ms / ms if ms > 0 else None,
     }
 
@@ -323,7 +337,8 @@ def main():
                        "global_cells": nr * nt * np_, "parallelism": f"phi-slab x{world}",
                        "iters_per_solve": iters / args.steps, "chunk": args.chunk,
                        "l2": "no flush: working set ~2.2 GB >> 126 MB L2",
-                       "step": "set_grid + set_coefficients + set_bc_r + solve to tol"},
+                       "step": "set_grid + set_coefficients + set_bc_r + solve to tol",
+                       "arith": "oracle-identical (no FMA, Dot2 dots)" if args.arith == 0 else "fast (FMA, plain sums)"},
             "cell_updates_per_s": nr * nt * np_ * value,
             "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),

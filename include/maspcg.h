@@ -96,13 +96,15 @@ typedef struct {
     long long kernel_launches;     /* kernels of this library enqueued (graph nodes count per replay) */
     long long solves;
     long long iterations;          /* PCG iterations executed (sum over solves) */
-    double matvec_ms;              /* summed CUDA-event time of stencil_matvec_dot launches (timing mode) */
+    double matvec_ms;              /* summed CUDA-event time of the stencil launches (stencil_matvec_dot, or pass A
+                                      of the fused path) in timing mode */
     long long matvec_launches;     /* launches covered by matvec_ms */
-    double update_ms;              /* update_jacobi_dots */
+    double update_ms;              /* update_jacobi_dots (or pass B of the fused path) */
     long long update_launches;
     double pupdate_ms;             /* p_update */
     long long pupdate_launches;
     double comm_ms;                /* halo + all-reduce time on the comm path (timing mode, P > 1) */
+    int path;                      /* iteration path of the last solve: 1 = three kernels, 2 = fused two passes */
 } maspcg_stats;
 
 /* Options for maspcg_set_option(). */
@@ -110,7 +112,12 @@ typedef enum {
     MASPCG_OPT_CHUNK = 1,        /* PCG iterations per CUDA-graph launch (1..256, default 16) */
     MASPCG_OPT_USE_GRAPHS = 2,   /* 1 (default): replay captured graphs; 0: eager launches */
     MASPCG_OPT_TIMING = 3,       /* 1: CUDA events around every hot kernel (forces eager launches) */
-    MASPCG_OPT_STENCIL = 4       /* stencil kernel variant: 0 = auto (default), 1 = flat, 2 = phi-marching tiles */
+    MASPCG_OPT_ARITH = 5,        /* 0 (default): oracle-identical arithmetic -- no FMA contraction, Dot2 (compensated)
+                                    dot products (R24); 1: FMA updates and plain tree sums (faster in FP64
+                                    issue, parity to the tolerance contract only) */
+    MASPCG_OPT_PATH = 4          /* iteration path: 0 = auto (default, = 2), 1 = three kernels (stencil+dot, update+dots,
+                                    p-update; 136 B/cell), 2 = fused two passes (p-update and the deferred x update folded
+                                    into a phi-marching tiled stencil + r update; 112 B/cell) */
 } maspcg_option;
 
 /* ---- lifetime ----------------------------------------------------------- */

@@ -24,7 +24,7 @@
  *
  * Style: triple loops in [k][j][i] order (phi outermost, r contiguous,
  * PAPER.md:128-139 Listing 1 with i fastest), left-to-right sums, no blocking,
- * no fusion, no reordering.  Built with -O2 -fno-fast-math -ffp-contract=off so
+ * no fusion, no reordering; dot products are evaluated accurately (Dot2, R24).  Built with -O2 -fno-fast-math -ffp-contract=off so
  * every product and sum is one IEEE fp64 rounding, in the order written.
  *
  * Pins (tests/test_oracle_pins.py, -m "not gpu"): sum of V closed form; sphere
@@ -299,10 +299,43 @@ int masoracle_rhs(int nr, int nt, int np, const double *rf, const double *tf,
 
 /* --------------------------------------------------------------- PCG (R6, R11-R14) */
 
+/* Dot products (R24): Dot2 of Ogita, Rump & Oishi (SIAM J. Sci. Comput. 26, 2005, Algorithm 5.3):
+ * each product is split exactly into h + r (TwoProduct, Dekker/Veltkamp, plain IEEE operations), the
+ * leading parts are summed with error-free TwoSum and every rounding error is accumulated separately;
+ * the result equals the dot product computed in twice the working precision and rounded once.  It is
+ * still the plain definition sum_i a_i b_i, only evaluated accurately -- so that the value does not
+ * depend on the order of summation (up to the final rounding).  Requires -ffp-contract=off. */
+static void mo_two_sum(double a, double b, double *x, double *y) {
+    double s = a + b;
+    double z = s - a;
+    *x = s;
+    *y = (a - (s - z)) + (b - z);
+}
+
+static void mo_split(double a, double *hi, double *lo) {
+    double c = 134217729.0 * a; /* 2^27 + 1 */
+    double h = c - (c - a);
+    *hi = h;
+    *lo = a - h;
+}
+
+static void mo_two_product(double a, double b, double *x, double *y) {
+    double p = a * b, ah, al, bh, bl;
+    mo_split(a, &ah, &al);
+    mo_split(b, &bh, &bl);
+    *x = p;
+    *y = al * bl - (((p - ah * bh) - al * bh) - ah * bl);
+}
+
 static double mo_dot(size_t n, const double *a, const double *b) {
-    double s = 0.0;
-    for (size_t c = 0; c < n; c++) s = s + a[c] * b[c];
-    return s;
+    double p = 0.0, s = 0.0;
+    for (size_t c = 0; c < n; c++) {
+        double h, r, q;
+        mo_two_product(a[c], b[c], &h, &r);
+        mo_two_sum(p, h, &p, &q);
+        s = s + (q + r);
+    }
+    return p + s;
 }
 
 /* Point-Jacobi PCG, Hestenes-Stiefel form with Fletcher-Reeves beta

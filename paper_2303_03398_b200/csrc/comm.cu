@@ -28,17 +28,22 @@ class NcclComm final : public Comm {
 
     // Ops to the same peer are matched in issue order, so this order is also right when
     // left == right (P = 2): the first send / receive between a pair carries "first plane -> hi halo".
-    int halo_padded(double *buf, size_t pl, int nloc, cudaStream_t st, std::string &err) override {
+    int halo_planes(const double *first, const double *last, double *lo_recv, double *hi_recv, size_t count,
+                    cudaStream_t st, std::string &err) override {
         ncclResult_t r;
         if ((r = ncclGroupStart()) != ncclSuccess) return fail(r, "ncclGroupStart", err);
-        r = ncclSend(buf + pl, pl, ncclDouble, left(), comm, st);                              // my first plane
-        if (r == ncclSuccess) r = ncclRecv(buf + (size_t)(nloc + 1) * pl, pl, ncclDouble, right(), comm, st);
-        if (r == ncclSuccess) r = ncclSend(buf + (size_t)nloc * pl, pl, ncclDouble, right(), comm, st);  // my last
-        if (r == ncclSuccess) r = ncclRecv(buf, pl, ncclDouble, left(), comm, st);
+        r = ncclSend(first, count, ncclDouble, left(), comm, st);                          // my first plane
+        if (r == ncclSuccess) r = ncclRecv(hi_recv, count, ncclDouble, right(), comm, st);  // right's first
+        if (r == ncclSuccess) r = ncclSend(last, count, ncclDouble, right(), comm, st);     // my last plane
+        if (r == ncclSuccess) r = ncclRecv(lo_recv, count, ncclDouble, left(), comm, st);   // left's last
         ncclResult_t r2 = ncclGroupEnd();
         if (r != ncclSuccess) return fail(r, "halo send/recv", err);
         if (r2 != ncclSuccess) return fail(r2, "ncclGroupEnd", err);
         return ST_OK;
+    }
+
+    int halo_padded(double *buf, size_t pl, int nloc, cudaStream_t st, std::string &err) override {
+        return halo_planes(buf + pl, buf + (size_t)nloc * pl, buf, buf + (size_t)(nloc + 1) * pl, pl, st, err);
     }
 
     int shift_right(const double *send, double *recv, size_t count, cudaStream_t st, std::string &err) override {
@@ -50,6 +55,11 @@ class NcclComm final : public Comm {
         if (r != ncclSuccess) return fail(r, "shift send/recv", err);
         if (r2 != ncclSuccess) return fail(r2, "ncclGroupEnd", err);
         return ST_OK;
+    }
+
+    int allgather(const double *send, double *recv, int count, cudaStream_t st, std::string &err) override {
+        ncclResult_t r = ncclAllGather(send, recv, count, ncclDouble, comm, st);
+        return r == ncclSuccess ? ST_OK : fail(r, "ncclAllGather", err);
     }
 
     int allreduce_sum(double *dev, int count, cudaStream_t st, std::string &err) override {
@@ -114,6 +124,7 @@ struct LoopbackGroup {
     long generation = 0;
     struct Slot {
         const double *buf = nullptr;   // padded array / send buffer published for this exchange
+        const double *buf2 = nullptr;  // second send buffer (halo_planes: last plane)
         double *dslot = nullptr;       // device scratch for sums
         int *islot = nullptr;
         cudaEvent_t e = nullptr, f = nullptr;
@@ -193,6 +204,21 @@ class LoopbackComm final : public Comm {
         return phase2(st, peers, 2, err);
     }
 
+    int halo_planes(const double *first, const double *last, double *lo_recv, double *hi_recv, size_t count,
+                    cudaStream_t st, std::string &err) override {
+        me().buf = first;
+        me().buf2 = last;
+        const int peers[2] = {left(), right()};
+        if (int s = phase1(st, peers, 2, err)) return s;
+        if (int s = ck(cudaMemcpyAsync(lo_recv, g->slots[left()].buf2, 8 * count, cudaMemcpyDeviceToDevice, st),
+                       "copy", err))
+            return s;
+        if (int s = ck(cudaMemcpyAsync(hi_recv, g->slots[right()].buf, 8 * count, cudaMemcpyDeviceToDevice, st),
+                       "copy", err))
+            return s;
+        return phase2(st, peers, 2, err);
+    }
+
     int shift_right(const double *send, double *recv, size_t count, cudaStream_t st, std::string &err) override {
         me().buf = send;
         const int from[1] = {left()}, readers[1] = {right()};
@@ -206,6 +232,24 @@ class LoopbackComm final : public Comm {
     int all_peers(int *p) const {
         for (int r = 0; r < nranks; ++r) p[r] = r;
         return nranks;
+    }
+
+    int allgather(const double *send, double *recv, int count, cudaStream_t st, std::string &err) override {
+        if (count > kLoopSlot) {
+            err = "loopback all-gather count too large";
+            return ST_E_INVALID;
+        }
+        if (int s = ck(cudaMemcpyAsync(me().dslot, send, 8 * count, cudaMemcpyDeviceToDevice, st), "copy", err))
+            return s;
+        int peers[kLoopMaxRanks];
+        const int np = all_peers(peers);
+        if (int s = phase1(st, peers, np, err)) return s;
+        for (int r = 0; r < nranks; ++r)
+            if (int s = ck(cudaMemcpyAsync(recv + (size_t)r * count, g->slots[r].dslot, 8 * count,
+                                           cudaMemcpyDeviceToDevice, st),
+                           "copy", err))
+                return s;
+        return phase2(st, peers, np, err);
     }
 
     int allreduce_sum(double *dev, int count, cudaStream_t st, std::string &err) override {

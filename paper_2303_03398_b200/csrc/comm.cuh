@@ -26,8 +26,13 @@ class Comm {
     // Padded array buf[nloc+2][plane]: buf[0] <- left's plane nloc (its last local plane),
     // buf[nloc+1] <- right's plane 1 (its first local plane).
     virtual int halo_padded(double *buf, size_t plane, int nloc, cudaStream_t st, std::string &err) = 0;
+    // lo_recv <- left's `last`, hi_recv <- right's `first` (each `count` doubles).
+    virtual int halo_planes(const double *first, const double *last, double *lo_recv, double *hi_recv, size_t count,
+                            cudaStream_t st, std::string &err) = 0;
     // recv[count] <- left's send[count] (ring shift towards higher ranks).
     virtual int shift_right(const double *send, double *recv, size_t count, cudaStream_t st, std::string &err) = 0;
+    // recv[r * count + i] <- rank r's send[i] (all-gather).
+    virtual int allgather(const double *send, double *recv, int count, cudaStream_t st, std::string &err) = 0;
     // In-place sum / max over ranks; every rank receives identical bits.
     virtual int allreduce_sum(double *dev, int count, cudaStream_t st, std::string &err) = 0;
     virtual int allreduce_max(int *dev, int count, cudaStream_t st, std::string &err) = 0;

@@ -26,6 +26,7 @@ enum : int { BC_DIRICHLET = 0, BC_NEUMANN0 = 1 };
 constexpr int kMaxChunk = 256;          // PCG iterations per graph launch (upper bound)
 constexpr int kRedBlocks = 1184;        // fixed grid of the streaming kernels (8 x 148)
 constexpr int kThreads = 256;           // threads per block of the streaming kernels
+constexpr int kMaxRanks = 16;           // all-gather scratch of the Dot2 all-reduce
 
 // Division by a runtime constant for 0 <= n < 2^31 (round-up multiplier
 // method): q = (n * m) >> p with p = 31 + ceil(log2 d), m = ceil(2^p / d).
@@ -55,15 +56,17 @@ inline FastDiv make_fastdiv(uint32_t d) {
 // read by every block at kernel entry.  A snapshot is copied to pinned host
 // memory once per graph chunk.
 struct Scalars {
-    double red1[2];          // [0] = p.Ap (local partial, then global after all-reduce)
-    double red2[2];          // [0] = r.z, [1] = r.r
-    double red3[4];          // setup: r.z, r.r, b.b
+    // Dot2 results as (p, s) pairs, value = p + s (arith.cuh): local, then global after the all-reduce
+    double red1[2];          // p.Ap
+    double red2[4];          // r.z, r.r
+    double red3[6];          // setup: r.z, r.r, b.b
     double rho;              // r.z of the current iterate
     double bn;               // ||b||
     double tolbn;            // tol * ||b||
     double tol;
     double hist0;            // ||r_0||
     double rn;               // ||r_iter||
+    double alpha;            // alpha of the last completed iteration (fused path: deferred x update)
     int iter;                // completed PCG iterations
     int maxit;
     int done;                // 1: every loop kernel returns at entry
@@ -71,9 +74,9 @@ struct Scalars {
     int zero_x;              // b == 0: x := 0 at the end
     int vinvalid;            // set_coefficients: 1 if any input is negative or non-finite
     int vshift;              // set_coefficients: 1 if any s > 0
-    int pad_;
+    int hist_count;          // fused path: history entries 1..hist_count are final
     unsigned int ticket[8];  // last-block tickets (reset by the last block)
-    double hist_ring[kMaxChunk];   // ||r_k|| at slot (k-1) % chunk
+    double hist_ring[2 * kMaxChunk];   // ||r_k|| at slot (k-1) % chunk (3-kernel) or % (2 kMaxChunk) (fused)
 };
 
 // Geometry handed to kernels by value.
@@ -118,8 +121,12 @@ struct DevArrays {
     double *sinc;   // [nt]
     double *dp;     // [nloc]  local
     double *hp;     // [nloc]  local: h^phi of face (k0 + k) + 1/2
+    // fused two-pass path
+    double *P[2];       // [nloc][nt][nr] search directions of even / odd iterations
+    double *rh, *dh, *ph;   // [2][nt][nr] received halo planes (lo, hi) of r, D, p_old (nranks > 1)
     // reductions
-    double *partials;   // [4][kRedBlocks]
+    double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums
+    double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce
     Scalars *sc;
 };
 

@@ -20,74 +20,13 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "arith.cuh"
 
 namespace maspcg {
 
 namespace {
 
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    return v;
-}
-
-// Reduce N values over the block (fixed tree), thread 0 gets the totals.
-template <int N>
-__device__ __forceinline__ void block_sum(double (&v)[N]) {
-    __shared__ double sm[N][kThreads / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int k = 0; k < N; ++k) v[k] = warp_sum(v[k]);
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < N; ++k) sm[k][warp] = v[k];
-    }
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-            double x = lane < (int)(blockDim.x >> 5) ? sm[k][lane] : 0.0;
-            v[k] = warp_sum(x);
-        }
-    }
-    __syncthreads();
-}
-
-// Block partials -> partials[k * kRedBlocks + slot]; returns true in the last
-// block to arrive (all partials of all `total` blocks visible), which then
-// holds the fixed-order totals in out[] (thread 0) and has reset the ticket.
-template <int N>
-__device__ __forceinline__ bool reduce_and_last(double (&v)[N], double *partials, unsigned *ticket,
-                                                unsigned slot, unsigned total, double (&out)[N]) {
-    __shared__ bool am_last;
-    block_sum<N>(v);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < N; ++k) partials[k * kRedBlocks + slot] = v[k];
-        __threadfence();
-        unsigned t = atomicAdd(ticket, 1u);
-        am_last = (t == total - 1);
-    }
-    __syncthreads();
-    if (!am_last) return false;
-    __threadfence();
-    double acc[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-        acc[k] = 0.0;
-        for (unsigned b = threadIdx.x; b < total; b += blockDim.x)
-            acc[k] += __ldcg(partials + k * kRedBlocks + b);
-    }
-    block_sum<N>(acc);
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < N; ++k) out[k] = acc[k];
-        *ticket = 0u;
-    }
-    return true;
-}
 
 __device__ __forceinline__ void decompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
     uint32_t row = d.div_r.div(c);
@@ -109,7 +48,7 @@ __device__ __forceinline__ void store_p(const Dims &d, double *p, uint32_t c, do
 
 // ---------------------------------------------------------------- assembly
 // SURVEY 8(c) item 3 (R3-R5, R8): face transmissibilities, s*V, validation.
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_assemble(Dims d, DevArrays a, const double *__restrict__ kr,
+__global__ void __launch_bounds__(kThreads) k_assemble(Dims d, DevArrays a, const double *__restrict__ kr,
                                                        const double *__restrict__ kt,
                                                        const double *__restrict__ kp,
                                                        const double *__restrict__ s) {
@@ -192,23 +131,26 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_fill_p(Dims d, DevArra
 
 // ---------------------------------------------------------------- stencil
 // y = A p over a virtual range: c = v + off0 + (v >= split ? off1 : 0).
-// WITH_DOT: block partials of p.y -> last block writes sc->red1[0].
+// WITH_DOT: block partials of p.y -> last block writes sc->red1 (Dot2 pair).
 // LOOP: returns at entry once sc->done is set.
+// Sum order = the oracle's: r_lo, r_hi, theta_lo, theta_hi, phi_lo, phi_hi, then D p - sum.
 struct Range {
     uint32_t vend, off0, split, off1;
 };
 
-template <bool WITH_DOT, bool LOOP>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_matvec_flat(Dims d, DevArrays a, double *__restrict__ y, Range rg,
-                                                          unsigned red_slot0, unsigned red_total) {
+template <bool WITH_DOT, bool LOOP, bool EXACT>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_matvec_flat(Dims d, DevArrays a, double *__restrict__ y,
+                                                                      Range rg, unsigned red_slot0,
+                                                                      unsigned red_total) {
     if (LOOP && *(volatile int *)&a.sc->done) return;
+    using A = Ar<EXACT>;
     const double *__restrict__ p = a.p;
     const double *__restrict__ Tr = a.Tr;
     const double *__restrict__ Tt = a.Tt;
     const double *__restrict__ Tp = a.Tp;
     const double *__restrict__ D = a.D;
     const size_t plane = d.plane;
-    double acc = 0.0;
+    Acc<EXACT> dot[1];
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < rg.vend; v += stride) {
         const uint32_t c = v + rg.off0 + (v >= rg.split ? rg.off1 : 0u);
@@ -217,30 +159,35 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_matvec_flat(Dims d, De
         const size_t cp = (size_t)c + plane;
         const double pc = __ldg(p + cp);
         double s = 0.0;
-        if (i > 0) s = fma(__ldg(Tr + c), __ldg(p + cp - 1), s);
-        if (i < d.nr - 1) s = fma(__ldg(Tr + c + 1), __ldg(p + cp + 1), s);
-        if (j > 0) s = fma(__ldg(Tt + c), __ldg(p + cp - d.nr), s);
-        if (j < d.nt - 1) s = fma(__ldg(Tt + c + d.nr), __ldg(p + cp + d.nr), s);
-        s = fma(__ldg(Tp + c), __ldg(p + cp - plane), s);
-        s = fma(__ldg(Tp + c + plane), __ldg(p + cp + plane), s);
-        const double q = fma(__ldg(D + c), pc, -s);
+        if (i > 0) s = A::acc(s, __ldg(Tr + c), __ldg(p + cp - 1));
+        if (i < d.nr - 1) s = A::acc(s, __ldg(Tr + c + 1), __ldg(p + cp + 1));
+        if (j > 0) s = A::acc(s, __ldg(Tt + c), __ldg(p + cp - d.nr));
+        if (j < d.nt - 1) s = A::acc(s, __ldg(Tt + c + d.nr), __ldg(p + cp + d.nr));
+        s = A::acc(s, __ldg(Tp + c), __ldg(p + cp - plane));
+        s = A::acc(s, __ldg(Tp + c + plane), __ldg(p + cp + plane));
+        const double q = A::diag_minus(__ldg(D + c), pc, s);
         y[c] = q;
-        if (WITH_DOT) acc = fma(pc, q, acc);
+        if (WITH_DOT) dot[0].add(pc, q);
     }
     if (WITH_DOT) {
-        double v1[1] = {acc}, out[1];
-        if (reduce_and_last<1>(v1, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total, out)) {
-            if (threadIdx.x == 0) a.sc->red1[0] = out[0];
+        Acc<EXACT> out[1];
+        if (reduce_last<EXACT, kThreads, 1>(dot, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total,
+                                            out)) {
+            if (threadIdx.x == 0) {
+                a.sc->red1[0] = out[0].p;
+                a.sc->red1[1] = out[0].s;
+            }
         }
     }
 }
 
 // ---------------------------------------------------------------- setup of a solve
 // b = V f + Dirichlet face terms (R5); r0 = b - q (q = A x0); z0 = r0/D; p0 = z0;
-// partials r.z, r.r, b.b -> sc->red3.
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_setup_residual(Dims d, DevArrays a, const double *__restrict__ f,
+// Dot2 partials r.z, r.r, b.b -> sc->red3.
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads) k_setup_residual(Dims d, DevArrays a, const double *__restrict__ f,
                                                              int din, int dout, unsigned total) {
-    double rz = 0.0, rr = 0.0, bb = 0.0;
+    Acc<EXACT> acc[3];
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
         int i, j, k;
@@ -250,35 +197,39 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_setup_residual(Dims d,
         double b = __dmul_rn(V, f[c]);
         if (din && i == 0) b = __dadd_rn(b, __dmul_rn(a.Tr[c], a.gin[row]));
         if (dout && i == d.nr - 1) b = __dadd_rn(b, __dmul_rn(a.TrB[row], a.gout[row]));
-        const double r = b - a.q[c];
-        const double z = r / a.D[c];
+        const double r = __dsub_rn(b, a.q[c]);
+        const double z = __ddiv_rn(r, a.D[c]);
         a.r[c] = r;
         store_p(d, a.p, c, z);
-        rz = fma(r, z, rz);
-        rr = fma(r, r, rr);
-        bb = fma(b, b, bb);
+        acc[0].add(r, z);
+        acc[1].add(r, r);
+        acc[2].add(b, b);
     }
-    double v3[3] = {rz, rr, bb}, out[3];
-    if (reduce_and_last<3>(v3, a.partials, &a.sc->ticket[3], blockIdx.x, total, out)) {
+    Acc<EXACT> out[3];
+    if (reduce_last<EXACT, kThreads, 3>(acc, a.partials, &a.sc->ticket[3], blockIdx.x, total, out)) {
         if (threadIdx.x == 0) {
-            a.sc->red3[0] = out[0];
-            a.sc->red3[1] = out[1];
-            a.sc->red3[2] = out[2];
+            for (int k = 0; k < 3; ++k) {
+                a.sc->red3[2 * k] = out[k].p;
+                a.sc->red3[2 * k + 1] = out[k].s;
+            }
         }
     }
 }
 
-// PCG start, after red3 holds global sums.
+// PCG start, after red3 holds the global Dot2 pairs.
 __global__ void k_setup_scalars(DevArrays a, double tol, int maxit) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     Scalars *sc = a.sc;
     sc->tol = tol;
     sc->maxit = maxit;
-    const double rz = sc->red3[0], rr = sc->red3[1], bb = sc->red3[2];
+    const double rz = __dadd_rn(sc->red3[0], sc->red3[1]);
+    const double rr = __dadd_rn(sc->red3[2], sc->red3[3]);
+    const double bb = __dadd_rn(sc->red3[4], sc->red3[5]);
     const double bn = sqrt(bb), h0 = sqrt(rr);
     sc->bn = bn;
-    sc->tolbn = sc->tol * bn;
+    sc->tolbn = __dmul_rn(sc->tol, bn);
     sc->iter = 0;
+    sc->hist_count = 0;
     sc->rho = rz;
     sc->zero_x = 0;
     sc->done = 1;
@@ -304,12 +255,15 @@ __global__ void k_setup_scalars(DevArrays a, double tol, int maxit) {
     }
 }
 
-// ---------------------------------------------------------------- PCG loop
-// alpha = rho / p.Ap; x += alpha p; r -= alpha q; z = r / D; partials r.z, r.r.
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_update(Dims d, DevArrays a, double *__restrict__ x, unsigned total) {
+// ---------------------------------------------------------------- PCG loop (three-kernel path)
+// alpha = rho / p.Ap; x += alpha p; r -= alpha q; z = r / D; Dot2 partials r.z, r.r.
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_update(Dims d, DevArrays a, double *__restrict__ x,
+                                                                 unsigned total) {
+    using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
-    const double pi = sc->red1[0];
+    const double pi = __dadd_rn(sc->red1[0], sc->red1[1]);
     if (!(pi > 0.0) || !isfinite(pi)) {        // breakdown: uniform decision in every block
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             sc->status = ST_E_BREAKDOWN;
@@ -317,48 +271,52 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_update(Dims d, DevArra
         }
         return;
     }
-    const double alpha = sc->rho / pi;
+    const double alpha = __ddiv_rn(sc->rho, pi);
     const double *__restrict__ p = a.p + d.plane;
     const double *__restrict__ q = a.q;
     const double *__restrict__ D = a.D;
     double *__restrict__ r = a.r;
-    double rz = 0.0, rr = 0.0;
+    Acc<EXACT> acc[2];
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
-        const double pc = __ldg(p + c);
-        x[c] = fma(alpha, pc, x[c]);
-        const double rc = fma(-alpha, __ldg(q + c), r[c]);
+        x[c] = A::axpy(alpha, __ldg(p + c), x[c]);
+        const double rc = A::ymax(r[c], alpha, __ldg(q + c));
         r[c] = rc;
-        const double z = rc / __ldg(D + c);
-        rz = fma(rc, z, rz);
-        rr = fma(rc, rc, rr);
+        const double z = __ddiv_rn(rc, __ldg(D + c));
+        acc[0].add(rc, z);
+        acc[1].add(rc, rc);
     }
-    double v2[2] = {rz, rr}, out[2];
-    if (reduce_and_last<2>(v2, a.partials, &sc->ticket[1], blockIdx.x, total, out)) {
+    Acc<EXACT> out[2];
+    if (reduce_last<EXACT, kThreads, 2>(acc, a.partials, &sc->ticket[1], blockIdx.x, total, out)) {
         if (threadIdx.x == 0) {
-            sc->red2[0] = out[0];
-            sc->red2[1] = out[1];
+            sc->red2[0] = out[0].p;
+            sc->red2[1] = out[0].s;
+            sc->red2[2] = out[1].p;
+            sc->red2[3] = out[1].s;
         }
     }
 }
 
 // Convergence test on ||r|| (R12); beta = r.z / rho (R11); p = r/D + beta p.
 // The last block advances the iteration counter and the scalars.
+template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArrays a, int chunk, unsigned total) {
+    using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
-    const double rz = sc->red2[0], rr = sc->red2[1];
+    const double rz = __dadd_rn(sc->red2[0], sc->red2[1]);
+    const double rr = __dadd_rn(sc->red2[2], sc->red2[3]);
     const double rn = sqrt(rr);
     const bool conv = rn <= sc->tolbn;
     const bool bad = !isfinite(rn) || !isfinite(rz);
     if (!conv && !bad) {
-        const double beta = rz / sc->rho;
+        const double beta = __ddiv_rn(rz, sc->rho);
         const double *__restrict__ r = a.r;
         const double *__restrict__ D = a.D;
         const uint32_t stride = gridDim.x * blockDim.x;
         for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
             const double pold = a.p[(size_t)c + d.plane];
-            const double pn = fma(beta, pold, __ldg(r + c) / __ldg(D + c));
+            const double pn = A::axpy(beta, pold, __ddiv_rn(__ldg(r + c), __ldg(D + c)));
             store_p(d, a.p, c, pn);
         }
     }
@@ -441,35 +399,71 @@ unsigned stencil_blocks(const Dims &d, StencilPart part) {
 }
 
 void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart part, bool with_dot, bool loop,
-                   unsigned red_slot0, unsigned red_total, cudaStream_t st) {
+                   unsigned red_slot0, unsigned red_total, bool exact, cudaStream_t st) {
     Range rg = make_range(d, part);
     if (rg.vend == 0) return;
     const unsigned g = grid_for(rg.vend);
-    if (with_dot) {
-        if (loop) k_matvec_flat<true, true><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);
-        else k_matvec_flat<true, false><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);
+#define MV(W, L, E) k_matvec_flat<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total)
+    if (exact) {
+        if (with_dot) {
+            if (loop) MV(true, true, true);
+            else MV(true, false, true);
+        } else MV(false, false, true);
     } else {
-        k_matvec_flat<false, false><<<g, kThreads, 0, st>>>(d, a, y, rg, 0, 0);
+        if (with_dot) {
+            if (loop) MV(true, true, false);
+            else MV(true, false, false);
+        } else MV(false, false, false);
     }
+#undef MV
 }
 
-void launch_setup_residual(const Dims &d, const DevArrays &a, const double *f, int din, int dout, cudaStream_t st) {
+void launch_setup_residual(const Dims &d, const DevArrays &a, const double *f, int din, int dout, bool exact,
+                           cudaStream_t st) {
     const unsigned g = grid_for(d.n);
-    k_setup_residual<<<g, kThreads, 0, st>>>(d, a, f, din, dout, g);
+    if (exact) k_setup_residual<true><<<g, kThreads, 0, st>>>(d, a, f, din, dout, g);
+    else k_setup_residual<false><<<g, kThreads, 0, st>>>(d, a, f, din, dout, g);
 }
 
 void launch_setup_scalars(const DevArrays &a, double tol, int maxit, cudaStream_t st) {
     k_setup_scalars<<<1, 32, 0, st>>>(a, tol, maxit);
 }
 
-void launch_update(const Dims &d, const DevArrays &a, double *x, cudaStream_t st) {
+void launch_update(const Dims &d, const DevArrays &a, double *x, bool exact, cudaStream_t st) {
     const unsigned g = grid_for(d.n);
-    k_update<<<g, kThreads, 0, st>>>(d, a, x, g);
+    if (exact) k_update<true><<<g, kThreads, 0, st>>>(d, a, x, g);
+    else k_update<false><<<g, kThreads, 0, st>>>(d, a, x, g);
 }
 
-void launch_pupdate(const Dims &d, const DevArrays &a, int chunk, cudaStream_t st) {
+void launch_pupdate(const Dims &d, const DevArrays &a, int chunk, bool exact, cudaStream_t st) {
     const unsigned g = grid_for(d.n);
-    k_pupdate<<<g, kThreads, 0, st>>>(d, a, chunk, g);
+    if (exact) k_pupdate<true><<<g, kThreads, 0, st>>>(d, a, chunk, g);
+    else k_pupdate<false><<<g, kThreads, 0, st>>>(d, a, chunk, g);
+}
+
+__global__ void k_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact) {
+    const int t = threadIdx.x;
+    if (t >= npairs) return;
+    if (exact) {
+        Acc<true> acc;
+        for (int r = 0; r < nranks; ++r) {   // rank order: identical bits on every rank
+            Acc<true> o;
+            o.p = gather[r * 2 * npairs + 2 * t];
+            o.s = gather[r * 2 * npairs + 2 * t + 1];
+            acc.add(o);
+        }
+        out[2 * t] = acc.p;
+        out[2 * t + 1] = acc.s;
+    } else {
+        double v = 0.0;
+        for (int r = 0; r < nranks; ++r) v = __dadd_rn(v, gather[r * 2 * npairs + 2 * t]);
+        out[2 * t] = v;
+        out[2 * t + 1] = 0.0;
+    }
+}
+
+void launch_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact, cudaStream_t st) {
+    k_dd_combine<<<1, 32, 0, st>>>(gather, nranks, npairs, out, exact);
 }
 
 void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st) {

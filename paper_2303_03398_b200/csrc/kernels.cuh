@@ -19,13 +19,17 @@ unsigned stencil_blocks(const Dims &d, StencilPart part);
 // y = A p over `part` of the slab.  with_dot: partial p.y into partial slots
 // [red_slot0, red_slot0 + blocks); the last of red_total blocks writes
 // sc->red1[0].  loop: early exit when sc->done.
+// exact: the oracle-identical arithmetic of arith.cuh (no FMA contraction, Dot2 dot products).
 void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart part, bool with_dot, bool loop,
-                   unsigned red_slot0, unsigned red_total, cudaStream_t st);
+                   unsigned red_slot0, unsigned red_total, bool exact, cudaStream_t st);
 
-void launch_setup_residual(const Dims &d, const DevArrays &a, const double *f, int din, int dout, cudaStream_t st);
+void launch_setup_residual(const Dims &d, const DevArrays &a, const double *f, int din, int dout, bool exact,
+                           cudaStream_t st);
 void launch_setup_scalars(const DevArrays &a, double tol, int maxit, cudaStream_t st);
-void launch_update(const Dims &d, const DevArrays &a, double *x, cudaStream_t st);
-void launch_pupdate(const Dims &d, const DevArrays &a, int chunk, cudaStream_t st);
+void launch_update(const Dims &d, const DevArrays &a, double *x, bool exact, cudaStream_t st);
+void launch_pupdate(const Dims &d, const DevArrays &a, int chunk, bool exact, cudaStream_t st);
+// out[2t..2t+1] = rank-ordered Dot2 combination of gather[r][2t..2t+1], t < npairs.
+void launch_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact, cudaStream_t st);
 void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st);
 
 }  // namespace maspcg

@@ -19,6 +19,7 @@
 #include "../../include/maspcg.h"
 #include "comm.cuh"
 #include "common.cuh"
+#include "fused.cuh"
 #include "kernels.cuh"
 
 using namespace maspcg;
@@ -69,7 +70,10 @@ struct maspcg_ctx {
     int g_chunk = 0, g_variant = -1;
 
     // options
-    int chunk = 16, use_graphs = 1, timing = 0, stencil_variant = 0;
+    int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
+    // fused two-pass path geometry (fused.cu)
+    int fused_bj = 1, fused_njt = 1, fused_blocks = 1;
+    cudaEvent_t ev_a = nullptr, ev_ph = nullptr;
     maspcg_stats stats{};
     std::vector<cudaEvent_t> tev;   // timing events [3 kernels][2][chunk]
 };
@@ -112,7 +116,13 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     };
     DevArrays t{};
     t.sc = (Scalars *)take(sizeof(Scalars));
-    t.partials = (double *)take(sizeof(double) * 4 * kRedBlocks);
+    t.partials = (double *)take(sizeof(double) * 8 * kRedBlocks);
+    t.gather = (double *)take(sizeof(double) * 8 * kMaxRanks);
+    t.P[0] = (double *)take(8 * n);
+    t.P[1] = (double *)take(8 * n);
+    t.rh = (double *)take(8 * 2 * plane);
+    t.dh = (double *)take(8 * 2 * plane);
+    t.ph = (double *)take(8 * 2 * plane);
     t.Tr = (double *)take(8 * n);
     t.TrB = (double *)take(8 * rows);
     t.Tt = (double *)take(8 * n);
@@ -182,9 +192,23 @@ maspcg_status halo_padded(maspcg_ctx *c, double *buf, cudaStream_t st) {
     return MASPCG_OK;
 }
 
-maspcg_status allreduce_sum(maspcg_ctx *c, double *dev, int count, cudaStream_t st) {
+// lo/hi halo planes of a [nloc][nt][nr] array: halo[0] <- left's last plane, halo[1] <- right's first
+maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaStream_t st) {
+    const size_t pl = (size_t)c->nt * c->nr;
+    COMM(c, c->comm->halo_planes(arr, arr + (size_t)(c->nloc - 1) * pl, halo, halo + pl, pl, st, c->err));
+    return MASPCG_OK;
+}
+
+bool use_fused(const maspcg_ctx *c) { return c->path_opt != 1; }
+bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
+int graph_key(const maspcg_ctx *c) { return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0); }
+
+// Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
+// order with the same error-free arithmetic (identical bits on every rank).
+maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStream_t st) {
     if (c->nranks == 1) return MASPCG_OK;
-    COMM(c, c->comm->allreduce_sum(dev, count, st, c->err));
+    COMM(c, c->comm->allgather(pairs, c->a.gather, 2 * npairs, st, c->err));
+    launch_dd_combine(c->a.gather, c->nranks, npairs, pairs, exact_arith(c), st);
     return MASPCG_OK;
 }
 
@@ -193,7 +217,7 @@ maspcg_status allreduce_sum(maspcg_ctx *c, double *dev, int count, cudaStream_t 
 maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st) {
     if (c->nranks == 1) {
         launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
-                      stencil_blocks(c->d, StencilPart::Full), st);
+                      stencil_blocks(c->d, StencilPart::Full), exact_arith(c), st);
         return MASPCG_OK;
     }
     CK(c, cudaEventRecord(c->ev_p, st));
@@ -202,9 +226,9 @@ maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool lo
     CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
     const unsigned gi = stencil_blocks(c->d, StencilPart::Interior);
     const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary);
-    launch_matvec(c->d, c->a, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, st);
+    launch_matvec(c->d, c->a, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, exact_arith(c), st);
     CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
-    launch_matvec(c->d, c->a, y, StencilPart::Boundary, with_dot, loop, gi, gi + gb, st);
+    launch_matvec(c->d, c->a, y, StencilPart::Boundary, with_dot, loop, gi, gi + gb, exact_arith(c), st);
     return MASPCG_OK;
 }
 
@@ -216,6 +240,7 @@ maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
         SET_ERR(c, MASPCG_E_SINGULAR, "shift is zero everywhere and no r boundary is Dirichlet: A is singular");
     launch_finalize_D(c->d, c->a, c->bc_in, c->bc_out, st);
     CK(c, cudaGetLastError());
+    if (c->nranks > 1) RET_IF(halo_planes(c, c->a.D, c->a.dh, st));   // D of the neighbours' boundary planes
     c->D_dirty = false;
     return MASPCG_OK;
 }
@@ -228,25 +253,80 @@ maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int i
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 0, it, c->chunk)], st));
     RET_IF(stencil_with_halo(c, c->a.q, true, true, st));
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 1, it, c->chunk)], st));
-    RET_IF(allreduce_sum(c, c->a.sc->red1, 1, st));
+    RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st));
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 0, it, c->chunk)], st));
-    launch_update(c->d, c->a, x, st);
+    launch_update(c->d, c->a, x, exact_arith(c), st);
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 1, it, c->chunk)], st));
-    RET_IF(allreduce_sum(c, c->a.sc->red2, 2, st));
+    RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st));
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 0, it, c->chunk)], st));
-    launch_pupdate(c->d, c->a, c->chunk, st);
+    launch_pupdate(c->d, c->a, c->chunk, exact_arith(c), st);
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 1, it, c->chunk)], st));
     return MASPCG_OK;
+}
+
+// One PCG iteration of the fused two-pass path (fused.cu).  slot: index within the chunk; the
+// chunk length is even so the p buffer parity of a slot is the same in every chunk.
+maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st, int slot) {
+    const bool tm = c->timing != 0;
+    const int par = (slot + 1) & 1;
+    const size_t pl = c->d.plane;
+    FusedArgs f{};
+    f.p_old = c->a.P[par ^ 1];
+    f.p_new = c->a.P[par];
+    f.x = x;
+    f.r = c->a.r;
+    if (c->nranks == 1) {   // periodic wrap planes of the slab itself (R9)
+        const size_t last = (size_t)(c->nloc - 1) * pl;
+        f.r_lo = c->a.r + last, f.r_hi = c->a.r;
+        f.d_lo = c->a.D + last, f.d_hi = c->a.D;
+        f.p_lo = f.p_old + last, f.p_hi = f.p_old;
+    } else {
+        f.r_lo = c->a.rh, f.r_hi = c->a.rh + pl;
+        f.d_lo = c->a.dh, f.d_hi = c->a.dh + pl;
+        f.p_lo = c->a.ph, f.p_hi = c->a.ph + pl;
+    }
+    f.bj = c->fused_bj;
+    f.n_jt = c->fused_njt;
+    f.div_r = c->d.div_r;
+    if (c->nranks > 1 && slot > 0) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // p_old halo of slot-1
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 0, slot, c->chunk)], st));
+    launch_pass_a(c->d, c->a, f, c->fused_blocks, exact_arith(c), st);
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 1, slot, c->chunk)], st));
+    if (c->nranks > 1) {
+        // p_it halo for the next pass A, on the communication stream, overlapped with pass B
+        CK(c, cudaEventRecord(c->ev_a, st));
+        CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_a, 0));
+        RET_IF(halo_planes(c, f.p_new, c->a.ph, c->comm_stream));
+        CK(c, cudaEventRecord(c->ev_ph, c->comm_stream));
+    }
+    RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st));
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 0, slot, c->chunk)], st));
+    launch_pass_b(c->d, c->a, exact_arith(c), st);
+    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 1, slot, c->chunk)], st));
+    RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st));
+    if (c->nranks > 1) {
+        RET_IF(halo_planes(c, c->a.r, c->a.rh, st));            // r_it halo (critical path, one plane each way)
+        if (slot == c->chunk - 1) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // join before the chunk ends
+    }
+    if (tm) {   // keep the 3-slot event layout: no third kernel on this path
+        CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 0, slot, c->chunk)], st));
+        CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 1, slot, c->chunk)], st));
+    }
+    return MASPCG_OK;
+}
+
+maspcg_status enqueue_any(maspcg_ctx *c, double *x, cudaStream_t st, int slot) {
+    return use_fused(c) ? enqueue_iteration_fused(c, x, st, slot) : enqueue_iteration(c, x, st, slot);
 }
 
 maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st) {
     const bool graphs = c->use_graphs && !c->timing;
     if (!graphs) {
-        for (int it = 0; it < c->chunk; ++it) RET_IF(enqueue_iteration(c, x, st, it));
+        for (int it = 0; it < c->chunk; ++it) RET_IF(enqueue_any(c, x, st, it));
         CK(c, cudaGetLastError());
         return MASPCG_OK;
     }
-    if (!c->gexec || c->g_x != x || c->g_chunk != c->chunk || c->g_variant != c->stencil_variant) {
+    if (!c->gexec || c->g_x != x || c->g_chunk != c->chunk || c->g_variant != graph_key(c)) {
         if (c->gexec) {
             cudaGraphExecDestroy(c->gexec);
             c->gexec = nullptr;
@@ -255,7 +335,7 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st) {
         cudaStream_t cs = c->cap_stream;
         CK(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         maspcg_status s = MASPCG_OK;
-        for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_iteration(c, x, cs, it);
+        for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_any(c, x, cs, it);
         cudaError_t e = cudaStreamEndCapture(cs, &g);
         if (s != MASPCG_OK) {
             if (g) cudaGraphDestroy(g);
@@ -267,7 +347,7 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st) {
         CK(c, ei);
         c->g_x = x;
         c->g_chunk = c->chunk;
-        c->g_variant = c->stencil_variant;
+        c->g_variant = graph_key(c);
     }
     CK(c, cudaGraphLaunch(c->gexec, st));
     return MASPCG_OK;
@@ -291,6 +371,7 @@ void accumulate_timing(maspcg_ctx *c, int iters_in_chunk) {
 }
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
+    if (use_fused(c)) return 2;
     if (c->nranks == 1) return 3;
     return 2 + (stencil_blocks(c->d, StencilPart::Interior) ? 1 : 0) + 1;
 }
@@ -309,14 +390,17 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     if (maxit < 0) SET_ERR(c, MASPCG_E_INVALID, "maxit must be >= 0");
     if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
     RET_IF(ensure_D(c, st));
+    const bool fused = use_fused(c);
+    if (fused && (c->chunk & 1)) c->chunk += 1;   // even chunks: fixed p-buffer parity per slot
     if (c->timing) RET_IF(maspcg_set_option(c, MASPCG_OPT_TIMING, 1));   // events for this chunk size
 
     // a3: r0 = b - A x0, z0 = r0/D, p0 = z0, dots; then PCG start scalars
     launch_fill_p(c->d, c->a, x, st);
     RET_IF(stencil_with_halo(c, c->a.q, false, false, st));
     launch_setup_residual(c->d, c->a, rhs, c->bc_in == BC_DIRICHLET && c->has_gin,
-                          c->bc_out == BC_DIRICHLET && c->has_gout, st);
-    RET_IF(allreduce_sum(c, c->a.sc->red3, 3, st));
+                          c->bc_out == BC_DIRICHLET && c->has_gout, exact_arith(c), st);
+    RET_IF(allreduce_dot2(c, c->a.sc->red3, 3, st));
+    if (fused && c->nranks > 1) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
     launch_setup_scalars(c->a, tol, maxit, st);
     CK(c, cudaGetLastError());
     long long launched = 4 + (c->nranks > 1 ? 1 : 0);
@@ -327,7 +411,8 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     CK(c, cudaEventSynchronize(c->ev_chunk[0]));   // start scalars (also orders the pinned writes above)
     Scalars s0 = *c->snap[0];
     if (hist) hist[0] = s0.hist0;
-    int status = s0.status, iters = 0;
+    int status = s0.status, iters = 0, hdone = 0;
+    const int ring = fused ? 2 * kMaxChunk : c->chunk;
     double rn = s0.rn, bn = s0.bn;
     bool done = s0.done != 0;
     const bool pipelined = !c->timing;
@@ -351,8 +436,10 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
             CK(c, cudaEventSynchronize(c->ev_chunk[cur]));
             const Scalars &s = *c->snap[cur];
             if (c->timing) accumulate_timing(c, s.iter - iters);
+            const int hnew = fused ? s.hist_count : s.iter;
             if (hist)
-                for (int k = iters + 1; k <= s.iter; ++k) hist[k] = s.hist_ring[(k - 1) % c->chunk];
+                for (int k = hdone + 1; k <= hnew; ++k) hist[k] = s.hist_ring[(k - 1) % ring];
+            hdone = hnew;
             iters = s.iter;
             status = s.status;
             rn = s.rn;
@@ -361,7 +448,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
                 break;
             }
             if (!next_issued) {
-                if (issued >= maxit + c->chunk) SET_ERR(c, MASPCG_E_CUDA, "PCG loop did not terminate");
+                if (issued >= maxit + 2 * c->chunk + 2) SET_ERR(c, MASPCG_E_CUDA, "PCG loop did not terminate");
                 RET_IF(issue(cur ^ 1));
             }
             cur ^= 1;
@@ -373,6 +460,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
     c->stats.kernel_launches += launched;
+    c->stats.path = fused ? 2 : 1;
     c->stats.solves += 1;
     c->stats.iterations += iters;
     if (info) {
@@ -435,6 +523,8 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_ph, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_chunk[0], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_chunk[1], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->snap[0], sizeof(Scalars));
@@ -464,6 +554,9 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->d.div_r = make_fastdiv((uint32_t)nr);
     c->d.div_t = make_fastdiv((uint32_t)nt);
     c->d.periodic_local = nranks == 1 ? 1 : 0;
+    c->fused_bj = fused_bj(nr, nt);
+    c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
+    c->fused_blocks = fused_blocks(nr, nt, c->nloc, c->fused_bj, cuda_device);
     *out = c;
     return MASPCG_OK;
 }
@@ -505,6 +598,8 @@ maspcg_status maspcg_destroy(maspcg_ctx *c) {
     for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
     if (c->ev_p) cudaEventDestroy(c->ev_p);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    if (c->ev_a) cudaEventDestroy(c->ev_a);
+    if (c->ev_ph) cudaEventDestroy(c->ev_ph);
     for (int b = 0; b < 2; ++b) {
         if (c->ev_chunk[b]) cudaEventDestroy(c->ev_chunk[b]);
         if (c->snap[b]) cudaFreeHost(c->snap[b]);
@@ -602,7 +697,7 @@ maspcg_status maspcg_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
     c->ws_bytes = bytes;
     layout(c, (char *)dev_ptr, &c->a);
     CK(c, cudaMemset(c->a.sc, 0, sizeof(Scalars)));
-    CK(c, cudaMemset(c->a.partials, 0, sizeof(double) * 4 * kRedBlocks));
+    CK(c, cudaMemset(c->a.partials, 0, sizeof(double) * 8 * kRedBlocks));
     CK(c, cudaDeviceSynchronize());
     c->metric_dirty = true;
     c->coef_set = false;
@@ -775,9 +870,13 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             break;
         case MASPCG_OPT_USE_GRAPHS: c->use_graphs = v ? 1 : 0; break;
         case MASPCG_OPT_TIMING: c->timing = v ? 1 : 0; break;
-        case MASPCG_OPT_STENCIL:
-            if (v < 0 || v > 2) SET_ERR(c, MASPCG_E_INVALID, "stencil variant must be 0, 1 or 2");
-            c->stencil_variant = (int)v;
+        case MASPCG_OPT_ARITH:
+            if (v < 0 || v > 1) SET_ERR(c, MASPCG_E_INVALID, "arith must be 0 (oracle-exact) or 1 (fast)");
+            c->arith = (int)v;
+            break;
+        case MASPCG_OPT_PATH:
+            if (v < 0 || v > 2) SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels) or 2 (fused)");
+            c->path_opt = (int)v;
             break;
         default: SET_ERR(c, MASPCG_E_INVALID, "unknown option %d", (int)opt);
     }

@@ -56,8 +56,14 @@ def gpu_solve(torch, M, prob, tol=None, maxit=None, chunk=16, x0=None, opts=None
     return st, info, hist, x.cpu().numpy(), S
 
 
-def assert_solve_parity(g, o):
+def assert_solve_parity(g, o, exact=True):
+    """The tolerance contract; with exact=True (the default arithmetic, MASPCG_OPT_ARITH = 0, R24)
+    also the stronger property that the iterates are the oracle's bit for bit."""
     st, info, hist, x, _ = g
+    if exact:
+        assert info["iters"] == o["iters"]
+        assert np.array_equal(hist, o["hist"]), np.abs(hist - o["hist"]).max()
+        assert np.array_equal(x, o["x"]), np.abs(x - o["x"]).max()
     assert st == o["status"], (st, o["status"])
     assert abs(info["iters"] - o["iters"]) <= 1, (info["iters"], o["iters"])
     nx = np.linalg.norm(o["x"])
@@ -122,36 +128,56 @@ def test_apply_parity(torch_cuda, M, oracle_mod, shape):
     assert apply_err(op, x, y).max() <= APPLY_TOL
 
 
+PATHS = [1, 2]   # MASPCG_OPT_PATH: three kernels, fused two passes
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", ["c1", "c2"])
-def test_solve_parity_configs(torch_cuda, M, oracle_mod, name):
+def test_solve_parity_fast_arithmetic(torch_cuda, M, oracle_mod, name, path):
+    """MASPCG_OPT_ARITH = 1 (FMA, plain tree sums): the tolerance contract only."""
+    p = inputs.make_problem(name)
+    o = oracle_mod.solve_problem(p)
+    g = gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: path, M.OPT_ARITH: M.ARITH_FAST})
+    assert_solve_parity(g, o, exact=False)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_solve_parity_configs(torch_cuda, M, oracle_mod, name, path):
     p = inputs.make_problem(name)
     o = oracle_mod.solve_problem(p)
     assert o["status"] == 0
-    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+    g = gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: path})
+    assert_solve_parity(g, o)
+    assert g[4].stats()["path"] == path
 
 
 @pytest.mark.parametrize("seed,shape,bc", [(1, (13, 7, 5), (0, 1)), (2, (33, 17, 9), (0, 0)),
                                           (3, (8, 12, 16), (1, 0)), (4, (5, 4, 1), (0, 1)),
                                           (5, (1, 9, 6), (1, 1)), (6, (20, 1, 3), (0, 0))])
-def test_solve_parity_random(torch_cuda, M, oracle_mod, seed, shape, bc):
+@pytest.mark.parametrize("path", PATHS)
+def test_solve_parity_random(torch_cuda, M, oracle_mod, seed, shape, bc, path):
     nr, nt, np_ = shape
     p = inputs.random_problem(nr, nt, np_, seed, bc_in=bc[0], bc_out=bc[1])
     o = oracle_mod.solve_problem(p)
-    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+    assert_solve_parity(gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: path}), o)
 
 
-def test_solve_parity_warm_start(torch_cuda, M, oracle_mod):
+@pytest.mark.parametrize("path", PATHS)
+def test_solve_parity_warm_start(torch_cuda, M, oracle_mod, path):
     p = inputs.make_problem("c2", x0_seed=9)
     o = oracle_mod.solve_problem(p)
-    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+    assert_solve_parity(gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: path}), o)
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("chunk,graphs,timing", [(1, 1, 0), (3, 1, 0), (16, 0, 0), (64, 1, 0), (7, 1, 1)])
-def test_solve_loop_modes_identical(torch_cuda, M, oracle_mod, chunk, graphs, timing):
+def test_solve_loop_modes_identical(torch_cuda, M, oracle_mod, chunk, graphs, timing, path):
     """Chunking, graph replay and timing mode change how kernels are issued, never the bits."""
     p = inputs.make_problem("c1")
-    ref = gpu_solve(torch_cuda, M, p, chunk=16)
-    g = gpu_solve(torch_cuda, M, p, chunk=chunk, opts={M.OPT_USE_GRAPHS: graphs, M.OPT_TIMING: timing})
+    ref = gpu_solve(torch_cuda, M, p, chunk=16, opts={M.OPT_PATH: path})
+    g = gpu_solve(torch_cuda, M, p, chunk=chunk,
+                  opts={M.OPT_PATH: path, M.OPT_USE_GRAPHS: graphs, M.OPT_TIMING: timing})
     assert g[0] == ref[0] and g[1]["iters"] == ref[1]["iters"]
     assert np.array_equal(g[2], ref[2]) and np.array_equal(g[3], ref[3])
     if timing:
@@ -167,11 +193,13 @@ def test_deterministic_run_to_run(torch_cuda, M):
     assert np.array_equal(a[3], b[3]) and np.array_equal(a[2], b[2])
 
 
-def test_edge_cases(torch_cuda, M, oracle_mod):
+@pytest.mark.parametrize("path", PATHS)
+def test_edge_cases(torch_cuda, M, oracle_mod, path):
     torch = torch_cuda
     p = inputs.random_problem(9, 6, 8, 77)
     o = oracle_mod.solve_problem(p)
     S = M.solver_for_problem(p)
+    S.set_option(M.OPT_PATH, path)
     f = dev(torch, p.f)
     # tol = 0: exactly maxit iterations
     x = dev(torch, p.x0)
@@ -186,6 +214,7 @@ def test_edge_cases(torch_cuda, M, oracle_mod):
     assert st == M.NOT_CONVERGED and info["iters"] == 0 and hist[0] == pytest.approx(o["hist"][0], rel=1e-13)
     # b = 0 (f = 0, g = 0): x = 0, OK, 0 iterations
     S0 = M.solver_for_problem(inputs.random_problem(9, 6, 8, 77, bc_in=1, bc_out=1))
+    S0.set_option(M.OPT_PATH, path)
     x = dev(torch, np.ones((8, 6, 9)))
     st, info, hist = S0.solve(dev(torch, np.zeros((8, 6, 9))), x, 1e-10, 50)
     assert st == M.OK and info["iters"] == 0 and not x.cpu().numpy().any()
@@ -250,11 +279,12 @@ def test_host_entry_points(torch_cuda, M, oracle_mod):
 
 @pytest.mark.slow
 def test_solve_parity_c3_half_resolution(torch_cuda, M, oracle_mod):
-    """c3 recipe (coronal viscosity, stretched grid) at 75 x 150 x 300 = 3.4 M cells."""
+    """c3 recipe (coronal viscosity, stretched grid) at 75 x 150 x 300 = 3.4 M cells, both paths."""
     p = inputs.make_problem("c3", shape=(75, 150, 300))
     o = oracle_mod.solve_problem(p)
     assert o["status"] == 0 and o["iters"] < 1000
-    assert_solve_parity(gpu_solve(torch_cuda, M, p), o)
+    for path in PATHS:
+        assert_solve_parity(gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: path}), o)
 
 
 @pytest.mark.slow
@@ -273,6 +303,7 @@ def test_c3_full_size(torch_cuda, M, oracle_mod):
     ost, ox, oit, ohist, obn, orn = op.pcg(b, p.x0, 0.0, 20)
     xg = x.cpu().numpy()
     assert info["iters"] == oit == 20
+    assert np.array_equal(xg, ox) and np.array_equal(hist, ohist)     # R24: identical iterates
     assert np.linalg.norm(xg - ox) <= SOL_TOL * np.linalg.norm(ox)
     assert_hist(hist, ohist, obn)
     # (2) apply at full size, sampled cells vs the oracle's full apply

@@ -69,13 +69,30 @@ def _worker(rank, world, port, out_dir):
             s[:, :, :-1] += Tr[:, :, 1:full.nr] * u[:, :, 1:]
             s[:, 1:, :] += Tt[:, 1:full.nt, :] * u[:, :-1, :]
             s[:, :-1, :] += Tt[:, 1:full.nt, :] * u[:, 1:, :]
-            s += Tp_lo * um + Tp_hi * up
+            s += Tp_lo * um
+            s += Tp_hi * up
             return D * u - s
 
-        def allsum(*v):
-            t = torch.tensor(v, dtype=torch.float64)
-            dist.all_reduce(t)
-            return t.numpy()
+        def split(a):
+            c = 134217729.0 * a
+            h = c - (c - a)
+            return h, a - h
+
+        def terms(a, b):
+            """exact expansion of the local part of a.b: a_i b_i = h_i + r_i (TwoProduct)"""
+            a, b = a.ravel(), b.ravel()
+            h = a * b
+            ah, al = split(a)
+            bh, bl = split(b)
+            return np.concatenate([h, al * bl - (((h - ah * bh) - al * bh) - ah * bl)])
+
+        def allsum(*pairs):
+            """global dot products, correctly rounded (R24): gather every rank's exact terms, fsum"""
+            import math
+            loc = [terms(a, b) for a, b in pairs]
+            out = [None] * world
+            dist.all_gather_object(out, loc)
+            return [math.fsum(np.concatenate([o[k] for o in out])) for k in range(len(pairs))]
 
         # distributed apply == slice of the oracle's global apply
         u = np.random.default_rng(5).standard_normal(full.x0.shape)
@@ -90,18 +107,18 @@ def _worker(rank, world, port, out_dir):
         r = b - apply(x)
         z = r / D
         p = z.copy()
-        rho, rr, bb = allsum((r * z).sum(), (r * r).sum(), (b * b).sum())
+        rho, rr, bb = allsum((r, z), (r, r), (b, b))
         bn = np.sqrt(bb)
         hist = [np.sqrt(rr)]
         it = 0
         for it in range(1, full.maxit + 1):
             q = apply(p)
-            (pi,) = allsum((p * q).sum())
+            (pi,) = allsum((p, q))
             alpha = rho / pi
-            x += alpha * p
-            r -= alpha * q
+            x = x + alpha * p
+            r = r - alpha * q
             z = r / D
-            rz, rr = allsum((r * z).sum(), (r * r).sum())
+            rz, rr = allsum((r, z), (r, r))
             hist.append(np.sqrt(rr))
             if hist[-1] <= full.tol * bn:
                 break
@@ -135,11 +152,10 @@ def test_two_rank_decomposition_reproduces_global_oracle(tmp_path, oracle_mod):
     assert abs(res[0]["iters"] - o["iters"]) <= 1
     x = np.concatenate([r["x"] for r in res], axis=0)
     assert np.linalg.norm(x - o["x"]) <= 1e-10 * np.linalg.norm(o["x"])
-    # history: this host model sums with numpy (pairwise) and a reordered stencil, which already
-    # moves c1's history by up to ~2e-10 around iteration 107 (CG amplifies rounding there); the
-    # 1e-10 history contract is the GPU path's (test_gpu_parity.py / test_gpu_multirank.py).
-    k = min(len(res[0]["hist"]), len(o["hist"]))
-    assert (np.abs(res[0]["hist"][:k] - o["hist"][:k]) / o["hist"][:k]).max() <= 1e-9
+    # same expressions in the same order + correctly rounded dot products (R24): the decomposed
+    # solve reproduces the oracle's iterates exactly, bit for bit
+    assert res[0]["iters"] == o["iters"]
+    assert np.array_equal(x, o["x"]) and np.array_equal(res[0]["hist"], o["hist"])
 
 
 def test_slab_extent_rules():
