@@ -11,16 +11,19 @@
 //   pass B  k_pass_b
 //       alpha = rho / (p.q); r -= alpha q; z = r/D; partials r.z, r.r        32 B/cell
 //
-// Same arithmetic as the three-kernel path (kernels.cu): p, x, q and r are formed with the same
-// FMA expressions in the same order, so only the dot-product trees differ.  PAPER.md credits
+// Same arithmetic as the three-kernel path (kernels.cu) and, with the default exact policy of
+// arith.cuh, as the oracle: identical iterates.  PAPER.md credits
 // kernel fusion and asynchronous launches for the best GPU version; this is that
 // fusion done by hand for sm_100a.
 //
 // Tiling (2.5-D phi march): the slab is cut into j-tiles of BJ theta rows; the (j-tile, plane)
-// pairs are split into equal contiguous segments, one per persistent block (2 blocks/SM).  A block
-// marches its segment plane by plane: phase 1 computes p_new on the tile plus one halo row on each
-// side into ring slot k%3 (and stores the owned rows to HBM, updates x); phase 2 applies the
-// 7-point stencil to plane k-1 from the ring.  The halo rows / the two halo planes of a segment are
+// pairs are split into equal contiguous segments, one per persistent block (1 block of 512 threads
+// per SM, ~160 KB of shared memory).  A block marches its segment plane by plane: phase 1 loads r,
+// D, p_old, x of up to kAM tile cells per thread in one batch, computes p_new into ring slot k%3
+// (plus the two halo rows), keeps D in a 2-plane shared ring and stores p_new and x; phase 2
+// applies the 7-point stencil to plane k-1 from the rings, carrying the upper T_phi face of each
+// cell in a register as the next plane's lower face -- so D and T_phi are read from HBM once
+// (re-reads across plane steps would miss in L2: ~150 blocks x ~250 KB per step).  The halo rows / the two halo planes of a segment are
 // recomputed from r, D, p_old (a few % extra reads, mostly L2 hits) instead of being exchanged.
 // Planes -1 and nloc come from halo pointers: the wrap planes on a single rank, received halo
 // buffers on several ranks.
@@ -34,7 +37,8 @@ namespace maspcg {
 
 namespace {
 
-constexpr int kAThreads = 512;
+constexpr int kAThreads = 512;   // one persistent block per SM (smem-bound)
+constexpr int kAM = 8;           // tile cells per thread per plane (register batches)
 
 // plane pointer of array `base` for local plane k in [-1, nloc] (halo pointers at the ends)
 __device__ __forceinline__ const double *plane_ptr(const double *base, const double *lo, const double *hi, int k,
@@ -46,9 +50,9 @@ __device__ __forceinline__ const double *plane_ptr(const double *base, const dou
 
 // ------------------------------------------------------------------------ pass A
 template <bool EXACT>
-__global__ void __launch_bounds__(kAThreads, 2) k_pass_a(Dims d, DevArrays a, FusedArgs f) {
+__global__ void __launch_bounds__(kAThreads, 1) k_pass_a(Dims d, DevArrays a, FusedArgs f) {
     using A = Ar<EXACT>;
-    extern __shared__ double ring[];   // [3][ext_rows * nr]
+    extern __shared__ double smem[];   // p ring [3][(bj+2) nr] | D ring [2][bj nr]
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
     const int it_done = sc->iter;
@@ -95,11 +99,16 @@ __global__ void __launch_bounds__(kAThreads, 2) k_pass_a(Dims d, DevArrays a, Fu
     const int nr = d.nr, nt = d.nt, nloc = d.nloc;
     const size_t plane = d.plane;
     const int bj = f.bj;
-    const int ext = (bj + 2) * nr;   // ring slot size
+    const int ext = (bj + 2) * nr;             // p ring slot: tile rows + one halo row on each side
+    const int own = bj * nr;                   // D ring slot: tile rows
+    double *ring = smem;                       // [3][ext]
+    double *dring = smem + 3 * ext;            // [2][own]
     const uint32_t T = (uint32_t)f.n_jt * (uint32_t)nloc;
     const uint32_t t_beg = (uint32_t)(((uint64_t)T * blockIdx.x) / total);
     const uint32_t t_end = (uint32_t)(((uint64_t)T * (blockIdx.x + 1)) / total);
+    const int tid = threadIdx.x;
     Acc<EXACT> dot[1];
+    double tp_carry[kAM];                      // T_phi upper face of the previous plane = lower face of this one
 
     uint32_t t = t_beg;
     while (t < t_end) {
@@ -109,58 +118,106 @@ __global__ void __launch_bounds__(kAThreads, 2) k_pass_a(Dims d, DevArrays a, Fu
         t += (uint32_t)(kb - ka + 1);
         const int j0 = jt * bj;
         const int rows = min(bj, nt - j0);
-        const int ext_n = (rows + 2) * nr;
+        const int own_n = rows * nr;
         for (int k = ka - 1; k <= kb + 1; ++k) {
-            // ---- phase 1: p_new on plane k, rows j0-1 .. j0+rows (ring slot k mod 3)
+            // ---- phase 1: p_new on plane k for the tile rows (batched loads, kAM cells per thread)
             double *slot = ring + (size_t)((k + 3) % 3) * ext;
+            double *dslot = dring + (size_t)(k & 1) * own;
             const double *rp = plane_ptr(f.r, f.r_lo, f.r_hi, k, nloc, plane);
             const double *dp = plane_ptr(a.D, f.d_lo, f.d_hi, k, nloc, plane);
             const double *pp = plane_ptr(pold, f.p_lo, f.p_hi, k, nloc, plane);
             const bool own_plane = k >= ka && k <= kb;
-            for (int l = threadIdx.x; l < ext_n; l += kAThreads) {
-                const int re = (int)f.div_r.div((uint32_t)l);      // ext row 0 .. rows+1
-                const int j = j0 - 1 + re;
-                if (j < 0 || j >= nt) continue;
-                const int i = l - re * nr;
-                const size_t g = (size_t)j * nr + i;
-                const double z = __ddiv_rn(__ldg(rp + g), __ldg(dp + g));
-                double pn = z;
-                double po = 0.0;
-                if (!first) {
-                    po = __ldg(pp + g);
-                    pn = A::axpy(beta, po, z);
+            const size_t tile0 = (size_t)j0 * nr;      // tile start within the plane
+            {
+                double rv[kAM], dv[kAM], pv[kAM], xv[kAM];
+#pragma unroll
+                for (int m = 0; m < kAM; ++m) {
+                    const int o = tid + m * kAThreads;
+                    rv[m] = dv[m] = 1.0;
+                    pv[m] = xv[m] = 0.0;
+                    if (o < own_n) {
+                        rv[m] = __ldg(rp + tile0 + o);
+                        dv[m] = __ldg(dp + tile0 + o);
+                        if (!first) {
+                            pv[m] = __ldg(pp + tile0 + o);
+                            if (own_plane) xv[m] = x[(size_t)k * plane + tile0 + o];
+                        }
+                    }
                 }
-                slot[l] = pn;
-                if (own_plane && re >= 1 && re <= rows) {
-                    const size_t gc = (size_t)k * plane + g;
-                    f.p_new[gc] = pn;
-                    if (!first) x[gc] = A::axpy(alpha, po, x[gc]);
+#pragma unroll
+                for (int m = 0; m < kAM; ++m) {
+                    const int o = tid + m * kAThreads;
+                    if (o < own_n) {
+                        const double z = __ddiv_rn(rv[m], dv[m]);
+                        const double pn = first ? z : A::axpy(beta, pv[m], z);
+                        slot[nr + o] = pn;
+                        dslot[o] = dv[m];
+                        if (own_plane) {
+                            const size_t gc = (size_t)k * plane + tile0 + o;
+                            f.p_new[gc] = pn;
+                            if (!first) x[gc] = A::axpy(alpha, pv[m], xv[m]);
+                        }
+                    }
                 }
             }
+            // the two halo rows of the tile (recomputed from r, D, p_old; not stored)
+            for (int h = tid; h < 2 * nr; h += kAThreads) {
+                const int top = h >= nr;
+                const int i = h - top * nr;
+                const int j = top ? j0 + rows : j0 - 1;
+                if (j < 0 || j >= nt) continue;
+                const size_t g = (size_t)j * nr + i;
+                const double z = __ddiv_rn(__ldg(rp + g), __ldg(dp + g));
+                slot[(top ? (rows + 1) * nr : 0) + i] = first ? z : A::axpy(beta, __ldg(pp + g), z);
+            }
             __syncthreads();
-            // ---- phase 2: stencil on plane k-1 (needs ring slots k-2, k-1, k)
+            // ---- phase 2: stencil on plane ks = k-1 from ring slots ks-1, ks, ks+1
             const int ks = k - 1;
             if (ks >= ka) {
-                const double *sm = ring + (size_t)((ks + 2) % 3) * ext;   // plane ks-1
-                const double *s0 = ring + (size_t)((ks + 3) % 3) * ext;   // plane ks
-                const double *sp = slot;                                   // plane ks+1
-                const size_t pbase = (size_t)ks * plane;
-                for (int l = nr + threadIdx.x; l < (rows + 1) * nr; l += kAThreads) {
-                    const int re = (int)f.div_r.div((uint32_t)l);
-                    const int j = j0 - 1 + re;
-                    const int i = l - re * nr;
-                    const size_t c = pbase + (size_t)j * nr + i;
-                    const double pc = s0[l];
-                    double s = 0.0;
-                    if (i > 0) s = A::acc(s, __ldg(a.Tr + c), s0[l - 1]);
-                    if (i < nr - 1) s = A::acc(s, __ldg(a.Tr + c + 1), s0[l + 1]);
-                    if (j > 0) s = A::acc(s, __ldg(a.Tt + c), s0[l - nr]);
-                    if (j < nt - 1) s = A::acc(s, __ldg(a.Tt + c + nr), s0[l + nr]);
-                    s = A::acc(s, __ldg(a.Tp + c), sm[l]);
-                    s = A::acc(s, __ldg(a.Tp + c + plane), sp[l]);
-                    const double q = A::diag_minus(__ldg(a.D + c), pc, s);
-                    a.q[c] = q;
-                    dot[0].add(pc, q);
+                const double *sm_ = ring + (size_t)((ks + 2) % 3) * ext;   // plane ks-1
+                const double *s0 = ring + (size_t)((ks + 3) % 3) * ext;    // plane ks
+                const double *sp = slot;                                    // plane ks+1
+                const double *dk = dring + (size_t)(ks & 1) * own;
+                const size_t pbase = (size_t)ks * plane + tile0;
+                double tr0[kAM], tr1[kAM], tt0[kAM], tt1[kAM], tph[kAM];
+#pragma unroll
+                for (int m = 0; m < kAM; ++m) {
+                    const int o = tid + m * kAThreads;
+                    tr0[m] = tr1[m] = tt0[m] = tt1[m] = tph[m] = 0.0;
+                    if (o < own_n) {
+                        const int jj = (int)f.div_r.div((uint32_t)o);
+                        const int i = o - jj * nr;
+                        const int j = j0 + jj;
+                        const size_t c = pbase + o;
+                        tr0[m] = __ldg(a.Tr + c);
+                        if (i < nr - 1) tr1[m] = __ldg(a.Tr + c + 1);
+                        tt0[m] = __ldg(a.Tt + c);
+                        if (j < nt - 1) tt1[m] = __ldg(a.Tt + c + nr);
+                        tph[m] = __ldg(a.Tp + c + plane);
+                        if (ks == ka) tp_carry[m] = __ldg(a.Tp + c);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < kAM; ++m) {
+                    const int o = tid + m * kAThreads;
+                    if (o < own_n) {
+                        const int jj = (int)f.div_r.div((uint32_t)o);
+                        const int i = o - jj * nr;
+                        const int j = j0 + jj;
+                        const int l = nr + o;
+                        const double pc = s0[l];
+                        double s = 0.0;
+                        if (i > 0) s = A::acc(s, tr0[m], s0[l - 1]);
+                        if (i < nr - 1) s = A::acc(s, tr1[m], s0[l + 1]);
+                        if (j > 0) s = A::acc(s, tt0[m], s0[l - nr]);
+                        if (j < nt - 1) s = A::acc(s, tt1[m], s0[l + nr]);
+                        s = A::acc(s, tp_carry[m], sm_[l]);
+                        s = A::acc(s, tph[m], sp[l]);
+                        const double q = A::diag_minus(dk[o], pc, s);
+                        a.q[pbase + o] = q;
+                        dot[0].add(pc, q);
+                        tp_carry[m] = tph[m];
+                    }
                 }
             }
             __syncthreads();
@@ -224,15 +281,15 @@ __global__ void __launch_bounds__(kThreads, kRedBlocks / 148) k_pass_b(Dims d, D
 
 // ------------------------------------------------------------------------ launchers
 int fused_bj(int nr, int nt) {
-    // ring of 3 planes of (BJ + 2) rows of nr doubles in <= ~96 KB -> 2 blocks per SM
-    int ext_rows = (96 * 1024) / (3 * 8 * nr);
-    int bj = ext_rows - 2;
-    if (bj < 1) bj = 1;
+    // tile rows: bj * nr <= kAM * kAThreads cells (one register batch per thread) and the shared
+    // memory (3 p planes of bj+2 rows + 2 D planes of bj rows) within ~200 KB.  0: not supported.
+    int bj = (kAM * kAThreads) / nr;
+    while (bj > 0 && fused_smem_bytes(nr, bj) > 200 * 1024) --bj;
     if (bj > nt) bj = nt;
     return bj;
 }
 
-size_t fused_smem_bytes(int nr, int bj) { return (size_t)3 * (bj + 2) * nr * sizeof(double); }
+size_t fused_smem_bytes(int nr, int bj) { return (size_t)(3 * (bj + 2) + 2 * bj) * nr * sizeof(double); }
 
 int fused_blocks(int nr, int nt, int nloc, int bj, int device) {
     static int cached_dev = -1, sms = 148;
@@ -248,7 +305,7 @@ int fused_blocks(int nr, int nt, int nloc, int bj, int device) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_pass_a<false>, kAThreads, smem);
     if (occ2 < occ) occ = occ2;
     if (occ < 1) occ = 1;
-    if (occ > 2) occ = 2;
+    if (occ > 1) occ = 1;
     const long long tiles = (long long)((nt + bj - 1) / bj) * nloc;
     long long b = (long long)sms * occ;
     if (b > tiles) b = tiles;

@@ -199,7 +199,7 @@ maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaSt
     return MASPCG_OK;
 }
 
-bool use_fused(const maspcg_ctx *c) { return c->path_opt != 1; }
+bool use_fused(const maspcg_ctx *c) { return c->path_opt != 1 && c->fused_bj > 0; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 int graph_key(const maspcg_ctx *c) { return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0); }
 
@@ -554,9 +554,11 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->d.div_r = make_fastdiv((uint32_t)nr);
     c->d.div_t = make_fastdiv((uint32_t)nt);
     c->d.periodic_local = nranks == 1 ? 1 : 0;
-    c->fused_bj = fused_bj(nr, nt);
-    c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
-    c->fused_blocks = fused_blocks(nr, nt, c->nloc, c->fused_bj, cuda_device);
+    c->fused_bj = fused_bj(nr, nt);   // 0: nr too large for one register batch per thread -> three kernels
+    if (c->fused_bj > 0) {
+        c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
+        c->fused_blocks = fused_blocks(nr, nt, c->nloc, c->fused_bj, cuda_device);
+    }
     *out = c;
     return MASPCG_OK;
 }

@@ -239,6 +239,8 @@ class Solver:
         if raise_on_error and st < 0:
             self._check(st)
         d = {"iters": info.iters, "bnorm": info.bnorm, "rnorm": info.rnorm, "rel_resid": info.rel_resid}
+        if st < 0:
+            d["error"] = (self._L.maspcg_last_error(self.ctx) or b"").decode()
         return st, d, hist[: max(info.iters, 0) + 1].copy()
 
     def apply(self, x, y=None, stream=None):
