@@ -46,6 +46,77 @@ __device__ __forceinline__ const double *plane_ptr(const double *base, const dou
     return k < 0 ? lo : (k >= nloc ? hi : base + (size_t)k * plane);
 }
 
+// Scalars of pass A: finalise iteration `iter` (R12, R13) and form beta (R11).
+struct PassAScalars {
+    bool first;
+    double alpha, beta, rz, rn;
+    int it_done;
+};
+
+// Reads the scalars; when iteration `iter` was the last, completes its deferred x update, lets the
+// last block publish status / history and returns true (the caller returns).
+template <bool EXACT>
+__device__ __forceinline__ bool pass_a_prologue(const Dims &d, const DevArrays &a, const FusedArgs &f,
+                                                PassAScalars &S) {
+    using A = Ar<EXACT>;
+    Scalars *sc = a.sc;
+    S.it_done = sc->iter;
+    S.first = S.it_done == 0;
+    S.rz = 0.0;
+    S.rn = 0.0;
+    bool stop = false, conv = false, bad = false;
+    if (!S.first) {
+        S.rz = __dadd_rn(sc->red2[0], sc->red2[1]);
+        S.rn = sqrt(__dadd_rn(sc->red2[2], sc->red2[3]));
+        conv = S.rn <= sc->tolbn;
+        bad = !isfinite(S.rn) || !isfinite(S.rz);
+        stop = conv || bad || S.it_done >= sc->maxit;
+    }
+    S.alpha = S.first ? 0.0 : sc->alpha;
+    S.beta = S.first ? 0.0 : __ddiv_rn(S.rz, sc->rho);
+    if (!stop) return false;
+    // iteration `it_done` is the last: complete its deferred x update and finish
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride)
+        f.x[c] = A::axpy(S.alpha, __ldg(f.p_old + c), f.x[c]);
+    __shared__ bool am_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        am_last = atomicAdd(&sc->ticket[4], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (am_last && threadIdx.x == 0) {
+        __threadfence();
+        sc->hist_ring[(S.it_done - 1) % (2 * kMaxChunk)] = S.rn;
+        sc->hist_count = S.it_done;
+        sc->rn = S.rn;
+        sc->status = conv ? ST_OK : (bad ? ST_E_BREAKDOWN : ST_NOT_CONVERGED);
+        sc->done = 1;
+        sc->ticket[4] = 0u;
+    }
+    return true;
+}
+
+// p.q -> red1 (Dot2 pair); the last block also publishes the history entry and rho of iteration `iter`.
+template <bool EXACT, int NT>
+__device__ __forceinline__ void pass_a_epilogue(const DevArrays &a, const PassAScalars &S, Acc<EXACT> (&dot)[1]) {
+    Scalars *sc = a.sc;
+    Acc<EXACT> out[1];
+    if (reduce_last<EXACT, NT, 1>(dot, a.partials, &sc->ticket[5], blockIdx.x, gridDim.x, out)) {
+        if (threadIdx.x == 0) {
+            sc->red1[0] = out[0].p;
+            sc->red1[1] = out[0].s;
+            if (!S.first) {
+                sc->hist_ring[(S.it_done - 1) % (2 * kMaxChunk)] = S.rn;
+                sc->hist_count = S.it_done;
+                sc->rn = S.rn;
+                sc->rho = S.rz;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------ pass A
@@ -55,46 +126,13 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a(Dims d, DevArrays a, Fu
     extern __shared__ double smem[];   // p ring [3][(bj+2) nr] | D ring [2][bj nr]
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
-    const int it_done = sc->iter;
-    const bool first = it_done == 0;
-    double rz = 0.0, rn = 0.0;
-    bool stop = false, conv = false, bad = false;
-    if (!first) {
-        rz = __dadd_rn(sc->red2[0], sc->red2[1]);
-        rn = sqrt(__dadd_rn(sc->red2[2], sc->red2[3]));
-        conv = rn <= sc->tolbn;
-        bad = !isfinite(rn) || !isfinite(rz);
-        stop = conv || bad || it_done >= sc->maxit;
-    }
-    const double alpha = first ? 0.0 : sc->alpha;
-    const double beta = first ? 0.0 : __ddiv_rn(rz, sc->rho);
+    PassAScalars S;
+    if (pass_a_prologue<EXACT>(d, a, f, S)) return;
+    const bool first = S.first;
+    const double alpha = S.alpha, beta = S.beta;
     const double *__restrict__ pold = f.p_old;
     double *__restrict__ x = f.x;
     const unsigned total = gridDim.x;
-
-    if (stop) {
-        // iteration `it_done` is the last: complete its deferred x update and finish
-        const uint32_t stride = gridDim.x * blockDim.x;
-        for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride)
-            x[c] = A::axpy(alpha, __ldg(pold + c), x[c]);
-        __shared__ bool am_last;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            am_last = atomicAdd(&sc->ticket[4], 1u) == total - 1;
-        }
-        __syncthreads();
-        if (am_last && threadIdx.x == 0) {
-            __threadfence();
-            sc->hist_ring[(it_done - 1) % (2 * kMaxChunk)] = rn;
-            sc->hist_count = it_done;
-            sc->rn = rn;
-            sc->status = conv ? ST_OK : (bad ? ST_E_BREAKDOWN : ST_NOT_CONVERGED);
-            sc->done = 1;
-            sc->ticket[4] = 0u;
-        }
-        return;
-    }
 
     const int nr = d.nr, nt = d.nt, nloc = d.nloc;
     const size_t plane = d.plane;
@@ -224,19 +262,202 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a(Dims d, DevArrays a, Fu
         }
     }
 
-    Acc<EXACT> out[1];
-    if (reduce_last<EXACT, kAThreads, 1>(dot, a.partials, &sc->ticket[5], blockIdx.x, total, out)) {
-        if (threadIdx.x == 0) {
-            sc->red1[0] = out[0].p;
-            sc->red1[1] = out[0].s;
-            if (!first) {
-                sc->hist_ring[(it_done - 1) % (2 * kMaxChunk)] = rn;
-                sc->hist_count = it_done;
-                sc->rn = rn;
-                sc->rho = rz;
+    pass_a_epilogue<EXACT, kAThreads>(a, S, dot);
+}
+
+// ------------------------------------------------------------------------ pass A, TMA variant
+// Same arithmetic as k_pass_a.  The grid is a lockstep tiling: block b owns j-tile b % njt (rows
+// [jt*nt/njt, (jt+1)*nt/njt)) over the plane chunk b / njt, so blocks on neighbouring tiles march
+// through the same planes at the same time and the halo rows they both read are L2 hits.  The
+// streams that phase 1 needs -- r, D, p_old on the tile rows plus one halo row each side, and x on
+// the tile rows -- are staged by the Tensor Memory Accelerator (cp.async.bulk, one 1-D bulk copy per
+// array and plane, completion on an mbarrier) into a 3-stage shared ring, two planes ahead of the
+// compute, so ~60 KB per SM are always in flight without holding registers.  T_r, T_theta, T_phi
+// are read once per cell in phase 2 with batched loads.  Requires nr even (16-byte row alignment).
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct TmaStage {
+    double *r, *D, *P, *X;   // r, D, p_old: ext rows (row 0 = tile row j0-1); X: tile rows
+};
+
+}  // namespace
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a, FusedArgs f) {
+    using A = Ar<EXACT>;
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) uint64_t bars[3];
+    Scalars *sc = a.sc;
+    if (*(volatile int *)&sc->done) return;
+    PassAScalars S;
+    if (pass_a_prologue<EXACT>(d, a, f, S)) return;
+    const bool first = S.first;
+    const double alpha = S.alpha, beta = S.beta;
+    double *__restrict__ x = f.x;
+
+    const int nr = d.nr, nt = d.nt, nloc = d.nloc;
+    const size_t plane = d.plane;
+    const int njt = f.n_jt;
+    const int jt = blockIdx.x % njt, ch = blockIdx.x / njt;
+    const int j0 = (int)(((long long)jt * nt) / njt), j1 = (int)(((long long)(jt + 1) * nt) / njt);
+    const int ka = (int)(((long long)ch * nloc) / f.nch), kb = (int)(((long long)(ch + 1) * nloc) / f.nch) - 1;
+    const int h = j1 - j0;
+    const int sext = (f.bj + 2) * nr, sown = f.bj * nr;   // f.bj = max tile rows
+    const size_t stage_sz = (size_t)3 * sext + sown;
+    // stage q: r | D | p_old on the ext rows, x on the tile rows
+    auto stage = [&](int q) -> TmaStage {
+        double *b = smem + (size_t)q * stage_sz;
+        return {b, b + sext, b + 2 * sext, b + 3 * sext};
+    };
+    double *ring = smem + (size_t)3 * (3 * sext + sown);   // [3][sext] p_new
+    const int tid = threadIdx.x;
+    uint32_t parity[3] = {0u, 0u, 0u};
+    if (tid == 0) {
+        for (int q = 0; q < 3; ++q) mbar_init(&bars[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int jr0 = max(j0 - 1, 0), jr1 = min(j1 + 1, nt);   // ext rows present in the grid
+    const int roff = jr0 - (j0 - 1);                         // 0, or 1 at the lower pole tile
+    // issue the bulk copies of plane k into stage q (thread 0)
+    auto issue = [&](int k, int q) {
+        const bool own_plane = k >= ka && k <= kb;
+        const double *rp = plane_ptr(f.r, f.r_lo, f.r_hi, k, nloc, plane);
+        const double *dp = plane_ptr(a.D, f.d_lo, f.d_hi, k, nloc, plane);
+        const double *pp = plane_ptr(f.p_old, f.p_lo, f.p_hi, k, nloc, plane);
+        const uint32_t eb = (uint32_t)(8 * (size_t)(jr1 - jr0) * nr);
+        const uint32_t ob = (uint32_t)(8 * (size_t)h * nr);
+        const bool wx = own_plane && !first;
+        const uint32_t bytes = eb * (first ? 2u : 3u) + (wx ? ob : 0u);
+        mbar_expect_tx(&bars[q], bytes);
+        const size_t e0 = (size_t)jr0 * nr;
+        const TmaStage sq = stage(q);
+        bulk_g2s(sq.r + (size_t)roff * nr, rp + e0, eb, &bars[q]);
+        bulk_g2s(sq.D + (size_t)roff * nr, dp + e0, eb, &bars[q]);
+        if (!first) bulk_g2s(sq.P + (size_t)roff * nr, pp + e0, eb, &bars[q]);
+        if (wx) bulk_g2s(sq.X, x + (size_t)k * plane + (size_t)j0 * nr, ob, &bars[q]);
+    };
+    if (tid == 0) {
+        issue(ka - 1, 0);
+        issue(ka, 1);
+    }
+
+    Acc<EXACT> dot[1];
+    double tp_carry[kAM];
+    const int ext_n = (h + 2) * nr, own_n = h * nr;
+    const bool carry_ok = own_n <= kAM * kAThreads;   // one register batch: T_phi carried across planes
+    const int nsteps = kb - ka + 3;   // planes ka-1 .. kb+1
+    for (int kk = 0; kk < nsteps; ++kk) {
+        const int k = ka - 1 + kk;
+        const int q = kk % 3;
+        mbar_wait(&bars[q], parity[q]);
+        parity[q] ^= 1u;
+        // ---- phase 1: p_new of plane k on the ext rows (from shared memory only)
+        const bool own_plane = k >= ka && k <= kb;
+        double *slot = ring + (size_t)q * sext;
+        const TmaStage S1 = stage(q);
+        for (int e = tid; e < ext_n; e += kAThreads) {
+            const int re = (int)f.div_r.div((uint32_t)e);
+            const int j = j0 - 1 + re;
+            if (j < 0 || j >= nt) continue;
+            const double z = __ddiv_rn(S1.r[e], S1.D[e]);
+            const double po = first ? 0.0 : S1.P[e];
+            const double pn = first ? z : A::axpy(beta, po, z);
+            slot[e] = pn;
+            if (own_plane && re >= 1 && re <= h) {
+                const size_t gc = (size_t)k * plane + (size_t)j * nr + (e - re * nr);
+                f.p_new[gc] = pn;
+                if (!first) x[gc] = A::axpy(alpha, po, S1.X[e - nr]);
             }
         }
+        __syncthreads();
+        // ---- phase 2: stencil of plane ks = k-1
+        const int ks = k - 1;
+        if (ks >= ka) {
+            const double *sm_ = ring + (size_t)((kk + 1) % 3) * sext;   // plane ks-1 (slot (kk-2)%3)
+            const double *s0 = ring + (size_t)((kk + 2) % 3) * sext;    // plane ks   (slot (kk-1)%3)
+            const double *sp = slot;                                     // plane ks+1
+            const double *dk = stage((kk + 2) % 3).D;                    // D of plane ks (ext rows)
+            const size_t pbase = (size_t)ks * plane + (size_t)j0 * nr;
+            for (int o0 = 0; o0 < own_n; o0 += kAM * kAThreads) {
+                double tr0[kAM], tr1[kAM], tt0[kAM], tt1[kAM], tph[kAM];
+#pragma unroll
+                for (int m = 0; m < kAM; ++m) {
+                    const int o = o0 + tid + m * kAThreads;
+                    tr0[m] = tr1[m] = tt0[m] = tt1[m] = tph[m] = 0.0;
+                    if (o < own_n) {
+                        const int jj = (int)f.div_r.div((uint32_t)o);
+                        const int i = o - jj * nr;
+                        const size_t c = pbase + o;
+                        tr0[m] = __ldg(a.Tr + c);
+                        if (i < nr - 1) tr1[m] = __ldg(a.Tr + c + 1);
+                        tt0[m] = __ldg(a.Tt + c);
+                        if (j0 + jj < nt - 1) tt1[m] = __ldg(a.Tt + c + nr);
+                        tph[m] = __ldg(a.Tp + c + plane);
+                        if (ks == ka || !carry_ok) tp_carry[m] = __ldg(a.Tp + c);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < kAM; ++m) {
+                    const int o = o0 + tid + m * kAThreads;
+                    if (o < own_n) {
+                        const int jj = (int)f.div_r.div((uint32_t)o);
+                        const int i = o - jj * nr;
+                        const int j = j0 + jj;
+                        const int l = nr + o;
+                        const double pc = s0[l];
+                        double s = 0.0;
+                        if (i > 0) s = A::acc(s, tr0[m], s0[l - 1]);
+                        if (i < nr - 1) s = A::acc(s, tr1[m], s0[l + 1]);
+                        if (j > 0) s = A::acc(s, tt0[m], s0[l - nr]);
+                        if (j < nt - 1) s = A::acc(s, tt1[m], s0[l + nr]);
+                        s = A::acc(s, tp_carry[m], sm_[l]);
+                        s = A::acc(s, tph[m], sp[l]);
+                        const double qv = A::diag_minus(dk[l], pc, s);
+                        a.q[pbase + o] = qv;
+                        dot[0].add(pc, qv);
+                        tp_carry[m] = tph[m];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- refill the stage of plane k-1 (consumed) with plane k+2
+        if (tid == 0 && kk + 2 < nsteps) {
+            fence_proxy_async();
+            issue(k + 2, (kk + 2) % 3);
+        }
     }
+    pass_a_epilogue<EXACT, kAThreads>(a, S, dot);
 }
 
 // ------------------------------------------------------------------------ pass B
@@ -291,29 +512,65 @@ int fused_bj(int nr, int nt) {
 
 size_t fused_smem_bytes(int nr, int bj) { return (size_t)(3 * (bj + 2) + 2 * bj) * nr * sizeof(double); }
 
-int fused_blocks(int nr, int nt, int nloc, int bj, int device) {
+static int sm_count(int device) {
     static int cached_dev = -1, sms = 148;
     if (cached_dev != device) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         cached_dev = device;
     }
+    return sms;
+}
+
+int fused_blocks(int nr, int nt, int nloc, int bj, int device) {
+    const int sms = sm_count(device);
     const size_t smem = fused_smem_bytes(nr, bj);
     cudaFuncSetAttribute(k_pass_a<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_pass_a<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int occ = 0, occ2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_a<true>, kAThreads, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_pass_a<false>, kAThreads, smem);
-    if (occ2 < occ) occ = occ2;
-    if (occ < 1) occ = 1;
-    if (occ > 1) occ = 1;
     const long long tiles = (long long)((nt + bj - 1) / bj) * nloc;
-    long long b = (long long)sms * occ;
+    long long b = sms;
     if (b > tiles) b = tiles;
     if (b > kRedBlocks) b = kRedBlocks;
     return (int)b;
 }
 
+size_t tma_smem_bytes(int nr, int hmax) { return (size_t)8 * nr * (15 * (size_t)hmax + 24); }
+
+bool fused_tma_geometry(int nr, int nt, int nloc, int device, int *njt, int *nch, int *hmax) {
+    if (nr % 2 != 0) return false;                          // 16-byte aligned rows for the bulk copies
+    const size_t limit = 220 * 1024;
+    const int sms = sm_count(device);
+    double best = -1.0;
+    for (int c = 1; c <= nloc && c <= sms; ++c) {
+        int t = sms / c;
+        if (t > nt) t = nt;
+        if (t < 1) break;
+        const int h = (nt + t - 1) / t;
+        if (tma_smem_bytes(nr, h) > limit) continue;
+        const double util = (double)t * c / sms;
+        // prefer full occupancy of the SMs, then taller tiles (fewer recomputed halo rows)
+        const double score = (util >= 0.97 ? 1.0 : util) * 1000.0 + h;
+        if (score > best) {
+            best = score;
+            *njt = t;
+            *nch = c;
+            *hmax = h;
+        }
+    }
+    if (best < 0) return false;
+    const size_t smem = tma_smem_bytes(nr, *hmax);
+    cudaFuncSetAttribute(k_pass_a_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_pass_a_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return true;
+}
+
 void launch_pass_a(const Dims &d, const DevArrays &a, const FusedArgs &f, int blocks, bool exact, cudaStream_t st) {
+    if (f.tma) {
+        const size_t smem = tma_smem_bytes(d.nr, f.bj);
+        const int grid = f.n_jt * f.nch;
+        if (exact) k_pass_a_tma<true><<<grid, kAThreads, smem, st>>>(d, a, f);
+        else k_pass_a_tma<false><<<grid, kAThreads, smem, st>>>(d, a, f);
+        return;
+    }
     const size_t smem = fused_smem_bytes(d.nr, f.bj);
     if (exact) k_pass_a<true><<<blocks, kAThreads, smem, st>>>(d, a, f);
     else k_pass_a<false><<<blocks, kAThreads, smem, st>>>(d, a, f);

@@ -73,6 +73,7 @@ struct maspcg_ctx {
     int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
     // fused two-pass path geometry (fused.cu)
     int fused_bj = 1, fused_njt = 1, fused_blocks = 1;
+    int tma_ok = 0, tma_njt = 1, tma_nch = 1, tma_hmax = 1, use_tma = 1;
     cudaEvent_t ev_a = nullptr, ev_ph = nullptr;
     maspcg_stats stats{};
     std::vector<cudaEvent_t> tev;   // timing events [3 kernels][2][chunk]
@@ -201,7 +202,9 @@ maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaSt
 
 bool use_fused(const maspcg_ctx *c) { return c->path_opt != 1 && c->fused_bj > 0; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
-int graph_key(const maspcg_ctx *c) { return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0); }
+int graph_key(const maspcg_ctx *c) {
+    return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0);
+}
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
 // order with the same error-free arithmetic (identical bits on every rank).
@@ -285,9 +288,18 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
         f.d_lo = c->a.dh, f.d_hi = c->a.dh + pl;
         f.p_lo = c->a.ph, f.p_hi = c->a.ph + pl;
     }
-    f.bj = c->fused_bj;
-    f.n_jt = c->fused_njt;
     f.div_r = c->d.div_r;
+    if (c->tma_ok && c->use_tma && ((uintptr_t)x & 15) == 0) {   // bulk copies need 16-byte aligned x
+        f.tma = 1;
+        f.bj = c->tma_hmax;
+        f.n_jt = c->tma_njt;
+        f.nch = c->tma_nch;
+    } else {
+        f.tma = 0;
+        f.bj = c->fused_bj;
+        f.n_jt = c->fused_njt;
+        f.nch = 1;
+    }
     if (c->nranks > 1 && slot > 0) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // p_old halo of slot-1
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 0, slot, c->chunk)], st));
     launch_pass_a(c->d, c->a, f, c->fused_blocks, exact_arith(c), st);
@@ -559,6 +571,7 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
         c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
         c->fused_blocks = fused_blocks(nr, nt, c->nloc, c->fused_bj, cuda_device);
     }
+    c->tma_ok = fused_tma_geometry(nr, nt, c->nloc, cuda_device, &c->tma_njt, &c->tma_nch, &c->tma_hmax) ? 1 : 0;
     *out = c;
     return MASPCG_OK;
 }
@@ -872,6 +885,9 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             break;
         case MASPCG_OPT_USE_GRAPHS: c->use_graphs = v ? 1 : 0; break;
         case MASPCG_OPT_TIMING: c->timing = v ? 1 : 0; break;
+        case MASPCG_OPT_TMA:
+            c->use_tma = v ? 1 : 0;
+            break;
         case MASPCG_OPT_ARITH:
             if (v < 0 || v > 1) SET_ERR(c, MASPCG_E_INVALID, "arith must be 0 (oracle-exact) or 1 (fast)");
             c->arith = (int)v;

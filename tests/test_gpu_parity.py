@@ -170,6 +170,18 @@ def test_solve_parity_warm_start(torch_cuda, M, oracle_mod, path):
     assert_solve_parity(gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: path}), o)
 
 
+@pytest.mark.parametrize("shape", [(16, 16, 32), (40, 3, 2), (64, 32, 8), (12, 20, 9), (150, 30, 12)])
+def test_fused_tma_and_register_variants_identical(torch_cuda, M, oracle_mod, shape):
+    """Pass A staged by TMA bulk copies (nr even) and the register-batched pass A give the oracle's
+    iterates bit for bit."""
+    nr, nt, np_ = shape
+    p = inputs.random_problem(nr, nt, np_, 300 + nr, bc_in=0, bc_out=1)
+    o = oracle_mod.solve_problem(p)
+    for tma in (1, 0):
+        g = gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: M.PATH_FUSED, M.OPT_TMA: tma})
+        assert_solve_parity(g, o)
+
+
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("chunk,graphs,timing", [(1, 1, 0), (3, 1, 0), (16, 0, 0), (64, 1, 0), (7, 1, 1)])
 def test_solve_loop_modes_identical(torch_cuda, M, oracle_mod, chunk, graphs, timing, path):
