@@ -181,6 +181,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=8)
     ap.add_argument("--path", type=int, default=0, help="0 auto (fused), 1 three kernels, 2 fused")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
+    ap.add_argument("--tma", type=int, default=1, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
     args = ap.parse_args()
     if args.warmup < 3 and args.maxit is None:
         args.warmup = 3
@@ -215,6 +216,7 @@ def main():
     S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk)
     S.set_option(maspcg.OPT_PATH, args.path)
     S.set_option(maspcg.OPT_ARITH, args.arith)
+    S.set_option(maspcg.OPT_TMA, args.tma)
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
 

@@ -39,6 +39,7 @@ namespace {
 
 constexpr int kAThreads = 512;   // one persistent block per SM (smem-bound)
 constexpr int kAM = 8;           // tile cells per thread per plane (register batches)
+constexpr int kAMT = 3;          // same for the TMA variant (tiles of <= 3 x 512 cells)
 
 // plane pointer of array `base` for local plane k in [-1, nloc] (halo pointers at the ends)
 __device__ __forceinline__ const double *plane_ptr(const double *base, const double *lo, const double *hi, int k,
@@ -372,9 +373,9 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
     }
 
     Acc<EXACT> dot[1];
-    double tp_carry[kAM];
+    double tp_carry[kAMT];
     const int ext_n = (h + 2) * nr, own_n = h * nr;
-    const bool carry_ok = own_n <= kAM * kAThreads;   // one register batch: T_phi carried across planes
+    const bool carry_ok = own_n <= kAMT * kAThreads;   // one register batch: T_phi carried across planes
     const int nsteps = kb - ka + 3;   // planes ka-1 .. kb+1
     for (int kk = 0; kk < nsteps; ++kk) {
         const int k = ka - 1 + kk;
@@ -408,10 +409,10 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
             const double *sp = slot;                                     // plane ks+1
             const double *dk = stage((kk + 2) % 3).D;                    // D of plane ks (ext rows)
             const size_t pbase = (size_t)ks * plane + (size_t)j0 * nr;
-            for (int o0 = 0; o0 < own_n; o0 += kAM * kAThreads) {
-                double tr0[kAM], tr1[kAM], tt0[kAM], tt1[kAM], tph[kAM];
+            for (int o0 = 0; o0 < own_n; o0 += kAMT * kAThreads) {
+                double tr0[kAMT], tr1[kAMT], tt0[kAMT], tt1[kAMT], tph[kAMT];
 #pragma unroll
-                for (int m = 0; m < kAM; ++m) {
+                for (int m = 0; m < kAMT; ++m) {
                     const int o = o0 + tid + m * kAThreads;
                     tr0[m] = tr1[m] = tt0[m] = tt1[m] = tph[m] = 0.0;
                     if (o < own_n) {
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
                     }
                 }
 #pragma unroll
-                for (int m = 0; m < kAM; ++m) {
+                for (int m = 0; m < kAMT; ++m) {
                     const int o = o0 + tid + m * kAThreads;
                     if (o < own_n) {
                         const int jj = (int)f.div_r.div((uint32_t)o);
@@ -547,8 +548,10 @@ bool fused_tma_geometry(int nr, int nt, int nloc, int device, int *njt, int *nch
         const int h = (nt + t - 1) / t;
         if (tma_smem_bytes(nr, h) > limit) continue;
         const double util = (double)t * c / sms;
-        // prefer full occupancy of the SMs, then taller tiles (fewer recomputed halo rows)
-        const double score = (util >= 0.97 ? 1.0 : util) * 1000.0 + h;
+        // prefer full occupancy of the SMs, tiles of one register batch per thread (T_phi carried),
+        // then taller tiles (fewer recomputed halo rows)
+        const bool one_batch = (long long)h * nr <= (long long)kAMT * kAThreads;
+        const double score = (util >= 0.97 ? 1.0 : util) * 1000.0 + (one_batch ? 100.0 : 0.0) + h;
         if (score > best) {
             best = score;
             *njt = t;
