@@ -39,7 +39,8 @@ namespace {
 
 constexpr int kAThreads = 512;   // one persistent block per SM (smem-bound)
 constexpr int kAM = 8;           // tile cells per thread per plane (register batches)
-constexpr int kAMT = 3;          // same for the TMA variant (tiles of <= 3 x 512 cells)
+constexpr int kTThreads = 1024;  // TMA variant: 32 warps per SM (no register staging of r, D, p, x)
+constexpr int kAMT = 2;          // TMA variant: tile cells per thread per plane (tiles of <= 2 x 1024 cells)
 
 // plane pointer of array `base` for local plane k in [-1, nloc] (halo pointers at the ends)
 __device__ __forceinline__ const double *plane_ptr(const double *base, const double *lo, const double *hi, int k,
@@ -312,7 +313,7 @@ struct TmaStage {
 }  // namespace
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a, FusedArgs f) {
+__global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a, FusedArgs f) {
     using A = Ar<EXACT>;
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) uint64_t bars[3];
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
     Acc<EXACT> dot[1];
     double tp_carry[kAMT];
     const int ext_n = (h + 2) * nr, own_n = h * nr;
-    const bool carry_ok = own_n <= kAMT * kAThreads;   // one register batch: T_phi carried across planes
+    const bool carry_ok = own_n <= kAMT * kTThreads;   // one register batch: T_phi carried across planes
     const int nsteps = kb - ka + 3;   // planes ka-1 .. kb+1
     for (int kk = 0; kk < nsteps; ++kk) {
         const int k = ka - 1 + kk;
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
         const bool own_plane = k >= ka && k <= kb;
         double *slot = ring + (size_t)q * sext;
         const TmaStage S1 = stage(q);
-        for (int e = tid; e < ext_n; e += kAThreads) {
+        for (int e = tid; e < ext_n; e += kTThreads) {
             const int re = (int)f.div_r.div((uint32_t)e);
             const int j = j0 - 1 + re;
             if (j < 0 || j >= nt) continue;
@@ -409,11 +410,11 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
             const double *sp = slot;                                     // plane ks+1
             const double *dk = stage((kk + 2) % 3).D;                    // D of plane ks (ext rows)
             const size_t pbase = (size_t)ks * plane + (size_t)j0 * nr;
-            for (int o0 = 0; o0 < own_n; o0 += kAMT * kAThreads) {
+            for (int o0 = 0; o0 < own_n; o0 += kAMT * kTThreads) {
                 double tr0[kAMT], tr1[kAMT], tt0[kAMT], tt1[kAMT], tph[kAMT];
 #pragma unroll
                 for (int m = 0; m < kAMT; ++m) {
-                    const int o = o0 + tid + m * kAThreads;
+                    const int o = o0 + tid + m * kTThreads;
                     tr0[m] = tr1[m] = tt0[m] = tt1[m] = tph[m] = 0.0;
                     if (o < own_n) {
                         const int jj = (int)f.div_r.div((uint32_t)o);
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
                 }
 #pragma unroll
                 for (int m = 0; m < kAMT; ++m) {
-                    const int o = o0 + tid + m * kAThreads;
+                    const int o = o0 + tid + m * kTThreads;
                     if (o < own_n) {
                         const int jj = (int)f.div_r.div((uint32_t)o);
                         const int i = o - jj * nr;
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a_tma(Dims d, DevArrays a
             issue(k + 2, (kk + 2) % 3);
         }
     }
-    pass_a_epilogue<EXACT, kAThreads>(a, S, dot);
+    pass_a_epilogue<EXACT, kTThreads>(a, S, dot);
 }
 
 // ------------------------------------------------------------------------ pass B
@@ -550,7 +551,7 @@ bool fused_tma_geometry(int nr, int nt, int nloc, int device, int *njt, int *nch
         const double util = (double)t * c / sms;
         // prefer full occupancy of the SMs, tiles of one register batch per thread (T_phi carried),
         // then taller tiles (fewer recomputed halo rows)
-        const bool one_batch = (long long)h * nr <= (long long)kAMT * kAThreads;
+        const bool one_batch = (long long)h * nr <= (long long)kAMT * kTThreads;
         const double score = (util >= 0.97 ? 1.0 : util) * 1000.0 + (one_batch ? 100.0 : 0.0) + h;
         if (score > best) {
             best = score;
@@ -570,8 +571,8 @@ void launch_pass_a(const Dims &d, const DevArrays &a, const FusedArgs &f, int bl
     if (f.tma) {
         const size_t smem = tma_smem_bytes(d.nr, f.bj);
         const int grid = f.n_jt * f.nch;
-        if (exact) k_pass_a_tma<true><<<grid, kAThreads, smem, st>>>(d, a, f);
-        else k_pass_a_tma<false><<<grid, kAThreads, smem, st>>>(d, a, f);
+        if (exact) k_pass_a_tma<true><<<grid, kTThreads, smem, st>>>(d, a, f);
+        else k_pass_a_tma<false><<<grid, kTThreads, smem, st>>>(d, a, f);
         return;
     }
     const size_t smem = fused_smem_bytes(d.nr, f.bj);

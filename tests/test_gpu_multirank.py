@@ -94,7 +94,8 @@ def test_multirank_solve_matches_oracle(M, oracle_mod, name, P, fn, path):
     o = oracle_mod.solve_problem(full)
     res = run_ranks(M, P, lambda r, g: solve_rank(M, slab_of(fn, P, r), r, g, path=path))
     # every rank agrees bit for bit on the scalars of the solve
-    assert all(r[0] >= 0 for r in res), [r[1] for r in res]
+    errs = [(r[0], r[1].get("error")) for r in res]
+    assert all(r[0] >= 0 for r in res), f"rank errors: {errs}"
     for st, info, hist, _, _ in res[1:]:
         assert st == res[0][0] and info == res[0][1] and np.array_equal(hist, res[0][2])
     st, info, hist = res[0][:3]
