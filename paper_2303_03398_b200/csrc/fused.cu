@@ -39,8 +39,7 @@ namespace {
 
 constexpr int kAThreads = 512;   // one persistent block per SM (smem-bound)
 constexpr int kAM = 8;           // tile cells per thread per plane (register batches)
-constexpr int kTThreads = 1024;  // TMA variant: 32 warps per SM (no register staging of r, D, p, x)
-constexpr int kAMT = 2;          // TMA variant: tile cells per thread per plane (tiles of <= 2 x 1024 cells)
+constexpr int kTThreads = 512;   // TMA variant: all inputs staged in shared memory, 16 warps per SM
 
 // plane pointer of array `base` for local plane k in [-1, nloc] (halo pointers at the ends)
 __device__ __forceinline__ const double *plane_ptr(const double *base, const double *lo, const double *hi, int k,
@@ -270,12 +269,13 @@ __global__ void __launch_bounds__(kAThreads, 1) k_pass_a(Dims d, DevArrays a, Fu
 // ------------------------------------------------------------------------ pass A, TMA variant
 // Same arithmetic as k_pass_a.  The grid is a lockstep tiling: block b owns j-tile b % njt (rows
 // [jt*nt/njt, (jt+1)*nt/njt)) over the plane chunk b / njt, so blocks on neighbouring tiles march
-// through the same planes at the same time and the halo rows they both read are L2 hits.  The
-// streams that phase 1 needs -- r, D, p_old on the tile rows plus one halo row each side, and x on
-// the tile rows -- are staged by the Tensor Memory Accelerator (cp.async.bulk, one 1-D bulk copy per
-// array and plane, completion on an mbarrier) into a 3-stage shared ring, two planes ahead of the
-// compute, so ~60 KB per SM are always in flight without holding registers.  T_r, T_theta, T_phi
-// are read once per cell in phase 2 with batched loads.  Requires nr even (16-byte row alignment).
+// through the same planes at the same time and the halo rows both read are L2 hits.  EVERY input
+// of a plane is staged by the Tensor Memory Accelerator -- one 1-D bulk copy (cp.async.bulk, i.e.
+// UBLKCP) per array and plane, completion counted on an mbarrier -- into a 3-stage shared ring
+// two planes ahead of the compute: r, D, p_old on the tile rows plus one halo row each side, x,
+// T_r, both T_phi faces on the tile rows, T_theta on the tile rows plus the row above.  No warp
+// ever waits on a global load; global memory sees only the bulk copies and the streaming stores
+// of p_new, x and q.  Requires nr even (16-byte aligned rows).
 namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -306,11 +306,31 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// one stage = all inputs of one plane of the tile (doubles; sext = (H+2) nr, sown = H nr, H = tallest tile)
 struct TmaStage {
-    double *r, *D, *P, *X;   // r, D, p_old: ext rows (row 0 = tile row j0-1); X: tile rows
+    double *r, *D, *P;           // ext rows: row 0 = tile row j0 - 1
+    double *X, *Tr, *Tplo, *Tphi; // tile rows
+    double *Tt;                   // tile rows + the row above
 };
+__device__ __forceinline__ TmaStage tma_stage(double *base, int sext, int sown) {
+    TmaStage t;
+    t.r = base;
+    t.D = base + sext;
+    t.P = base + 2 * sext;
+    t.X = base + 3 * sext;
+    t.Tr = t.X + sown;
+    t.Tplo = t.Tr + sown;
+    t.Tphi = t.Tplo + sown;
+    t.Tt = t.Tphi + sown;
+    return t;
+}
 
 }  // namespace
+
+__host__ __device__ size_t tma_stage_doubles(int nr, int hmax) { return (size_t)nr * (3 * (hmax + 2) + 4 * hmax + hmax + 1); }
+size_t tma_smem_bytes(int nr, int hmax) {
+    return 8 * (3 * tma_stage_doubles(nr, hmax) + (size_t)3 * (hmax + 2) * nr);
+}
 
 template <bool EXACT>
 __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a, FusedArgs f) {
@@ -332,14 +352,9 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a
     const int j0 = (int)(((long long)jt * nt) / njt), j1 = (int)(((long long)(jt + 1) * nt) / njt);
     const int ka = (int)(((long long)ch * nloc) / f.nch), kb = (int)(((long long)(ch + 1) * nloc) / f.nch) - 1;
     const int h = j1 - j0;
-    const int sext = (f.bj + 2) * nr, sown = f.bj * nr;   // f.bj = max tile rows
-    const size_t stage_sz = (size_t)3 * sext + sown;
-    // stage q: r | D | p_old on the ext rows, x on the tile rows
-    auto stage = [&](int q) -> TmaStage {
-        double *b = smem + (size_t)q * stage_sz;
-        return {b, b + sext, b + 2 * sext, b + 3 * sext};
-    };
-    double *ring = smem + (size_t)3 * (3 * sext + sown);   // [3][sext] p_new
+    const int sext = (f.bj + 2) * nr, sown = f.bj * nr;   // f.bj = tallest tile
+    const size_t stage_sz = tma_stage_doubles(nr, f.bj);
+    double *ring = smem + 3 * stage_sz;                     // [3][sext] p_new
     const int tid = threadIdx.x;
     uint32_t parity[3] = {0u, 0u, 0u};
     if (tid == 0) {
@@ -349,24 +364,35 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a
     __syncthreads();
 
     const int jr0 = max(j0 - 1, 0), jr1 = min(j1 + 1, nt);   // ext rows present in the grid
-    const int roff = jr0 - (j0 - 1);                         // 0, or 1 at the lower pole tile
-    // issue the bulk copies of plane k into stage q (thread 0)
+    const int roff = jr0 - (j0 - 1);                         // 0, or 1 on the tile at the lower pole
+    const int ttrows = min(h + 1, nt - j0);                  // T_theta: tile rows + the row above
+    // thread 0: bulk copies of every input of plane k into stage q
     auto issue = [&](int k, int q) {
+        const TmaStage sq = tma_stage(smem + (size_t)q * stage_sz, sext, sown);
         const bool own_plane = k >= ka && k <= kb;
         const double *rp = plane_ptr(f.r, f.r_lo, f.r_hi, k, nloc, plane);
         const double *dp = plane_ptr(a.D, f.d_lo, f.d_hi, k, nloc, plane);
         const double *pp = plane_ptr(f.p_old, f.p_lo, f.p_hi, k, nloc, plane);
         const uint32_t eb = (uint32_t)(8 * (size_t)(jr1 - jr0) * nr);
         const uint32_t ob = (uint32_t)(8 * (size_t)h * nr);
+        const uint32_t tb = (uint32_t)(8 * (size_t)ttrows * nr);
         const bool wx = own_plane && !first;
-        const uint32_t bytes = eb * (first ? 2u : 3u) + (wx ? ob : 0u);
+        uint32_t bytes = eb * (first ? 2u : 3u);
+        if (wx) bytes += ob;
+        if (own_plane) bytes += 3u * ob + tb;
         mbar_expect_tx(&bars[q], bytes);
         const size_t e0 = (size_t)jr0 * nr;
-        const TmaStage sq = stage(q);
         bulk_g2s(sq.r + (size_t)roff * nr, rp + e0, eb, &bars[q]);
         bulk_g2s(sq.D + (size_t)roff * nr, dp + e0, eb, &bars[q]);
         if (!first) bulk_g2s(sq.P + (size_t)roff * nr, pp + e0, eb, &bars[q]);
-        if (wx) bulk_g2s(sq.X, x + (size_t)k * plane + (size_t)j0 * nr, ob, &bars[q]);
+        if (own_plane) {
+            const size_t c0 = (size_t)k * plane + (size_t)j0 * nr;
+            if (wx) bulk_g2s(sq.X, x + c0, ob, &bars[q]);
+            bulk_g2s(sq.Tr, a.Tr + c0, ob, &bars[q]);
+            bulk_g2s(sq.Tplo, a.Tp + c0, ob, &bars[q]);
+            bulk_g2s(sq.Tphi, a.Tp + c0 + plane, ob, &bars[q]);
+            bulk_g2s(sq.Tt, a.Tt + c0, tb, &bars[q]);
+        }
     };
     if (tid == 0) {
         issue(ka - 1, 0);
@@ -374,19 +400,17 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a
     }
 
     Acc<EXACT> dot[1];
-    double tp_carry[kAMT];
     const int ext_n = (h + 2) * nr, own_n = h * nr;
-    const bool carry_ok = own_n <= kAMT * kTThreads;   // one register batch: T_phi carried across planes
     const int nsteps = kb - ka + 3;   // planes ka-1 .. kb+1
     for (int kk = 0; kk < nsteps; ++kk) {
         const int k = ka - 1 + kk;
         const int q = kk % 3;
         mbar_wait(&bars[q], parity[q]);
         parity[q] ^= 1u;
-        // ---- phase 1: p_new of plane k on the ext rows (from shared memory only)
+        // ---- phase 1: p_new of plane k on the ext rows (shared memory only)
         const bool own_plane = k >= ka && k <= kb;
         double *slot = ring + (size_t)q * sext;
-        const TmaStage S1 = stage(q);
+        const TmaStage S1 = tma_stage(smem + (size_t)q * stage_sz, sext, sown);
         for (int e = tid; e < ext_n; e += kTThreads) {
             const int re = (int)f.div_r.div((uint32_t)e);
             const int j = j0 - 1 + re;
@@ -396,64 +420,40 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a
             const double pn = first ? z : A::axpy(beta, po, z);
             slot[e] = pn;
             if (own_plane && re >= 1 && re <= h) {
-                const size_t gc = (size_t)k * plane + (size_t)j * nr + (e - re * nr);
+                const size_t gc = (size_t)k * plane + (size_t)(j0 - 1) * nr + e;
                 f.p_new[gc] = pn;
                 if (!first) x[gc] = A::axpy(alpha, po, S1.X[e - nr]);
             }
         }
         __syncthreads();
-        // ---- phase 2: stencil of plane ks = k-1
+        // ---- phase 2: stencil of plane ks = k-1 (its stage is (kk-1) % 3, shared memory only)
         const int ks = k - 1;
         if (ks >= ka) {
-            const double *sm_ = ring + (size_t)((kk + 1) % 3) * sext;   // plane ks-1 (slot (kk-2)%3)
-            const double *s0 = ring + (size_t)((kk + 2) % 3) * sext;    // plane ks   (slot (kk-1)%3)
+            const double *sm_ = ring + (size_t)((kk + 1) % 3) * sext;   // plane ks-1
+            const double *s0 = ring + (size_t)((kk + 2) % 3) * sext;    // plane ks
             const double *sp = slot;                                     // plane ks+1
-            const double *dk = stage((kk + 2) % 3).D;                    // D of plane ks (ext rows)
+            const TmaStage S2 = tma_stage(smem + (size_t)((kk + 2) % 3) * stage_sz, sext, sown);
             const size_t pbase = (size_t)ks * plane + (size_t)j0 * nr;
-            for (int o0 = 0; o0 < own_n; o0 += kAMT * kTThreads) {
-                double tr0[kAMT], tr1[kAMT], tt0[kAMT], tt1[kAMT], tph[kAMT];
-#pragma unroll
-                for (int m = 0; m < kAMT; ++m) {
-                    const int o = o0 + tid + m * kTThreads;
-                    tr0[m] = tr1[m] = tt0[m] = tt1[m] = tph[m] = 0.0;
-                    if (o < own_n) {
-                        const int jj = (int)f.div_r.div((uint32_t)o);
-                        const int i = o - jj * nr;
-                        const size_t c = pbase + o;
-                        tr0[m] = __ldg(a.Tr + c);
-                        if (i < nr - 1) tr1[m] = __ldg(a.Tr + c + 1);
-                        tt0[m] = __ldg(a.Tt + c);
-                        if (j0 + jj < nt - 1) tt1[m] = __ldg(a.Tt + c + nr);
-                        tph[m] = __ldg(a.Tp + c + plane);
-                        if (ks == ka || !carry_ok) tp_carry[m] = __ldg(a.Tp + c);
-                    }
-                }
-#pragma unroll
-                for (int m = 0; m < kAMT; ++m) {
-                    const int o = o0 + tid + m * kTThreads;
-                    if (o < own_n) {
-                        const int jj = (int)f.div_r.div((uint32_t)o);
-                        const int i = o - jj * nr;
-                        const int j = j0 + jj;
-                        const int l = nr + o;
-                        const double pc = s0[l];
-                        double s = 0.0;
-                        if (i > 0) s = A::acc(s, tr0[m], s0[l - 1]);
-                        if (i < nr - 1) s = A::acc(s, tr1[m], s0[l + 1]);
-                        if (j > 0) s = A::acc(s, tt0[m], s0[l - nr]);
-                        if (j < nt - 1) s = A::acc(s, tt1[m], s0[l + nr]);
-                        s = A::acc(s, tp_carry[m], sm_[l]);
-                        s = A::acc(s, tph[m], sp[l]);
-                        const double qv = A::diag_minus(dk[l], pc, s);
-                        a.q[pbase + o] = qv;
-                        dot[0].add(pc, qv);
-                        tp_carry[m] = tph[m];
-                    }
-                }
+            for (int o = tid; o < own_n; o += kTThreads) {
+                const int jj = (int)f.div_r.div((uint32_t)o);
+                const int i = o - jj * nr;
+                const int j = j0 + jj;
+                const int l = nr + o;
+                const double pc = s0[l];
+                double s = 0.0;
+                if (i > 0) s = A::acc(s, S2.Tr[o], s0[l - 1]);
+                if (i < nr - 1) s = A::acc(s, S2.Tr[o + 1], s0[l + 1]);
+                if (j > 0) s = A::acc(s, S2.Tt[o], s0[l - nr]);
+                if (j < nt - 1) s = A::acc(s, S2.Tt[o + nr], s0[l + nr]);
+                s = A::acc(s, S2.Tplo[o], sm_[l]);
+                s = A::acc(s, S2.Tphi[o], sp[l]);
+                const double qv = A::diag_minus(S2.D[l], pc, s);
+                a.q[pbase + o] = qv;
+                dot[0].add(pc, qv);
             }
         }
         __syncthreads();
-        // ---- refill the stage of plane k-1 (consumed) with plane k+2
+        // ---- refill the stage of plane k-1 (fully consumed) with plane k+2
         if (tid == 0 && kk + 2 < nsteps) {
             fence_proxy_async();
             issue(k + 2, (kk + 2) % 3);
@@ -535,11 +535,10 @@ int fused_blocks(int nr, int nt, int nloc, int bj, int device) {
     return (int)b;
 }
 
-size_t tma_smem_bytes(int nr, int hmax) { return (size_t)8 * nr * (15 * (size_t)hmax + 24); }
 
 bool fused_tma_geometry(int nr, int nt, int nloc, int device, int *njt, int *nch, int *hmax) {
     if (nr % 2 != 0) return false;                          // 16-byte aligned rows for the bulk copies
-    const size_t limit = 220 * 1024;
+    const size_t limit = 224 * 1024;
     const int sms = sm_count(device);
     double best = -1.0;
     for (int c = 1; c <= nloc && c <= sms; ++c) {
@@ -549,10 +548,8 @@ bool fused_tma_geometry(int nr, int nt, int nloc, int device, int *njt, int *nch
         const int h = (nt + t - 1) / t;
         if (tma_smem_bytes(nr, h) > limit) continue;
         const double util = (double)t * c / sms;
-        // prefer full occupancy of the SMs, tiles of one register batch per thread (T_phi carried),
-        // then taller tiles (fewer recomputed halo rows)
-        const bool one_batch = (long long)h * nr <= (long long)kAMT * kTThreads;
-        const double score = (util >= 0.97 ? 1.0 : util) * 1000.0 + (one_batch ? 100.0 : 0.0) + h;
+        // prefer full occupancy of the SMs, then taller tiles (fewer recomputed halo rows)
+        const double score = (util >= 0.97 ? 1.0 : util) * 1000.0 + h;
         if (score > best) {
             best = score;
             *njt = t;
