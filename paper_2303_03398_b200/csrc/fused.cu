@@ -366,13 +366,18 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a
     const int jr0 = max(j0 - 1, 0), jr1 = min(j1 + 1, nt);   // ext rows present in the grid
     const int roff = jr0 - (j0 - 1);                         // 0, or 1 on the tile at the lower pole
     const int ttrows = min(h + 1, nt - j0);                  // T_theta: tile rows + the row above
-    // thread 0: bulk copies of every input of plane k into stage q
-    auto issue = [&](int k, int q) {
+    // thread 0: bulk copies of every input of plane k into stage q (kernel-parameter pointers are
+    // copied to registers first: no reference to the parameter space inside the helper)
+    const double *const gTr = a.Tr, *const gTt = a.Tt, *const gTp = a.Tp, *const gD = a.D;
+    const double *const fr = f.r, *const frlo = f.r_lo, *const frhi = f.r_hi;
+    const double *const fdlo = f.d_lo, *const fdhi = f.d_hi;
+    const double *const fp = f.p_old, *const fplo = f.p_lo, *const fphi = f.p_hi;
+    auto issue = [=](int k, int q) {
         const TmaStage sq = tma_stage(smem + (size_t)q * stage_sz, sext, sown);
         const bool own_plane = k >= ka && k <= kb;
-        const double *rp = plane_ptr(f.r, f.r_lo, f.r_hi, k, nloc, plane);
-        const double *dp = plane_ptr(a.D, f.d_lo, f.d_hi, k, nloc, plane);
-        const double *pp = plane_ptr(f.p_old, f.p_lo, f.p_hi, k, nloc, plane);
+        const double *rp = plane_ptr(fr, frlo, frhi, k, nloc, plane);
+        const double *dp = plane_ptr(gD, fdlo, fdhi, k, nloc, plane);
+        const double *pp = plane_ptr(fp, fplo, fphi, k, nloc, plane);
         const uint32_t eb = (uint32_t)(8 * (size_t)(jr1 - jr0) * nr);
         const uint32_t ob = (uint32_t)(8 * (size_t)h * nr);
         const uint32_t tb = (uint32_t)(8 * (size_t)ttrows * nr);
@@ -380,18 +385,19 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a
         uint32_t bytes = eb * (first ? 2u : 3u);
         if (wx) bytes += ob;
         if (own_plane) bytes += 3u * ob + tb;
-        mbar_expect_tx(&bars[q], bytes);
+        uint64_t *bar = &bars[q];
+        mbar_expect_tx(bar, bytes);
         const size_t e0 = (size_t)jr0 * nr;
-        bulk_g2s(sq.r + (size_t)roff * nr, rp + e0, eb, &bars[q]);
-        bulk_g2s(sq.D + (size_t)roff * nr, dp + e0, eb, &bars[q]);
-        if (!first) bulk_g2s(sq.P + (size_t)roff * nr, pp + e0, eb, &bars[q]);
+        bulk_g2s(sq.r + (size_t)roff * nr, rp + e0, eb, bar);
+        bulk_g2s(sq.D + (size_t)roff * nr, dp + e0, eb, bar);
+        if (!first) bulk_g2s(sq.P + (size_t)roff * nr, pp + e0, eb, bar);
         if (own_plane) {
             const size_t c0 = (size_t)k * plane + (size_t)j0 * nr;
-            if (wx) bulk_g2s(sq.X, x + c0, ob, &bars[q]);
-            bulk_g2s(sq.Tr, a.Tr + c0, ob, &bars[q]);
-            bulk_g2s(sq.Tplo, a.Tp + c0, ob, &bars[q]);
-            bulk_g2s(sq.Tphi, a.Tp + c0 + plane, ob, &bars[q]);
-            bulk_g2s(sq.Tt, a.Tt + c0, tb, &bars[q]);
+            if (wx) bulk_g2s(sq.X, x + c0, ob, bar);
+            bulk_g2s(sq.Tr, gTr + c0, ob, bar);
+            bulk_g2s(sq.Tplo, gTp + c0, ob, bar);
+            bulk_g2s(sq.Tphi, gTp + c0 + plane, ob, bar);
+            bulk_g2s(sq.Tt, gTt + c0, tb, bar);
         }
     };
     if (tid == 0) {
