@@ -305,6 +305,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// p + off (elements) as one explicit 64-bit add.  ptxas 12.9 lowered `(base + c0) + plane` feeding a
+// bulk-copy source operand to a 32-bit uniform LEA (dropping the high word of the address); forming
+// every bulk-copy source address here keeps it 64-bit.
+__device__ __forceinline__ const double *gaddr(const double *p, size_t off) {
+    const double *r;
+    asm("add.s64 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(off * sizeof(double)));
+    return r;
+}
 
 // one stage = all inputs of one plane of the tile (doubles; sext = (H+2) nr, sown = H nr, H = tallest tile)
 struct TmaStage {
@@ -388,16 +396,16 @@ __global__ void __launch_bounds__(kTThreads, 1) k_pass_a_tma(Dims d, DevArrays a
         uint64_t *bar = &bars[q];
         mbar_expect_tx(bar, bytes);
         const size_t e0 = (size_t)jr0 * nr;
-        bulk_g2s(sq.r + (size_t)roff * nr, rp + e0, eb, bar);
-        bulk_g2s(sq.D + (size_t)roff * nr, dp + e0, eb, bar);
-        if (!first) bulk_g2s(sq.P + (size_t)roff * nr, pp + e0, eb, bar);
+        bulk_g2s(sq.r + (size_t)roff * nr, gaddr(rp, e0), eb, bar);
+        bulk_g2s(sq.D + (size_t)roff * nr, gaddr(dp, e0), eb, bar);
+        if (!first) bulk_g2s(sq.P + (size_t)roff * nr, gaddr(pp, e0), eb, bar);
         if (own_plane) {
             const size_t c0 = (size_t)k * plane + (size_t)j0 * nr;
-            if (wx) bulk_g2s(sq.X, x + c0, ob, bar);
-            bulk_g2s(sq.Tr, gTr + c0, ob, bar);
-            bulk_g2s(sq.Tplo, gTp + c0, ob, bar);
-            bulk_g2s(sq.Tphi, gTp + c0 + plane, ob, bar);
-            bulk_g2s(sq.Tt, gTt + c0, tb, bar);
+            if (wx) bulk_g2s(sq.X, gaddr(x, c0), ob, bar);
+            bulk_g2s(sq.Tr, gaddr(gTr, c0), ob, bar);
+            bulk_g2s(sq.Tplo, gaddr(gTp, c0), ob, bar);
+            bulk_g2s(sq.Tphi, gaddr(gTp, c0 + plane), ob, bar);
+            bulk_g2s(sq.Tt, gaddr(gTt, c0), tb, bar);
         }
     };
     if (tid == 0) {
