@@ -35,7 +35,7 @@ UNIT = "PCG iterations/s"
 # algorithmic bytes per cell of each kernel
 PATHS = {
     1: {"name": "three kernels", "stencil": ("stencil_matvec_dot (k_matvec_flat)", 48),
-        "update": ("update_jacobi_dots (k_update)", 56), "pupdate": ("p_update (k_pupdate)", 32), "iter": 136},
+        "update": ("update_jacobi_dots (k_update)", 32), "pupdate": ("x_and_p_update (k_pupdate)", 48), "iter": 128},
     2: {"name": "fused two passes", "stencil": ("pass A: p-update + x-update + stencil + p.q (k_pass_a)", 80),
         "update": ("pass B: r-update + Jacobi + r.z, r.r (k_pass_b)", 32), "pupdate": None, "iter": 112},
 }

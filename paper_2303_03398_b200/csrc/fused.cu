@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kAThreads = 512;   // one persistent block per SM (smem-bound)
 constexpr int kAM = 8;           // tile cells per thread per plane (register batches)
-constexpr int kTThreads = 512;   // TMA variant: all inputs staged in shared memory, 16 warps per SM
+constexpr int kTThreads = 1024;  // TMA variant: all inputs staged in shared memory, 32 warps per SM
 
 // plane pointer of array `base` for local plane k in [-1, nloc] (halo pointers at the ends)
 __device__ __forceinline__ const double *plane_ptr(const double *base, const double *lo, const double *hi, int k,

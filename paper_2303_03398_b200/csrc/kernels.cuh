@@ -26,8 +26,8 @@ void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart par
 void launch_setup_residual(const Dims &d, const DevArrays &a, const double *f, int din, int dout, bool exact,
                            cudaStream_t st);
 void launch_setup_scalars(const DevArrays &a, double tol, int maxit, cudaStream_t st);
-void launch_update(const Dims &d, const DevArrays &a, double *x, bool exact, cudaStream_t st);
-void launch_pupdate(const Dims &d, const DevArrays &a, int chunk, bool exact, cudaStream_t st);
+void launch_update(const Dims &d, const DevArrays &a, bool exact, cudaStream_t st);
+void launch_pupdate(const Dims &d, const DevArrays &a, double *x, int chunk, bool exact, cudaStream_t st);
 // out[2t..2t+1] = rank-ordered Dot2 combination of gather[r][2t..2t+1], t < npairs.
 void launch_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact, cudaStream_t st);
 void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st);

@@ -258,11 +258,11 @@ maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int i
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 1, it, c->chunk)], st));
     RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st));
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 0, it, c->chunk)], st));
-    launch_update(c->d, c->a, x, exact_arith(c), st);
+    launch_update(c->d, c->a, exact_arith(c), st);
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 1, it, c->chunk)], st));
     RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st));
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 0, it, c->chunk)], st));
-    launch_pupdate(c->d, c->a, c->chunk, exact_arith(c), st);
+    launch_pupdate(c->d, c->a, x, c->chunk, exact_arith(c), st);
     if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 1, it, c->chunk)], st));
     return MASPCG_OK;
 }
