@@ -179,7 +179,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
-    ap.add_argument("--path", type=int, default=0, help="0 auto (fused), 1 three kernels, 2 fused")
+    ap.add_argument("--path", type=int, default=0, help="0 auto (= 1), 1 three kernels, 2 fused two passes")
+    ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=1, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
     args = ap.parse_args()
@@ -217,6 +218,7 @@ def main():
     S.set_option(maspcg.OPT_PATH, args.path)
     S.set_option(maspcg.OPT_ARITH, args.arith)
     S.set_option(maspcg.OPT_TMA, args.tma)
+    S.set_option(maspcg.OPT_VEC, args.vec)
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
 

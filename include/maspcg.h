@@ -115,11 +115,13 @@ typedef enum {
     MASPCG_OPT_ARITH = 5,        /* 0 (default): oracle-identical arithmetic -- no FMA contraction, Dot2 (compensated)
                                     dot products (R24); 1: FMA updates and plain tree sums (faster in FP64
                                     issue, parity to the tolerance contract only) */
+    MASPCG_OPT_VEC = 7,          /* three-kernel path: 1 (default) two cells per thread with 16-byte loads when nr is
+                                    even; 0: one cell per thread */
     MASPCG_OPT_TMA = 6,          /* fused path: 1 (default) stage pass A's streams with TMA bulk copies when nr is
                                     even; 0: register-batched loads */
-    MASPCG_OPT_PATH = 4          /* iteration path: 0 = auto (default, = 2), 1 = three kernels (stencil+dot, update+dots,
-                                    p-update; 136 B/cell), 2 = fused two passes (p-update and the deferred x update folded
-                                    into a phi-marching tiled stencil + r update; 112 B/cell) */
+    MASPCG_OPT_PATH = 4          /* iteration path: 0 = auto (default, = 1), 1 = three streaming kernels (stencil+p.q,
+                                    r-update+Jacobi+dots, deferred x-update+p-update; 128 B/cell), 2 = fused two passes
+                                    (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell) */
 } maspcg_option;
 
 /* ---- lifetime ----------------------------------------------------------- */

@@ -88,6 +88,7 @@ struct Dims {
     FastDiv div_r;          // / nr
     FastDiv div_t;          // / nt
     int periodic_local;     // 1: single rank, halo planes are written by the kernels
+    int vec_ok;             // 1: the 16-byte vector kernels may be used (MASPCG_OPT_VEC)
 };
 
 // Device pointers into the workspace.

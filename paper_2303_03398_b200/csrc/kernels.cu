@@ -27,6 +27,7 @@ namespace maspcg {
 namespace {
 
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
+constexpr int kVecBlocks = 4;                   // vector kernels: 4 blocks of 256 threads per SM (<= 64 registers)
 
 __device__ __forceinline__ void decompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
     uint32_t row = d.div_r.div(c);
@@ -357,10 +358,211 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArr
     }
 }
 
+
+// ---------------------------------------------------------------- 16-byte vector variants (nr even)
+// Two r-neighbour cells (i, i+1), i even, per thread: every stream is one 16-byte load or store
+// (LDG.E.128), halving the load/store instructions of the memory-bound kernels.  Same per-cell
+// arithmetic in the same order as the scalar kernels; used when nr is even and x is 16-B aligned.
+__device__ __forceinline__ double2 ld2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
+__device__ __forceinline__ double2 ld2rw(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+__device__ __forceinline__ void st2(double *p, double a, double b) {
+    *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
+
+template <bool WITH_DOT, bool LOOP, bool EXACT>
+__global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, DevArrays a, double *__restrict__ y,
+                                                                      Range rg, unsigned red_slot0,
+                                                                      unsigned red_total) {
+    if (LOOP && *(volatile int *)&a.sc->done) return;
+    using A = Ar<EXACT>;
+    const double *__restrict__ p = a.p;
+    const double *__restrict__ Tr = a.Tr;
+    const double *__restrict__ Tt = a.Tt;
+    const double *__restrict__ Tp = a.Tp;
+    const double *__restrict__ D = a.D;
+    const size_t plane = d.plane;
+    const int nr = d.nr, nt = d.nt;
+    Acc<EXACT> dot[1];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = rg.vend >> 1;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < npair; v += stride) {
+        const uint32_t v2 = 2u * v;
+        const uint32_t c = v2 + rg.off0 + (v2 >= rg.split ? rg.off1 : 0u);
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        const size_t cp = (size_t)c + plane;
+        const double2 pc = ld2(p + cp);
+        const double2 trv = ld2(Tr + c);
+        const double2 ttl = ld2(Tt + c);
+        const double2 tpl = ld2(Tp + c);
+        const double2 tph = ld2(Tp + c + plane);
+        const double2 pkm = ld2(p + cp - plane);
+        const double2 pkp = ld2(p + cp + plane);
+        const double2 dv = ld2(D + c);
+        const bool jlo = j > 0, jhi = j < nt - 1, ilo = i > 0, ihi = i + 2 < nr;
+        double2 ptm = make_double2(0.0, 0.0), ptp = ptm, tth = ptm;
+        if (jlo) ptm = ld2(p + cp - nr);
+        if (jhi) {
+            ptp = ld2(p + cp + nr);
+            tth = ld2(Tt + c + nr);
+        }
+        const double pm = ilo ? __ldg(p + cp - 1) : 0.0;
+        const double pp2 = ihi ? __ldg(p + cp + 2) : 0.0;
+        const double tr2 = ihi ? __ldg(Tr + c + 2) : 0.0;
+        // cell i
+        double s = 0.0;
+        if (ilo) s = A::acc(s, trv.x, pm);
+        s = A::acc(s, trv.y, pc.y);
+        if (jlo) s = A::acc(s, ttl.x, ptm.x);
+        if (jhi) s = A::acc(s, tth.x, ptp.x);
+        s = A::acc(s, tpl.x, pkm.x);
+        s = A::acc(s, tph.x, pkp.x);
+        const double q0 = A::diag_minus(dv.x, pc.x, s);
+        // cell i+1
+        s = 0.0;
+        s = A::acc(s, trv.y, pc.x);
+        if (ihi) s = A::acc(s, tr2, pp2);
+        if (jlo) s = A::acc(s, ttl.y, ptm.y);
+        if (jhi) s = A::acc(s, tth.y, ptp.y);
+        s = A::acc(s, tpl.y, pkm.y);
+        s = A::acc(s, tph.y, pkp.y);
+        const double q1 = A::diag_minus(dv.y, pc.y, s);
+        st2(y + c, q0, q1);
+        if (WITH_DOT) {
+            dot[0].add(pc.x, q0);
+            dot[0].add(pc.y, q1);
+        }
+    }
+    if (WITH_DOT) {
+        Acc<EXACT> out[1];
+        if (reduce_last<EXACT, kThreads, 1>(dot, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total,
+                                            out)) {
+            if (threadIdx.x == 0) {
+                a.sc->red1[0] = out[0].p;
+                a.sc->red1[1] = out[0].s;
+            }
+        }
+    }
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, DevArrays a, unsigned total) {
+    using A = Ar<EXACT>;
+    Scalars *sc = a.sc;
+    if (*(volatile int *)&sc->done) return;
+    const double pi = __dadd_rn(sc->red1[0], sc->red1[1]);
+    if (!(pi > 0.0) || !isfinite(pi)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            sc->status = ST_E_BREAKDOWN;
+            sc->done = 1;
+        }
+        return;
+    }
+    const double alpha = __ddiv_rn(sc->rho, pi);
+    double *__restrict__ r = a.r;
+    Acc<EXACT> acc[2];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = d.n >> 1;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < npair; v += stride) {
+        const uint32_t c = 2u * v;
+        const double2 rv = ld2rw(r + c), qv = ld2(a.q + c), dv = ld2(a.D + c);
+        const double r0 = A::ymax(rv.x, alpha, qv.x), r1 = A::ymax(rv.y, alpha, qv.y);
+        st2(r + c, r0, r1);
+        const double z0 = __ddiv_rn(r0, dv.x), z1 = __ddiv_rn(r1, dv.y);
+        acc[0].add(r0, z0);
+        acc[0].add(r1, z1);
+        acc[1].add(r0, r0);
+        acc[1].add(r1, r1);
+    }
+    Acc<EXACT> out[2];
+    if (reduce_last<EXACT, kThreads, 2>(acc, a.partials, &sc->ticket[1], blockIdx.x, total, out)) {
+        if (threadIdx.x == 0) {
+            sc->red2[0] = out[0].p;
+            sc->red2[1] = out[0].s;
+            sc->red2[2] = out[1].p;
+            sc->red2[3] = out[1].s;
+            sc->alpha = alpha;
+        }
+    }
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, DevArrays a, double *__restrict__ x, int chunk,
+                                                           unsigned total) {
+    using A = Ar<EXACT>;
+    Scalars *sc = a.sc;
+    if (*(volatile int *)&sc->done) return;
+    const double rz = __dadd_rn(sc->red2[0], sc->red2[1]);
+    const double rr = __dadd_rn(sc->red2[2], sc->red2[3]);
+    const double rn = sqrt(rr);
+    const bool conv = rn <= sc->tolbn;
+    const bool bad = !isfinite(rn) || !isfinite(rz);
+    const bool last = conv || bad || sc->iter + 1 >= sc->maxit;
+    const double alpha = sc->alpha;
+    const double beta = last ? 0.0 : __ddiv_rn(rz, sc->rho);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = d.n >> 1;
+    double *__restrict__ p = a.p;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < npair; v += stride) {
+        const uint32_t c = 2u * v;
+        const double2 po = ld2rw(p + (size_t)c + d.plane), xv = ld2rw(x + c);
+        st2(x + c, A::axpy(alpha, po.x, xv.x), A::axpy(alpha, po.y, xv.y));
+        if (!last) {
+            const double2 rv = ld2(a.r + c), dv = ld2(a.D + c);
+            const double p0 = A::axpy(beta, po.x, __ddiv_rn(rv.x, dv.x));
+            const double p1 = A::axpy(beta, po.y, __ddiv_rn(rv.y, dv.y));
+            st2(p + (size_t)c + d.plane, p0, p1);
+            if (d.periodic_local) {
+                if (c < d.plane) st2(p + (size_t)c + (size_t)(d.nloc + 1) * d.plane, p0, p1);
+                if (c >= d.n - d.plane) st2(p + (size_t)c - (size_t)(d.nloc - 1) * d.plane, p0, p1);
+            }
+        }
+    }
+    __shared__ bool am_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
+    }
+    __syncthreads();
+    if (am_last && threadIdx.x == 0) {
+        __threadfence();
+        const int it = sc->iter + 1;
+        sc->iter = it;
+        sc->rn = rn;
+        sc->hist_ring[(it - 1) % chunk] = rn;
+        if (conv) {
+            sc->status = ST_OK;
+            sc->done = 1;
+        } else if (bad) {
+            sc->status = ST_E_BREAKDOWN;
+            sc->done = 1;
+        } else if (it >= sc->maxit) {
+            sc->status = ST_NOT_CONVERGED;
+            sc->done = 1;
+        }
+        sc->rho = rz;
+        sc->ticket[2] = 0u;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_zero_x_if(Dims d, DevArrays a, double *__restrict__ x) {
     if (!a.sc->zero_x) return;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) x[c] = 0.0;
+}
+
+// 16-byte vector kernels: nr even (pairs never straddle a row; every plane offset even) and the
+// caller's array 16-byte aligned (workspace arrays are 256-byte aligned).
+inline bool use_vec2(const Dims &d, const void *x) {
+    return d.vec_ok && (d.nr % 2 == 0) && (((uintptr_t)x & 15) == 0);
+}
+
+inline unsigned grid_vec2(uint32_t n) {   // n cells, two per thread
+    uint64_t g = (n / 2 + kThreads - 1) / kThreads;
+    if (g < 1) g = 1;
+    if (g > (uint64_t)(148 * kVecBlocks)) g = 148 * kVecBlocks;
+    return (unsigned)g;
 }
 
 inline unsigned grid_for(uint32_t n) {
@@ -402,17 +604,23 @@ static Range make_range(const Dims &d, StencilPart part) {
     return rg;
 }
 
-unsigned stencil_blocks(const Dims &d, StencilPart part) {
+unsigned stencil_blocks(const Dims &d, StencilPart part, const double *y) {
     Range rg = make_range(d, part);
-    return rg.vend ? grid_for(rg.vend) : 0u;
+    if (!rg.vend) return 0u;
+    return use_vec2(d, y) ? grid_vec2(rg.vend) : grid_for(rg.vend);
 }
 
 void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart part, bool with_dot, bool loop,
                    unsigned red_slot0, unsigned red_total, bool exact, cudaStream_t st) {
     Range rg = make_range(d, part);
     if (rg.vend == 0) return;
-    const unsigned g = grid_for(rg.vend);
-#define MV(W, L, E) k_matvec_flat<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total)
+    const bool vec = use_vec2(d, y);
+    const unsigned g = vec ? grid_vec2(rg.vend) : grid_for(rg.vend);
+#define MV(W, L, E)                                                                             \
+    do {                                                                                        \
+        if (vec) k_matvec_vec2<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total); \
+        else k_matvec_flat<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);     \
+    } while (0)
     if (exact) {
         if (with_dot) {
             if (loop) MV(true, true, true);
@@ -439,12 +647,24 @@ void launch_setup_scalars(const DevArrays &a, double tol, int maxit, cudaStream_
 }
 
 void launch_update(const Dims &d, const DevArrays &a, bool exact, cudaStream_t st) {
+    if (use_vec2(d, nullptr)) {
+        const unsigned gv = grid_vec2(d.n);
+        if (exact) k_update_vec2<true><<<gv, kThreads, 0, st>>>(d, a, gv);
+        else k_update_vec2<false><<<gv, kThreads, 0, st>>>(d, a, gv);
+        return;
+    }
     const unsigned g = grid_for(d.n);
     if (exact) k_update<true><<<g, kThreads, 0, st>>>(d, a, g);
     else k_update<false><<<g, kThreads, 0, st>>>(d, a, g);
 }
 
 void launch_pupdate(const Dims &d, const DevArrays &a, double *x, int chunk, bool exact, cudaStream_t st) {
+    if (use_vec2(d, x)) {
+        const unsigned gv = grid_vec2(d.n);
+        if (exact) k_pupdate_vec2<true><<<gv, kThreads, 0, st>>>(d, a, x, chunk, gv);
+        else k_pupdate_vec2<false><<<gv, kThreads, 0, st>>>(d, a, x, chunk, gv);
+        return;
+    }
     const unsigned g = grid_for(d.n);
     if (exact) k_pupdate<true><<<g, kThreads, 0, st>>>(d, a, x, chunk, g);
     else k_pupdate<false><<<g, kThreads, 0, st>>>(d, a, x, chunk, g);

@@ -15,7 +15,7 @@ void launch_finalize_D(const Dims &d, const DevArrays &a, int bc_in, int bc_out,
 void launch_fill_p(const Dims &d, const DevArrays &a, const double *x, cudaStream_t st);
 
 // Number of blocks launch_matvec uses for `part` (0: nothing to do).
-unsigned stencil_blocks(const Dims &d, StencilPart part);
+unsigned stencil_blocks(const Dims &d, StencilPart part, const double *y);
 // y = A p over `part` of the slab.  with_dot: partial p.y into partial slots
 // [red_slot0, red_slot0 + blocks); the last of red_total blocks writes
 // sc->red1[0].  loop: early exit when sc->done.

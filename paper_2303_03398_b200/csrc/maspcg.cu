@@ -200,10 +200,10 @@ maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaSt
     return MASPCG_OK;
 }
 
-bool use_fused(const maspcg_ctx *c) { return c->path_opt != 1 && c->fused_bj > 0; }
+bool use_fused(const maspcg_ctx *c) { return c->path_opt == 2 && c->fused_bj > 0; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 int graph_key(const maspcg_ctx *c) {
-    return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0);
+    return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -220,15 +220,15 @@ maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStrea
 maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st) {
     if (c->nranks == 1) {
         launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
-                      stencil_blocks(c->d, StencilPart::Full), exact_arith(c), st);
+                      stencil_blocks(c->d, StencilPart::Full, y), exact_arith(c), st);
         return MASPCG_OK;
     }
     CK(c, cudaEventRecord(c->ev_p, st));
     CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
     RET_IF(halo_padded(c, c->a.p, c->comm_stream));
     CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
-    const unsigned gi = stencil_blocks(c->d, StencilPart::Interior);
-    const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary);
+    const unsigned gi = stencil_blocks(c->d, StencilPart::Interior, y);
+    const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary, y);
     launch_matvec(c->d, c->a, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, exact_arith(c), st);
     CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
     launch_matvec(c->d, c->a, y, StencilPart::Boundary, with_dot, loop, gi, gi + gb, exact_arith(c), st);
@@ -385,7 +385,7 @@ void accumulate_timing(maspcg_ctx *c, int iters_in_chunk) {
 long long kernels_per_iteration(const maspcg_ctx *c) {
     if (use_fused(c)) return 2;
     if (c->nranks == 1) return 3;
-    return 2 + (stencil_blocks(c->d, StencilPart::Interior) ? 1 : 0) + 1;
+    return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
 }
 
 bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
@@ -566,6 +566,7 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->d.div_r = make_fastdiv((uint32_t)nr);
     c->d.div_t = make_fastdiv((uint32_t)nt);
     c->d.periodic_local = nranks == 1 ? 1 : 0;
+    c->d.vec_ok = 1;
     c->fused_bj = fused_bj(nr, nt);   // 0: nr too large for one register batch per thread -> three kernels
     if (c->fused_bj > 0) {
         c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
@@ -885,6 +886,9 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             break;
         case MASPCG_OPT_USE_GRAPHS: c->use_graphs = v ? 1 : 0; break;
         case MASPCG_OPT_TIMING: c->timing = v ? 1 : 0; break;
+        case MASPCG_OPT_VEC:
+            c->d.vec_ok = v ? 1 : 0;
+            break;
         case MASPCG_OPT_TMA:
             c->use_tma = v ? 1 : 0;
             break;

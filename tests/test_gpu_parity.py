@@ -182,6 +182,17 @@ def test_fused_tma_and_register_variants_identical(torch_cuda, M, oracle_mod, sh
         assert_solve_parity(g, o)
 
 
+@pytest.mark.parametrize("shape", [(16, 16, 32), (40, 3, 2), (64, 32, 8), (13, 7, 5), (150, 30, 12)])
+def test_vector_and_scalar_kernels_identical(torch_cuda, M, oracle_mod, shape):
+    """Three-kernel path with 16-byte vector kernels (nr even) and scalar kernels: oracle iterates."""
+    nr, nt, np_ = shape
+    p = inputs.random_problem(nr, nt, np_, 400 + nr, bc_in=0, bc_out=1)
+    o = oracle_mod.solve_problem(p)
+    for vec in (1, 0):
+        g = gpu_solve(torch_cuda, M, p, opts={M.OPT_PATH: M.PATH_THREE_KERNELS, M.OPT_VEC: vec})
+        assert_solve_parity(g, o)
+
+
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("chunk,graphs,timing", [(1, 1, 0), (3, 1, 0), (16, 0, 0), (64, 1, 0), (7, 1, 1)])
 def test_solve_loop_modes_identical(torch_cuda, M, oracle_mod, chunk, graphs, timing, path):
