@@ -235,7 +235,8 @@ MASPCG_API maspcg_status maspcg_apply(maspcg_ctx *ctx, const double *x, double *
  * decomposition (halo planes, split interior/boundary stencil, all-reduced
  * scalars) can be verified against the oracle on a single GPU.
  * Every rank must call every function concurrently from its own thread, as with
- * MPI.  Loopback contexts never use CUDA graphs.  The group must outlive its
+ * MPI (including maspcg_destroy, which is collective for loopback contexts).
+ * Loopback contexts never use CUDA graphs.  The group must outlive its
  * contexts.  nranks in [1, 16]. */
 MASPCG_API maspcg_status maspcg_loopback_group_create(int nranks, void **group);
 MASPCG_API maspcg_status maspcg_loopback_group_destroy(void *group);

@@ -158,6 +158,9 @@ class LoopbackComm final : public Comm {
    public:
     LoopbackGroup *g = nullptr;
     ~LoopbackComm() override {
+        // collective, like every loopback call: a peer may still be issuing cudaStreamWaitEvent on
+        // this rank's events from the last exchange, so nobody destroys them before all arrive
+        g->barrier();
         auto &s = g->slots[rank];
         if (s.dslot) cudaFree(s.dslot);
         if (s.islot) cudaFree(s.islot);
