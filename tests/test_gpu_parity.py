@@ -338,3 +338,43 @@ def test_c3_full_size(torch_cuda, M, oracle_mod):
     assert st == M.OK and hist[-1] <= p.tol * info["bnorm"]
     true_r = np.linalg.norm(b - op.apply(x.cpu().numpy())) / np.linalg.norm(b)
     assert true_r <= 2 * p.tol
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("shape,min_iters", [((40, 40, 80), 1000), ((80, 80, 160), 2400)])
+def test_c4_recipe_long_high_contrast_solve_exact(torch_cuda, M, oracle_mod, shape, min_iters):
+    """c4 physics (kappa = (T 10^{0.4 G})^{5/2}, contrast ~4e5) solved to 1e-10 (1,060 and 2,504
+    iterations): long CG runs where rounding differences grow past 1e-10 in the history after ~1,000
+    iterations.  With the default arithmetic (R24) the GPU reproduces the
+    oracle's iterates exactly over the whole solve."""
+    p = inputs.make_problem("c4", shape=shape)
+    o = oracle_mod.solve_problem(p, tol=1e-10, maxit=20000)
+    assert o["status"] == 0 and o["iters"] >= min_iters
+    for path in PATHS:
+        g = gpu_solve(torch_cuda, M, p, tol=1e-10, maxit=20000, opts={M.OPT_PATH: path})
+        assert_solve_parity(g, o)
+
+
+@pytest.mark.slow
+def test_c5_warm_started_time_loop_exact(torch_cuda, M, oracle_mod):
+    """c5: repeated implicit solves of a backward-Euler time loop (f = s u^{n-1}, x0 = u^{n-1}) at
+    50 x 75 x 150; every step matches the oracle's iterates exactly."""
+    torch = torch_cuda
+    p = inputs.make_problem("c5", shape=(50, 75, 150))
+    S = M.solver_for_problem(p)
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, p.bc_in, p.bc_out)
+    f = p.f.copy()
+    u_o = p.x0.copy()
+    x = dev(torch, p.x0)
+    iters = []
+    for step in range(3):
+        b = op.rhs(f, p.g_in, p.g_out)
+        ost, ox, oit, ohist, obn, orn = op.pcg(b, u_o, p.tol, p.maxit)
+        st, info, hist = S.solve(dev(torch, f), x, p.tol, p.maxit)
+        xg = x.cpu().numpy()
+        assert st == ost == 0 and info["iters"] == oit
+        assert np.array_equal(xg, ox) and np.array_equal(hist, ohist)
+        iters.append(oit)
+        u_o = ox
+        f = p.s * ox          # caller's time loop: b = s V u^{n-1}
+    assert iters[1] < iters[0]  # warm starts converge faster (R12: tolerance relative to ||b||)
