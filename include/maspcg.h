@@ -190,6 +190,22 @@ MASPCG_API maspcg_status maspcg_set_coefficients_host(maspcg_ctx *ctx, const dou
                                                       const double *kt, const double *kp,
                                                       const double *shift, void *cuda_stream);
 
+/* Per-time-step assembly from physical fields (the implicit
+ * viscosity / thermal-conduction terms of MAS's time loop; reading R25 of DESIGN.md).
+ *   field  DEVICE [nloc][nt][nr], cell-centred (e.g. temperature T, or density rho)
+ *   kappa_c = kappa0 * field_c^(half_power/2), evaluated as ((kappa0 f) f ...) sqrt(f):
+ *            half_power 5 = Spitzer conduction kappa0 T^(5/2); 2 = viscosity nu rho (kappa0 = nu)
+ *   face coefficient = ARITHMETIC (a+b)/2 or HARMONIC 2ab/(a+b) mean of the two cells of an
+ *            interior face (phi periodic; across ranks the neighbour's plane is exchanged);
+ *            the adjacent cell's value on an r or theta boundary face
+ *   shift  s_c = inv_dt * rho_c (rho DEVICE [nloc][nt][nr], or NULL for s = inv_dt)
+ * Then exactly as maspcg_set_coefficients (E_INVALID if a value is negative or non-finite, e.g.
+ * a negative field with an odd half_power).  Collective for nranks > 1.  Synchronises the stream. */
+typedef enum { MASPCG_MEAN_ARITHMETIC = 0, MASPCG_MEAN_HARMONIC = 1 } maspcg_face_mean;
+MASPCG_API maspcg_status maspcg_set_coefficients_from_fields(maspcg_ctx *ctx, const double *field, double kappa0,
+                                                             int half_power, maspcg_face_mean mean,
+                                                             const double *rho, double inv_dt, void *cuda_stream);
+
 /* Radial boundary conditions (R7): inner (r = r_faces[0]) and outer
  * (r = r_faces[nr]) each DIRICHLET (value on the face; g [nloc][nt], DEVICE,
  * copied; NULL means 0) or NEUMANN0 (zero flux; g ignored).  May precede or

@@ -50,6 +50,7 @@ def lib():
             "masoracle_apply": [i, i, i, d, d, d, d, d, d],
             "masoracle_rhs": [i, i, i, d, d, d, d, d, i, d, i, d, d],
             "masoracle_pcg": [i, i, i, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
+            "masoracle_face_coefficients": [i, i, i, d, ctypes.c_double, i, i, d, ctypes.c_double, d, d, d, d],
         }.items():
             fn = getattr(_lib, name)
             fn.argtypes = args
@@ -84,6 +85,21 @@ def volumes(rf, tf, pf) -> np.ndarray:
     if st:
         raise OracleError(st, "volumes")
     return V
+
+
+def face_coefficients(field, kappa0, half_power, mean, rho=None, inv_dt=1.0):
+    """(kr, kt, kp, s) of the global grid from a cell field (NEXT-1, reading R25)."""
+    field = _c(field)
+    np_, nt, nr = field.shape
+    kr = np.empty((np_, nt, nr + 1))
+    kt = np.empty((np_, nt + 1, nr))
+    kp = np.empty((np_, nt, nr))
+    s = np.empty((np_, nt, nr))
+    st = lib().masoracle_face_coefficients(nr, nt, np_, _p(field), float(kappa0), int(half_power), int(mean),
+                                           _p(_c(rho)), float(inv_dt), _p(kr), _p(kt), _p(kp), _p(s))
+    if st:
+        raise OracleError(st, "face_coefficients")
+    return kr, kt, kp, s
 
 
 class Operator:

@@ -241,6 +241,67 @@ int masoracle_assemble(int nr, int nt, int np, const double *rf, const double *t
     return MO_OK;
 }
 
+/* ------------------------------------------------- face coefficients from fields (NEXT-1) */
+
+/* kappa of a cell from a physical field (R25): kappa = kappa0 * f^(m/2), evaluated as
+ * kappa0 * f * f * ... (m/2 factors) * sqrt(f) (if m odd), left to right -- e.g. Spitzer
+ * conduction kappa0 T^(5/2) = ((kappa0 T) T) sqrt(T), viscosity nu rho with m = 2. */
+static double mo_kappa(double kappa0, int half_power, double f) {
+    double v = kappa0;
+    for (int m = 0; m < half_power / 2; m++) v = v * f;
+    if (half_power % 2) v = v * sqrt(f);
+    return v;
+}
+
+/* mean of the two cells of a face (R25): arithmetic (a + b)/2 or harmonic 2ab/(a + b) (0 if a + b == 0) */
+static double mo_face_mean(int mode, double a, double b) {
+    if (mode == 0) return 0.5 * (a + b);
+    double sum = a + b;
+    return sum == 0.0 ? 0.0 : ((2.0 * a) * b) / sum;
+}
+
+/* Face diffusion coefficients and shift of the global grid from cell fields (SURVEY 8(f) NEXT-1:
+ * the per-time-step assembly of MAS's implicit parabolic terms):
+ *   kappa_c = kappa0 field_c^(half_power/2); kr, kt: mean of the two cells of an interior face, the
+ *   adjacent cell's value on a boundary face; kp (face k+1/2): mean of planes k and k+1 (mod np);
+ *   s_c = inv_dt * rho_c (rho == NULL: inv_dt).  Layouts as masoracle_assemble's inputs.
+ * Returns E_INVALID for half_power outside [0, 16] or mean not in {0, 1}.                       */
+int masoracle_face_coefficients(int nr, int nt, int np, const double *field, double kappa0,
+                                int half_power, int mean, const double *rho, double inv_dt,
+                                double *kr, double *kt, double *kp, double *s) {
+    if (half_power < 0 || half_power > 16 || (mean != 0 && mean != 1)) return MO_E_INVALID;
+    for (int k = 0; k < np; k++) {
+        int kp1 = (k + 1) % np;
+        for (int j = 0; j < nt; j++) {
+            for (int i = 0; i <= nr; i++) {
+                double v;
+                if (i == 0) v = mo_kappa(kappa0, half_power, field[IDX(k, j, 0, nt, nr)]);
+                else if (i == nr) v = mo_kappa(kappa0, half_power, field[IDX(k, j, nr - 1, nt, nr)]);
+                else v = mo_face_mean(mean, mo_kappa(kappa0, half_power, field[IDX(k, j, i - 1, nt, nr)]),
+                                      mo_kappa(kappa0, half_power, field[IDX(k, j, i, nt, nr)]));
+                kr[IDX(k, j, i, nt, nr + 1)] = v;
+            }
+        }
+        for (int j = 0; j <= nt; j++)
+            for (int i = 0; i < nr; i++) {
+                double v;
+                if (j == 0) v = mo_kappa(kappa0, half_power, field[IDX(k, 0, i, nt, nr)]);
+                else if (j == nt) v = mo_kappa(kappa0, half_power, field[IDX(k, nt - 1, i, nt, nr)]);
+                else v = mo_face_mean(mean, mo_kappa(kappa0, half_power, field[IDX(k, j - 1, i, nt, nr)]),
+                                      mo_kappa(kappa0, half_power, field[IDX(k, j, i, nt, nr)]));
+                kt[IDX(k, j, i, nt + 1, nr)] = v;
+            }
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i < nr; i++) {
+                size_t c = IDX(k, j, i, nt, nr);
+                kp[c] = mo_face_mean(mean, mo_kappa(kappa0, half_power, field[c]),
+                                     mo_kappa(kappa0, half_power, field[IDX(kp1, j, i, nt, nr)]));
+                s[c] = rho ? inv_dt * rho[c] : inv_dt;
+            }
+    }
+    return MO_OK;
+}
+
 /* ------------------------------------------------------------------ apply (R4) */
 
 /* y = A u with (A u)_c = D_c u_c - sum over the interior faces f of c of

@@ -125,6 +125,7 @@ struct DevArrays {
     // fused two-pass path
     double *P[2];       // [nloc][nt][nr] search directions of even / odd iterations
     double *rh, *dh, *ph;   // [2][nt][nr] received halo planes (lo, hi) of r, D, p_old (nranks > 1)
+    double *fh;             // [2][nt][nr] received halo planes of a physical field (from_fields, nranks > 1)
     // reductions
     double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums
     double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce

@@ -100,6 +100,48 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Dims d, DevArrays a, cons
 }
 
 // D = sV + Tr_lo + Tr_hi + Tt_lo + Tt_hi + Tp_lo + Tp_hi  (R7, R10)
+// ---------------------------------------------------------------- coefficients from fields (NEXT-1)
+// kappa_c = kappa0 f_c^(m/2) as ((kappa0 f) f ...) sqrt(f) -- the same product as the oracle (R25).
+__device__ __forceinline__ double kappa_of(double kappa0, int half_power, double f) {
+    double v = kappa0;
+    for (int m = 0; m < half_power / 2; ++m) v = __dmul_rn(v, f);
+    if (half_power & 1) v = __dmul_rn(v, __dsqrt_rn(f));
+    return v;
+}
+__device__ __forceinline__ double face_mean(int mode, double a, double b) {
+    if (mode == 0) return __dmul_rn(0.5, __dadd_rn(a, b));
+    const double sum = __dadd_rn(a, b);
+    return sum == 0.0 ? 0.0 : __ddiv_rn(__dmul_rn(__dmul_rn(2.0, a), b), sum);
+}
+
+// Face coefficients of the local slab into kr [nloc][nt][nr+1], kt [nloc][nt+1][nr], kp, s.
+// f_hi: the plane after the slab (plane 0 on a single rank, the right neighbour's first plane otherwise).
+__global__ void __launch_bounds__(kThreads) k_face_coeffs(Dims d, const double *__restrict__ f,
+                                                          const double *__restrict__ f_hi,
+                                                          const double *__restrict__ rho, double kappa0,
+                                                          int half_power, int mean, double inv_dt,
+                                                          double *__restrict__ kr, double *__restrict__ kt,
+                                                          double *__restrict__ kp, double *__restrict__ s) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        const uint32_t row = (uint32_t)k * d.nt + j;
+        const double kc = kappa_of(kappa0, half_power, f[c]);
+        // r-faces: lower face i (one-sided at i = 0) and, on the last cell, the outer face nr
+        kr[(size_t)row * (d.nr + 1) + i] = (i == 0) ? kc : face_mean(mean, kappa_of(kappa0, half_power, f[c - 1]), kc);
+        if (i == d.nr - 1) kr[(size_t)row * (d.nr + 1) + d.nr] = kc;
+        // theta-faces: lower face j (one-sided at j = 0) and, on the last row, face nt
+        const size_t tb = ((size_t)k * (d.nt + 1) + j) * d.nr + i;
+        kt[tb] = (j == 0) ? kc : face_mean(mean, kappa_of(kappa0, half_power, f[c - d.nr]), kc);
+        if (j == d.nt - 1) kt[tb + d.nr] = kc;
+        // phi-face k+1/2
+        const double fn = (k == d.nloc - 1) ? f_hi[c - (size_t)k * d.plane] : f[c + d.plane];
+        kp[c] = face_mean(mean, kc, kappa_of(kappa0, half_power, fn));
+        s[c] = rho ? __dmul_rn(inv_dt, rho[c]) : inv_dt;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_finalize_D(Dims d, DevArrays a, int bc_in, int bc_out) {
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
@@ -578,6 +620,13 @@ inline unsigned grid_for(uint32_t n) {
 void launch_assemble(const Dims &d, const DevArrays &a, const double *kr, const double *kt, const double *kp,
                      const double *s, cudaStream_t st) {
     k_assemble<<<grid_for(d.n), kThreads, 0, st>>>(d, a, kr, kt, kp, s);
+}
+
+void launch_face_coeffs(const Dims &d, const double *f, const double *f_hi, const double *rho, double kappa0,
+                        int half_power, int mean, double inv_dt, double *kr, double *kt, double *kp, double *s,
+                        cudaStream_t st) {
+    k_face_coeffs<<<grid_for(d.n), kThreads, 0, st>>>(d, f, f_hi, rho, kappa0, half_power, mean, inv_dt, kr, kt,
+                                                      kp, s);
 }
 
 void launch_finalize_D(const Dims &d, const DevArrays &a, int bc_in, int bc_out, cudaStream_t st) {

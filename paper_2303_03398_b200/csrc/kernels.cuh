@@ -11,6 +11,10 @@ enum class StencilPart { Full, Interior, Boundary };
 
 void launch_assemble(const Dims &d, const DevArrays &a, const double *kr, const double *kt, const double *kp,
                      const double *s, cudaStream_t st);
+// Face coefficients kr, kt, kp and shift s of the local slab from a cell field (NEXT-1, R25).
+void launch_face_coeffs(const Dims &d, const double *f, const double *f_hi, const double *rho, double kappa0,
+                        int half_power, int mean, double inv_dt, double *kr, double *kt, double *kp, double *s,
+                        cudaStream_t st);
 void launch_finalize_D(const Dims &d, const DevArrays &a, int bc_in, int bc_out, cudaStream_t st);
 void launch_fill_p(const Dims &d, const DevArrays &a, const double *x, cudaStream_t st);
 

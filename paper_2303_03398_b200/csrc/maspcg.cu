@@ -124,6 +124,7 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     t.rh = (double *)take(8 * 2 * plane);
     t.dh = (double *)take(8 * 2 * plane);
     t.ph = (double *)take(8 * 2 * plane);
+    t.fh = (double *)take(8 * 2 * plane);
     t.Tr = (double *)take(8 * n);
     t.TrB = (double *)take(8 * rows);
     t.Tt = (double *)take(8 * n);
@@ -757,6 +758,33 @@ maspcg_status maspcg_set_coefficients(maspcg_ctx *c, const double *kr, const dou
     c->any_shift = c->vflags_host[1];
     c->coef_set = true;
     return MASPCG_OK;
+}
+
+maspcg_status maspcg_set_coefficients_from_fields(maspcg_ctx *c, const double *field, double kappa0, int half_power,
+                                                  maspcg_face_mean mean, const double *rho, double inv_dt,
+                                                  void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!field) SET_ERR(c, MASPCG_E_INVALID, "field must be non-NULL");
+    if (half_power < 0 || half_power > 16) SET_ERR(c, MASPCG_E_INVALID, "half_power must be in [0, 16]");
+    if (mean != MASPCG_MEAN_ARITHMETIC && mean != MASPCG_MEAN_HARMONIC)
+        SET_ERR(c, MASPCG_E_INVALID, "mean must be ARITHMETIC or HARMONIC");
+    if (!std::isfinite(kappa0) || !std::isfinite(inv_dt)) SET_ERR(c, MASPCG_E_INVALID, "kappa0 and inv_dt must be finite");
+    if (!c->grid_set || !c->ws) SET_ERR(c, MASPCG_E_STATE, "set_grid and set_workspace must precede set_coefficients");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t pl = c->d.plane;
+    const double *f_hi = field;   // single rank: the plane after the slab is plane 0 (periodic)
+    if (c->nranks > 1) {
+        // the right neighbour's first plane of the field -> fh[1]
+        COMM(c, c->comm->halo_planes(field, field + (size_t)(c->nloc - 1) * pl, c->a.fh, c->a.fh + pl, pl, st,
+                                     c->err));
+        f_hi = c->a.fh + pl;
+    }
+    launch_face_coeffs(c->d, field, f_hi, rho, kappa0, half_power, (int)mean, inv_dt, c->a.skr, c->a.skt, c->a.skp,
+                       c->a.ss, st);
+    CK(c, cudaGetLastError());
+    c->stats.kernel_launches += 1;
+    return maspcg_set_coefficients(c, c->a.skr, c->a.skt, c->a.skp, c->a.ss, stream);
 }
 
 maspcg_status maspcg_set_coefficients_host(maspcg_ctx *c, const double *kr, const double *kt, const double *kp,

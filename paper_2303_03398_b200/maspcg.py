@@ -26,6 +26,7 @@ E_INVALID, E_STATE, E_SINGULAR, E_BREAKDOWN, E_CUDA, E_NCCL, E_NOMEM = -1, -2, -
 STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "E_INVALID", -2: "E_STATE", -3: "E_SINGULAR",
                 -4: "E_BREAKDOWN", -5: "E_CUDA", -6: "E_NCCL", -7: "E_NOMEM"}
 BC_DIRICHLET, BC_NEUMANN0 = 0, 1
+MEAN_ARITHMETIC, MEAN_HARMONIC = 0, 1
 OPT_CHUNK, OPT_USE_GRAPHS, OPT_TIMING, OPT_PATH, OPT_ARITH, OPT_TMA, OPT_VEC = 1, 2, 3, 4, 5, 6, 7
 ARITH_EXACT, ARITH_FAST = 0, 1
 PATH_AUTO, PATH_THREE_KERNELS, PATH_FUSED = 0, 1, 2
@@ -66,6 +67,7 @@ SIGNATURES = {
     "maspcg_set_workspace": ([_V, _V, _SZ], _I),
     "maspcg_set_coefficients": ([_V, _V, _V, _V, _V, _V], _I),
     "maspcg_set_coefficients_host": ([_V, _V, _V, _V, _V, _V], _I),
+    "maspcg_set_coefficients_from_fields": ([_V, _V, _D, _I, _I, _V, _D, _V], _I),
     "maspcg_set_bc_r": ([_V, _I, _V, _I, _V, _V], _I),
     "maspcg_set_bc_r_host": ([_V, _I, _V, _I, _V, _V], _I),
     "maspcg_solve": ([_V, _V, _V, _D, _I, _V, ctypes.POINTER(Info), _V], _I),
@@ -221,6 +223,12 @@ class Solver:
         host = isinstance(kr, np.ndarray)
         fn = self._L.maspcg_set_coefficients_host if host else self._L.maspcg_set_coefficients
         self._check(fn(self.ctx, _ptr(kr), _ptr(kt), _ptr(kp), _ptr(s), _stream(stream)))
+
+    def set_coefficients_from_fields(self, field, kappa0: float, half_power: int, mean: int = MEAN_ARITHMETIC,
+                                     rho=None, inv_dt: float = 1.0, stream=None):
+        """maspcg_set_coefficients_from_fields: kappa = kappa0 field^(half_power/2) on faces, s = inv_dt rho."""
+        self._check(self._L.maspcg_set_coefficients_from_fields(self.ctx, _ptr(field), float(kappa0), int(half_power),
+                                                                int(mean), _ptr(rho), float(inv_dt), _stream(stream)))
 
     def set_bc_r(self, bc_in: int, g_in, bc_out: int, g_out, stream=None):
         host = isinstance(g_in, np.ndarray) or isinstance(g_out, np.ndarray) or (g_in is None and g_out is None)

@@ -156,3 +156,32 @@ def test_multirank_errors_agree(M):
             S.close()
 
     assert run_ranks(M, 2, rank) == [M.E_INVALID, M.E_INVALID]
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_multirank_coefficients_from_fields(M, oracle_mod, P):
+    """NEXT-1 across ranks: the phi face of each slab's last plane needs the right neighbour's first
+    plane of the field (exchanged); every slab operator equals the oracle's slice bit for bit."""
+    import torch
+    fn = lambda k0, n: inputs.random_problem(10, 7, 6, 33, k0=k0 or 0, nloc=n)
+    full = fn(None, None)
+    T = np.random.default_rng(P).uniform(0.4, 2.0, (full.np, full.nt, full.nr))
+
+    def rank(r, g):
+        p = slab_of(fn, P, r)
+        S = M.Solver(p.nr, p.nt, p.np, p.rf, p.tf, p.pf, loopback=(g, r))
+        Tl = torch.from_numpy(T[p.k0:p.k0 + p.nloc].copy()).cuda()
+        S.set_coefficients_from_fields(Tl, 1.3, 5, M.MEAN_HARMONIC, None, 4.0)
+        S.set_bc_r(p.bc_in, torch.from_numpy(p.g_in).cuda(), p.bc_out, None)
+        ops = S.get_operator()
+        S.close()
+        return ops
+
+    res = run_ranks(M, P, rank)
+    kr, kt, kp, s = oracle_mod.face_coefficients(T, 1.3, 5, 1, None, 4.0)
+    op = oracle_mod.Operator(full.rf, full.tf, full.pf, kr, kt, kp, s, full.bc_in, full.bc_out)
+    for r, (Tr, Tt, Tp, D) in enumerate(res):
+        k0, nloc = inputs.slab_extent(full.np, r, P)
+        sl = slice(k0, k0 + nloc)
+        assert np.array_equal(Tr, op.Tr[sl]) and np.array_equal(Tt, op.Tt[sl])
+        assert np.array_equal(Tp, op.Tp[sl]) and np.array_equal(D, op.D[sl])

@@ -378,3 +378,52 @@ def test_c5_warm_started_time_loop_exact(torch_cuda, M, oracle_mod):
         u_o = ox
         f = p.s * ox          # caller's time loop: b = s V u^{n-1}
     assert iters[1] < iters[0]  # warm starts converge faster (R12: tolerance relative to ||b||)
+
+
+@pytest.mark.parametrize("mean,half_power,with_rho", [(0, 5, True), (1, 5, False), (1, 2, True), (0, 0, False)])
+def test_coefficients_from_fields_bitwise(torch_cuda, M, oracle_mod, mean, half_power, with_rho):
+    """maspcg_set_coefficients_from_fields (NEXT-1): face kappa from a cell field and the shift from
+    rho, assembled on the device -- the operator equals the oracle's bit for bit."""
+    torch = torch_cuda
+    p = inputs.random_problem(14, 9, 10, 500 + half_power)
+    rng = np.random.default_rng(half_power + 10 * mean)
+    T = rng.uniform(0.3, 2.0, (p.np, p.nt, p.nr))
+    rho = rng.uniform(0.5, 1.5, T.shape) if with_rho else None
+    S = M.Solver(p.nr, p.nt, p.np, p.rf, p.tf, p.pf)
+    S.set_coefficients_from_fields(dev(torch, T), 0.8, half_power, mean, dev(torch, rho), 25.0)
+    S.set_bc_r(p.bc_in, dev(torch, p.g_in), p.bc_out, None)
+    kr, kt, kp, s = oracle_mod.face_coefficients(T, 0.8, half_power, mean, rho, 25.0)
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, kr, kt, kp, s, p.bc_in, p.bc_out)
+    for g, o in zip(S.get_operator(), (op.Tr, op.Tt, op.Tp, op.D)):
+        assert np.array_equal(g, o)
+    with pytest.raises(M.MaspcgError) as e:          # T^(5/2) of a negative temperature -> NaN
+        S.set_coefficients_from_fields(dev(torch, -T), 1.0, 5, mean, None, 1.0)
+    assert e.value.status == M.E_INVALID
+
+
+@pytest.mark.slow
+def test_nonlinear_conduction_time_loop_exact(torch_cuda, M, oracle_mod):
+    """Backward-Euler thermal conduction with lagged kappa(T) = kappa0 T^(5/2) (the per-step
+    assembly of NEXT-1 feeding the PCG of every step): 4 steps of (rho/dt - div kappa(T^n) grad) T^{n+1}
+    = rho/dt T^n on the c2 grid, identical to the oracle step by step."""
+    torch = torch_cuda
+    p = inputs.make_problem("c2", shape=(32, 32, 64))
+    rc = inputs.midpoints(p.rf)
+    T = np.broadcast_to(inputs.t_profile(1.0 + 0.02 * (rc - 1.0))[None, None, :], (p.np, p.nt, p.nr)).copy()
+    T *= 1.0 + 0.1 * inputs.white_noise(9, p.nr, p.nt, 0, p.np)
+    rho = np.broadcast_to(inputs.rho_hydro(rc)[None, None, :], T.shape).copy()
+    dt = 0.05
+    S = M.Solver(p.nr, p.nt, p.np, p.rf, p.tf, p.pf)
+    S.set_bc_r(M.BC_DIRICHLET, dev(torch, T[:, :, 0].copy()), M.BC_NEUMANN0, None)
+    Tg, To = dev(torch, T), T.copy()
+    for step in range(4):
+        S.set_coefficients_from_fields(Tg.clone(), 1.0, 5, M.MEAN_HARMONIC, dev(torch, rho), 1.0 / dt)
+        f = (rho / dt) * To                           # per-unit-volume source s T^n
+        kr, kt, kp, s = oracle_mod.face_coefficients(To, 1.0, 5, 1, rho, 1.0 / dt)
+        op = oracle_mod.Operator(p.rf, p.tf, p.pf, kr, kt, kp, s, 0, 1)
+        b = op.rhs(f, T[:, :, 0].copy(), None)
+        ost, ox, oit, ohist, obn, orn = op.pcg(b, To, 1e-10, 5000)
+        st, info, hist = S.solve(dev(torch, f), Tg, 1e-10, 5000)
+        assert st == ost == 0 and info["iters"] == oit
+        assert np.array_equal(Tg.cpu().numpy(), ox) and np.array_equal(hist, ohist)
+        To = ox

@@ -368,3 +368,48 @@ def test_config_c1_iteration_count(oracle_mod):
     r = oracle_mod.solve_problem(inputs.make_problem("c1"))
     assert r["status"] == 0 and r["iters"] == 130
     assert r["hist"][-1] <= 1e-10 * r["bnorm"]
+
+
+# ------------------------------------------------------------------ face coefficients from fields (NEXT-1, R25)
+def test_face_coefficients_closed_forms(oracle_mod):
+    """Constant field c: every face kappa = kappa0 c^(m/2) (both means); m = 0 gives kappa0; the shift
+    is inv_dt * rho.  Two-cell hand values: kappa = [1, 32] (T = [1, 4], m = 5) -> arithmetic 33/2,
+    harmonic 2*32/33 on the shared face."""
+    f = np.full((3, 4, 5), 2.0)
+    rho = np.random.default_rng(1).uniform(0.5, 2.0, f.shape)
+    for mean in (0, 1):
+        kr, kt, kp, s = oracle_mod.face_coefficients(f, 1.5, 5, mean, rho, 10.0)
+        for a in (kr, kt, kp):
+            np.testing.assert_allclose(a, 1.5 * 2.0 ** 2.5, rtol=2e-16 * 8)
+        np.testing.assert_array_equal(s, 10.0 * rho)
+        kr, kt, kp, s = oracle_mod.face_coefficients(f, 0.7, 0, mean)
+        assert (kr == 0.7).all() and (kp == 0.7).all() and (s == 1.0).all()
+    T = np.array([1.0, 4.0]).reshape(1, 1, 2)
+    kr, kt, kp, s = oracle_mod.face_coefficients(T, 1.0, 5, 0)
+    assert kr.ravel().tolist() == [1.0, 16.5, 32.0]
+    kr, kt, kp, s = oracle_mod.face_coefficients(T, 1.0, 5, 1)
+    assert kr.ravel()[0] == 1.0 and kr.ravel()[2] == 32.0
+    assert kr.ravel()[1] == pytest.approx(64.0 / 33.0, rel=1e-15)
+
+
+def test_face_coefficients_means_and_periodic_wrap(oracle_mod):
+    """Harmonic <= arithmetic with equality only for equal neighbours; the phi face of the last plane
+    averages it with plane 0; boundary r / theta faces take the adjacent cell's kappa."""
+    rng = np.random.default_rng(3)
+    f = rng.uniform(0.2, 3.0, (6, 5, 7))
+    ka = oracle_mod.face_coefficients(f, 2.0, 5, 0)
+    kh = oracle_mod.face_coefficients(f, 2.0, 5, 1)
+    for a, h in zip(ka[:3], kh[:3]):
+        assert (h <= a * (1 + 1e-15)).all()
+    kap = 2.0 * f ** 2.5
+    np.testing.assert_allclose(ka[2][-1], 0.5 * (kap[-1] + kap[0]), rtol=1e-14)
+    np.testing.assert_allclose(ka[0][:, :, 0], kap[:, :, 0], rtol=1e-14)
+    np.testing.assert_allclose(ka[0][:, :, -1], kap[:, :, -1], rtol=1e-14)
+    np.testing.assert_allclose(ka[1][:, 0, :], kap[:, 0, :], rtol=1e-14)
+    # the operator assembled from these faces is still symmetric positive definite
+    p = inputs.random_problem(7, 5, 6, 1)
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, *kh[:3], kh[3] * 0 + 1.0, 0, 1)
+    x, y = rng.standard_normal(op.shape), rng.standard_normal(op.shape)
+    assert abs(np.vdot(x, op.apply(y)) - np.vdot(y, op.apply(x))) <= 1e-12 * np.vdot(np.abs(x), np.abs(op.apply(np.abs(y))))
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.face_coefficients(f, 1.0, 17, 0)
