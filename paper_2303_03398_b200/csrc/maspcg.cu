@@ -65,7 +65,7 @@ struct maspcg_ctx {
     int *vflags_host = nullptr;
 
     // graph cache (one captured chunk of `chunk` iterations)
-    cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // one captured chunk per timing-event set
     const void *g_x = nullptr;
     int g_chunk = 0, g_variant = -1;
 
@@ -76,7 +76,8 @@ struct maspcg_ctx {
     int tma_ok = 0, tma_njt = 1, tma_nch = 1, tma_hmax = 1, use_tma = 1;
     cudaEvent_t ev_a = nullptr, ev_ph = nullptr;
     maspcg_stats stats{};
-    std::vector<cudaEvent_t> tev;   // timing events [3 kernels][2][chunk]
+    std::vector<cudaEvent_t> tev;   // timing events [2 sets][3 kernels][2][chunk]
+    int tset = 0;                   // event set of the chunk being enqueued
 };
 
 #define SET_ERR(ctx, code, ...)                                              \
@@ -251,20 +252,27 @@ maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
 
 int timing_ev_index(int kern, int which, int it, int chunk) { return (kern * 2 + which) * chunk + it; }
 
+// Record timing event (kern, which) of iteration slot `it` of the current set.  External records so
+// that, inside a stream capture, the graph node records the event at every replay.
+cudaError_t record_timing(maspcg_ctx *c, int kern, int which, int it, cudaStream_t st) {
+    const size_t idx = (size_t)c->tset * 6 * c->chunk + timing_ev_index(kern, which, it, c->chunk);
+    return cudaEventRecordWithFlags(c->tev[idx], st, cudaEventRecordExternal);
+}
+
 // One PCG iteration.  it: index within the chunk (timing).
 maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int it) {
     const bool tm = c->timing != 0;
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 0, it, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 0, 0, it, st));
     RET_IF(stencil_with_halo(c, c->a.q, true, true, st));
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 1, it, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 0, 1, it, st));
     RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st));
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 0, it, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 1, 0, it, st));
     launch_update(c->d, c->a, exact_arith(c), st);
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 1, it, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 1, 1, it, st));
     RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st));
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 0, it, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 2, 0, it, st));
     launch_pupdate(c->d, c->a, x, c->chunk, exact_arith(c), st);
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 1, it, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 2, 1, it, st));
     return MASPCG_OK;
 }
 
@@ -302,9 +310,9 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
         f.nch = 1;
     }
     if (c->nranks > 1 && slot > 0) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // p_old halo of slot-1
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 0, slot, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 0, 0, slot, st));
     launch_pass_a(c->d, c->a, f, c->fused_blocks, exact_arith(c), st);
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(0, 1, slot, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 0, 1, slot, st));
     if (c->nranks > 1) {
         // p_it halo for the next pass A, on the communication stream, overlapped with pass B
         CK(c, cudaEventRecord(c->ev_a, st));
@@ -313,17 +321,17 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
         CK(c, cudaEventRecord(c->ev_ph, c->comm_stream));
     }
     RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st));
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 0, slot, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 1, 0, slot, st));
     launch_pass_b(c->d, c->a, exact_arith(c), st);
-    if (tm) CK(c, cudaEventRecord(c->tev[timing_ev_index(1, 1, slot, c->chunk)], st));
+    if (tm) CK(c, record_timing(c, 1, 1, slot, st));
     RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st));
     if (c->nranks > 1) {
         RET_IF(halo_planes(c, c->a.r, c->a.rh, st));            // r_it halo (critical path, one plane each way)
         if (slot == c->chunk - 1) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // join before the chunk ends
     }
     if (tm) {   // keep the 3-slot event layout: no third kernel on this path
-        CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 0, slot, c->chunk)], st));
-        CK(c, cudaEventRecord(c->tev[timing_ev_index(2, 1, slot, c->chunk)], st));
+        CK(c, record_timing(c, 2, 0, slot, st));
+        CK(c, record_timing(c, 2, 1, slot, st));
     }
     return MASPCG_OK;
 }
@@ -332,47 +340,55 @@ maspcg_status enqueue_any(maspcg_ctx *c, double *x, cudaStream_t st, int slot) {
     return use_fused(c) ? enqueue_iteration_fused(c, x, st, slot) : enqueue_iteration(c, x, st, slot);
 }
 
-maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st) {
-    const bool graphs = c->use_graphs && !c->timing;
-    if (!graphs) {
+maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st, int set) {
+    c->tset = set;
+    if (!c->use_graphs) {
         for (int it = 0; it < c->chunk; ++it) RET_IF(enqueue_any(c, x, st, it));
         CK(c, cudaGetLastError());
         return MASPCG_OK;
     }
-    if (!c->gexec || c->g_x != x || c->g_chunk != c->chunk || c->g_variant != graph_key(c)) {
-        if (c->gexec) {
-            cudaGraphExecDestroy(c->gexec);
-            c->gexec = nullptr;
+    const int key = graph_key(c) | (c->timing ? 16 : 0);
+    if (!c->gexec[0] || c->g_x != x || c->g_chunk != c->chunk || c->g_variant != key) {
+        for (int b = 0; b < 2; ++b) {
+            if (c->gexec[b]) {
+                cudaGraphExecDestroy(c->gexec[b]);
+                c->gexec[b] = nullptr;
+            }
         }
-        cudaGraph_t g = nullptr;
-        cudaStream_t cs = c->cap_stream;
-        CK(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        maspcg_status s = MASPCG_OK;
-        for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_any(c, x, cs, it);
-        cudaError_t e = cudaStreamEndCapture(cs, &g);
-        if (s != MASPCG_OK) {
-            if (g) cudaGraphDestroy(g);
-            return s;
+        for (int b = 0; b < 2; ++b) {   // identical graphs except for the timing-event set
+            c->tset = b;
+            cudaGraph_t g = nullptr;
+            cudaStream_t cs = c->cap_stream;
+            CK(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            maspcg_status s = MASPCG_OK;
+            for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_any(c, x, cs, it);
+            cudaError_t e = cudaStreamEndCapture(cs, &g);
+            if (s != MASPCG_OK) {
+                if (g) cudaGraphDestroy(g);
+                return s;
+            }
+            CK(c, e);
+            cudaError_t ei = cudaGraphInstantiate(&c->gexec[b], g, 0);
+            cudaGraphDestroy(g);
+            CK(c, ei);
         }
-        CK(c, e);
-        cudaError_t ei = cudaGraphInstantiate(&c->gexec, g, 0);
-        cudaGraphDestroy(g);
-        CK(c, ei);
         c->g_x = x;
         c->g_chunk = c->chunk;
-        c->g_variant = graph_key(c);
+        c->g_variant = key;
+        c->tset = set;
     }
-    CK(c, cudaGraphLaunch(c->gexec, st));
+    CK(c, cudaGraphLaunch(c->gexec[set], st));
     return MASPCG_OK;
 }
 
-void accumulate_timing(maspcg_ctx *c, int iters_in_chunk) {
+void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
+    const size_t base = (size_t)set * 6 * c->chunk;
     for (int it = 0; it < iters_in_chunk; ++it) {
         float ms[3];
         for (int k = 0; k < 3; ++k) {
             ms[k] = 0.f;
-            cudaEventElapsedTime(&ms[k], c->tev[timing_ev_index(k, 0, it, c->chunk)],
-                                 c->tev[timing_ev_index(k, 1, it, c->chunk)]);
+            cudaEventElapsedTime(&ms[k], c->tev[base + timing_ev_index(k, 0, it, c->chunk)],
+                                 c->tev[base + timing_ev_index(k, 1, it, c->chunk)]);
         }
         c->stats.matvec_ms += ms[0];
         c->stats.matvec_launches += 1;
@@ -428,10 +444,10 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     const int ring = fused ? 2 * kMaxChunk : c->chunk;
     double rn = s0.rn, bn = s0.bn;
     bool done = s0.done != 0;
-    const bool pipelined = !c->timing;
+    const bool pipelined = true;   // timing events alternate between two sets, like the snapshots
     int issued = 0, cur = 0;
     auto issue = [&](int b) -> maspcg_status {
-        RET_IF(enqueue_chunk(c, x, st));
+        RET_IF(enqueue_chunk(c, x, st, b));
         CK(c, cudaMemcpyAsync(c->snap[b], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
         CK(c, cudaEventRecord(c->ev_chunk[b], st));
         issued += c->chunk;
@@ -448,7 +464,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
             }
             CK(c, cudaEventSynchronize(c->ev_chunk[cur]));
             const Scalars &s = *c->snap[cur];
-            if (c->timing) accumulate_timing(c, s.iter - iters);
+            if (c->timing) accumulate_timing(c, cur, s.iter - iters);
             const int hnew = fused ? s.hist_count : s.iter;
             if (hist)
                 for (int k = hdone + 1; k <= hnew; ++k) hist[k] = s.hist_ring[(k - 1) % ring];
@@ -611,7 +627,8 @@ maspcg_status maspcg_destroy(maspcg_ctx *c) {
     if (!c) return MASPCG_OK;
     cudaSetDevice(c->device);
     delete c->comm;
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (int b = 0; b < 2; ++b)
+        if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
     for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
     if (c->ev_p) cudaEventDestroy(c->ev_p);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -720,9 +737,11 @@ maspcg_status maspcg_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
     c->coef_set = false;
     c->bc_set = false;
     c->D_dirty = true;
-    if (c->gexec) {
-        cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
+    for (int b = 0; b < 2; ++b) {
+        if (c->gexec[b]) {
+            cudaGraphExecDestroy(c->gexec[b]);
+            c->gexec[b] = nullptr;
+        }
     }
     return MASPCG_OK;
 }
@@ -931,7 +950,7 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
         default: SET_ERR(c, MASPCG_E_INVALID, "unknown option %d", (int)opt);
     }
     if (c->timing) {
-        const size_t need = (size_t)3 * 2 * c->chunk;
+        const size_t need = (size_t)2 * 3 * 2 * c->chunk;
         RET_IF(bind_device(c));
         while (c->tev.size() < need) {
             cudaEvent_t e;
