@@ -38,6 +38,8 @@ PATHS = {
         "update": ("update_jacobi_dots (k_update)", 32), "pupdate": ("x_and_p_update (k_pupdate)", 48), "iter": 128},
     2: {"name": "fused two passes", "stencil": ("pass A: p-update + x-update + stencil + p.q (k_pass_a)", 80),
         "update": ("pass B: r-update + Jacobi + r.z, r.r (k_pass_b)", 32), "pupdate": None, "iter": 112},
+    3: {"name": "wave", "stencil": ("wave: x/p-update + stencil + p.q, flag-ordered (k_wave)", 80),
+        "update": ("update_jacobi_dots (k_update_vec2)", 32), "pupdate": None, "iter": 112},
 }
 
 
@@ -179,7 +181,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
-    ap.add_argument("--path", type=int, default=0, help="0 auto (= 1), 1 three kernels, 2 fused two passes")
+    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 three kernels, 2 fused two passes, 3 wave")
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=1, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")

@@ -122,7 +122,10 @@ typedef enum {
                                     even; 0: register-batched loads */
     MASPCG_OPT_PATH = 4          /* iteration path: 0 = auto (default, = 1), 1 = three streaming kernels (stencil+p.q,
                                     r-update+Jacobi+dots, deferred x-update+p-update; 128 B/cell), 2 = fused two passes
-                                    (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell) */
+                                    (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell),
+                                    3 = wave (single rank): r-update, then the p-update of iteration k and the stencil
+                                    of iteration k+1 in one persistent kernel ordered by plane-completion flags, p and D
+                                    re-read from L2 (112 B/cell of HBM traffic) */
 } maspcg_option;
 
 /* ---- lifetime ----------------------------------------------------------- */

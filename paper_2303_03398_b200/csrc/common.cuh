@@ -126,6 +126,10 @@ struct DevArrays {
     double *P[2];       // [nloc][nt][nr] search directions of even / odd iterations
     double *rh, *dh, *ph;   // [2][nt][nr] received halo planes (lo, hi) of r, D, p_old (nranks > 1)
     double *fh;             // [2][nt][nr] received halo planes of a physical field (from_fields, nranks > 1)
+    // wave path (wave.cu)
+    unsigned *wave_counter; // work-item counter
+    unsigned *wave_flags;   // [nloc] completed A-tiles per plane
+    double *wave_partials;  // [nloc * tiles per plane][2]
     // reductions
     double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums
     double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce

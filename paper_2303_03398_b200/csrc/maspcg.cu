@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "wave.cuh"
 
 using namespace maspcg;
 
@@ -73,7 +74,8 @@ struct maspcg_ctx {
     int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
     // fused two-pass path geometry (fused.cu)
     int fused_bj = 1, fused_njt = 1, fused_blocks = 1;
-    int tma_ok = 0, tma_njt = 1, tma_nch = 1, tma_hmax = 1, use_tma = 1;
+    int tma_ok = 0, tma_njt = 1, tma_nch = 1, tma_hmax = 1, use_tma = 0;
+    int wave_grid = 1;   // path 3: co-resident grid of k_wave
     cudaEvent_t ev_a = nullptr, ev_ph = nullptr;
     maspcg_stats stats{};
     std::vector<cudaEvent_t> tev;   // timing events [2 sets][3 kernels][2][chunk]
@@ -126,6 +128,10 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     t.dh = (double *)take(8 * 2 * plane);
     t.ph = (double *)take(8 * 2 * plane);
     t.fh = (double *)take(8 * 2 * plane);
+    const size_t tpp = (size_t)wave_tiles_per_plane((uint32_t)plane);
+    t.wave_counter = (unsigned *)take(256);
+    t.wave_flags = (unsigned *)take(4 * (size_t)c->nloc);
+    t.wave_partials = (double *)take(8 * 2 * tpp * c->nloc);
     t.Tr = (double *)take(8 * n);
     t.TrB = (double *)take(8 * rows);
     t.Tt = (double *)take(8 * n);
@@ -203,9 +209,11 @@ maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaSt
 }
 
 bool use_fused(const maspcg_ctx *c) { return c->path_opt == 2 && c->fused_bj > 0; }
+bool use_wave(const maspcg_ctx *c) { return c->path_opt == 3 && c->nranks == 1; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 int graph_key(const maspcg_ctx *c) {
-    return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0);
+    return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
+           (use_wave(c) ? 32 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -336,7 +344,30 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
     return MASPCG_OK;
 }
 
+// One PCG iteration of the wave path (wave.cu): the r-update of iteration k, then the p-update of
+// iteration k and the stencil of iteration k+1 in one flag-ordered kernel (single rank).
+maspcg_status enqueue_iteration_wave(maspcg_ctx *c, double *x, cudaStream_t st, int it) {
+    const bool tm = c->timing != 0;
+    if (tm) CK(c, record_timing(c, 1, 0, it, st));
+    launch_update(c->d, c->a, exact_arith(c), st);
+    if (tm) CK(c, record_timing(c, 1, 1, it, st));
+    WaveArgs w{};
+    w.counter = c->a.wave_counter;
+    w.flags = c->a.wave_flags;
+    w.tile_partials = c->a.wave_partials;
+    w.tpp = wave_tiles_per_plane(c->d.plane);
+    if (tm) CK(c, record_timing(c, 0, 0, it, st));
+    launch_wave(c->d, c->a, w, x, c->chunk, c->wave_grid, exact_arith(c), st);
+    if (tm) CK(c, record_timing(c, 0, 1, it, st));
+    if (tm) {
+        CK(c, record_timing(c, 2, 0, it, st));
+        CK(c, record_timing(c, 2, 1, it, st));
+    }
+    return MASPCG_OK;
+}
+
 maspcg_status enqueue_any(maspcg_ctx *c, double *x, cudaStream_t st, int slot) {
+    if (use_wave(c)) return enqueue_iteration_wave(c, x, st, slot);
     return use_fused(c) ? enqueue_iteration_fused(c, x, st, slot) : enqueue_iteration(c, x, st, slot);
 }
 
@@ -400,7 +431,7 @@ void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
 }
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
-    if (use_fused(c)) return 2;
+    if (use_fused(c) || use_wave(c)) return 2;
     if (c->nranks == 1) return 3;
     return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
 }
@@ -431,6 +462,14 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     RET_IF(allreduce_dot2(c, c->a.sc->red3, 3, st));
     if (fused && c->nranks > 1) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
     launch_setup_scalars(c->a, tol, maxit, st);
+    if (use_wave(c)) {
+        // the wave kernel fuses the stencil of iteration k+1 into the p-update of iteration k, so the
+        // first stencil (q = A p0, p0.q) runs here; the dispatch counter and flags start from zero
+        CK(c, cudaMemsetAsync(c->a.wave_counter, 0, sizeof(unsigned), st));
+        CK(c, cudaMemsetAsync(c->a.wave_flags, 0, sizeof(unsigned) * c->nloc, st));
+        launch_matvec(c->d, c->a, c->a.q, StencilPart::Full, true, true, 0,
+                      stencil_blocks(c->d, StencilPart::Full, c->a.q), exact_arith(c), st);
+    }
     CK(c, cudaGetLastError());
     long long launched = 4 + (c->nranks > 1 ? 1 : 0);
 
@@ -489,7 +528,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
     c->stats.kernel_launches += launched;
-    c->stats.path = fused ? 2 : 1;
+    c->stats.path = use_wave(c) ? 3 : (fused ? 2 : 1);
     c->stats.solves += 1;
     c->stats.iterations += iters;
     if (info) {
@@ -589,6 +628,7 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
         c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
         c->fused_blocks = fused_blocks(nr, nt, c->nloc, c->fused_bj, cuda_device);
     }
+    c->wave_grid = wave_grid(cuda_device);
     c->tma_ok = fused_tma_geometry(nr, nt, c->nloc, cuda_device, &c->tma_njt, &c->tma_nch, &c->tma_hmax) ? 1 : 0;
     *out = c;
     return MASPCG_OK;
@@ -944,7 +984,8 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             c->arith = (int)v;
             break;
         case MASPCG_OPT_PATH:
-            if (v < 0 || v > 2) SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels) or 2 (fused)");
+            if (v < 0 || v > 3)
+                SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels), 2 (fused) or 3 (wave)");
             c->path_opt = (int)v;
             break;
         default: SET_ERR(c, MASPCG_E_INVALID, "unknown option %d", (int)opt);

@@ -128,7 +128,7 @@ def test_apply_parity(torch_cuda, M, oracle_mod, shape):
     assert apply_err(op, x, y).max() <= APPLY_TOL
 
 
-PATHS = [1, 2]   # MASPCG_OPT_PATH: three kernels, fused two passes
+PATHS = [1, 2, 3]   # MASPCG_OPT_PATH: three kernels, fused two passes, wave (flag-ordered p-update + stencil)
 
 
 @pytest.mark.parametrize("path", PATHS)
