@@ -184,7 +184,7 @@ def main():
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 three kernels, 2 fused two passes, 3 wave")
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
-    ap.add_argument("--tma", type=int, default=1, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
+    ap.add_argument("--tma", type=int, default=0, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
     args = ap.parse_args()
     if args.warmup < 3 and args.maxit is None:
         args.warmup = 3

@@ -42,6 +42,8 @@ __device__ __forceinline__ void wdecompose(const Dims &d, uint32_t c, int &i, in
 }
 
 
+__device__ __forceinline__ double2 ldcg2(const double *p) { return __ldcg(reinterpret_cast<const double2 *>(p)); }
+
 }  // namespace
 
 template <bool EXACT>
@@ -163,7 +165,51 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveBlocksPerSM) k_wave(Dims d,
             }
             __syncthreads();
             Acc<EXACT> dot[1];
+            const bool vecB = (nr % 2 == 0);   // pairs (i, i+1), i even, never straddle a row
             for (uint32_t c = c0 + 2u * tid; c < c1; c += 2u * kWaveThreads) {
+                if (vecB) {
+                    int i, j, k;
+                    wdecompose(d, c, i, j, k);
+                    const size_t cp = (size_t)c + plane;
+                    const double2 pc = ldcg2(p + cp);
+                    const double2 trv = __ldg(reinterpret_cast<const double2 *>(Tr + c));
+                    const double2 ttl = __ldg(reinterpret_cast<const double2 *>(Tt + c));
+                    const double2 tpl = __ldg(reinterpret_cast<const double2 *>(Tp + c));
+                    const double2 tph = __ldg(reinterpret_cast<const double2 *>(Tp + c + plane));
+                    const double2 pkm = ldcg2(p + cp - plane);
+                    const double2 pkp = ldcg2(p + cp + plane);
+                    const double2 dv = __ldg(reinterpret_cast<const double2 *>(D + c));
+                    const bool jlo = j > 0, jhi = j < nt - 1, ilo = i > 0, ihi = i + 2 < nr;
+                    double2 ptm = make_double2(0.0, 0.0), ptp = ptm, tth = ptm;
+                    if (jlo) ptm = ldcg2(p + cp - nr);
+                    if (jhi) {
+                        ptp = ldcg2(p + cp + nr);
+                        tth = __ldg(reinterpret_cast<const double2 *>(Tt + c + nr));
+                    }
+                    const double pm = ilo ? __ldcg(p + cp - 1) : 0.0;
+                    const double pp2 = ihi ? __ldcg(p + cp + 2) : 0.0;
+                    const double tr2 = ihi ? __ldg(Tr + c + 2) : 0.0;
+                    double s = 0.0;
+                    if (ilo) s = A::acc(s, trv.x, pm);
+                    s = A::acc(s, trv.y, pc.y);
+                    if (jlo) s = A::acc(s, ttl.x, ptm.x);
+                    if (jhi) s = A::acc(s, tth.x, ptp.x);
+                    s = A::acc(s, tpl.x, pkm.x);
+                    s = A::acc(s, tph.x, pkp.x);
+                    const double q0 = A::diag_minus(dv.x, pc.x, s);
+                    s = 0.0;
+                    s = A::acc(s, trv.y, pc.x);
+                    if (ihi) s = A::acc(s, tr2, pp2);
+                    if (jlo) s = A::acc(s, ttl.y, ptm.y);
+                    if (jhi) s = A::acc(s, tth.y, ptp.y);
+                    s = A::acc(s, tpl.y, pkm.y);
+                    s = A::acc(s, tph.y, pkp.y);
+                    const double q1 = A::diag_minus(dv.y, pc.y, s);
+                    *reinterpret_cast<double2 *>(a.q + c) = make_double2(q0, q1);
+                    dot[0].add(pc.x, q0);
+                    dot[0].add(pc.y, q1);
+                    continue;
+                }
                 const int nc = (c + 1 < c1) ? 2 : 1;
                 for (int e = 0; e < nc; ++e) {
                     const uint32_t cc = c + e;
