@@ -12,10 +12,12 @@
 //
 // Scheduling: the slab is cut into tiles of kWaveTile consecutive cells inside a plane (TPP tiles
 // per plane).  Work item u (dispatched in order through an atomic counter) = A on tile u and B on
-// tile u - kLag*TPP, where B visits the planes in the order 1, 2, ..., nloc-1, 0 (plane 0 needs
+// tile u - lag*TPP, where B visits the planes in the order 1, 2, ..., nloc-1, 0 (plane 0 needs
 // plane nloc-1 through the periodic halo).  A B-tile on plane k waits (spin, nanosleep back-off)
 // until all A-tiles of planes k-1, k, k+1 (mod nloc) have been published (store, __threadfence,
-// atomicAdd on the plane's flag); kLag = 3 planes of slack makes the wait rare.  A-tiles never
+// atomicAdd on the plane's flag).  lag = planes in progress across the grid + 2, so waits are rare
+// while the A->B reuse distance (lag planes of traffic, ~30 MB on c3) stays well inside the L2:
+// small tiles (1024 cells) and 2 blocks per SM keep the in-progress window short.  A-tiles never
 // wait, and the grid is exactly the co-resident capacity, so the scheme cannot deadlock.  B reads
 // p through L2 (ld.global.cg) because another SM wrote it.  The p.q partial of every B-tile goes
 // to its own slot and the last block combines the slots in tile order: deterministic.
@@ -30,8 +32,7 @@ namespace maspcg {
 namespace {
 
 constexpr int kWaveThreads = 256;
-constexpr int kWaveBlocksPerSM = 4;
-constexpr int kLag = 3;
+constexpr int kWaveBlocksPerSM = 2;
 
 __device__ __forceinline__ void wdecompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
     const uint32_t row = d.div_r.div(c);
@@ -92,7 +93,8 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveBlocksPerSM) k_wave(Dims d,
     const int nloc = d.nloc, nr = d.nr, nt = d.nt;
     const int tpp = w.tpp;
     const uint32_t ntile = (uint32_t)nloc * tpp;
-    const uint32_t nitems = ntile + (uint32_t)kLag * tpp;
+    const int lag = min(w.lag, nloc);
+    const uint32_t nitems = ntile + (uint32_t)lag * tpp;
     const double *__restrict__ r = a.r;
     const double *__restrict__ D = a.D;
     const double *__restrict__ Tr = a.Tr;
@@ -146,8 +148,8 @@ __global__ void __launch_bounds__(kWaveThreads, kWaveBlocksPerSM) k_wave(Dims d,
             }
         }
         // ---------------- B: q = A p_new on tile b = u - kLag*TPP (planes in the order 1..nloc-1, 0)
-        if (u >= (uint32_t)kLag * tpp) {
-            const uint32_t b = u - (uint32_t)kLag * tpp;
+        if (u >= (uint32_t)lag * tpp) {
+            const uint32_t b = u - (uint32_t)lag * tpp;
             const int ord = (int)(b / tpp);
             const int kB = (ord + 1) % nloc;
             const uint32_t c0 = (uint32_t)kB * plane + (b - (uint32_t)ord * tpp) * (uint32_t)kWaveTile;

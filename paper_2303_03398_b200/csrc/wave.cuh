@@ -7,13 +7,14 @@
 
 namespace maspcg {
 
-constexpr int kWaveTile = 4096;   // cells per tile (contiguous inside one phi-plane)
+constexpr int kWaveTile = 1024;   // cells per tile (contiguous inside one phi-plane)
 
 struct WaveArgs {
     unsigned *counter;        // work-item dispatch counter (reset by the last block)
     unsigned *flags;          // [nloc] A-tiles completed per plane (reset by the last block)
     double *tile_partials;    // [nloc * tpp][2] Dot2 pairs of p.q per B-tile
     int tpp;                  // tiles per plane
+    int lag;                  // B trails A by lag planes (> the planes in progress across the grid)
 };
 
 inline int wave_tiles_per_plane(uint32_t plane) { return (int)((plane + kWaveTile - 1) / kWaveTile); }
