@@ -32,7 +32,7 @@ namespace maspcg {
 namespace {
 
 constexpr int kWaveThreads = 256;
-constexpr int kWaveBlocksPerSM = 2;
+constexpr int kWaveBlocksPerSM = 4;
 
 __device__ __forceinline__ void wdecompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
     const uint32_t row = d.div_r.div(c);
