@@ -356,7 +356,7 @@ maspcg_status enqueue_iteration_wave(maspcg_ctx *c, double *x, cudaStream_t st, 
     w.flags = c->a.wave_flags;
     w.tile_partials = c->a.wave_partials;
     w.tpp = wave_tiles_per_plane(c->d.plane);
-    w.lag = (c->wave_grid + w.tpp - 1) / w.tpp + 2;
+    w.lag = 3;   // measured best on c3 (4096-cell tiles): a longer lag costs more in L2 misses than it saves in waits
     if (tm) CK(c, record_timing(c, 0, 0, it, st));
     launch_wave(c->d, c->a, w, x, c->chunk, c->wave_grid, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 0, 1, it, st));

@@ -7,7 +7,7 @@
 
 namespace maspcg {
 
-constexpr int kWaveTile = 1024;   // cells per tile (contiguous inside one phi-plane)
+constexpr int kWaveTile = 4096;   // cells per tile (contiguous inside one phi-plane)
 
 struct WaveArgs {
     unsigned *counter;        // work-item dispatch counter (reset by the last block)
