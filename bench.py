@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 three kernels, 2 fused two passes, 3 wave")
+    ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch of the loop kernels")
+    ap.add_argument("--kernel-timing", type=int, default=1, help="CUDA events around each hot kernel in the timed region")
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=0, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
@@ -221,6 +223,7 @@ def main():
     S.set_option(maspcg.OPT_ARITH, args.arith)
     S.set_option(maspcg.OPT_TMA, args.tma)
     S.set_option(maspcg.OPT_VEC, args.vec)
+    S.set_option(maspcg.OPT_PDL, args.pdl)
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
 
@@ -249,7 +252,7 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    S.set_option(maspcg.OPT_TIMING, 1)
+    S.set_option(maspcg.OPT_TIMING, args.kernel_timing)
     S.reset_stats()
     if world > 1:
         dist.barrier()

@@ -116,6 +116,8 @@ typedef enum {
     MASPCG_OPT_ARITH = 5,        /* 0 (default): oracle-identical arithmetic -- no FMA contraction, Dot2 (compensated)
                                     dot products (R24); 1: FMA updates and plain tree sums (faster in FP64
                                     issue, parity to the tolerance contract only) */
+    MASPCG_OPT_PDL = 8,          /* 1 (default): programmatic dependent launch of the vector loop kernels (the next
+                                    kernel's blocks are resident before the previous one retires); 0: plain launches */
     MASPCG_OPT_VEC = 7,          /* three-kernel path: 1 (default) two cells per thread with 16-byte loads when nr is
                                     even; 0: one cell per thread */
     MASPCG_OPT_TMA = 6,          /* fused path: 1 (default) stage pass A's streams with TMA bulk copies when nr is

@@ -89,6 +89,7 @@ struct Dims {
     FastDiv div_t;          // / nt
     int periodic_local;     // 1: single rank, halo planes are written by the kernels
     int vec_ok;             // 1: the 16-byte vector kernels may be used (MASPCG_OPT_VEC)
+    int pdl;                // 1: launch the vector loop kernels with programmatic dependent launch
 };
 
 // Device pointers into the workspace.

@@ -26,6 +26,13 @@ namespace maspcg {
 
 namespace {
 
+// Programmatic dependent launch (PDL): the loop kernels are launched with programmatic stream
+// serialisation, so the next kernel's blocks are scheduled onto SMs as this kernel's blocks retire
+// (hiding the launch latency and the reduction tail); griddepcontrol.wait then blocks until the
+// previous grid has completed and its memory is visible, before any dependent data is read.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
 constexpr int kVecBlocks = 4;                   // vector kernels: 4 blocks of 256 threads per SM (<= 64 registers)
 
@@ -415,6 +422,8 @@ template <bool WITH_DOT, bool LOOP, bool EXACT>
 __global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, DevArrays a, double *__restrict__ y,
                                                                       Range rg, unsigned red_slot0,
                                                                       unsigned red_total) {
+    pdl_wait();
+    pdl_trigger();
     if (LOOP && *(volatile int *)&a.sc->done) return;
     using A = Ar<EXACT>;
     const double *__restrict__ p = a.p;
@@ -489,6 +498,8 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, De
 
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, DevArrays a, unsigned total) {
+    pdl_wait();
+    pdl_trigger();
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
@@ -531,6 +542,8 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
 template <bool EXACT>
 __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, DevArrays a, double *__restrict__ x, int chunk,
                                                            unsigned total) {
+    pdl_wait();
+    pdl_trigger();
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
@@ -600,6 +613,21 @@ inline bool use_vec2(const Dims &d, const void *x) {
     return d.vec_ok && (d.nr % 2 == 0) && (((uintptr_t)x & 15) == 0);
 }
 
+template <typename... KArgs, typename... Args>
+void launch_pdl(bool pdl, void (*kern)(KArgs...), unsigned grid, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline unsigned grid_vec2(uint32_t n) {   // n cells, two per thread
     uint64_t g = (n / 2 + kThreads - 1) / kThreads;
     if (g < 1) g = 1;
@@ -667,7 +695,7 @@ void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart par
     const unsigned g = vec ? grid_vec2(rg.vend) : grid_for(rg.vend);
 #define MV(W, L, E)                                                                             \
     do {                                                                                        \
-        if (vec) k_matvec_vec2<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total); \
+        if (vec) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E>, g, st, d, a, y, rg, red_slot0, red_total); \
         else k_matvec_flat<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);     \
     } while (0)
     if (exact) {
@@ -698,8 +726,8 @@ void launch_setup_scalars(const DevArrays &a, double tol, int maxit, cudaStream_
 void launch_update(const Dims &d, const DevArrays &a, bool exact, cudaStream_t st) {
     if (use_vec2(d, nullptr)) {
         const unsigned gv = grid_vec2(d.n);
-        if (exact) k_update_vec2<true><<<gv, kThreads, 0, st>>>(d, a, gv);
-        else k_update_vec2<false><<<gv, kThreads, 0, st>>>(d, a, gv);
+        if (exact) launch_pdl(d.pdl != 0, k_update_vec2<true>, gv, st, d, a, gv);
+        else launch_pdl(d.pdl != 0, k_update_vec2<false>, gv, st, d, a, gv);
         return;
     }
     const unsigned g = grid_for(d.n);
@@ -710,8 +738,8 @@ void launch_update(const Dims &d, const DevArrays &a, bool exact, cudaStream_t s
 void launch_pupdate(const Dims &d, const DevArrays &a, double *x, int chunk, bool exact, cudaStream_t st) {
     if (use_vec2(d, x)) {
         const unsigned gv = grid_vec2(d.n);
-        if (exact) k_pupdate_vec2<true><<<gv, kThreads, 0, st>>>(d, a, x, chunk, gv);
-        else k_pupdate_vec2<false><<<gv, kThreads, 0, st>>>(d, a, x, chunk, gv);
+        if (exact) launch_pdl(d.pdl != 0, k_pupdate_vec2<true>, gv, st, d, a, x, chunk, gv);
+        else launch_pdl(d.pdl != 0, k_pupdate_vec2<false>, gv, st, d, a, x, chunk, gv);
         return;
     }
     const unsigned g = grid_for(d.n);

@@ -213,7 +213,7 @@ bool use_wave(const maspcg_ctx *c) { return c->path_opt == 3 && c->nranks == 1; 
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
-           (use_wave(c) ? 32 : 0);
+           (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -624,6 +624,7 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->d.div_t = make_fastdiv((uint32_t)nt);
     c->d.periodic_local = nranks == 1 ? 1 : 0;
     c->d.vec_ok = 1;
+    c->d.pdl = 1;
     c->fused_bj = fused_bj(nr, nt);   // 0: nr too large for one register batch per thread -> three kernels
     if (c->fused_bj > 0) {
         c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
@@ -974,6 +975,9 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             break;
         case MASPCG_OPT_USE_GRAPHS: c->use_graphs = v ? 1 : 0; break;
         case MASPCG_OPT_TIMING: c->timing = v ? 1 : 0; break;
+        case MASPCG_OPT_PDL:
+            c->d.pdl = v ? 1 : 0;
+            break;
         case MASPCG_OPT_VEC:
             c->d.vec_ok = v ? 1 : 0;
             break;

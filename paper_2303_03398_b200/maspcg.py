@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "E_INVALID", -2: "E_STATE", -3:
                 -4: "E_BREAKDOWN", -5: "E_CUDA", -6: "E_NCCL", -7: "E_NOMEM"}
 BC_DIRICHLET, BC_NEUMANN0 = 0, 1
 MEAN_ARITHMETIC, MEAN_HARMONIC = 0, 1
-OPT_CHUNK, OPT_USE_GRAPHS, OPT_TIMING, OPT_PATH, OPT_ARITH, OPT_TMA, OPT_VEC = 1, 2, 3, 4, 5, 6, 7
+OPT_CHUNK, OPT_USE_GRAPHS, OPT_TIMING, OPT_PATH, OPT_ARITH, OPT_TMA, OPT_VEC, OPT_PDL = 1, 2, 3, 4, 5, 6, 7, 8
 ARITH_EXACT, ARITH_FAST = 0, 1
 PATH_AUTO, PATH_THREE_KERNELS, PATH_FUSED = 0, 1, 2
 

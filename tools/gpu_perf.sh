@@ -5,7 +5,7 @@ TAG=${1:-perf}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
 B="python bench.py --steps 3 --warmup 3 --maxit 300 --no-cpu-baseline --no-e2e"
-for v in "--path 3" "--path 1" "--path 2" "--path 3 --arith 1"; do
+for v in "--path 1" "--path 1 --pdl 0" "--path 1 --kernel-timing 0" "--path 1 --pdl 0 --kernel-timing 0"; do
   echo "== $v" >> gpurun_out/perf_$TAG.txt
   timeout 300 $B $v >> gpurun_out/perf_$TAG.txt 2>&1
 done
