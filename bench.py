@@ -183,7 +183,9 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=8)
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 three kernels, 2 fused two passes, 3 wave")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch of the loop kernels")
-    ap.add_argument("--kernel-timing", type=int, default=1, help="CUDA events around each hot kernel in the timed region")
+    ap.add_argument("--kernel-timing", type=int, default=2,
+                    help="CUDA events around the hot kernels in the timed region: 2 sampled (slot 0 of every "
+                         "graph chunk), 1 every iteration, 0 none")
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=0, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
@@ -285,13 +287,18 @@ def main():
     mv_ms = stats["matvec_ms"] / max(stats["matvec_launches"], 1)
     achieved = st_bpc * ncell_local / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
     traffic, traffic_src = ncu_traffic_per_launch(stats["path"])
-    kern_ms = stats["matvec_ms"] + stats["update_ms"] + stats["pupdate_ms"]
+    # sampled timing: average per launch over the timed launches, times the launches of the run
+    avg = lambda k: stats[k + "_ms"] / stats[k + "_launches"] if stats[k + "_launches"] else 0.0
+    kern_ms = (avg("matvec") + avg("update") + avg("pupdate")) * iters
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": st_name, "path": path["name"],
                 "algorithmic_bytes_per_launch": st_bpc * ncell_local,
                 "avg_launch_ms": mv_ms, "peak_source": peak_src,
-                "share_of_step": stats["matvec_ms"] / ms if ms > 0 else None,
+                "share_of_step": avg("matvec") * iters / ms if ms > 0 else None,
+                "timed_launches": stats["matvec_launches"],
+                "timing": {2: "sampled: every chunk-th iteration (slot 0 of each CUDA-graph chunk)",
+                           1: "every iteration", 0: "off"}[args.kernel_timing],
                 "traffic_source": traffic_src}
 
     def gbps(key, bpc):

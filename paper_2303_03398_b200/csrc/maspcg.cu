@@ -260,6 +260,11 @@ maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
 
 int timing_ev_index(int kern, int which, int it, int chunk) { return (kern * 2 + which) * chunk + it; }
 
+// Timing mode 1: events around every hot kernel of every iteration.  Timing mode 2 (sampled):
+// only in slot 0 of each chunk -- every chunk-th iteration -- so the event records (which serialise
+// the kernels they separate) cost ~1/chunk of their full-timing overhead.
+bool timed_slot(const maspcg_ctx *c, int slot) { return c->timing == 1 || (c->timing == 2 && slot == 0); }
+
 // Record timing event (kern, which) of iteration slot `it` of the current set.  External records so
 // that, inside a stream capture, the graph node records the event at every replay.
 cudaError_t record_timing(maspcg_ctx *c, int kern, int which, int it, cudaStream_t st) {
@@ -269,7 +274,7 @@ cudaError_t record_timing(maspcg_ctx *c, int kern, int which, int it, cudaStream
 
 // One PCG iteration.  it: index within the chunk (timing).
 maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int it) {
-    const bool tm = c->timing != 0;
+    const bool tm = timed_slot(c, it);
     if (tm) CK(c, record_timing(c, 0, 0, it, st));
     RET_IF(stencil_with_halo(c, c->a.q, true, true, st));
     if (tm) CK(c, record_timing(c, 0, 1, it, st));
@@ -287,7 +292,7 @@ maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int i
 // One PCG iteration of the fused two-pass path (fused.cu).  slot: index within the chunk; the
 // chunk length is even so the p buffer parity of a slot is the same in every chunk.
 maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st, int slot) {
-    const bool tm = c->timing != 0;
+    const bool tm = timed_slot(c, slot);
     const int par = (slot + 1) & 1;
     const size_t pl = c->d.plane;
     FusedArgs f{};
@@ -347,7 +352,7 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
 // One PCG iteration of the wave path (wave.cu): the r-update of iteration k, then the p-update of
 // iteration k and the stencil of iteration k+1 in one flag-ordered kernel (single rank).
 maspcg_status enqueue_iteration_wave(maspcg_ctx *c, double *x, cudaStream_t st, int it) {
-    const bool tm = c->timing != 0;
+    const bool tm = timed_slot(c, it);
     if (tm) CK(c, record_timing(c, 1, 0, it, st));
     launch_update(c->d, c->a, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 1, 1, it, st));
@@ -416,6 +421,7 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st, int set) 
 void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
     const size_t base = (size_t)set * 6 * c->chunk;
     for (int it = 0; it < iters_in_chunk; ++it) {
+        if (!timed_slot(c, it)) continue;
         float ms[3];
         for (int k = 0; k < 3; ++k) {
             ms[k] = 0.f;
@@ -453,7 +459,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     RET_IF(ensure_D(c, st));
     const bool fused = use_fused(c);
     if (fused && (c->chunk & 1)) c->chunk += 1;   // even chunks: fixed p-buffer parity per slot
-    if (c->timing) RET_IF(maspcg_set_option(c, MASPCG_OPT_TIMING, 1));   // events for this chunk size
+    if (c->timing) RET_IF(maspcg_set_option(c, MASPCG_OPT_TIMING, c->timing));   // events for this chunk size
 
     // a3: r0 = b - A x0, z0 = r0/D, p0 = z0, dots; then PCG start scalars
     launch_fill_p(c->d, c->a, x, st);
@@ -974,7 +980,10 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             c->chunk = (int)v;
             break;
         case MASPCG_OPT_USE_GRAPHS: c->use_graphs = v ? 1 : 0; break;
-        case MASPCG_OPT_TIMING: c->timing = v ? 1 : 0; break;
+        case MASPCG_OPT_TIMING:
+            if (v < 0 || v > 2) SET_ERR(c, MASPCG_E_INVALID, "timing must be 0, 1 (every iteration) or 2 (sampled)");
+            c->timing = (int)v;
+            break;
         case MASPCG_OPT_PDL:
             c->d.pdl = v ? 1 : 0;
             break;
