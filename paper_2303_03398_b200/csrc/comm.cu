@@ -15,8 +15,12 @@ namespace maspcg {
 // ============================================================== NCCL
 class NcclComm final : public Comm {
    public:
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;        // collectives (all-gather of Dot2 pairs, validation all-reduce)
+    ncclComm_t halo = nullptr;        // point-to-point halo planes: its own communicator (ncclCommSplit), so a
+                                      // halo on the communication stream may overlap a collective on the
+                                      // compute stream without two streams sharing one communicator
     ~NcclComm() override {
+        if (halo) ncclCommDestroy(halo);
         if (comm) ncclCommDestroy(comm);
     }
     bool capturable() const override { return true; }
@@ -32,10 +36,10 @@ class NcclComm final : public Comm {
                     cudaStream_t st, std::string &err) override {
         ncclResult_t r;
         if ((r = ncclGroupStart()) != ncclSuccess) return fail(r, "ncclGroupStart", err);
-        r = ncclSend(first, count, ncclDouble, left(), comm, st);                          // my first plane
-        if (r == ncclSuccess) r = ncclRecv(hi_recv, count, ncclDouble, right(), comm, st);  // right's first
-        if (r == ncclSuccess) r = ncclSend(last, count, ncclDouble, right(), comm, st);     // my last plane
-        if (r == ncclSuccess) r = ncclRecv(lo_recv, count, ncclDouble, left(), comm, st);   // left's last
+        r = ncclSend(first, count, ncclDouble, left(), halo, st);                          // my first plane
+        if (r == ncclSuccess) r = ncclRecv(hi_recv, count, ncclDouble, right(), halo, st);  // right's first
+        if (r == ncclSuccess) r = ncclSend(last, count, ncclDouble, right(), halo, st);     // my last plane
+        if (r == ncclSuccess) r = ncclRecv(lo_recv, count, ncclDouble, left(), halo, st);   // left's last
         ncclResult_t r2 = ncclGroupEnd();
         if (r != ncclSuccess) return fail(r, "halo send/recv", err);
         if (r2 != ncclSuccess) return fail(r2, "ncclGroupEnd", err);
@@ -49,8 +53,8 @@ class NcclComm final : public Comm {
     int shift_right(const double *send, double *recv, size_t count, cudaStream_t st, std::string &err) override {
         ncclResult_t r;
         if ((r = ncclGroupStart()) != ncclSuccess) return fail(r, "ncclGroupStart", err);
-        r = ncclSend(send, count, ncclDouble, right(), comm, st);
-        if (r == ncclSuccess) r = ncclRecv(recv, count, ncclDouble, left(), comm, st);
+        r = ncclSend(send, count, ncclDouble, right(), halo, st);
+        if (r == ncclSuccess) r = ncclRecv(recv, count, ncclDouble, left(), halo, st);
         ncclResult_t r2 = ncclGroupEnd();
         if (r != ncclSuccess) return fail(r, "shift send/recv", err);
         if (r2 != ncclSuccess) return fail(r2, "ncclGroupEnd", err);
@@ -83,6 +87,14 @@ Comm *make_nccl_comm(const void *unique_id, int rank, int nranks, int *status, s
     if (r != ncclSuccess) {
         err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
         c->comm = nullptr;
+        delete c;
+        *status = ST_E_NCCL;
+        return nullptr;
+    }
+    r = ncclCommSplit(c->comm, 0, rank, &c->halo, nullptr);   // collective, same rank order
+    if (r != ncclSuccess) {
+        err = std::string("ncclCommSplit: ") + ncclGetErrorString(r);
+        c->halo = nullptr;
         delete c;
         *status = ST_E_NCCL;
         return nullptr;
