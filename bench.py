@@ -178,6 +178,9 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--chunk", type=int, default=16)
     ap.add_argument("--maxit", type=int, default=None, help="fixed-iteration mode (tol=0), e.g. for ncu")
+    ap.add_argument("--from-fields", action="store_true",
+                    help="assemble the coefficients each step on the device from the cell density (NEXT-1): "
+                         "kappa = nu rho (arithmetic face means), s = rho / dt")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
@@ -220,6 +223,10 @@ def main():
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     kr, kt, kp, s, f, x0 = (T(a) for a in (prob.kr, prob.kt, prob.kp, prob.s, prob.f, prob.x0))
 
+    rho_cells = None
+    if args.from_fields:
+        rc = inputs.midpoints(prob.rf)
+        rho_cells = T(np.broadcast_to(inputs.rho_hydro(rc)[None, None, :], prob.s.shape))
     S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk)
     S.set_option(maspcg.OPT_PATH, args.path)
     S.set_option(maspcg.OPT_ARITH, args.arith)
@@ -236,7 +243,10 @@ def main():
 
     def step():
         S.set_grid(prob.rf, prob.tf, prob.pf)                         # a1
-        S.set_coefficients(kr, kt, kp, s)                             # a2
+        if args.from_fields:                                          # a2 from physical fields (NEXT-1)
+            S.set_coefficients_from_fields(rho_cells, 1e-3, 2, maspcg.MEAN_ARITHMETIC, rho_cells, 1.0 / 1e-2)
+        else:
+            S.set_coefficients(kr, kt, kp, s)                         # a2
         S.set_bc_r(prob.bc_in, None, prob.bc_out, None)
         if warm:
             # the caller's time loop (not the solver path): step 0 solves with the c3-like f from x0;
@@ -366,7 +376,9 @@ def main():
                        "global_cells": nr * nt * np_, "parallelism": f"phi-slab x{world}",
                        "iters_per_solve": iters / args.steps, "chunk": args.chunk,
                        "l2": "no flush: working set ~2.2 GB >> 126 MB L2",
-                       "step": "set_grid + set_coefficients + set_bc_r + solve to tol",
+                       "step": ("set_grid + set_coefficients_from_fields(rho; kappa = 1e-3 rho, s = rho/1e-2) + "
+                                "set_bc_r + solve to tol") if args.from_fields else
+                               "set_grid + set_coefficients + set_bc_r + solve to tol",
                        "arith": "oracle-identical (no FMA, Dot2 dots)" if args.arith == 0 else "fast (FMA, plain sums)"},
             "cell_updates_per_s": nr * nt * np_ * value,
             "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
