@@ -51,6 +51,7 @@ def lib():
             "masoracle_rhs": [i, i, i, d, d, d, d, d, i, d, i, d, d],
             "masoracle_pcg": [i, i, i, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
             "masoracle_face_coefficients": [i, i, i, d, ctypes.c_double, i, i, d, ctypes.c_double, d, d, d, d],
+            "masoracle_rkl2_step": [i, i, i, d, d, d, d, d, d, d, d, ctypes.c_double, i, d],
         }.items():
             fn = getattr(_lib, name)
             fn.argtypes = args
@@ -144,6 +145,20 @@ class Operator:
         if st:
             raise OracleError(st, "rhs")
         return b
+
+    def rkl2_step(self, u, s, tau, stages, g_in=None, g_out=None):
+        """One RKL2 super-time-step of V du/dt = b_D - K u (NEXT-4, reading R26); s = the shift the
+        operator was assembled with (K = A - diag(s V))."""
+        V = volumes(self.rf, self.tf, self.pf)
+        sV = _c(s) * V
+        bD = self.rhs(np.zeros(self.shape), g_in, g_out)
+        u = _c(u)
+        out = np.empty(self.shape)
+        st = lib().masoracle_rkl2_step(self.nr, self.nt, self.np, _p(self.Tr), _p(self.Tt), _p(self.Tp),
+                                       _p(self.D), _p(sV), _p(V), _p(bD), _p(u), float(tau), int(stages), _p(out))
+        if st:
+            raise OracleError(st, "rkl2_step")
+        return out
 
     def pcg(self, b, x0, tol, maxit):
         """Returns (status, x, iters, hist[0..iters], bnorm, rnorm)."""

@@ -468,6 +468,87 @@ done:
     return status;
 }
 
+/* ---------------------------------------------------- super-time-stepping (NEXT-4) */
+
+/* RKL2 coefficients (Meyer, Balsara & Aslam 2014, J. Comput. Phys. 257, eq. 16-17; reading R26):
+ * b_j = (j^2 + j - 2) / (2 j (j + 1)) for j >= 2, b_0 = b_1 = b_2; a_j = 1 - b_j;
+ * w1 = 4 / (s^2 + s - 2); mu~_1 = b_1 w1; for j >= 2:
+ * mu_j = (2j - 1)/j * b_j / b_{j-1}, nu_j = -(j - 1)/j * b_j / b_{j-2}, mu~_j = mu_j w1,
+ * gamma~_j = -a_{j-1} mu~_j.  Evaluated left to right exactly as written.                   */
+static double mo_rkl2_b(int j) {
+    if (j < 2) j = 2;
+    return ((double)j * j + j - 2.0) / (2.0 * j * (j + 1.0));
+}
+
+void masoracle_rkl2_coefficients(int s, int j, double *mu, double *nu, double *mut, double *gat) {
+    double w1 = 4.0 / ((double)s * s + s - 2.0);
+    if (j == 1) {
+        *mu = 1.0; *nu = 0.0; *mut = mo_rkl2_b(1) * w1; *gat = 0.0;
+        return;
+    }
+    double bj = mo_rkl2_b(j), bj1 = mo_rkl2_b(j - 1), bj2 = mo_rkl2_b(j - 2);
+    *mu = (2.0 * j - 1.0) / j * bj / bj1;
+    *nu = -((double)j - 1.0) / j * bj / bj2;
+    *mut = *mu * w1;
+    *gat = -(1.0 - bj1) * *mut;
+}
+
+/* L(u) = (b_D - K u) / V, the explicit form of the diffusion term of the operator (K = A - diag(sV),
+ * b_D the Dirichlet face terms of masoracle_rhs with f = 0):  Ku = (A u) - (s V) u. */
+static void mo_L(int nr, int nt, int np, const double *Tr, const double *Tt, const double *Tp,
+                 const double *D, const double *sV, const double *V, const double *bD, const double *u,
+                 double *y, double *L) {
+    masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, u, y);
+    size_t n = (size_t)nr * nt * np;
+    for (size_t c = 0; c < n; c++) {
+        double Ku = y[c] - sV[c] * u[c];
+        L[c] = (bD[c] - Ku) / V[c];
+    }
+}
+
+/* One RKL2 super-time-step of  V du/dt = b_D - K u  over tau with `stages` >= 2 stages
+ * (reading R26).  sV = s * V (as assembled), V the cell volumes, bD the
+ * Dirichlet terms; u [np][nt][nr] in, out [np][nt][nr] out (may alias u).
+ *   Y0 = u; Y1 = Y0 + (mu~_1 tau) L(Y0);
+ *   Yj = mu_j Y_{j-1} + nu_j Y_{j-2} + (1 - mu_j - nu_j) Y0 + (mu~_j tau) L(Y_{j-1}) + (gamma~_j tau) L(Y0)
+ * (terms added left to right); out = Y_s.                                                     */
+int masoracle_rkl2_step(int nr, int nt, int np, const double *Tr, const double *Tt, const double *Tp,
+                        const double *D, const double *sV, const double *V, const double *bD,
+                        const double *u, double tau, int stages, double *out) {
+    if (stages < 2) return MO_E_INVALID;
+    size_t n = (size_t)nr * nt * np;
+    double *Y0 = malloc(8 * n), *Ya = malloc(8 * n), *Yb = malloc(8 * n), *Yc = malloc(8 * n);
+    double *L0 = malloc(8 * n), *Lj = malloc(8 * n), *y = malloc(8 * n);
+    if (!Y0 || !Ya || !Yb || !Yc || !L0 || !Lj || !y) {
+        free(Y0); free(Ya); free(Yb); free(Yc); free(L0); free(Lj); free(y);
+        return MO_E_NOMEM;
+    }
+    memcpy(Y0, u, 8 * n);
+    mo_L(nr, nt, np, Tr, Tt, Tp, D, sV, V, bD, Y0, y, L0);
+    double mu, nu, mut, gat;
+    masoracle_rkl2_coefficients(stages, 1, &mu, &nu, &mut, &gat);
+    double m1 = mut * tau;
+    for (size_t c = 0; c < n; c++) Ya[c] = Y0[c] + m1 * L0[c];   /* Ya = Y1, Yb = Y0 (= Y_{j-2} at j = 2) */
+    memcpy(Yb, Y0, 8 * n);
+    for (int j = 2; j <= stages; j++) {
+        masoracle_rkl2_coefficients(stages, j, &mu, &nu, &mut, &gat);
+        double w0 = 1.0 - mu - nu, mt = mut * tau, gt = gat * tau;
+        mo_L(nr, nt, np, Tr, Tt, Tp, D, sV, V, bD, Ya, y, Lj);
+        for (size_t c = 0; c < n; c++) {
+            double t = mu * Ya[c];
+            t = t + nu * Yb[c];
+            t = t + w0 * Y0[c];
+            t = t + mt * Lj[c];
+            t = t + gt * L0[c];
+            Yc[c] = t;
+        }
+        double *tmp = Yb; Yb = Ya; Ya = Yc; Yc = tmp;   /* Y_{j-2} <- Y_{j-1}, Y_{j-1} <- Y_j */
+    }
+    memcpy(out, Ya, 8 * n);
+    free(Y0); free(Ya); free(Yb); free(Yc); free(L0); free(Lj); free(y);
+    return MO_OK;
+}
+
 /* Whole pipeline on the global grid: assemble (R3-R10), rhs (R5), PCG (R6,
  * R11-R14).  x holds x0 on entry and the iterate on exit.                  */
 int masoracle_solve(int nr, int nt, int np, const double *rf, const double *tf,

@@ -413,3 +413,75 @@ def test_face_coefficients_means_and_periodic_wrap(oracle_mod):
     assert abs(np.vdot(x, op.apply(y)) - np.vdot(y, op.apply(x))) <= 1e-12 * np.vdot(np.abs(x), np.abs(op.apply(np.abs(y))))
     with pytest.raises(oracle_mod.OracleError):
         oracle_mod.face_coefficients(f, 1.0, 17, 0)
+
+
+# ------------------------------------------------------------------ super-time-stepping (NEXT-4, R26)
+def _dense_K_over_V(oracle_mod, op, s):
+    """M = V^{-1} K with K = A - diag(sV) (A from the oracle's apply, column by column)."""
+    A = dense(op)
+    V = oracle_mod.volumes(op.rf, op.tf, op.pf).ravel()
+    K = A - np.diag(s.ravel() * V)
+    return K / V[:, None], V
+
+
+def test_rkl2_preserves_steady_states(oracle_mod):
+    """u = const with Neumann walls (L u = 0), and u = c with Dirichlet g = c on both walls (K u = b_D):
+    the RKL2 step returns u up to rounding."""
+    p = inputs.random_problem(6, 5, 8, 71, bc_in=1, bc_out=1)
+    op = op_from(oracle_mod, p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, 1, 1)
+    M, V = _dense_K_over_V(oracle_mod, op, p.s)
+    tau = 0.9 * (7 * 7 + 7 - 2) / 4.0 * 2.0 / np.linalg.eigvals(M).real.max()   # inside the stability bound
+    u = np.full(op.shape, 1.7)
+    out = op.rkl2_step(u, p.s, tau, 7)
+    assert np.abs(out - u).max() <= 1e-13 * 1.7
+    p = inputs.random_problem(6, 5, 8, 72, shift=False, bc_in=0, bc_out=0)
+    op = op_from(oracle_mod, p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, 0, 0)
+    M, V = _dense_K_over_V(oracle_mod, op, p.s)
+    tau = 0.9 * (5 * 5 + 5 - 2) / 4.0 * 2.0 / np.linalg.eigvals(M).real.max()
+    g = np.full((8, 5), 2.5)
+    out = op.rkl2_step(np.full(op.shape, 2.5), p.s, tau, 5, g, g)
+    assert np.abs(out - 2.5).max() <= 1e-13 * 2.5
+
+
+def test_rkl2_second_order_against_matrix_exponential(oracle_mod):
+    """V du/dt = -K u (Neumann walls): RKL2 with s = 6 stages converges to expm(-T V^-1 K) u0 at
+    second order in tau (errors fall ~4x per halving)."""
+    import scipy.linalg
+    p = inputs.random_problem(4, 4, 8, 73, bc_in=1, bc_out=1)
+    op = op_from(oracle_mod, p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, 1, 1)
+    M, V = _dense_K_over_V(oracle_mod, op, p.s)
+    u0 = np.random.default_rng(4).standard_normal(op.shape)
+    lam = np.abs(np.linalg.eigvals(M)).max()
+    T = 4.0 / lam
+    exact = (scipy.linalg.expm(-T * M) @ u0.ravel()).reshape(op.shape)
+    errs = []
+    for m in (8, 16, 32):
+        u = u0.copy()
+        for _ in range(m):
+            u = op.rkl2_step(u, p.s, T / m, 6)
+        errs.append(np.abs(u - exact).max())
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert all(1.8 < o < 2.3 for o in orders), (errs, orders)
+
+
+def test_rkl2_stable_up_to_its_bound(oracle_mod):
+    """tau = 0.99 (s^2 + s - 2)/4 * dt_FE (dt_FE = 2 / lambda_max of V^-1 K): 30 steps of a random
+    initial state never increase the V-weighted energy (RKL2 is stable up to that bound), while a
+    forward-Euler-sized step times 1.3 * (s^2+s-2)/4 blows up."""
+    p = inputs.random_problem(5, 4, 6, 74, bc_in=1, bc_out=1)
+    op = op_from(oracle_mod, p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, 1, 1)
+    M, V = _dense_K_over_V(oracle_mod, op, p.s)
+    lam = np.linalg.eigvals(M).real.max()
+    s = 8
+    bound = (s * s + s - 2) / 4.0 * 2.0 / lam
+    u = np.random.default_rng(5).standard_normal(op.shape)
+    energy = lambda v: float((V * v.ravel() ** 2).sum())
+    e0 = energy(u)
+    for _ in range(30):
+        u = op.rkl2_step(u, p.s, 0.99 * bound, s)
+        assert energy(u) <= e0 * (1 + 1e-12)
+        e0 = energy(u)
+    v = np.random.default_rng(6).standard_normal(op.shape)
+    for _ in range(30):
+        v = op.rkl2_step(v, p.s, 1.3 * bound, s)
+    assert energy(v) > 1e3 * energy(np.random.default_rng(6).standard_normal(op.shape))
