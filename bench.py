@@ -181,6 +181,8 @@ def main():
     ap.add_argument("--from-fields", action="store_true",
                     help="assemble the coefficients each step on the device from the cell density (NEXT-1): "
                          "kappa = nu rho (arithmetic face means), s = rho / dt")
+    ap.add_argument("--sts-stages", type=int, default=0,
+                    help="also time RKL2 super-time-steps with this many stages (NEXT-4), 0 = off")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
@@ -356,6 +358,26 @@ def main():
         e2e = {"value": it_h / th, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": 1e3 * th / args.steps, "api": "maspcg_set_coefficients_host + maspcg_solve_host"}
 
+    # ---- explicit super-time-stepping of the same operator (NEXT-4): stage throughput
+    sts = None
+    if args.sts_stages >= 2:
+        dt_fe = S.sts_dt_limit()
+        ns = args.sts_stages
+        tau = 0.9 * (ns * ns + ns - 2) / 4.0 * dt_fe
+        u = x0.clone()
+        S.sts_step(u, tau, ns)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            S.sts_step(u, tau, ns)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sms = e0.elapsed_time(e1) / args.steps
+        stage_ms = sms / ns
+        sts = {"stages": ns, "tau_over_dt_fe": tau / dt_fe, "ms_per_step": sms, "stages_per_s": 1e3 / stage_ms,
+               "stage_GBps": 80 * ncell_local / (stage_ms * 1e-3) / 1e9, "bytes_per_cell_per_stage": 80}
+
     # ---- CPU baseline: the oracle as it stands on this box's host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -381,7 +403,7 @@ def main():
                                "set_grid + set_coefficients + set_bc_r + solve to tol",
                        "arith": "oracle-identical (no FMA, Dot2 dots)" if args.arith == 0 else "fast (FMA, plain sums)"},
             "cell_updates_per_s": nr * nt * np_ * value,
-            "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "sts": sts,
             "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

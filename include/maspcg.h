@@ -247,6 +247,19 @@ MASPCG_API maspcg_status maspcg_solve_host(maspcg_ctx *ctx, const double *rhs, d
                                            double tol, int maxit, double *resid_hist,
                                            maspcg_info *info, void *cuda_stream);
 
+/* ---- explicit super-time-stepping of the same parabolic term (R26) ---- */
+
+/* One RKL2 super-time-step (Meyer, Balsara & Aslam 2014) of the semi-discrete diffusion equation
+ *   V du/dt = b_D - K u,   K = A - diag(s V)  (the operator of set_coefficients / set_bc_r without
+ *   its shift; b_D the Dirichlet face terms),
+ * over tau with `stages` (2..4096) stages, in place on u (DEVICE [nloc][nt][nr]).  Stable for
+ * tau <= (stages^2 + stages - 2) / 4 * dt_fe (maspcg_sts_dt_limit).  No dot products, one halo
+ * exchange per stage (P > 1).  E_INVALID for bad arguments, E_STATE before coefficients / BCs. */
+MASPCG_API maspcg_status maspcg_sts_step(maspcg_ctx *ctx, double *u, double tau, int stages, void *cuda_stream);
+/* dt_fe = 2 / max_c (K_cc + sum_f T_f) / V_c: the Gershgorin bound of the forward-Euler limit of
+ * the explicit step (global over ranks; HOST output; synchronises the stream). */
+MASPCG_API maspcg_status maspcg_sts_dt_limit(maspcg_ctx *ctx, double *dt_fe, void *cuda_stream);
+
 /* y = A x on the local slab (DEVICE [nloc][nt][nr] each; halo exchanged
  * internally; x and y must not alias).  For tests and operator checks. */
 MASPCG_API maspcg_status maspcg_apply(maspcg_ctx *ctx, const double *x, double *y,

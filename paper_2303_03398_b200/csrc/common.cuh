@@ -127,6 +127,9 @@ struct DevArrays {
     double *P[2];       // [nloc][nt][nr] search directions of even / odd iterations
     double *rh, *dh, *ph;   // [2][nt][nr] received halo planes (lo, hi) of r, D, p_old (nranks > 1)
     double *fh;             // [2][nt][nr] received halo planes of a physical field (from_fields, nranks > 1)
+    // super-time-stepping (NEXT-4)
+    double *sy[4];          // [nloc+2][nt][nr] x4: three rotating RKL2 stages and Y0
+    double *sl0;            // [nloc][nt][nr]   L(Y0)
     // wave path (wave.cu)
     unsigned *wave_counter; // work-item counter
     unsigned *wave_flags;   // [nloc] completed A-tiles per plane

@@ -601,6 +601,95 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
     }
 }
 
+// ---------------------------------------------------------------- super-time-stepping (NEXT-4, R26)
+// L(u) = (b_D - K u) / V with K u = (A u) - (s V) u, A u summed exactly like the stencil kernels.
+template <bool EXACT>
+__device__ __forceinline__ double sts_L(const Dims &d, const DevArrays &a, const double *__restrict__ u, uint32_t c,
+                                        int din, int dout) {
+    using A = Ar<EXACT>;
+    int i, j, k;
+    decompose(d, c, i, j, k);
+    const size_t plane = d.plane, cp = (size_t)c + plane;
+    const double pc = u[cp];
+    double s = 0.0;
+    if (i > 0) s = A::acc(s, a.Tr[c], u[cp - 1]);
+    if (i < d.nr - 1) s = A::acc(s, a.Tr[c + 1], u[cp + 1]);
+    if (j > 0) s = A::acc(s, a.Tt[c], u[cp - d.nr]);
+    if (j < d.nt - 1) s = A::acc(s, a.Tt[c + d.nr], u[cp + d.nr]);
+    s = A::acc(s, a.Tp[c], u[cp - plane]);
+    s = A::acc(s, a.Tp[c + plane], u[cp + plane]);
+    const double y = A::diag_minus(a.D[c], pc, s);
+    const double Ku = __dsub_rn(y, __dmul_rn(a.sV[c], pc));
+    const uint32_t row = (uint32_t)k * d.nt + j;
+    double b = 0.0;
+    if (din && i == 0) b = __dadd_rn(b, __dmul_rn(a.Tr[c], a.gin[row]));
+    if (dout && i == d.nr - 1) b = __dadd_rn(b, __dmul_rn(a.TrB[row], a.gout[row]));
+    const double V = __dmul_rn(__dmul_rn(a.R3[i], a.C[j]), a.dp[k]);
+    return __ddiv_rn(__dsub_rn(b, Ku), V);
+}
+
+// stage 1: L0 = L(Y0); Y1 = Y0 + (mu~_1 tau) L0 (into a padded buffer, periodic copies on one rank)
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads) k_sts_first(Dims d, DevArrays a, const double *__restrict__ y0p,
+                                                        double *__restrict__ l0, double *__restrict__ y1p,
+                                                        double m1, int din, int dout) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        const double L = sts_L<EXACT>(d, a, y0p, c, din, dout);
+        l0[c] = L;
+        store_p(d, y1p, c, __dadd_rn(y0p[(size_t)c + d.plane], __dmul_rn(m1, L)));
+    }
+}
+
+// stage j >= 2: Yj = mu Y_{j-1} + nu Y_{j-2} + w0 Y0 + mt L(Y_{j-1}) + gt L0, added left to right
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads) k_sts_stage(Dims d, DevArrays a, const double *__restrict__ yj1p,
+                                                        const double *__restrict__ yj2p,
+                                                        const double *__restrict__ y0p,
+                                                        const double *__restrict__ l0, double *__restrict__ yjp,
+                                                        double mu, double nu, double w0, double mt, double gt,
+                                                        int din, int dout) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const size_t plane = d.plane;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        const double L = sts_L<EXACT>(d, a, yj1p, c, din, dout);
+        double t = __dmul_rn(mu, yj1p[(size_t)c + plane]);
+        t = __dadd_rn(t, __dmul_rn(nu, yj2p[(size_t)c + plane]));
+        t = __dadd_rn(t, __dmul_rn(w0, y0p[(size_t)c + plane]));
+        t = __dadd_rn(t, __dmul_rn(mt, L));
+        t = __dadd_rn(t, __dmul_rn(gt, l0[c]));
+        store_p(d, yjp, c, t);
+    }
+}
+
+// Gershgorin bound of lambda_max(V^-1 K): max_c (K_cc + sum_f T_f) / V_c, block maxima -> out[block]
+__global__ void __launch_bounds__(kThreads) k_sts_gershgorin(Dims d, DevArrays a, double *out) {
+    double m = 0.0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        double off = 0.0;
+        if (i > 0) off += a.Tr[c];
+        if (i < d.nr - 1) off += a.Tr[c + 1];
+        if (j > 0) off += a.Tt[c];
+        if (j < d.nt - 1) off += a.Tt[c + d.nr];
+        off += a.Tp[c] + a.Tp[(size_t)c + d.plane];
+        const double kdiag = a.D[c] - a.sV[c];
+        const double V = __dmul_rn(__dmul_rn(a.R3[i], a.C[j]), a.dp[k]);
+        m = fmax(m, (kdiag + off) / V);
+    }
+    __shared__ double sm[kThreads / 32];
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) v = fmax(v, sm[w]);
+        out[blockIdx.x] = v;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_zero_x_if(Dims d, DevArrays a, double *__restrict__ x) {
     if (!a.sc->zero_x) return;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -770,6 +859,27 @@ __global__ void k_dd_combine(const double *gather, int nranks, int npairs, doubl
 
 void launch_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact, cudaStream_t st) {
     k_dd_combine<<<1, 32, 0, st>>>(gather, nranks, npairs, out, exact);
+}
+
+void launch_sts_first(const Dims &d, const DevArrays &a, const double *y0p, double *l0, double *y1p, double m1,
+                      int din, int dout, bool exact, cudaStream_t st) {
+    const unsigned g = grid_for(d.n);
+    if (exact) k_sts_first<true><<<g, kThreads, 0, st>>>(d, a, y0p, l0, y1p, m1, din, dout);
+    else k_sts_first<false><<<g, kThreads, 0, st>>>(d, a, y0p, l0, y1p, m1, din, dout);
+}
+
+void launch_sts_stage(const Dims &d, const DevArrays &a, const double *yj1p, const double *yj2p, const double *y0p,
+                      const double *l0, double *yjp, double mu, double nu, double w0, double mt, double gt, int din,
+                      int dout, bool exact, cudaStream_t st) {
+    const unsigned g = grid_for(d.n);
+    if (exact) k_sts_stage<true><<<g, kThreads, 0, st>>>(d, a, yj1p, yj2p, y0p, l0, yjp, mu, nu, w0, mt, gt, din, dout);
+    else k_sts_stage<false><<<g, kThreads, 0, st>>>(d, a, yj1p, yj2p, y0p, l0, yjp, mu, nu, w0, mt, gt, din, dout);
+}
+
+unsigned launch_sts_gershgorin(const Dims &d, const DevArrays &a, double *out, cudaStream_t st) {
+    const unsigned g = grid_for(d.n);
+    k_sts_gershgorin<<<g, kThreads, 0, st>>>(d, a, out);
+    return g;
 }
 
 void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st) {

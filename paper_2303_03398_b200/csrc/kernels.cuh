@@ -34,6 +34,14 @@ void launch_update(const Dims &d, const DevArrays &a, bool exact, cudaStream_t s
 void launch_pupdate(const Dims &d, const DevArrays &a, double *x, int chunk, bool exact, cudaStream_t st);
 // out[2t..2t+1] = rank-ordered Dot2 combination of gather[r][2t..2t+1], t < npairs.
 void launch_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact, cudaStream_t st);
+// RKL2 super-time-stepping stages (NEXT-4, R26); *p arguments are padded [nloc+2][nt][nr] arrays.
+void launch_sts_first(const Dims &d, const DevArrays &a, const double *y0p, double *l0, double *y1p, double m1,
+                      int din, int dout, bool exact, cudaStream_t st);
+void launch_sts_stage(const Dims &d, const DevArrays &a, const double *yj1p, const double *yj2p, const double *y0p,
+                      const double *l0, double *yjp, double mu, double nu, double w0, double mt, double gt, int din,
+                      int dout, bool exact, cudaStream_t st);
+// per-block maxima of the Gershgorin bound of lambda_max(V^-1 K) into out[0..blocks); returns blocks
+unsigned launch_sts_gershgorin(const Dims &d, const DevArrays &a, double *out, cudaStream_t st);
 void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st);
 
 }  // namespace maspcg

@@ -128,6 +128,8 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     t.dh = (double *)take(8 * 2 * plane);
     t.ph = (double *)take(8 * 2 * plane);
     t.fh = (double *)take(8 * 2 * plane);
+    for (int b = 0; b < 4; ++b) t.sy[b] = (double *)take(8 * (n + 2 * plane));   // STS: Y0 and 3 rotating stages
+    t.sl0 = (double *)take(8 * n);
     const size_t tpp = (size_t)wave_tiles_per_plane((uint32_t)plane);
     t.wave_counter = (unsigned *)take(256);
     t.wave_flags = (unsigned *)take(4 * (size_t)c->nloc);
@@ -937,6 +939,93 @@ maspcg_status maspcg_apply(maspcg_ctx *c, const double *x, double *y, void *stre
     RET_IF(stencil_with_halo(c, y, false, false, st));
     CK(c, cudaGetLastError());
     c->stats.kernel_launches += 2 + (c->nranks > 1 ? 1 : 0);
+    return MASPCG_OK;
+}
+
+// RKL2 coefficients (Meyer, Balsara & Aslam 2014; R26), the same formulas in the same order as the
+// oracle's: b_j = (j^2 + j - 2) / (2 j (j + 1)) (b_0 = b_1 = b_2), w1 = 4 / (s^2 + s - 2), ...
+static double rkl2_b(int j) {
+    if (j < 2) j = 2;
+    return ((double)j * j + j - 2.0) / (2.0 * j * (j + 1.0));
+}
+static void rkl2_coefficients(int s, int j, double *mu, double *nu, double *mut, double *gat) {
+    const double w1 = 4.0 / ((double)s * s + s - 2.0);
+    if (j == 1) {
+        *mu = 1.0;
+        *nu = 0.0;
+        *mut = rkl2_b(1) * w1;
+        *gat = 0.0;
+        return;
+    }
+    const double bj = rkl2_b(j), bj1 = rkl2_b(j - 1), bj2 = rkl2_b(j - 2);
+    *mu = (2.0 * j - 1.0) / j * bj / bj1;
+    *nu = -((double)j - 1.0) / j * bj / bj2;
+    *mut = *mu * w1;
+    *gat = -(1.0 - bj1) * *mut;
+}
+
+maspcg_status maspcg_sts_step(maspcg_ctx *c, double *u, double tau, int stages, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!u) SET_ERR(c, MASPCG_E_INVALID, "u must be non-NULL");
+    if (stages < 2 || stages > 4096) SET_ERR(c, MASPCG_E_INVALID, "stages must be in [2, 4096]");
+    if (!(tau > 0.0) || !std::isfinite(tau)) SET_ERR(c, MASPCG_E_INVALID, "tau must be finite and > 0");
+    if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_D(c, st));
+    const bool ex = exact_arith(c);
+    const int din = c->bc_in == BC_DIRICHLET && c->has_gin, dout = c->bc_out == BC_DIRICHLET && c->has_gout;
+    DevArrays y0 = c->a;
+    y0.p = c->a.sy[3];
+    launch_fill_p(c->d, y0, u, st);                     // Y0 (padded, periodic copies on one rank)
+    if (c->nranks > 1) RET_IF(halo_padded(c, c->a.sy[3], st));
+    double mu, nu, mut, gat;
+    rkl2_coefficients(stages, 1, &mu, &nu, &mut, &gat);
+    launch_sts_first(c->d, c->a, c->a.sy[3], c->a.sl0, c->a.sy[0], mut * tau, din, dout, ex, st);
+    if (c->nranks > 1) RET_IF(halo_padded(c, c->a.sy[0], st));
+    const double *yj2 = c->a.sy[3], *yj1 = c->a.sy[0];
+    int next = 1;
+    for (int j = 2; j <= stages; ++j) {
+        rkl2_coefficients(stages, j, &mu, &nu, &mut, &gat);
+        const double w0 = 1.0 - mu - nu;
+        double *out = c->a.sy[next];
+        launch_sts_stage(c->d, c->a, yj1, yj2, c->a.sy[3], c->a.sl0, out, mu, nu, w0, mut * tau, gat * tau, din, dout,
+                         ex, st);
+        if (c->nranks > 1) RET_IF(halo_padded(c, out, st));
+        yj2 = yj1;
+        yj1 = out;
+        next = (next + 1) % 3;
+    }
+    CK(c, cudaGetLastError());
+    const size_t n = (size_t)c->nloc * c->nt * c->nr;
+    CK(c, cudaMemcpyAsync(u, yj1 + c->d.plane, 8 * n, cudaMemcpyDeviceToDevice, st));
+    c->stats.kernel_launches += 1 + stages;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_sts_dt_limit(maspcg_ctx *c, double *dt_fe, void *stream) {
+    if (!c || !dt_fe) return MASPCG_E_INVALID;
+    if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_D(c, st));
+    const unsigned g = launch_sts_gershgorin(c->d, c->a, c->a.partials, st);
+    CK(c, cudaGetLastError());
+    std::vector<double> h(g);
+    CK(c, cudaMemcpyAsync(h.data(), c->a.partials, 8 * g, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    double m = 0.0;
+    for (double v : h) m = std::fmax(m, v);
+    if (c->nranks > 1) {
+        CK(c, cudaMemcpyAsync(c->a.partials, &m, 8, cudaMemcpyHostToDevice, st));
+        COMM(c, c->comm->allgather(c->a.partials, c->a.gather, 1, st, c->err));
+        std::vector<double> all(c->nranks);
+        CK(c, cudaMemcpyAsync(all.data(), c->a.gather, 8 * c->nranks, cudaMemcpyDeviceToHost, st));
+        CK(c, cudaStreamSynchronize(st));
+        for (double v : all) m = std::fmax(m, v);
+    }
+    if (!(m > 0.0)) SET_ERR(c, MASPCG_E_INVALID, "no diffusion coupling: the explicit step is unbounded");
+    *dt_fe = 2.0 / m;
     return MASPCG_OK;
 }
 

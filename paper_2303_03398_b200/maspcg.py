@@ -73,6 +73,8 @@ SIGNATURES = {
     "maspcg_solve": ([_V, _V, _V, _D, _I, _V, ctypes.POINTER(Info), _V], _I),
     "maspcg_solve_host": ([_V, _V, _V, _D, _I, _V, ctypes.POINTER(Info), _V], _I),
     "maspcg_apply": ([_V, _V, _V, _V], _I),
+    "maspcg_sts_step": ([_V, _V, _D, _I, _V], _I),
+    "maspcg_sts_dt_limit": ([_V, ctypes.POINTER(_D), _V], _I),
     "maspcg_get_operator": ([_V, _V, _V, _V, _V, _V], _I),
     "maspcg_set_option": ([_V, _I, ctypes.c_longlong], _I),
     "maspcg_get_stats": ([_V, ctypes.POINTER(Stats)], _I),
@@ -257,6 +259,17 @@ class Solver:
             y = torch.empty_like(x)
         self._check(self._L.maspcg_apply(self.ctx, _ptr(x), _ptr(y), _stream(stream)))
         return y
+
+    def sts_step(self, u, tau: float, stages: int, stream=None):
+        """maspcg_sts_step: one RKL2 super-time-step of V du/dt = b_D - K u, in place on u."""
+        self._check(self._L.maspcg_sts_step(self.ctx, _ptr(u), float(tau), int(stages), _stream(stream)))
+        return u
+
+    def sts_dt_limit(self, stream=None) -> float:
+        """maspcg_sts_dt_limit: the forward-Euler step bound 2 / max_c (K_cc + sum T)/V_c."""
+        v = ctypes.c_double()
+        self._check(self._L.maspcg_sts_dt_limit(self.ctx, ctypes.byref(v), _stream(stream)))
+        return v.value
 
     def get_operator(self, stream=None):
         nloc, nt, nr = self.local_shape

@@ -185,3 +185,33 @@ def test_multirank_coefficients_from_fields(M, oracle_mod, P):
         sl = slice(k0, k0 + nloc)
         assert np.array_equal(Tr, op.Tr[sl]) and np.array_equal(Tt, op.Tt[sl])
         assert np.array_equal(Tp, op.Tp[sl]) and np.array_equal(D, op.D[sl])
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_multirank_sts_step(M, oracle_mod, P):
+    """RKL2 stages across ranks (one halo exchange per stage): bitwise equal to the oracle."""
+    import torch
+    fn = lambda k0, n: inputs.random_problem(10, 6, 8, 44, bc_in=0, bc_out=1, k0=k0 or 0, nloc=n)
+    full = fn(None, None)
+    u0 = np.random.default_rng(P).standard_normal((full.np, full.nt, full.nr))
+    op = oracle_mod.Operator(full.rf, full.tf, full.pf, full.kr, full.kt, full.kp, full.s, full.bc_in, full.bc_out)
+
+    def rank(r, g):
+        p = slab_of(fn, P, r)
+        S = M.solver_for_problem(p, loopback=(g, r))
+        dt = S.sts_dt_limit()
+        u = torch.from_numpy(u0[p.k0:p.k0 + p.nloc].copy()).cuda()
+        for _ in range(2):
+            S.sts_step(u, 0.8 * 20 * dt, 5)
+        out = (dt, u.cpu().numpy())
+        S.close()
+        return out
+
+    res = run_ranks(M, P, rank)
+    dts = {r[0] for r in res}
+    assert len(dts) == 1
+    dt = dts.pop()
+    uo = u0.copy()
+    for _ in range(2):
+        uo = op.rkl2_step(uo, full.s, 0.8 * 20 * dt, 5, full.g_in, full.g_out)
+    assert np.array_equal(np.concatenate([r[1] for r in res], axis=0), uo)

@@ -427,3 +427,32 @@ def test_nonlinear_conduction_time_loop_exact(torch_cuda, M, oracle_mod):
         assert st == ost == 0 and info["iters"] == oit
         assert np.array_equal(Tg.cpu().numpy(), ox) and np.array_equal(hist, ohist)
         To = ox
+
+
+@pytest.mark.parametrize("bc,stages", [((1, 1), 6), ((0, 1), 10), ((0, 0), 3)])
+def test_sts_step_bitwise(torch_cuda, M, oracle_mod, bc, stages):
+    """maspcg_sts_step (NEXT-4): RKL2 super-time-steps of V du/dt = b_D - K u equal the oracle's bit for
+    bit; maspcg_sts_dt_limit is a valid forward-Euler bound (dt * lambda_max(V^-1 K) <= 2)."""
+    torch = torch_cuda
+    p = inputs.random_problem(12, 7, 8, 600 + stages, bc_in=bc[0], bc_out=bc[1])
+    S = M.solver_for_problem(p)
+    dt = S.sts_dt_limit()
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, *bc)
+    n = p.np * p.nt * p.nr
+    A = np.empty((n, n))
+    for c in range(n):
+        e = np.zeros(n)
+        e[c] = 1.0
+        A[:, c] = op.apply(e.reshape(op.shape)).ravel()
+    V = oracle_mod.volumes(p.rf, p.tf, p.pf).ravel()
+    lam = np.linalg.eigvals((A - np.diag(p.s.ravel() * V)) / V[:, None]).real.max()
+    assert dt * lam <= 2.0 * (1 + 1e-12) and dt * lam > 0.2
+    tau = 0.9 * (stages * stages + stages - 2) / 4.0 * dt
+    u0 = np.random.default_rng(stages).standard_normal(op.shape)
+    ug = dev(torch, u0)
+    uo = u0.copy()
+    for _ in range(3):
+        S.sts_step(ug, tau, stages)
+        uo = op.rkl2_step(uo, p.s, tau, stages, p.g_in, p.g_out)
+    torch.cuda.synchronize()
+    assert np.array_equal(ug.cpu().numpy(), uo)

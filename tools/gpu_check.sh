@@ -12,7 +12,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 timeout 600 python bench.py --path 2 --no-cpu-baseline --no-e2e > gpurun_out/bench_path2_$TAG.json 2>> gpurun_out/bench_$TAG.err
 timeout 600 python bench.py --arith 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_fast_$TAG.json 2>> gpurun_out/bench_$TAG.err
-timeout 600 python bench.py --path 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_path3_$TAG.json 2>> gpurun_out/bench_$TAG.err
+timeout 600 python bench.py --path 3 --no-cpu-baseline --no-e2e --sts-stages 10 > gpurun_out/bench_path3_$TAG.json 2>> gpurun_out/bench_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 1 --warmup 0 --maxit 30 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_bench_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_matvec_vec2|k_update_vec2|k_pupdate_vec2" -s 4 -c 3 \
