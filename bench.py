@@ -183,6 +183,8 @@ def main():
                          "kappa = nu rho (arithmetic face means), s = rho / dt")
     ap.add_argument("--sts-stages", type=int, default=0,
                     help="also time RKL2 super-time-steps with this many stages (NEXT-4), 0 = off")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="N=1 with a one-rank NCCL communicator (the multi-rank code path, halos to itself)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
@@ -229,7 +231,8 @@ def main():
     if args.from_fields:
         rc = inputs.midpoints(prob.rf)
         rho_cells = T(np.broadcast_to(inputs.rho_hydro(rc)[None, None, :], prob.s.shape))
-    S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk)
+    S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk,
+                      force_comm=args.force_comm)
     S.set_option(maspcg.OPT_PATH, args.path)
     S.set_option(maspcg.OPT_ARITH, args.arith)
     S.set_option(maspcg.OPT_TMA, args.tma)
@@ -395,7 +398,8 @@ def main():
             "data": "synthetic (seeded generators, paper_2303_03398_b200/inputs.py; SURVEY 8(d) recipe)",
             "config": {"workload": f"{args.config} {nr}x{nt}x{np_} coronal viscosity solve "
                                    f"(BASELINE.json configs[2]), tol={tol:g}, Jacobi-PCG fp64",
-                       "global_cells": nr * nt * np_, "parallelism": f"phi-slab x{world}",
+                       "global_cells": nr * nt * np_,
+                       "parallelism": f"phi-slab x{world}" + (" (one-rank NCCL communicator)" if args.force_comm else ""),
                        "iters_per_solve": iters / args.steps, "chunk": args.chunk,
                        "l2": "no flush: working set ~2.2 GB >> 126 MB L2",
                        "step": ("set_grid + set_coefficients_from_fields(rho; kappa = 1e-3 rho, s = rho/1e-2) + "

@@ -143,8 +143,11 @@ MASPCG_API maspcg_status maspcg_get_unique_id(void *out);
 /* Create a context for rank `rank` of `nranks` on CUDA device `cuda_device`.
  * nr, nt, np: GLOBAL cell counts (>= 1; np % nranks == 0; the local slab must
  * hold < 2^31 cells including two halo planes).  nccl_unique_id: the 128
- * bytes from maspcg_get_unique_id, or NULL iff nranks == 1.  Collective over
- * all ranks when nranks > 1 (ncclCommInitRank).  *out receives the context. */
+ * bytes from maspcg_get_unique_id; required when nranks > 1.  With nranks == 1
+ * it may be NULL (no communicator: the periodic phi wrap is a local copy) or an
+ * id (a one-rank NCCL communicator: the multi-rank code path, halos sent to
+ * itself -- used to exercise NCCL on a single GPU).  Collective over all ranks
+ * when an id is given (ncclCommInitRank).  *out receives the context. */
 MASPCG_API maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks,
                                        const void *nccl_unique_id, int cuda_device,
                                        maspcg_ctx **out);

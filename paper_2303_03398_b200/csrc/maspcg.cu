@@ -38,7 +38,7 @@ thread_local std::string g_create_error;
 struct maspcg_ctx {
     int nr = 0, nt = 0, np = 0, rank = 0, nranks = 1, device = 0;
     int k0 = 0, nloc = 0;
-    Comm *comm = nullptr;            // nullptr when nranks == 1
+    Comm *comm = nullptr;            // nullptr: one rank, periodic wrap done locally
     std::string err;
 
     // grid (host copies of the 1-D metric)
@@ -211,7 +211,7 @@ maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaSt
 }
 
 bool use_fused(const maspcg_ctx *c) { return c->path_opt == 2 && c->fused_bj > 0; }
-bool use_wave(const maspcg_ctx *c) { return c->path_opt == 3 && c->nranks == 1; }
+bool use_wave(const maspcg_ctx *c) { return c->path_opt == 3 && !c->comm; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
@@ -221,7 +221,7 @@ int graph_key(const maspcg_ctx *c) {
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
 // order with the same error-free arithmetic (identical bits on every rank).
 maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStream_t st) {
-    if (c->nranks == 1) return MASPCG_OK;
+    if (!c->comm) return MASPCG_OK;
     COMM(c, c->comm->allgather(pairs, c->a.gather, 2 * npairs, st, c->err));
     launch_dd_combine(c->a.gather, c->nranks, npairs, pairs, exact_arith(c), st);
     return MASPCG_OK;
@@ -230,7 +230,7 @@ maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStrea
 // Halo exchange of p (P > 1) overlapped with the interior of the stencil on
 // the caller's stream; joins before the boundary planes.
 maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st) {
-    if (c->nranks == 1) {
+    if (!c->comm) {
         launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
                       stencil_blocks(c->d, StencilPart::Full, y), exact_arith(c), st);
         return MASPCG_OK;
@@ -255,7 +255,7 @@ maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
         SET_ERR(c, MASPCG_E_SINGULAR, "shift is zero everywhere and no r boundary is Dirichlet: A is singular");
     launch_finalize_D(c->d, c->a, c->bc_in, c->bc_out, st);
     CK(c, cudaGetLastError());
-    if (c->nranks > 1) RET_IF(halo_planes(c, c->a.D, c->a.dh, st));   // D of the neighbours' boundary planes
+    if (c->comm) RET_IF(halo_planes(c, c->a.D, c->a.dh, st));   // D of the neighbours' boundary planes
     c->D_dirty = false;
     return MASPCG_OK;
 }
@@ -302,7 +302,7 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
     f.p_new = c->a.P[par];
     f.x = x;
     f.r = c->a.r;
-    if (c->nranks == 1) {   // periodic wrap planes of the slab itself (R9)
+    if (!c->comm) {   // periodic wrap planes of the slab itself (R9)
         const size_t last = (size_t)(c->nloc - 1) * pl;
         f.r_lo = c->a.r + last, f.r_hi = c->a.r;
         f.d_lo = c->a.D + last, f.d_hi = c->a.D;
@@ -324,11 +324,11 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
         f.n_jt = c->fused_njt;
         f.nch = 1;
     }
-    if (c->nranks > 1 && slot > 0) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // p_old halo of slot-1
+    if (c->comm && slot > 0) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // p_old halo of slot-1
     if (tm) CK(c, record_timing(c, 0, 0, slot, st));
     launch_pass_a(c->d, c->a, f, c->fused_blocks, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 0, 1, slot, st));
-    if (c->nranks > 1) {
+    if (c->comm) {
         // p_it halo for the next pass A, on the communication stream, overlapped with pass B
         CK(c, cudaEventRecord(c->ev_a, st));
         CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_a, 0));
@@ -340,7 +340,7 @@ maspcg_status enqueue_iteration_fused(maspcg_ctx *c, double *x, cudaStream_t st,
     launch_pass_b(c->d, c->a, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 1, 1, slot, st));
     RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st));
-    if (c->nranks > 1) {
+    if (c->comm) {
         RET_IF(halo_planes(c, c->a.r, c->a.rh, st));            // r_it halo (critical path, one plane each way)
         if (slot == c->chunk - 1) CK(c, cudaStreamWaitEvent(st, c->ev_ph, 0));   // join before the chunk ends
     }
@@ -441,7 +441,7 @@ void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
     if (use_fused(c) || use_wave(c)) return 2;
-    if (c->nranks == 1) return 3;
+    if (!c->comm) return 3;
     return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
 }
 
@@ -469,7 +469,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     launch_setup_residual(c->d, c->a, rhs, c->bc_in == BC_DIRICHLET && c->has_gin,
                           c->bc_out == BC_DIRICHLET && c->has_gout, exact_arith(c), st);
     RET_IF(allreduce_dot2(c, c->a.sc->red3, 3, st));
-    if (fused && c->nranks > 1) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
+    if (fused && c->comm) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
     launch_setup_scalars(c->a, tol, maxit, st);
     if (use_wave(c)) {
         // the wave kernel fuses the stencil of iteration k+1 into the p-update of iteration k, so the
@@ -480,7 +480,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
                       stencil_blocks(c->d, StencilPart::Full, c->a.q), exact_arith(c), st);
     }
     CK(c, cudaGetLastError());
-    long long launched = 4 + (c->nranks > 1 ? 1 : 0);
+    long long launched = 4 + (c->comm ? 1 : 0);
 
     // PCG loop: chunks of `chunk` iterations, one speculative chunk in flight.
     CK(c, cudaMemcpyAsync(c->snap[0], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
@@ -581,8 +581,8 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     if (nr < 1 || nt < 1 || np < 1) return fail(MASPCG_E_INVALID, "nr, nt, np must be >= 1");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(MASPCG_E_INVALID, "bad rank / nranks");
     if (np % nranks != 0) return fail(MASPCG_E_INVALID, "np must be divisible by nranks");
-    if (!group && (nranks > 1) != (nccl_unique_id != nullptr))
-        return fail(MASPCG_E_INVALID, "nccl_unique_id must be given iff nranks > 1");
+    if (!group && nranks > 1 && !nccl_unique_id)
+        return fail(MASPCG_E_INVALID, "nccl_unique_id must be given when nranks > 1");
     const long long nloc = np / nranks;
     if ((nloc + 2) * (long long)nt * nr >= (1ll << 31))
         return fail(MASPCG_E_INVALID, "local slab too large (>= 2^31 cells with halos)");
@@ -612,7 +612,7 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
         maspcg_destroy(c);
         return MASPCG_E_CUDA;
     }
-    if (nranks > 1) {
+    if (nranks > 1 || group || nccl_unique_id) {   // a communicator (also at nranks == 1 when one is given)
         int st = ST_OK;
         c->comm = group ? make_loopback_comm((LoopbackGroup *)group, rank, nranks, &st, g_create_error)
                         : make_nccl_comm(nccl_unique_id, rank, nranks, &st, g_create_error);
@@ -630,7 +630,7 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->d.n = (uint32_t)((size_t)c->nloc * nt * nr);
     c->d.div_r = make_fastdiv((uint32_t)nr);
     c->d.div_t = make_fastdiv((uint32_t)nt);
-    c->d.periodic_local = nranks == 1 ? 1 : 0;
+    c->d.periodic_local = c->comm ? 0 : 1;
     c->d.vec_ok = 1;
     c->d.pdl = 1;
     c->fused_bj = fused_bj(nr, nt);   // 0: nr too large for one register batch per thread -> three kernels
@@ -808,7 +808,7 @@ maspcg_status maspcg_set_coefficients(maspcg_ctx *c, const double *kr, const dou
     launch_assemble(c->d, c->a, kr, kt, kp, shift, st);
     CK(c, cudaGetLastError());
     const size_t pl = c->d.plane;
-    if (c->nranks == 1) {
+    if (!c->comm) {
         // face (np-1)+1/2 is the lower phi face of plane 0 (periodic, R9)
         CK(c, cudaMemcpyAsync(c->a.Tp, c->a.Tp + (size_t)c->nloc * pl, 8 * pl, cudaMemcpyDeviceToDevice, st));
     } else {
@@ -843,7 +843,7 @@ maspcg_status maspcg_set_coefficients_from_fields(maspcg_ctx *c, const double *f
     cudaStream_t st = (cudaStream_t)stream;
     const size_t pl = c->d.plane;
     const double *f_hi = field;   // single rank: the plane after the slab is plane 0 (periodic)
-    if (c->nranks > 1) {
+    if (c->comm) {
         // the right neighbour's first plane of the field -> fh[1]
         COMM(c, c->comm->halo_planes(field, field + (size_t)(c->nloc - 1) * pl, c->a.fh, c->a.fh + pl, pl, st,
                                      c->err));
@@ -938,7 +938,7 @@ maspcg_status maspcg_apply(maspcg_ctx *c, const double *x, double *y, void *stre
     launch_fill_p(c->d, c->a, x, st);
     RET_IF(stencil_with_halo(c, y, false, false, st));
     CK(c, cudaGetLastError());
-    c->stats.kernel_launches += 2 + (c->nranks > 1 ? 1 : 0);
+    c->stats.kernel_launches += 2 + (c->comm ? 1 : 0);
     return MASPCG_OK;
 }
 
@@ -978,11 +978,11 @@ maspcg_status maspcg_sts_step(maspcg_ctx *c, double *u, double tau, int stages, 
     DevArrays y0 = c->a;
     y0.p = c->a.sy[3];
     launch_fill_p(c->d, y0, u, st);                     // Y0 (padded, periodic copies on one rank)
-    if (c->nranks > 1) RET_IF(halo_padded(c, c->a.sy[3], st));
+    if (c->comm) RET_IF(halo_padded(c, c->a.sy[3], st));
     double mu, nu, mut, gat;
     rkl2_coefficients(stages, 1, &mu, &nu, &mut, &gat);
     launch_sts_first(c->d, c->a, c->a.sy[3], c->a.sl0, c->a.sy[0], mut * tau, din, dout, ex, st);
-    if (c->nranks > 1) RET_IF(halo_padded(c, c->a.sy[0], st));
+    if (c->comm) RET_IF(halo_padded(c, c->a.sy[0], st));
     const double *yj2 = c->a.sy[3], *yj1 = c->a.sy[0];
     int next = 1;
     for (int j = 2; j <= stages; ++j) {
@@ -991,7 +991,7 @@ maspcg_status maspcg_sts_step(maspcg_ctx *c, double *u, double tau, int stages, 
         double *out = c->a.sy[next];
         launch_sts_stage(c->d, c->a, yj1, yj2, c->a.sy[3], c->a.sl0, out, mu, nu, w0, mut * tau, gat * tau, din, dout,
                          ex, st);
-        if (c->nranks > 1) RET_IF(halo_padded(c, out, st));
+        if (c->comm) RET_IF(halo_padded(c, out, st));
         yj2 = yj1;
         yj1 = out;
         next = (next + 1) % 3;
@@ -1016,7 +1016,7 @@ maspcg_status maspcg_sts_dt_limit(maspcg_ctx *c, double *dt_fe, void *stream) {
     CK(c, cudaStreamSynchronize(st));
     double m = 0.0;
     for (double v : h) m = std::fmax(m, v);
-    if (c->nranks > 1) {
+    if (c->comm) {
         CK(c, cudaMemcpyAsync(c->a.partials, &m, 8, cudaMemcpyHostToDevice, st));
         COMM(c, c->comm->allgather(c->a.partials, c->a.gather, 1, st, c->err));
         std::vector<double> all(c->nranks);

@@ -136,7 +136,8 @@ class Solver:
     torch's current device)."""
 
     def __init__(self, nr: int, nt: int, np_: int, rf, tf, pf, *, group=None, device: int | None = None,
-                 chunk: int = 16, loopback: "tuple[LoopbackGroup, int] | None" = None):
+                 chunk: int = 16, loopback: "tuple[LoopbackGroup, int] | None" = None,
+                 force_comm: bool = False):
         import torch
         import torch.distributed as dist
         self._L = lib()
@@ -160,7 +161,12 @@ class Solver:
                 raise MaspcgError(st, self._L.maspcg_last_error(None).decode())
             self._init_after_create(ctx, nr, nt, np_, rf, tf, pf, chunk)
             return
-        if self.nranks > 1:
+        if self.nranks == 1 and force_comm:
+            # one rank with a real NCCL communicator: the multi-rank code path (halo send/recv to itself,
+            # all-gathers of one) on one GPU -- the periodic wrap then goes through NCCL
+            uid = ctypes.create_string_buffer(128)
+            self._check(self._L.maspcg_get_unique_id(uid), None)
+        elif self.nranks > 1:
             buf = ctypes.create_string_buffer(128)
             if self.rank == 0:
                 self._check(self._L.maspcg_get_unique_id(buf), None)
@@ -308,12 +314,12 @@ class LoopbackGroup:
             self.handle = None
 
 
-def solver_for_problem(prob, *, group=None, device=None, chunk=16, stream=None, loopback=None):
+def solver_for_problem(prob, *, group=None, device=None, chunk=16, stream=None, loopback=None, force_comm=False):
     """Create a Solver for an inputs.Problem slab and upload its coefficients and BCs (device copies)."""
     import torch
     dev = f"cuda:{torch.cuda.current_device() if device is None else device}"
     S = Solver(prob.nr, prob.nt, prob.np, prob.rf, prob.tf, prob.pf, group=group, device=device, chunk=chunk,
-               loopback=loopback)
+               loopback=loopback, force_comm=force_comm)
     assert (S.k0, S.nloc) == (prob.k0, prob.nloc), "problem slab does not match the library's decomposition"
     T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     S.set_coefficients(T(prob.kr), T(prob.kt), T(prob.kp), T(prob.s), stream)

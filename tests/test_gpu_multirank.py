@@ -78,6 +78,7 @@ def solve_rank(M, prob, r, group, tol=None, maxit=None, path=0):
 
 
 CASES = [
+    ("c1", 1, lambda k0, n: inputs.make_problem("c1", k0, n)),   # one rank with a communicator: halo to itself
     ("c1", 2, lambda k0, n: inputs.make_problem("c1", k0, n)),
     ("c1", 4, lambda k0, n: inputs.make_problem("c1", k0, n)),
     ("c2", 2, lambda k0, n: inputs.make_problem("c2", k0, n)),
