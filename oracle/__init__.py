@@ -18,6 +18,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "masoracle.c")
+SRC_VV = os.path.join(HERE, "masoracle_vv.c")   # staggered vector viscosity
 LIB = os.path.join(HERE, "libmasoracle.so")
 
 OK, NOT_CONVERGED, E_INVALID, E_SINGULAR, E_BREAKDOWN, E_NOMEM = 0, 1, -1, -3, -4, -7
@@ -28,9 +29,10 @@ CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared", "-st
 
 def build(force: bool = False) -> str:
     """Compile libmasoracle.so with gcc (plain C99, no contraction, no fast-math)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+    newest = max(os.path.getmtime(SRC), os.path.getmtime(SRC_VV))
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         tmp = LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, SRC_VV, "-lm"])
         os.replace(tmp, LIB)
     return LIB
 
@@ -52,6 +54,15 @@ def lib():
             "masoracle_pcg": [i, i, i, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
             "masoracle_face_coefficients": [i, i, i, d, ctypes.c_double, i, i, d, ctypes.c_double, d, d, d, d],
             "masoracle_rkl2_step": [i, i, i, d, d, d, d, d, d, d, d, ctypes.c_double, i, d],
+            "masoracle_vv_check_grid": [i, i, i, d, d, d],
+            "masoracle_vv_coefficients": [i, i, i, d, d, d, d, d, i, i, d, d, d, d, d, d, d],
+            "masoracle_vv_div": [i, i, i, d, d, d, d, d, d, d],
+            "masoracle_vv_curl": [i, i, i, d, d, d, d, d, d, d, d, d, d, d],
+            "masoracle_vv_apply": [i, i, i, d, d, d, d, d, d, d, d, d, d, d, d, d, d],
+            "masoracle_vv_diag": [i, i, i, d, d, d, d, d, d, d, d, d, d, d],
+            "masoracle_vv_mass": [i, i, i, d, d, d, d],
+            "masoracle_vv_rhs": [i, i, i, d, d, d, d, d, d, d, d, d, d, d, d, d, d],
+            "masoracle_vv_pcg": [i, i, i, d, d, d, d, d, d, d, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
         }.items():
             fn = getattr(_lib, name)
             fn.argtypes = args
@@ -181,4 +192,131 @@ def solve_problem(prob, tol=None, maxit=None, x0=None):
     st, x, iters, hist, bn, rn = op.pcg(b, prob.x0 if x0 is None else x0,
                                         prob.tol if tol is None else tol,
                                         prob.maxit if maxit is None else maxit)
+    return dict(status=st, x=x, iters=iters, hist=hist, bnorm=bn, rnorm=rn, op=op, b=b)
+
+
+# ----------------------------------------------------------------------------------------------
+# Staggered vector viscosity (oracle/masoracle_vv.c, R27-R31)
+NO_SLIP, FREE_SLIP = 0, 1
+
+
+class VVOperator:
+    """Vector viscosity operator of the global grid: s v + curl(nu curl v) - grad(nu div v) on the
+    staggered (MAC) spherical grid with the polar-axis ring treatment.  Vectors are [np][3][nt][nr]
+    (lower faces; component 0 r, 1 theta, 2 phi); wall data [3][np][nt] or None."""
+
+    def __init__(self, rf, tf, pf, nu, s, bc_in=NO_SLIP, bc_out=NO_SLIP):
+        self.rf, self.tf, self.pf = _c(rf), _c(tf), _c(pf)
+        self.nr, self.nt, self.np = self.rf.size - 1, self.tf.size - 1, self.pf.size - 1
+        nr, nt, np_ = self.nr, self.nt, self.np
+        self.bc_in, self.bc_out = int(bc_in), int(bc_out)
+        nu, s = _c(nu), _c(s)
+        assert nu.shape == (np_, nt, nr) and s.shape == (np_, nt, nr)
+        self.wc = np.empty((np_, nt, nr))
+        self.Wr = np.empty((np_, nt, nr))
+        self.Wt = np.empty((np_, nt, nr + 1))
+        self.Wp = np.empty((np_, nt, nr + 1))
+        self.WN = np.empty(nr)
+        self.WS = np.empty(nr)
+        self.sM = np.empty((np_, 3, nt, nr))
+        st = lib().masoracle_vv_coefficients(nr, nt, np_, *self._g(), _p(nu), _p(s), self.bc_in, self.bc_out,
+                                             _p(self.wc), _p(self.Wr), _p(self.Wt), _p(self.Wp), _p(self.WN),
+                                             _p(self.WS), _p(self.sM))
+        if st:
+            raise OracleError(st, "vv_coefficients")
+        self.D = np.empty((np_, 3, nt, nr))
+        st = lib().masoracle_vv_diag(nr, nt, np_, *self._g(), *self._co(), _p(self.D))
+        if st:
+            raise OracleError(st, "vv_diag")
+
+    def _g(self):
+        return _p(self.rf), _p(self.tf), _p(self.pf)
+
+    def _co(self):
+        return (_p(self.wc), _p(self.Wr), _p(self.Wt), _p(self.Wp), _p(self.WN), _p(self.WS), _p(self.sM))
+
+    @property
+    def shape(self):
+        return (self.np, 3, self.nt, self.nr)
+
+    def unknown_mask(self):
+        m = np.ones(self.shape, dtype=bool)
+        m[:, 0, :, 0] = False
+        m[:, 1, 0, :] = False
+        return m
+
+    def apply(self, v, g_in=None, g_out=None) -> np.ndarray:
+        v = _c(v)
+        assert v.shape == self.shape
+        y = np.empty(self.shape)
+        st = lib().masoracle_vv_apply(self.nr, self.nt, self.np, *self._g(), *self._co(), _p(v), _p(_c(g_in)),
+                                      _p(_c(g_out)), _p(y))
+        if st:
+            raise OracleError(st, "vv_apply")
+        return y
+
+    def mass(self) -> np.ndarray:
+        M = np.empty(self.shape)
+        st = lib().masoracle_vv_mass(self.nr, self.nt, self.np, *self._g(), _p(M))
+        if st:
+            raise OracleError(st, "vv_mass")
+        return M
+
+    def rhs(self, f, g_in=None, g_out=None) -> np.ndarray:
+        f = _c(f)
+        b = np.empty(self.shape)
+        st = lib().masoracle_vv_rhs(self.nr, self.nt, self.np, *self._g(), *self._co(), _p(f), _p(_c(g_in)),
+                                    _p(_c(g_out)), _p(b))
+        if st:
+            raise OracleError(st, "vv_rhs")
+        return b
+
+    def pcg(self, b, x0, tol, maxit):
+        """Returns (status, x, iters, hist[0..iters], bnorm, rnorm)."""
+        b = _c(b)
+        x = np.array(_c(x0), copy=True)
+        hist = np.zeros(maxit + 1)
+        iters = ctypes.c_int(0)
+        bn, rn = ctypes.c_double(0), ctypes.c_double(0)
+        st = lib().masoracle_vv_pcg(self.nr, self.nt, self.np, *self._g(), *self._co(), _p(self.D), _p(b), _p(x),
+                                    float(tol), int(maxit), _p(hist), ctypes.byref(iters), ctypes.byref(bn),
+                                    ctypes.byref(rn))
+        return st, x, iters.value, hist[: iters.value + 1].copy(), bn.value, rn.value
+
+
+def vv_check_grid(rf, tf, pf) -> int:
+    rf, tf, pf = _c(rf), _c(tf), _c(pf)
+    return lib().masoracle_vv_check_grid(rf.size - 1, tf.size - 1, pf.size - 1, _p(rf), _p(tf), _p(pf))
+
+
+def vv_div(rf, tf, pf, v, g_in=None, g_out=None) -> np.ndarray:
+    """Net outflow delta [np][nt][nr] of a face vector v [np][3][nt][nr]."""
+    rf, tf, pf, v = _c(rf), _c(tf), _c(pf), _c(v)
+    nr, nt, np_ = rf.size - 1, tf.size - 1, pf.size - 1
+    out = np.empty((np_, nt, nr))
+    st = lib().masoracle_vv_div(nr, nt, np_, _p(rf), _p(tf), _p(pf), _p(v), _p(_c(g_in)), _p(_c(g_out)), _p(out))
+    if st:
+        raise OracleError(st, "vv_div")
+    return out
+
+
+def vv_curl(rf, tf, pf, v, g_in=None, g_out=None):
+    """Circulations (Gr [np][nt][nr], GN [nr], GS [nr], Gt [np][nt][nr+1], Gp [np][nt][nr+1])."""
+    rf, tf, pf, v = _c(rf), _c(tf), _c(pf), _c(v)
+    nr, nt, np_ = rf.size - 1, tf.size - 1, pf.size - 1
+    Gr = np.empty((np_, nt, nr))
+    GN, GS = np.empty(nr), np.empty(nr)
+    Gt = np.empty((np_, nt, nr + 1))
+    Gp = np.empty((np_, nt, nr + 1))
+    st = lib().masoracle_vv_curl(nr, nt, np_, _p(rf), _p(tf), _p(pf), _p(v), _p(_c(g_in)), _p(_c(g_out)), _p(Gr),
+                                 _p(GN), _p(GS), _p(Gt), _p(Gp))
+    if st:
+        raise OracleError(st, "vv_curl")
+    return Gr, GN, GS, Gt, Gp
+
+
+def vv_solve(rf, tf, pf, nu, s, f, x0, tol, maxit, bc_in=NO_SLIP, bc_out=NO_SLIP, g_in=None, g_out=None):
+    op = VVOperator(rf, tf, pf, nu, s, bc_in, bc_out)
+    b = op.rhs(f, g_in, g_out)
+    st, x, iters, hist, bn, rn = op.pcg(b, x0, tol, maxit)
     return dict(status=st, x=x, iters=iters, hist=hist, bnorm=bn, rnorm=rn, op=op, b=b)
