@@ -104,7 +104,8 @@ typedef struct {
     double pupdate_ms;             /* p_update */
     long long pupdate_launches;
     double comm_ms;                /* halo + all-reduce time on the comm path (timing mode, P > 1) */
-    int path;                      /* iteration path of the last solve: 1 = three kernels, 2 = fused two passes */
+    int path;                      /* iteration path of the last solve: 1 = three kernels, 2 = fused two passes,
+                                      3 = wave, 4 = vector viscosity (ring + matvec + update + p-update) */
 } maspcg_stats;
 
 /* Options for maspcg_set_option(). */
@@ -267,6 +268,55 @@ MASPCG_API maspcg_status maspcg_sts_dt_limit(maspcg_ctx *ctx, double *dt_fe, voi
  * internally; x and y must not alias).  For tests and operator checks. */
 MASPCG_API maspcg_status maspcg_apply(maspcg_ctx *ctx, const double *x, double *y,
                                       void *cuda_stream);
+
+/* ---- staggered vector viscosity with the pole treatment (R27-R31) ---------- */
+
+/* The "viscosity solver" of PAPER.md:290 (Sec. V-C, Fig. 4) on MAS's staggered grid:
+ * velocity components on their faces (v_r on r-faces, v_theta on theta-faces, v_phi on phi-faces),
+ * the implicit viscous step
+ *     s v + curl(nu curl v) - grad(nu div v) = f          (= s v - nu lap v for constant nu)
+ * discretised from the energy  1/2 sum_cells nu/V (net outflow)^2 + 1/2 sum_edges W (circulation)^2
+ * (mimetic div-curl form, symmetric positive definite for s >= 0 with the walls below).  The polar
+ * axis is one r-edge per radius whose circulation is the sum over the whole pole ring of v_phi times
+ * its length -- the per-radius array reduction sum0(i) of PAPER.md:147-157 (Listing 3), a ring
+ * reduction plus, across phi-slabs, an all-gather in every matvec.  Requires a full sphere in theta
+ * (t_faces[0] = 0, t_faces[nt] = pi) and np >= 2.  Solved by the same point-Jacobi PCG (R11-R14).
+ *
+ * Layouts (DEVICE, the local slab): vectors [nloc][3][nt][nr] -- inside every phi-plane the three
+ * components (0 r, 1 theta, 2 phi) of the LOWER faces of its cells; the slots v_r(i = 0) (inner
+ * wall face) and v_theta(j = 0) (north-pole face) are not unknowns: ignored on input, 0 on output;
+ * the outer wall face and the south-pole face are not stored.  Cell fields [nloc][nt][nr].  Wall
+ * data [nloc][3][nt]: [0] the normal velocity on the wall face (j, k), [1] the tangential v_theta
+ * at (t_faces[j], phi_c[k]), [2] the tangential v_phi at (theta_c[j], p_faces[k]).
+ *
+ * The vector operator has its own caller-owned workspace (maspcg_vv_workspace_bytes; 256-byte
+ * aligned); the context's base workspace (maspcg_set_workspace) must also be set.  The PCG options
+ * (chunk, graphs, timing, arith) apply; the iteration path is always the streaming kernels. */
+typedef enum { MASPCG_WALL_NO_SLIP = 0, MASPCG_WALL_FREE_SLIP = 1 } maspcg_wall;
+
+MASPCG_API size_t maspcg_vv_workspace_bytes(const maspcg_ctx *ctx);
+MASPCG_API maspcg_status maspcg_vv_set_workspace(maspcg_ctx *ctx, void *dev_ptr, size_t bytes);
+/* Cell viscosity nu >= 0 and cell shift s >= 0 (e.g. rho / dt), DEVICE [nloc][nt][nr], copied.
+ * Edge viscosities are the arithmetic means of the cells around each edge (the pole ring for the
+ * axis), face shifts the means of the two cells of the face (R28).  E_INVALID for a negative or
+ * non-finite value (agreed across ranks) or a grid without both poles; E_STATE before set_grid /
+ * set_workspace / vv_set_workspace.  The operator is (re)assembled lazily at the next vv call. */
+MASPCG_API maspcg_status maspcg_vv_set_coefficients(maspcg_ctx *ctx, const double *nu, const double *shift,
+                                                    void *cuda_stream);
+/* r walls (R30): NO_SLIP -- the wall edges carry circulations closed through the tangential wall
+ * velocity; FREE_SLIP -- no vorticity penalty on the wall edges (zero tangential stress).  Both
+ * prescribe the normal velocity g[0].  g_inner / g_outer DEVICE [nloc][3][nt] or NULL (= 0). */
+MASPCG_API maspcg_status maspcg_vv_set_bc_r(maspcg_ctx *ctx, maspcg_wall inner, const double *g_inner,
+                                            maspcg_wall outer, const double *g_outer, void *cuda_stream);
+/* y = A x (homogeneous walls), DEVICE [nloc][3][nt][nr]; x and y must not alias. */
+MASPCG_API maspcg_status maspcg_vv_apply(maspcg_ctx *ctx, const double *x, double *y, void *cuda_stream);
+/* Solve A v = b, b = M f - A(0; g) (R31: M the face masses area x centre distance, f per unit
+ * volume DEVICE [nloc][3][nt][nr]), by Jacobi PCG from x (DEVICE [nloc][3][nt][nr], in: x0, out:
+ * the iterate; must not alias f).  tol, maxit, resid_hist, info and the return codes as maspcg_solve. */
+MASPCG_API maspcg_status maspcg_vv_solve(maspcg_ctx *ctx, const double *f, double *x, double tol, int maxit,
+                                         double *resid_hist, maspcg_info *info, void *cuda_stream);
+/* The Jacobi diagonal, HOST [nloc][3][nt][nr] (1 on the non-unknown slots); for tests. */
+MASPCG_API maspcg_status maspcg_vv_get_diag(maspcg_ctx *ctx, double *D, void *cuda_stream);
 
 /* ---- in-process multi-rank emulation (TEST ONLY) ------------------------------ */
 

@@ -320,3 +320,13 @@ def vv_solve(rf, tf, pf, nu, s, f, x0, tol, maxit, bc_in=NO_SLIP, bc_out=NO_SLIP
     b = op.rhs(f, g_in, g_out)
     st, x, iters, hist, bn, rn = op.pcg(b, x0, tol, maxit)
     return dict(status=st, x=x, iters=iters, hist=hist, bnorm=bn, rnorm=rn, op=op, b=b)
+
+
+def vv_solve_problem(prob, tol=None, maxit=None, x0=None):
+    """Solve an ``inputs.VVProblem`` covering the whole global grid (k0 = 0, nloc = np); the wall data
+    [np][3][nt] are passed to the oracle in its [3][np][nt] layout."""
+    assert prob.k0 == 0 and prob.nloc == prob.np, "the oracle works on the global grid"
+    T = lambda g: None if g is None else np.ascontiguousarray(np.transpose(g, (1, 0, 2)))
+    return vv_solve(prob.rf, prob.tf, prob.pf, prob.nu, prob.s, prob.f, prob.x0 if x0 is None else x0,
+                    prob.tol if tol is None else tol, prob.maxit if maxit is None else maxit,
+                    prob.wall_in, prob.wall_out, T(prob.g_in), T(prob.g_out))

@@ -105,7 +105,7 @@ Comm *make_nccl_comm(const void *unique_id, int rank, int nranks, int *status, s
 
 // ============================================================== loopback (test-only)
 constexpr int kLoopMaxRanks = 16;
-constexpr int kLoopSlot = 16;
+constexpr int kLoopSlot = 16384;   // doubles per rank: the scalar dots and the vector operator's pole rings (4 nr)
 
 struct LoopSlots {
     const double *d[kLoopMaxRanks];

@@ -837,8 +837,7 @@ void launch_pupdate(const Dims &d, const DevArrays &a, double *x, int chunk, boo
 }
 
 __global__ void k_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact) {
-    const int t = threadIdx.x;
-    if (t >= npairs) return;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < npairs; t += gridDim.x * blockDim.x) {
     if (exact) {
         Acc<true> acc;
         for (int r = 0; r < nranks; ++r) {   // rank order: identical bits on every rank
@@ -855,10 +854,11 @@ __global__ void k_dd_combine(const double *gather, int nranks, int npairs, doubl
         out[2 * t] = v;
         out[2 * t + 1] = 0.0;
     }
+    }
 }
 
 void launch_dd_combine(const double *gather, int nranks, int npairs, double *out, bool exact, cudaStream_t st) {
-    k_dd_combine<<<1, 32, 0, st>>>(gather, nranks, npairs, out, exact);
+    k_dd_combine<<<(npairs + 127) / 128, 128, 0, st>>>(gather, nranks, npairs, out, exact);
 }
 
 void launch_sts_first(const Dims &d, const DevArrays &a, const double *y0p, double *l0, double *y1p, double m1,

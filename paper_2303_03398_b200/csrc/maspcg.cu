@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "vv.cuh"
 #include "wave.cuh"
 
 using namespace maspcg;
@@ -80,6 +81,19 @@ struct maspcg_ctx {
     maspcg_stats stats{};
     std::vector<cudaEvent_t> tev;   // timing events [2 sets][3 kernels][2][chunk]
     int tset = 0;                   // event set of the chunk being enqueued
+
+    // staggered vector viscosity (NEXT-2, vv.cu): its own workspace, 1-D metric and state; the PCG
+    // driver runs on it with d / a swapped for the vector Dims dv and arrays (vmode = 1)
+    std::vector<double> vv_rf, vv_rce, vv_rhor, vv_dR2, vv_rc2, vv_Cs, vv_dpp, vv_hmp;
+    double vv_cap[2] = {0.0, 0.0};
+    int vv_grid_ok = 0;              // both poles in t_faces and np >= 2
+    void *vv_ws = nullptr;
+    size_t vv_ws_bytes = 0;
+    VVArrays va{};
+    VVDims vd{};
+    Dims dv{};
+    bool vv_coef_set = false, vv_bc_set = false, vv_dirty = true;
+    int vmode = 0;
 };
 
 #define SET_ERR(ctx, code, ...)                                              \
@@ -199,7 +213,7 @@ maspcg_status ensure_metric(maspcg_ctx *c, cudaStream_t st) {
     } while (0)
 
 maspcg_status halo_padded(maspcg_ctx *c, double *buf, cudaStream_t st) {
-    COMM(c, c->comm->halo_padded(buf, (size_t)c->nt * c->nr, c->nloc, st, c->err));
+    COMM(c, c->comm->halo_padded(buf, c->d.plane, c->nloc, st, c->err));
     return MASPCG_OK;
 }
 
@@ -210,12 +224,12 @@ maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaSt
     return MASPCG_OK;
 }
 
-bool use_fused(const maspcg_ctx *c) { return c->path_opt == 2 && c->fused_bj > 0; }
-bool use_wave(const maspcg_ctx *c) { return c->path_opt == 3 && !c->comm; }
+bool use_fused(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 2 && c->fused_bj > 0; }
+bool use_wave(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 3 && !c->comm; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
-           (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0);
+           (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -227,9 +241,129 @@ maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStrea
     return MASPCG_OK;
 }
 
+// ------------------------------------------------------------ vector viscosity (NEXT-2, vv.cu)
+size_t vv_layout(const maspcg_ctx *c, char *base, VVArrays *out) {
+    const size_t nr = c->nr, nt = c->nt, nloc = c->nloc, pl1 = nt * nr;
+    size_t off = 0;
+    auto take = [&](size_t doubles) -> double * {
+        double *p = base ? (double *)(base + off) : nullptr;
+        off = align_up(off + 8 * doubles, 256);
+        return p;
+    };
+    VVArrays t{};
+    t.rf = take(nr + 1); t.rf2 = take(nr + 1); t.hr = take(nr + 1); t.dr = take(nr); t.R3 = take(nr);
+    t.rce = take(nr + 2); t.rhor = take(nr + 1); t.dR2 = take(nr); t.rc2 = take(nr);
+    t.C = take(nt); t.dt = take(nt); t.ht = take(nt + 1); t.Cs = take(nt + 1); t.sinc = take(nt); t.sinf = take(nt + 1);
+    t.dpp = take(nloc + 2); t.hmp = take(nloc + 2); t.cap = take(2);
+    t.wc = take((nloc + 2) * pl1); t.Wr = take((nloc + 2) * pl1); t.Wt = take((nloc + 2) * pl1);
+    t.WtO = take((nloc + 2) * nt); t.Wp = take(nloc * pl1); t.WpO = take(nloc * nt);
+    t.WN = take(nr); t.WS = take(nr);
+    t.sM = take(3 * nloc * pl1); t.D = take(3 * nloc * pl1); t.bw = take(3 * nloc * pl1);
+    t.nu = take(nloc * pl1); t.s = take(nloc * pl1); t.nulo = take(2 * pl1); t.slo = take(2 * pl1);
+    t.gin = take((nloc + 2) * 3 * nt); t.gout = take((nloc + 2) * 3 * nt);
+    t.p = take((nloc + 2) * 3 * pl1); t.q = take(3 * nloc * pl1); t.r = take(3 * nloc * pl1);
+    t.ring = take(4 * nr); t.nuring = take(4 * nr); t.gather = take((size_t)kMaxRanks * 4 * nr);
+    if (out) *out = t;
+    return off;
+}
+
+// halo planes of a padded [nloc+2][plane] array: received from the neighbours, or the periodic copies
+maspcg_status pad_planes(maspcg_ctx *c, double *buf, size_t plane, cudaStream_t st) {
+    if (c->comm) {
+        COMM(c, c->comm->halo_padded(buf, plane, c->nloc, st, c->err));
+        return MASPCG_OK;
+    }
+    CK(c, cudaMemcpyAsync(buf, buf + (size_t)c->nloc * plane, 8 * plane, cudaMemcpyDeviceToDevice, st));
+    CK(c, cudaMemcpyAsync(buf + (size_t)(c->nloc + 1) * plane, buf + plane, 8 * plane, cudaMemcpyDeviceToDevice, st));
+    return MASPCG_OK;
+}
+
+// global ring pairs: all-gather the ranks' Dot2 pairs [2 nr] and combine them in rank order
+maspcg_status vv_ring_allreduce(maspcg_ctx *c, double *ring, cudaStream_t st) {
+    if (!c->comm) return MASPCG_OK;
+    COMM(c, c->comm->allgather(ring, c->va.gather, 4 * c->nr, st, c->err));
+    launch_dd_combine(c->va.gather, c->nranks, 2 * c->nr, ring, exact_arith(c), st);
+    return MASPCG_OK;
+}
+
+// Lazy assembly after vv_set_coefficients / vv_set_bc_r: metric, coefficients and their halo planes,
+// the axis weights (pole-ring means of nu), the Jacobi diagonal and the wall part of the rhs.
+maspcg_status ensure_vv(maspcg_ctx *c, cudaStream_t st) {
+    if (!c->vv_ws) SET_ERR(c, MASPCG_E_STATE, "vv_set_workspace must precede the vector-viscosity calls");
+    if (!c->vv_coef_set || !c->vv_bc_set)
+        SET_ERR(c, MASPCG_E_STATE, "vv_set_coefficients and vv_set_bc_r must precede vv_solve / vv_apply");
+    if (!c->vv_dirty) return MASPCG_OK;
+    VVArrays &a = c->va;
+    auto up = [&](double *dst, const double *src, size_t n) {
+        return cudaMemcpyAsync(dst, src, 8 * n, cudaMemcpyHostToDevice, st);
+    };
+    CK(c, up(a.rf, c->vv_rf.data(), c->nr + 1));
+    CK(c, up(a.rf2, c->rf2.data(), c->nr + 1));
+    CK(c, up(a.hr, c->hr.data(), c->nr + 1));
+    CK(c, up(a.dr, c->dr.data(), c->nr));
+    CK(c, up(a.R3, c->R3.data(), c->nr));
+    CK(c, up(a.rce, c->vv_rce.data(), c->nr + 2));
+    CK(c, up(a.rhor, c->vv_rhor.data(), c->nr + 1));
+    CK(c, up(a.dR2, c->vv_dR2.data(), c->nr));
+    CK(c, up(a.rc2, c->vv_rc2.data(), c->nr));
+    CK(c, up(a.C, c->C.data(), c->nt));
+    CK(c, up(a.dt, c->dt.data(), c->nt));
+    CK(c, up(a.ht, c->ht.data(), c->nt + 1));
+    CK(c, up(a.Cs, c->vv_Cs.data(), c->nt + 1));
+    CK(c, up(a.sinc, c->sinc.data(), c->nt));
+    CK(c, up(a.sinf, c->sinf.data(), c->nt + 1));
+    CK(c, up(a.dpp, c->vv_dpp.data(), c->nloc + 2));
+    CK(c, up(a.hmp, c->vv_hmp.data(), c->nloc + 2));
+    CK(c, up(a.cap, c->vv_cap, 2));
+    const size_t pl1 = (size_t)c->nt * c->nr;
+    if (c->comm) {   // plane k0 - 1 of nu and s (the cells below the first phi-faces of the slab)
+        COMM(c, c->comm->halo_planes(a.nu, a.nu + (size_t)(c->nloc - 1) * pl1, a.nulo, a.nulo + pl1, pl1, st, c->err));
+        COMM(c, c->comm->halo_planes(a.s, a.s + (size_t)(c->nloc - 1) * pl1, a.slo, a.slo + pl1, pl1, st, c->err));
+    } else {
+        CK(c, cudaMemcpyAsync(a.nulo, a.nu + (size_t)(c->nloc - 1) * pl1, 8 * pl1, cudaMemcpyDeviceToDevice, st));
+        CK(c, cudaMemcpyAsync(a.slo, a.s + (size_t)(c->nloc - 1) * pl1, 8 * pl1, cudaMemcpyDeviceToDevice, st));
+    }
+    launch_vv_coef(c->vd, a, st);
+    CK(c, cudaGetLastError());
+    RET_IF(pad_planes(c, a.wc, pl1, st));
+    RET_IF(pad_planes(c, a.Wr, pl1, st));
+    RET_IF(pad_planes(c, a.Wt, pl1, st));
+    RET_IF(pad_planes(c, a.WtO, c->nt, st));
+    launch_vv_ring(c->vd, a, 0, exact_arith(c), st);
+    RET_IF(vv_ring_allreduce(c, a.nuring, st));
+    launch_vv_axis_weights(c->vd, a, c->np, st);
+    launch_vv_diag(c->vd, a, st);
+    // bw = A(0; g): the operator on p = 0 with the wall data
+    CK(c, cudaMemsetAsync(a.p, 0, 8 * (size_t)(c->nloc + 2) * 3 * pl1, st));
+    CK(c, cudaMemsetAsync(a.ring, 0, 8 * 4 * (size_t)c->nr, st));
+    launch_vv_matvec(c->vd, a, c->a, a.bw, false, false, true, true, st);
+    CK(c, cudaGetLastError());
+    CK(c, cudaStreamSynchronize(st));   // host metric vectors may change with the next set_grid
+    c->stats.kernel_launches += 6;
+    c->vv_dirty = false;
+    return MASPCG_OK;
+}
+
+// q = A p of the vector operator: the pole-ring sums (Listing 3's per-radius reduction, all-gathered
+// across the phi-slabs) on the caller's stream while the p halo planes travel on the comm stream.
+maspcg_status vv_stencil(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st) {
+    if (c->comm) {
+        CK(c, cudaEventRecord(c->ev_p, st));
+        CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
+        COMM(c, c->comm->halo_padded(c->va.p, c->d.plane, c->nloc, c->comm_stream, c->err));
+        CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+    }
+    launch_vv_ring(c->vd, c->va, 1, exact_arith(c), st);
+    RET_IF(vv_ring_allreduce(c, c->va.ring, st));
+    if (c->comm) CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+    launch_vv_matvec(c->vd, c->va, c->a, y, with_dot, loop, false, exact_arith(c), st);
+    return MASPCG_OK;
+}
+
 // Halo exchange of p (P > 1) overlapped with the interior of the stencil on
 // the caller's stream; joins before the boundary planes.
 maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st) {
+    if (c->vmode) return vv_stencil(c, y, with_dot, loop, st);
     if (!c->comm) {
         launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
                       stencil_blocks(c->d, StencilPart::Full, y), exact_arith(c), st);
@@ -440,6 +574,7 @@ void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
 }
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
+    if (c->vmode) return 4 + (c->comm ? 1 : 0);   // ring sums (+ combine), matvec, update, p-update
     if (use_fused(c) || use_wave(c)) return 2;
     if (!c->comm) return 3;
     return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
@@ -452,22 +587,26 @@ bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
 
 maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol, int maxit, double *hist,
                          maspcg_info *info, cudaStream_t st) {
-    const size_t n = (size_t)c->nloc * c->nt * c->nr;
+    const size_t n = c->d.n;
     if (!rhs || !x) SET_ERR(c, MASPCG_E_INVALID, "rhs and x must be non-NULL");
     if (overlaps(rhs, 8 * n, x, 8 * n)) SET_ERR(c, MASPCG_E_INVALID, "x must not alias rhs");
     if (!(tol >= 0.0) || !std::isfinite(tol)) SET_ERR(c, MASPCG_E_INVALID, "tol must be finite and >= 0");
     if (maxit < 0) SET_ERR(c, MASPCG_E_INVALID, "maxit must be >= 0");
     if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
-    RET_IF(ensure_D(c, st));
+    RET_IF(c->vmode ? ensure_vv(c, st) : ensure_D(c, st));
     const bool fused = use_fused(c);
     if (fused && (c->chunk & 1)) c->chunk += 1;   // even chunks: fixed p-buffer parity per slot
     if (c->timing) RET_IF(maspcg_set_option(c, MASPCG_OPT_TIMING, c->timing));   // events for this chunk size
 
     // a3: r0 = b - A x0, z0 = r0/D, p0 = z0, dots; then PCG start scalars
+    if (c->vmode) launch_vv_mask(c->vd, x, st);   // the non-unknown slots of x are 0
     launch_fill_p(c->d, c->a, x, st);
     RET_IF(stencil_with_halo(c, c->a.q, false, false, st));
-    launch_setup_residual(c->d, c->a, rhs, c->bc_in == BC_DIRICHLET && c->has_gin,
-                          c->bc_out == BC_DIRICHLET && c->has_gout, exact_arith(c), st);
+    if (c->vmode)
+        launch_vv_setup_residual(c->vd, c->va, c->a, c->d, rhs, exact_arith(c), st);
+    else
+        launch_setup_residual(c->d, c->a, rhs, c->bc_in == BC_DIRICHLET && c->has_gin,
+                              c->bc_out == BC_DIRICHLET && c->has_gout, exact_arith(c), st);
     RET_IF(allreduce_dot2(c, c->a.sc->red3, 3, st));
     if (fused && c->comm) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
     launch_setup_scalars(c->a, tol, maxit, st);
@@ -537,7 +676,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
     c->stats.kernel_launches += launched;
-    c->stats.path = use_wave(c) ? 3 : (fused ? 2 : 1);
+    c->stats.path = c->vmode ? 4 : (use_wave(c) ? 3 : (fused ? 2 : 1));
     c->stats.solves += 1;
     c->stats.iterations += iters;
     if (info) {
@@ -549,6 +688,33 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     if (status == MASPCG_E_BREAKDOWN) c->err = "PCG breakdown: p.Ap <= 0 or a non-finite residual";
     return (maspcg_status)status;
 }
+
+// Runs the PCG driver on the vector operator: the flat kernels see n = nloc * 3 nt * nr values with
+// 3 nt * nr per phi-plane, and p, q, r, D are the vector arrays.
+struct VModeGuard {
+    maspcg_ctx *c;
+    Dims d;
+    DevArrays a;
+    explicit VModeGuard(maspcg_ctx *cc) : c(cc), d(cc->d), a(cc->a) {
+        Dims v = cc->d;
+        v.nt = 3 * cc->nt;
+        v.plane = (uint32_t)(3 * (size_t)cc->nt * cc->nr);
+        v.n = (uint32_t)((size_t)cc->nloc * v.plane);
+        v.div_t = make_fastdiv((uint32_t)v.nt);
+        cc->dv = v;
+        cc->d = v;
+        cc->a.p = cc->va.p;
+        cc->a.q = cc->va.q;
+        cc->a.r = cc->va.r;
+        cc->a.D = cc->va.D;
+        cc->vmode = 1;
+    }
+    ~VModeGuard() {
+        c->d = d;
+        c->a = a;
+        c->vmode = 0;
+    }
+};
 
 }  // namespace
 
@@ -754,6 +920,38 @@ maspcg_status maspcg_set_grid(maspcg_ctx *c, const double *rf, const double *tf,
     hpg[np - 1] = (pc[0] + kTwoPi) - pc[np - 1];
     c->dp_loc.assign(dpg.begin() + c->k0, dpg.begin() + c->k0 + c->nloc);
     c->hp_loc.assign(hpg.begin() + c->k0, hpg.begin() + c->k0 + c->nloc);
+
+    // vector-viscosity metric (NEXT-2, R27): the expressions of the vector oracle's grid
+    c->vv_grid_ok = (tf[0] == 0.0 && std::fabs(tf[nt] - kPi) <= 1e-12 && np >= 2) ? 1 : 0;
+    c->vv_rf.assign(rf, rf + nr + 1);
+    c->vv_rce.assign(nr + 2, 0.0);
+    c->vv_rce[0] = rf[0];
+    for (int i = 0; i < nr; ++i) c->vv_rce[i + 1] = rc[i];
+    c->vv_rce[nr + 1] = rf[nr];
+    c->vv_rhor.assign(nr + 1, 0.0);
+    for (int e = 0; e <= nr; ++e) c->vv_rhor[e] = c->hr[e] * (0.5 * (c->vv_rce[e] + c->vv_rce[e + 1]));
+    c->vv_dR2.assign(nr, 0.0);
+    c->vv_rc2.assign(nr, 0.0);
+    for (int i = 0; i < nr; ++i) {
+        c->vv_dR2[i] = rc[i] * c->dr[i];
+        c->vv_rc2[i] = rc[i] * rc[i];
+    }
+    c->vv_Cs.assign(nt + 1, 0.0);
+    for (int j = 1; j < nt; ++j) c->vv_Cs[j] = 2.0 * std::sin(0.5 * (tc[j - 1] + tc[j])) * std::sin(0.5 * c->ht[j]);
+    {
+        const double sN = std::sin(0.5 * tc[0]), cS = std::cos(0.5 * tc[nt - 1]);
+        c->vv_cap[0] = (2.0 * kTwoPi) * (sN * sN);
+        c->vv_cap[1] = (2.0 * kTwoPi) * (cS * cS);
+    }
+    c->vv_dpp.assign(c->nloc + 2, 0.0);
+    c->vv_hmp.assign(c->nloc + 2, 0.0);
+    for (int kk = 0; kk < c->nloc + 2; ++kk) {
+        const int kg = ((c->k0 + kk - 1) % np + np) % np;   // global plane k0 - 1 + kk (periodic)
+        c->vv_dpp[kk] = dpg[kg];
+        c->vv_hmp[kk] = hpg[(kg + np - 1) % np];           // centre distance across the lower phi-face of kg
+    }
+    c->vv_dirty = true;
+    c->vv_coef_set = false;
 
     c->grid_set = true;
     c->metric_dirty = true;
@@ -1058,6 +1256,129 @@ maspcg_status maspcg_get_operator(maspcg_ctx *c, double *Tr, double *Tt, double 
         }
     if (Tp) memcpy(Tp, tp.data() + pl, 8 * n);
     if (D) memcpy(D, dd.data(), 8 * n);
+    return MASPCG_OK;
+}
+
+// ------------------------------------------------------------ vector viscosity (NEXT-2)
+size_t maspcg_vv_workspace_bytes(const maspcg_ctx *c) { return c ? vv_layout(c, nullptr, nullptr) : 0; }
+
+maspcg_status maspcg_vv_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!dev_ptr || ((uintptr_t)dev_ptr & 255)) SET_ERR(c, MASPCG_E_INVALID, "workspace must be 256-byte aligned");
+    if ((size_t)(c->nloc + 2) * 3 * c->nt * c->nr >= (1ull << 31))
+        SET_ERR(c, MASPCG_E_INVALID, "local slab too large for the vector operator (>= 2^31 face values)");
+    const size_t need = vv_layout(c, nullptr, nullptr);
+    if (bytes < need) SET_ERR(c, MASPCG_E_NOMEM, "vv workspace too small: %zu < %zu bytes", bytes, need);
+    RET_IF(bind_device(c));
+    c->vv_ws = dev_ptr;
+    c->vv_ws_bytes = bytes;
+    vv_layout(c, (char *)dev_ptr, &c->va);
+    VVDims &v = c->vd;
+    v.nr = c->nr;
+    v.nt = c->nt;
+    v.nloc = c->nloc;
+    v.plane1 = (uint32_t)((size_t)c->nt * c->nr);
+    v.plane3 = 3 * v.plane1;
+    v.ncell = (uint32_t)((size_t)c->nloc * v.plane1);
+    v.div_r = make_fastdiv((uint32_t)c->nr);
+    v.div_t = make_fastdiv((uint32_t)c->nt);
+    c->vv_coef_set = c->vv_bc_set = false;
+    c->vv_dirty = true;
+    for (int b = 0; b < 2; ++b) {
+        if (c->gexec[b]) {
+            cudaGraphExecDestroy(c->gexec[b]);
+            c->gexec[b] = nullptr;
+        }
+    }
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_vv_set_coefficients(maspcg_ctx *c, const double *nu, const double *shift, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!nu || !shift) SET_ERR(c, MASPCG_E_INVALID, "nu and shift must be non-NULL");
+    if (!c->grid_set || !c->ws || !c->vv_ws)
+        SET_ERR(c, MASPCG_E_STATE, "set_grid, set_workspace and vv_set_workspace must precede vv_set_coefficients");
+    if (!c->vv_grid_ok)
+        SET_ERR(c, MASPCG_E_INVALID, "the vector operator needs both poles (t_faces[0] = 0, t_faces[nt] = pi) and np >= 2");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)c->nloc * c->nt * c->nr;
+    CK(c, cudaMemcpyAsync(c->va.nu, nu, 8 * n, cudaMemcpyDeviceToDevice, st));
+    CK(c, cudaMemcpyAsync(c->va.s, shift, 8 * n, cudaMemcpyDeviceToDevice, st));
+    CK(c, cudaMemsetAsync(&c->a.sc->vinvalid, 0, sizeof(int), st));
+    launch_vv_validate(c->vd, c->va.nu, c->va.s, &c->a.sc->vinvalid, st);
+    CK(c, cudaGetLastError());
+    if (c->comm) COMM(c, c->comm->allreduce_max(&c->a.sc->vinvalid, 1, st, c->err));
+    CK(c, cudaMemcpyAsync(c->vflags_host, &c->a.sc->vinvalid, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    c->stats.kernel_launches += 1;
+    c->vv_dirty = true;
+    if (c->vflags_host[0]) {
+        c->vv_coef_set = false;
+        SET_ERR(c, MASPCG_E_INVALID, "the viscosity or the shift is negative or non-finite");
+    }
+    c->vv_coef_set = true;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_vv_set_bc_r(maspcg_ctx *c, maspcg_wall inner, const double *g_inner, maspcg_wall outer,
+                                 const double *g_outer, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if ((inner != MASPCG_WALL_NO_SLIP && inner != MASPCG_WALL_FREE_SLIP) ||
+        (outer != MASPCG_WALL_NO_SLIP && outer != MASPCG_WALL_FREE_SLIP))
+        SET_ERR(c, MASPCG_E_INVALID, "wall type must be NO_SLIP or FREE_SLIP");
+    if (!c->vv_ws) SET_ERR(c, MASPCG_E_STATE, "vv_set_workspace must precede vv_set_bc_r");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t wplane = 3 * (size_t)c->nt, wsz = (size_t)(c->nloc + 2) * wplane;
+    CK(c, cudaMemsetAsync(c->va.gin, 0, 8 * wsz, st));
+    CK(c, cudaMemsetAsync(c->va.gout, 0, 8 * wsz, st));
+    if (g_inner)
+        CK(c, cudaMemcpyAsync(c->va.gin + wplane, g_inner, 8 * (size_t)c->nloc * wplane, cudaMemcpyDeviceToDevice, st));
+    if (g_outer)
+        CK(c, cudaMemcpyAsync(c->va.gout + wplane, g_outer, 8 * (size_t)c->nloc * wplane, cudaMemcpyDeviceToDevice, st));
+    RET_IF(pad_planes(c, c->va.gin, wplane, st));
+    RET_IF(pad_planes(c, c->va.gout, wplane, st));
+    c->vd.wall_in = (int)inner;
+    c->vd.wall_out = (int)outer;
+    c->vv_bc_set = true;
+    c->vv_dirty = true;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_vv_apply(maspcg_ctx *c, const double *x, double *y, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!x || !y) SET_ERR(c, MASPCG_E_INVALID, "x and y must be non-NULL");
+    const size_t n = 3 * (size_t)c->nloc * c->nt * c->nr;
+    if (overlaps(x, 8 * n, y, 8 * n)) SET_ERR(c, MASPCG_E_INVALID, "x and y must not alias");
+    if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_vv(c, st));
+    VModeGuard g(c);
+    launch_fill_p(c->d, c->a, x, st);
+    RET_IF(stencil_with_halo(c, y, false, false, st));
+    CK(c, cudaGetLastError());
+    c->stats.kernel_launches += 3 + (c->comm ? 1 : 0);
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_vv_solve(maspcg_ctx *c, const double *f, double *x, double tol, int maxit, double *hist,
+                              maspcg_info *info, void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!c->vv_ws) SET_ERR(c, MASPCG_E_STATE, "vv_set_workspace must precede vv_solve");
+    RET_IF(bind_device(c));
+    VModeGuard g(c);
+    return solve_impl(c, f, x, tol, maxit, hist, info, (cudaStream_t)stream);
+}
+
+maspcg_status maspcg_vv_get_diag(maspcg_ctx *c, double *D, void *stream) {
+    if (!c || !D) return MASPCG_E_INVALID;
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_vv(c, st));
+    CK(c, cudaMemcpyAsync(D, c->va.D, 8 * 3 * (size_t)c->nloc * c->nt * c->nr, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
     return MASPCG_OK;
 }
 

@@ -261,3 +261,93 @@ def random_problem(nr: int, nt: int, np_: int, seed: int, *, bc_in=BC_DIRICHLET,
     x0 = np.zeros((nloc, nt, nr))
     return Problem(f"rand{seed}", nr, nt, np_, k0, nloc, rf, tf, pf, kr, kt, kp, s, f, x0,
                    bc_in, bc_out, g_in, g_out, 1e-10, 20000)
+
+
+# --------------------------------------------------------------------------- vector viscosity (NEXT-2)
+WALL_NO_SLIP, WALL_FREE_SLIP = 0, 1
+
+
+@dataclasses.dataclass
+class VVProblem:
+    """One rank's share of a generated staggered vector-viscosity problem.
+    Vectors are [nloc][3][nt][nr] (component 0 r, 1 theta, 2 phi on the LOWER faces of each cell),
+    wall data [nloc][3][nt]; the oracle takes the global [np][3][nt][nr] and [3][np][nt]."""
+    name: str
+    nr: int
+    nt: int
+    np: int
+    k0: int
+    nloc: int
+    rf: np.ndarray
+    tf: np.ndarray
+    pf: np.ndarray
+    nu: np.ndarray          # [nloc][nt][nr] cell viscosity
+    s: np.ndarray           # [nloc][nt][nr] cell shift
+    f: np.ndarray           # [nloc][3][nt][nr] per-unit-volume forcing
+    x0: np.ndarray          # [nloc][3][nt][nr]
+    wall_in: int
+    wall_out: int
+    g_in: np.ndarray | None  # [nloc][3][nt]
+    g_out: np.ndarray | None
+    tol: float
+    maxit: int
+
+    @property
+    def shape(self):
+        return (self.nloc, 3, self.nt, self.nr)
+
+
+VV_CONFIGS = {
+    # c3 grid with the viscosity of c3 (BASELINE.json configs[2]) as a staggered vector solve
+    "c3v": (150, 300, 600),
+    "c2v": (64, 64, 128),
+}
+
+
+def make_vv_problem(name: str, k0: int | None = None, nloc: int | None = None, *,
+                    shape: tuple[int, int, int] | None = None, seed: int = 1,
+                    wall_in: int = WALL_NO_SLIP, wall_out: int = WALL_FREE_SLIP,
+                    x0_seed: int | None = None) -> VVProblem:
+    """``rand``: random nu in [0.5, 2] and s in [0.5, 1.5] per cell, white-noise forcing and wall data,
+    stretched grid r in [1, 3] (needs ``shape``).  ``c3v`` / ``c2v``: the coronal grid of c3 / c2 with
+    nu = 1e-3 rho(r) and s = rho(r)/dt (dt = 1e-2), forcing s (0.5 G_c(theta, phi) e^{-(r-1)/5} + 0.05 w)
+    per component (G_c three seeded angular fields), v = 0 on the inner wall, free-slip outer wall."""
+    if name == "rand":
+        assert shape is not None
+        nr, nt, np_ = shape
+    else:
+        nr, nt, np_ = shape if shape is not None else VV_CONFIGS[name]
+    if k0 is None:
+        k0, nloc = 0, np_
+    assert nloc is not None
+    tol, maxit = 1e-10, 20000
+    if name == "rand":
+        rf, tf, pf = rfaces(nr, 1.0, 3.0, 2.0), tfaces(nt, 0.2), pfaces(np_)
+        base = seed * 16
+        u = lambda s_: 0.5 * (1.0 + white_noise(base + s_, nr, nt, k0, nloc))
+        nu = 0.5 + 1.5 * u(1)
+        s = 0.5 + u(2)
+        f = np.stack([white_noise(base + 3 + c, nr, nt, k0, nloc) for c in range(3)], axis=1)
+        gw = lambda s_: np.stack([white_noise(base + s_ + c, 1, nt, k0, nloc)[:, :, 0] for c in range(3)], axis=1)
+        g_in, g_out = gw(8), gw(12)
+    else:
+        rf = rfaces(nr, 1.0, 30.0, 4.0 if name == "c2v" else 5.33)
+        tf, pf = tfaces(nt, 0.1), pfaces(np_)
+        rc, tc, pc = midpoints(rf), midpoints(tf), midpoints(pf)
+        rho_c = rho_hydro(rc)
+        nu = np.broadcast_to(1e-3 * rho_c[None, None, :], (nloc, nt, nr)).copy()
+        s = np.broadcast_to(rho_c[None, None, :] / 1e-2, (nloc, nt, nr)).copy()
+        pos = [(rf[:-1], tc, pc), (rc, tf[:-1], pc), (rc, tc, pf[:-1])]   # lower-face centres per component
+        f = np.empty((nloc, 3, nt, nr))
+        for c, (r, t, p) in enumerate(pos):
+            G = angular_field(t, p[k0:k0 + nloc], 3 + c)[:, :, None]
+            sr = (rho_hydro(r) / 1e-2)[None, None, :]
+            f[:, c] = sr * (0.5 * G * np.exp(-(r - 1.0) / 5.0)[None, None, :]
+                            + 0.05 * white_noise(20 + c, nr, nt, k0, nloc))
+        g_in = g_out = None
+    x0 = np.zeros((nloc, 3, nt, nr)) if x0_seed is None else \
+        0.1 * np.stack([white_noise(x0_seed + c, nr, nt, k0, nloc) for c in range(3)], axis=1)
+    return VVProblem(name, nr, nt, np_, k0, nloc, rf, tf, pf, np.ascontiguousarray(nu), np.ascontiguousarray(s),
+                     np.ascontiguousarray(f), np.ascontiguousarray(x0), wall_in, wall_out,
+                     None if g_in is None else np.ascontiguousarray(g_in),
+                     None if g_out is None else np.ascontiguousarray(g_out), tol, maxit)

@@ -26,6 +26,7 @@ E_INVALID, E_STATE, E_SINGULAR, E_BREAKDOWN, E_CUDA, E_NCCL, E_NOMEM = -1, -2, -
 STATUS_NAMES = {0: "OK", 1: "NOT_CONVERGED", -1: "E_INVALID", -2: "E_STATE", -3: "E_SINGULAR",
                 -4: "E_BREAKDOWN", -5: "E_CUDA", -6: "E_NCCL", -7: "E_NOMEM"}
 BC_DIRICHLET, BC_NEUMANN0 = 0, 1
+WALL_NO_SLIP, WALL_FREE_SLIP = 0, 1
 MEAN_ARITHMETIC, MEAN_HARMONIC = 0, 1
 OPT_CHUNK, OPT_USE_GRAPHS, OPT_TIMING, OPT_PATH, OPT_ARITH, OPT_TMA, OPT_VEC, OPT_PDL = 1, 2, 3, 4, 5, 6, 7, 8
 ARITH_EXACT, ARITH_FAST = 0, 1
@@ -83,6 +84,13 @@ SIGNATURES = {
     "maspcg_loopback_group_create": ([_I, ctypes.POINTER(_V)], _I),
     "maspcg_loopback_group_destroy": ([_V], _I),
     "maspcg_create_loopback": ([_I, _I, _I, _I, _I, _V, _I, ctypes.POINTER(_V)], _I),
+    "maspcg_vv_workspace_bytes": ([_V], _SZ),
+    "maspcg_vv_set_workspace": ([_V, _V, _SZ], _I),
+    "maspcg_vv_set_coefficients": ([_V, _V, _V, _V], _I),
+    "maspcg_vv_set_bc_r": ([_V, _I, _V, _I, _V, _V], _I),
+    "maspcg_vv_apply": ([_V, _V, _V, _V], _I),
+    "maspcg_vv_solve": ([_V, _V, _V, _D, _I, _V, ctypes.POINTER(Info), _V], _I),
+    "maspcg_vv_get_diag": ([_V, _V, _V], _I),
 }
 
 _lib = None
@@ -286,6 +294,57 @@ class Solver:
         self._check(self._L.maspcg_get_operator(self.ctx, _ptr(Tr), _ptr(Tt), _ptr(Tp), _ptr(D),
                                                 _stream(stream)))
         return Tr, Tt, Tp, D
+
+    # ---------------------------------------------------------------- vector viscosity (NEXT-2)
+    @property
+    def vv_local_shape(self):
+        return (self.nloc, 3, self.nt, self.nr)
+
+    def vv_enable(self):
+        """Allocate and attach the vector operator's workspace (maspcg_vv_workspace_bytes / _set_workspace)."""
+        import torch
+        if getattr(self, "vv_workspace", None) is not None:
+            return
+        nbytes = self._L.maspcg_vv_workspace_bytes(self.ctx)
+        self.vv_workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        base = self.vv_workspace.data_ptr()
+        self._check(self._L.maspcg_vv_set_workspace(self.ctx, base + (-base) % 256, nbytes))
+
+    def vv_set_coefficients(self, nu, s, stream=None):
+        """maspcg_vv_set_coefficients: cell viscosity and shift, device [nloc][nt][nr]."""
+        self.vv_enable()
+        self._check(self._L.maspcg_vv_set_coefficients(self.ctx, _ptr(nu), _ptr(s), _stream(stream)))
+
+    def vv_set_bc_r(self, wall_in: int, g_in, wall_out: int, g_out, stream=None):
+        """maspcg_vv_set_bc_r: wall types and wall data, device [nloc][3][nt] or None."""
+        self.vv_enable()
+        self._check(self._L.maspcg_vv_set_bc_r(self.ctx, int(wall_in), _ptr(g_in), int(wall_out), _ptr(g_out),
+                                               _stream(stream)))
+
+    def vv_apply(self, x, y=None, stream=None):
+        import torch
+        if y is None:
+            y = torch.empty_like(x)
+        self._check(self._L.maspcg_vv_apply(self.ctx, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def vv_solve(self, f, x, tol: float, maxit: int, stream=None, raise_on_error: bool = True):
+        """maspcg_vv_solve (device [nloc][3][nt][nr]); returns (status, info_dict, hist)."""
+        hist = np.zeros(maxit + 1)
+        info = Info()
+        st = self._L.maspcg_vv_solve(self.ctx, _ptr(f), _ptr(x), float(tol), int(maxit), hist.ctypes.data,
+                                     ctypes.byref(info), _stream(stream))
+        if raise_on_error and st < 0:
+            self._check(st)
+        d = {"iters": info.iters, "bnorm": info.bnorm, "rnorm": info.rnorm, "rel_resid": info.rel_resid}
+        if st < 0:
+            d["error"] = (self._L.maspcg_last_error(self.ctx) or b"").decode()
+        return st, d, hist[: max(info.iters, 0) + 1].copy()
+
+    def vv_get_diag(self, stream=None) -> np.ndarray:
+        D = np.empty(self.vv_local_shape)
+        self._check(self._L.maspcg_vv_get_diag(self.ctx, _ptr(D), _stream(stream)))
+        return D
 
     def stats(self) -> dict:
         s = Stats()
