@@ -129,6 +129,165 @@ def oracle_sample(prob, iters: int):
     return 1.0 / per_iter, t3 - t0, per_iter
 
 
+VV_BYTES = {"matvec": 104, "update": 96, "pupdate": 144, "iter": 344}   # algorithmic B/cell
+
+
+def oracle_vv_sample(prob, iters: int):
+    """Time the vector oracle (as it stands, single-threaded) on the full grid: coefficients, diagonal
+    and rhs once, then `iters` PCG iterations (tol = 0).  Returns (iterations/s, CPU seconds, s/iter)."""
+    import oracle
+    T = lambda g: None if g is None else np.ascontiguousarray(np.transpose(g, (1, 0, 2)))
+    t0 = time.perf_counter()
+    op = oracle.VVOperator(prob.rf, prob.tf, prob.pf, prob.nu, prob.s, prob.wall_in, prob.wall_out)
+    b = op.rhs(prob.f, T(prob.g_in), T(prob.g_out))
+    t1 = time.perf_counter()
+    op.pcg(b, prob.x0, 0.0, 0)
+    t2 = time.perf_counter()
+    op.pcg(b, prob.x0, 0.0, iters)
+    t3 = time.perf_counter()
+    per_iter = ((t3 - t2) - (t2 - t1)) / iters
+    return 1.0 / per_iter, t3 - t0, per_iter
+
+
+def run_vv(args):
+    """--operator vv: the staggered vector viscosity solve on the coronal grid of
+    c3 (config c3v): per step vv_set_coefficients + vv_set_bc_r + vv_solve to 1e-10."""
+    import torch
+    import torch.distributed as dist
+    from paper_2303_03398_b200 import inputs, maspcg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    cfg = args.config if args.config in inputs.VV_CONFIGS else "c3v"
+    nr, nt, np_ = inputs.VV_CONFIGS[cfg]
+    k0, nloc = inputs.slab_extent(np_, rank, world)
+    prob = inputs.make_vv_problem(cfg, k0, nloc)
+    tol = 0.0 if args.maxit else prob.tol
+    maxit = args.maxit if args.maxit else prob.maxit
+    T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    nu, s, f, x0 = T(prob.nu), T(prob.s), T(prob.f), T(prob.x0)
+    S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk,
+                      force_comm=args.force_comm)
+    S.set_option(maspcg.OPT_ARITH, args.arith)
+    S.vv_enable()
+    x = torch.empty_like(x0)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        S.vv_set_coefficients(nu, s)
+        S.vv_set_bc_r(prob.wall_in, None, prob.wall_out, None)
+        x.copy_(x0)
+        st, info, hist = S.vv_solve(f, x, tol, maxit)
+        if st < 0:
+            raise RuntimeError(f"vv solve failed: {st} {info.get('error')}")
+        return info["iters"]
+
+    for _ in range(args.warmup):
+        step()
+    S.set_option(maspcg.OPT_TIMING, args.kernel_timing)
+    S.reset_stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            iters += step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    stats = S.stats()
+    S.set_option(maspcg.OPT_TIMING, 0)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sec = ms / 1e3
+    value = iters / sec
+    ncl = prob.nloc * nt * nr
+    peak, peak_src = peaks()
+    avg = lambda k: stats[k + "_ms"] / stats[k + "_launches"] if stats[k + "_launches"] else 0.0
+    mv_ms = avg("matvec")
+    achieved = VV_BYTES["matvec"] * ncl / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_vv_matvec.json")) as fh:
+            traffic = float(json.load(fh)["kernels"][0]["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    gb = lambda k: VV_BYTES[k] * ncl / (avg(k) * 1e-3) / 1e9 if avg(k) > 0 else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "kernel": "vv pole-ring sums + vector stencil + p.q (k_vv_ring + k_vv_matvec)",
+                "algorithmic_bytes_per_launch": VV_BYTES["matvec"] * ncl, "avg_launch_ms": mv_ms,
+                "peak_source": peak_src, "share_of_step": avg("matvec") * iters / ms if ms > 0 else None,
+                "timed_launches": stats["matvec_launches"]}
+    per_kernel = {"update_GBps": gb("update"), "p_update_GBps": gb("pupdate"),
+                  "iteration_bytes_per_cell": VV_BYTES["iter"],
+                  "iteration_GBps": VV_BYTES["iter"] * ncl * iters / sec / 1e9}
+    # end to end through the public API from pinned host buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        hnu, hs, hf, hx0 = pin(prob.nu), pin(prob.s), pin(prob.f), pin(prob.x0)
+        hx = torch.empty_like(hx0).pin_memory()
+
+        def step_host():
+            dnu, ds, df = hnu.to(dev, non_blocking=True), hs.to(dev, non_blocking=True), hf.to(dev, non_blocking=True)
+            S.vv_set_coefficients(dnu, ds)
+            S.vv_set_bc_r(prob.wall_in, None, prob.wall_out, None)
+            dx = hx0.to(dev, non_blocking=True)
+            st, info, hist = S.vv_solve(df, dx, tol, maxit)
+            hx.copy_(dx)
+            return info["iters"]
+
+        step_host()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        it_h = sum(step_host() for _ in range(args.steps))
+        torch.cuda.synchronize()
+        th = time.perf_counter() - t0
+        e2e = {"value": it_h / th, "unit": UNIT,
+               "h2d_bytes_per_step": hnu.numel() * 8 + hs.numel() * 8 + hf.numel() * 8 + hx0.numel() * 8,
+               "d2h_bytes_per_step": hx.numel() * 8, "ms_per_step": 1e3 * th / args.steps,
+               "api": "pinned host -> device copies + maspcg_vv_set_coefficients + maspcg_vv_solve + device -> host"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ips, cpu_s, per_it = oracle_vv_sample(inputs.make_vv_problem(cfg), max(1, args.ref_iters // 4))
+        cpu = {"value": ips, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle/masoracle_vv.c (single-threaded C, -O2) on the full {cfg} grid: coefficients, "
+                         f"diagonal, rhs once, then {max(1, args.ref_iters // 4)} PCG iterations (tol=0); "
+                         f"{cpu_s:.1f} s of CPU work, {per_it * 1e3:.0f} ms/iteration"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, paper_2303_03398_b200/inputs.py make_vv_problem)",
+            "config": {"workload": f"{cfg} {nr}x{nt}x{np_} staggered vector viscosity solve (SURVEY 8(f) NEXT-2; "
+                                   f"grid and viscosity of BASELINE.json configs[2]), tol={tol:g}, Jacobi-PCG fp64",
+                       "global_cells": nr * nt * np_, "unknowns": 3 * nr * nt * np_,
+                       "parallelism": f"phi-slab x{world}", "iters_per_solve": iters / args.steps,
+                       "chunk": args.chunk, "l2": "no flush: working set ~4 GB >> 126 MB L2",
+                       "step": "vv_set_coefficients + vv_set_bc_r + vv_solve to tol"},
+            "cell_updates_per_s": nr * nt * np_ * value,
+            "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle as it stands on the box's host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -196,11 +355,16 @@ def main():
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=0, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
+    ap.add_argument("--operator", default="scalar", choices=["scalar", "vv"],
+                    help="scalar: the 7-point parabolic solve (default); vv: the staggered vector viscosity "
+                         "(NEXT-2) on the c3 grid (config c3v)")
     args = ap.parse_args()
     if args.warmup < 3 and args.maxit is None:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.operator == "vv":
+        return run_vv(args)
 
     import torch
     import torch.distributed as dist

@@ -259,6 +259,8 @@ size_t vv_layout(const maspcg_ctx *c, char *base, VVArrays *out) {
     t.WtO = take((nloc + 2) * nt); t.Wp = take(nloc * pl1); t.WpO = take(nloc * nt);
     t.WN = take(nr); t.WS = take(nr);
     t.sM = take(3 * nloc * pl1); t.D = take(3 * nloc * pl1); t.bw = take(3 * nloc * pl1);
+    t.E = take((nloc + 2) * pl1); t.TR = take((nloc + 2) * pl1); t.TT = take((nloc + 2) * pl1);
+    t.TP = take((nloc + 2) * pl1); t.TTO = take((nloc + 2) * nt); t.TPO = take((nloc + 2) * nt);
     t.nu = take(nloc * pl1); t.s = take(nloc * pl1); t.nulo = take(2 * pl1); t.slo = take(2 * pl1);
     t.gin = take((nloc + 2) * 3 * nt); t.gout = take((nloc + 2) * 3 * nt);
     t.p = take((nloc + 2) * 3 * pl1); t.q = take(3 * nloc * pl1); t.r = take(3 * nloc * pl1);
@@ -574,7 +576,7 @@ void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
 }
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
-    if (c->vmode) return 4 + (c->comm ? 1 : 0);   // ring sums (+ combine), matvec, update, p-update
+    if (c->vmode) return 5 + (c->comm ? 1 : 0);   // ring sums (+ combine), terms, rows, update, p-update
     if (use_fused(c) || use_wave(c)) return 2;
     if (!c->comm) return 3;
     return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;

@@ -76,47 +76,59 @@ struct Field {
         if (e == v.nr) return go(k, 0, j);
         return P(k, 0, j, e);
     }
-    // e = wc * delta of cell (i, j, k), k in [-1, nloc-1]
-    __device__ __forceinline__ double ediv(int i, int j, int k) const {
-        const double fr_lo = mul(g.A_r(i, j, k), vr(k, j, i));
-        const double fr_hi = mul(g.A_r(i + 1, j, k), vr(k, j, i + 1));
-        const double ft_lo = (j == 0) ? 0.0 : mul(g.A_t(i, j, k), P(k, 1, j, i));
-        const double ft_hi = (j == v.nt - 1) ? 0.0 : mul(g.A_t(i, j + 1, k), P(k, 1, j + 1, i));
+    // e = wc * delta of cell (i, j, k), k in [-1, nloc-1], from the face values of the cell
+    __device__ __forceinline__ double ediv_v(int i, int j, int k, double vrl, double vrh, double vtl, double vth,
+                                             double vpl, double vph) const {
+        const double fr_lo = mul(g.A_r(i, j, k), vrl);
+        const double fr_hi = mul(g.A_r(i + 1, j, k), vrh);
+        const double ft_lo = (j == 0) ? 0.0 : mul(g.A_t(i, j, k), vtl);
+        const double ft_hi = (j == v.nt - 1) ? 0.0 : mul(g.A_t(i, j + 1, k), vth);
         const double ap = g.A_p(i, j);
-        const double fp_lo = mul(ap, P(k, 2, j, i));
-        const double fp_hi = mul(ap, P(k + 1, 2, j, i));
+        const double fp_lo = mul(ap, vpl);
+        const double fp_hi = mul(ap, vph);
         double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
         d = add(d, sub(fp_hi, fp_lo));
         return mul(__ldg(a.wc + PC(v, k, j, i)), d);
     }
-    // r-edge at theta-face j (1..nt-1), phi-face k (k in [0, nloc])
-    __device__ __forceinline__ double Gr(int i, int j, int k) const {
-        const double gp_a = mul(g.L_p(i + 1, j, k), P(k, 2, j, i));
-        const double gp_b = mul(g.L_p(i + 1, j - 1, k), P(k, 2, j - 1, i));
+    // r-edge at theta-face j (1..nt-1), phi-face k: v_phi(j), v_phi(j-1), v_theta(k), v_theta(k-1)
+    __device__ __forceinline__ double Gr_v(int i, int j, int k, double vpj, double vpjm, double vtk, double vtkm) const {
+        const double gp_a = mul(g.L_p(i + 1, j, k), vpj);
+        const double gp_b = mul(g.L_p(i + 1, j - 1, k), vpjm);
         const double lt = g.L_t(i + 1, j);
-        const double gt_a = mul(lt, P(k, 1, j, i));
-        const double gt_b = mul(lt, P(k - 1, 1, j, i));
+        const double gt_a = mul(lt, vtk);
+        const double gt_b = mul(lt, vtkm);
         return sub(sub(gp_a, gp_b), sub(gt_a, gt_b));
     }
-    // theta-edge at r-face e (0..nr), phi-face k (k in [0, nloc])
-    __device__ __forceinline__ double Gt(int e, int j, int k) const {
-        const double gr_a = mul(a.hr[e], vr(k, j, e));
-        const double gr_b = mul(a.hr[e], vr(k - 1, j, e));
-        const double up = (e < v.nr) ? P(k, 2, j, e) : go(k, 2, j);
-        const double dn = (e > 0) ? P(k, 2, j, e - 1) : gi(k, 2, j);
+    // theta-edge at r-face e (0..nr), phi-face k: v_r(e, k), v_r(e, k-1), v_phi above / below the face
+    __device__ __forceinline__ double Gt_v(int e, int j, int k, double vrk, double vrkm, double up, double dn) const {
+        const double gr_a = mul(a.hr[e], vrk);
+        const double gr_b = mul(a.hr[e], vrkm);
         const double gp_a = mul(g.L_p(e + 1, j, k), up);
         const double gp_b = mul(g.L_p(e, j, k), dn);
         return sub(sub(gr_a, gr_b), sub(gp_a, gp_b));
     }
-    // phi-edge at r-face e (0..nr), theta-face j (1..nt-1)
-    __device__ __forceinline__ double Gp(int e, int j, int k) const {
-        const double up = (e < v.nr) ? P(k, 1, j, e) : go(k, 1, j);
-        const double dn = (e > 0) ? P(k, 1, j, e - 1) : gi(k, 1, j);
+    // phi-edge at r-face e (0..nr), theta-face j (1..nt-1): v_theta above / below, v_r(e, j), v_r(e, j-1)
+    __device__ __forceinline__ double Gp_v(int e, int j, double up, double dn, double vrj, double vrjm) const {
         const double gt_a = mul(g.L_t(e + 1, j), up);
         const double gt_b = mul(g.L_t(e, j), dn);
-        const double gr_a = mul(a.hr[e], vr(k, j, e));
-        const double gr_b = mul(a.hr[e], vr(k, j - 1, e));
+        const double gr_a = mul(a.hr[e], vrj);
+        const double gr_b = mul(a.hr[e], vrjm);
         return sub(sub(gt_a, gt_b), sub(gr_a, gr_b));
+    }
+    __device__ __forceinline__ double ediv(int i, int j, int k) const {
+        return ediv_v(i, j, k, vr(k, j, i), vr(k, j, i + 1), (j == 0) ? 0.0 : P(k, 1, j, i),
+                      (j == v.nt - 1) ? 0.0 : P(k, 1, j + 1, i), P(k, 2, j, i), P(k + 1, 2, j, i));
+    }
+    __device__ __forceinline__ double Gr(int i, int j, int k) const {
+        return Gr_v(i, j, k, P(k, 2, j, i), P(k, 2, j - 1, i), P(k, 1, j, i), P(k - 1, 1, j, i));
+    }
+    __device__ __forceinline__ double Gt(int e, int j, int k) const {
+        return Gt_v(e, j, k, vr(k, j, e), vr(k - 1, j, e), (e < v.nr) ? P(k, 2, j, e) : go(k, 2, j),
+                    (e > 0) ? P(k, 2, j, e - 1) : gi(k, 2, j));
+    }
+    __device__ __forceinline__ double Gp(int e, int j, int k) const {
+        return Gp_v(e, j, (e < v.nr) ? P(k, 1, j, e) : go(k, 1, j), (e > 0) ? P(k, 1, j, e - 1) : gi(k, 1, j),
+                    vr(k, j, e), vr(k, j - 1, e));
     }
 };
 
@@ -294,57 +306,95 @@ __global__ void __launch_bounds__(kVVThreads) k_vv_diag(VVDims v, VVArrays a) {
     }
 }
 
-// ------------------------------------------------------------ the operator (the oracle's apply)
-template <bool WITH_DOT, bool LOOP, bool WALL, bool EXACT>
-__global__ void __launch_bounds__(kVVThreads) k_vv_matvec(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
-                                                          unsigned total) {
-    if (LOOP && *(volatile int *)&base.sc->done) return;
+// ------------------------------------------------------------ the operator (the oracle's apply), two phases
+// Phase 1 (k_vv_terms): per cell of planes -1 .. nloc the products the rows combine -- the outflow term
+// e = wc delta (planes -1 .. nloc-1) and the edge terms tau = W Gamma of the cell's lower r-, theta- and
+// phi-edges (planes 0 .. nloc; the outer-wall edges of the last radial cell into side arrays).
+// Phase 2 (k_vv_rows): the three rows of every local cell from those terms, sM p and the polar-axis
+// terms WN GN, WS GS of the ring sums; Dot2 partial of p.q.  Each product is the one the oracle forms
+// (e = wc * delta, W * Gamma), so the rows are bit-identical.  48 + 32 + 80 + 24 = 184 B/cell instead
+// of the 104 of a fused kernel, but every load is a coalesced stream with no recomputation: the fused
+// form was issue- and occupancy-bound (152 registers, ~1,300 instructions per cell).
+template <bool WALL>
+__global__ void __launch_bounds__(kVVThreads) k_vv_terms(VVDims v, VVArrays a, DevArrays base, int loop) {
+    if (loop && *(volatile int *)&base.sc->done) return;
     const Field<WALL> F{v, a, a.p, Geo{a}};
-    const Geo &g = F.g;
-    // the polar-axis circulations of this radius are read per cell from the ring pairs
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t n = v.ncell + 2 * v.plane1;   // planes -1 .. nloc
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
+        int i, j, k;
+        cell_of(v, c, i, j, k);
+        k -= 1;
+        const size_t pc = PC(v, k, j, i);
+        if (k <= v.nloc - 1) a.E[pc] = F.ediv(i, j, k);
+        if (k >= 0) {
+            a.TR[pc] = (j >= 1) ? mul(__ldg(a.Wr + pc), F.Gr(i, j, k)) : 0.0;
+            a.TT[pc] = mul(__ldg(a.Wt + pc), F.Gt(i, j, k));
+            a.TP[pc] = (j >= 1 && k <= v.nloc - 1) ? mul(Wp_at(v, a, i, j, k), F.Gp(i, j, k)) : 0.0;
+            if (i == v.nr - 1) {
+                const size_t w = (size_t)(k + 1) * v.nt + j;
+                a.TTO[w] = mul(__ldg(a.WtO + w), F.Gt(v.nr, j, k));
+                a.TPO[w] = (j >= 1 && k <= v.nloc - 1) ? mul(Wp_at(v, a, v.nr, j, k), F.Gp(v.nr, j, k)) : 0.0;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ double TT_at(const VVDims &v, const VVArrays &a, int e, int j, int k) {
+    return (e < v.nr) ? __ldg(a.TT + PC(v, k, j, e)) : __ldg(a.TTO + (size_t)(k + 1) * v.nt + j);
+}
+__device__ __forceinline__ double TP_at(const VVDims &v, const VVArrays &a, int e, int j, int k) {
+    return (e < v.nr) ? __ldg(a.TP + PC(v, k, j, e)) : __ldg(a.TPO + (size_t)(k + 1) * v.nt + j);
+}
+
+template <bool WITH_DOT, bool LOOP, bool EXACT>
+__global__ void __launch_bounds__(kVVThreads) k_vv_rows(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
+                                                        unsigned total) {
+    if (LOOP && *(volatile int *)&base.sc->done) return;
+    const Geo g{a};
+    const double *__restrict__ E = a.E;
     Acc<EXACT> dot[1];
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < v.ncell; c += stride) {
         int i, j, k;
         cell_of(v, c, i, j, k);
-        const double e0 = F.ediv(i, j, k);
+        const size_t pc = PC(v, k, j, i);
+        const double e0 = __ldg(E + pc);
         // r-face i
         double yr = 0.0;
-        const double pr = F.P(k, 0, j, i);
+        const double pr = __ldg(a.p + PV(v, k, 0, j, i));
         if (i >= 1) {
             yr = mul(__ldg(a.sM + UV(v, k, 0, j, i)), pr);
-            yr = add(yr, mul(g.A_r(i, j, k), sub(F.ediv(i - 1, j, k), e0)));
-            double cc = mul(Wt_at(v, a, i, j, k), F.Gt(i, j, k));
-            cc = sub(cc, mul(Wt_at(v, a, i, j, k + 1), F.Gt(i, j, k + 1)));
-            if (j >= 1) cc = sub(cc, mul(Wp_at(v, a, i, j, k), F.Gp(i, j, k)));
-            if (j + 1 <= v.nt - 1) cc = add(cc, mul(Wp_at(v, a, i, j + 1, k), F.Gp(i, j + 1, k)));
+            yr = add(yr, mul(g.A_r(i, j, k), sub(__ldg(E + pc - 1), e0)));
+            double cc = __ldg(a.TT + pc);
+            cc = sub(cc, __ldg(a.TT + pc + v.plane1));
+            if (j >= 1) cc = sub(cc, __ldg(a.TP + pc));
+            if (j + 1 <= v.nt - 1) cc = add(cc, __ldg(a.TP + pc + v.nr));
             yr = add(yr, mul(a.hr[i], cc));
         }
         // theta-face j
         double yt = 0.0;
-        const double pt = F.P(k, 1, j, i);
+        const double pt = __ldg(a.p + PV(v, k, 1, j, i));
         if (j >= 1) {
             yt = mul(__ldg(a.sM + UV(v, k, 1, j, i)), pt);
-            yt = add(yt, mul(g.A_t(i, j, k), sub(F.ediv(i, j - 1, k), e0)));
-            double cc = sub(mul(__ldg(a.Wr + PC(v, k + 1, j, i)), F.Gr(i, j, k + 1)),
-                            mul(__ldg(a.Wr + PC(v, k, j, i)), F.Gr(i, j, k)));
-            cc = add(cc, mul(Wp_at(v, a, i, j, k), F.Gp(i, j, k)));
-            cc = sub(cc, mul(Wp_at(v, a, i + 1, j, k), F.Gp(i + 1, j, k)));
+            yt = add(yt, mul(g.A_t(i, j, k), sub(__ldg(E + pc - v.nr), e0)));
+            double cc = sub(__ldg(a.TR + pc + v.plane1), __ldg(a.TR + pc));
+            cc = add(cc, __ldg(a.TP + pc));
+            cc = sub(cc, TP_at(v, a, i + 1, j, k));
             yt = add(yt, mul(g.L_t(i + 1, j), cc));
         }
         // phi-face k
-        const double pp = F.P(k, 2, j, i);
+        const double pp = __ldg(a.p + PV(v, k, 2, j, i));
         double yp = mul(__ldg(a.sM + UV(v, k, 2, j, i)), pp);
-        yp = add(yp, mul(g.A_p(i, j), sub(F.ediv(i, j, k - 1), e0)));
-        double lo, hi;
-        if (j == 0) lo = mul(__ldg(a.WN + i), add(__ldg(a.ring + 2 * i), __ldg(a.ring + 2 * i + 1)));
-        else lo = mul(__ldg(a.Wr + PC(v, k, j, i)), F.Gr(i, j, k));
-        if (j == v.nt - 1)
-            hi = mul(__ldg(a.WS + i), -add(__ldg(a.ring + 2 * (v.nr + i)), __ldg(a.ring + 2 * (v.nr + i) + 1)));
-        else hi = mul(__ldg(a.Wr + PC(v, k, j + 1, i)), F.Gr(i, j + 1, k));
+        yp = add(yp, mul(g.A_p(i, j), sub(__ldg(E + pc - v.plane1), e0)));
+        const double lo = (j == 0) ? mul(__ldg(a.WN + i), add(__ldg(a.ring + 2 * i), __ldg(a.ring + 2 * i + 1)))
+                                   : __ldg(a.TR + pc);
+        const double hi = (j == v.nt - 1)
+                              ? mul(__ldg(a.WS + i), -add(__ldg(a.ring + 2 * (v.nr + i)), __ldg(a.ring + 2 * (v.nr + i) + 1)))
+                              : __ldg(a.TR + pc + v.nr);
         double cc = sub(lo, hi);
-        cc = sub(cc, mul(Wt_at(v, a, i, j, k), F.Gt(i, j, k)));
-        cc = add(cc, mul(Wt_at(v, a, i + 1, j, k), F.Gt(i + 1, j, k)));
+        cc = sub(cc, __ldg(a.TT + pc));
+        cc = add(cc, TT_at(v, a, i + 1, j, k));
         yp = add(yp, mul(g.L_p(i + 1, j, k), cc));
         y[UV(v, k, 0, j, i)] = yr;
         y[UV(v, k, 1, j, i)] = yt;
@@ -353,6 +403,208 @@ __global__ void __launch_bounds__(kVVThreads) k_vv_matvec(VVDims v, VVArrays a, 
             dot[0].add(pr, yr);
             dot[0].add(pt, yt);
             dot[0].add(pp, yp);
+        }
+    }
+    if (WITH_DOT) {
+        Acc<EXACT> out[1];
+        if (reduce_last<EXACT, kVVThreads, 1>(dot, base.partials, &base.sc->ticket[0], blockIdx.x, total, out)) {
+            if (threadIdx.x == 0) {
+                base.sc->red1[0] = out[0].p;
+                base.sc->red1[1] = out[0].s;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ 16-byte pair variants (nr even)
+// Two r-neighbour cells (i0, i0 + 1), i0 even, per thread: every stream is one 16-byte load / store and
+// the shared neighbours are loaded once.  The per-cell arithmetic is the value-based helpers above, so
+// the results are the scalar kernels' bit for bit.  The scalar kernels were latency-bound (about 40 %
+// issue utilisation and 35-48 % of DRAM bandwidth at 50 % occupancy).
+__device__ __forceinline__ double2 L2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
+__device__ __forceinline__ void S2(double *p, double x, double y) {
+    *reinterpret_cast<double2 *>(p) = make_double2(x, y);
+}
+
+template <bool WALL>
+__global__ void __launch_bounds__(kVVThreads, 3) k_vv_terms2(VVDims v, VVArrays a, DevArrays base, int loop) {
+    if (loop && *(volatile int *)&base.sc->done) return;
+    const Field<WALL> F{v, a, a.p, Geo{a}};
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = (v.ncell + 2 * v.plane1) >> 1;   // planes -1 .. nloc
+    const int nr = v.nr, nt = v.nt;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += stride) {
+        int i0, j, k;
+        cell_of(v, 2 * t, i0, j, k);
+        k -= 1;
+        // every load up front (addresses clamped into the arrays; unused values are discarded), so the
+        // memory system sees all of the thread's requests before the first use
+        const int km = k > -1 ? k - 1 : -1, kp = k < v.nloc ? k + 1 : v.nloc, jm = j > 0 ? j - 1 : 0;
+        const int jp = j < nt - 1 ? j + 1 : j, kw = k < 0 ? 0 : (k > v.nloc - 1 ? v.nloc - 1 : k);
+        const size_t pc = PC(v, k, j, i0);
+        const bool last = (i0 + 2 == nr);
+        const double2 R = L2(a.p + PV(v, k, 0, j, i0));
+        const double2 T = L2(a.p + PV(v, k, 1, j, i0));
+        const double2 Pp = L2(a.p + PV(v, k, 2, j, i0));
+        const double2 Tj1 = L2(a.p + PV(v, k, 1, jp, i0));
+        const double2 Pk1 = L2(a.p + PV(v, kp, 2, j, i0));
+        const double2 Rm = L2(a.p + PV(v, km, 0, j, i0));
+        const double2 Pjm = L2(a.p + PV(v, k, 2, jm, i0));
+        const double2 Tkm = L2(a.p + PV(v, km, 1, j, i0));
+        const double2 Rjm = L2(a.p + PV(v, k, 0, jm, i0));
+        const double r2 = __ldg(a.p + PV(v, k, 0, j, last ? i0 : i0 + 2));
+        const double pm1 = __ldg(a.p + PV(v, k, 2, j, i0 > 0 ? i0 - 1 : 0));
+        const double tm1 = __ldg(a.p + PV(v, k, 1, j, i0 > 0 ? i0 - 1 : 0));
+        const double2 wt = L2(a.Wt + pc), wr = L2(a.Wr + pc), wp = L2(a.Wp + UC(v, kw, j, i0));
+        const double vr0 = (i0 == 0) ? F.gi(k, 0, j) : R.x;          // v_r on r-face i0 (wall at 0)
+        const double vr2 = last ? F.go(k, 0, j) : r2;
+        if (k <= v.nloc - 1) {
+            const double e0 = F.ediv_v(i0, j, k, vr0, R.y, T.x, Tj1.x, Pp.x, Pk1.x);
+            const double e1 = F.ediv_v(i0 + 1, j, k, R.y, vr2, T.y, Tj1.y, Pp.y, Pk1.y);
+            S2(a.E + pc, e0, e1);
+        }
+        if (k >= 0) {
+            const double vrm0 = (i0 == 0) ? F.gi(k - 1, 0, j) : Rm.x;
+            const double dn0 = (i0 == 0) ? F.gi(k, 2, j) : pm1;
+            S2(a.TT + pc, mul(wt.x, F.Gt_v(i0, j, k, vr0, vrm0, Pp.x, dn0)),
+               mul(wt.y, F.Gt_v(i0 + 1, j, k, R.y, Rm.y, Pp.y, Pp.x)));
+            double tr0 = 0.0, tr1 = 0.0, tp0 = 0.0, tp1 = 0.0;
+            if (j >= 1) {
+                tr0 = mul(wr.x, F.Gr_v(i0, j, k, Pp.x, Pjm.x, T.x, Tkm.x));
+                tr1 = mul(wr.y, F.Gr_v(i0 + 1, j, k, Pp.y, Pjm.y, T.y, Tkm.y));
+                if (k <= v.nloc - 1) {
+                    const double vrjm0 = (i0 == 0) ? F.gi(k, 0, j - 1) : Rjm.x;
+                    const double tdn0 = (i0 == 0) ? F.gi(k, 1, j) : tm1;
+                    tp0 = mul(wp.x, F.Gp_v(i0, j, T.x, tdn0, vr0, vrjm0));
+                    tp1 = mul(wp.y, F.Gp_v(i0 + 1, j, T.y, T.x, R.y, Rjm.y));
+                }
+            }
+            S2(a.TR + pc, tr0, tr1);
+            S2(a.TP + pc, tp0, tp1);
+            if (last) {
+                const size_t w = (size_t)(k + 1) * nt + j;
+                a.TTO[w] = mul(__ldg(a.WtO + w), F.Gt_v(nr, j, k, F.go(k, 0, j), F.go(k - 1, 0, j), F.go(k, 2, j), Pp.y));
+                a.TPO[w] = (j >= 1 && k <= v.nloc - 1)
+                               ? mul(__ldg(a.WpO + (size_t)k * nt + j),
+                                     F.Gp_v(nr, j, F.go(k, 1, j), T.y, F.go(k, 0, j), F.go(k, 0, j - 1)))
+                               : 0.0;
+            }
+        }
+    }
+}
+
+template <bool WITH_DOT, bool LOOP, bool EXACT>
+__global__ void __launch_bounds__(kVVThreads, 3) k_vv_rows2(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
+                                                         unsigned total) {
+    if (LOOP && *(volatile int *)&base.sc->done) return;
+    const Geo g{a};
+    const double *__restrict__ E = a.E;
+    const int nr = v.nr, nt = v.nt;
+    const uint32_t pl = v.plane1;
+    Acc<EXACT> dot[1];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = v.ncell >> 1;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += stride) {
+        int i0, j, k;
+        cell_of(v, 2 * t, i0, j, k);
+        const size_t pc = PC(v, k, j, i0);
+        const bool last = (i0 + 2 == nr);
+        const double2 e = L2(E + pc);
+        const double2 pr = L2(a.p + PV(v, k, 0, j, i0));
+        const double2 pt = L2(a.p + PV(v, k, 1, j, i0));
+        const double2 pp = L2(a.p + PV(v, k, 2, j, i0));
+        const double2 tt = L2(a.TT + pc), tt1 = L2(a.TT + pc + pl);
+        const double tt2 = last ? __ldg(a.TTO + (size_t)(k + 1) * nt + j) : __ldg(a.TT + pc + 2);
+        const double2 tr = L2(a.TR + pc);
+        const double2 tp = L2(a.TP + pc);
+        const double tp2 = last ? __ldg(a.TPO + (size_t)(k + 1) * nt + j) : __ldg(a.TP + pc + 2);
+        // the remaining streams up front (addresses inside the padded arrays; unused values discarded)
+        const double em1 = __ldg(E + pc - 1);
+        const double2 tpj = L2(a.TP + pc + nr);
+        const double2 ej = L2(E + pc - nr);
+        const double2 ek = L2(E + pc - pl);
+        const double2 tr1 = L2(a.TR + pc + pl);
+        const double2 trj = L2(a.TR + pc + nr);
+        const double2 sm0 = L2(a.sM + UV(v, k, 0, j, i0));
+        const double2 sm1 = L2(a.sM + UV(v, k, 1, j, i0));
+        const double2 sm2 = L2(a.sM + UV(v, k, 2, j, i0));
+        // r-faces i0 (i0 >= 1) and i0 + 1
+        double yr0 = 0.0, yr1;
+        {
+            const double2 sm = sm0;
+            if (i0 >= 1) {
+                yr0 = mul(sm.x, pr.x);
+                yr0 = add(yr0, mul(g.A_r(i0, j, k), sub(em1, e.x)));
+                double cc = sub(tt.x, tt1.x);
+                if (j >= 1) cc = sub(cc, tp.x);
+                if (j + 1 <= nt - 1) cc = add(cc, tpj.x);
+                yr0 = add(yr0, mul(a.hr[i0], cc));
+            }
+            yr1 = mul(sm.y, pr.y);
+            yr1 = add(yr1, mul(g.A_r(i0 + 1, j, k), sub(e.x, e.y)));
+            double cc = sub(tt.y, tt1.y);
+            if (j >= 1) cc = sub(cc, tp.y);
+            if (j + 1 <= nt - 1) cc = add(cc, tpj.y);
+            yr1 = add(yr1, mul(a.hr[i0 + 1], cc));
+        }
+        // theta-faces j (j >= 1)
+        double yt0 = 0.0, yt1 = 0.0;
+        if (j >= 1) {
+            const double2 sm = sm1;
+            yt0 = mul(sm.x, pt.x);
+            yt0 = add(yt0, mul(g.A_t(i0, j, k), sub(ej.x, e.x)));
+            double cc = sub(tr1.x, tr.x);
+            cc = add(cc, tp.x);
+            cc = sub(cc, tp.y);
+            yt0 = add(yt0, mul(g.L_t(i0 + 1, j), cc));
+            yt1 = mul(sm.y, pt.y);
+            yt1 = add(yt1, mul(g.A_t(i0 + 1, j, k), sub(ej.y, e.y)));
+            cc = sub(tr1.y, tr.y);
+            cc = add(cc, tp.y);
+            cc = sub(cc, tp2);
+            yt1 = add(yt1, mul(g.L_t(i0 + 2, j), cc));
+        }
+        // phi-faces k
+        double yp0, yp1;
+        {
+            const double2 sm = sm2;
+            double2 lo, hi;
+            if (j == 0) {
+                lo.x = mul(__ldg(a.WN + i0), add(__ldg(a.ring + 2 * i0), __ldg(a.ring + 2 * i0 + 1)));
+                lo.y = mul(__ldg(a.WN + i0 + 1), add(__ldg(a.ring + 2 * i0 + 2), __ldg(a.ring + 2 * i0 + 3)));
+            } else {
+                lo = tr;
+            }
+            if (j == nt - 1) {
+                const double *rs = a.ring + 2 * (nr + i0);
+                hi.x = mul(__ldg(a.WS + i0), -add(__ldg(rs), __ldg(rs + 1)));
+                hi.y = mul(__ldg(a.WS + i0 + 1), -add(__ldg(rs + 2), __ldg(rs + 3)));
+            } else {
+                hi = trj;
+            }
+            yp0 = mul(sm.x, pp.x);
+            yp0 = add(yp0, mul(g.A_p(i0, j), sub(ek.x, e.x)));
+            double cc = sub(lo.x, hi.x);
+            cc = sub(cc, tt.x);
+            cc = add(cc, tt.y);
+            yp0 = add(yp0, mul(g.L_p(i0 + 1, j, k), cc));
+            yp1 = mul(sm.y, pp.y);
+            yp1 = add(yp1, mul(g.A_p(i0 + 1, j), sub(ek.y, e.y)));
+            cc = sub(lo.y, hi.y);
+            cc = sub(cc, tt.y);
+            cc = add(cc, tt2);
+            yp1 = add(yp1, mul(g.L_p(i0 + 2, j, k), cc));
+        }
+        S2(y + UV(v, k, 0, j, i0), yr0, yr1);
+        S2(y + UV(v, k, 1, j, i0), yt0, yt1);
+        S2(y + UV(v, k, 2, j, i0), yp0, yp1);
+        if (WITH_DOT) {
+            dot[0].add(pr.x, yr0);
+            dot[0].add(pt.x, yt0);
+            dot[0].add(pp.x, yp0);
+            dot[0].add(pr.y, yr1);
+            dot[0].add(pt.y, yt1);
+            dot[0].add(pp.y, yp1);
         }
     }
     if (WITH_DOT) {
@@ -425,6 +677,24 @@ __global__ void __launch_bounds__(kVVThreads) k_vv_mask(VVDims v, double *__rest
     }
 }
 
+// all blocks resident at once (no partial last wave): SMs x the kernel's occupancy, at most one block per
+// 256 work items
+template <typename K>
+unsigned resident_grid(K kern, uint32_t n) {
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kVVThreads, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    uint64_t g = (n + kVVThreads - 1) / kVVThreads;
+    const uint64_t cap = (uint64_t)sms * per_sm < (uint64_t)kRedBlocks ? (uint64_t)sms * per_sm : kRedBlocks;
+    if (g > cap) g = cap;
+    return g < 1 ? 1u : (unsigned)g;
+}
+
 inline unsigned vv_grid(uint32_t n) {
     uint64_t g = (n + kVVThreads - 1) / kVVThreads;
     if (g < 1) g = 1;
@@ -458,20 +728,36 @@ void launch_vv_diag(const VVDims &v, const VVArrays &a, cudaStream_t st) {
 
 void launch_vv_matvec(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
                       bool wall, bool exact, cudaStream_t st) {
-    const unsigned g = vv_grid(v.ncell);
-#define VM(W, L, WL, E) k_vv_matvec<W, L, WL, E><<<g, kVVThreads, 0, st>>>(v, a, base, y, g)
-    if (wall) {
-        VM(false, false, true, true);
-    } else if (!with_dot) {
-        VM(false, false, false, true);
-    } else if (exact) {
-        if (loop) VM(true, true, false, true);
-        else VM(true, false, false, true);
+    const bool pair = (v.nr % 2 == 0) && (((uintptr_t)y & 15) == 0);
+    const uint32_t nt1 = v.ncell + 2 * v.plane1;
+    if (pair) {
+        if (wall) k_vv_terms2<true><<<resident_grid(k_vv_terms2<true>, nt1 / 2), kVVThreads, 0, st>>>(v, a, base, 0);
+        else k_vv_terms2<false><<<resident_grid(k_vv_terms2<false>, nt1 / 2), kVVThreads, 0, st>>>(v, a, base, loop ? 1 : 0);
     } else {
-        if (loop) VM(true, true, false, false);
-        else VM(true, false, false, false);
+        const unsigned gt = vv_grid(nt1);
+        if (wall) k_vv_terms<true><<<gt, kVVThreads, 0, st>>>(v, a, base, 0);
+        else k_vv_terms<false><<<gt, kVVThreads, 0, st>>>(v, a, base, loop ? 1 : 0);
     }
-#undef VM
+#define VR(W, L, E)                                                                                   \
+    do {                                                                                              \
+        if (pair) {                                                                                   \
+            const unsigned g = resident_grid(k_vv_rows2<W, L, E>, v.ncell / 2);                        \
+            k_vv_rows2<W, L, E><<<g, kVVThreads, 0, st>>>(v, a, base, y, g);                          \
+        } else {                                                                                      \
+            const unsigned g = vv_grid(v.ncell);                                                      \
+            k_vv_rows<W, L, E><<<g, kVVThreads, 0, st>>>(v, a, base, y, g);                           \
+        }                                                                                             \
+    } while (0)
+    if (!with_dot) {
+        VR(false, false, true);
+    } else if (exact) {
+        if (loop) VR(true, true, true);
+        else VR(true, false, true);
+    } else {
+        if (loop) VR(true, true, false);
+        else VR(true, false, false);
+    }
+#undef VR
 }
 
 void launch_vv_setup_residual(const VVDims &v, const VVArrays &a, const DevArrays &base, const Dims &dv,

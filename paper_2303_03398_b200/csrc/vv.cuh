@@ -42,6 +42,10 @@ struct VVArrays {
     double *sM;     // [nloc][3][nt][nr] s_f M_f
     double *D;      // [nloc][3][nt][nr] Jacobi diagonal (1 on non-unknown slots)
     double *bw;     // [nloc][3][nt][nr] A(0; g): the wall-data part of the rhs
+    // matvec phase-1 terms (planes -1 .. nloc; padded like wc)
+    double *E;      // [nloc+2][nt][nr] wc * delta
+    double *TR, *TT, *TP;   // [nloc+2][nt][nr] W Gamma of the lower r-, theta-, phi-edges of each cell
+    double *TTO, *TPO;      // [nloc+2][nt]     the same on the outer wall (r-face nr)
     // inputs (consumed copies) and wall data
     double *nu, *s;          // [nloc][nt][nr]
     double *nulo, *slo;      // [nt][nr] plane k0-1 of nu, s (received, nranks > 1)
