@@ -54,6 +54,7 @@ def lib():
             "masoracle_pcg": [i, i, i, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
             "masoracle_face_coefficients": [i, i, i, d, ctypes.c_double, i, i, d, ctypes.c_double, d, d, d, d],
             "masoracle_rkl2_step": [i, i, i, d, d, d, d, d, d, d, d, ctypes.c_double, i, d],
+            "masoracle_pcg_cg1": [i, i, i, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
             "masoracle_vv_check_grid": [i, i, i, d, d, d],
             "masoracle_vv_coefficients": [i, i, i, d, d, d, d, d, i, i, d, d, d, d, d, d, d],
             "masoracle_vv_div": [i, i, i, d, d, d, d, d, d, d],
@@ -171,27 +172,29 @@ class Operator:
             raise OracleError(st, "rkl2_step")
         return out
 
-    def pcg(self, b, x0, tol, maxit):
-        """Returns (status, x, iters, hist[0..iters], bnorm, rnorm)."""
+    def pcg(self, b, x0, tol, maxit, variant="hs"):
+        """Returns (status, x, iters, hist[0..iters], bnorm, rnorm).  variant "hs": the Hestenes-Stiefel
+        PCG of SURVEY 8(c) item 7; "cg1": the single-reduction Chronopoulos-Gear variant (R32)."""
         b = _c(b)
         x = np.array(_c(x0), copy=True)
         hist = np.zeros(maxit + 1)
         iters = ctypes.c_int(0)
         bn, rn = ctypes.c_double(0), ctypes.c_double(0)
-        st = lib().masoracle_pcg(self.nr, self.nt, self.np, _p(self.Tr), _p(self.Tt), _p(self.Tp),
+        fn = lib().masoracle_pcg if variant == "hs" else lib().masoracle_pcg_cg1
+        st = fn(self.nr, self.nt, self.np, _p(self.Tr), _p(self.Tt), _p(self.Tp),
                                  _p(self.D), _p(b), _p(x), float(tol), int(maxit), _p(hist),
                                  ctypes.byref(iters), ctypes.byref(bn), ctypes.byref(rn))
         return st, x, iters.value, hist[: iters.value + 1].copy(), bn.value, rn.value
 
 
-def solve_problem(prob, tol=None, maxit=None, x0=None):
+def solve_problem(prob, tol=None, maxit=None, x0=None, variant="hs"):
     """Solve an ``inputs.Problem`` covering the whole global grid (k0 = 0, nloc = np)."""
     assert prob.k0 == 0 and prob.nloc == prob.np, "the oracle works on the global grid"
     op = Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
     b = op.rhs(prob.f, prob.g_in, prob.g_out)
     st, x, iters, hist, bn, rn = op.pcg(b, prob.x0 if x0 is None else x0,
                                         prob.tol if tol is None else tol,
-                                        prob.maxit if maxit is None else maxit)
+                                        prob.maxit if maxit is None else maxit, variant)
     return dict(status=st, x=x, iters=iters, hist=hist, bnorm=bn, rnorm=rn, op=op, b=b)
 
 

@@ -468,6 +468,81 @@ done:
     return status;
 }
 
+/* Single-reduction point-Jacobi PCG: the Chronopoulos-Gear variant (Chronopoulos & Gear, J. Comput.
+ * Appl. Math. 25, 1989; SURVEY 8(f) NEXT-3 "single-reduction (Chronopoulos-Gear) ... CG"; reading R32).
+ * All three dot products of an iteration follow ONE operator application, so a distributed solve needs
+ * one all-reduce per iteration instead of two:
+ *   r0 = b - A x0; u0 = r0/D; w0 = A u0; gamma0 = r0.u0; delta0 = w0.u0; hist[0] = ||r0||
+ *   for k = 1..maxit:
+ *     k == 1: beta = 0, den = delta;  else: beta = gamma/gamma_old, den = delta - (beta gamma)/alpha_old
+ *     den <= 0 or non-finite -> E_BREAKDOWN
+ *     alpha = gamma/den; p = u + beta p; s = w + beta s; x += alpha p; r -= alpha s
+ *     hist[k] = ||r||; hist[k] <= tol*bn -> OK, iters k
+ *     u = r/D; w = A u; gamma_old = gamma; alpha_old = alpha; gamma = r.u; delta = w.u
+ * In exact arithmetic s = A p, den = p.Ap and the iterates are those of masoracle_pcg; in floating
+ * point they differ at rounding level (the recurrences replace p.Ap).  Early exits, norms and the
+ * stopping test as masoracle_pcg (R12-R14). */
+int masoracle_pcg_cg1(int nr, int nt, int np, const double *Tr, const double *Tt, const double *Tp, const double *D,
+                      const double *b, double *x, double tol, int maxit, double *hist, int *iters, double *bnorm,
+                      double *rnorm) {
+    size_t n = (size_t)nr * nt * np;
+    if (maxit < 0 || !(tol >= 0.0)) return MO_E_INVALID;
+    *iters = 0;
+    double bn = sqrt(mo_dot(n, b, b));
+    *bnorm = bn;
+    if (!isfinite(bn)) { *rnorm = bn; return MO_E_BREAKDOWN; }
+    if (bn == 0.0) {
+        for (size_t c = 0; c < n; c++) x[c] = 0.0;
+        if (hist) hist[0] = 0.0;
+        *rnorm = 0.0;
+        return MO_OK;
+    }
+    double *r = malloc(sizeof(double) * n), *u = malloc(sizeof(double) * n), *w = malloc(sizeof(double) * n);
+    double *p = calloc(n, sizeof(double)), *s = calloc(n, sizeof(double));
+    if (!r || !u || !w || !p || !s) { free(r); free(u); free(w); free(p); free(s); return MO_E_NOMEM; }
+    int status = MO_NOT_CONVERGED;
+    masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, x, w);
+    for (size_t c = 0; c < n; c++) r[c] = b[c] - w[c];
+    double rn = sqrt(mo_dot(n, r, r));
+    if (hist) hist[0] = rn;
+    *rnorm = rn;
+    if (!isfinite(rn)) { status = MO_E_BREAKDOWN; goto done; }
+    if (rn <= tol * bn) { status = MO_OK; goto done; }
+    for (size_t c = 0; c < n; c++) u[c] = r[c] / D[c];
+    masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, u, w);
+    double gamma = mo_dot(n, r, u), delta = mo_dot(n, w, u), gamma_old = 0.0, alpha_old = 0.0;
+    for (int k = 1; k <= maxit; k++) {
+        double beta = 0.0, den = delta;
+        if (k > 1) {
+            beta = gamma / gamma_old;
+            double t = beta * gamma;
+            t = t / alpha_old;
+            den = delta - t;
+        }
+        if (!(den > 0.0) || !isfinite(den) || !isfinite(gamma)) { status = MO_E_BREAKDOWN; break; }
+        double alpha = gamma / den;
+        for (size_t c = 0; c < n; c++) p[c] = u[c] + beta * p[c];
+        for (size_t c = 0; c < n; c++) s[c] = w[c] + beta * s[c];
+        for (size_t c = 0; c < n; c++) x[c] = x[c] + alpha * p[c];
+        for (size_t c = 0; c < n; c++) r[c] = r[c] - alpha * s[c];
+        rn = sqrt(mo_dot(n, r, r));
+        if (hist) hist[k] = rn;
+        *iters = k;
+        *rnorm = rn;
+        if (!isfinite(rn)) { status = MO_E_BREAKDOWN; break; }
+        if (rn <= tol * bn) { status = MO_OK; break; }
+        for (size_t c = 0; c < n; c++) u[c] = r[c] / D[c];
+        masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, u, w);
+        gamma_old = gamma;
+        alpha_old = alpha;
+        gamma = mo_dot(n, r, u);
+        delta = mo_dot(n, w, u);
+    }
+done:
+    free(r); free(u); free(w); free(p); free(s);
+    return status;
+}
+
 /* ---------------------------------------------------- super-time-stepping (NEXT-4) */
 
 /* RKL2 coefficients (Meyer, Balsara & Aslam 2014, J. Comput. Phys. 257, eq. 16-17; reading R26):

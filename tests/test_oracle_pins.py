@@ -485,3 +485,57 @@ def test_rkl2_stable_up_to_its_bound(oracle_mod):
     for _ in range(30):
         v = op.rkl2_step(v, p.s, 1.3 * bound, s)
     assert energy(v) > 1e3 * energy(np.random.default_rng(6).standard_normal(op.shape))
+
+
+# ------------------------------------------------------------------ single-reduction PCG (NEXT-3, R32)
+@pytest.mark.parametrize("seed,shape,bc", [(21, (4, 4, 8), (0, 1)), (23, (3, 5, 4), (1, 0)), (24, (5, 3, 2), (0, 0))])
+def test_cg1_matches_dense_lu(oracle_mod, seed, shape, bc):
+    """Chronopoulos-Gear PCG at tol 1e-14 = dense LU to 1e-12; its recurrence residual tracks b - A x."""
+    nr, nt, np_ = shape
+    p = inputs.random_problem(nr, nt, np_, seed, bc_in=bc[0], bc_out=bc[1])
+    op = op_from(oracle_mod, p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, *bc)
+    A = dense(op)
+    b = op.rhs(p.f, p.g_in, p.g_out)
+    x_lu = np.linalg.solve(A, b.ravel())
+    st, x, iters, hist, bn, rn = op.pcg(b, np.zeros(op.shape), 1e-14, 500, variant="cg1")
+    assert st == 0
+    assert np.linalg.norm(x.ravel() - x_lu) <= 1e-12 * np.linalg.norm(x_lu)
+    assert hist[-1] <= 1e-14 * bn and hist[-2] > 1e-14 * bn
+    assert np.linalg.norm(b.ravel() - A @ x.ravel()) <= 1e-13 * bn
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_cg1_is_cg_in_exact_arithmetic(oracle_mod, name):
+    """In exact arithmetic the Chronopoulos-Gear recurrences reproduce CG (s = A p, den = p.Ap), so on
+    the configs both variants need the same iterations (c1 130, c2 406), their solutions agree
+    to 1e-13 and their residual histories to 1e-8 above the rounding floor."""
+    p = inputs.make_problem(name)
+    a = oracle_mod.solve_problem(p)
+    c = oracle_mod.solve_problem(p, variant="cg1")
+    assert a["status"] == c["status"] == 0 and a["iters"] == c["iters"]
+    assert np.linalg.norm(a["x"] - c["x"]) <= 1e-13 * np.linalg.norm(a["x"])
+    floor = 1e-12 * a["bnorm"]
+    m = a["hist"] > floor
+    assert np.max(np.abs(a["hist"][m] - c["hist"][m]) / a["hist"][m]) <= 1e-8
+
+
+def test_cg1_special_cases(oracle_mod):
+    """kappa = 0 -> one iteration, x = f/s; the circulant phi ring within floor(np/2)+1 iterations;
+    tol = 0 -> exactly maxit iterations; b = 0 -> x = 0."""
+    nr, nt, np_ = 6, 5, 4
+    p = inputs.random_problem(nr, nt, np_, 41, bc_in=1, bc_out=1)
+    z = lambda a: np.zeros_like(a)
+    op = op_from(oracle_mod, p.rf, p.tf, p.pf, z(p.kr), z(p.kt), z(p.kp), p.s, 1, 1)
+    st, x, iters, *_ = op.pcg(op.rhs(p.f), np.zeros(op.shape), 1e-12, 10, variant="cg1")
+    assert st == 0 and iters == 1
+    np.testing.assert_allclose(x, p.f / p.s, rtol=1e-15)
+    rf, tf, pf = np.array([1.0, 2.0]), np.array([PI / 3, 2 * PI / 3]), inputs.pfaces(16)
+    kr, kt, kp, s = const_fields(1, 1, 16, kappa=1.0, s=0.2)
+    op = op_from(oracle_mod, rf, tf, pf, kr, kt, kp, s, 1, 1)
+    bb = np.random.default_rng(7).standard_normal(16).reshape(op.shape)
+    st, x, iters, *_ = op.pcg(bb, np.zeros(op.shape), 1e-14, 100, variant="cg1")
+    assert st == 0 and iters <= 16 // 2 + 1
+    st, x, iters, hist, *_ = op.pcg(bb, np.zeros(op.shape), 0.0, 5, variant="cg1")
+    assert st == oracle_mod.NOT_CONVERGED and iters == 5 and hist.size == 6
+    st, x, iters, *_ = op.pcg(np.zeros(op.shape), bb, 1e-10, 5, variant="cg1")
+    assert st == 0 and iters == 0 and not x.any()
