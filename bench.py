@@ -40,6 +40,9 @@ PATHS = {
         "update": ("pass B: r-update + Jacobi + r.z, r.r (k_pass_b)", 32), "pupdate": None, "iter": 112},
     3: {"name": "wave", "stencil": ("wave: x/p-update + stencil + p.q, flag-ordered (k_wave)", 80),
         "update": ("update_jacobi_dots (k_update_vec2)", 32), "pupdate": None, "iter": 112},
+    4: {"name": "single reduction (Chronopoulos-Gear)",
+        "stencil": ("cg1 matvec: u = r/D on the fly, w = A u, Dot2 r.u, w.u, r.r (k_cg1_matvec)", 48),
+        "update": ("cg1 update: convergence, p, s, x, r (k_cg1_update)", 80), "pupdate": None, "iter": 128},
 }
 
 
@@ -347,7 +350,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
-    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 three kernels, 2 fused two passes, 3 wave")
+    ap.add_argument("--path", type=int, default=0,
+                    help="0 auto, 1 three kernels, 2 fused two passes, 3 wave, 4 single reduction (Chronopoulos-Gear)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch of the loop kernels")
     ap.add_argument("--kernel-timing", type=int, default=2,
                     help="CUDA events around the hot kernels in the timed region: 2 sampled (slot 0 of every "

@@ -105,7 +105,7 @@ typedef struct {
     long long pupdate_launches;
     double comm_ms;                /* halo + all-reduce time on the comm path (timing mode, P > 1) */
     int path;                      /* iteration path of the last solve: 1 = three kernels, 2 = fused two passes,
-                                      3 = wave, 4 = vector viscosity (ring + matvec + update + p-update) */
+                                      3 = wave, 4 = single reduction, 5 = vector viscosity */
 } maspcg_stats;
 
 /* Options for maspcg_set_option(). */
@@ -131,7 +131,10 @@ typedef enum {
                                     (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell),
                                     3 = wave (single rank): r-update, then the p-update of iteration k and the stencil
                                     of iteration k+1 in one persistent kernel ordered by plane-completion flags, p and D
-                                    re-read from L2 (112 B/cell of HBM traffic) */
+                                    re-read from L2 (112 B/cell of HBM traffic); 4 = single reduction (Chronopoulos-Gear
+                                    PCG, R32): an update kernel and a matvec that forms u = r/D on the fly and reduces
+                                    r.u, w.u and r.r together -- ONE all-reduce per iteration on P > 1 (128 B/cell);
+                                    its iterates are those of the oracle's single-reduction variant */
 } maspcg_option;
 
 /* ---- lifetime ----------------------------------------------------------- */

@@ -67,6 +67,9 @@ struct Scalars {
     double hist0;            // ||r_0||
     double rn;               // ||r_iter||
     double alpha;            // alpha of the last completed iteration (fused path: deferred x update)
+    double red_cg[6];        // single-reduction path: (gamma = r.u, delta = w.u, r.r) Dot2 pairs
+    double cg_gamma_old;     // single-reduction path: gamma and alpha of the previous iteration
+    double cg_alpha_old;
     int iter;                // completed PCG iterations
     int maxit;
     int done;                // 1: every loop kernel returns at entry
@@ -127,6 +130,10 @@ struct DevArrays {
     double *P[2];       // [nloc][nt][nr] search directions of even / odd iterations
     double *rh, *dh, *ph;   // [2][nt][nr] received halo planes (lo, hi) of r, D, p_old (nranks > 1)
     double *fh;             // [2][nt][nr] received halo planes of a physical field (from_fields, nranks > 1)
+    // single-reduction (Chronopoulos-Gear) path, MASPCG_OPT_PATH = 4 (cg1.cu); p lives in q
+    double *cgr;            // [nloc+2][nt][nr] r with halo planes
+    double *cgw;            // [nloc][nt][nr]   w = A u, u = r / D
+    double *cgs;            // [nloc][nt][nr]   s (= A p in exact arithmetic)
     // super-time-stepping (NEXT-4)
     double *sy[4];          // [nloc+2][nt][nr] x4: three rotating RKL2 stages and Y0
     double *sl0;            // [nloc][nt][nr]   L(Y0)

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/maspcg.h"
+#include "cg1.cuh"
 #include "comm.cuh"
 #include "common.cuh"
 #include "fused.cuh"
@@ -144,6 +145,9 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     t.fh = (double *)take(8 * 2 * plane);
     for (int b = 0; b < 4; ++b) t.sy[b] = (double *)take(8 * (n + 2 * plane));   // STS: Y0 and 3 rotating stages
     t.sl0 = (double *)take(8 * n);
+    t.cgr = (double *)take(8 * (n + 2 * plane));
+    t.cgw = (double *)take(8 * n);
+    t.cgs = (double *)take(8 * n);
     const size_t tpp = (size_t)wave_tiles_per_plane((uint32_t)plane);
     t.wave_counter = (unsigned *)take(256);
     t.wave_flags = (unsigned *)take(4 * (size_t)c->nloc);
@@ -227,9 +231,10 @@ maspcg_status halo_planes(maspcg_ctx *c, const double *arr, double *halo, cudaSt
 bool use_fused(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 2 && c->fused_bj > 0; }
 bool use_wave(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 3 && !c->comm; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
+bool use_cg1(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 4; }
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
-           (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0);
+           (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0) | (use_cg1(c) ? 256 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -510,7 +515,44 @@ maspcg_status enqueue_iteration_wave(maspcg_ctx *c, double *x, cudaStream_t st, 
     return MASPCG_OK;
 }
 
+// One iteration of the single-reduction path (cg1.cu): update (with the convergence test of the
+// previous iterate), r halo planes overlapped with the interior of the matvec, one all-reduce.
+maspcg_status cg1_matvec(maspcg_ctx *c, bool loop, cudaStream_t st) {
+    if (!c->comm) {
+        launch_cg1_matvec(c->d, c->a, StencilPart::Full, loop, 0, cg1_matvec_blocks(c->d, StencilPart::Full),
+                          exact_arith(c), st);
+        return MASPCG_OK;
+    }
+    CK(c, cudaEventRecord(c->ev_p, st));
+    CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
+    RET_IF(halo_padded(c, c->a.cgr, c->comm_stream));
+    CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
+    const unsigned gi = cg1_matvec_blocks(c->d, StencilPart::Interior);
+    const unsigned gb = cg1_matvec_blocks(c->d, StencilPart::Boundary);
+    launch_cg1_matvec(c->d, c->a, StencilPart::Interior, loop, 0, gi + gb, exact_arith(c), st);
+    CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+    launch_cg1_matvec(c->d, c->a, StencilPart::Boundary, loop, gi, gi + gb, exact_arith(c), st);
+    return MASPCG_OK;
+}
+
+maspcg_status enqueue_iteration_cg1(maspcg_ctx *c, double *x, cudaStream_t st, int it) {
+    const bool tm = timed_slot(c, it);
+    if (tm) CK(c, record_timing(c, 1, 0, it, st));
+    launch_cg1_update(c->d, c->a, x, exact_arith(c), st);
+    if (tm) CK(c, record_timing(c, 1, 1, it, st));
+    if (tm) CK(c, record_timing(c, 0, 0, it, st));
+    RET_IF(cg1_matvec(c, true, st));
+    if (tm) CK(c, record_timing(c, 0, 1, it, st));
+    RET_IF(allreduce_dot2(c, c->a.sc->red_cg, 3, st));
+    if (tm) {
+        CK(c, record_timing(c, 2, 0, it, st));
+        CK(c, record_timing(c, 2, 1, it, st));
+    }
+    return MASPCG_OK;
+}
+
 maspcg_status enqueue_any(maspcg_ctx *c, double *x, cudaStream_t st, int slot) {
+    if (use_cg1(c)) return enqueue_iteration_cg1(c, x, st, slot);
     if (use_wave(c)) return enqueue_iteration_wave(c, x, st, slot);
     return use_fused(c) ? enqueue_iteration_fused(c, x, st, slot) : enqueue_iteration(c, x, st, slot);
 }
@@ -577,6 +619,7 @@ void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
     if (c->vmode) return 5 + (c->comm ? 1 : 0);   // ring sums (+ combine), terms, rows, update, p-update
+    if (use_cg1(c)) return 2 + (c->comm ? 2 : 0);   // update, matvec (interior + boundary, combine)
     if (use_fused(c) || use_wave(c)) return 2;
     if (!c->comm) return 3;
     return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
@@ -609,9 +652,23 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     else
         launch_setup_residual(c->d, c->a, rhs, c->bc_in == BC_DIRICHLET && c->has_gin,
                               c->bc_out == BC_DIRICHLET && c->has_gout, exact_arith(c), st);
+    if (use_cg1(c)) {   // the local r0.u0 and r0.r0 travel with the first w.u (one all-reduce)
+        CK(c, cudaMemcpyAsync(c->a.sc->red_cg, c->a.sc->red3, 16, cudaMemcpyDeviceToDevice, st));
+        CK(c, cudaMemcpyAsync(c->a.sc->red_cg + 4, c->a.sc->red3 + 2, 16, cudaMemcpyDeviceToDevice, st));
+    }
     RET_IF(allreduce_dot2(c, c->a.sc->red3, 3, st));
     if (fused && c->comm) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
     launch_setup_scalars(c->a, tol, maxit, st);
+    const bool cg1 = use_cg1(c);
+    if (cg1) {
+        // single-reduction start: u0 = z0 (the padded p of the setup, periodic copies included), p = s = 0,
+        // then w0 = A u0 and delta0 = w0.u0
+        CK(c, cudaMemcpyAsync(c->a.cgr, c->a.p, 8 * (n + 2 * (size_t)c->d.plane), cudaMemcpyDeviceToDevice, st));
+        CK(c, cudaMemsetAsync(c->a.q, 0, 8 * n, st));
+        CK(c, cudaMemsetAsync(c->a.cgs, 0, 8 * n, st));
+        RET_IF(cg1_matvec(c, true, st));
+        RET_IF(allreduce_dot2(c, c->a.sc->red_cg, 3, st));
+    }
     if (use_wave(c)) {
         // the wave kernel fuses the stencil of iteration k+1 into the p-update of iteration k, so the
         // first stencil (q = A p0, p0.q) runs here; the dispatch counter and flags start from zero
@@ -630,7 +687,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     Scalars s0 = *c->snap[0];
     if (hist) hist[0] = s0.hist0;
     int status = s0.status, iters = 0, hdone = 0;
-    const int ring = fused ? 2 * kMaxChunk : c->chunk;
+    const int ring = (fused || cg1) ? 2 * kMaxChunk : c->chunk;
     double rn = s0.rn, bn = s0.bn;
     bool done = s0.done != 0;
     const bool pipelined = true;   // timing events alternate between two sets, like the snapshots
@@ -654,7 +711,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
             CK(c, cudaEventSynchronize(c->ev_chunk[cur]));
             const Scalars &s = *c->snap[cur];
             if (c->timing) accumulate_timing(c, cur, s.iter - iters);
-            const int hnew = fused ? s.hist_count : s.iter;
+            const int hnew = (fused || cg1) ? s.hist_count : s.iter;
             if (hist)
                 for (int k = hdone + 1; k <= hnew; ++k) hist[k] = s.hist_ring[(k - 1) % ring];
             hdone = hnew;
@@ -678,7 +735,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
     c->stats.kernel_launches += launched;
-    c->stats.path = c->vmode ? 4 : (use_wave(c) ? 3 : (fused ? 2 : 1));
+    c->stats.path = c->vmode ? 5 : (cg1 ? 4 : (use_wave(c) ? 3 : (fused ? 2 : 1)));
     c->stats.solves += 1;
     c->stats.iterations += iters;
     if (info) {
@@ -844,9 +901,13 @@ maspcg_status maspcg_create_loopback(int nr, int nt, int np, int rank, int nrank
 maspcg_status maspcg_destroy(maspcg_ctx *c) {
     if (!c) return MASPCG_OK;
     cudaSetDevice(c->device);
-    delete c->comm;
+    // captured graphs hold NCCL work of the communicator: release them (after the device is idle)
+    // before the communicator is finalised, or ncclCommDestroy waits on them forever
+    cudaDeviceSynchronize();
     for (int b = 0; b < 2; ++b)
         if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
+    c->gexec[0] = c->gexec[1] = nullptr;
+    delete c->comm;
     for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
     if (c->ev_p) cudaEventDestroy(c->ev_p);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -1410,8 +1471,9 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             c->arith = (int)v;
             break;
         case MASPCG_OPT_PATH:
-            if (v < 0 || v > 3)
-                SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels), 2 (fused) or 3 (wave)");
+            if (v < 0 || v > 4)
+                SET_ERR(c, MASPCG_E_INVALID,
+                        "path must be 0 (auto), 1 (three kernels), 2 (fused), 3 (wave) or 4 (single reduction)");
             c->path_opt = (int)v;
             break;
         default: SET_ERR(c, MASPCG_E_INVALID, "unknown option %d", (int)opt);

@@ -92,7 +92,7 @@ def test_vv_solve_exact(M, oracle_mod, shape, walls):
     assert info["iters"] == o["iters"]
     assert np.array_equal(hist, o["hist"])
     assert np.array_equal(x, o["x"])
-    assert stats["path"] == 4
+    assert stats["path"] == 5
 
 
 @pytest.mark.parametrize("name,shape", [("c2v", None), ("c2v", (40, 60, 96))])
