@@ -29,6 +29,24 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# Only the JSON line goes to stdout: file descriptor 1 is pointed at stderr for the whole run (NCCL
+# and other libraries print e.g. "NCCL version ..." on stdout), and emit() writes to the saved stdout.
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        _JSON_OUT = sys.stdout
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
+
+
+def protect_stdout():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
 METRIC = "PCG iterations/s & matvec HBM GB/s (% of peak) at 1/2/4/8 B200"
 UNIT = "PCG iterations/s"
@@ -41,8 +59,9 @@ PATHS = {
     3: {"name": "wave", "stencil": ("wave: x/p-update + stencil + p.q, flag-ordered (k_wave)", 80),
         "update": ("update_jacobi_dots (k_update_vec2)", 32), "pupdate": None, "iter": 112},
     4: {"name": "single reduction (Chronopoulos-Gear)",
-        "stencil": ("cg1 matvec: u = r/D on the fly, w = A u, Dot2 r.u, w.u, r.r (k_cg1_matvec)", 48),
-        "update": ("cg1 update: convergence, p, s, x, r (k_cg1_update)", 80), "pupdate": None, "iter": 128},
+        "stencil": ("cg1 matvec: w = A u, Dot2 w.u (k_cg1_matvec)", 48),
+        "update": ("cg1 update: convergence, p, s, x, r, u = r/D, Dot2 r.u, r.r (k_cg1_update)", 88),
+        "pupdate": None, "iter": 136},
 }
 
 
@@ -286,7 +305,7 @@ def run_vv(args):
             "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -328,7 +347,7 @@ def run_reference(args):
                                    f"(tol=0), operator assembled once before timing"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -363,6 +382,7 @@ def main():
                     help="scalar: the 7-point parabolic solve (default); vv: the staggered vector viscosity "
                          "(NEXT-2) on the c3 grid (config c3v)")
     args = ap.parse_args()
+    protect_stdout()
     if args.warmup < 3 and args.maxit is None:
         args.warmup = 3
     if args.impl == "reference":
@@ -578,7 +598,7 @@ def main():
             "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "sts": sts,
             "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 

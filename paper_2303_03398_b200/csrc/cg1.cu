@@ -6,9 +6,10 @@
 //           x += alpha p, r -= alpha s; u' = r / D (stored, with halo planes); Dot2 partials r.u', r.r
 //                                                                   88 B/cell: r, D, w, p, s, x / p, s, x, r, u
 //   matvec  w = A u (u with halo planes), Dot2 partial w.u          48 B/cell: u, D, T_r, T_t, T_p / w
+//           -- the stencil kernel of the three-kernel path (kernels.cu) applied to u, writing w
 //
-// All three dot products of an iteration (r.u and r.r from the update, w.u from the matvec) are
-// all-reduced TOGETHER after the matvec, so on P > 1 ranks they travel in ONE all-gather instead of
+// All three dot products of an iteration (r.u and r.r from the update into red2, w.u from the matvec
+// into red1, adjacent in Scalars) are all-reduced TOGETHER after the matvec, so on P > 1 ranks they travel in ONE all-gather instead of
 // two -- the latency floor of strong scaling.  136 B/cell per iteration (the three-kernel
 // path: 128).  In exact arithmetic s = A p and the iterates are those of the Hestenes-Stiefel path; in
 // floating point they differ at rounding level, hence the oracle's own variant.  Same rounding policy
@@ -25,7 +26,8 @@ namespace maspcg {
 
 namespace {
 
-constexpr int kCgBlocks = 4;   // resident 256-thread blocks per SM (<= 64 registers)
+constexpr int kCgBlocks = 4;      // matvec: resident 256-thread blocks per SM (<= 64 registers)
+constexpr int kCgUpdBlocks = 3;   // update: 3 per SM (<= 85 registers: no spills in the pair loop)
 
 __device__ __forceinline__ void pdl_wait_cg() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger_cg() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -38,80 +40,6 @@ __device__ __forceinline__ void decompose_cg(const Dims &d, uint32_t c, int &i, 
     k = (int)kk;
 }
 
-struct Range1 {
-    uint32_t vend, off0, split, off1;
-};
-
-Range1 make_range1(const Dims &d, StencilPart part) {
-    const uint32_t pl = d.plane;
-    switch (part) {
-        case StencilPart::Interior: return {d.nloc > 2 ? (uint32_t)(d.nloc - 2) * pl : 0u, pl, 0xffffffffu, 0u};
-        case StencilPart::Boundary:
-            if (d.nloc == 1) return {pl, 0u, 0xffffffffu, 0u};
-            return {2u * pl, 0u, pl, (uint32_t)(d.nloc - 2) * pl};
-        default: return {d.n, 0u, 0xffffffffu, 0u};
-    }
-}
-
-// w of one cell: D u - sum T u_nb in the oracle's order (r_lo, r_hi, theta_lo, theta_hi, phi_lo, phi_hi)
-template <bool EXACT>
-__device__ __forceinline__ double cell_w(const Dims &d, const DevArrays &a, uint32_t c, int i, int j, double uc,
-                                         double dc) {
-    using A = Ar<EXACT>;
-    const double *__restrict__ u = a.cgr + d.plane;   // u[c] of local cell c, halo planes at -plane / +n
-    double s = 0.0;
-    if (i > 0) s = A::acc(s, __ldg(a.Tr + c), __ldg(u + c - 1));
-    if (i < d.nr - 1) s = A::acc(s, __ldg(a.Tr + c + 1), __ldg(u + c + 1));
-    if (j > 0) s = A::acc(s, __ldg(a.Tt + c), __ldg(u + c - d.nr));
-    if (j < d.nt - 1) s = A::acc(s, __ldg(a.Tt + c + d.nr), __ldg(u + c + d.nr));
-    s = A::acc(s, __ldg(a.Tp + c), __ldg(u + (size_t)c - d.plane));
-    s = A::acc(s, __ldg(a.Tp + c + d.plane), __ldg(u + (size_t)c + d.plane));
-    return A::diag_minus(dc, uc, s);
-}
-
-template <bool LOOP, bool EXACT>
-__global__ void __launch_bounds__(kThreads, kCgBlocks) k_cg1_matvec(Dims d, DevArrays a, Range1 rg, unsigned red_slot0,
-                                                                    unsigned red_total, int pair) {
-    pdl_wait_cg();
-    pdl_trigger_cg();
-    if (LOOP && *(volatile int *)&a.sc->done) return;
-    const double *__restrict__ u = a.cgr + d.plane;
-    Acc<EXACT> acc[1];
-    const uint32_t stride = gridDim.x * blockDim.x;
-    if (pair) {
-        // two r-neighbour cells per thread (nr even): 16-byte loads of the pair's own streams
-        for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; 2 * v < rg.vend; v += stride) {
-            const uint32_t c0 = 2 * v + rg.off0 + (2 * v >= rg.split ? rg.off1 : 0u);
-            int i, j, k;
-            decompose_cg(d, c0, i, j, k);
-            const double2 uu = __ldg(reinterpret_cast<const double2 *>(u + c0));
-            const double2 dd = __ldg(reinterpret_cast<const double2 *>(a.D + c0));
-            const double w0 = cell_w<EXACT>(d, a, c0, i, j, uu.x, dd.x);
-            const double w1 = cell_w<EXACT>(d, a, c0 + 1, i + 1, j, uu.y, dd.y);
-            *reinterpret_cast<double2 *>(a.cgw + c0) = make_double2(w0, w1);
-            acc[0].add(w0, uu.x);
-            acc[0].add(w1, uu.y);
-        }
-    } else {
-        for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < rg.vend; v += stride) {
-            const uint32_t c = v + rg.off0 + (v >= rg.split ? rg.off1 : 0u);
-            int i, j, k;
-            decompose_cg(d, c, i, j, k);
-            const double uc = __ldg(u + c);
-            const double w = cell_w<EXACT>(d, a, c, i, j, uc, __ldg(a.D + c));
-            a.cgw[c] = w;
-            acc[0].add(w, uc);
-        }
-    }
-    Acc<EXACT> out[1];
-    if (reduce_last<EXACT, kThreads, 1>(acc, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total, out)) {
-        if (threadIdx.x == 0) {
-            a.sc->red_cg[2] = out[0].p;
-            a.sc->red_cg[3] = out[0].s;
-        }
-    }
-}
-
 __device__ __forceinline__ void store_r(const Dims &d, double *rp, uint32_t c, double v) {
     rp[(size_t)c + d.plane] = v;
     if (d.periodic_local) {
@@ -121,8 +49,8 @@ __device__ __forceinline__ void store_r(const Dims &d, double *rp, uint32_t c, d
 }
 
 template <bool EXACT>
-__global__ void __launch_bounds__(kThreads, kCgBlocks) k_cg1_update(Dims d, DevArrays a, double *__restrict__ x,
-                                                                    unsigned total) {
+__global__ void __launch_bounds__(kThreads, kCgUpdBlocks) k_cg1_update(Dims d, DevArrays a, double *__restrict__ x,
+                                                                    unsigned total, int pair) {
     pdl_wait_cg();
     pdl_trigger_cg();
     using A = Ar<EXACT>;
@@ -131,7 +59,7 @@ __global__ void __launch_bounds__(kThreads, kCgBlocks) k_cg1_update(Dims d, DevA
     const int it = sc->iter;
     // the previous iterate r_it (its r.r came with this iteration's reduction): history, stopping test
     if (it > 0) {
-        const double rn = sqrt(__dadd_rn(sc->red_cg[4], sc->red_cg[5]));
+        const double rn = sqrt(__dadd_rn(sc->red2[2], sc->red2[3]));
         const bool conv = rn <= sc->tolbn, bad = !isfinite(rn);
         if (conv || bad || it >= sc->maxit) {
             if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -144,8 +72,8 @@ __global__ void __launch_bounds__(kThreads, kCgBlocks) k_cg1_update(Dims d, DevA
             return;
         }
     }
-    const double gamma = __dadd_rn(sc->red_cg[0], sc->red_cg[1]);
-    const double delta = __dadd_rn(sc->red_cg[2], sc->red_cg[3]);
+    const double gamma = __dadd_rn(sc->red2[0], sc->red2[1]);
+    const double delta = __dadd_rn(sc->red1[0], sc->red1[1]);
     double beta = 0.0, den = delta;
     if (it > 0) {
         beta = __ddiv_rn(gamma, sc->cg_gamma_old);
@@ -154,7 +82,7 @@ __global__ void __launch_bounds__(kThreads, kCgBlocks) k_cg1_update(Dims d, DevA
     if (!(den > 0.0) || !isfinite(den) || !isfinite(gamma)) {   // uniform decision in every block
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             if (it > 0) {
-                const double rn = sqrt(__dadd_rn(sc->red_cg[4], sc->red_cg[5]));
+                const double rn = sqrt(__dadd_rn(sc->red2[2], sc->red2[3]));
                 sc->rn = rn;
                 sc->hist_ring[(it - 1) % (2 * kMaxChunk)] = rn;
                 sc->hist_count = it;
@@ -171,6 +99,35 @@ __global__ void __launch_bounds__(kThreads, kCgBlocks) k_cg1_update(Dims d, DevA
     double *__restrict__ s = a.cgs;
     Acc<EXACT> acc[2];
     const uint32_t stride = gridDim.x * blockDim.x;
+    if (pair) {   // two values per thread, 16-byte loads and stores (n and the plane are even)
+        for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; 2 * v < d.n; v += stride) {
+            const uint32_t c = 2 * v;
+            const double2 rc = *reinterpret_cast<const double2 *>(r + c);
+            const double2 dc = __ldg(reinterpret_cast<const double2 *>(a.D + c));
+            const double2 po = *reinterpret_cast<const double2 *>(p + c);
+            const double2 so = *reinterpret_cast<const double2 *>(s + c);
+            const double2 wc = __ldg(reinterpret_cast<const double2 *>(a.cgw + c));
+            const double2 xo = *reinterpret_cast<const double2 *>(x + c);
+            const double p0 = A::axpy(beta, po.x, __ddiv_rn(rc.x, dc.x));
+            const double p1 = A::axpy(beta, po.y, __ddiv_rn(rc.y, dc.y));
+            const double s0 = A::axpy(beta, so.x, wc.x), s1 = A::axpy(beta, so.y, wc.y);
+            *reinterpret_cast<double2 *>(p + c) = make_double2(p0, p1);
+            *reinterpret_cast<double2 *>(s + c) = make_double2(s0, s1);
+            *reinterpret_cast<double2 *>(x + c) = make_double2(A::axpy(alpha, p0, xo.x), A::axpy(alpha, p1, xo.y));
+            const double r0 = A::ymax(rc.x, alpha, s0), r1 = A::ymax(rc.y, alpha, s1);
+            *reinterpret_cast<double2 *>(r + c) = make_double2(r0, r1);
+            const double u0 = __ddiv_rn(r0, dc.x), u1 = __ddiv_rn(r1, dc.y);
+            *reinterpret_cast<double2 *>(up + (size_t)c + d.plane) = make_double2(u0, u1);
+            if (d.periodic_local) {
+                if (c < d.plane) *reinterpret_cast<double2 *>(up + (size_t)c + (size_t)(d.nloc + 1) * d.plane) = make_double2(u0, u1);
+                if (c >= d.n - d.plane) *reinterpret_cast<double2 *>(up + (size_t)c - (size_t)(d.nloc - 1) * d.plane) = make_double2(u0, u1);
+            }
+            acc[0].add(r0, u0);
+            acc[0].add(r1, u1);
+            acc[1].add(r0, r0);
+            acc[1].add(r1, r1);
+        }
+    } else
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
         const double rc = r[c], dc = __ldg(a.D + c);
         const double u = __ddiv_rn(rc, dc);
@@ -190,15 +147,15 @@ __global__ void __launch_bounds__(kThreads, kCgBlocks) k_cg1_update(Dims d, DevA
     if (reduce_last<EXACT, kThreads, 2>(acc, a.partials, &sc->ticket[1], blockIdx.x, total, out)) {
         if (threadIdx.x == 0) {
             if (it > 0) {   // the history entry of r_it (checked above)
-                const double rn = sqrt(__dadd_rn(sc->red_cg[4], sc->red_cg[5]));
+                const double rn = sqrt(__dadd_rn(sc->red2[2], sc->red2[3]));
                 sc->rn = rn;
                 sc->hist_ring[(it - 1) % (2 * kMaxChunk)] = rn;
                 sc->hist_count = it;
             }
-            sc->red_cg[0] = out[0].p;   // local r.u and r.r of the new iterate: all-reduced with w.u
-            sc->red_cg[1] = out[0].s;
-            sc->red_cg[4] = out[1].p;
-            sc->red_cg[5] = out[1].s;
+            sc->red2[0] = out[0].p;   // local r.u and r.r of the new iterate: all-reduced with w.u (red1)
+            sc->red2[1] = out[0].s;
+            sc->red2[2] = out[1].p;
+            sc->red2[3] = out[1].s;
             sc->iter = it + 1;
             sc->cg_gamma_old = gamma;
             sc->cg_alpha_old = alpha;
@@ -222,40 +179,20 @@ void launch_cg_pdl(bool pdl, void (*kern)(KArgs...), unsigned grid, cudaStream_t
 
 inline bool cg_pair(const Dims &d) { return d.vec_ok && (d.nr % 2 == 0); }
 
-inline unsigned cg_grid(uint32_t work) {
+inline unsigned cg_grid(uint32_t work, int per_sm = kCgBlocks) {
     uint64_t g = (work + kThreads - 1) / kThreads;
     if (g < 1) g = 1;
-    if (g > (uint64_t)(148 * kCgBlocks)) g = 148 * kCgBlocks;
+    if (g > (uint64_t)(148 * per_sm)) g = 148 * per_sm;
     return (unsigned)g;
 }
 
 }  // namespace
 
-unsigned cg1_matvec_blocks(const Dims &d, StencilPart part) {
-    const Range1 rg = make_range1(d, part);
-    if (!rg.vend) return 0u;
-    return cg_grid(cg_pair(d) ? rg.vend / 2 : rg.vend);
-}
-
-void launch_cg1_matvec(const Dims &d, const DevArrays &a, StencilPart part, bool loop, unsigned red_slot0,
-                       unsigned red_total, bool exact, cudaStream_t st) {
-    const Range1 rg = make_range1(d, part);
-    if (!rg.vend) return;
-    const int pair = cg_pair(d) ? 1 : 0;
-    const unsigned g = cg_grid(pair ? rg.vend / 2 : rg.vend);
-    if (exact) {
-        if (loop) launch_cg_pdl(d.pdl != 0, k_cg1_matvec<true, true>, g, st, d, a, rg, red_slot0, red_total, pair);
-        else launch_cg_pdl(d.pdl != 0, k_cg1_matvec<false, true>, g, st, d, a, rg, red_slot0, red_total, pair);
-    } else {
-        if (loop) launch_cg_pdl(d.pdl != 0, k_cg1_matvec<true, false>, g, st, d, a, rg, red_slot0, red_total, pair);
-        else launch_cg_pdl(d.pdl != 0, k_cg1_matvec<false, false>, g, st, d, a, rg, red_slot0, red_total, pair);
-    }
-}
-
 void launch_cg1_update(const Dims &d, const DevArrays &a, double *x, bool exact, cudaStream_t st) {
-    const unsigned g = cg_grid(d.n);
-    if (exact) launch_cg_pdl(d.pdl != 0, k_cg1_update<true>, g, st, d, a, x, g);
-    else launch_cg_pdl(d.pdl != 0, k_cg1_update<false>, g, st, d, a, x, g);
+    const int pair = (cg_pair(d) && ((uintptr_t)x & 15) == 0) ? 1 : 0;
+    const unsigned g = cg_grid(pair ? d.n / 2 : d.n, kCgUpdBlocks);
+    if (exact) launch_cg_pdl(d.pdl != 0, k_cg1_update<true>, g, st, d, a, x, g, pair);
+    else launch_cg_pdl(d.pdl != 0, k_cg1_update<false>, g, st, d, a, x, g, pair);
 }
 
 }  // namespace maspcg

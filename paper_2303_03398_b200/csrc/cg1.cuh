@@ -11,15 +11,10 @@
 
 namespace maspcg {
 
-// w = A u with u = r / D formed on the fly (r from the padded cgr, D with its halo planes: periodic
-// on one rank, a.dh otherwise) over `part` of the slab; Dot2 partials of r.u, w.u, r.r into partial
-// slots [red_slot0, red_slot0 + blocks); the last of red_total blocks writes sc->red_cg.
-// loop: early exit when sc->done.
-void launch_cg1_matvec(const Dims &d, const DevArrays &a, StencilPart part, bool loop, unsigned red_slot0,
-                       unsigned red_total, bool exact, cudaStream_t st);
-unsigned cg1_matvec_blocks(const Dims &d, StencilPart part);
-// The convergence test of the previous iterate (from red_cg), then beta, alpha and p = u + beta p,
-// s = w + beta s, x += alpha p, r -= alpha s (r into cgr, periodic copies on one rank).
+// The convergence test of the previous iterate (r.r in red2[2..3]), then beta (gamma = r.u in red2[0..1]),
+// alpha (delta = w.u in red1), p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s, u = r / D
+// (into the padded cgr, periodic copies on one rank) and the local Dot2 r.u, r.r of the new iterate.
+// The matvec w = A u is launch_matvec of kernels.cuh on a DevArrays whose p is cgr.
 void launch_cg1_update(const Dims &d, const DevArrays &a, double *x, bool exact, cudaStream_t st);
 
 }  // namespace maspcg

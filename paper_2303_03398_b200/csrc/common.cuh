@@ -67,7 +67,6 @@ struct Scalars {
     double hist0;            // ||r_0||
     double rn;               // ||r_iter||
     double alpha;            // alpha of the last completed iteration (fused path: deferred x update)
-    double red_cg[6];        // single-reduction path: (gamma = r.u, delta = w.u, r.r) Dot2 pairs
     double cg_gamma_old;     // single-reduction path: gamma and alpha of the previous iteration
     double cg_alpha_old;
     int iter;                // completed PCG iterations

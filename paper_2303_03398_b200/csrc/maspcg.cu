@@ -11,6 +11,7 @@
 #include <nccl.h>   // ncclGetUniqueId only; the communicator lives in comm.cu
 
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -517,21 +518,27 @@ maspcg_status enqueue_iteration_wave(maspcg_ctx *c, double *x, cudaStream_t st, 
 
 // One iteration of the single-reduction path (cg1.cu): update (with the convergence test of the
 // previous iterate), r halo planes overlapped with the interior of the matvec, one all-reduce.
+static_assert(offsetof(Scalars, red2) == offsetof(Scalars, red1) + 2 * sizeof(double),
+              "the single-reduction path all-reduces red1 and red2 as one block of 3 Dot2 pairs");
+
 maspcg_status cg1_matvec(maspcg_ctx *c, bool loop, cudaStream_t st) {
+    DevArrays au = c->a;   // the stencil of the three-kernel path applied to u (padded cgr), writing w
+    au.p = c->a.cgr;
+    double *w = c->a.cgw;
     if (!c->comm) {
-        launch_cg1_matvec(c->d, c->a, StencilPart::Full, loop, 0, cg1_matvec_blocks(c->d, StencilPart::Full),
-                          exact_arith(c), st);
+        launch_matvec(c->d, au, w, StencilPart::Full, true, loop, 0, stencil_blocks(c->d, StencilPart::Full, w),
+                      exact_arith(c), st);
         return MASPCG_OK;
     }
     CK(c, cudaEventRecord(c->ev_p, st));
     CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
     RET_IF(halo_padded(c, c->a.cgr, c->comm_stream));
     CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
-    const unsigned gi = cg1_matvec_blocks(c->d, StencilPart::Interior);
-    const unsigned gb = cg1_matvec_blocks(c->d, StencilPart::Boundary);
-    launch_cg1_matvec(c->d, c->a, StencilPart::Interior, loop, 0, gi + gb, exact_arith(c), st);
+    const unsigned gi = stencil_blocks(c->d, StencilPart::Interior, w);
+    const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary, w);
+    launch_matvec(c->d, au, w, StencilPart::Interior, true, loop, 0, gi + gb, exact_arith(c), st);
     CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
-    launch_cg1_matvec(c->d, c->a, StencilPart::Boundary, loop, gi, gi + gb, exact_arith(c), st);
+    launch_matvec(c->d, au, w, StencilPart::Boundary, true, loop, gi, gi + gb, exact_arith(c), st);
     return MASPCG_OK;
 }
 
@@ -543,7 +550,7 @@ maspcg_status enqueue_iteration_cg1(maspcg_ctx *c, double *x, cudaStream_t st, i
     if (tm) CK(c, record_timing(c, 0, 0, it, st));
     RET_IF(cg1_matvec(c, true, st));
     if (tm) CK(c, record_timing(c, 0, 1, it, st));
-    RET_IF(allreduce_dot2(c, c->a.sc->red_cg, 3, st));
+    RET_IF(allreduce_dot2(c, c->a.sc->red1, 3, st));   // red1 (w.u) and red2 (r.u, r.r) together
     if (tm) {
         CK(c, record_timing(c, 2, 0, it, st));
         CK(c, record_timing(c, 2, 1, it, st));
@@ -619,7 +626,7 @@ void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
     if (c->vmode) return 5 + (c->comm ? 1 : 0);   // ring sums (+ combine), terms, rows, update, p-update
-    if (use_cg1(c)) return 2 + (c->comm ? 2 : 0);   // update, matvec (interior + boundary, combine)
+    if (use_cg1(c)) return 2 + (c->comm ? 2 : 0);   // update, matvec (+ boundary part, combine on P > 1)
     if (use_fused(c) || use_wave(c)) return 2;
     if (!c->comm) return 3;
     return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
@@ -652,10 +659,8 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     else
         launch_setup_residual(c->d, c->a, rhs, c->bc_in == BC_DIRICHLET && c->has_gin,
                               c->bc_out == BC_DIRICHLET && c->has_gout, exact_arith(c), st);
-    if (use_cg1(c)) {   // the local r0.u0 and r0.r0 travel with the first w.u (one all-reduce)
-        CK(c, cudaMemcpyAsync(c->a.sc->red_cg, c->a.sc->red3, 16, cudaMemcpyDeviceToDevice, st));
-        CK(c, cudaMemcpyAsync(c->a.sc->red_cg + 4, c->a.sc->red3 + 2, 16, cudaMemcpyDeviceToDevice, st));
-    }
+    if (use_cg1(c))   // the local r0.u0 and r0.r0 travel with the first w.u (one all-reduce)
+        CK(c, cudaMemcpyAsync(c->a.sc->red2, c->a.sc->red3, 32, cudaMemcpyDeviceToDevice, st));
     RET_IF(allreduce_dot2(c, c->a.sc->red3, 3, st));
     if (fused && c->comm) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
     launch_setup_scalars(c->a, tol, maxit, st);
@@ -667,7 +672,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
         CK(c, cudaMemsetAsync(c->a.q, 0, 8 * n, st));
         CK(c, cudaMemsetAsync(c->a.cgs, 0, 8 * n, st));
         RET_IF(cg1_matvec(c, true, st));
-        RET_IF(allreduce_dot2(c, c->a.sc->red_cg, 3, st));
+        RET_IF(allreduce_dot2(c, c->a.sc->red1, 3, st));
     }
     if (use_wave(c)) {
         // the wave kernel fuses the stencil of iteration k+1 into the p-update of iteration k, so the
