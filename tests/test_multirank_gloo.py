@@ -167,3 +167,71 @@ def test_slab_extent_rules():
     # slabs tile the global index range
     ext = [inputs.slab_extent(128, r, 4) for r in range(4)]
     assert [e[0] for e in ext] == [0, 32, 64, 96] and all(e[1] == 32 for e in ext)
+
+
+def _vv_worker(rank, world, port, out_dir):
+    """Vector viscosity (NEXT-2) host logic over gloo: phi-slabs of the [np][3][nt][nr] vector, the
+    3-component halo planes, and the pole-ring reduction of Listing 3 decomposed as
+    the library does it -- each rank sums its own planes of the ring, the partial sums travel in one
+    all-gather and are combined in rank order -- against the global oracle's axis circulations."""
+    import math
+    import sys
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    from paper_2303_03398_b200 import inputs
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        res = {}
+        shape = (6, 5, 8)
+        full = inputs.make_vv_problem("rand", shape=shape, seed=3)
+        k0, nloc = inputs.slab_extent(full.np, rank, world)
+        slab = inputs.make_vv_problem("rand", k0, nloc, shape=shape, seed=3)
+        sl = slice(k0, k0 + nloc)
+        for name in ("nu", "s", "f", "g_in", "g_out"):
+            assert np.array_equal(getattr(slab, name), getattr(full, name)[sl]), name
+        v = np.random.default_rng(11).standard_normal((full.np, 3, full.nt, full.nr))
+        vloc = v[sl].copy()
+        # 3-component halo planes: lo <- left's last plane, hi <- right's first plane
+        L, R = (rank - 1) % world, (rank + 1) % world
+        lo, hi = torch.empty(vloc[0].shape, dtype=torch.float64), torch.empty(vloc[0].shape, dtype=torch.float64)
+        reqs = [dist.isend(torch.from_numpy(vloc[0].copy()), L, tag=1), dist.isend(torch.from_numpy(vloc[-1].copy()), R, tag=2),
+                dist.irecv(hi, R, tag=1), dist.irecv(lo, L, tag=2)]
+        for q in reqs:
+            q.wait()
+        res["halo_ok"] = bool(np.array_equal(lo.numpy(), v[(k0 - 1) % full.np]) and
+                              np.array_equal(hi.numpy(), v[(k0 + nloc) % full.np]))
+        # the ring sums: sum_k l_phi v_phi(i, pole row, k) with l_phi = (rc sin tc) h_phi across the lower face
+        rc, tc, pc = inputs.midpoints(full.rf), inputs.midpoints(full.tf), inputs.midpoints(full.pf)
+        hlo = pc - np.roll(pc, 1)
+        hlo[0] += 2 * math.pi
+        part = []
+        for j in (0, full.nt - 1):
+            for i in range(full.nr):
+                terms = [((rc[i] * math.sin(tc[j])) * hlo[k]) * v[k, 2, j, i] for k in range(k0, k0 + nloc)]
+                part.append(math.fsum(terms))
+        out = [None] * world
+        dist.all_gather_object(out, part)
+        ring = np.array([math.fsum([o[t] for o in out]) for t in range(2 * full.nr)])
+        res["ring"] = ring
+        _, GN, GS, _, _ = oracle.vv_curl(full.rf, full.tf, full.pf, v)
+        res["GN"], res["GS"] = GN, GS
+        np.save(os.path.join(out_dir, f"vv_rank{rank}.npy"), res, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_vector_viscosity_decomposition(tmp_path, oracle_mod):
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_vv_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    res = [np.load(tmp_path / f"vv_rank{r}.npy", allow_pickle=True).item() for r in range(world)]
+    for r in res:
+        assert r["halo_ok"]
+        nr = r["GN"].size
+        assert np.array_equal(r["ring"], res[0]["ring"])     # identical on every rank
+        # the rank-decomposed ring sums are the global axis circulations (Dot2 there, fsum here)
+        np.testing.assert_allclose(r["ring"][:nr], r["GN"], rtol=1e-14, atol=0)
+        np.testing.assert_allclose(-r["ring"][nr:], r["GS"], rtol=1e-14, atol=0)
