@@ -366,6 +366,9 @@ def main():
                     help="also time RKL2 super-time-steps with this many stages (NEXT-4), 0 = off")
     ap.add_argument("--force-comm", action="store_true",
                     help="N=1 with a one-rank NCCL communicator (the multi-rank code path, halos to itself)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1 (or --force-comm): NCCL, or the peer-memory communicator (exchanges as kernels "
+                         "storing into the peers' workspaces over NVLink, CUDA IPC)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=8)
@@ -419,8 +422,9 @@ def main():
     if args.from_fields:
         rc = inputs.midpoints(prob.rf)
         rho_cells = T(np.broadcast_to(inputs.rho_hydro(rc)[None, None, :], prob.s.shape))
+    use_peer = args.comm == "peer" and (world > 1 or args.force_comm)
     S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk,
-                      force_comm=args.force_comm)
+                      force_comm=args.force_comm and not use_peer, comm="peer" if use_peer else "nccl")
     S.set_option(maspcg.OPT_PATH, args.path)
     S.set_option(maspcg.OPT_ARITH, args.arith)
     S.set_option(maspcg.OPT_TMA, args.tma)
@@ -587,7 +591,9 @@ def main():
             "config": {"workload": f"{args.config} {nr}x{nt}x{np_} coronal viscosity solve "
                                    f"(BASELINE.json configs[2]), tol={tol:g}, Jacobi-PCG fp64",
                        "global_cells": nr * nt * np_,
-                       "parallelism": f"phi-slab x{world}" + (" (one-rank NCCL communicator)" if args.force_comm else ""),
+                       "parallelism": f"phi-slab x{world}" + (
+                           (" (one-rank peer-memory communicator)" if use_peer else " (one-rank NCCL communicator)")
+                           if args.force_comm else (" peer-memory communicator" if use_peer else "")),
                        "iters_per_solve": iters / args.steps, "chunk": args.chunk,
                        "l2": "no flush: working set ~2.2 GB >> 126 MB L2",
                        "step": ("set_grid + set_coefficients_from_fields(rho; kappa = 1e-3 rho, s = rho/1e-2) + "

@@ -321,6 +321,23 @@ MASPCG_API maspcg_status maspcg_vv_solve(maspcg_ctx *ctx, const double *f, doubl
 /* The Jacobi diagonal, HOST [nloc][3][nt][nr] (1 on the non-unknown slots); for tests. */
 MASPCG_API maspcg_status maspcg_vv_get_diag(maspcg_ctx *ctx, double *D, void *cuda_stream);
 
+/* ---- peer-memory communicator (SURVEY 8(e) lever 4: in-kernel exchanges) ---------------------- */
+
+/* As maspcg_create, but the halo planes, all-gathers and flag all-reduces are kernels that store into
+ * the peers' workspaces over NVLink / NVSwitch and signal with system-scope release flags (no NCCL, no
+ * host round trip; captured into the CUDA graphs).  One process (one CUDA context) per rank; every rank
+ * calls every function in the same order.  After maspcg_set_workspace (region 0) and
+ * maspcg_vv_set_workspace (region 1) every rank exports its region (maspcg_peer_export, 80 bytes: the
+ * CUDA IPC handle of the workspace's allocation, offset, size), the caller all-gathers the bytes (e.g.
+ * torch.distributed) and imports every peer's (maspcg_peer_import), then barriers before the next call.
+ * nranks == 1 needs no import (the rank pushes to itself).  group must be NULL (ranks sharing one context
+ * could spin on each other inside one device: E_INVALID).  The fused iteration path (MASPCG_OPT_PATH 2)
+ * is not available in this mode (E_INVALID at solve). */
+MASPCG_API maspcg_status maspcg_create_peer(int nr, int nt, int np, int rank, int nranks, void *group,
+                                            int cuda_device, maspcg_ctx **out);
+MASPCG_API maspcg_status maspcg_peer_export(maspcg_ctx *ctx, int region, void *out /* 80 bytes, host */);
+MASPCG_API maspcg_status maspcg_peer_import(maspcg_ctx *ctx, int region, int rank, const void *in /* 80 bytes */);
+
 /* ---- in-process multi-rank emulation (TEST ONLY) ------------------------------ */
 
 /* A loopback group lets `nranks` contexts live in ONE process on ONE device, one

@@ -32,13 +32,6 @@ constexpr int kCgUpdBlocks = 3;   // update: 3 per SM (<= 85 registers: no spill
 __device__ __forceinline__ void pdl_wait_cg() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger_cg() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-__device__ __forceinline__ void decompose_cg(const Dims &d, uint32_t c, int &i, int &j, int &k) {
-    const uint32_t row = d.div_r.div(c);
-    i = (int)(c - row * (uint32_t)d.nr);
-    const uint32_t kk = d.div_t.div(row);
-    j = (int)(row - kk * (uint32_t)d.nt);
-    k = (int)kk;
-}
 
 __device__ __forceinline__ void store_r(const Dims &d, double *rp, uint32_t c, double v) {
     rp[(size_t)c + d.plane] = v;

@@ -166,6 +166,7 @@ LoopbackGroup *loopback_group_create(int nranks) {
 
 void loopback_group_destroy(LoopbackGroup *g) { delete g; }
 
+
 class LoopbackComm final : public Comm {
    public:
     LoopbackGroup *g = nullptr;

@@ -13,6 +13,8 @@
 
 #include <string>
 
+#include "common.cuh"
+
 namespace maspcg {
 
 class Comm {
@@ -45,5 +47,20 @@ struct LoopbackGroup;
 LoopbackGroup *loopback_group_create(int nranks);
 void loopback_group_destroy(LoopbackGroup *g);
 Comm *make_loopback_comm(LoopbackGroup *g, int rank, int nranks, int *status, std::string &err);
+
+// ---- peer-memory communicator (peer.cu) ----
+// Every rank's workspaces (region 0: the base workspace, 1: the vector-viscosity workspace) have the same
+// layout; a local address inside a region maps to the same offset in the peer's region.
+struct PeerTable {
+    char *base[kP2PRegions][kP2PMaxRanks] = {};
+    size_t bytes[kP2PRegions] = {};
+    void *mapping[kP2PRegions][kP2PMaxRanks] = {};   // CUDA IPC mappings to close
+    P2PArea *area = nullptr;                         // this rank's flags / epochs / staging (in region 0)
+};
+Comm *make_peer_comm(PeerTable *tab, int rank, int nranks, int *status, std::string &err);
+// CUDA IPC: export a region (handle of its allocation + offset + size: kP2PHandleBytes), import a peer's.
+int peer_export(const void *base, size_t bytes, void *out, std::string &err);
+int peer_import(const void *in, char **base, size_t *bytes, void **mapping, std::string &err);
+void peer_close(void *mapping);
 
 }  // namespace maspcg

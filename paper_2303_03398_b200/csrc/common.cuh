@@ -81,6 +81,22 @@ struct Scalars {
     double hist_ring[2 * kMaxChunk];   // ||r_k|| at slot (k-1) % chunk (3-kernel) or % (2 kMaxChunk) (fused)
 };
 
+// Peer-memory communicator (peer.cu): flags, epochs and double-buffered staging of one rank, in its
+// workspace; peers store into it over NVLink.
+constexpr int kP2PMaxRanks = 16;
+constexpr int kP2PRegions = 2;
+constexpr int kP2PStage = 16384;     // doubles per rank slot of an all-gather
+constexpr int kP2PIStage = 64;       // ints per rank slot of an all-reduce(max)
+constexpr int kP2PHandleBytes = 64 + 16;
+enum : int { P2P_FROM_LEFT = 0, P2P_FROM_RIGHT, P2P_SHIFT, P2P_GATHER, P2P_MAX, P2P_HALO, kP2PKinds };
+struct P2PArea {
+    unsigned long long flags[kP2PKinds][kP2PMaxRanks];   // written by the senders (epoch of their last exchange)
+    unsigned long long epoch[kP2PKinds];                  // this rank's exchange counters
+    unsigned int ticket[kP2PKinds];
+    int istage[2][kP2PMaxRanks][kP2PIStage];
+    double stage[2][kP2PMaxRanks][kP2PStage];
+};
+
 // Geometry handed to kernels by value.
 struct Dims {
     int nr, nt, nloc;       // local slab shape
@@ -141,6 +157,7 @@ struct DevArrays {
     unsigned *wave_flags;   // [nloc] completed A-tiles per plane
     double *wave_partials;  // [nloc * tiles per plane][2]
     // reductions
+    P2PArea *p2p;       // peer-memory communicator area
     double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums
     double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce
     Scalars *sc;

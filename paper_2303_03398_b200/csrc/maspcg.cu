@@ -42,6 +42,7 @@ struct maspcg_ctx {
     int nr = 0, nt = 0, np = 0, rank = 0, nranks = 1, device = 0;
     int k0 = 0, nloc = 0;
     Comm *comm = nullptr;            // nullptr: one rank, periodic wrap done locally
+    PeerTable *ptab = nullptr;       // peer-memory communicator: the ranks' workspace regions
     std::string err;
 
     // grid (host copies of the 1-D metric)
@@ -137,6 +138,7 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     DevArrays t{};
     t.sc = (Scalars *)take(sizeof(Scalars));
     t.partials = (double *)take(sizeof(double) * 8 * kRedBlocks);
+    t.p2p = (P2PArea *)take(sizeof(P2PArea));
     t.gather = (double *)take(sizeof(double) * 8 * kMaxRanks);
     t.P[0] = (double *)take(8 * n);
     t.P[1] = (double *)take(8 * n);
@@ -346,6 +348,12 @@ maspcg_status ensure_vv(maspcg_ctx *c, cudaStream_t st) {
     CK(c, cudaMemsetAsync(a.ring, 0, 8 * 4 * (size_t)c->nr, st));
     launch_vv_matvec(c->vd, a, c->a, a.bw, false, false, true, true, st);
     CK(c, cudaGetLastError());
+    if (c->comm) {
+        // p (halo planes included) was zeroed above; no rank may push its next planes into our halos before
+        // that: one more collective orders every rank's zeroing before any rank's next exchange
+        CK(c, cudaMemsetAsync(&c->a.sc->vinvalid, 0, sizeof(int), st));
+        COMM(c, c->comm->allreduce_max(&c->a.sc->vinvalid, 1, st, c->err));
+    }
     CK(c, cudaStreamSynchronize(st));   // host metric vectors may change with the next set_grid
     c->stats.kernel_launches += 6;
     c->vv_dirty = false;
@@ -647,6 +655,8 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
     RET_IF(c->vmode ? ensure_vv(c, st) : ensure_D(c, st));
     const bool fused = use_fused(c);
+    if (fused && c->ptab)
+        SET_ERR(c, MASPCG_E_INVALID, "the fused path (2) is not available with the peer-memory communicator");
     if (fused && (c->chunk & 1)) c->chunk += 1;   // even chunks: fixed p-buffer parity per slot
     if (c->timing) RET_IF(maspcg_set_option(c, MASPCG_OPT_TIMING, c->timing));   // events for this chunk size
 
@@ -668,7 +678,12 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     if (cg1) {
         // single-reduction start: u0 = z0 (the padded p of the setup, periodic copies included), p = s = 0,
         // then w0 = A u0 and delta0 = w0.u0
-        CK(c, cudaMemcpyAsync(c->a.cgr, c->a.p, 8 * (n + 2 * (size_t)c->d.plane), cudaMemcpyDeviceToDevice, st));
+        // (halo planes only on a single rank: with a communicator they arrive by the exchange -- a peer may
+        // already have pushed them, so they must not be overwritten locally)
+        if (c->comm)
+            CK(c, cudaMemcpyAsync(c->a.cgr + c->d.plane, c->a.p + c->d.plane, 8 * n, cudaMemcpyDeviceToDevice, st));
+        else
+            CK(c, cudaMemcpyAsync(c->a.cgr, c->a.p, 8 * (n + 2 * (size_t)c->d.plane), cudaMemcpyDeviceToDevice, st));
         CK(c, cudaMemsetAsync(c->a.q, 0, 8 * n, st));
         CK(c, cudaMemsetAsync(c->a.cgs, 0, 8 * n, st));
         RET_IF(cg1_matvec(c, true, st));
@@ -801,7 +816,7 @@ maspcg_status maspcg_get_unique_id(void *out) {
 }
 
 static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, const void *nccl_unique_id,
-                                 void *group, int cuda_device, maspcg_ctx **out) {
+                                 void *group, int cuda_device, maspcg_ctx **out, bool peer = false) {
     if (!out) return MASPCG_E_INVALID;
     *out = nullptr;
     auto fail = [](maspcg_status s, const char *m) {
@@ -811,8 +826,12 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     if (nr < 1 || nt < 1 || np < 1) return fail(MASPCG_E_INVALID, "nr, nt, np must be >= 1");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(MASPCG_E_INVALID, "bad rank / nranks");
     if (np % nranks != 0) return fail(MASPCG_E_INVALID, "np must be divisible by nranks");
-    if (!group && nranks > 1 && !nccl_unique_id)
+    if (!peer && !group && nranks > 1 && !nccl_unique_id)
         return fail(MASPCG_E_INVALID, "nccl_unique_id must be given when nranks > 1");
+    if (peer && nranks > kP2PMaxRanks) return fail(MASPCG_E_INVALID, "the peer communicator supports at most 16 ranks");
+    if (peer && group)
+        return fail(MASPCG_E_INVALID, "peer mode needs one CUDA context per rank (processes, CUDA IPC): ranks sharing "
+                                      "a context could spin on each other inside one device");
     const long long nloc = np / nranks;
     if ((nloc + 2) * (long long)nt * nr >= (1ll << 31))
         return fail(MASPCG_E_INVALID, "local slab too large (>= 2^31 cells with halos)");
@@ -842,7 +861,15 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
         maspcg_destroy(c);
         return MASPCG_E_CUDA;
     }
-    if (nranks > 1 || group || nccl_unique_id) {   // a communicator (also at nranks == 1 when one is given)
+    if (peer) {   // peer-memory communicator (peer.cu), also at nranks == 1 (pushes to itself)
+        int st = ST_OK;
+        c->ptab = new PeerTable();
+        c->comm = make_peer_comm(c->ptab, rank, nranks, &st, g_create_error);
+        if (!c->comm) {
+            maspcg_destroy(c);
+            return (maspcg_status)st;
+        }
+    } else if (nranks > 1 || group || nccl_unique_id) {   // a communicator (also at nranks == 1 when one is given)
         int st = ST_OK;
         c->comm = group ? make_loopback_comm((LoopbackGroup *)group, rank, nranks, &st, g_create_error)
                         : make_nccl_comm(nccl_unique_id, rank, nranks, &st, g_create_error);
@@ -879,6 +906,11 @@ maspcg_status maspcg_create(int nr, int nt, int np, int rank, int nranks, const 
     return create_impl(nr, nt, np, rank, nranks, nccl_unique_id, nullptr, cuda_device, out);
 }
 
+maspcg_status maspcg_create_peer(int nr, int nt, int np, int rank, int nranks, void *group, int cuda_device,
+                                 maspcg_ctx **out) {
+    return create_impl(nr, nt, np, rank, nranks, nullptr, group, cuda_device, out, true);
+}
+
 maspcg_status maspcg_loopback_group_create(int nranks, void **group) {
     if (!group) return MASPCG_E_INVALID;
     *group = loopback_group_create(nranks);
@@ -913,6 +945,12 @@ maspcg_status maspcg_destroy(maspcg_ctx *c) {
         if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
     c->gexec[0] = c->gexec[1] = nullptr;
     delete c->comm;
+    if (c->ptab) {
+        for (int g = 0; g < kP2PRegions; ++g)
+            for (int r = 0; r < kP2PMaxRanks; ++r) peer_close(c->ptab->mapping[g][r]);
+        delete c->ptab;
+        c->ptab = nullptr;
+    }
     for (cudaEvent_t e : c->tev) cudaEventDestroy(e);
     if (c->ev_p) cudaEventDestroy(c->ev_p);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
@@ -1035,6 +1073,27 @@ maspcg_status maspcg_local_extent(const maspcg_ctx *c, int *k0, int *nloc) {
     return MASPCG_OK;
 }
 
+// Peer mode: this rank's region `g` (workspace base, size); the peers' regions arrive by maspcg_peer_import.
+static maspcg_status peer_register(maspcg_ctx *c, int g, char *base, size_t bytes) {
+    if (!c->ptab) return MASPCG_OK;
+    PeerTable *t = c->ptab;
+    if (g == 0) {
+        t->area = c->a.p2p;
+        CK(c, cudaMemset(t->area, 0, sizeof(P2PArea)));
+        CK(c, cudaDeviceSynchronize());
+    }
+    t->bytes[g] = bytes;
+    for (int r = 0; r < kP2PMaxRanks; ++r) {
+        if (r != c->rank && t->mapping[g][r]) {
+            peer_close(t->mapping[g][r]);
+            t->mapping[g][r] = nullptr;
+        }
+        t->base[g][r] = nullptr;
+    }
+    t->base[g][c->rank] = base;
+    return MASPCG_OK;
+}
+
 size_t maspcg_workspace_bytes(const maspcg_ctx *c) { return c ? layout(c, nullptr, nullptr) : 0; }
 
 maspcg_status maspcg_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
@@ -1049,6 +1108,7 @@ maspcg_status maspcg_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
     CK(c, cudaMemset(c->a.sc, 0, sizeof(Scalars)));
     CK(c, cudaMemset(c->a.partials, 0, sizeof(double) * 8 * kRedBlocks));
     CK(c, cudaDeviceSynchronize());
+    RET_IF(peer_register(c, 0, (char *)dev_ptr, need));
     c->metric_dirty = true;
     c->coef_set = false;
     c->bc_set = false;
@@ -1352,6 +1412,7 @@ maspcg_status maspcg_vv_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes
     v.div_t = make_fastdiv((uint32_t)c->nt);
     c->vv_coef_set = c->vv_bc_set = false;
     c->vv_dirty = true;
+    RET_IF(peer_register(c, 1, (char *)dev_ptr, need));
     for (int b = 0; b < 2; ++b) {
         if (c->gexec[b]) {
             cudaGraphExecDestroy(c->gexec[b]);
@@ -1398,13 +1459,13 @@ maspcg_status maspcg_vv_set_bc_r(maspcg_ctx *c, maspcg_wall inner, const double 
     if (!c->vv_ws) SET_ERR(c, MASPCG_E_STATE, "vv_set_workspace must precede vv_set_bc_r");
     RET_IF(bind_device(c));
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t wplane = 3 * (size_t)c->nt, wsz = (size_t)(c->nloc + 2) * wplane;
-    CK(c, cudaMemsetAsync(c->va.gin, 0, 8 * wsz, st));
-    CK(c, cudaMemsetAsync(c->va.gout, 0, 8 * wsz, st));
-    if (g_inner)
-        CK(c, cudaMemcpyAsync(c->va.gin + wplane, g_inner, 8 * (size_t)c->nloc * wplane, cudaMemcpyDeviceToDevice, st));
-    if (g_outer)
-        CK(c, cudaMemcpyAsync(c->va.gout + wplane, g_outer, 8 * (size_t)c->nloc * wplane, cudaMemcpyDeviceToDevice, st));
+    // local planes only: the halo planes arrive by the exchange (with the peer communicator a neighbour may
+    // already have stored them, so they are never written locally)
+    const size_t wplane = 3 * (size_t)c->nt, wloc = (size_t)c->nloc * wplane;
+    if (g_inner) CK(c, cudaMemcpyAsync(c->va.gin + wplane, g_inner, 8 * wloc, cudaMemcpyDeviceToDevice, st));
+    else CK(c, cudaMemsetAsync(c->va.gin + wplane, 0, 8 * wloc, st));
+    if (g_outer) CK(c, cudaMemcpyAsync(c->va.gout + wplane, g_outer, 8 * wloc, cudaMemcpyDeviceToDevice, st));
+    else CK(c, cudaMemsetAsync(c->va.gout + wplane, 0, 8 * wloc, st));
     RET_IF(pad_planes(c, c->va.gin, wplane, st));
     RET_IF(pad_planes(c, c->va.gout, wplane, st));
     c->vd.wall_in = (int)inner;
@@ -1447,6 +1508,38 @@ maspcg_status maspcg_vv_get_diag(maspcg_ctx *c, double *D, void *stream) {
     RET_IF(ensure_vv(c, st));
     CK(c, cudaMemcpyAsync(D, c->va.D, 8 * 3 * (size_t)c->nloc * c->nt * c->nr, cudaMemcpyDeviceToHost, st));
     CK(c, cudaStreamSynchronize(st));
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_peer_export(maspcg_ctx *c, int region, void *out) {
+    if (!c || !out) return MASPCG_E_INVALID;
+    if (!c->ptab) SET_ERR(c, MASPCG_E_STATE, "not a peer-memory context (maspcg_create_peer)");
+    if (region < 0 || region >= kP2PRegions || !c->ptab->base[region][c->rank])
+        SET_ERR(c, MASPCG_E_STATE, "region %d has no workspace yet", region);
+    RET_IF(bind_device(c));
+    int st = peer_export(c->ptab->base[region][c->rank], c->ptab->bytes[region], out, c->err);
+    return (maspcg_status)st;
+}
+
+maspcg_status maspcg_peer_import(maspcg_ctx *c, int region, int rank, const void *in) {
+    if (!c || !in) return MASPCG_E_INVALID;
+    if (!c->ptab) SET_ERR(c, MASPCG_E_STATE, "not a peer-memory context (maspcg_create_peer)");
+    if (region < 0 || region >= kP2PRegions || rank < 0 || rank >= c->nranks)
+        SET_ERR(c, MASPCG_E_INVALID, "bad region or rank");
+    if (rank == c->rank) return MASPCG_OK;
+    RET_IF(bind_device(c));
+    char *base = nullptr;
+    size_t bytes = 0;
+    void *map = nullptr;
+    int st = peer_import(in, &base, &bytes, &map, c->err);
+    if (st != ST_OK) return (maspcg_status)st;
+    if (bytes != c->ptab->bytes[region]) {
+        peer_close(map);
+        SET_ERR(c, MASPCG_E_INVALID, "peer region size %zu differs from ours (%zu)", bytes, c->ptab->bytes[region]);
+    }
+    if (c->ptab->mapping[region][rank]) peer_close(c->ptab->mapping[region][rank]);
+    c->ptab->mapping[region][rank] = map;
+    c->ptab->base[region][rank] = base;
     return MASPCG_OK;
 }
 

@@ -91,7 +91,11 @@ SIGNATURES = {
     "maspcg_vv_apply": ([_V, _V, _V, _V], _I),
     "maspcg_vv_solve": ([_V, _V, _V, _D, _I, _V, ctypes.POINTER(Info), _V], _I),
     "maspcg_vv_get_diag": ([_V, _V, _V], _I),
+    "maspcg_create_peer": ([_I, _I, _I, _I, _I, _V, _I, ctypes.POINTER(_V)], _I),
+    "maspcg_peer_export": ([_V, _I, _V], _I),
+    "maspcg_peer_import": ([_V, _I, _I, _V], _I),
 }
+P2P_HANDLE_BYTES = 80
 
 _lib = None
 
@@ -145,11 +149,16 @@ class Solver:
 
     def __init__(self, nr: int, nt: int, np_: int, rf, tf, pf, *, group=None, device: int | None = None,
                  chunk: int = 16, loopback: "tuple[LoopbackGroup, int] | None" = None,
-                 force_comm: bool = False):
+                 force_comm: bool = False, comm: str = "nccl"):
+        """comm: "nccl" (NCCL send/recv and all-gathers) or "peer" (maspcg_create_peer: exchanges as
+        kernels storing into the peers' workspaces over NVLink; with `loopback` the ranks share this
+        process, otherwise the workspaces are mapped by CUDA IPC handles exchanged over `group`)."""
         import torch
         import torch.distributed as dist
         self._L = lib()
         self.ctx = None
+        self.comm = comm
+        self.group = group
         if not torch.cuda.is_available():
             raise MaspcgError(E_CUDA, "no CUDA device visible (libmaspcg has no CPU fallback)")
         if loopback is not None:
@@ -161,6 +170,16 @@ class Solver:
             self.rank, self.nranks = 0, 1
         self.device = torch.cuda.current_device() if device is None else int(device)
         uid = None
+        self._ipc = comm == "peer" and loopback is None and self.nranks > 1
+        if comm == "peer":
+            ctx = ctypes.c_void_p()
+            st = self._L.maspcg_create_peer(nr, nt, np_, self.rank, self.nranks,
+                                            loopback[0].handle if loopback is not None else None, self.device,
+                                            ctypes.byref(ctx))
+            if st != OK:
+                raise MaspcgError(st, self._L.maspcg_last_error(None).decode())
+            self._init_after_create(ctx, nr, nt, np_, rf, tf, pf, chunk)
+            return
         if loopback is not None:
             ctx = ctypes.c_void_p()
             st = self._L.maspcg_create_loopback(nr, nt, np_, self.rank, self.nranks, lgroup.handle, self.device,
@@ -201,7 +220,23 @@ class Solver:
         base = self.workspace.data_ptr()
         off = (-base) % 256
         self._check(self._L.maspcg_set_workspace(ctx, base + off, nbytes))
+        if getattr(self, "_ipc", False):
+            self._peer_exchange(0)
         self.set_option(OPT_CHUNK, chunk)
+
+    def _peer_exchange(self, region: int):
+        """Peer mode across processes: all-gather the CUDA IPC handles of workspace `region` over the
+        process group and map every peer's (maspcg_peer_export / maspcg_peer_import)."""
+        import torch.distributed as dist
+        buf = ctypes.create_string_buffer(P2P_HANDLE_BYTES)
+        self._check(self._L.maspcg_peer_export(self.ctx, region, buf))
+        allh = [None] * self.nranks
+        dist.all_gather_object(allh, buf.raw, group=self.group)
+        for r, h in enumerate(allh):
+            if r != self.rank:
+                hb = ctypes.create_string_buffer(h, P2P_HANDLE_BYTES)
+                self._check(self._L.maspcg_peer_import(self.ctx, region, r, hb))
+        dist.barrier(group=self.group)
 
     # ---------------------------------------------------------------- plumbing
     def _check(self, st: int, ctx="self", ok=(OK,)):
@@ -309,6 +344,8 @@ class Solver:
         self.vv_workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
         base = self.vv_workspace.data_ptr()
         self._check(self._L.maspcg_vv_set_workspace(self.ctx, base + (-base) % 256, nbytes))
+        if getattr(self, "_ipc", False):
+            self._peer_exchange(1)
 
     def vv_set_coefficients(self, nu, s, stream=None):
         """maspcg_vv_set_coefficients: cell viscosity and shift, device [nloc][nt][nr]."""
@@ -373,12 +410,13 @@ class LoopbackGroup:
             self.handle = None
 
 
-def solver_for_problem(prob, *, group=None, device=None, chunk=16, stream=None, loopback=None, force_comm=False):
+def solver_for_problem(prob, *, group=None, device=None, chunk=16, stream=None, loopback=None, force_comm=False,
+                       comm="nccl"):
     """Create a Solver for an inputs.Problem slab and upload its coefficients and BCs (device copies)."""
     import torch
     dev = f"cuda:{torch.cuda.current_device() if device is None else device}"
     S = Solver(prob.nr, prob.nt, prob.np, prob.rf, prob.tf, prob.pf, group=group, device=device, chunk=chunk,
-               loopback=loopback, force_comm=force_comm)
+               loopback=loopback, force_comm=force_comm, comm=comm)
     assert (S.k0, S.nloc) == (prob.k0, prob.nloc), "problem slab does not match the library's decomposition"
     T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     S.set_coefficients(T(prob.kr), T(prob.kt), T(prob.kp), T(prob.s), stream)
