@@ -38,6 +38,13 @@ class Comm {
     // In-place sum / max over ranks; every rank receives identical bits.
     virtual int allreduce_sum(double *dev, int count, cudaStream_t st, std::string &err) = 0;
     virtual int allreduce_max(int *dev, int count, cudaStream_t st, std::string &err) = 0;
+    // Global value of `npairs` Dot2 (p, s) pairs in place, combined in rank order, in ONE device step
+    // (peer communicator); false: the caller all-gathers and combines with its own kernel.
+    virtual bool has_pair_allreduce() const { return false; }
+    virtual int allreduce_pairs(double *, int, bool, cudaStream_t, std::string &err) {
+        err = "pair all-reduce not implemented by this communicator";
+        return ST_E_INVALID;
+    }
 };
 
 // Returns nullptr and sets *status / err on failure.

@@ -244,6 +244,10 @@ int graph_key(const maspcg_ctx *c) {
 // order with the same error-free arithmetic (identical bits on every rank).
 maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStream_t st) {
     if (!c->comm) return MASPCG_OK;
+    if (c->comm->has_pair_allreduce()) {   // peer communicator: push, wait and combine in one kernel
+        COMM(c, c->comm->allreduce_pairs(pairs, npairs, exact_arith(c), st, c->err));
+        return MASPCG_OK;
+    }
     COMM(c, c->comm->allgather(pairs, c->a.gather, 2 * npairs, st, c->err));
     launch_dd_combine(c->a.gather, c->nranks, npairs, pairs, exact_arith(c), st);
     return MASPCG_OK;
@@ -291,6 +295,10 @@ maspcg_status pad_planes(maspcg_ctx *c, double *buf, size_t plane, cudaStream_t 
 // global ring pairs: all-gather the ranks' Dot2 pairs [2 nr] and combine them in rank order
 maspcg_status vv_ring_allreduce(maspcg_ctx *c, double *ring, cudaStream_t st) {
     if (!c->comm) return MASPCG_OK;
+    if (c->comm->has_pair_allreduce()) {
+        COMM(c, c->comm->allreduce_pairs(ring, 2 * c->nr, exact_arith(c), st, c->err));
+        return MASPCG_OK;
+    }
     COMM(c, c->comm->allgather(ring, c->va.gather, 4 * c->nr, st, c->err));
     launch_dd_combine(c->va.gather, c->nranks, 2 * c->nr, ring, exact_arith(c), st);
     return MASPCG_OK;

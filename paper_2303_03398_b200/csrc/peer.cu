@@ -1,6 +1,6 @@
 // peer.cu -- the peer-memory communicator (SURVEY.md 8(e) lever 4: in-kernel exchanges instead of NCCL
 // calls): every exchange is a kernel that STORES into the receiving rank's memory over NVLink / NVSwitch
-// (CUDA IPC mappings of the peers' workspaces, or plain pointers for ranks sharing one device) and
+// (CUDA IPC mappings of the peers' workspaces, one process and one CUDA context per rank) and
 // signals it with a system-scope release flag; the receiver's 1-block wait kernel spins on its flags
 // with system-scope acquires.  No host round trip, no NCCL launch: the whole iteration, exchanges
 // included, is device work and is captured into the CUDA graphs.
@@ -8,8 +8,10 @@
 //   halo (the phi-slab planes of SURVEY 8(e)):  my first plane -> the left rank's upper halo plane,
 //       my last plane -> the right rank's lower halo plane (one push kernel, coalesced 16-byte stores),
 //       then wait for the two planes pushed into my halos;
-//   all-gather (the Dot2 pairs of the dot products): a 1-block kernel stores my pairs into slot [rank]
-//       of every rank's staging area, signals, waits for all, copies the staging into `recv`;
+//   all-reduce of the Dot2 pairs of the dot products: a 1-block kernel stores my pairs into slot [rank]
+//       of every rank's staging area, signals, waits for all and combines them in rank order (one graph
+//       node on the critical path of each PCG reduction); the plain all-gather is the same without the
+//       combination;
 //   all-reduce(max) of the validation flags: the same with ints, combined in rank order.
 //
 // Ordering.  Every exchange has a device-side epoch counter (the same sequence of exchanges runs on every
@@ -25,6 +27,7 @@
 #include <cstring>
 #include <string>
 
+#include "arith.cuh"
 #include "comm.cuh"
 #include "common.cuh"
 
@@ -112,6 +115,49 @@ __global__ void k_p2p_gather(const double *__restrict__ send, double *__restrict
     for (int r = 0; r < nranks; ++r)
         for (int t = threadIdx.x; t < count; t += blockDim.x)
             recv[(size_t)r * count + t] = __ldcg(&me->stage[par][r][t]);
+}
+
+// all-reduce of npairs Dot2 (p, s) pairs in place: push, signal, wait, then the rank-ordered error-free
+// combination of kernels.cu's k_dd_combine -- gather and combine in one kernel (one graph node on the
+// critical path of every PCG reduction)
+template <bool EXACT>
+__global__ void k_p2p_pairs(double *pairs, int npairs, P2PArea *me, Peers pe, int rank, int nranks) {
+    __shared__ unsigned long long e_s;
+    if (threadIdx.x == 0) e_s = me->epoch[P2P_GATHER] + 1;
+    __syncthreads();
+    const unsigned long long e = e_s;
+    const int par = (int)(e & 1);
+    const int count = 2 * npairs;
+    for (int r = 0; r < nranks; ++r)
+        for (int t = threadIdx.x; t < count; t += blockDim.x)
+            pe.dst[r][((size_t)par * kP2PMaxRanks + rank) * kP2PStage + t] = pairs[t];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        me->epoch[P2P_GATHER] = e;
+        for (int r = 0; r < nranks; ++r) st_release_sys(pe.flag[r], e);
+        for (int r = 0; r < nranks; ++r)
+            while (ld_acquire_sys(&me->flags[P2P_GATHER][r]) < e) __nanosleep(32);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
+        if (EXACT) {
+            Acc<true> acc;
+            for (int r = 0; r < nranks; ++r) {   // rank order: identical bits on every rank
+                Acc<true> o;
+                o.p = __ldcg(&me->stage[par][r][2 * t]);
+                o.s = __ldcg(&me->stage[par][r][2 * t + 1]);
+                acc.add(o);
+            }
+            pairs[2 * t] = acc.p;
+            pairs[2 * t + 1] = acc.s;
+        } else {
+            double v = 0.0;
+            for (int r = 0; r < nranks; ++r) v = __dadd_rn(v, __ldcg(&me->stage[par][r][2 * t]));
+            pairs[2 * t] = v;
+            pairs[2 * t + 1] = 0.0;
+        }
+    }
 }
 
 // all-reduce(max) of `count` ints (<= kP2PIStage), in place, rank order
@@ -206,6 +252,19 @@ class PeerComm final : public Comm {
             if (!pe.dst[r] || !pe.flag[r]) return fail("peer area not mapped", err);
         }
         k_p2p_gather<<<1, 256, 0, st>>>(send, recv, count, area(), pe, rank, nranks);
+        return ck(cudaGetLastError(), err);
+    }
+    bool has_pair_allreduce() const override { return true; }
+    int allreduce_pairs(double *pairs, int npairs, bool exact, cudaStream_t st, std::string &err) override {
+        if (2 * npairs > kP2PStage) return fail("pair all-reduce count too large", err);
+        Peers pe{};
+        for (int r = 0; r < nranks; ++r) {
+            pe.dst[r] = at(&area()->stage[0][0][0], r);
+            pe.flag[r] = at(&area()->flags[P2P_GATHER][rank], r);
+            if (!pe.dst[r] || !pe.flag[r]) return fail("peer area not mapped", err);
+        }
+        if (exact) k_p2p_pairs<true><<<1, 128, 0, st>>>(pairs, npairs, area(), pe, rank, nranks);
+        else k_p2p_pairs<false><<<1, 128, 0, st>>>(pairs, npairs, area(), pe, rank, nranks);
         return ck(cudaGetLastError(), err);
     }
     int allreduce_sum(double *, int, cudaStream_t, std::string &err) override {
