@@ -376,8 +376,8 @@ def main():
                     help="0 auto, 1 three kernels, 2 fused two passes, 3 wave, 4 single reduction (Chronopoulos-Gear)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch of the loop kernels")
     ap.add_argument("--kernel-timing", type=int, default=2,
-                    help="CUDA events around the hot kernels in the timed region: 2 sampled (slot 0 of every "
-                         "graph chunk), 1 every iteration, 0 none")
+                    help="CUDA events around the hot kernels in the timed region: 2 sampled (the middle slot of "
+                         "every graph chunk), 3 sampled (slot 0), 1 every iteration, 0 none")
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=0, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
@@ -504,7 +504,8 @@ def main():
                 "avg_launch_ms": mv_ms, "peak_source": peak_src,
                 "share_of_step": avg("matvec") * iters / ms if ms > 0 else None,
                 "timed_launches": stats["matvec_launches"],
-                "timing": {2: "sampled: every chunk-th iteration (slot 0 of each CUDA-graph chunk)",
+                "timing": {2: "sampled: every chunk-th iteration (the middle slot of each CUDA-graph chunk)",
+                           3: "sampled: every chunk-th iteration (slot 0 of each CUDA-graph chunk)",
                            1: "every iteration", 0: "off"}[args.kernel_timing],
                 "traffic_source": traffic_src}
 

@@ -113,8 +113,9 @@ typedef enum {
     MASPCG_OPT_CHUNK = 1,        /* PCG iterations per CUDA-graph launch (1..256, default 16) */
     MASPCG_OPT_USE_GRAPHS = 2,   /* 1 (default): replay captured graphs; 0: eager launches */
     MASPCG_OPT_TIMING = 3,       /* 1: CUDA events around every hot kernel of every iteration; 2: the same on every
-                                    chunk-th iteration only (slot 0 of each graph chunk; the records serialise the
-                                    kernels they separate, so sampling keeps the timed run close to untimed speed).
+                                    chunk-th iteration only (the middle slot of each graph chunk; the records
+                                    serialise the kernels they separate, so sampling keeps the timed run close to
+                                    untimed speed); 3: as 2 in slot 0 (the first kernels of each graph launch).
                                     Events are recorded by event nodes inside the captured graphs; two event sets
                                     alternate with the two chunks in flight */
     MASPCG_OPT_ARITH = 5,        /* 0 (default): oracle-identical arithmetic -- no FMA contraction, Dot2 (compensated)

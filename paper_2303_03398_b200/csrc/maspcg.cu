@@ -420,10 +420,13 @@ maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
 
 int timing_ev_index(int kern, int which, int it, int chunk) { return (kern * 2 + which) * chunk + it; }
 
-// Timing mode 1: events around every hot kernel of every iteration.  Timing mode 2 (sampled):
-// only in slot 0 of each chunk -- every chunk-th iteration -- so the event records (which serialise
-// the kernels they separate) cost ~1/chunk of their full-timing overhead.
-bool timed_slot(const maspcg_ctx *c, int slot) { return c->timing == 1 || (c->timing == 2 && slot == 0); }
+// Timing mode 1: events around every hot kernel of every iteration.  Timing mode 2 (sampled): only in
+// the middle slot of each chunk -- every chunk-th iteration, in the steady state of the graph's kernel
+// pipeline -- so the event records (which serialise the kernels they separate) cost ~1/chunk of their
+// full-timing overhead; mode 3: the same in slot 0 (the first kernels of each graph launch).
+bool timed_slot(const maspcg_ctx *c, int slot) {
+    return c->timing == 1 || (c->timing == 2 && slot == c->chunk / 2) || (c->timing == 3 && slot == 0);
+}
 
 // Record timing event (kern, which) of iteration slot `it` of the current set.  External records so
 // that, inside a stream capture, the graph node records the event at every replay.
@@ -1560,7 +1563,9 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             break;
         case MASPCG_OPT_USE_GRAPHS: c->use_graphs = v ? 1 : 0; break;
         case MASPCG_OPT_TIMING:
-            if (v < 0 || v > 2) SET_ERR(c, MASPCG_E_INVALID, "timing must be 0, 1 (every iteration) or 2 (sampled)");
+            if (v < 0 || v > 3)
+                SET_ERR(c, MASPCG_E_INVALID, "timing must be 0, 1 (every iteration), 2 (sampled, middle slot) or 3 "
+                                             "(sampled, slot 0)");
             c->timing = (int)v;
             break;
         case MASPCG_OPT_PDL:
