@@ -40,6 +40,23 @@ class Comm {
     virtual int allreduce_max(int *dev, int count, cudaStream_t st, std::string &err) = 0;
     // Global value of `npairs` Dot2 (p, s) pairs in place, combined in rank order, in ONE device step
     // (peer communicator); false: the caller all-gathers and combines with its own kernel.
+    // Peer communicator: the halo exchange of a padded buffer split in three, so a producing kernel can
+    // store its boundary planes itself (fused): the neighbours' halo addresses and flags, a push of the
+    // current planes (without waiting), and the wait (returns at once when *done is set).
+    virtual bool fusable_halo() const { return false; }
+    virtual int halo_targets(double *, size_t, int, double **, double **, unsigned long long **,
+                             unsigned long long **, std::string &err) {
+        err = "fused halo exchange not implemented by this communicator";
+        return ST_E_INVALID;
+    }
+    virtual int halo_push(double *, size_t, int, cudaStream_t, std::string &err) {
+        err = "fused halo exchange not implemented by this communicator";
+        return ST_E_INVALID;
+    }
+    virtual int halo_wait(const int *, cudaStream_t, std::string &err) {
+        err = "fused halo exchange not implemented by this communicator";
+        return ST_E_INVALID;
+    }
     virtual bool has_pair_allreduce() const { return false; }
     virtual int allreduce_pairs(double *, int, bool, cudaStream_t, std::string &err) {
         err = "pair all-reduce not implemented by this communicator";

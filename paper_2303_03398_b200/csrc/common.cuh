@@ -158,6 +158,13 @@ struct DevArrays {
     double *wave_partials;  // [nloc * tiles per plane][2]
     // reductions
     P2PArea *p2p;       // peer-memory communicator area
+    // peer mode, three-kernel path: the p-update stores its first plane into the left rank's upper halo
+    // and its last plane into the right rank's lower halo (NVLink stores fused into the update) and
+    // releases their flags; nullptr otherwise
+    double *peer_p_hi;                  // left rank's p + (nloc+1) plane
+    double *peer_p_lo;                  // right rank's p
+    unsigned long long *peer_flag_hi;   // left rank's flags[FROM_RIGHT][0]
+    unsigned long long *peer_flag_lo;   // right rank's flags[FROM_LEFT][0]
     double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums
     double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce
     Scalars *sc;

@@ -31,6 +31,17 @@ namespace {
 // (hiding the launch latency and the reduction tail); griddepcontrol.wait then blocks until the
 // previous grid has completed and its memory is visible, before any dependent data is read.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void st_release_sys64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// peer mode: after a p-update that stored its boundary planes into the neighbours' halos, release them
+__device__ __forceinline__ void release_p_halo(const DevArrays &a) {
+    __threadfence_system();
+    const unsigned long long e = a.p2p->epoch[P2P_HALO] + 1;
+    a.p2p->epoch[P2P_HALO] = e;
+    st_release_sys64(a.peer_flag_hi, e);
+    st_release_sys64(a.peer_flag_lo, e);
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
@@ -377,17 +388,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArr
             x[c] = A::axpy(alpha, pold, x[c]);
             const double pn = A::axpy(beta, pold, __ddiv_rn(__ldg(r + c), __ldg(D + c)));
             store_p(d, a.p, c, pn);
+            if (a.peer_p_lo) {   // peer mode: the boundary planes straight into the neighbours' halos
+                if (c < d.plane) a.peer_p_hi[c] = pn;
+                if (c >= d.n - d.plane) a.peer_p_lo[c - (d.n - d.plane)] = pn;
+            }
         }
     }
     __shared__ bool am_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        if (a.peer_p_lo) __threadfence_system();
+        else __threadfence();
         am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
     }
     __syncthreads();
     if (am_last && threadIdx.x == 0) {
         __threadfence();
+        if (a.peer_p_lo && !last) release_p_halo(a);
         const int it = sc->iter + 1;
         sc->iter = it;
         sc->rn = rn;
@@ -570,18 +587,23 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
             if (d.periodic_local) {
                 if (c < d.plane) st2(p + (size_t)c + (size_t)(d.nloc + 1) * d.plane, p0, p1);
                 if (c >= d.n - d.plane) st2(p + (size_t)c - (size_t)(d.nloc - 1) * d.plane, p0, p1);
+            } else if (a.peer_p_lo) {   // peer mode: the boundary planes straight into the neighbours' halos
+                if (c < d.plane) st2(a.peer_p_hi + c, p0, p1);
+                if (c >= d.n - d.plane) st2(a.peer_p_lo + (c - (d.n - d.plane)), p0, p1);
             }
         }
     }
     __shared__ bool am_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        if (a.peer_p_lo) __threadfence_system();
+        else __threadfence();
         am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
     }
     __syncthreads();
     if (am_last && threadIdx.x == 0) {
         __threadfence();
+        if (a.peer_p_lo && !last) release_p_halo(a);
         const int it = sc->iter + 1;
         sc->iter = it;
         sc->rn = rn;

@@ -76,6 +76,7 @@ struct maspcg_ctx {
 
     // options
     int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
+    int fuse_halo = 1;   // peer communicator: halo stores fused into the p-update (MASPCG_OPT_FUSE_HALO)
     // fused two-pass path geometry (fused.cu)
     int fused_bj = 1, fused_njt = 1, fused_blocks = 1;
     int tma_ok = 0, tma_njt = 1, tma_nch = 1, tma_hmax = 1, use_tma = 0;
@@ -237,7 +238,8 @@ bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 bool use_cg1(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 4; }
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
-           (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0) | (use_cg1(c) ? 256 : 0);
+           (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0) | (use_cg1(c) ? 256 : 0) |
+           (c->a.peer_p_lo ? 512 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -395,7 +397,10 @@ maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool lo
     }
     CK(c, cudaEventRecord(c->ev_p, st));
     CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
-    RET_IF(halo_padded(c, c->a.p, c->comm_stream));
+    if (loop && c->a.peer_p_lo)   // the p-update already stored its planes into the neighbours' halos
+        COMM(c, c->comm->halo_wait(&c->a.sc->done, c->comm_stream, c->err));
+    else
+        RET_IF(halo_padded(c, c->a.p, c->comm_stream));
     CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
     const unsigned gi = stencil_blocks(c->d, StencilPart::Interior, y);
     const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary, y);
@@ -686,6 +691,15 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     if (fused && c->comm) RET_IF(halo_planes(c, c->a.r, c->a.rh, st));   // r0 halo for pass A
     launch_setup_scalars(c->a, tol, maxit, st);
     const bool cg1 = use_cg1(c);
+    // peer communicator, three-kernel path: the p-update stores its boundary planes into the neighbours'
+    // halos itself (fused); the loop's stencils only wait.  p0 (from the setup) is pushed once here.
+    c->a.peer_p_lo = c->a.peer_p_hi = nullptr;
+    c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
+    if (c->comm && c->comm->fusable_halo() && !fused && !cg1 && !use_wave(c) && !c->vmode && c->fuse_halo) {
+        COMM(c, c->comm->halo_targets(c->a.p, c->d.plane, c->nloc, &c->a.peer_p_hi, &c->a.peer_p_lo,
+                                      &c->a.peer_flag_hi, &c->a.peer_flag_lo, c->err));
+        COMM(c, c->comm->halo_push(c->a.p, c->d.plane, c->nloc, st, c->err));
+    }
     if (cg1) {
         // single-reduction start: u0 = z0 (the padded p of the setup, periodic copies included), p = s = 0,
         // then w0 = A u0 and delta0 = w0.u0
@@ -762,6 +776,8 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     }
     launch_zero_x_if(c->d, c->a, x, st);
     launched += 1;
+    c->a.peer_p_lo = c->a.peer_p_hi = nullptr;   // only the loop's p-updates store into the neighbours
+    c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
     CK(c, cudaGetLastError());
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
@@ -1581,6 +1597,7 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             if (v < 0 || v > 1) SET_ERR(c, MASPCG_E_INVALID, "arith must be 0 (oracle-exact) or 1 (fast)");
             c->arith = (int)v;
             break;
+        case MASPCG_OPT_FUSE_HALO: c->fuse_halo = v ? 1 : 0; break;
         case MASPCG_OPT_PATH:
             if (v < 0 || v > 4)
                 SET_ERR(c, MASPCG_E_INVALID,

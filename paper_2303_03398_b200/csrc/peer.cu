@@ -92,6 +92,16 @@ __global__ void k_p2p_wait(P2PArea *me, const unsigned long long *f0, const unsi
         while (ld_acquire_sys(f1) < e) __nanosleep(64);
 }
 
+// as k_p2p_wait for the halo planes of the PCG loop: returns at once when the solve is done (the p-update
+// of the final iteration stores no planes, on every rank alike)
+__global__ void k_p2p_wait_loop(P2PArea *me, const int *done, int kind) {
+    if (threadIdx.x != 0) return;
+    if (*(volatile const int *)done) return;
+    const unsigned long long e = *(volatile unsigned long long *)&me->epoch[kind];
+    while (ld_acquire_sys(&me->flags[P2P_FROM_LEFT][0]) < e) __nanosleep(64);
+    while (ld_acquire_sys(&me->flags[P2P_FROM_RIGHT][0]) < e) __nanosleep(64);
+}
+
 // all-gather of `count` doubles (<= kP2PStage): push to every rank's staging slot [rank], signal, wait, copy
 __global__ void k_p2p_gather(const double *__restrict__ send, double *__restrict__ recv, int count, P2PArea *me,
                              Peers pe, int rank, int nranks) {
@@ -252,6 +262,30 @@ class PeerComm final : public Comm {
             if (!pe.dst[r] || !pe.flag[r]) return fail("peer area not mapped", err);
         }
         k_p2p_gather<<<1, 256, 0, st>>>(send, recv, count, area(), pe, rank, nranks);
+        return ck(cudaGetLastError(), err);
+    }
+    bool fusable_halo() const override { return true; }
+    int halo_targets(double *buf, size_t pl, int nloc, double **hi_dst, double **lo_dst, unsigned long long **flag_hi,
+                     unsigned long long **flag_lo, std::string &err) override {
+        *hi_dst = at(buf + (size_t)(nloc + 1) * pl, left());   // my first plane -> left's upper halo
+        *lo_dst = at(buf, right());                            // my last plane -> right's lower halo
+        *flag_hi = at(&area()->flags[P2P_FROM_RIGHT][0], left());
+        *flag_lo = at(&area()->flags[P2P_FROM_LEFT][0], right());
+        if (!*hi_dst || !*lo_dst || !*flag_hi || !*flag_lo) return fail("halo buffer outside the registered workspaces", err);
+        return ST_OK;
+    }
+    int halo_push(double *buf, size_t pl, int nloc, cudaStream_t st, std::string &err) override {
+        double *hi, *lo;
+        unsigned long long *fh, *fl;
+        if (int s = halo_targets(buf, pl, nloc, &hi, &lo, &fh, &fl, err)) return s;
+        unsigned g = (unsigned)((pl / 2 + 255) / 256);
+        if (g < 1) g = 1;
+        if (g > 296) g = 296;
+        k_p2p_push<<<g, 256, 0, st>>>(buf + pl, buf + (size_t)nloc * pl, hi, lo, pl, area(), fh, fl, P2P_HALO, g);
+        return ck(cudaGetLastError(), err);
+    }
+    int halo_wait(const int *done, cudaStream_t st, std::string &err) override {
+        k_p2p_wait_loop<<<1, 32, 0, st>>>(area(), done, P2P_HALO);
         return ck(cudaGetLastError(), err);
     }
     bool has_pair_allreduce() const override { return true; }

@@ -86,9 +86,11 @@ def _ipc_worker(rank, world, port, out_dir):
                                                                       k0=k0 or 0, nloc=n))]:
             k0, nloc = inputs.slab_extent(fn(None, None).np, rank, world)
             p = fn(k0, nloc)
-            for path in (1, 4):
+            for path in (1, 4, "1nofuse"):
                 S = maspcg.solver_for_problem(p, comm="peer")   # CUDA IPC handles all-gathered over gloo
-                S.set_option(maspcg.OPT_PATH, path)
+                S.set_option(maspcg.OPT_PATH, 1 if path == "1nofuse" else path)
+                if path == "1nofuse":   # the halo push as its own kernel instead of inside the p-update
+                    S.set_option(maspcg.OPT_FUSE_HALO, 0)
                 x = T(p.x0)
                 st, info, hist = S.solve(T(p.f), x, p.tol, p.maxit)
                 torch.cuda.synchronize()
@@ -128,8 +130,8 @@ def test_peer_processes_ipc(tmp_path, oracle_mod, world):
     res = [np.load(tmp_path / f"ipc{r}.npy", allow_pickle=True).item() for r in range(world)]
     probs = {"c1": inputs.make_problem("c1"), "rand": inputs.random_problem(10, 6, 8, 31, bc_in=0, bc_out=1)}
     for name, p in probs.items():
-        for path in (1, 4):
-            o = oracle_mod.solve_problem(p, variant="hs" if path == 1 else "cg1")
+        for path in (1, 4, "1nofuse"):
+            o = oracle_mod.solve_problem(p, variant="cg1" if path == 4 else "hs")
             for r in res:
                 st, it, hist, _ = r[(name, path)]
                 assert st == o["status"] == 0 and it == o["iters"] and np.array_equal(hist, o["hist"]), (name, path)
