@@ -165,6 +165,8 @@ struct DevArrays {
     double *peer_p_lo;                  // right rank's p
     unsigned long long *peer_flag_hi;   // left rank's flags[FROM_RIGHT][0]
     unsigned long long *peer_flag_lo;   // right rank's flags[FROM_LEFT][0]
+    int gather_ranks;   // > 0: the loop's dot products arrive all-gathered (gather[rank][pairs]) and the
+                        // consuming kernel combines them in rank order itself (no combine kernel)
     double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums
     double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce
     Scalars *sc;

@@ -316,6 +316,27 @@ __global__ void k_setup_scalars(DevArrays a, double tol, int maxit) {
     }
 }
 
+// Value of Dot2 pair t of `npairs`: the local / already combined pair, or -- gather_ranks > 0 -- the
+// rank-ordered combination of the all-gathered pairs, exactly as k_dd_combine forms it (so the consumer
+// kernel replaces the combine kernel on the critical path of every reduction).
+template <bool EXACT>
+__device__ __forceinline__ double pair_value(const DevArrays &a, const double *local, int t, int npairs) {
+    if (a.gather_ranks == 0) return __dadd_rn(local[2 * t], local[2 * t + 1]);
+    if (EXACT) {
+        Acc<true> acc;
+        for (int r = 0; r < a.gather_ranks; ++r) {
+            Acc<true> o;
+            o.p = a.gather[r * 2 * npairs + 2 * t];
+            o.s = a.gather[r * 2 * npairs + 2 * t + 1];
+            acc.add(o);
+        }
+        return __dadd_rn(acc.p, acc.s);
+    }
+    double v = 0.0;
+    for (int r = 0; r < a.gather_ranks; ++r) v = __dadd_rn(v, a.gather[r * 2 * npairs + 2 * t]);
+    return __dadd_rn(v, 0.0);
+}
+
 // ---------------------------------------------------------------- PCG loop (three-kernel path)
 // alpha = rho / p.Ap; r -= alpha q; z = r / D; Dot2 partials r.z, r.r.  The x update of this
 // iteration (x += alpha p) is deferred to k_pupdate, which reads p anyway (32 instead of 56 B/cell
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_update(Dims d, DevArra
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
-    const double pi = __dadd_rn(sc->red1[0], sc->red1[1]);
+    const double pi = pair_value<EXACT>(a, sc->red1, 0, 1);
     if (!(pi > 0.0) || !isfinite(pi)) {        // breakdown: uniform decision in every block; x = x_{k-1}
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             sc->status = ST_E_BREAKDOWN;
@@ -368,8 +389,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArr
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
-    const double rz = __dadd_rn(sc->red2[0], sc->red2[1]);
-    const double rr = __dadd_rn(sc->red2[2], sc->red2[3]);
+    const double rz = pair_value<EXACT>(a, sc->red2, 0, 2);
+    const double rr = pair_value<EXACT>(a, sc->red2, 1, 2);
     const double rn = sqrt(rr);
     const bool conv = rn <= sc->tolbn;
     const bool bad = !isfinite(rn) || !isfinite(rz);
@@ -520,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
-    const double pi = __dadd_rn(sc->red1[0], sc->red1[1]);
+    const double pi = pair_value<EXACT>(a, sc->red1, 0, 1);
     if (!(pi > 0.0) || !isfinite(pi)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             sc->status = ST_E_BREAKDOWN;
@@ -564,8 +585,8 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
     if (*(volatile int *)&sc->done) return;
-    const double rz = __dadd_rn(sc->red2[0], sc->red2[1]);
-    const double rr = __dadd_rn(sc->red2[2], sc->red2[3]);
+    const double rz = pair_value<EXACT>(a, sc->red2, 0, 2);
+    const double rr = pair_value<EXACT>(a, sc->red2, 1, 2);
     const double rn = sqrt(rr);
     const bool conv = rn <= sc->tolbn;
     const bool bad = !isfinite(rn) || !isfinite(rz);

@@ -239,19 +239,21 @@ bool use_cg1(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 4; }
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
            (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0) | (use_cg1(c) ? 256 : 0) |
-           (c->a.peer_p_lo ? 512 : 0);
+           (c->a.peer_p_lo ? 512 : 0) | (c->a.gather_ranks ? 1024 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
 // order with the same error-free arithmetic (identical bits on every rank).
-maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStream_t st) {
+// consumer_combines: the loop kernel that reads the pairs combines the gathered ones itself (gather_ranks).
+maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStream_t st,
+                             bool consumer_combines = false) {
     if (!c->comm) return MASPCG_OK;
     if (c->comm->has_pair_allreduce()) {   // peer communicator: push, wait and combine in one kernel
         COMM(c, c->comm->allreduce_pairs(pairs, npairs, exact_arith(c), st, c->err));
         return MASPCG_OK;
     }
     COMM(c, c->comm->allgather(pairs, c->a.gather, 2 * npairs, st, c->err));
-    launch_dd_combine(c->a.gather, c->nranks, npairs, pairs, exact_arith(c), st);
+    if (!consumer_combines) launch_dd_combine(c->a.gather, c->nranks, npairs, pairs, exact_arith(c), st);
     return MASPCG_OK;
 }
 
@@ -446,11 +448,11 @@ maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int i
     if (tm) CK(c, record_timing(c, 0, 0, it, st));
     RET_IF(stencil_with_halo(c, c->a.q, true, true, st));
     if (tm) CK(c, record_timing(c, 0, 1, it, st));
-    RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st));
+    RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st, c->a.gather_ranks > 0));
     if (tm) CK(c, record_timing(c, 1, 0, it, st));
     launch_update(c->d, c->a, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 1, 1, it, st));
-    RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st));
+    RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st, c->a.gather_ranks > 0));
     if (tm) CK(c, record_timing(c, 2, 0, it, st));
     launch_pupdate(c->d, c->a, x, c->chunk, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 2, 1, it, st));
@@ -653,7 +655,9 @@ long long kernels_per_iteration(const maspcg_ctx *c) {
     if (use_cg1(c)) return 2 + (c->comm ? 2 : 0);   // update, matvec (+ boundary part, combine on P > 1)
     if (use_fused(c) || use_wave(c)) return 2;
     if (!c->comm) return 3;
-    return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
+    // update, p-update, stencil interior + boundary; the peer communicator's halo wait and pair all-reduces
+    return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1 +
+           (c->comm->has_pair_allreduce() ? 3 : 0);
 }
 
 bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
@@ -695,6 +699,9 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     // halos itself (fused); the loop's stencils only wait.  p0 (from the setup) is pushed once here.
     c->a.peer_p_lo = c->a.peer_p_hi = nullptr;
     c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
+    // NCCL / loopback all-gathers in the three-kernel loop: the update and p-update kernels combine the
+    // gathered Dot2 pairs themselves (no combine kernel between the all-gather and its consumer)
+    c->a.gather_ranks = (c->comm && !c->comm->has_pair_allreduce() && !fused && !cg1 && !use_wave(c)) ? c->nranks : 0;
     if (c->comm && c->comm->fusable_halo() && !fused && !cg1 && !use_wave(c) && !c->vmode && c->fuse_halo) {
         COMM(c, c->comm->halo_targets(c->a.p, c->d.plane, c->nloc, &c->a.peer_p_hi, &c->a.peer_p_lo,
                                       &c->a.peer_flag_hi, &c->a.peer_flag_lo, c->err));
@@ -778,6 +785,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     launched += 1;
     c->a.peer_p_lo = c->a.peer_p_hi = nullptr;   // only the loop's p-updates store into the neighbours
     c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
+    c->a.gather_ranks = 0;
     CK(c, cudaGetLastError());
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
