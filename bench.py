@@ -357,6 +357,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
+    ap.add_argument("--shape", default=None,
+                    help="nr,nt,np override of the config's grid (same recipe), e.g. 150,300,75 = the per-GPU "
+                         "phi-slab of c3 at 8 GPUs, for one-GPU projections of the strong-scaling iteration")
     ap.add_argument("--chunk", type=int, default=16)
     ap.add_argument("--maxit", type=int, default=None, help="fixed-iteration mode (tol=0), e.g. for ncu")
     ap.add_argument("--from-fields", action="store_true",
@@ -409,10 +412,13 @@ def main():
 
     # ---- synthetic input of this rank's slab (decomposition-independent generator)
     nr, nt, np_ = inputs.CONFIGS[args.config]
-    if args.config == "c4":
+    shape = tuple(int(v) for v in args.shape.split(",")) if args.shape else None
+    if shape:
+        nr, nt, np_ = shape
+    if args.config == "c4" and not shape:
         np_ *= world
     k0, nloc = inputs.slab_extent(np_, rank, world)
-    prob = inputs.make_problem(args.config, k0, nloc, nranks=world)
+    prob = inputs.make_problem(args.config, k0, nloc, nranks=world, shape=shape)
     tol = 0.0 if args.maxit else prob.tol
     maxit = args.maxit if args.maxit else prob.maxit
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
@@ -577,7 +583,7 @@ def main():
     # ---- CPU baseline: the oracle as it stands on this box's host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ips, cpu_s, per_it = oracle_sample(inputs.make_problem(args.config), args.ref_iters)
+        ips, cpu_s, per_it = oracle_sample(inputs.make_problem(args.config, shape=shape), args.ref_iters)
         cpu = {"value": ips, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"oracle/masoracle.c (single-threaded C, -O2) on the full {args.config} grid: operator "
                          f"assembly + rhs + r0 once, then {args.ref_iters} PCG iterations (tol=0); "

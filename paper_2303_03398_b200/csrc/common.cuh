@@ -88,7 +88,8 @@ constexpr int kP2PRegions = 2;
 constexpr int kP2PStage = 16384;     // doubles per rank slot of an all-gather
 constexpr int kP2PIStage = 64;       // ints per rank slot of an all-reduce(max)
 constexpr int kP2PHandleBytes = 64 + 16;
-enum : int { P2P_FROM_LEFT = 0, P2P_FROM_RIGHT, P2P_SHIFT, P2P_GATHER, P2P_MAX, P2P_HALO, kP2PKinds };
+enum : int { P2P_FROM_LEFT = 0, P2P_FROM_RIGHT, P2P_SHIFT, P2P_GATHER, P2P_MAX, P2P_HALO, P2P_LL, kP2PKinds };
+constexpr int kP2PLLOffset = kP2PStage / 2;   // a rank slot: plain all-gather doubles, then LL words
 struct P2PArea {
     unsigned long long flags[kP2PKinds][kP2PMaxRanks];   // written by the senders (epoch of their last exchange)
     unsigned long long epoch[kP2PKinds];                  // this rank's exchange counters

@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArr
     const bool last = conv || bad || sc->iter + 1 >= sc->maxit;
     const double alpha = sc->alpha;
     const double beta = last ? 0.0 : __ddiv_rn(rz, sc->rho);
+    int peer_st = 0;
     const double *__restrict__ r = a.r;
     const double *__restrict__ D = a.D;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -410,15 +411,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArr
             const double pn = A::axpy(beta, pold, __ddiv_rn(__ldg(r + c), __ldg(D + c)));
             store_p(d, a.p, c, pn);
             if (a.peer_p_lo) {   // peer mode: the boundary planes straight into the neighbours' halos
-                if (c < d.plane) a.peer_p_hi[c] = pn;
-                if (c >= d.n - d.plane) a.peer_p_lo[c - (d.n - d.plane)] = pn;
+                if (c < d.plane) a.peer_p_hi[c] = pn, peer_st = 1;
+                if (c >= d.n - d.plane) a.peer_p_lo[c - (d.n - d.plane)] = pn, peer_st = 1;
             }
         }
     }
     __shared__ bool am_last;
-    __syncthreads();
+    peer_st = __syncthreads_or(peer_st);   // only blocks that stored into a peer pay the system-scope fence
     if (threadIdx.x == 0) {
-        if (a.peer_p_lo) __threadfence_system();
+        if (peer_st) __threadfence_system();
         else __threadfence();
         am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
     }
@@ -593,6 +594,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
     const bool last = conv || bad || sc->iter + 1 >= sc->maxit;
     const double alpha = sc->alpha;
     const double beta = last ? 0.0 : __ddiv_rn(rz, sc->rho);
+    int peer_st = 0;
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t npair = d.n >> 1;
     double *__restrict__ p = a.p;
@@ -609,15 +611,15 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
                 if (c < d.plane) st2(p + (size_t)c + (size_t)(d.nloc + 1) * d.plane, p0, p1);
                 if (c >= d.n - d.plane) st2(p + (size_t)c - (size_t)(d.nloc - 1) * d.plane, p0, p1);
             } else if (a.peer_p_lo) {   // peer mode: the boundary planes straight into the neighbours' halos
-                if (c < d.plane) st2(a.peer_p_hi + c, p0, p1);
-                if (c >= d.n - d.plane) st2(a.peer_p_lo + (c - (d.n - d.plane)), p0, p1);
+                if (c < d.plane) st2(a.peer_p_hi + c, p0, p1), peer_st = 1;
+                if (c >= d.n - d.plane) st2(a.peer_p_lo + (c - (d.n - d.plane)), p0, p1), peer_st = 1;
             }
         }
     }
     __shared__ bool am_last;
-    __syncthreads();
+    peer_st = __syncthreads_or(peer_st);   // only blocks that stored into a peer pay the system-scope fence
     if (threadIdx.x == 0) {
-        if (a.peer_p_lo) __threadfence_system();
+        if (peer_st) __threadfence_system();
         else __threadfence();
         am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
     }

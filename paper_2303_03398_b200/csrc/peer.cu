@@ -127,43 +127,66 @@ __global__ void k_p2p_gather(const double *__restrict__ send, double *__restrict
             recv[(size_t)r * count + t] = __ldcg(&me->stage[par][r][t]);
 }
 
-// all-reduce of npairs Dot2 (p, s) pairs in place: push, signal, wait, then the rank-ordered error-free
-// combination of kernels.cu's k_dd_combine -- gather and combine in one kernel (one graph node on the
-// critical path of every PCG reduction)
+// all-reduce of npairs Dot2 (p, s) pairs in place, with the LL ("low latency") protocol of NCCL: every
+// 8-byte store carries 4 bytes of data and the 4-byte epoch, so it is single-copy atomic and the receiver
+// polls the data itself -- no system-scope fence and no separate flag on the critical path of each PCG
+// reduction.  A double travels as two such words.  Staging (reinterpreted as 64-bit words, double-
+// buffered by epoch parity as above); then the rank-ordered error-free combination of k_dd_combine.
+__device__ __forceinline__ void st_word_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_word_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned int e) {
+    unsigned long long lo, hi;
+    while (((lo = ld_word_sys(w)) >> 32) != e) __nanosleep(20);
+    while (((hi = ld_word_sys(w + 1)) >> 32) != e) __nanosleep(20);
+    return __hiloint2double((int)(unsigned int)hi, (int)(unsigned int)lo);
+}
+
 template <bool EXACT>
 __global__ void k_p2p_pairs(double *pairs, int npairs, P2PArea *me, Peers pe, int rank, int nranks) {
-    __shared__ unsigned long long e_s;
-    if (threadIdx.x == 0) e_s = me->epoch[P2P_GATHER] + 1;
-    __syncthreads();
-    const unsigned long long e = e_s;
-    const int par = (int)(e & 1);
-    const int count = 2 * npairs;
-    for (int r = 0; r < nranks; ++r)
-        for (int t = threadIdx.x; t < count; t += blockDim.x)
-            pe.dst[r][((size_t)par * kP2PMaxRanks + rank) * kP2PStage + t] = pairs[t];
-    __syncthreads();
+    __shared__ unsigned int e_s;
     if (threadIdx.x == 0) {
-        __threadfence_system();
-        me->epoch[P2P_GATHER] = e;
-        for (int r = 0; r < nranks; ++r) st_release_sys(pe.flag[r], e);
-        for (int r = 0; r < nranks; ++r)
-            while (ld_acquire_sys(&me->flags[P2P_GATHER][r]) < e) __nanosleep(32);
+        e_s = (unsigned int)(me->epoch[P2P_LL] + 1);
+        me->epoch[P2P_LL] = me->epoch[P2P_LL] + 1;
     }
     __syncthreads();
+    const unsigned int e = e_s;
+    const int par = (int)(e & 1u);
+    const int count = 2 * npairs;   // doubles
+    const size_t slot_words = kP2PStage;   // words per rank slot (the double staging reinterpreted)
+    for (int r = 0; r < nranks; ++r) {
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(pe.dst[r]) +
+                                  ((size_t)par * kP2PMaxRanks + rank) * slot_words + kP2PLLOffset;
+        for (int t = threadIdx.x; t < count; t += blockDim.x) {
+            const double v = pairs[t];
+            const unsigned long long tag = (unsigned long long)e << 32;
+            st_word_sys(dst + 2 * t, tag | (unsigned int)__double2loint(v));
+            st_word_sys(dst + 2 * t + 1, tag | (unsigned int)__double2hiint(v));
+        }
+    }
+    __syncthreads();
+    const unsigned long long *mine = reinterpret_cast<const unsigned long long *>(&me->stage[0][0][0]);
     for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
         if (EXACT) {
             Acc<true> acc;
             for (int r = 0; r < nranks; ++r) {   // rank order: identical bits on every rank
+                const unsigned long long *w = mine + ((size_t)par * kP2PMaxRanks + r) * slot_words + kP2PLLOffset + 4 * t;
                 Acc<true> o;
-                o.p = __ldcg(&me->stage[par][r][2 * t]);
-                o.s = __ldcg(&me->stage[par][r][2 * t + 1]);
+                o.p = ll_recv(w, e);
+                o.s = ll_recv(w + 2, e);
                 acc.add(o);
             }
             pairs[2 * t] = acc.p;
             pairs[2 * t + 1] = acc.s;
         } else {
             double v = 0.0;
-            for (int r = 0; r < nranks; ++r) v = __dadd_rn(v, __ldcg(&me->stage[par][r][2 * t]));
+            for (int r = 0; r < nranks; ++r)
+                v = __dadd_rn(v, ll_recv(mine + ((size_t)par * kP2PMaxRanks + r) * slot_words + kP2PLLOffset + 4 * t, e));
             pairs[2 * t] = v;
             pairs[2 * t + 1] = 0.0;
         }
@@ -254,7 +277,7 @@ class PeerComm final : public Comm {
         return ck(cudaGetLastError(), err);
     }
     int allgather(const double *send, double *recv, int count, cudaStream_t st, std::string &err) override {
-        if (count > kP2PStage) return fail("all-gather count too large", err);
+        if (count > kP2PLLOffset) return fail("all-gather count too large", err);
         Peers pe{};
         for (int r = 0; r < nranks; ++r) {
             pe.dst[r] = at(&area()->stage[0][0][0], r);
@@ -290,7 +313,7 @@ class PeerComm final : public Comm {
     }
     bool has_pair_allreduce() const override { return true; }
     int allreduce_pairs(double *pairs, int npairs, bool exact, cudaStream_t st, std::string &err) override {
-        if (2 * npairs > kP2PStage) return fail("pair all-reduce count too large", err);
+        if (4 * npairs > kP2PStage - kP2PLLOffset) return fail("pair all-reduce count too large", err);
         Peers pe{};
         for (int r = 0; r < nranks; ++r) {
             pe.dst[r] = at(&area()->stage[0][0][0], r);
