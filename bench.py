@@ -62,6 +62,9 @@ PATHS = {
         "stencil": ("cg1 matvec: w = A u, Dot2 w.u (k_cg1_matvec)", 48),
         "update": ("cg1 update: convergence, p, s, x, r, u = r/D, Dot2 r.u, r.r (k_cg1_update)", 88),
         "pupdate": None, "iter": 136},
+    6: {"name": "persistent (one cooperative kernel per chunk, grid barriers)",
+        "stencil": ("persistent chunk kernel (k_persist)", 128), "update": ("(inside k_persist)", 0),
+        "pupdate": None, "iter": 128},
 }
 
 

@@ -105,7 +105,7 @@ typedef struct {
     long long pupdate_launches;
     double comm_ms;                /* halo + all-reduce time on the comm path (timing mode, P > 1) */
     int path;                      /* iteration path of the last solve: 1 = three kernels, 2 = fused two passes,
-                                      3 = wave, 4 = single reduction, 5 = vector viscosity */
+                                      3 = wave, 4 = single reduction, 5 = vector viscosity, 6 = persistent */
 } maspcg_stats;
 
 /* Options for maspcg_set_option(). */
@@ -138,7 +138,10 @@ typedef enum {
                                     re-read from L2 (112 B/cell of HBM traffic); 4 = single reduction (Chronopoulos-Gear
                                     PCG, R32): an update kernel and a matvec that forms u = r/D on the fly and reduces
                                     r.u, w.u and r.r together -- ONE all-reduce per iteration on P > 1 (128 B/cell);
-                                    its iterates are those of the oracle's single-reduction variant */
+                                    its iterates are those of the oracle's single-reduction variant; 5 = persistent
+                                    (single rank, nr even): one cooperative kernel runs a chunk of iterations, the
+                                    three phases of each separated by grid-wide (reduction) barriers instead of kernel
+                                    boundaries (the arithmetic, traffic and iterates of path 1) */
 } maspcg_option;
 
 /* ---- lifetime ----------------------------------------------------------- */

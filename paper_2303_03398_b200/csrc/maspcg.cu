@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "persist.cuh"
 #include "vv.cuh"
 #include "wave.cuh"
 
@@ -77,6 +78,7 @@ struct maspcg_ctx {
     // options
     int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
     int fuse_halo = 1;   // peer communicator: halo stores fused into the p-update (MASPCG_OPT_FUSE_HALO)
+    unsigned persist_grid = 0;   // path 5: co-resident grid of the persistent kernel
     // fused two-pass path geometry (fused.cu)
     int fused_bj = 1, fused_njt = 1, fused_blocks = 1;
     int tma_ok = 0, tma_njt = 1, tma_nch = 1, tma_hmax = 1, use_tma = 0;
@@ -236,6 +238,10 @@ bool use_fused(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 2 && c-
 bool use_wave(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 3 && !c->comm; }
 bool exact_arith(const maspcg_ctx *c) { return c->arith == 0; }
 bool use_cg1(const maspcg_ctx *c) { return !c->vmode && c->path_opt == 4; }
+// persistent iteration kernel (persist.cu): single rank, 16-byte pairs
+bool use_persist(const maspcg_ctx *c, const void *x) {
+    return !c->vmode && c->path_opt == 5 && !c->comm && c->d.vec_ok && (c->nr % 2 == 0) && (((uintptr_t)x & 15) == 0);
+}
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
            (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0) | (use_cg1(c) ? 256 : 0) |
@@ -592,6 +598,11 @@ maspcg_status enqueue_any(maspcg_ctx *c, double *x, cudaStream_t st, int slot) {
 
 maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st, int set) {
     c->tset = set;
+    if (use_persist(c, x)) {   // one cooperative launch runs the whole chunk
+        if (!c->persist_grid) c->persist_grid = persist_grid(c->device);
+        CK(c, launch_persist(c->d, c->a, x, c->chunk, c->chunk, c->persist_grid, exact_arith(c), st));
+        return MASPCG_OK;
+    }
     if (!c->use_graphs) {
         for (int it = 0; it < c->chunk; ++it) RET_IF(enqueue_any(c, x, st, it));
         CK(c, cudaGetLastError());
@@ -749,7 +760,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
         CK(c, cudaMemcpyAsync(c->snap[b], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
         CK(c, cudaEventRecord(c->ev_chunk[b], st));
         issued += c->chunk;
-        launched += (long long)c->chunk * kernels_per_iteration(c);
+        launched += use_persist(c, x) ? 1 : (long long)c->chunk * kernels_per_iteration(c);
         return MASPCG_OK;
     };
     if (!done) {
@@ -790,7 +801,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;
     c->stats.kernel_launches += launched;
-    c->stats.path = c->vmode ? 5 : (cg1 ? 4 : (use_wave(c) ? 3 : (fused ? 2 : 1)));
+    c->stats.path = c->vmode ? 5 : (cg1 ? 4 : (use_wave(c) ? 3 : (fused ? 2 : (use_persist(c, x) ? 6 : 1))));
     c->stats.solves += 1;
     c->stats.iterations += iters;
     if (info) {
@@ -1607,9 +1618,9 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             break;
         case MASPCG_OPT_FUSE_HALO: c->fuse_halo = v ? 1 : 0; break;
         case MASPCG_OPT_PATH:
-            if (v < 0 || v > 4)
-                SET_ERR(c, MASPCG_E_INVALID,
-                        "path must be 0 (auto), 1 (three kernels), 2 (fused), 3 (wave) or 4 (single reduction)");
+            if (v < 0 || v > 5)
+                SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels), 2 (fused), 3 (wave), 4 (single "
+                                             "reduction) or 5 (persistent)");
             c->path_opt = (int)v;
             break;
         default: SET_ERR(c, MASPCG_E_INVALID, "unknown option %d", (int)opt);
