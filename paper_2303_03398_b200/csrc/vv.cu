@@ -11,6 +11,8 @@
 // registers instead of storing them (which would cost 64 B/cell more).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "arith.cuh"
 #include "common.cuh"
 #include "vv.cuh"
@@ -79,6 +81,10 @@ struct Field {
     // e = wc * delta of cell (i, j, k), k in [-1, nloc-1], from the face values of the cell
     __device__ __forceinline__ double ediv_v(int i, int j, int k, double vrl, double vrh, double vtl, double vth,
                                              double vpl, double vph) const {
+        return ediv_w(i, j, k, vrl, vrh, vtl, vth, vpl, vph, __ldg(a.wc + PC(v, k, j, i)));
+    }
+    __device__ __forceinline__ double ediv_w(int i, int j, int k, double vrl, double vrh, double vtl, double vth,
+                                             double vpl, double vph, double wcv) const {
         const double fr_lo = mul(g.A_r(i, j, k), vrl);
         const double fr_hi = mul(g.A_r(i + 1, j, k), vrh);
         const double ft_lo = (j == 0) ? 0.0 : mul(g.A_t(i, j, k), vtl);
@@ -88,7 +94,7 @@ struct Field {
         const double fp_hi = mul(ap, vph);
         double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
         d = add(d, sub(fp_hi, fp_lo));
-        return mul(__ldg(a.wc + PC(v, k, j, i)), d);
+        return mul(wcv, d);
     }
     // r-edge at theta-face j (1..nt-1), phi-face k: v_phi(j), v_phi(j-1), v_theta(k), v_theta(k-1)
     __device__ __forceinline__ double Gr_v(int i, int j, int k, double vpj, double vpjm, double vtk, double vtkm) const {
@@ -493,6 +499,106 @@ __global__ void __launch_bounds__(kVVThreads, 3) k_vv_terms2(VVDims v, VVArrays 
     }
 }
 
+// The same phase with its 16-byte streams staged by cp.async into shared memory one grid-stride
+// iteration ahead (double-buffered, each thread copying and reading only its own slots, so no block
+// barrier): the HBM latency of an iteration's loads overlaps the previous iteration's arithmetic.
+constexpr int kStg = 11;   // staged streams per pair
+__device__ __forceinline__ void cp16(double2 *dst, const double *src) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <bool WALL>
+__global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays a, DevArrays base, int loop) {
+    if (loop && *(volatile int *)&base.sc->done) return;
+    extern __shared__ double2 stg[];   // [2][kStg][kVVThreads]
+    const Field<WALL> F{v, a, a.p, Geo{a}};
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = (v.ncell + 2 * v.plane1) >> 1;   // planes -1 .. nloc
+    const int nr = v.nr, nt = v.nt;
+    auto slot = [&](int stage, int s) -> double2 * { return stg + ((size_t)stage * kStg + s) * kVVThreads + threadIdx.x; };
+    auto issue = [&](uint32_t t, int stage) {
+        if (t < npair) {
+            int i0, j, k;
+            cell_of(v, 2 * t, i0, j, k);
+            k -= 1;
+            const int km = k > -1 ? k - 1 : -1, kp = k < v.nloc ? k + 1 : v.nloc;
+            const int jp = j < nt - 1 ? j + 1 : j, kw = k < 0 ? 0 : (k > v.nloc - 1 ? v.nloc - 1 : k);
+            const size_t pc = PC(v, k, j, i0);
+            cp16(slot(stage, 0), a.p + PV(v, k, 0, j, i0));
+            cp16(slot(stage, 1), a.p + PV(v, k, 1, j, i0));
+            cp16(slot(stage, 2), a.p + PV(v, k, 2, j, i0));
+            cp16(slot(stage, 3), a.p + PV(v, k, 1, jp, i0));
+            cp16(slot(stage, 4), a.p + PV(v, kp, 2, j, i0));
+            cp16(slot(stage, 5), a.p + PV(v, km, 0, j, i0));
+            cp16(slot(stage, 6), a.p + PV(v, km, 1, j, i0));
+            cp16(slot(stage, 7), a.Wt + pc);
+            cp16(slot(stage, 8), a.Wr + pc);
+            cp16(slot(stage, 9), a.Wp + UC(v, kw, j, i0));
+            cp16(slot(stage, 10), a.wc + pc);
+        }
+        cp_commit();
+    };
+    uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    issue(t, 0);
+    for (int it = 0; t < npair; t += stride, ++it) {
+        const int st = it & 1;
+        issue(t + stride, st ^ 1);
+        cp_wait1();   // this thread's copies of stage st have landed
+        int i0, j, k;
+        cell_of(v, 2 * t, i0, j, k);
+        k -= 1;
+        const int jm = j > 0 ? j - 1 : 0;
+        const size_t pc = PC(v, k, j, i0);
+        const bool last = (i0 + 2 == nr);
+        const double2 R = *slot(st, 0), T = *slot(st, 1), Pp = *slot(st, 2), Tj1 = *slot(st, 3), Pk1 = *slot(st, 4);
+        const double2 Rm = *slot(st, 5), Tkm = *slot(st, 6), wt = *slot(st, 7), wr = *slot(st, 8), wp = *slot(st, 9);
+        const double2 wcv = *slot(st, 10);
+        const double2 Pjm = L2(a.p + PV(v, k, 2, jm, i0));
+        const double2 Rjm = L2(a.p + PV(v, k, 0, jm, i0));
+        const double r2 = __ldg(a.p + PV(v, k, 0, j, last ? i0 : i0 + 2));
+        const double pm1 = __ldg(a.p + PV(v, k, 2, j, i0 > 0 ? i0 - 1 : 0));
+        const double tm1 = __ldg(a.p + PV(v, k, 1, j, i0 > 0 ? i0 - 1 : 0));
+        const double vr0 = (i0 == 0) ? F.gi(k, 0, j) : R.x;          // v_r on r-face i0 (wall at 0)
+        const double vr2 = last ? F.go(k, 0, j) : r2;
+        if (k <= v.nloc - 1) {
+            const double e0 = F.ediv_w(i0, j, k, vr0, R.y, T.x, Tj1.x, Pp.x, Pk1.x, wcv.x);
+            const double e1 = F.ediv_w(i0 + 1, j, k, R.y, vr2, T.y, Tj1.y, Pp.y, Pk1.y, wcv.y);
+            S2(a.E + pc, e0, e1);
+        }
+        if (k >= 0) {
+            const double vrm0 = (i0 == 0) ? F.gi(k - 1, 0, j) : Rm.x;
+            const double dn0 = (i0 == 0) ? F.gi(k, 2, j) : pm1;
+            S2(a.TT + pc, mul(wt.x, F.Gt_v(i0, j, k, vr0, vrm0, Pp.x, dn0)),
+               mul(wt.y, F.Gt_v(i0 + 1, j, k, R.y, Rm.y, Pp.y, Pp.x)));
+            double tr0 = 0.0, tr1 = 0.0, tp0 = 0.0, tp1 = 0.0;
+            if (j >= 1) {
+                tr0 = mul(wr.x, F.Gr_v(i0, j, k, Pp.x, Pjm.x, T.x, Tkm.x));
+                tr1 = mul(wr.y, F.Gr_v(i0 + 1, j, k, Pp.y, Pjm.y, T.y, Tkm.y));
+                if (k <= v.nloc - 1) {
+                    const double vrjm0 = (i0 == 0) ? F.gi(k, 0, j - 1) : Rjm.x;
+                    const double tdn0 = (i0 == 0) ? F.gi(k, 1, j) : tm1;
+                    tp0 = mul(wp.x, F.Gp_v(i0, j, T.x, tdn0, vr0, vrjm0));
+                    tp1 = mul(wp.y, F.Gp_v(i0 + 1, j, T.y, T.x, R.y, Rjm.y));
+                }
+            }
+            S2(a.TR + pc, tr0, tr1);
+            S2(a.TP + pc, tp0, tp1);
+            if (last) {
+                const size_t w = (size_t)(k + 1) * nt + j;
+                a.TTO[w] = mul(__ldg(a.WtO + w), F.Gt_v(nr, j, k, F.go(k, 0, j), F.go(k - 1, 0, j), F.go(k, 2, j), Pp.y));
+                a.TPO[w] = (j >= 1 && k <= v.nloc - 1)
+                               ? mul(__ldg(a.WpO + (size_t)k * nt + j),
+                                     F.Gp_v(nr, j, F.go(k, 1, j), T.y, F.go(k, 0, j), F.go(k, 0, j - 1)))
+                               : 0.0;
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 template <bool WITH_DOT, bool LOOP, bool EXACT>
 __global__ void __launch_bounds__(kVVThreads, 3) k_vv_rows2(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
                                                          unsigned total) {
@@ -504,6 +610,7 @@ __global__ void __launch_bounds__(kVVThreads, 3) k_vv_rows2(VVDims v, VVArrays a
     Acc<EXACT> dot[1];
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t npair = v.ncell >> 1;
+    // (staging these streams with cp.async as in k_vv_terms3 measured slower here: 643 vs 513 us)
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += stride) {
         int i0, j, k;
         cell_of(v, 2 * t, i0, j, k);
@@ -513,10 +620,14 @@ __global__ void __launch_bounds__(kVVThreads, 3) k_vv_rows2(VVDims v, VVArrays a
         const double2 pr = L2(a.p + PV(v, k, 0, j, i0));
         const double2 pt = L2(a.p + PV(v, k, 1, j, i0));
         const double2 pp = L2(a.p + PV(v, k, 2, j, i0));
-        const double2 tt = L2(a.TT + pc), tt1 = L2(a.TT + pc + pl);
-        const double tt2 = last ? __ldg(a.TTO + (size_t)(k + 1) * nt + j) : __ldg(a.TT + pc + 2);
+        const double2 tt = L2(a.TT + pc);
         const double2 tr = L2(a.TR + pc);
         const double2 tp = L2(a.TP + pc);
+        const double2 sm0 = L2(a.sM + UV(v, k, 0, j, i0));
+        const double2 sm1 = L2(a.sM + UV(v, k, 1, j, i0));
+        const double2 sm2 = L2(a.sM + UV(v, k, 2, j, i0));
+        const double2 tt1 = L2(a.TT + pc + pl);
+        const double tt2 = last ? __ldg(a.TTO + (size_t)(k + 1) * nt + j) : __ldg(a.TT + pc + 2);
         const double tp2 = last ? __ldg(a.TPO + (size_t)(k + 1) * nt + j) : __ldg(a.TP + pc + 2);
         // the remaining streams up front (addresses inside the padded arrays; unused values discarded)
         const double em1 = __ldg(E + pc - 1);
@@ -525,9 +636,6 @@ __global__ void __launch_bounds__(kVVThreads, 3) k_vv_rows2(VVDims v, VVArrays a
         const double2 ek = L2(E + pc - pl);
         const double2 tr1 = L2(a.TR + pc + pl);
         const double2 trj = L2(a.TR + pc + nr);
-        const double2 sm0 = L2(a.sM + UV(v, k, 0, j, i0));
-        const double2 sm1 = L2(a.sM + UV(v, k, 1, j, i0));
-        const double2 sm2 = L2(a.sM + UV(v, k, 2, j, i0));
         // r-faces i0 (i0 >= 1) and i0 + 1
         double yr0 = 0.0, yr1;
         {
@@ -680,19 +788,29 @@ __global__ void __launch_bounds__(kVVThreads) k_vv_mask(VVDims v, double *__rest
 // all blocks resident at once (no partial last wave): SMs x the kernel's occupancy, at most one block per
 // 256 work items
 template <typename K>
-unsigned resident_grid(K kern, uint32_t n) {
+unsigned resident_grid(K kern, uint32_t n, size_t smem = 0) {
     static int per_sm = 0, sms = 0;
     if (!per_sm) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kVVThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kVVThreads, smem);
         if (per_sm < 1) per_sm = 1;
     }
     uint64_t g = (n + kVVThreads - 1) / kVVThreads;
     const uint64_t cap = (uint64_t)sms * per_sm < (uint64_t)kRedBlocks ? (uint64_t)sms * per_sm : kRedBlocks;
     if (g > cap) g = cap;
     return g < 1 ? 1u : (unsigned)g;
+}
+
+// MASPCG_VV_STAGED=0 selects the register-only first phase (for comparisons)
+inline bool vv_staged() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MASPCG_VV_STAGED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
 }
 
 inline unsigned vv_grid(uint32_t n) {
@@ -730,7 +848,17 @@ void launch_vv_matvec(const VVDims &v, const VVArrays &a, const DevArrays &base,
                       bool wall, bool exact, cudaStream_t st) {
     const bool pair = (v.nr % 2 == 0) && (((uintptr_t)y & 15) == 0);
     const uint32_t nt1 = v.ncell + 2 * v.plane1;
-    if (pair) {
+    if (pair && vv_staged()) {
+        const size_t sm = sizeof(double2) * 2 * kStg * kVVThreads;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_vv_terms3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            cudaFuncSetAttribute(k_vv_terms3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr = true;
+        }
+        if (wall) k_vv_terms3<true><<<resident_grid(k_vv_terms3<true>, nt1 / 2, sm), kVVThreads, sm, st>>>(v, a, base, 0);
+        else k_vv_terms3<false><<<resident_grid(k_vv_terms3<false>, nt1 / 2, sm), kVVThreads, sm, st>>>(v, a, base, loop ? 1 : 0);
+    } else if (pair) {
         if (wall) k_vv_terms2<true><<<resident_grid(k_vv_terms2<true>, nt1 / 2), kVVThreads, 0, st>>>(v, a, base, 0);
         else k_vv_terms2<false><<<resident_grid(k_vv_terms2<false>, nt1 / 2), kVVThreads, 0, st>>>(v, a, base, loop ? 1 : 0);
     } else {
