@@ -530,6 +530,13 @@ def main():
         "iteration_GBps": path["iter"] * ncell_local * iters / sec / 1e9,
         "kernels_share_of_step": kern_ms / ms if ms > 0 else None,
     }
+    if stats["comm_launches"]:
+        # the Fig. 3 analogue (MPI time share): the reductions on the critical path and the
+        # halo exchange overlapped with the interior planes, per sampled iteration
+        red = stats["comm_ms"] / stats["comm_launches"]
+        per_kernel.update({"allreduce_ms_per_iteration": red,
+                           "halo_ms_per_iteration": stats["halo_ms"] / stats["comm_launches"],
+                           "allreduce_share_of_iteration": red * iters / ms if ms > 0 else None})
 
     # ---- end to end through the C ABI with HOST buffers (copies inside the timed region)
     e2e = None

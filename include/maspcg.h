@@ -103,7 +103,11 @@ typedef struct {
     long long update_launches;
     double pupdate_ms;             /* p_update */
     long long pupdate_launches;
-    double comm_ms;                /* halo + all-reduce time on the comm path (timing mode, P > 1) */
+    double comm_ms;                /* the two all-reduces of the sampled iterations (timing mode, P > 1, path 1): the
+                                      analogue of the MPI time of PAPER.md:282 (Fig. 3) on the critical path */
+    double halo_ms;                /* the halo exchange of those iterations on the comm stream (overlapped with the
+                                      interior planes of the stencil) */
+    long long comm_launches;       /* sampled iterations covered by comm_ms / halo_ms */
     int path;                      /* iteration path of the last solve: 1 = three kernels, 2 = fused two passes,
                                       3 = wave, 4 = single reduction, 5 = vector viscosity, 6 = persistent */
 } maspcg_stats;

@@ -85,7 +85,8 @@ struct maspcg_ctx {
     int wave_grid = 1;   // path 3: co-resident grid of k_wave
     cudaEvent_t ev_a = nullptr, ev_ph = nullptr;
     maspcg_stats stats{};
-    std::vector<cudaEvent_t> tev;   // timing events [2 sets][3 kernels][2][chunk]
+    std::vector<cudaEvent_t> tev;   // timing events [2 sets][6 kinds][2][chunk]: matvec, update, p-update,
+                                    // all-reduce #1, all-reduce #2, halo (P > 1)
     int tset = 0;                   // event set of the chunk being enqueued
 
     // staggered vector viscosity (NEXT-2, vv.cu): its own workspace, 1-D metric and state; the PCG
@@ -396,7 +397,9 @@ maspcg_status vv_stencil(maspcg_ctx *c, double *y, bool with_dot, bool loop, cud
 
 // Halo exchange of p (P > 1) overlapped with the interior of the stencil on
 // the caller's stream; joins before the boundary planes.
-maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st) {
+cudaError_t record_timing(maspcg_ctx *c, int kern, int which, int it, cudaStream_t st);
+
+maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st, int tslot = -1) {
     if (c->vmode) return vv_stencil(c, y, with_dot, loop, st);
     if (!c->comm) {
         launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
@@ -405,10 +408,12 @@ maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool lo
     }
     CK(c, cudaEventRecord(c->ev_p, st));
     CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
+    if (tslot >= 0) CK(c, record_timing(c, 5, 0, tslot, c->comm_stream));
     if (loop && c->a.peer_p_lo)   // the p-update already stored its planes into the neighbours' halos
         COMM(c, c->comm->halo_wait(&c->a.sc->done, c->comm_stream, c->err));
     else
         RET_IF(halo_padded(c, c->a.p, c->comm_stream));
+    if (tslot >= 0) CK(c, record_timing(c, 5, 1, tslot, c->comm_stream));
     CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
     const unsigned gi = stencil_blocks(c->d, StencilPart::Interior, y);
     const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary, y);
@@ -444,21 +449,26 @@ bool timed_slot(const maspcg_ctx *c, int slot) {
 // Record timing event (kern, which) of iteration slot `it` of the current set.  External records so
 // that, inside a stream capture, the graph node records the event at every replay.
 cudaError_t record_timing(maspcg_ctx *c, int kern, int which, int it, cudaStream_t st) {
-    const size_t idx = (size_t)c->tset * 6 * c->chunk + timing_ev_index(kern, which, it, c->chunk);
+    const size_t idx = (size_t)c->tset * 12 * c->chunk + timing_ev_index(kern, which, it, c->chunk);
     return cudaEventRecordWithFlags(c->tev[idx], st, cudaEventRecordExternal);
 }
 
 // One PCG iteration.  it: index within the chunk (timing).
 maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int it) {
     const bool tm = timed_slot(c, it);
+    const bool tc = tm && c->comm;
     if (tm) CK(c, record_timing(c, 0, 0, it, st));
-    RET_IF(stencil_with_halo(c, c->a.q, true, true, st));
+    RET_IF(stencil_with_halo(c, c->a.q, true, true, st, tc ? it : -1));
     if (tm) CK(c, record_timing(c, 0, 1, it, st));
+    if (tc) CK(c, record_timing(c, 3, 0, it, st));
     RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st, c->a.gather_ranks > 0));
+    if (tc) CK(c, record_timing(c, 3, 1, it, st));
     if (tm) CK(c, record_timing(c, 1, 0, it, st));
     launch_update(c->d, c->a, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 1, 1, it, st));
+    if (tc) CK(c, record_timing(c, 4, 0, it, st));
     RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st, c->a.gather_ranks > 0));
+    if (tc) CK(c, record_timing(c, 4, 1, it, st));
     if (tm) CK(c, record_timing(c, 2, 0, it, st));
     launch_pupdate(c->d, c->a, x, c->chunk, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 2, 1, it, st));
@@ -643,22 +653,27 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st, int set) 
 }
 
 void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
-    const size_t base = (size_t)set * 6 * c->chunk;
+    const size_t base = (size_t)set * 12 * c->chunk;
+    const bool comm = c->comm && !use_fused(c) && !use_cg1(c) && !use_wave(c);   // events of enqueue_iteration
     for (int it = 0; it < iters_in_chunk; ++it) {
         if (!timed_slot(c, it)) continue;
-        float ms[3];
-        for (int k = 0; k < 3; ++k) {
-            ms[k] = 0.f;
+        float ms[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int k = 0; k < (comm ? 6 : 3); ++k)
             cudaEventElapsedTime(&ms[k], c->tev[base + timing_ev_index(k, 0, it, c->chunk)],
                                  c->tev[base + timing_ev_index(k, 1, it, c->chunk)]);
-        }
         c->stats.matvec_ms += ms[0];
         c->stats.matvec_launches += 1;
         c->stats.update_ms += ms[1];
         c->stats.update_launches += 1;
         c->stats.pupdate_ms += ms[2];
         c->stats.pupdate_launches += 1;
+        if (comm) {   // the Fig. 3 analogue (MPI time): the two reductions and the halo
+            c->stats.comm_ms += ms[3] + ms[4];
+            c->stats.halo_ms += ms[5];
+            c->stats.comm_launches += 1;
+        }
     }
+    cudaGetLastError();   // elapsed-time queries of events that were not recorded on this path
 }
 
 long long kernels_per_iteration(const maspcg_ctx *c) {
@@ -1626,7 +1641,7 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
         default: SET_ERR(c, MASPCG_E_INVALID, "unknown option %d", (int)opt);
     }
     if (c->timing) {
-        const size_t need = (size_t)2 * 3 * 2 * c->chunk;
+        const size_t need = (size_t)2 * 6 * 2 * c->chunk;
         RET_IF(bind_device(c));
         while (c->tev.size() < need) {
             cudaEvent_t e;

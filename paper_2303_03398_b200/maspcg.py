@@ -50,7 +50,8 @@ class Stats(ctypes.Structure):
                 ("iterations", ctypes.c_longlong), ("matvec_ms", ctypes.c_double),
                 ("matvec_launches", ctypes.c_longlong), ("update_ms", ctypes.c_double),
                 ("update_launches", ctypes.c_longlong), ("pupdate_ms", ctypes.c_double),
-                ("pupdate_launches", ctypes.c_longlong), ("comm_ms", ctypes.c_double), ("path", ctypes.c_int)]
+                ("pupdate_launches", ctypes.c_longlong), ("comm_ms", ctypes.c_double), ("halo_ms", ctypes.c_double),
+                ("comm_launches", ctypes.c_longlong), ("path", ctypes.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
