@@ -58,6 +58,11 @@ class Comm {
         return ST_E_INVALID;
     }
     virtual bool has_pair_allreduce() const { return false; }
+    // peer communicator: every rank's staging area (for kernels that push their own LL words)
+    virtual int ll_targets(double **, std::string &err) {
+        err = "LL staging not available on this communicator";
+        return ST_E_INVALID;
+    }
     virtual int allreduce_pairs(double *, int, bool, cudaStream_t, std::string &err) {
         err = "pair all-reduce not implemented by this communicator";
         return ST_E_INVALID;

@@ -166,6 +166,10 @@ struct DevArrays {
     double *peer_p_lo;                  // right rank's p
     unsigned long long *peer_flag_hi;   // left rank's flags[FROM_RIGHT][0]
     unsigned long long *peer_flag_lo;   // right rank's flags[FROM_LEFT][0]
+    // peer communicator, path 1: the loop's Dot2 pairs are pushed to every rank by the last block of the
+    // producing kernel (LL words) and combined by the consuming kernel -- no reduction kernel at all
+    int p2p_ll, p2p_rank, p2p_nranks;
+    double *peer_stage[kP2PMaxRanks];   // rank r's P2PArea::stage, mapped into this process
     int gather_ranks;   // > 0: the loop's dot products arrive all-gathered (gather[rank][pairs]) and the
                         // consuming kernel combines them in rank order itself (no combine kernel)
     double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums

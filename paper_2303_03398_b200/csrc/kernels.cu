@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "arith.cuh"
+#include "p2p_ll.cuh"
 
 namespace maspcg {
 
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_matvec_flat(Dims d, De
             if (threadIdx.x == 0) {
                 a.sc->red1[0] = out[0].p;
                 a.sc->red1[1] = out[0].s;
+                if (a.p2p_ll) ll_push_pairs(a, a.sc->red1, 1);   // to every rank (peer communicator)
             }
         }
     }
@@ -321,6 +323,14 @@ __global__ void k_setup_scalars(DevArrays a, double tol, int maxit) {
 // kernel replaces the combine kernel on the critical path of every reduction).
 template <bool EXACT>
 __device__ __forceinline__ double pair_value(const DevArrays &a, const double *local, int t, int npairs) {
+    if (a.p2p_ll) {   // LL words of every rank, polled by the block at once; the first call fetches all pairs
+        __shared__ double v_s[2];
+        if (t == 0) {
+            __syncthreads();
+            ll_block_values<EXACT>(a, npairs, v_s);
+        }
+        return v_s[t];
+    }
     if (a.gather_ranks == 0) return __dadd_rn(local[2 * t], local[2 * t + 1]);
     if (EXACT) {
         Acc<true> acc;
@@ -375,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_update(Dims d, DevArra
             sc->red2[2] = out[1].p;
             sc->red2[3] = out[1].s;
             sc->alpha = alpha;
+            if (a.p2p_ll) ll_push_pairs(a, sc->red2, 2);
         }
     }
 }
@@ -530,6 +541,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, De
             if (threadIdx.x == 0) {
                 a.sc->red1[0] = out[0].p;
                 a.sc->red1[1] = out[0].s;
+                if (a.p2p_ll) ll_push_pairs(a, a.sc->red1, 1);   // to every rank (peer communicator)
             }
         }
     }
@@ -574,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
             sc->red2[2] = out[1].p;
             sc->red2[3] = out[1].s;
             sc->alpha = alpha;
+            if (a.p2p_ll) ll_push_pairs(a, sc->red2, 2);
         }
     }
 }

@@ -246,7 +246,7 @@ bool use_persist(const maspcg_ctx *c, const void *x) {
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
            (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0) | (use_cg1(c) ? 256 : 0) |
-           (c->a.peer_p_lo ? 512 : 0) | (c->a.gather_ranks ? 1024 : 0);
+           (c->a.peer_p_lo ? 512 : 0) | (c->a.gather_ranks ? 1024 : 0) | (c->a.p2p_ll ? 2048 : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -461,13 +461,13 @@ maspcg_status enqueue_iteration(maspcg_ctx *c, double *x, cudaStream_t st, int i
     RET_IF(stencil_with_halo(c, c->a.q, true, true, st, tc ? it : -1));
     if (tm) CK(c, record_timing(c, 0, 1, it, st));
     if (tc) CK(c, record_timing(c, 3, 0, it, st));
-    RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st, c->a.gather_ranks > 0));
+    if (!c->a.p2p_ll) RET_IF(allreduce_dot2(c, c->a.sc->red1, 1, st, c->a.gather_ranks > 0));
     if (tc) CK(c, record_timing(c, 3, 1, it, st));
     if (tm) CK(c, record_timing(c, 1, 0, it, st));
     launch_update(c->d, c->a, exact_arith(c), st);
     if (tm) CK(c, record_timing(c, 1, 1, it, st));
     if (tc) CK(c, record_timing(c, 4, 0, it, st));
-    RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st, c->a.gather_ranks > 0));
+    if (!c->a.p2p_ll) RET_IF(allreduce_dot2(c, c->a.sc->red2, 2, st, c->a.gather_ranks > 0));
     if (tc) CK(c, record_timing(c, 4, 1, it, st));
     if (tm) CK(c, record_timing(c, 2, 0, it, st));
     launch_pupdate(c->d, c->a, x, c->chunk, exact_arith(c), st);
@@ -725,6 +725,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     // halos itself (fused); the loop's stencils only wait.  p0 (from the setup) is pushed once here.
     c->a.peer_p_lo = c->a.peer_p_hi = nullptr;
     c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
+    c->a.p2p_ll = 0;
     // NCCL / loopback all-gathers in the three-kernel loop: the update and p-update kernels combine the
     // gathered Dot2 pairs themselves (no combine kernel between the all-gather and its consumer)
     c->a.gather_ranks = (c->comm && !c->comm->has_pair_allreduce() && !fused && !cg1 && !use_wave(c)) ? c->nranks : 0;
@@ -732,6 +733,13 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
         COMM(c, c->comm->halo_targets(c->a.p, c->d.plane, c->nloc, &c->a.peer_p_hi, &c->a.peer_p_lo,
                                       &c->a.peer_flag_hi, &c->a.peer_flag_lo, c->err));
         COMM(c, c->comm->halo_push(c->a.p, c->d.plane, c->nloc, st, c->err));
+        // and the two reductions of every iteration: pushed by the producing kernels, combined by the
+        // consuming ones (no reduction kernel)
+        COMM(c, c->comm->ll_targets(c->a.peer_stage, c->err));
+        c->a.p2p_ll = 1;
+        c->a.p2p_rank = c->rank;
+        c->a.p2p_nranks = c->nranks;
+        c->a.gather_ranks = 0;
     }
     if (cg1) {
         // single-reduction start: u0 = z0 (the padded p of the setup, periodic copies included), p = s = 0,
@@ -812,6 +820,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     c->a.peer_p_lo = c->a.peer_p_hi = nullptr;   // only the loop's p-updates store into the neighbours
     c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
     c->a.gather_ranks = 0;
+    c->a.p2p_ll = 0;
     CK(c, cudaGetLastError());
     CK(c, cudaStreamSynchronize(st));
     if (status < 0 && status != MASPCG_E_BREAKDOWN) status = MASPCG_E_CUDA;

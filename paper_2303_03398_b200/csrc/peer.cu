@@ -30,6 +30,7 @@
 #include "arith.cuh"
 #include "comm.cuh"
 #include "common.cuh"
+#include "p2p_ll.cuh"
 
 namespace maspcg {
 
@@ -132,21 +133,6 @@ __global__ void k_p2p_gather(const double *__restrict__ send, double *__restrict
 // polls the data itself -- no system-scope fence and no separate flag on the critical path of each PCG
 // reduction.  A double travels as two such words.  Staging (reinterpreted as 64-bit words, double-
 // buffered by epoch parity as above); then the rank-ordered error-free combination of k_dd_combine.
-__device__ __forceinline__ void st_word_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_word_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned int e) {
-    unsigned long long lo, hi;
-    while (((lo = ld_word_sys(w)) >> 32) != e) __nanosleep(20);
-    while (((hi = ld_word_sys(w + 1)) >> 32) != e) __nanosleep(20);
-    return __hiloint2double((int)(unsigned int)hi, (int)(unsigned int)lo);
-}
-
 template <bool EXACT>
 __global__ void k_p2p_pairs(double *pairs, int npairs, P2PArea *me, Peers pe, int rank, int nranks) {
     __shared__ unsigned int e_s;
@@ -165,8 +151,8 @@ __global__ void k_p2p_pairs(double *pairs, int npairs, P2PArea *me, Peers pe, in
         for (int t = threadIdx.x; t < count; t += blockDim.x) {
             const double v = pairs[t];
             const unsigned long long tag = (unsigned long long)e << 32;
-            st_word_sys(dst + 2 * t, tag | (unsigned int)__double2loint(v));
-            st_word_sys(dst + 2 * t + 1, tag | (unsigned int)__double2hiint(v));
+            ll_st(dst + 2 * t, tag | (unsigned int)__double2loint(v));
+            ll_st(dst + 2 * t + 1, tag | (unsigned int)__double2hiint(v));
         }
     }
     __syncthreads();
@@ -312,6 +298,13 @@ class PeerComm final : public Comm {
         return ck(cudaGetLastError(), err);
     }
     bool has_pair_allreduce() const override { return true; }
+    int ll_targets(double **stage, std::string &err) override {
+        for (int r = 0; r < nranks; ++r) {
+            stage[r] = at(&area()->stage[0][0][0], r);
+            if (!stage[r]) return fail("peer area not mapped", err);
+        }
+        return ST_OK;
+    }
     int allreduce_pairs(double *pairs, int npairs, bool exact, cudaStream_t st, std::string &err) override {
         if (4 * npairs > kP2PStage - kP2PLLOffset) return fail("pair all-reduce count too large", err);
         Peers pe{};
