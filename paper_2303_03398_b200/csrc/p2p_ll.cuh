@@ -87,27 +87,4 @@ __device__ __forceinline__ void ll_block_values(const DevArrays &a, int npairs, 
     __syncthreads();
 }
 
-// one thread: the value of pair t (of npairs) of the current LL epoch, combined in rank order exactly as
-// k_dd_combine does, then p + s
-template <bool EXACT>
-__device__ __forceinline__ double ll_pair_value(const DevArrays &a, int t) {
-    P2PArea *me = a.p2p;
-    const unsigned int e = (unsigned int)(*(volatile unsigned long long *)&me->epoch[P2P_LL]);
-    double *mine = &me->stage[0][0][0];
-    if (EXACT) {
-        Acc<true> acc;
-        for (int r = 0; r < a.p2p_nranks; ++r) {
-            const unsigned long long *w = ll_slot(mine, (int)(e & 1u), r) + 4 * t;
-            Acc<true> o;
-            o.p = ll_recv(w, e);
-            o.s = ll_recv(w + 2, e);
-            acc.add(o);
-        }
-        return __dadd_rn(acc.p, acc.s);
-    }
-    double v = 0.0;
-    for (int r = 0; r < a.p2p_nranks; ++r) v = __dadd_rn(v, ll_recv(ll_slot(mine, (int)(e & 1u), r) + 4 * t, e));
-    return __dadd_rn(v, 0.0);
-}
-
 }  // namespace maspcg
