@@ -52,14 +52,14 @@ METRIC = "PCG iterations/s & matvec HBM GB/s (% of peak) at 1/2/4/8 B200"
 UNIT = "PCG iterations/s"
 # algorithmic bytes per cell of each kernel
 PATHS = {
-    1: {"name": "three kernels", "stencil": ("stencil_matvec_dot (k_matvec_flat)", 48),
-        "update": ("update_jacobi_dots (k_update)", 32), "pupdate": ("x_and_p_update (k_pupdate)", 48), "iter": 128},
+    1: {"name": "three kernels", "stencil": ("stencil_matvec_dot (k_matvec_vec2; k_matvec_flat for odd nr)", 48),
+        "update": ("update_jacobi_dots (k_update_vec2; k_update for odd nr)", 32), "pupdate": ("x_and_p_update (k_pupdate_vec2; k_pupdate for odd nr)", 48), "iter": 128},
     2: {"name": "fused two passes", "stencil": ("pass A: p-update + x-update + stencil + p.q (k_pass_a)", 80),
         "update": ("pass B: r-update + Jacobi + r.z, r.r (k_pass_b)", 32), "pupdate": None, "iter": 112},
     3: {"name": "wave", "stencil": ("wave: x/p-update + stencil + p.q, flag-ordered (k_wave)", 80),
         "update": ("update_jacobi_dots (k_update_vec2)", 32), "pupdate": None, "iter": 112},
     4: {"name": "single reduction (Chronopoulos-Gear)",
-        "stencil": ("cg1 matvec: w = A u, Dot2 w.u (k_cg1_matvec)", 48),
+        "stencil": ("cg1 matvec: w = A u, Dot2 w.u (the stencil kernel k_matvec_vec2 on u)", 48),
         "update": ("cg1 update: convergence, p, s, x, r, u = r/D, Dot2 r.u, r.r (k_cg1_update)", 88),
         "pupdate": None, "iter": 136},
     6: {"name": "persistent (one cooperative kernel per chunk, grid barriers)",
