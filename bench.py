@@ -38,6 +38,8 @@ def emit(line: dict):
     global _JSON_OUT
     if _JSON_OUT is None:
         _JSON_OUT = sys.stdout
+    if SHARED_GPU:
+        line["test_mode"] = "MASPCG_BENCH_SHARED_GPU: every rank on cuda:0, not a measurement"
     _JSON_OUT.write(json.dumps(line) + "\n")
     _JSON_OUT.flush()
 
@@ -50,6 +52,33 @@ def protect_stdout():
 
 METRIC = "PCG iterations/s & matvec HBM GB/s (% of peak) at 1/2/4/8 B200"
 UNIT = "PCG iterations/s"
+# Test mode only (MASPCG_BENCH_SHARED_GPU=1, with --comm peer): every torchrun rank on cuda:0 and a gloo
+# process group, so the N > 1 code path of this script (slabs, peer communicator, barriers, max over
+# ranks, rank-0 output) runs on a one-GPU box.  Never used for a reported number.
+SHARED_GPU = os.environ.get("MASPCG_BENCH_SHARED_GPU") == "1"
+
+
+def init_dist(world):
+    import torch
+    import torch.distributed as dist
+    local = 0 if SHARED_GPU else int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        if SHARED_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return local
+
+
+def max_over_ranks(v, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], device="cpu" if SHARED_GPU else dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # algorithmic bytes per cell of each kernel
 PATHS = {
     1: {"name": "three kernels", "stencil": ("stencil_matvec_dot (k_matvec_vec2; k_matvec_flat for odd nr)", 48),
@@ -183,10 +212,7 @@ def run_vv(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    local = init_dist(world)
     dev = torch.device(f"cuda:{local}")
     cfg = args.config if args.config in inputs.VV_CONFIGS else "c3v"
     nr, nt, np_ = inputs.VV_CONFIGS[cfg]
@@ -233,9 +259,7 @@ def run_vv(args):
     stats = S.stats()
     S.set_option(maspcg.OPT_TIMING, 0)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     sec = ms / 1e3
     value = iters / sec
     ncl = prob.nloc * nt * nr
@@ -405,12 +429,9 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    local = init_dist(world)
     dev = torch.device(f"cuda:{local}")
 
     # ---- synthetic input of this rank's slab (decomposition-independent generator)
@@ -489,9 +510,7 @@ def main():
     stats = S.stats()
     S.set_option(maspcg.OPT_TIMING, 0)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     sec = ms / 1e3
     value = iters / sec                                 # global solve iterations (strong scaling)
     ncell_local = prob.ncell_local
@@ -564,9 +583,7 @@ def main():
         torch.cuda.synchronize()
         th = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([th], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            th = float(t.item())
+            th = max_over_ranks(th, dev)
         e2e = {"value": it_h / th, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": 1e3 * th / args.steps, "api": "maspcg_set_coefficients_host + maspcg_solve_host"}
 
