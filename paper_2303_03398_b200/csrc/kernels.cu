@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, De
     }
 }
 
-template <bool EXACT>
+template <bool EXACT, bool UP2>
 __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, DevArrays a, unsigned total, int rev) {
     pdl_wait();
     pdl_trigger();
@@ -569,10 +569,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
     Acc<EXACT> acc[2];
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t npair = d.n >> 1;
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < npair; w += stride) {
-        const uint32_t v = rev ? npair - 1 - w : w;
-        const uint32_t c = 2u * v;
-        const double2 rv = ld2rw(r + c), qv = ld2(a.q + c), dv = ld2(a.D + c);
+    auto body = [&](uint32_t c, double2 rv, double2 qv, double2 dv) {
         const double r0 = A::ymax(rv.x, alpha, qv.x), r1 = A::ymax(rv.y, alpha, qv.y);
         st2(r + c, r0, r1);
         const double z0 = __ddiv_rn(r0, dv.x), z1 = __ddiv_rn(r1, dv.y);
@@ -580,6 +577,20 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
         acc[0].add(r1, z1);
         acc[1].add(r0, r0);
         acc[1].add(r1, r1);
+    };
+    uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (UP2) {   // two pairs per trip, loads first; the same per-thread order of the sums
+        for (; w + stride < npair; w += 2 * stride) {
+            const uint32_t c0 = 2u * (rev ? npair - 1 - w : w), c1 = 2u * (rev ? npair - 1 - (w + stride) : w + stride);
+            const double2 rv0 = ld2rw(r + c0), qv0 = ld2(a.q + c0), dv0 = ld2(a.D + c0);
+            const double2 rv1 = ld2rw(r + c1), qv1 = ld2(a.q + c1), dv1 = ld2(a.D + c1);
+            body(c0, rv0, qv0, dv0);
+            body(c1, rv1, qv1, dv1);
+        }
+    }
+    for (; w < npair; w += stride) {
+        const uint32_t c = 2u * (rev ? npair - 1 - w : w);
+        body(c, ld2rw(r + c), ld2(a.q + c), ld2(a.D + c));
     }
     Acc<EXACT> out[2];
     if (reduce_last<EXACT, kThreads, 2>(acc, a.partials, &sc->ticket[1], blockIdx.x, total, out)) {
@@ -594,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
     }
 }
 
-template <bool EXACT>
+template <bool EXACT, bool PU2>
 __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, DevArrays a, double *__restrict__ x, int chunk,
                                                            unsigned total) {
     pdl_wait();
@@ -614,12 +625,9 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t npair = d.n >> 1;
     double *__restrict__ p = a.p;
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < npair; v += stride) {
-        const uint32_t c = 2u * v;
-        const double2 po = ld2rw(p + (size_t)c + d.plane), xv = ld2rw(x + c);
+    auto store = [&](uint32_t c, double2 po, double2 xv, double2 rv, double2 dv) {
         st2(x + c, A::axpy(alpha, po.x, xv.x), A::axpy(alpha, po.y, xv.y));
         if (!last) {
-            const double2 rv = ld2(a.r + c), dv = ld2(a.D + c);
             const double p0 = A::axpy(beta, po.x, __ddiv_rn(rv.x, dv.x));
             const double p1 = A::axpy(beta, po.y, __ddiv_rn(rv.y, dv.y));
             st2(p + (size_t)c + d.plane, p0, p1);
@@ -631,6 +639,26 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
                 if (c >= d.n - d.plane) st2(a.peer_p_lo + (c - (d.n - d.plane)), p0, p1), peer_st = 1;
             }
         }
+    };
+    const double2 z2 = make_double2(0.0, 0.0);
+    uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (PU2) {
+        // two pairs per thread and trip: all eight 16-byte loads issued before the first store
+        for (; v + stride < npair; v += 2 * stride) {
+            const uint32_t c0 = 2u * v, c1 = 2u * (v + stride);
+            const double2 po0 = ld2rw(p + (size_t)c0 + d.plane), xv0 = ld2rw(x + c0);
+            const double2 po1 = ld2rw(p + (size_t)c1 + d.plane), xv1 = ld2rw(x + c1);
+            const double2 rv0 = last ? z2 : ld2(a.r + c0), dv0 = last ? z2 : ld2(a.D + c0);
+            const double2 rv1 = last ? z2 : ld2(a.r + c1), dv1 = last ? z2 : ld2(a.D + c1);
+            store(c0, po0, xv0, rv0, dv0);
+            store(c1, po1, xv1, rv1, dv1);
+        }
+    }
+    for (; v < npair; v += stride) {
+        const uint32_t c = 2u * v;
+        const double2 po = ld2rw(p + (size_t)c + d.plane), xv = ld2rw(x + c);
+        const double2 rv = last ? z2 : ld2(a.r + c), dv = last ? z2 : ld2(a.D + c);
+        store(c, po, xv, rv, dv);
     }
     __shared__ bool am_last;
     peer_st = __syncthreads_or(peer_st);   // only blocks that stored into a peer pay the system-scope fence
@@ -880,8 +908,15 @@ void launch_update(const Dims &d, const DevArrays &a, bool exact, cudaStream_t s
         // and ends on the cells the ascending p-update reads first; +0.4 % iterations/s on c3.
         // MASPCG_REV_UPDATE=0 restores the ascending order.
         static const int rev = getenv("MASPCG_REV_UPDATE") ? atoi(getenv("MASPCG_REV_UPDATE")) : 1;
-        if (exact) launch_pdl(d.pdl != 0, k_update_vec2<true>, gv, st, d, a, gv, rev);
-        else launch_pdl(d.pdl != 0, k_update_vec2<false>, gv, st, d, a, gv, rev);
+        // two pairs per thread and trip (6 loads in flight before the first use): 6.38 vs 5.96 TB/s live
+        static const int up2 = getenv("MASPCG_UPDATE2") ? atoi(getenv("MASPCG_UPDATE2")) : 1;
+        if (up2) {
+            if (exact) launch_pdl(d.pdl != 0, k_update_vec2<true, true>, gv, st, d, a, gv, rev);
+            else launch_pdl(d.pdl != 0, k_update_vec2<false, true>, gv, st, d, a, gv, rev);
+        } else {
+            if (exact) launch_pdl(d.pdl != 0, k_update_vec2<true, false>, gv, st, d, a, gv, rev);
+            else launch_pdl(d.pdl != 0, k_update_vec2<false, false>, gv, st, d, a, gv, rev);
+        }
         return;
     }
     const unsigned g = grid_for(d.n);
@@ -892,8 +927,15 @@ void launch_update(const Dims &d, const DevArrays &a, bool exact, cudaStream_t s
 void launch_pupdate(const Dims &d, const DevArrays &a, double *x, int chunk, bool exact, cudaStream_t st) {
     if (use_vec2(d, x)) {
         const unsigned gv = grid_vec2(d.n);
-        if (exact) launch_pdl(d.pdl != 0, k_pupdate_vec2<true>, gv, st, d, a, x, chunk, gv);
-        else launch_pdl(d.pdl != 0, k_pupdate_vec2<false>, gv, st, d, a, x, chunk, gv);
+        // one pair per trip with its four loads ahead of the x store (6.46 TB/s live; two pairs: 6.32)
+        static const int pu2 = getenv("MASPCG_PUPDATE2") ? atoi(getenv("MASPCG_PUPDATE2")) : 0;
+        if (pu2) {
+            if (exact) launch_pdl(d.pdl != 0, k_pupdate_vec2<true, true>, gv, st, d, a, x, chunk, gv);
+            else launch_pdl(d.pdl != 0, k_pupdate_vec2<false, true>, gv, st, d, a, x, chunk, gv);
+        } else {
+            if (exact) launch_pdl(d.pdl != 0, k_pupdate_vec2<true, false>, gv, st, d, a, x, chunk, gv);
+            else launch_pdl(d.pdl != 0, k_pupdate_vec2<false, false>, gv, st, d, a, x, chunk, gv);
+        }
         return;
     }
     const unsigned g = grid_for(d.n);
