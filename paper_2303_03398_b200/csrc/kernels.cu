@@ -470,7 +470,7 @@ __device__ __forceinline__ void st2(double *p, double a, double b) {
     *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
 
-template <bool WITH_DOT, bool LOOP, bool EXACT>
+template <bool WITH_DOT, bool LOOP, bool EXACT, bool MV2>
 __global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, DevArrays a, double *__restrict__ y,
                                                                       Range rg, unsigned red_slot0,
                                                                       unsigned red_total) {
@@ -488,54 +488,74 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, De
     Acc<EXACT> dot[1];
     const uint32_t stride = gridDim.x * blockDim.x;
     const uint32_t npair = rg.vend >> 1;
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < npair; v += stride) {
+    // the loads of one pair (all issued before its first use), then its arithmetic
+    struct PairIn {
+        double2 pc, trv, ttl, tpl, tph, pkm, pkp, dv, ptm, ptp, tth;
+        double pm, pp2, tr2;
+        uint32_t c;
+        bool jlo, jhi, ilo, ihi;
+    };
+    auto load = [&](uint32_t v) {
+        PairIn q;
         const uint32_t v2 = 2u * v;
-        const uint32_t c = v2 + rg.off0 + (v2 >= rg.split ? rg.off1 : 0u);
+        q.c = v2 + rg.off0 + (v2 >= rg.split ? rg.off1 : 0u);
         int i, j, k;
-        decompose(d, c, i, j, k);
-        const size_t cp = (size_t)c + plane;
-        const double2 pc = ld2(p + cp);
-        const double2 trv = ld2(Tr + c);
-        const double2 ttl = ld2(Tt + c);
-        const double2 tpl = ld2(Tp + c);
-        const double2 tph = ld2(Tp + c + plane);
-        const double2 pkm = ld2(p + cp - plane);
-        const double2 pkp = ld2(p + cp + plane);
-        const double2 dv = ld2(D + c);
-        const bool jlo = j > 0, jhi = j < nt - 1, ilo = i > 0, ihi = i + 2 < nr;
-        double2 ptm = make_double2(0.0, 0.0), ptp = ptm, tth = ptm;
-        if (jlo) ptm = ld2(p + cp - nr);
-        if (jhi) {
-            ptp = ld2(p + cp + nr);
-            tth = ld2(Tt + c + nr);
+        decompose(d, q.c, i, j, k);
+        const size_t cp = (size_t)q.c + plane;
+        q.pc = ld2(p + cp);
+        q.trv = ld2(Tr + q.c);
+        q.ttl = ld2(Tt + q.c);
+        q.tpl = ld2(Tp + q.c);
+        q.tph = ld2(Tp + q.c + plane);
+        q.pkm = ld2(p + cp - plane);
+        q.pkp = ld2(p + cp + plane);
+        q.dv = ld2(D + q.c);
+        q.jlo = j > 0, q.jhi = j < nt - 1, q.ilo = i > 0, q.ihi = i + 2 < nr;
+        q.ptm = make_double2(0.0, 0.0), q.ptp = q.ptm, q.tth = q.ptm;
+        if (q.jlo) q.ptm = ld2(p + cp - nr);
+        if (q.jhi) {
+            q.ptp = ld2(p + cp + nr);
+            q.tth = ld2(Tt + q.c + nr);
         }
-        const double pm = ilo ? __ldg(p + cp - 1) : 0.0;
-        const double pp2 = ihi ? __ldg(p + cp + 2) : 0.0;
-        const double tr2 = ihi ? __ldg(Tr + c + 2) : 0.0;
+        q.pm = q.ilo ? __ldg(p + cp - 1) : 0.0;
+        q.pp2 = q.ihi ? __ldg(p + cp + 2) : 0.0;
+        q.tr2 = q.ihi ? __ldg(Tr + q.c + 2) : 0.0;
+        return q;
+    };
+    auto compute = [&](const PairIn &q) {
         // cell i
         double s = 0.0;
-        if (ilo) s = A::acc(s, trv.x, pm);
-        s = A::acc(s, trv.y, pc.y);
-        if (jlo) s = A::acc(s, ttl.x, ptm.x);
-        if (jhi) s = A::acc(s, tth.x, ptp.x);
-        s = A::acc(s, tpl.x, pkm.x);
-        s = A::acc(s, tph.x, pkp.x);
-        const double q0 = A::diag_minus(dv.x, pc.x, s);
+        if (q.ilo) s = A::acc(s, q.trv.x, q.pm);
+        s = A::acc(s, q.trv.y, q.pc.y);
+        if (q.jlo) s = A::acc(s, q.ttl.x, q.ptm.x);
+        if (q.jhi) s = A::acc(s, q.tth.x, q.ptp.x);
+        s = A::acc(s, q.tpl.x, q.pkm.x);
+        s = A::acc(s, q.tph.x, q.pkp.x);
+        const double q0 = A::diag_minus(q.dv.x, q.pc.x, s);
         // cell i+1
         s = 0.0;
-        s = A::acc(s, trv.y, pc.x);
-        if (ihi) s = A::acc(s, tr2, pp2);
-        if (jlo) s = A::acc(s, ttl.y, ptm.y);
-        if (jhi) s = A::acc(s, tth.y, ptp.y);
-        s = A::acc(s, tpl.y, pkm.y);
-        s = A::acc(s, tph.y, pkp.y);
-        const double q1 = A::diag_minus(dv.y, pc.y, s);
-        st2(y + c, q0, q1);
+        s = A::acc(s, q.trv.y, q.pc.x);
+        if (q.ihi) s = A::acc(s, q.tr2, q.pp2);
+        if (q.jlo) s = A::acc(s, q.ttl.y, q.ptm.y);
+        if (q.jhi) s = A::acc(s, q.tth.y, q.ptp.y);
+        s = A::acc(s, q.tpl.y, q.pkm.y);
+        s = A::acc(s, q.tph.y, q.pkp.y);
+        const double q1 = A::diag_minus(q.dv.y, q.pc.y, s);
+        st2(y + q.c, q0, q1);
         if (WITH_DOT) {
-            dot[0].add(pc.x, q0);
-            dot[0].add(pc.y, q1);
+            dot[0].add(q.pc.x, q0);
+            dot[0].add(q.pc.y, q1);
+        }
+    };
+    uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (MV2) {   // two pairs per trip: the second pair's loads are in flight during the first's arithmetic
+        for (; v + stride < npair; v += 2 * stride) {
+            const PairIn a0 = load(v), a1 = load(v + stride);
+            compute(a0);
+            compute(a1);
         }
     }
+    for (; v < npair; v += stride) compute(load(v));
     if (WITH_DOT) {
         Acc<EXACT> out[1];
         if (reduce_last<EXACT, kThreads, 1>(dot, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total,
@@ -871,9 +891,12 @@ void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart par
     if (rg.vend == 0) return;
     const bool vec = use_vec2(d, y);
     const unsigned g = vec ? grid_vec2(rg.vend) : grid_for(rg.vend);
+    // MASPCG_MATVEC2=1: two pairs per trip -- measured slower (5.98 vs 6.07 TB/s live: 64 registers, spills)
+    static const int mv2 = getenv("MASPCG_MATVEC2") ? atoi(getenv("MASPCG_MATVEC2")) : 0;
 #define MV(W, L, E)                                                                             \
     do {                                                                                        \
-        if (vec) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E>, g, st, d, a, y, rg, red_slot0, red_total); \
+        if (vec && mv2) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E, true>, g, st, d, a, y, rg, red_slot0, red_total); \
+        else if (vec) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E, false>, g, st, d, a, y, rg, red_slot0, red_total); \
         else k_matvec_flat<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);     \
     } while (0)
     if (exact) {
