@@ -405,6 +405,9 @@ def main():
     ap.add_argument("--path", type=int, default=0,
                     help="0 auto, 1 three kernels, 2 fused two passes, 3 wave, 4 single reduction (Chronopoulos-Gear)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch of the loop kernels")
+    ap.add_argument("--fuse-halo", type=int, default=2,
+                    help="--comm peer: 1 halo stores in the p-update + wait kernel, 2 + the stencil acquires the "
+                         "flags itself, 0 separate push kernel (MASPCG_OPT_FUSE_HALO)")
     ap.add_argument("--kernel-timing", type=int, default=2,
                     help="CUDA events around the hot kernels in the timed region: 2 sampled (the middle slot of "
                          "every graph chunk), 3 sampled (slot 0), 1 every iteration, 0 none")
@@ -460,6 +463,7 @@ def main():
     S.set_option(maspcg.OPT_TMA, args.tma)
     S.set_option(maspcg.OPT_VEC, args.vec)
     S.set_option(maspcg.OPT_PDL, args.pdl)
+    S.set_option(maspcg.OPT_FUSE_HALO, args.fuse_halo)
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
 

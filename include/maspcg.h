@@ -131,9 +131,14 @@ typedef enum {
                                     even; 0: one cell per thread */
     MASPCG_OPT_TMA = 6,          /* fused path: 1 (default) stage pass A's streams with TMA bulk copies when nr is
                                     even; 0: register-batched loads */
-    MASPCG_OPT_FUSE_HALO = 9,    /* peer communicator, path 1: 1 (default) the p-update kernel stores its boundary
+    MASPCG_OPT_FUSE_HALO = 9,    /* peer communicator, path 1: 1 the p-update kernel stores its boundary
                                     planes straight into the neighbours' halo planes over NVLink and releases their
-                                    flags (compute and exchange in one kernel); 0: a separate push kernel */
+                                    flags (compute and exchange in one kernel), the next stencil waits for the
+                                    neighbours' flags in a 1-thread kernel on the communication stream and runs as an
+                                    interior and a boundary launch; 2 (default): as 1, but every stencil block
+                                    acquires the flags itself and the stencil is one launch (no wait kernel, no
+                                    split; 92.2 vs 95.7 us per iteration on the P = 8 slab of c3, one rank);
+                                    0: a separate push kernel */
     MASPCG_OPT_PATH = 4          /* iteration path: 0 = auto (default, = 1), 1 = three streaming kernels (stencil+p.q,
                                     r-update+Jacobi+dots, deferred x-update+p-update; 128 B/cell), 2 = fused two passes
                                     (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell),

@@ -169,6 +169,9 @@ struct DevArrays {
     // peer communicator, path 1: the loop's Dot2 pairs are pushed to every rank by the last block of the
     // producing kernel (LL words) and combined by the consuming kernel -- no reduction kernel at all
     int p2p_ll, p2p_rank, p2p_nranks;
+    // peer communicator, path 1: the loop's stencil acquires the neighbours' halo flags itself (thread 0
+    // of every block, before any load) instead of a separate wait kernel and an interior/boundary split
+    int peer_wait;
     double *peer_stage[kP2PMaxRanks];   // rank r's P2PArea::stage, mapped into this process
     int gather_ranks;   // > 0: the loop's dot products arrive all-gathered (gather[rank][pairs]) and the
                         // consuming kernel combines them in rank order itself (no combine kernel)

@@ -45,6 +45,21 @@ __device__ __forceinline__ void release_p_halo(const DevArrays &a) {
     st_release_sys64(a.peer_flag_hi, e);
     st_release_sys64(a.peer_flag_lo, e);
 }
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// peer mode, loop stencil: wait until both neighbours have released this iteration's halo planes (stored
+// by their p-updates); every block waits before its first load, so no halo line is cached in L1 early
+__device__ __forceinline__ void acquire_p_halo(const DevArrays &a) {
+    if (threadIdx.x == 0) {
+        const unsigned long long e = *(volatile unsigned long long *)&a.p2p->epoch[P2P_HALO];
+        while (ld_acquire_sys64(&a.p2p->flags[P2P_FROM_LEFT][0]) < e) __nanosleep(32);
+        while (ld_acquire_sys64(&a.p2p->flags[P2P_FROM_RIGHT][0]) < e) __nanosleep(32);
+    }
+    __syncthreads();
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
@@ -207,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_matvec_flat(Dims d, De
                                                                       Range rg, unsigned red_slot0,
                                                                       unsigned red_total) {
     if (LOOP && *(volatile int *)&a.sc->done) return;
+    if (LOOP && a.peer_wait) acquire_p_halo(a);
     using A = Ar<EXACT>;
     const double *__restrict__ p = a.p;
     const double *__restrict__ Tr = a.Tr;
@@ -477,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, De
     pdl_wait();
     pdl_trigger();
     if (LOOP && *(volatile int *)&a.sc->done) return;
+    if (LOOP && a.peer_wait) acquire_p_halo(a);
     using A = Ar<EXACT>;
     const double *__restrict__ p = a.p;
     const double *__restrict__ Tr = a.Tr;

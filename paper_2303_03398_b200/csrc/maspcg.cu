@@ -77,7 +77,8 @@ struct maspcg_ctx {
 
     // options
     int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
-    int fuse_halo = 1;   // peer communicator: halo stores fused into the p-update (MASPCG_OPT_FUSE_HALO)
+    int fuse_halo = 2;   // peer communicator: halo stores fused into the p-update, acquired by the stencil
+                         // (MASPCG_OPT_FUSE_HALO)
     unsigned persist_grid = 0;   // path 5: co-resident grid of the persistent kernel
     // fused two-pass path geometry (fused.cu)
     int fused_bj = 1, fused_njt = 1, fused_blocks = 1;
@@ -406,6 +407,11 @@ maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool lo
                       stencil_blocks(c->d, StencilPart::Full, y), exact_arith(c), st);
         return MASPCG_OK;
     }
+    if (loop && c->a.peer_wait) {   // the stencil acquires the pushed halo planes itself
+        launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
+                      stencil_blocks(c->d, StencilPart::Full, y), exact_arith(c), st);
+        return MASPCG_OK;
+    }
     CK(c, cudaEventRecord(c->ev_p, st));
     CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_p, 0));
     if (tslot >= 0) CK(c, record_timing(c, 5, 0, tslot, c->comm_stream));
@@ -681,9 +687,14 @@ long long kernels_per_iteration(const maspcg_ctx *c) {
     if (use_cg1(c)) return 2 + (c->comm ? 2 : 0);   // update, matvec (+ boundary part, combine on P > 1)
     if (use_fused(c) || use_wave(c)) return 2;
     if (!c->comm) return 3;
-    // update, p-update, stencil interior + boundary; the peer communicator's halo wait and pair all-reduces
-    return 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1 +
-           (c->comm->has_pair_allreduce() ? 3 : 0);
+    // peer communicator, fused: update, p-update, one stencil (halo stores, halo acquire and the Dot2
+    // pair exchanges all inside these three kernels)
+    if (c->a.peer_wait) return 3;
+    // update, p-update, stencil interior + boundary
+    long long k = 2 + (stencil_blocks(c->d, StencilPart::Interior, c->a.q) ? 1 : 0) + 1;
+    if (c->a.p2p_ll) return k + 1;                   // + the halo wait kernel (pairs inside the kernels)
+    if (c->comm->has_pair_allreduce()) return k + 4;   // + halo push and wait, two pair all-reduces
+    return k;                                          // NCCL / loopback: their own launches only
 }
 
 bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
@@ -726,6 +737,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     c->a.peer_p_lo = c->a.peer_p_hi = nullptr;
     c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
     c->a.p2p_ll = 0;
+    c->a.peer_wait = 0;
     // NCCL / loopback all-gathers in the three-kernel loop: the update and p-update kernels combine the
     // gathered Dot2 pairs themselves (no combine kernel between the all-gather and its consumer)
     c->a.gather_ranks = (c->comm && !c->comm->has_pair_allreduce() && !fused && !cg1 && !use_wave(c)) ? c->nranks : 0;
@@ -740,6 +752,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
         c->a.p2p_rank = c->rank;
         c->a.p2p_nranks = c->nranks;
         c->a.gather_ranks = 0;
+        c->a.peer_wait = c->fuse_halo == 2 ? 1 : 0;
     }
     if (cg1) {
         // single-reduction start: u0 = z0 (the padded p of the setup, periodic copies included), p = s = 0,
@@ -1640,7 +1653,7 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             if (v < 0 || v > 1) SET_ERR(c, MASPCG_E_INVALID, "arith must be 0 (oracle-exact) or 1 (fast)");
             c->arith = (int)v;
             break;
-        case MASPCG_OPT_FUSE_HALO: c->fuse_halo = v ? 1 : 0; break;
+        case MASPCG_OPT_FUSE_HALO: c->fuse_halo = v < 0 ? 0 : (v > 2 ? 2 : v); break;
         case MASPCG_OPT_PATH:
             if (v < 0 || v > 5)
                 SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels), 2 (fused), 3 (wave), 4 (single "

@@ -36,12 +36,13 @@ def dev(a):
     return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def solve(M, prob, path, graphs=1, loopback=None):
+def solve(M, prob, path, graphs=1, loopback=None, fuse_halo=1):
     import torch
     S = M.solver_for_problem(prob, loopback=loopback, comm="peer")
     try:
         S.set_option(M.OPT_PATH, path)
         S.set_option(M.OPT_USE_GRAPHS, graphs)
+        S.set_option(M.OPT_FUSE_HALO, fuse_halo)
         x = dev(prob.x0)
         st, info, hist = S.solve(dev(prob.f), x, prob.tol, prob.maxit, raise_on_error=False)
         torch.cuda.current_stream().synchronize()
@@ -50,13 +51,14 @@ def solve(M, prob, path, graphs=1, loopback=None):
         S.close()
 
 
-@pytest.mark.parametrize("path", [1, 4])
+@pytest.mark.parametrize("path,fuse_halo", [(1, 1), (1, 2), (1, 0), (4, 1)])
 @pytest.mark.parametrize("graphs", [1, 0])
-def test_peer_single_rank(M, oracle_mod, path, graphs):
-    """One rank: every halo plane and all-gather goes through the push kernels to itself."""
+def test_peer_single_rank(M, oracle_mod, path, fuse_halo, graphs):
+    """One rank: every halo plane and all-gather goes through the push kernels to itself (fuse_halo 2:
+    the stencil blocks acquire the halo flags themselves)."""
     p = inputs.make_problem("c1")
     o = oracle_mod.solve_problem(p, variant="hs" if path == 1 else "cg1")
-    st, info, hist, x = solve(M, p, path, graphs)
+    st, info, hist, x = solve(M, p, path, graphs, fuse_halo=fuse_halo)
     assert st == 0 and info["iters"] == o["iters"]
     assert np.array_equal(hist, o["hist"]) and np.array_equal(x, o["x"])
 
@@ -86,11 +88,15 @@ def _ipc_worker(rank, world, port, out_dir):
                                                                       k0=k0 or 0, nloc=n))]:
             k0, nloc = inputs.slab_extent(fn(None, None).np, rank, world)
             p = fn(k0, nloc)
-            for path in (1, 4, "1nofuse"):
+            for path in (1, 4, "1nofuse", "1acquire"):
                 S = maspcg.solver_for_problem(p, comm="peer")   # CUDA IPC handles all-gathered over gloo
-                S.set_option(maspcg.OPT_PATH, 1 if path == "1nofuse" else path)
+                S.set_option(maspcg.OPT_PATH, 4 if path == 4 else 1)
+                if path == 1:   # halo stores in the p-update, a wait kernel before a split stencil
+                    S.set_option(maspcg.OPT_FUSE_HALO, 1)
                 if path == "1nofuse":   # the halo push as its own kernel instead of inside the p-update
                     S.set_option(maspcg.OPT_FUSE_HALO, 0)
+                if path == "1acquire":   # the stencil blocks acquire the halo flags (one stencil launch)
+                    S.set_option(maspcg.OPT_FUSE_HALO, 2)
                 x = T(p.x0)
                 st, info, hist = S.solve(T(p.f), x, p.tol, p.maxit)
                 torch.cuda.synchronize()
@@ -130,7 +136,7 @@ def test_peer_processes_ipc(tmp_path, oracle_mod, world):
     res = [np.load(tmp_path / f"ipc{r}.npy", allow_pickle=True).item() for r in range(world)]
     probs = {"c1": inputs.make_problem("c1"), "rand": inputs.random_problem(10, 6, 8, 31, bc_in=0, bc_out=1)}
     for name, p in probs.items():
-        for path in (1, 4, "1nofuse"):
+        for path in (1, 4, "1nofuse", "1acquire"):
             o = oracle_mod.solve_problem(p, variant="cg1" if path == 4 else "hs")
             for r in res:
                 st, it, hist, _ = r[(name, path)]
