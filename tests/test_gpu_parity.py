@@ -429,12 +429,13 @@ def test_nonlinear_conduction_time_loop_exact(torch_cuda, M, oracle_mod):
         To = ox
 
 
-@pytest.mark.parametrize("bc,stages", [((1, 1), 6), ((0, 1), 10), ((0, 0), 3)])
-def test_sts_step_bitwise(torch_cuda, M, oracle_mod, bc, stages):
+@pytest.mark.parametrize("bc,stages,nr", [((1, 1), 6, 12), ((0, 1), 10, 12), ((0, 0), 3, 12), ((1, 0), 5, 11)])
+def test_sts_step_bitwise(torch_cuda, M, oracle_mod, bc, stages, nr):
     """maspcg_sts_step (NEXT-4): RKL2 super-time-steps of V du/dt = b_D - K u equal the oracle's bit for
-    bit; maspcg_sts_dt_limit is a valid forward-Euler bound (dt * lambda_max(V^-1 K) <= 2)."""
+    bit (even nr: the two-cells-per-thread stage kernel; odd nr: one cell per thread);
+    maspcg_sts_dt_limit is a valid forward-Euler bound (dt * lambda_max(V^-1 K) <= 2)."""
     torch = torch_cuda
-    p = inputs.random_problem(12, 7, 8, 600 + stages, bc_in=bc[0], bc_out=bc[1])
+    p = inputs.random_problem(nr, 7, 8, 600 + stages, bc_in=bc[0], bc_out=bc[1])
     S = M.solver_for_problem(p)
     dt = S.sts_dt_limit()
     op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, *bc)
