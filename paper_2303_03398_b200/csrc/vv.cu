@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kVVThreads, 3) k_vv_terms2(VVDims v, VVArrays 
 // The same phase with its 16-byte streams staged by cp.async into shared memory one grid-stride
 // iteration ahead (double-buffered, each thread copying and reading only its own slots, so no block
 // barrier): the HBM latency of an iteration's loads overlaps the previous iteration's arithmetic.
-constexpr int kStg = 11;   // staged streams per pair
+constexpr int kStg = 13;   // staged streams per pair
 __device__ __forceinline__ void cp16(double2 *dst, const double *src) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
@@ -538,6 +538,9 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays 
             cp16(slot(stage, 8), a.Wr + pc);
             cp16(slot(stage, 9), a.Wp + UC(v, kw, j, i0));
             cp16(slot(stage, 10), a.wc + pc);
+            const int jm = j > 0 ? j - 1 : 0;
+            cp16(slot(stage, 11), a.p + PV(v, k, 2, jm, i0));
+            cp16(slot(stage, 12), a.p + PV(v, k, 0, jm, i0));
         }
         cp_commit();
     };
@@ -545,22 +548,26 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays 
     issue(t, 0);
     for (int it = 0; t < npair; t += stride, ++it) {
         const int st = it & 1;
+        const unsigned act = __activemask();
+        __syncwarp(act);   // the neighbouring lanes have finished reading this lane's slots of stage st ^ 1
         issue(t + stride, st ^ 1);
-        cp_wait1();   // this thread's copies of stage st have landed
+        cp_wait1();        // this thread's copies of stage st have landed
+        __syncwarp(act);   // ... and the other lanes' (r2, pm1, tm1 come from the neighbouring lanes' slots)
         int i0, j, k;
         cell_of(v, 2 * t, i0, j, k);
         k -= 1;
-        const int jm = j > 0 ? j - 1 : 0;
         const size_t pc = PC(v, k, j, i0);
         const bool last = (i0 + 2 == nr);
         const double2 R = *slot(st, 0), T = *slot(st, 1), Pp = *slot(st, 2), Tj1 = *slot(st, 3), Pk1 = *slot(st, 4);
         const double2 Rm = *slot(st, 5), Tkm = *slot(st, 6), wt = *slot(st, 7), wr = *slot(st, 8), wp = *slot(st, 9);
-        const double2 wcv = *slot(st, 10);
-        const double2 Pjm = L2(a.p + PV(v, k, 2, jm, i0));
-        const double2 Rjm = L2(a.p + PV(v, k, 0, jm, i0));
-        const double r2 = __ldg(a.p + PV(v, k, 0, j, last ? i0 : i0 + 2));
-        const double pm1 = __ldg(a.p + PV(v, k, 2, j, i0 > 0 ? i0 - 1 : 0));
-        const double tm1 = __ldg(a.p + PV(v, k, 1, j, i0 > 0 ? i0 - 1 : 0));
+        const double2 wcv = *slot(st, 10), Pjm = *slot(st, 11), Rjm = *slot(st, 12);
+        // the r-neighbours of the pair: pair t + 1 (i0 + 2) and pair t - 1 (i0 - 1) of the same row are the
+        // neighbouring lanes' staged pairs (grid-stride trips keep consecutive pairs in consecutive lanes)
+        const int lane = threadIdx.x & 31;
+        const bool up_in = lane < 31 && t + 1 < npair, dn_in = lane > 0;
+        const double r2 = last ? 0.0 : (up_in ? slot(st, 0)[1].x : __ldg(a.p + PV(v, k, 0, j, i0 + 2)));
+        const double pm1 = i0 == 0 ? 0.0 : (dn_in ? slot(st, 2)[-1].y : __ldg(a.p + PV(v, k, 2, j, i0 - 1)));
+        const double tm1 = i0 == 0 ? 0.0 : (dn_in ? slot(st, 1)[-1].y : __ldg(a.p + PV(v, k, 1, j, i0 - 1)));
         const double vr0 = (i0 == 0) ? F.gi(k, 0, j) : R.x;          // v_r on r-face i0 (wall at 0)
         const double vr2 = last ? F.go(k, 0, j) : r2;
         if (k <= v.nloc - 1) {
