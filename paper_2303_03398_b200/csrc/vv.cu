@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays 
 }
 
 template <bool WITH_DOT, bool LOOP, bool EXACT>
-__global__ void __launch_bounds__(kVVThreads, 3) k_vv_rows2(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
+__global__ void __launch_bounds__(kVVThreads, 2) k_vv_rows2(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
                                                          unsigned total) {
     if (LOOP && *(volatile int *)&base.sc->done) return;
     const Geo g{a};
