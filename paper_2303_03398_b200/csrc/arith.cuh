@@ -124,7 +124,7 @@ __device__ __forceinline__ void block_combine(Acc<EXACT> (&v)[N]) {
     __syncthreads();
 }
 
-// Per-block partials -> partials[(2k + {0,1}) * kRedBlocks + slot]; the last-arriving block (atomic
+// Per-block partials -> partials[(2k + {0,1}) * kPartialSlots + slot]; the last-arriving block (atomic
 // ticket) combines all `total` partials in a fixed order and returns true (thread 0 holds out[]).
 template <bool EXACT, int NT, int N>
 __device__ __forceinline__ bool reduce_last(Acc<EXACT> (&v)[N], double *partials, unsigned *ticket, unsigned slot,
@@ -134,8 +134,8 @@ __device__ __forceinline__ bool reduce_last(Acc<EXACT> (&v)[N], double *partials
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            partials[(2 * k) * kRedBlocks + slot] = v[k].p;
-            partials[(2 * k + 1) * kRedBlocks + slot] = v[k].s;
+            partials[(2 * k) * kPartialSlots + slot] = v[k].p;
+            partials[(2 * k + 1) * kPartialSlots + slot] = v[k].s;
         }
         __threadfence();
         am_last = atomicAdd(ticket, 1u) == total - 1;
@@ -148,8 +148,8 @@ __device__ __forceinline__ bool reduce_last(Acc<EXACT> (&v)[N], double *partials
     for (int k = 0; k < N; ++k)
         for (unsigned b = threadIdx.x; b < total; b += NT) {
             Acc<EXACT> o;
-            o.p = __ldcg(partials + (2 * k) * kRedBlocks + b);
-            o.s = __ldcg(partials + (2 * k + 1) * kRedBlocks + b);
+            o.p = __ldcg(partials + (2 * k) * kPartialSlots + b);
+            o.s = __ldcg(partials + (2 * k + 1) * kPartialSlots + b);
             acc[k].add(o);
         }
     block_combine<EXACT, NT, N>(acc);

@@ -25,6 +25,7 @@ enum : int { BC_DIRICHLET = 0, BC_NEUMANN0 = 1 };
 
 constexpr int kMaxChunk = 256;          // PCG iterations per graph launch (upper bound)
 constexpr int kRedBlocks = 1184;        // fixed grid of the streaming kernels (8 x 148)
+constexpr int kPartialSlots = 2048;     // per-block Dot2 partial slots of one reduction (>= every grid that reduces)
 constexpr int kThreads = 256;           // threads per block of the streaming kernels
 constexpr int kMaxRanks = 16;           // all-gather scratch of the Dot2 all-reduce
 
@@ -175,7 +176,7 @@ struct DevArrays {
     double *peer_stage[kP2PMaxRanks];   // rank r's P2PArea::stage, mapped into this process
     int gather_ranks;   // > 0: the loop's dot products arrive all-gathered (gather[rank][pairs]) and the
                         // consuming kernel combines them in rank order itself (no combine kernel)
-    double *partials;   // [8][kRedBlocks]  Dot2 (p, s) partials of up to 4 sums
+    double *partials;   // [8][kPartialSlots]  Dot2 (p, s) partials of up to 4 sums
     double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce
     Scalars *sc;
 };

@@ -64,6 +64,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
 constexpr int kVecBlocks = 4;                   // vector kernels: 4 blocks of 256 threads per SM (<= 64 registers)
+constexpr int kMvBlocks = 5;                    // the vector stencil: 5 blocks per SM (<= 51 registers)
 
 __device__ __forceinline__ void decompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
     uint32_t row = d.div_r.div(c);
@@ -487,7 +488,7 @@ __device__ __forceinline__ void st2(double *p, double a, double b) {
 }
 
 template <bool WITH_DOT, bool LOOP, bool EXACT, bool MV2>
-__global__ void __launch_bounds__(kThreads, kVecBlocks) k_matvec_vec2(Dims d, DevArrays a, double *__restrict__ y,
+__global__ void __launch_bounds__(kThreads, kMvBlocks) k_matvec_vec2(Dims d, DevArrays a, double *__restrict__ y,
                                                                       Range rg, unsigned red_slot0,
                                                                       unsigned red_total) {
     pdl_wait();
@@ -843,6 +844,13 @@ void launch_pdl(bool pdl, void (*kern)(KArgs...), unsigned grid, cudaStream_t st
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+inline unsigned grid_mv2(uint32_t n) {    // the vector stencil: n cells, two per thread
+    uint64_t g = (n / 2 + kThreads - 1) / kThreads;
+    if (g < 1) g = 1;
+    if (g > (uint64_t)(148 * kMvBlocks)) g = 148 * kMvBlocks;
+    return (unsigned)g;
+}
+
 inline unsigned grid_vec2(uint32_t n) {   // n cells, two per thread
     uint64_t g = (n / 2 + kThreads - 1) / kThreads;
     if (g < 1) g = 1;
@@ -899,7 +907,7 @@ static Range make_range(const Dims &d, StencilPart part) {
 unsigned stencil_blocks(const Dims &d, StencilPart part, const double *y) {
     Range rg = make_range(d, part);
     if (!rg.vend) return 0u;
-    return use_vec2(d, y) ? grid_vec2(rg.vend) : grid_for(rg.vend);
+    return use_vec2(d, y) ? grid_mv2(rg.vend) : grid_for(rg.vend);
 }
 
 void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart part, bool with_dot, bool loop,
@@ -907,7 +915,7 @@ void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart par
     Range rg = make_range(d, part);
     if (rg.vend == 0) return;
     const bool vec = use_vec2(d, y);
-    const unsigned g = vec ? grid_vec2(rg.vend) : grid_for(rg.vend);
+    const unsigned g = vec ? grid_mv2(rg.vend) : grid_for(rg.vend);
     // MASPCG_MATVEC2=1: two pairs per trip -- measured slower (5.98 vs 6.07 TB/s live: 64 registers, spills)
     static const int mv2 = getenv("MASPCG_MATVEC2") ? atoi(getenv("MASPCG_MATVEC2")) : 0;
 #define MV(W, L, E)                                                                             \

@@ -142,7 +142,7 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     };
     DevArrays t{};
     t.sc = (Scalars *)take(sizeof(Scalars));
-    t.partials = (double *)take(sizeof(double) * 8 * kRedBlocks);
+    t.partials = (double *)take(sizeof(double) * 8 * kPartialSlots);
     t.p2p = (P2PArea *)take(sizeof(P2PArea));
     t.gather = (double *)take(sizeof(double) * 8 * kMaxRanks);
     t.P[0] = (double *)take(8 * n);
@@ -1189,7 +1189,7 @@ maspcg_status maspcg_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
     c->ws_bytes = bytes;
     layout(c, (char *)dev_ptr, &c->a);
     CK(c, cudaMemset(c->a.sc, 0, sizeof(Scalars)));
-    CK(c, cudaMemset(c->a.partials, 0, sizeof(double) * 8 * kRedBlocks));
+    CK(c, cudaMemset(c->a.partials, 0, sizeof(double) * 8 * kPartialSlots));
     CK(c, cudaDeviceSynchronize());
     RET_IF(peer_register(c, 0, (char *)dev_ptr, need));
     c->metric_dirty = true;
