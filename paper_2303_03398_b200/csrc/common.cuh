@@ -25,7 +25,8 @@ enum : int { BC_DIRICHLET = 0, BC_NEUMANN0 = 1 };
 
 constexpr int kMaxChunk = 256;          // PCG iterations per graph launch (upper bound)
 constexpr int kRedBlocks = 1184;        // fixed grid of the streaming kernels (8 x 148)
-constexpr int kPartialSlots = 2048;     // per-block Dot2 partial slots of one reduction (>= every grid that reduces)
+constexpr int kPartialSlots = 2560;     // per-block Dot2 partial slots of one reduction: >= the interior +
+                                        // boundary stencil grids together (2 x kRedBlocks for the scalar kernels)
 constexpr int kThreads = 256;           // threads per block of the streaming kernels
 constexpr int kMaxRanks = 16;           // all-gather scratch of the Dot2 all-reduce
 

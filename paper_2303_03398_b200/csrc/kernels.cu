@@ -65,6 +65,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
 constexpr int kVecBlocks = 4;                   // vector kernels: 4 blocks of 256 threads per SM (<= 64 registers)
 constexpr int kMvBlocks = 5;                    // the vector stencil: 5 blocks per SM (<= 51 registers)
+static_assert(kPartialSlots >= 2 * kRedBlocks && kPartialSlots >= 2 * 148 * kMvBlocks,
+              "a split stencil (interior + boundary launches) must fit the Dot2 partial slots");
 
 __device__ __forceinline__ void decompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
     uint32_t row = d.div_r.div(c);

@@ -116,6 +116,20 @@ def test_multirank_solve_matches_oracle(M, oracle_mod, name, P, fn, path):
         assert np.array_equal(Tp, op.Tp[sl]) and np.array_equal(D, op.D[sl])
 
 
+@pytest.mark.parametrize("nr", [63, 64])
+def test_multirank_large_slab_split_reduction(M, oracle_mod, nr):
+    """A slab whose interior and boundary stencil launches together have more blocks than one launch may
+    (odd nr, one cell per thread: 1,184 + 32 blocks; even nr: the 16-byte pair kernels): the p.q partial
+    slots of both launches must not overlap.  Five iterations, bit for bit against the oracle."""
+    fn = lambda k0, n: inputs.random_problem(nr, 64, 160, 41, k0=k0 or 0, nloc=n)
+    full = fn(None, None)
+    o = oracle_mod.solve_problem(full, tol=0.0, maxit=5)
+    res = run_ranks(M, 2, lambda r, g: solve_rank(M, slab_of(fn, 2, r), r, g, tol=0.0, maxit=5, path=1))
+    for st, info, hist, _, _ in res:
+        assert info["iters"] == 5 and np.array_equal(hist, o["hist"])
+    assert np.array_equal(np.concatenate([r[3] for r in res], axis=0), o["x"])
+
+
 @pytest.mark.parametrize("P", [2, 4])
 def test_multirank_apply(M, oracle_mod, P):
     import torch
