@@ -1170,17 +1170,13 @@ bool launch_fused(const VVDims &v, const VVArrays &a, const DevArrays &base, dou
     const int njt = (v.nt + tj - 1) / tj;
     if (njt > kRedBlocks) return false;
     const size_t sm = fused_smem(v.nr, tj);
-    static int cached_nr = -1, cached_tj = -1, per_sm = 0, sms = 0;
-    if (cached_nr != v.nr || cached_tj != tj) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_vv_fused<W, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vv_fused<W, L, E>, kVVThreads, sm);
-        if (per_sm < 1) per_sm = 1;
-        cached_nr = v.nr;
-        cached_tj = tj;
-    }
+    // queried at every launch (host-side only; no shared state between contexts of different shapes)
+    int dev = 0, per_sm = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_vv_fused<W, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vv_fused<W, L, E>, kVVThreads, sm);
+    if (per_sm < 1) per_sm = 1;
     int target = sms * per_sm;
     if (target > kRedBlocks) target = kRedBlocks;
     int nkc = target / njt;   // one resident wave: a partial second wave would double the time
