@@ -1174,7 +1174,7 @@ bool launch_fused(const VVDims &v, const VVArrays &a, const DevArrays &base, dou
     int dev = 0, per_sm = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_vv_fused<W, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_vv_fused<W, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);   // the cap
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vv_fused<W, L, E>, kVVThreads, sm);
     if (per_sm < 1) per_sm = 1;
     int target = sms * per_sm;
