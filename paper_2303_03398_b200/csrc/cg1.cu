@@ -27,7 +27,7 @@ namespace maspcg {
 namespace {
 
 constexpr int kCgBlocks = 4;      // matvec: resident 256-thread blocks per SM (<= 64 registers)
-constexpr int kCgUpdBlocks = 3;   // update: 3 per SM (<= 85 registers: no spills in the pair loop)
+constexpr int kCgUpdBlocks = 2;   // update: 2 per SM (1,694-1,698 vs 1,646-1,667 it/s at 3 and 1,557-1,561 at 4)
 
 __device__ __forceinline__ void pdl_wait_cg() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger_cg() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
