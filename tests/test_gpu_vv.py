@@ -106,6 +106,24 @@ def test_vv_coronal_solve_exact(M, oracle_mod, name, shape):
     assert np.array_equal(hist, o["hist"]) and np.array_equal(x, o["x"])
 
 
+@pytest.mark.timeout(600, method="thread")
+def test_vv_c3v_full_size_operator_bitwise(M, oracle_mod):
+    """The bench workload of `bench.py --operator vv` (c3v: 150 x 300 x 600 cells, 81 M unknowns): the
+    Jacobi diagonal and y = A x of the device operator equal the oracle's on every entry."""
+    import torch
+    p = inputs.make_vv_problem("c3v")
+    op = oracle_op(oracle_mod, p)
+    S = gpu_solver(M, p)
+    try:
+        assert np.array_equal(S.vv_get_diag(), op.D)
+        x = np.stack([inputs.white_noise(7 + c, p.nr, p.nt, 0, p.np) for c in range(3)], axis=1)
+        y = S.vv_apply(dev(x))
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), op.apply(x))
+    finally:
+        S.close()
+
+
 @pytest.mark.parametrize("tj", [1, 3, 6])
 @pytest.mark.parametrize("shape,walls", [((8, 4, 2), (0, 1)), ((16, 16, 32), (1, 0)), ((20, 30, 48), (0, 1))])
 def test_vv_fused_operator_exact(M, oracle_mod, monkeypatch, tj, shape, walls):
