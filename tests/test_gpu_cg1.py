@@ -101,6 +101,14 @@ def test_cg1_c3_half_resolution_exact(M, oracle_mod):
     assert_same(gpu_cg1(M, p), oracle_mod.solve_problem(p, variant="cg1"))
 
 
+def test_cg1_c3_full_size_exact(M, oracle_mod):
+    """The full c3 grid (27 M cells) in the bench's launch configuration (graphs, chunk 16): 12 fixed
+    iterations of the single-reduction path identical to the oracle's variant."""
+    p = inputs.make_problem("c3")
+    o = oracle_mod.solve_problem(p, tol=0.0, maxit=12, variant="cg1")
+    assert_same(gpu_cg1(M, p, tol=0.0, maxit=12), o)
+
+
 # ------------------------------------------------------------------ multi-rank (loopback, one GPU)
 def run_ranks(M, P, fn):
     import torch
