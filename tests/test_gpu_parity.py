@@ -457,3 +457,22 @@ def test_sts_step_bitwise(torch_cuda, M, oracle_mod, bc, stages, nr):
         uo = op.rkl2_step(uo, p.s, tau, stages, p.g_in, p.g_out)
     torch.cuda.synchronize()
     assert np.array_equal(ug.cpu().numpy(), uo)
+
+
+@pytest.mark.timeout(600, method="thread")
+def test_sts_c3_full_size_bitwise(torch_cuda, M, oracle_mod):
+    """`bench.py --sts-stages` workload: one 10-stage RKL2 step on the full c3 grid (27 M cells, the
+    two-plane halo copies and the Dirichlet inner boundary included) equals the oracle's bit for bit."""
+    torch = torch_cuda
+    p = inputs.make_problem("c3")
+    S = M.solver_for_problem(p)
+    dt = S.sts_dt_limit()
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, p.bc_in, p.bc_out)
+    tau = 0.9 * (10 * 10 + 10 - 2) / 4.0 * dt
+    u0 = np.random.default_rng(10).standard_normal(op.shape)
+    ug = dev(torch, u0)
+    S.sts_step(ug, tau, 10)
+    torch.cuda.synchronize()
+    uo = op.rkl2_step(u0, p.s, tau, 10, p.g_in, p.g_out)
+    assert np.array_equal(ug.cpu().numpy(), uo)
+    S.close()
