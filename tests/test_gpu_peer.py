@@ -180,3 +180,13 @@ def test_peer_single_rank_vv_and_group_rejected(M, oracle_mod):
         M.Solver(4, 4, 8, inputs.rfaces(4, 1, 2, 0), inputs.tfaces(4, 0.0), inputs.pfaces(8), loopback=(g, 0),
                  comm="peer")
     g.close()
+
+
+def test_peer_single_rank_c3_full_size(M, oracle_mod):
+    """The full c3 grid through the peer communicator with one rank (halo stores into its own halos by
+    the p-update, the stencil acquiring them, LL pair words to itself): 20 iterations bit for bit."""
+    p = inputs.make_problem("c3")
+    o = oracle_mod.solve_problem(p, tol=0.0, maxit=20)
+    p.tol, p.maxit = 0.0, 20
+    st, info, hist, x = solve(M, p, 1, 1, fuse_halo=2)
+    assert info["iters"] == 20 and np.array_equal(hist, o["hist"]) and np.array_equal(x, o["x"])
