@@ -97,6 +97,66 @@ PATHS = {
 }
 
 
+# BASELINE.json configs[i] of each workload name
+CONFIG_INFO = {
+    "c1": ("configs[0]", "tiny spherical shell, uniform grid, constant coefficient"),
+    "c2": ("configs[1]", "nonuniform stretched grid, radially varying thermal-conduction coefficient"),
+    "c3": ("configs[2]", "coronal-relaxation-shaped viscosity solve"),
+    "c4": ("configs[3]", "weak-scaling per-GPU slab, high-contrast thermal-conduction coefficients"),
+    "c5": ("configs[4]", "repeated warm-started implicit solves of a time loop (paper-sized grid)"),
+}
+
+
+def workload(cfg, nr, nt, np_, tol, maxit, shape):
+    idx, desc = CONFIG_INFO.get(cfg, ("-", cfg))
+    w = f"{cfg} {nr}x{nt}x{np_} {desc} (BASELINE.json {idx})"
+    if shape:
+        w += " [grid overridden by --shape]"
+    return w + (f", tol={tol:g}" if tol > 0 else f", tol=0 maxit={maxit}") + ", Jacobi-PCG fp64"
+
+
+def make_config(args, nr, nt, np_, tol, maxit, shape, world, par_note=""):
+    """The workload description, identical for both arms (ours and --impl reference)."""
+    ws = 80 * nr * nt * np_ / max(world, 1)   # Tr, Tt, Tp, D, sV, p, q, r, x, rhs per rank (~10 doubles/cell)
+    l2 = (f"no flush: the per-GPU working set ({ws / 1e6:.0f} MB) exceeds the 126 MB L2 between steps"
+          if ws > 126e6 else
+          f"no flush: the per-GPU working set ({ws / 1e6:.1f} MB) is L2-resident (no HBM roofline claim)")
+    return {"workload": workload(args.config, nr, nt, np_, tol, maxit, shape), "global_cells": nr * nt * np_,
+            "parallelism": f"phi-slab x{world}" + par_note, "l2": l2}
+
+
+def step_stats(ms_list):
+    a = np.asarray(ms_list, dtype=np.float64)
+    if a.size == 0:
+        return None
+    return {"min": float(a.min()), "median": float(np.median(a)), "mean": float(a.mean()), "max": float(a.max())}
+
+
+def host_cpu_info():
+    """lscpu model / sockets / cores and this process's CPU affinity (the cores the oracle may use)."""
+    info = {"affinity_cpus": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=20).stdout
+        kv = {}
+        for ln in out.splitlines():
+            if ":" in ln:
+                k, v = ln.split(":", 1)
+                kv[k.strip()] = v.strip()
+        sockets = int(kv.get("Socket(s)", "0") or 0)
+        cps = int(kv.get("Core(s) per socket", "0") or 0)
+        info.update({"model": kv.get("Model name"), "sockets": sockets, "cores_per_socket": cps,
+                     "threads_per_core": int(kv.get("Thread(s) per core", "0") or 0),
+                     "logical_cpus": int(kv.get("CPU(s)", "0") or 0), "physical_cores": sockets * cps or None})
+    except Exception as e:   # lscpu missing: affinity only
+        info["lscpu_error"] = str(e)
+    return info
+
+
+def omp_threads(info):
+    phys = info.get("physical_cores") or info["affinity_cpus"]
+    return max(1, min(phys, info["affinity_cpus"]))
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -167,10 +227,12 @@ def ncu_traffic_per_launch(path_id: int):
         return None, None
 
 
-def oracle_sample(prob, iters: int):
-    """Time the CPU oracle (as it stands, single-threaded) on the full c3 grid: setup once, then
-    `iters` PCG iterations (tol = 0).  Returns (iterations/s, seconds of CPU work, description)."""
+def oracle_sample(prob, iters: int, openmp: bool = False):
+    """Time the CPU oracle (as it stands; single-threaded, or its -fopenmp build on all host cores) on
+    the full grid: setup once, then `iters` PCG iterations (tol = 0).  Returns (iterations/s, seconds of
+    CPU work, seconds per iteration)."""
     import oracle
+    oracle.use_openmp(openmp)
     t0 = time.perf_counter()
     op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
     b = op.rhs(prob.f, prob.g_in, prob.g_out)
@@ -179,8 +241,27 @@ def oracle_sample(prob, iters: int):
     t2 = time.perf_counter()
     op.pcg(b, prob.x0, 0.0, iters)
     t3 = time.perf_counter()
+    oracle.use_openmp(False)
     per_iter = ((t3 - t2) - (t2 - t1)) / iters
     return 1.0 / per_iter, t3 - t0, per_iter
+
+
+def cpu_baseline_block(prob, cfg, iters1: int, iters_all: int):
+    """cpu_baseline: the oracle on all physical host cores (-fopenmp build of the same source:
+    per-cell loops threaded, dot products sequential) and single-threaded, on a bounded sample."""
+    info = host_cpu_info()
+    nth = omp_threads(info)
+    os.environ["OMP_NUM_THREADS"] = str(nth)   # read when the -fopenmp library initialises
+    ips1, s1, per1 = oracle_sample(prob, iters1, openmp=False)
+    ipsn, sn, pern = oracle_sample(prob, iters_all, openmp=True)
+    return {"value": ipsn, "unit": UNIT, "cores": nth, "kind": "oracle",
+            "sample": f"oracle/masoracle.c built with -fopenmp, OMP_NUM_THREADS={nth} (physical cores in this "
+                      f"process's affinity), on the full {cfg} grid: operator assembly + rhs + r0 once, then "
+                      f"{iters_all} PCG iterations (tol=0); {sn:.1f} s of CPU work, {pern * 1e3:.0f} ms/iteration",
+            "single_thread": {"value": ips1, "cores": 1,
+                              "sample": f"plain build, 1 thread, {iters1} PCG iterations; {s1:.1f} s of CPU work, "
+                                        f"{per1 * 1e3:.0f} ms/iteration"},
+            "host": info}
 
 
 VV_BYTES = {"matvec": 104, "update": 96, "pupdate": 144, "iter": 344}   # algorithmic B/cell (DESIGN.md 7)
@@ -240,26 +321,35 @@ def run_vv(args):
 
     for _ in range(args.warmup):
         step()
+    if warm:   # the timed steps are the time loop from its start: step 0 cold, steps 1.. warm-started
+        x.copy_(x0)
+        nstep[0] = 0
     S.set_option(maspcg.OPT_TIMING, args.kernel_timing)
     S.reset_stats()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = 0
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    iters, step_iters = 0, []
     with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            iters += step()
-        ev1.record(stream)
+        evs[0].record(stream)
+        for k in range(args.steps):
+            it = step()
+            iters += it
+            step_iters.append(it)
+            evs[k + 1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
+    ms = evs[0].elapsed_time(evs[-1])
+    step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     stats = S.stats()
     S.set_option(maspcg.OPT_TIMING, 0)
     if world > 1:
         ms = max_over_ranks(ms, dev)
+        t = torch.tensor(step_ms, dtype=torch.float64, device="cpu" if SHARED_GPU else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = t.cpu().tolist()
     sec = ms / 1e3
     value = iters / sec
     ncl = prob.nloc * nt * nr
@@ -338,43 +428,85 @@ def run_vv(args):
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands on the box's host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle as it stands on the box's host cores (rank 0 only; other ranks
+    exit without work).  Same metric, unit and config as our arm; each step is a bounded sample of that
+    workload: PCG iterations (tol = 0) of the oracle's -fopenmp build on all physical cores, on the
+    full grid, with the operator assembled once before timing."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
     from paper_2303_03398_b200 import inputs
+    info = host_cpu_info()
+    nth = omp_threads(info)
+    os.environ["OMP_NUM_THREADS"] = str(nth)
     oracle.build()
-    prob = inputs.make_problem(args.config)
+    oracle.build(openmp=True)
+    oracle.use_openmp(True)
+    shape = tuple(int(v) for v in args.shape.split(",")) if args.shape else None
+    prob = inputs.make_problem(args.config, shape=shape)
+    tol = 0.0 if args.maxit else prob.tol
+    maxit = args.maxit if args.maxit else prob.maxit
     op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
     b = op.rhs(prob.f, prob.g_in, prob.g_out)
     m = args.ref_iters
     for _ in range(args.warmup):
         op.pcg(b, prob.x0, 0.0, 1)
+    per_step, t_setup_all = [], 0.0
     t0 = time.perf_counter()
-    t_setup = 0.0
     for _ in range(args.steps):
         ts = time.perf_counter()
-        op.pcg(b, prob.x0, 0.0, 0)
-        t_setup += time.perf_counter() - ts
+        op.pcg(b, prob.x0, 0.0, 0)          # the r0 = b - A x0 setup alone (removed below)
+        t_setup = time.perf_counter() - ts
         op.pcg(b, prob.x0, 0.0, m)
+        te = time.perf_counter()
+        per_step.append(1e3 * (te - ts - 2 * t_setup))
+        t_setup_all += t_setup
     dt = time.perf_counter() - t0
     # each pcg(m) call repeats the r0 = b - A x0 setup, timed separately and removed
-    value = args.steps * m / (dt - 2 * t_setup) if dt > 2 * t_setup else args.steps * m / dt
-    cores = 1
+    value = args.steps * m / (dt - 2 * t_setup_all) if dt > 2 * t_setup_all else args.steps * m / dt
+    oracle.use_openmp(False)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded generators, paper_2303_03398_b200/inputs.py)",
-        "config": {"workload": f"{args.config} {prob.nr}x{prob.nt}x{prob.np} coronal viscosity solve (BASELINE.json configs[2])",
-                   "global_cells": prob.ncell_global, "parallelism": "none (CPU oracle, 1 thread)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"oracle/masoracle.c PCG on the full c3 grid, {m} iterations per step "
-                                   f"(tol=0), operator assembled once before timing"},
+        "data": "synthetic (seeded generators, paper_2303_03398_b200/inputs.py; SURVEY 8(d) recipe)",
+        "config": make_config(args, prob.nr, prob.nt, prob.np, tol, maxit, shape, 1),
+        "step_ms": step_stats(per_step),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "oracle",
+                         "sample": f"oracle/masoracle.c built with -fopenmp (per-cell loops threaded, dot products "
+                                   f"sequential), OMP_NUM_THREADS={nth}, PCG on the full {args.config} grid: {m} "
+                                   f"iterations (tol=0) per step, operator assembled once before timing",
+                         "host": info},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
+
+
+def self_launch(args) -> bool:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: launch the N ranks ourselves with
+    torch.distributed.run on 127.0.0.1 (rank 0's stdout is ours, so its JSON line is the only output).
+    Refuses (exit 2) when fewer than N GPUs are visible instead of silently running one rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    if not SHARED_GPU:
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but {n} CUDA device(s) visible; refusing to run fewer ranks",
+                  file=sys.stderr)
+            sys.exit(2)
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # NCCL's init lines (rank count, transports) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr)
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def main():
@@ -411,6 +543,9 @@ def main():
     ap.add_argument("--kernel-timing", type=int, default=2,
                     help="CUDA events around the hot kernels in the timed region: 2 sampled (the middle slot of "
                          "every graph chunk), 3 sampled (slot 0), 1 every iteration, 0 none")
+    ap.add_argument("--l2-keep", type=int, default=1,
+                    help="1 (default): L2 residency of the loop's most-reused arrays when the slab is small "
+                         "(MASPCG_OPT_L2_KEEP auto); 0: off")
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=0, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
@@ -418,6 +553,7 @@ def main():
                     help="scalar: the 7-point parabolic solve (default); vv: the staggered vector viscosity "
                          "(NEXT-2) on the c3 grid (config c3v)")
     args = ap.parse_args()
+    self_launch(args)
     protect_stdout()
     if args.warmup < 3 and args.maxit is None:
         args.warmup = 3
@@ -433,7 +569,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world != args.gpus:
-        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     local = init_dist(world)
     dev = torch.device(f"cuda:{local}")
 
@@ -464,6 +601,7 @@ def main():
     S.set_option(maspcg.OPT_VEC, args.vec)
     S.set_option(maspcg.OPT_PDL, args.pdl)
     S.set_option(maspcg.OPT_FUSE_HALO, args.fuse_halo)
+    S.set_option(maspcg.OPT_L2_KEEP, args.l2_keep)
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
 
@@ -495,26 +633,35 @@ def main():
 
     for _ in range(args.warmup):
         step()
+    if warm:   # the timed steps are the time loop from its start: step 0 cold, steps 1.. warm-started
+        x.copy_(x0)
+        nstep[0] = 0
     S.set_option(maspcg.OPT_TIMING, args.kernel_timing)
     S.reset_stats()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = 0
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    iters, step_iters = 0, []
     with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            iters += step()
-        ev1.record(stream)
+        evs[0].record(stream)
+        for k in range(args.steps):
+            it = step()
+            iters += it
+            step_iters.append(it)
+            evs[k + 1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = ev0.elapsed_time(ev1)
+    ms = evs[0].elapsed_time(evs[-1])
+    step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     stats = S.stats()
     S.set_option(maspcg.OPT_TIMING, 0)
     if world > 1:
         ms = max_over_ranks(ms, dev)
+        t = torch.tensor(step_ms, dtype=torch.float64, device="cpu" if SHARED_GPU else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = t.cpu().tolist()
     sec = ms / 1e3
     value = iters / sec                                 # global solve iterations (strong scaling)
     ncell_local = prob.ncell_local
@@ -614,30 +761,28 @@ def main():
     # ---- CPU baseline: the oracle as it stands on this box's host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ips, cpu_s, per_it = oracle_sample(inputs.make_problem(args.config, shape=shape), args.ref_iters)
-        cpu = {"value": ips, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle/masoracle.c (single-threaded C, -O2) on the full {args.config} grid: operator "
-                         f"assembly + rhs + r0 once, then {args.ref_iters} PCG iterations (tol=0); "
-                         f"{cpu_s:.1f} s of CPU work, {per_it * 1e3:.0f} ms/iteration"}
+        cpu = cpu_baseline_block(inputs.make_problem(args.config, shape=shape), args.config, args.ref_iters,
+                                 4 * args.ref_iters)
 
     if rank == 0:
+        par_note = ((" (one-rank peer-memory communicator)" if use_peer else " (one-rank NCCL communicator)")
+                    if args.force_comm else (" peer-memory communicator" if use_peer else ""))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if (args.config == "c4" and not shape) else "strong", "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic (seeded generators, paper_2303_03398_b200/inputs.py; SURVEY 8(d) recipe)",
-            "config": {"workload": f"{args.config} {nr}x{nt}x{np_} coronal viscosity solve "
-                                   f"(BASELINE.json configs[2]), tol={tol:g}, Jacobi-PCG fp64",
-                       "global_cells": nr * nt * np_,
-                       "parallelism": f"phi-slab x{world}" + (
-                           (" (one-rank peer-memory communicator)" if use_peer else " (one-rank NCCL communicator)")
-                           if args.force_comm else (" peer-memory communicator" if use_peer else "")),
-                       "iters_per_solve": iters / args.steps, "chunk": args.chunk,
-                       "l2": "no flush: working set ~2.2 GB >> 126 MB L2",
-                       "step": ("set_grid + set_coefficients_from_fields(rho; kappa = 1e-3 rho, s = rho/1e-2) + "
-                                "set_bc_r + solve to tol") if args.from_fields else
-                               "set_grid + set_coefficients + set_bc_r + solve to tol",
-                       "arith": "oracle-identical (no FMA, Dot2 dots)" if args.arith == 0 else "fast (FMA, plain sums)"},
+            "config": make_config(args, nr, nt, np_, tol, maxit, shape, world, par_note),
+            "run": {"iters_per_solve": iters / args.steps, "chunk": args.chunk,
+                    "step": ("set_grid + set_coefficients_from_fields(rho; kappa = 1e-3 rho, s = rho/1e-2) + "
+                             "set_bc_r + solve to tol") if args.from_fields else
+                            "set_grid + set_coefficients + set_bc_r + solve to tol",
+                    "arith": "oracle-identical (no FMA, Dot2 dots)" if args.arith == 0 else "fast (FMA, plain sums)",
+                    "l2_keep": "auto (MASPCG_OPT_L2_KEEP)" if args.l2_keep else "off"},
+            "step_ms": step_stats(step_ms),
+            "per_step": [{"iters": int(i), "ms": float(m)} for i, m in zip(step_iters, step_ms)]
+            if args.steps <= 64 else None,
             "cell_updates_per_s": nr * nt * np_ * value,
             "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "sts": sts,
             "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),

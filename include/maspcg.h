@@ -139,7 +139,15 @@ typedef enum {
                                     acquires the flags itself and the stencil is one launch (no wait kernel, no
                                     split; 92.2 vs 95.7 us per iteration on the P = 8 slab of c3, one rank);
                                     0: a separate push kernel */
-    MASPCG_OPT_PATH = 4          /* iteration path: 0 = auto (default, = 1), 1 = three streaming kernels (stencil+p.q,
+    MASPCG_OPT_L2_KEEP = 10,     /* three-kernel path (nr even): L2 residency of the loop's arrays.  1 (default,
+                                    auto): when the local slab is small enough (P = 4, 8 of c3), the arrays with the
+                                    most accesses per iteration and byte -- D (3 reads), p and r (3 accesses each),
+                                    then x, q and the face coefficients -- are loaded and stored with an L2
+                                    evict_last policy, greedily up to 3/4 of the L2 (the last one partially, by a
+                                    fractional policy); their lines are returned to the normal priority after the
+                                    solve.  The "super" scaling of PAPER.md:277 (§V-C).  0: plain loads and stores.
+                                    Arithmetic and results are unaffected. */
+    MASPCG_OPT_PATH = 4         /* iteration path: 0 = auto (default, = 1), 1 = three streaming kernels (stencil+p.q,
                                     r-update+Jacobi+dots, deferred x-update+p-update; 128 B/cell), 2 = fused two passes
                                     (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell),
                                     3 = wave (single rank): r-update, then the p-update of iteration k and the stencil

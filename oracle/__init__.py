@@ -20,6 +20,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "masoracle.c")
 SRC_VV = os.path.join(HERE, "masoracle_vv.c")   # staggered vector viscosity
 LIB = os.path.join(HERE, "libmasoracle.so")
+# The same sources built with -fopenmp: the per-cell loops of apply and of the PCG vector updates run on
+# all host cores (identical values; dot products stay sequential).  Used only to time the oracle as a
+# CPU baseline on the GPU box (bench.py cpu_baseline, --impl reference), never as a checker.
+LIB_OMP = os.path.join(HERE, "libmasoracle_omp.so")
 
 OK, NOT_CONVERGED, E_INVALID, E_SINGULAR, E_BREAKDOWN, E_NOMEM = 0, 1, -1, -3, -4, -7
 BC_DIRICHLET, BC_NEUMANN0 = 0, 1
@@ -27,23 +31,33 @@ BC_DIRICHLET, BC_NEUMANN0 = 0, 1
 CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared", "-std=c99"]
 
 
-def build(force: bool = False) -> str:
-    """Compile libmasoracle.so with gcc (plain C99, no contraction, no fast-math)."""
-    newest = max(os.path.getmtime(SRC), os.path.getmtime(SRC_VV))
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        tmp = LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, SRC, SRC_VV, "-lm"])
-        os.replace(tmp, LIB)
-    return LIB
+def build(force: bool = False, openmp: bool = False) -> str:
+    """Compile libmasoracle.so with gcc (plain C99, no contraction, no fast-math); openmp: the
+    -fopenmp timing build libmasoracle_omp.so of the same sources."""
+    out = LIB_OMP if openmp else LIB
+    newest = max(os.path.getmtime(SRC), os.path.getmtime(SRC_VV), os.path.getmtime(__file__))
+    if force or not os.path.exists(out) or os.path.getmtime(out) < newest:
+        tmp = out + f".tmp{os.getpid()}"
+        extra = ["-fopenmp"] if openmp else []
+        subprocess.check_call(["gcc", *CFLAGS, *extra, "-o", tmp, SRC, SRC_VV, "-lm"])
+        os.replace(tmp, out)
+    return out
 
 
-_lib = None
+_libs = {}
+_openmp = False
+
+
+def use_openmp(on: bool) -> None:
+    """Select the -fopenmp build for the following calls (bench.py's CPU timings only)."""
+    global _openmp
+    _openmp = bool(on)
 
 
 def lib():
-    global _lib
-    if _lib is None:
-        _lib = ctypes.CDLL(build())
+    key = _openmp
+    if key not in _libs:
+        _lib = ctypes.CDLL(build(openmp=key))
         d, i = ctypes.c_void_p, ctypes.c_int
         for name, args in {
             "masoracle_check_grid": [i, i, i, d, d, d],
@@ -68,7 +82,8 @@ def lib():
             fn = getattr(_lib, name)
             fn.argtypes = args
             fn.restype = i
-    return _lib
+        _libs[key] = _lib
+    return _libs[key]
 
 
 def _p(a):

@@ -311,6 +311,9 @@ int masoracle_face_coefficients(int nr, int nt, int np, const double *field, dou
  * theta-boundary faces carry no flux; phi wraps periodically (R9).          */
 int masoracle_apply(int nr, int nt, int np, const double *Tr, const double *Tt,
                     const double *Tp, const double *D, const double *u, double *y) {
+    /* each y[c] is computed independently; the pragma (the -fopenmp timing build of bench.py's
+     * cpu_baseline only) splits the planes across threads without changing any value */
+#pragma omp parallel for schedule(static)
     for (int k = 0; k < np; k++) {
         int km = (k + np - 1) % np, kp1 = (k + 1) % np;
         for (int j = 0; j < nt; j++)
@@ -434,8 +437,11 @@ int masoracle_pcg(int nr, int nt, int np, const double *Tr, const double *Tt,
     int status = MO_NOT_CONVERGED;
 
     masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, x, q);
+#pragma omp parallel for schedule(static)
     for (size_t c = 0; c < n; c++) r[c] = b[c] - q[c];
+#pragma omp parallel for schedule(static)
     for (size_t c = 0; c < n; c++) z[c] = r[c] / D[c];
+#pragma omp parallel for schedule(static)
     for (size_t c = 0; c < n; c++) p[c] = z[c];
     double rho = mo_dot(n, r, z);
     double rn = sqrt(mo_dot(n, r, r));
@@ -449,7 +455,9 @@ int masoracle_pcg(int nr, int nt, int np, const double *Tr, const double *Tt,
         double pi = mo_dot(n, p, q);
         if (!(pi > 0.0) || !isfinite(pi)) { status = MO_E_BREAKDOWN; break; }
         double alpha = rho / pi;
+#pragma omp parallel for schedule(static)
         for (size_t c = 0; c < n; c++) x[c] = x[c] + alpha * p[c];
+#pragma omp parallel for schedule(static)
         for (size_t c = 0; c < n; c++) r[c] = r[c] - alpha * q[c];
         rn = sqrt(mo_dot(n, r, r));
         if (hist) hist[k] = rn;
@@ -457,10 +465,12 @@ int masoracle_pcg(int nr, int nt, int np, const double *Tr, const double *Tt,
         *rnorm = rn;
         if (!isfinite(rn)) { status = MO_E_BREAKDOWN; break; }
         if (rn <= tol * bn) { status = MO_OK; break; }
+#pragma omp parallel for schedule(static)
         for (size_t c = 0; c < n; c++) z[c] = r[c] / D[c];
         double rho_new = mo_dot(n, r, z);
         double beta = rho_new / rho;
         rho = rho_new;
+#pragma omp parallel for schedule(static)
         for (size_t c = 0; c < n; c++) p[c] = z[c] + beta * p[c];
     }
 done:

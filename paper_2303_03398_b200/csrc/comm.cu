@@ -113,19 +113,19 @@ struct LoopSlots {
 };
 
 __global__ void k_gather_sum(LoopSlots s, int nranks, int count, double *out) {
-    const int t = threadIdx.x;
-    if (t >= count) return;
-    double v = 0.0;
-    for (int r = 0; r < nranks; ++r) v += s.d[r][t];   // fixed rank order: identical bits everywhere
-    out[t] = v;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int r = 0; r < nranks; ++r) v += s.d[r][t];   // fixed rank order: identical bits everywhere
+        out[t] = v;
+    }
 }
 
 __global__ void k_gather_max(LoopSlots s, int nranks, int count, int *out) {
-    const int t = threadIdx.x;
-    if (t >= count) return;
-    int v = s.i[0][t];
-    for (int r = 1; r < nranks; ++r) v = max(v, s.i[r][t]);
-    out[t] = v;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < count; t += gridDim.x * blockDim.x) {
+        int v = s.i[0][t];
+        for (int r = 1; r < nranks; ++r) v = max(v, s.i[r][t]);
+        out[t] = v;
+    }
 }
 
 struct LoopbackGroup {
@@ -280,7 +280,7 @@ class LoopbackComm final : public Comm {
         if (int s = phase1(st, peers, np, err)) return s;
         LoopSlots ls{};
         for (int r = 0; r < nranks; ++r) ls.d[r] = g->slots[r].dslot;
-        k_gather_sum<<<1, 32, 0, st>>>(ls, nranks, count, dev);
+        k_gather_sum<<<(count + 255) / 256, 256, 0, st>>>(ls, nranks, count, dev);
         if (int s = ck(cudaGetLastError(), "k_gather_sum", err)) return s;
         return phase2(st, peers, np, err);
     }
@@ -297,7 +297,7 @@ class LoopbackComm final : public Comm {
         if (int s = phase1(st, peers, np, err)) return s;
         LoopSlots ls{};
         for (int r = 0; r < nranks; ++r) ls.i[r] = g->slots[r].islot;
-        k_gather_max<<<1, 32, 0, st>>>(ls, nranks, count, dev);
+        k_gather_max<<<(count + 255) / 256, 256, 0, st>>>(ls, nranks, count, dev);
         if (int s = ck(cudaGetLastError(), "k_gather_max", err)) return s;
         return phase2(st, peers, np, err);
     }

@@ -111,7 +111,16 @@ struct Dims {
     int periodic_local;     // 1: single rank, halo planes are written by the kernels
     int vec_ok;             // 1: the 16-byte vector kernels may be used (MASPCG_OPT_VEC)
     int pdl;                // 1: launch the vector loop kernels with programmatic dependent launch
+    // L2 residency of the loop's arrays (vector kernels of path 1): 2 bits per array class L2A_* --
+    // L2_NORMAL, L2_KEEP (every line evict_last), L2_KEEP_FRAC (the fraction l2_frac of the lines
+    // evict_last), L2_FIRST (evict_first).  0 everywhere: plain loads and stores.
+    uint32_t l2_mask;
+    float l2_frac;
 };
+
+// Array classes of Dims::l2_mask and their residency codes.
+enum : int { L2A_D = 0, L2A_P, L2A_R, L2A_X, L2A_Q, L2A_T, kL2Arrays };
+enum : uint32_t { L2_NORMAL = 0u, L2_KEEP = 1u, L2_KEEP_FRAC = 2u, L2_FIRST = 3u };
 
 // Device pointers into the workspace.
 struct DevArrays {

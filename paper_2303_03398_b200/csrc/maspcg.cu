@@ -79,6 +79,10 @@ struct maspcg_ctx {
     int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
     int fuse_halo = 2;   // peer communicator: halo stores fused into the p-update, acquired by the stencil
                          // (MASPCG_OPT_FUSE_HALO)
+    int l2_keep = 1;            // MASPCG_OPT_L2_KEEP: L2 residency plan of the three-kernel loop (plan_l2)
+    size_t l2_bytes = 0;        // L2 capacity of the device
+    uint32_t g_l2mask = 0;      // the plan the cached graphs were captured with
+    float g_l2frac = 1.f;
     unsigned persist_grid = 0;   // path 5: co-resident grid of the persistent kernel
     // fused two-pass path geometry (fused.cu)
     int fused_bj = 1, fused_njt = 1, fused_blocks = 1;
@@ -390,8 +394,13 @@ maspcg_status vv_stencil(maspcg_ctx *c, double *y, bool with_dot, bool loop, cud
         CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
     }
     launch_vv_ring(c->vd, c->va, 1, exact_arith(c), st);
+    // NCCL: the halo send/recv (split communicator, comm stream) and the ring all-gather must not run
+    // concurrently -- NCCL does not guarantee progress of two communicators' kernels at once unless both
+    // are co-resident; join the halo first.  The peer communicator's exchanges are independent kernels.
+    const bool serial = c->comm && !c->comm->has_pair_allreduce();
+    if (serial) CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
     RET_IF(vv_ring_allreduce(c, c->va.ring, st));
-    if (c->comm) CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
+    if (c->comm && !serial) CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
     launch_vv_matvec(c->vd, c->va, c->a, y, with_dot, loop, false, exact_arith(c), st);
     return MASPCG_OK;
 }
@@ -423,7 +432,13 @@ maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool lo
     CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
     const unsigned gi = stencil_blocks(c->d, StencilPart::Interior, y);
     const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary, y);
-    launch_matvec(c->d, c->a, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, exact_arith(c), st);
+    // The interior launch without programmatic dependent launch (MASPCG_INTERIOR_PDL=0, default): with PDL
+    // its blocks become resident while the previous p-update still runs and hold every SM slot, so the
+    // exchange kernel on the comm stream cannot start until the interior stencil retires.
+    static const int ipdl = getenv("MASPCG_INTERIOR_PDL") ? atoi(getenv("MASPCG_INTERIOR_PDL")) : 0;
+    Dims di = c->d;
+    if (!ipdl) di.pdl = 0;
+    launch_matvec(di, c->a, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, exact_arith(c), st);
     CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
     launch_matvec(c->d, c->a, y, StencilPart::Boundary, with_dot, loop, gi, gi + gb, exact_arith(c), st);
     return MASPCG_OK;
@@ -624,8 +639,9 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st, int set) 
         CK(c, cudaGetLastError());
         return MASPCG_OK;
     }
-    const int key = graph_key(c) | (c->timing ? 16 : 0);
-    if (!c->gexec[0] || c->g_x != x || c->g_chunk != c->chunk || c->g_variant != key) {
+    const int key = graph_key(c) | (c->timing ? 16 : 0) | (c->timing << 12);
+    if (!c->gexec[0] || c->g_x != x || c->g_chunk != c->chunk || c->g_variant != key ||
+        c->g_l2mask != c->d.l2_mask || c->g_l2frac != c->d.l2_frac) {
         for (int b = 0; b < 2; ++b) {
             if (c->gexec[b]) {
                 cudaGraphExecDestroy(c->gexec[b]);
@@ -652,6 +668,8 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st, int set) 
         c->g_x = x;
         c->g_chunk = c->chunk;
         c->g_variant = key;
+        c->g_l2mask = c->d.l2_mask;
+        c->g_l2frac = c->d.l2_frac;
         c->tset = set;
     }
     CK(c, cudaGraphLaunch(c->gexec[set], st));
@@ -700,6 +718,66 @@ long long kernels_per_iteration(const maspcg_ctx *c) {
 bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
     const char *pa = (const char *)a, *pb = (const char *)b;
     return pa < pb + nb && pb < pa + na;
+}
+
+// L2 residency plan of the three-kernel loop (MASPCG_OPT_L2_KEEP; "super" scaling).  The
+// classes in order of HBM bytes saved per resident byte and iteration: D (read by all three kernels),
+// p (stencil read, p-update read and write), r (update read and write, p-update read) -- 3 accesses
+// each --, then x and q (2), then the face coefficients T_r, T_theta, T_phi (1).  Greedy up to
+// `budget` of the L2; the first class that does not fit is kept by the fraction that does.
+// MASPCG_L2_MASK / MASPCG_L2_FRAC (explicit plan) and MASPCG_L2_BUDGET override it for A/B runs.
+struct L2Range {
+    const void *p;
+    size_t bytes;
+};
+int l2_ranges(const maspcg_ctx *c, const double *x, L2Range out[8]) {
+    const size_t n8 = 8 * (size_t)c->d.n, pl8 = 8 * (size_t)c->d.plane;
+    int m = 0;
+    auto add = [&](int cls, const void *p, size_t b) {
+        if (((c->d.l2_mask >> (2 * cls)) & 3u) == L2_KEEP || ((c->d.l2_mask >> (2 * cls)) & 3u) == L2_KEEP_FRAC)
+            out[m++] = L2Range{p, b};
+    };
+    add(L2A_D, c->a.D, n8);
+    add(L2A_P, c->a.p, n8 + 2 * pl8);
+    add(L2A_R, c->a.r, n8);
+    add(L2A_X, x, n8);
+    add(L2A_Q, c->a.q, n8);
+    add(L2A_T, c->a.Tr, n8);
+    add(L2A_T, c->a.Tt, n8);
+    add(L2A_T, c->a.Tp, n8 + pl8);
+    return m;
+}
+
+void plan_l2(maspcg_ctx *c, const double *x) {
+    c->d.l2_mask = 0u;
+    c->d.l2_frac = 1.f;
+    if (!c->l2_keep || c->vmode || use_fused(c) || use_cg1(c) || use_wave(c) || use_persist(c, x)) return;
+    if (!c->d.vec_ok || (c->nr % 2) || ((uintptr_t)x & 15)) return;   // the 16-byte kernels carry the hints
+    if (const char *e = getenv("MASPCG_L2_MASK")) {
+        c->d.l2_mask = (uint32_t)strtoul(e, nullptr, 0);
+        if (const char *f = getenv("MASPCG_L2_FRAC")) c->d.l2_frac = (float)atof(f);
+        return;
+    }
+    double budget = 0.75;
+    if (const char *e = getenv("MASPCG_L2_BUDGET")) budget = atof(e);
+    const double n8 = 8.0 * c->d.n, pl8 = 8.0 * c->d.plane;
+    const struct {
+        int cls;
+        double bytes;
+    } order[] = {{L2A_D, n8}, {L2A_P, n8 + 2 * pl8}, {L2A_R, n8}, {L2A_X, n8}, {L2A_Q, n8}, {L2A_T, 3 * n8 + pl8}};
+    double left = budget * (double)c->l2_bytes;
+    for (const auto &o : order) {
+        if (o.bytes <= left) {
+            c->d.l2_mask |= L2_KEEP << (2 * o.cls);
+            left -= o.bytes;
+            continue;
+        }
+        if (left >= 0.05 * o.bytes) {
+            c->d.l2_mask |= L2_KEEP_FRAC << (2 * o.cls);
+            c->d.l2_frac = (float)(left / o.bytes);
+        }
+        break;
+    }
 }
 
 maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol, int maxit, double *hist,
@@ -778,6 +856,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     }
     CK(c, cudaGetLastError());
     long long launched = 4 + (c->comm ? 1 : 0);
+    plan_l2(c, x);
 
     // PCG loop: chunks of `chunk` iterations, one speculative chunk in flight.
     CK(c, cudaMemcpyAsync(c->snap[0], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
@@ -830,6 +909,14 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     }
     launch_zero_x_if(c->d, c->a, x, st);
     launched += 1;
+    if (c->d.l2_mask) {   // the kept lines go back to the normal eviction priority
+        L2Range rs[8];
+        const int m = l2_ranges(c, x, rs);
+        for (int i = 0; i < m; ++i) launch_l2_demote(rs[i].p, rs[i].bytes, st);
+        launched += m;
+        c->d.l2_mask = 0u;
+        c->d.l2_frac = 1.f;
+    }
     c->a.peer_p_lo = c->a.peer_p_hi = nullptr;   // only the loop's p-updates store into the neighbours
     c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
     c->a.gather_ranks = 0;
@@ -912,6 +999,8 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     if (!peer && !group && nranks > 1 && !nccl_unique_id)
         return fail(MASPCG_E_INVALID, "nccl_unique_id must be given when nranks > 1");
     if (peer && nranks > kP2PMaxRanks) return fail(MASPCG_E_INVALID, "the peer communicator supports at most 16 ranks");
+    // the all-gather scratch of the Dot2 all-reduces (a.gather, va.gather) holds kMaxRanks rank slots
+    if (nranks > kMaxRanks) return fail(MASPCG_E_INVALID, "at most 16 ranks (all-gather scratch of the reductions)");
     if (peer && group)
         return fail(MASPCG_E_INVALID, "peer mode needs one CUDA context per rank (processes, CUDA IPC): ranks sharing "
                                       "a context could spin on each other inside one device");
@@ -928,7 +1017,11 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->nloc = (int)nloc;
     c->k0 = rank * (int)nloc;
     cudaError_t e = cudaSetDevice(cuda_device);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    // the communication stream at the highest priority: its exchange kernels (NCCL send/recv, peer pushes)
+    // are dispatched ahead of pending stencil blocks
+    int prio_lo = 0, prio_hi = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio_hi);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
@@ -973,6 +1066,11 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->d.periodic_local = c->comm ? 0 : 1;
     c->d.vec_ok = 1;
     c->d.pdl = 1;
+    {
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cuda_device);
+        c->l2_bytes = (size_t)(l2 > 0 ? l2 : 0);
+    }
     c->fused_bj = fused_bj(nr, nt);   // 0: nr too large for one register batch per thread -> three kernels
     if (c->fused_bj > 0) {
         c->fused_njt = (nt + c->fused_bj - 1) / c->fused_bj;
@@ -1654,6 +1752,7 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             c->arith = (int)v;
             break;
         case MASPCG_OPT_FUSE_HALO: c->fuse_halo = v < 0 ? 0 : (v > 2 ? 2 : v); break;
+        case MASPCG_OPT_L2_KEEP: c->l2_keep = v ? 1 : 0; break;
         case MASPCG_OPT_PATH:
             if (v < 0 || v > 5)
                 SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels), 2 (fused), 3 (wave), 4 (single "

@@ -539,3 +539,19 @@ def test_cg1_special_cases(oracle_mod):
     assert st == oracle_mod.NOT_CONVERGED and iters == 5 and hist.size == 6
     st, x, iters, *_ = op.pcg(np.zeros(op.shape), bb, 1e-10, 5, variant="cg1")
     assert st == 0 and iters == 0 and not x.any()
+
+
+# ------------------------------------------------------------------ the -fopenmp timing build (bench.py cpu_baseline)
+def test_openmp_build_gives_identical_iterates(oracle_mod):
+    """The -fopenmp build that bench.py times on all host cores (cpu_baseline, --impl reference) is the
+    same oracle: its per-cell loops only run on several threads and the dot products stay sequential,
+    so c1's solve (solution, count and history) is identical bit for bit to the plain build."""
+    p = inputs.make_problem("c1")
+    a = oracle_mod.solve_problem(p)
+    oracle_mod.use_openmp(True)
+    try:
+        b = oracle_mod.solve_problem(p)
+    finally:
+        oracle_mod.use_openmp(False)
+    assert a["iters"] == b["iters"] == 130
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["hist"], b["hist"])
