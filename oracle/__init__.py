@@ -69,6 +69,10 @@ def lib():
             "masoracle_face_coefficients": [i, i, i, d, ctypes.c_double, i, i, d, ctypes.c_double, d, d, d, d],
             "masoracle_rkl2_step": [i, i, i, d, d, d, d, d, d, d, d, ctypes.c_double, i, d],
             "masoracle_pcg_cg1": [i, i, i, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
+            "masoracle_aniso_edges": [i, i, i, d, d, d, d, d, d, d, d, d],
+            "masoracle_aniso_apply": [i, i, i, d, d, d, d, d, d, d, d, d],
+            "masoracle_aniso_diag": [i, i, i, d, d, d, d, d],
+            "masoracle_aniso_pcg": [i, i, i, d, d, d, d, d, d, d, d, d, d, ctypes.c_double, i, d, d, d, d],
             "masoracle_vv_check_grid": [i, i, i, d, d, d],
             "masoracle_vv_coefficients": [i, i, i, d, d, d, d, d, i, i, d, d, d, d, d, d, d],
             "masoracle_vv_div": [i, i, i, d, d, d, d, d, d, d],
@@ -210,6 +214,64 @@ def solve_problem(prob, tol=None, maxit=None, x0=None, variant="hs"):
     st, x, iters, hist, bn, rn = op.pcg(b, prob.x0 if x0 is None else x0,
                                         prob.tol if tol is None else tol,
                                         prob.maxit if maxit is None else maxit, variant)
+    return dict(status=st, x=x, iters=iters, hist=hist, bnorm=bn, rnorm=rn, op=op, b=b)
+
+
+# ----------------------------------------------------------------------------------------------
+# Field-aligned anisotropic conduction (masoracle.c, R33)
+class AnisoOperator(Operator):
+    """The 19-point field-aligned operator: the 7-point operator of the diagonal face coefficients
+    kr, kt, kp (kappa_perp + kappa_par b_a^2) plus the cross terms of the edge coefficients
+    krt [np][nt+1][nr+1], krp [np][nt][nr+1], ktp [np][nt+1][nr] (kappa_par b_a b_b at edge centres)."""
+
+    def __init__(self, rf, tf, pf, kr, kt, kp, s, bc_in, bc_out, krt, krp, ktp):
+        super().__init__(rf, tf, pf, kr, kt, kp, s, bc_in, bc_out)
+        nr, nt, np_ = self.nr, self.nt, self.np
+        krt, krp, ktp = _c(krt), _c(krp), _c(ktp)
+        assert krt.shape == (np_, nt + 1, nr + 1) and krp.shape == (np_, nt, nr + 1)
+        assert ktp.shape == (np_, nt + 1, nr)
+        self.Xrt = np.empty((np_, nt + 1, nr + 1))
+        self.Xrp = np.empty((np_, nt, nr + 1))
+        self.Xtp = np.empty((np_, nt + 1, nr))
+        st = lib().masoracle_aniso_edges(nr, nt, np_, _p(self.rf), _p(self.tf), _p(self.pf), _p(krt), _p(krp),
+                                         _p(ktp), _p(self.Xrt), _p(self.Xrp), _p(self.Xtp))
+        if st:
+            raise OracleError(st, "aniso_edges")
+        self.D7 = self.D
+        self.Dj = np.empty(self.shape)
+        lib().masoracle_aniso_diag(nr, nt, np_, _p(self.D7), _p(self.Xrt), _p(self.Xrp), _p(self.Xtp), _p(self.Dj))
+
+    def _ptrs(self):
+        return (_p(self.Tr), _p(self.Tt), _p(self.Tp), _p(self.D7), _p(self.Xrt), _p(self.Xrp), _p(self.Xtp))
+
+    def apply(self, u) -> np.ndarray:
+        u = _c(u)
+        assert u.shape == self.shape
+        y = np.empty(self.shape)
+        lib().masoracle_aniso_apply(self.nr, self.nt, self.np, *self._ptrs(), _p(u), _p(y))
+        return y
+
+    def pcg(self, b, x0, tol, maxit, variant="hs"):
+        assert variant == "hs"
+        b = _c(b)
+        x = np.array(_c(x0), copy=True)
+        hist = np.zeros(maxit + 1)
+        iters = ctypes.c_int(0)
+        bn, rn = ctypes.c_double(0), ctypes.c_double(0)
+        st = lib().masoracle_aniso_pcg(self.nr, self.nt, self.np, *self._ptrs(), _p(self.Dj), _p(b), _p(x),
+                                       float(tol), int(maxit), _p(hist), ctypes.byref(iters), ctypes.byref(bn),
+                                       ctypes.byref(rn))
+        return st, x, iters.value, hist[: iters.value + 1].copy(), bn.value, rn.value
+
+
+def solve_aniso_problem(prob, tol=None, maxit=None, x0=None):
+    """Solve an ``inputs.AnisoProblem`` covering the whole global grid."""
+    assert prob.k0 == 0 and prob.nloc == prob.np, "the oracle works on the global grid"
+    op = AnisoOperator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out,
+                       prob.krt, prob.krp, prob.ktp)
+    b = op.rhs(prob.f, prob.g_in, prob.g_out)
+    st, x, iters, hist, bn, rn = op.pcg(b, prob.x0 if x0 is None else x0, prob.tol if tol is None else tol,
+                                        prob.maxit if maxit is None else maxit)
     return dict(status=st, x=x, iters=iters, hist=hist, bnorm=bn, rnorm=rn, op=op, b=b)
 
 

@@ -415,11 +415,30 @@ static double mo_dot(size_t n, const double *a, const double *b) {
  * Norms are unweighted Euclidean norms of the volume-weighted system; hist is
  * the recurrence residual.  Non-finite ||b|| or hist -> E_BREAKDOWN.
  * hist must hold maxit+1 doubles (or be NULL).                               */
+/* The operator of a PCG solve: y = A u (the 7-point operator, or the field-aligned one of NEXT-4). */
+typedef struct {
+    int nr, nt, np;
+    const double *Tr, *Tt, *Tp, *D;      /* 7-point part (D: its own diagonal) */
+    const double *Xrt, *Xrp, *Xtp;       /* field-aligned cross terms, or NULL */
+} mo_op;
+
+static void mo_op_apply(const mo_op *op, const double *u, double *y);
+
+static int mo_pcg(const mo_op *op, const double *D, const double *b, double *x, double tol, int maxit,
+                  double *hist, int *iters, double *bnorm, double *rnorm);
+
 int masoracle_pcg(int nr, int nt, int np, const double *Tr, const double *Tt,
                   const double *Tp, const double *D, const double *b, double *x,
                   double tol, int maxit, double *hist, int *iters, double *bnorm,
                   double *rnorm) {
-    size_t n = (size_t)nr * nt * np;
+    mo_op op = {nr, nt, np, Tr, Tt, Tp, D, NULL, NULL, NULL};
+    return mo_pcg(&op, D, b, x, tol, maxit, hist, iters, bnorm, rnorm);
+}
+
+/* PCG on any operator `op` with the Jacobi diagonal D (the algorithm of masoracle_pcg above). */
+static int mo_pcg(const mo_op *op, const double *D, const double *b, double *x, double tol, int maxit,
+                  double *hist, int *iters, double *bnorm, double *rnorm) {
+    size_t n = (size_t)op->nr * op->nt * op->np;
     if (maxit < 0 || !(tol >= 0.0)) return MO_E_INVALID;
     *iters = 0;
     double bn = sqrt(mo_dot(n, b, b));
@@ -436,7 +455,7 @@ int masoracle_pcg(int nr, int nt, int np, const double *Tr, const double *Tt,
     if (!r || !z || !p || !q) { free(r); free(z); free(p); free(q); return MO_E_NOMEM; }
     int status = MO_NOT_CONVERGED;
 
-    masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, x, q);
+    mo_op_apply(op, x, q);
 #pragma omp parallel for schedule(static)
     for (size_t c = 0; c < n; c++) r[c] = b[c] - q[c];
 #pragma omp parallel for schedule(static)
@@ -451,7 +470,7 @@ int masoracle_pcg(int nr, int nt, int np, const double *Tr, const double *Tt,
     if (rn <= tol * bn) { status = MO_OK; goto done; }
 
     for (int k = 1; k <= maxit; k++) {
-        masoracle_apply(nr, nt, np, Tr, Tt, Tp, D, p, q);
+        mo_op_apply(op, p, q);
         double pi = mo_dot(n, p, q);
         if (!(pi > 0.0) || !isfinite(pi)) { status = MO_E_BREAKDOWN; break; }
         double alpha = rho / pi;
@@ -657,4 +676,186 @@ int masoracle_solve(int nr, int nt, int np, const double *rf, const double *tf,
 out:
     free(Tr); free(Tt); free(Tp); free(D); free(b);
     return st;
+}
+
+/* ============================================ field-aligned anisotropic conduction (NEXT-4, R33)
+ *
+ * "field-aligned anisotropic conduction (b.b.grad T, a 19-point stencil; not
+ * described in the paper)" -- the usual coronal form of the thermal-conduction term of MAS's "full
+ * thermodynamic MHD model" (Sec. V-A) on its staggered spherical grid (PAPER.md:56,
+ * Sec. III).  PAPER.md gives no formula; everything here is reading R33:
+ *
+ *   flux q = -K grad T with K = kappa_perp I + kappa_par b b^T (b a unit vector), in the volume-weighted
+ *   symmetric form A = diag(sV) + Hessian of the discrete energy
+ *       E(T) = 1/2 sum_faces T_f (dT_f)^2  +  sum_edges X_e (a_e.T)(b_e.T)
+ *   -- the first sum is the 7-point operator with face coefficients K_aa = kappa_perp + kappa_par b_a^2
+ *   (caller's kr, kt, kp: the diagonal terms of (b.grad T)^2); the second the cross terms
+ *   2 b_a b_b d_a T d_b T, each on the edges where an a-face meets a b-face: a_e.T and b_e.T are the
+ *   two face differences of the 2x2 cells around the edge, averaged (a_e.T = da/2, b_e.T = db/2), and
+ *       X_e = k_ab(edge) * V_dual(e) / (h_a * h_b)   (k_ab = kappa_par b_a b_b at the edge centre)
+ *   with V_dual the exact volume between the four cell centres and h the metric distances of the two
+ *   differences at the edge.  Only edges between two interior faces carry a cross term (boundary
+ *   faces: the normal term only, R7, R8).  A couples a cell to its 6 face and 12 edge neighbours
+ *   (19 points); it is symmetric by construction, annihilates constants, reduces to the 7-point
+ *   operator when b = r^ (kt = kp = kappa_perp, no cross terms), and for constant coefficients on a
+ *   uniform grid its symbol 4 x^T (cc^T + diag(1 - c_a^2)) x, x_a = b_a sin(xi_a/2), c_a = cos(xi_a/2),
+ *   is >= 0: semi-definite, definite with a floor kappa_perp > 0 or a shift.
+ *
+ * Edge metric (1-D factors, exact integrals of the dual volumes):
+ *   r-theta edge (r face ie, theta face je, plane k):  X = k * gr_ie * gt_je * dphi_k
+ *   r-phi edge (r face ie, row j, phi face k+1/2):     X = k * gr_ie * cs_j
+ *   theta-phi edge (theta face je, column i, phi face k+1/2): X = k * q_i * gts_je
+ *     gr_ie  = (rc_ie^2 + rc_ie rc_ie-1 + rc_ie-1^2) / (3 r_f[ie])   [(rc^3 - rc'^3)/3 / (h^r r_f)]
+ *     gt_je  = (cos tc_je-1 - cos tc_je) / h^t_je = 2 sin((tc_je-1 + tc_je)/2) sin(h^t_je/2) / h^t_je
+ *     cs_j   = 2 sin(dtheta_j / 2)                                  [C_j / sin tc_j]
+ *     q_i    = R3_i / rc_i^2,   gts_je = gt_je / sin t_f[je]
+ * stored as Xq = X / 4 (the two averages' factors 1/2 folded in), so that
+ *   (A u)_c = (D7_c u_c - 7-point neighbour sum) + sum_{12 edges of c} Xq_e (s_a db + s_b da)
+ * with da, db the sums of the two a- and b-differences around the edge and s_a, s_b = +1 when c is on
+ * the high side of the edge's a- / b-face, -1 otherwise; diag(A)_c = D7_c + sum_e Xq_e (2 s_a s_b).
+ * Edge order of a cell (i, j, k): r-theta (i,j) (i+1,j) (i,j+1) (i+1,j+1); r-phi (i,k-1/2) (i+1,k-1/2)
+ * (i,k+1/2) (i+1,k+1/2); theta-phi (j,k-1/2) (j+1,k-1/2) (j,k+1/2) (j+1,k+1/2); left-to-right sums.
+ *
+ * Layouts: krt, Xrt [np][nt+1][nr+1] (edge (ie, je) of plane k); krp, Xrp [np][nt][nr+1] (edge (ie, j)
+ * on phi face k+1/2); ktp, Xtp [np][nt+1][nr] (edge (je, i) on phi face k+1/2).  Pins:
+ * tests/test_oracle_aniso_pins.py.                                                                     */
+
+/* Edge weights Xq (= X / 4) from the cross coefficients kappa_par b_a b_b given at the edge centres;
+ * 0 on edges with a boundary face.  E_INVALID for a non-finite coefficient (any sign is allowed).  */
+int masoracle_aniso_edges(int nr, int nt, int np, const double *rf, const double *tf, const double *pf,
+                          const double *krt, const double *krp, const double *ktp,
+                          double *Xrt, double *Xrp, double *Xtp) {
+    int st = masoracle_check_grid(nr, nt, np, rf, tf, pf);
+    if (st) return st;
+    size_t nrt = (size_t)np * (nt + 1) * (nr + 1), nrp = (size_t)np * nt * (nr + 1), ntp = (size_t)np * (nt + 1) * nr;
+    for (size_t c = 0; c < nrt; c++) if (!isfinite(krt[c])) return MO_E_INVALID;
+    for (size_t c = 0; c < nrp; c++) if (!isfinite(krp[c])) return MO_E_INVALID;
+    for (size_t c = 0; c < ntp; c++) if (!isfinite(ktp[c])) return MO_E_INVALID;
+    mo_grid g;
+    if (mo_grid_build(nr, nt, np, rf, tf, pf, &g)) return MO_E_NOMEM;
+    for (int k = 0; k < np; k++)
+        for (int je = 0; je <= nt; je++)
+            for (int ie = 0; ie <= nr; ie++) {
+                size_t e = IDX(k, je, ie, nt + 1, nr + 1);
+                if (ie < 1 || ie > nr - 1 || je < 1 || je > nt - 1) { Xrt[e] = 0.0; continue; }
+                double gr = (g.rc[ie] * g.rc[ie] + g.rc[ie] * g.rc[ie - 1] + g.rc[ie - 1] * g.rc[ie - 1]) / (3.0 * rf[ie]);
+                double gt = 2.0 * sin(0.5 * (g.tc[je - 1] + g.tc[je])) * sin(0.5 * g.ht[je]) / g.ht[je];
+                Xrt[e] = krt[e] * gr * gt * g.dp[k] * 0.25;
+            }
+    for (int k = 0; k < np; k++)
+        for (int j = 0; j < nt; j++)
+            for (int ie = 0; ie <= nr; ie++) {
+                size_t e = IDX(k, j, ie, nt, nr + 1);
+                if (ie < 1 || ie > nr - 1) { Xrp[e] = 0.0; continue; }
+                double gr = (g.rc[ie] * g.rc[ie] + g.rc[ie] * g.rc[ie - 1] + g.rc[ie - 1] * g.rc[ie - 1]) / (3.0 * rf[ie]);
+                double cs = 2.0 * sin(0.5 * g.dt[j]);
+                Xrp[e] = krp[e] * gr * cs * 0.25;
+            }
+    for (int k = 0; k < np; k++)
+        for (int je = 0; je <= nt; je++)
+            for (int i = 0; i < nr; i++) {
+                size_t e = IDX(k, je, i, nt + 1, nr);
+                if (je < 1 || je > nt - 1) { Xtp[e] = 0.0; continue; }
+                double q = g.R3[i] / (g.rc[i] * g.rc[i]);
+                double gt = 2.0 * sin(0.5 * (g.tc[je - 1] + g.tc[je])) * sin(0.5 * g.ht[je]) / g.ht[je];
+                double gts = gt / g.sinf_[je];
+                Xtp[e] = ktp[e] * q * gts * 0.25;
+            }
+    mo_grid_free(&g);
+    return MO_OK;
+}
+
+/* The cross sum of cell (k, j, i) in the edge order of R33 (diag = 0), or its diagonal
+ * sum_e Xq_e (2 s_a s_b) (diag = 1). */
+static double mo_aniso_cross(const mo_op *op, const double *u, int k, int j, int i, int diag) {
+    const int nr = op->nr, nt = op->nt, np = op->np;
+    const int km = (k + np - 1) % np, kp1 = (k + 1) % np;
+    double sx = 0.0;
+    /* r-theta edges of plane k */
+    for (int e = 0; e < 4; e++) {
+        int ie = i + (e & 1), je = j + (e >> 1);
+        if (ie < 1 || ie > nr - 1 || je < 1 || je > nt - 1) continue;
+        double sa = (ie == i) ? 1.0 : -1.0, sb = (je == j) ? 1.0 : -1.0;
+        double X = op->Xrt[IDX(k, je, ie, nt + 1, nr + 1)];
+        if (diag) { sx = sx + X * (2.0 * sa * sb); continue; }
+        double u00 = u[IDX(k, je - 1, ie - 1, nt, nr)], u10 = u[IDX(k, je - 1, ie, nt, nr)];
+        double u01 = u[IDX(k, je, ie - 1, nt, nr)], u11 = u[IDX(k, je, ie, nt, nr)];
+        double da = (u10 - u00) + (u11 - u01);   /* the two r-differences */
+        double db = (u01 - u00) + (u11 - u10);   /* the two theta-differences */
+        sx = sx + X * (sa * db + sb * da);
+    }
+    /* r-phi edges of row j: faces k-1/2 (planes km, k) and k+1/2 (planes k, kp1) */
+    for (int e = 0; e < 4; e++) {
+        int ie = i + (e & 1), hi = e >> 1;
+        if (ie < 1 || ie > nr - 1) continue;
+        int ka = hi ? k : km, kb = hi ? kp1 : k;
+        double sa = (ie == i) ? 1.0 : -1.0, sb = hi ? -1.0 : 1.0;
+        double X = op->Xrp[IDX(ka, j, ie, nt, nr + 1)];
+        if (diag) { sx = sx + X * (2.0 * sa * sb); continue; }
+        double ua0 = u[IDX(ka, j, ie - 1, nt, nr)], ua1 = u[IDX(ka, j, ie, nt, nr)];
+        double ub0 = u[IDX(kb, j, ie - 1, nt, nr)], ub1 = u[IDX(kb, j, ie, nt, nr)];
+        double da = (ua1 - ua0) + (ub1 - ub0);   /* the two r-differences */
+        double db = (ub0 - ua0) + (ub1 - ua1);   /* the two phi-differences */
+        sx = sx + X * (sa * db + sb * da);
+    }
+    /* theta-phi edges of column i */
+    for (int e = 0; e < 4; e++) {
+        int je = j + (e & 1), hi = e >> 1;
+        if (je < 1 || je > nt - 1) continue;
+        int ka = hi ? k : km, kb = hi ? kp1 : k;
+        double sa = (je == j) ? 1.0 : -1.0, sb = hi ? -1.0 : 1.0;
+        double X = op->Xtp[IDX(ka, je, i, nt + 1, nr)];
+        if (diag) { sx = sx + X * (2.0 * sa * sb); continue; }
+        double ua0 = u[IDX(ka, je - 1, i, nt, nr)], ua1 = u[IDX(ka, je, i, nt, nr)];
+        double ub0 = u[IDX(kb, je - 1, i, nt, nr)], ub1 = u[IDX(kb, je, i, nt, nr)];
+        double da = (ua1 - ua0) + (ub1 - ub0);   /* the two theta-differences */
+        double db = (ub0 - ua0) + (ub1 - ua1);   /* the two phi-differences */
+        sx = sx + X * (sa * db + sb * da);
+    }
+    return sx;
+}
+
+static void mo_op_apply(const mo_op *op, const double *u, double *y) {
+    masoracle_apply(op->nr, op->nt, op->np, op->Tr, op->Tt, op->Tp, op->D, u, y);
+    if (!op->Xrt) return;
+#pragma omp parallel for schedule(static)
+    for (int k = 0; k < op->np; k++)
+        for (int j = 0; j < op->nt; j++)
+            for (int i = 0; i < op->nr; i++) {
+                size_t c = IDX(k, j, i, op->nt, op->nr);
+                y[c] = y[c] + mo_aniso_cross(op, u, k, j, i, 0);
+            }
+}
+
+/* y = A u of the field-aligned operator: the 7-point operator (Tr, Tt, Tp, its diagonal D7 from
+ * masoracle_assemble with the face coefficients K_aa) plus the cross terms. */
+int masoracle_aniso_apply(int nr, int nt, int np, const double *Tr, const double *Tt, const double *Tp,
+                          const double *D7, const double *Xrt, const double *Xrp, const double *Xtp,
+                          const double *u, double *y) {
+    mo_op op = {nr, nt, np, Tr, Tt, Tp, D7, Xrt, Xrp, Xtp};
+    mo_op_apply(&op, u, y);
+    return MO_OK;
+}
+
+/* Jacobi diagonal of the field-aligned operator: Dj = D7 + sum_e Xq_e (2 s_a s_b). */
+int masoracle_aniso_diag(int nr, int nt, int np, const double *D7, const double *Xrt, const double *Xrp,
+                         const double *Xtp, double *Dj) {
+    mo_op op = {nr, nt, np, NULL, NULL, NULL, D7, Xrt, Xrp, Xtp};
+    for (int k = 0; k < np; k++)
+        for (int j = 0; j < nt; j++)
+            for (int i = 0; i < nr; i++) {
+                size_t c = IDX(k, j, i, nt, nr);
+                Dj[c] = D7[c] + mo_aniso_cross(&op, NULL, k, j, i, 1);
+            }
+    return MO_OK;
+}
+
+/* Point-Jacobi PCG (masoracle_pcg's algorithm, R6, R11-R14) on the field-aligned operator with the
+ * Jacobi diagonal Dj (masoracle_aniso_diag). */
+int masoracle_aniso_pcg(int nr, int nt, int np, const double *Tr, const double *Tt, const double *Tp,
+                        const double *D7, const double *Xrt, const double *Xrp, const double *Xtp,
+                        const double *Dj, const double *b, double *x, double tol, int maxit, double *hist,
+                        int *iters, double *bnorm, double *rnorm) {
+    mo_op op = {nr, nt, np, Tr, Tt, Tp, D7, Xrt, Xrp, Xtp};
+    return mo_pcg(&op, Dj, b, x, tol, maxit, hist, iters, bnorm, rnorm);
 }

@@ -351,3 +351,112 @@ def make_vv_problem(name: str, k0: int | None = None, nloc: int | None = None, *
                      np.ascontiguousarray(f), np.ascontiguousarray(x0), wall_in, wall_out,
                      None if g_in is None else np.ascontiguousarray(g_in),
                      None if g_out is None else np.ascontiguousarray(g_out), tol, maxit)
+
+
+# --------------------------------------------------------------------------- field-aligned conduction (NEXT-4)
+def b_field(r: np.ndarray, th: np.ndarray, ph: np.ndarray):
+    """Unit vector of a coronal-like magnetic field (dipole + open monopole flux + spiral, with a
+    non-axisymmetric perturbation; B_r >= (2.5 r - 2)/r^3 > 0 on r >= 1, so no null points):
+        B_r = (2 cos th + 2.5 r)/r^3, B_th = sin th (1 + 0.3 cos ph)/r^3, B_ph = -sin th (0.5 r + 0.2 sin 2ph)/r^3.
+    Returns (b_r, b_th, b_ph) broadcast over the inputs."""
+    r, th, ph = np.broadcast_arrays(r, th, ph)
+    Br = (2.0 * np.cos(th) + 2.5 * r) / r ** 3
+    Bt = np.sin(th) * (1.0 + 0.3 * np.cos(ph)) / r ** 3
+    Bp = -np.sin(th) * (0.5 * r + 0.2 * np.sin(2.0 * ph)) / r ** 3
+    n = np.sqrt(Br * Br + Bt * Bt + Bp * Bp)
+    return Br / n, Bt / n, Bp / n
+
+
+@dataclasses.dataclass
+class AnisoProblem(Problem):
+    """A Problem with field-aligned conduction: kr, kt, kp are the diagonal face coefficients
+    kappa_perp + kappa_par b_a^2, and the edge coefficients kappa_par b_a b_b are
+    krt [nloc][nt+1][nr+1] (edge r-face ie, theta-face je, plane k), krp [nloc][nt][nr+1] (r-face ie, row j,
+    phi face k+1/2), ktp [nloc][nt+1][nr] (theta-face je, column i, phi face k+1/2)."""
+    krt: np.ndarray = None
+    krp: np.ndarray = None
+    ktp: np.ndarray = None
+
+
+def aniso_coefficients(kpar, kperp, bfun, rf, tf, pf, k0, nloc):
+    """kr, kt, kp (kappa_perp + kappa_par b_a^2 at face centres) and krt, krp, ktp (kappa_par b_a b_b at
+    edge centres) of the phi-slab [k0, k0 + nloc); kpar(r, th, ph), kperp(r, th, ph), bfun(r, th, ph) ->
+    (b_r, b_th, b_ph).  Evaluation only (generator): no method arithmetic."""
+    rc, tc, pc = midpoints(rf), midpoints(tf), midpoints(pf)
+    phc, phf = pc[k0:k0 + nloc], pf[k0 + 1:k0 + nloc + 1]
+    R = lambda r: r[None, None, :]
+    T = lambda t: t[None, :, None]
+    P = lambda p: p[:, None, None]
+
+    def at(r, t, p, a, b=None):
+        shp = np.broadcast_shapes(r.shape, t.shape, p.shape)
+        bb = bfun(r, t, p)
+        kpa = np.broadcast_to(kpar(r, t, p), shp)
+        if b is None:
+            return np.broadcast_to(kperp(r, t, p), shp) + kpa * bb[a] * bb[a]
+        return kpa * bb[a] * bb[b]
+
+    kr = at(R(rf), T(tc), P(phc), 0)
+    kt = at(R(rc), T(tf), P(phc), 1)
+    kp = at(R(rc), T(tc), P(phf), 2)
+    krt = at(R(rf), T(tf), P(phc), 0, 1)
+    krp = at(R(rf), T(tc), P(phf), 0, 2)
+    ktp = at(R(rc), T(tf), P(phf), 1, 2)
+    c = lambda x: np.ascontiguousarray(x, dtype=np.float64)
+    return c(kr), c(kt), c(kp), c(krt), c(krp), c(ktp)
+
+
+ANISO_CONFIGS = {
+    # field-aligned thermal conduction on the grids of BASELINE.json configs[0..2] (SURVEY 8(f) NEXT-4)
+    "c1a": (16, 16, 32),
+    "c2a": (64, 64, 128),
+    "c3a": (150, 300, 600),
+}
+
+
+def make_aniso_problem(name: str, k0: int | None = None, nloc: int | None = None, *,
+                       shape: tuple[int, int, int] | None = None) -> AnisoProblem:
+    """Field-aligned conduction on the grid of c1 / c2 / c3: kappa_par = (0.3 + 0.7 e^{-(r-1)/5})^{5/2}
+    (the T^{5/2} profile of c2) along b_field, an isotropic floor kappa_perp = 1e-2 kappa_par, shift
+    s = 1/dt (dt = 1e-2; c1a: s = 1), rhs and boundary conditions as the base config."""
+    base = {"c1a": "c1", "c2a": "c2", "c3a": "c3"}[name]
+    nr, nt, np_ = shape if shape is not None else ANISO_CONFIGS[name]
+    if k0 is None:
+        k0, nloc = 0, np_
+    p = make_problem(base, k0, nloc, shape=(nr, nt, np_))
+    if base == "c1":
+        kpar = lambda r, t, p_: np.ones(np.broadcast_shapes(r.shape, t.shape, p_.shape))
+        s = np.ones((nloc, nt, nr))
+    else:
+        kpar = lambda r, t, p_: np.broadcast_to((0.3 + 0.7 * np.exp(-(r - 1.0) / 5.0)) ** 2.5,
+                                                np.broadcast_shapes(r.shape, t.shape, p_.shape))
+        s = np.full((nloc, nt, nr), 1.0 / 1e-2)
+    kperp = lambda r, t, p_: 1e-2 * kpar(r, t, p_)
+    kr, kt, kp, krt, krp, ktp = aniso_coefficients(kpar, kperp, b_field, p.rf, p.tf, p.pf, k0, nloc)
+    f = p.f if base == "c1" else p.f / p.s * s
+    return AnisoProblem(name, nr, nt, np_, k0, nloc, p.rf, p.tf, p.pf, kr, kt, kp, np.ascontiguousarray(s),
+                        np.ascontiguousarray(f), p.x0, p.bc_in, p.bc_out, p.g_in, p.g_out, p.tol, p.maxit,
+                        krt, krp, ktp)
+
+
+def random_aniso_problem(nr: int, nt: int, np_: int, seed: int, *, bc_in=BC_DIRICHLET, bc_out=BC_NEUMANN0,
+                         k0=0, nloc=None, shift=True) -> AnisoProblem:
+    """Small random field-aligned problem for parity tests: rough kappa_par in [0.5, 2] at every face and
+    edge (white noise), the smooth b_field, kappa_perp = 0.2, random s in [0.5, 1.5], rhs and wall data."""
+    nloc = np_ if nloc is None else nloc
+    p = random_problem(nr, nt, np_, seed, bc_in=bc_in, bc_out=bc_out, k0=k0, nloc=nloc, shift=shift)
+    rng_seed = seed * 16 + 9
+
+    def rough(r, t, ph):
+        shp = np.broadcast_shapes(r.shape, t.shape, ph.shape)
+        n = int(np.prod(shp))
+        # decomposition-independent: noise indexed by the evaluation point's global coordinates
+        key = np.round((np.broadcast_to(r, shp) * 7919.0 + np.broadcast_to(t, shp) * 104729.0 +
+                        np.broadcast_to(ph, shp) * 1299709.0) * 1e6).astype(np.uint64).reshape(n)
+        w = (splitmix64(key ^ np.uint64(rng_seed)) >> np.uint64(11)).astype(np.float64) / float(1 << 53)
+        return (0.5 + 1.5 * w).reshape(shp)
+
+    kperp = lambda r, t, ph: np.full(np.broadcast_shapes(r.shape, t.shape, ph.shape), 0.2)
+    kr, kt, kp, krt, krp, ktp = aniso_coefficients(rough, kperp, b_field, p.rf, p.tf, p.pf, k0, nloc)
+    return AnisoProblem(f"arand{seed}", nr, nt, np_, k0, nloc, p.rf, p.tf, p.pf, kr, kt, kp, p.s, p.f, p.x0,
+                        p.bc_in, p.bc_out, p.g_in, p.g_out, p.tol, p.maxit, krt, krp, ktp)
