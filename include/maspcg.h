@@ -345,6 +345,42 @@ MASPCG_API maspcg_status maspcg_vv_solve(maspcg_ctx *ctx, const double *f, doubl
 /* The Jacobi diagonal, HOST [nloc][3][nt][nr] (1 on the non-unknown slots); for tests. */
 MASPCG_API maspcg_status maspcg_vv_get_diag(maspcg_ctx *ctx, double *D, void *cuda_stream);
 
+/* ---- field-aligned anisotropic conduction (reading R33 of DESIGN.md) ------------ */
+
+/* The thermal-conduction term of MAS's "full thermodynamic MHD model" (Sec. V-A) in its
+ * usual coronal form: heat flux -K grad T along the magnetic field, K = kappa_perp I + kappa_par b b^T
+ * (b a unit vector), on the cell-centred grid of the scalar operator (the paper gives no
+ * formula).  Volume-weighted symmetric form (R33): the 7-point operator of the DIAGONAL face coefficients
+ * K_aa = kappa_perp + kappa_par b_a^2 -- the caller passes them as kr, kt, kp to maspcg_set_coefficients
+ * (with the shift s as usual) -- plus CROSS terms kappa_par b_a b_b on the edges where an a-face meets a
+ * b-face, each the product of the two averaged face differences around the edge weighted by the exact
+ * volume between the four cell centres over the two metric distances.  19-point stencil; symmetric;
+ * constants in the kernel of the conduction part; b = r^ gives the radial 7-point operator; positive
+ * definite with an isotropic floor kappa_perp > 0 or a shift (semi-definite without them on uniform
+ * grids).  Only edges between two interior faces carry a cross term.  Solved by the same Jacobi PCG
+ * (R11-R14) on the three-kernel path (MASPCG_OPT_PATH 0 / 1; other paths and super-time-stepping
+ * return E_INVALID while cross terms are set), with the Jacobi diagonal including the cross terms.
+ *
+ * The cross terms live in their own caller-owned workspace (maspcg_aniso_workspace_bytes, 256-byte
+ * aligned; about 4 doubles per cell). */
+MASPCG_API size_t maspcg_aniso_workspace_bytes(const maspcg_ctx *ctx);
+MASPCG_API maspcg_status maspcg_aniso_set_workspace(maspcg_ctx *ctx, void *dev_ptr, size_t bytes);
+/* Cross coefficients kappa_par b_a b_b (any sign, finite) at the edge centres, DEVICE, consumed into the
+ * library's edge weights (the caller may free them afterwards):
+ *   krt [nloc][nt+1][nr+1]: edge (r-face ie, theta-face je) of plane k, at (r_f[ie], t_f[je], phi_c[k]);
+ *   krp [nloc][nt][nr+1]:   edge (r-face ie, row j) on phi-face k+1/2, at (r_f[ie], theta_c[j], p_f[k+1]);
+ *   ktp [nloc][nt+1][nr]:   edge (theta-face je, column i) on phi-face k+1/2, at (r_c[i], t_f[je], p_f[k+1]).
+ * Entries on boundary faces are read (validated) but carry no term.  All three NULL: back to the 7-point
+ * operator.  E_INVALID for a non-finite entry (agreed across ranks) or a partial set of NULLs; E_STATE
+ * before set_grid / set_workspace / aniso_set_workspace.  The Jacobi diagonal is rebuilt lazily. */
+MASPCG_API maspcg_status maspcg_set_aniso_coefficients(maspcg_ctx *ctx, const double *krt, const double *krp,
+                                                       const double *ktp, void *cuda_stream);
+/* Copy the edge weights Xq = X/4 and the 7-point diagonal D7 (host or device pointers, NULL skips) in the
+ * library's layout [nloc][nt][nr]: Xrt (lower r-face i, lower theta-face j), Xrp / Xtp (the phi-face k+1/2
+ * of plane k; lower r-face i / lower theta-face j); 0 where a face is a boundary face.  For tests. */
+MASPCG_API maspcg_status maspcg_aniso_get_operator(maspcg_ctx *ctx, double *Xrt, double *Xrp, double *Xtp,
+                                                   double *D7, void *cuda_stream);
+
 /* ---- peer-memory communicator (SURVEY 8(e) lever 4: in-kernel exchanges) ---------------------- */
 
 /* As maspcg_create, but the halo planes, all-gathers and flag all-reduces are kernels that store into

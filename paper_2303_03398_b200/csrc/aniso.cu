@@ -1,0 +1,262 @@
+// aniso.cu -- sm_100a kernels of the field-aligned anisotropic conduction operator (
+// reading R33 of DESIGN.md).  The operator: flux -K grad T, K = kappa_perp I + kappa_par b b^T, in the
+// volume-weighted energy form -- the 7-point operator of the diagonal face coefficients K_aa (the
+// caller's kr, kt, kp through the ordinary assembly) plus, on every edge between two interior faces of
+// directions a and b, the cross term X_e (a_e.T)(b_e.T) of kappa_par b_a b_b (19-point stencil).  The
+// thermal-conduction term of MAS's "full thermodynamic MHD model" (Sec. V-A) on its
+// "non-uniform staggered spherical grid" (Sec. III); the paper gives no formula.
+//
+// Arithmetic (bitwise equal to the CPU oracle of R33): the edge weights with one IEEE rounding
+// per operation in the order of the R33 formulas; per cell y = (D7 p - 7-point sum) + sum over the
+// cell's 12 edges, in the fixed R33 order, of Xq (s_a db + s_b da), da and db the sums of the edge's
+// two a- and b-differences.  Bandwidth: p (8, neighbours from L1/L2), T_r, T_theta, T_phi, D7 (32),
+// Xrt, Xrp, Xtp (24), y (8) = 72 B/cell of algorithmic traffic per apply.
+#include <cuda_runtime.h>
+
+#include "aniso.cuh"
+#include "arith.cuh"
+#include "common.cuh"
+#include "loopdev.cuh"
+#include "p2p_ll.cuh"
+
+namespace maspcg {
+
+namespace {
+
+constexpr int kAnisoBlocks = 4;   // resident blocks of 256 threads per SM (<= 64 registers)
+
+// ---------------------------------------------------------------- edge weights (setup)
+__global__ void __launch_bounds__(kThreads) k_aniso_edges(Dims d, DevArrays a, AnisoArrays x,
+                                                           const double *__restrict__ krt,
+                                                           const double *__restrict__ krp,
+                                                           const double *__restrict__ ktp) {
+    int bad = 0;
+    const int nr = d.nr, nt = d.nt;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        // r-theta edge (i, j) of plane k; the caller's krt row also holds the boundary edges i = nr, j = nt
+        const size_t ert = ((size_t)k * (nt + 1) + j) * (nr + 1) + i;
+        const double kq = krt[ert];
+        bad |= !isfinite(kq);
+        if (i == nr - 1) bad |= !isfinite(krt[ert + 1]);
+        if (j == nt - 1) {
+            bad |= !isfinite(krt[ert + nr + 1]);
+            if (i == nr - 1) bad |= !isfinite(krt[ert + nr + 2]);
+        }
+        x.Xrt[c] = (i >= 1 && j >= 1)
+                       ? __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(kq, x.gr[i]), x.gt[j]), a.dp[k]), 0.25)
+                       : 0.0;
+        // r-phi edge (i, row j) on face k+1/2 -> plane k+1
+        const size_t erp = ((size_t)k * nt + j) * (nr + 1) + i;
+        const double kp = krp[erp];
+        bad |= !isfinite(kp);
+        if (i == nr - 1) bad |= !isfinite(krp[erp + 1]);
+        x.Xrp[(size_t)c + d.plane] = (i >= 1) ? __dmul_rn(__dmul_rn(__dmul_rn(kp, x.gr[i]), x.cs[j]), 0.25) : 0.0;
+        // theta-phi edge (j, column i) on face k+1/2 -> plane k+1
+        const size_t etp = ((size_t)k * (nt + 1) + j) * nr + i;
+        const double kt = ktp[etp];
+        bad |= !isfinite(kt);
+        if (j == nt - 1) bad |= !isfinite(ktp[etp + nr]);
+        x.Xtp[(size_t)c + d.plane] = (j >= 1) ? __dmul_rn(__dmul_rn(__dmul_rn(kt, x.qr[i]), x.gts[j]), 0.25) : 0.0;
+    }
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0 && bad) atomicOr(&a.sc->vinvalid, 1);
+}
+
+// ---------------------------------------------------------------- Jacobi diagonal
+// diag(A) = D7 + sum over the 12 edges (R33 order) of Xq (2 s_a s_b); 2 s_a s_b Xq is exact (+-2 Xq).
+__global__ void __launch_bounds__(kThreads) k_aniso_diag(Dims d, DevArrays a, AnisoArrays x) {
+    const int nr = d.nr, nt = d.nt;
+    const size_t plane = d.plane;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < d.n; c += stride) {
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        double s = 0.0;
+        auto add = [&](double X, bool plus) { s = __dadd_rn(s, plus ? __dmul_rn(X, 2.0) : __dmul_rn(X, -2.0)); };
+        const size_t row = (size_t)j * nr;
+        const size_t pk = (size_t)k * plane;
+        // r-theta: (i, j) ++, (i+1, j) -+, (i, j+1) +-, (i+1, j+1) --
+        if (i >= 1 && j >= 1) add(x.Xrt[pk + row + i], true);
+        if (i + 1 <= nr - 1 && j >= 1) add(x.Xrt[pk + row + i + 1], false);
+        if (i >= 1 && j + 1 <= nt - 1) add(x.Xrt[pk + row + nr + i], false);
+        if (i + 1 <= nr - 1 && j + 1 <= nt - 1) add(x.Xrt[pk + row + nr + i + 1], true);
+        // r-phi: (i, lo) ++, (i+1, lo) -+, (i, hi) +-, (i+1, hi) --
+        const size_t lo = pk, hi = pk + plane;
+        if (i >= 1) add(x.Xrp[lo + row + i], true);
+        if (i + 1 <= nr - 1) add(x.Xrp[lo + row + i + 1], false);
+        if (i >= 1) add(x.Xrp[hi + row + i], false);
+        if (i + 1 <= nr - 1) add(x.Xrp[hi + row + i + 1], true);
+        // theta-phi: (j, lo) ++, (j+1, lo) -+, (j, hi) +-, (j+1, hi) --
+        if (j >= 1) add(x.Xtp[lo + row + i], true);
+        if (j + 1 <= nt - 1) add(x.Xtp[lo + row + nr + i], false);
+        if (j >= 1) add(x.Xtp[hi + row + i], false);
+        if (j + 1 <= nt - 1) add(x.Xtp[hi + row + nr + i], true);
+        const double d7 = a.D[c];
+        x.D7[c] = d7;
+        a.D[c] = __dadd_rn(d7, s);
+    }
+}
+
+// ---------------------------------------------------------------- operator apply (one cell per thread)
+template <bool EXACT>
+struct Cross {
+    double s = 0.0;
+    // one edge: Xq (s_a db + s_b da), da = (a1 - a0) + (b1 - b0), db = (b0' ...) given as the four values of the
+    // 2x2 block (u00 = lo a, lo b; u10 = hi a, lo b; u01 = lo a, hi b; u11 = hi a, hi b)
+    __device__ __forceinline__ void edge(double X, double u00, double u10, double u01, double u11, bool sa_plus,
+                                         bool sb_plus) {
+        const double da = __dadd_rn(__dsub_rn(u10, u00), __dsub_rn(u11, u01));   // the two a-differences
+        const double db = __dadd_rn(__dsub_rn(u01, u00), __dsub_rn(u11, u10));   // the two b-differences
+        const double v = __dadd_rn(sa_plus ? db : -db, sb_plus ? da : -da);
+        s = EXACT ? __dadd_rn(s, __dmul_rn(X, v)) : fma(X, v, s);
+    }
+};
+
+template <bool WITH_DOT, bool LOOP, bool EXACT>
+__global__ void __launch_bounds__(kThreads, kAnisoBlocks) k_aniso_flat(Dims d, DevArrays a, AnisoArrays x,
+                                                                       double *__restrict__ y, Range rg,
+                                                                       unsigned red_slot0, unsigned red_total) {
+    pdl_wait();
+    pdl_trigger();
+    if (LOOP && *(volatile int *)&a.sc->done) return;
+    if (LOOP && a.peer_wait) acquire_p_halo(a);
+    const bool coh = LOOP && a.peer_wait;   // peer-written halo planes: coherent loads (loopdev.cuh)
+    using A = Ar<EXACT>;
+    const double *__restrict__ p = a.p;
+    const int nr = d.nr, nt = d.nt, nloc = d.nloc;
+    const size_t plane = d.plane;
+    Acc<EXACT> dot[1];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < rg.vend; v += stride) {
+        const uint32_t c = v + rg.off0 + (v >= rg.split ? rg.off1 : 0u);
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        // p of local plane kk (-1 .. nloc, halo planes included), row jj, column ii
+        auto P = [&](int kk, int jj, int ii) -> double {
+            const double *q = p + (size_t)(kk + 1) * plane + (size_t)jj * nr + ii;
+            return (coh && (kk < 0 || kk >= nloc)) ? __ldcg(q) : __ldg(q);
+        };
+        const bool il = i > 0, ih = i < nr - 1, jl = j > 0, jh = j < nt - 1;
+        const double pc = P(k, j, i);
+        const double pim = il ? P(k, j, i - 1) : 0.0, pip = ih ? P(k, j, i + 1) : 0.0;
+        const double pjm = jl ? P(k, j - 1, i) : 0.0, pjp = jh ? P(k, j + 1, i) : 0.0;
+        const double pkm = P(k - 1, j, i), pkp = P(k + 1, j, i);
+        // the 7-point part, the oracle's order (r_lo, r_hi, t_lo, t_hi, p_lo, p_hi; D7 p - sum)
+        double s = 0.0;
+        if (il) s = A::acc(s, __ldg(a.Tr + c), pim);
+        if (ih) s = A::acc(s, __ldg(a.Tr + c + 1), pip);
+        if (jl) s = A::acc(s, __ldg(a.Tt + c), pjm);
+        if (jh) s = A::acc(s, __ldg(a.Tt + c + nr), pjp);
+        s = A::acc(s, __ldg(a.Tp + c), pkm);
+        s = A::acc(s, __ldg(a.Tp + c + plane), pkp);
+        const double y7 = A::diag_minus(__ldg(x.D7 + c), pc, s);
+        // the cross terms, R33 edge order
+        Cross<EXACT> cr;
+        const size_t pk = (size_t)k * plane, row = (size_t)j * nr;
+        // r-theta edges of plane k: a = r, b = theta
+        const double pjm_im = (jl && il) ? P(k, j - 1, i - 1) : 0.0, pjm_ip = (jl && ih) ? P(k, j - 1, i + 1) : 0.0;
+        const double pjp_im = (jh && il) ? P(k, j + 1, i - 1) : 0.0, pjp_ip = (jh && ih) ? P(k, j + 1, i + 1) : 0.0;
+        if (il && jl) cr.edge(__ldg(x.Xrt + pk + row + i), pjm_im, pjm, pim, pc, true, true);
+        if (ih && jl) cr.edge(__ldg(x.Xrt + pk + row + i + 1), pjm, pjm_ip, pc, pip, false, true);
+        if (il && jh) cr.edge(__ldg(x.Xrt + pk + row + nr + i), pim, pc, pjp_im, pjp, true, false);
+        if (ih && jh) cr.edge(__ldg(x.Xrt + pk + row + nr + i + 1), pc, pip, pjp, pjp_ip, false, false);
+        // r-phi edges of row j: a = r, b = phi; face k-1/2 (planes k-1, k: Xrp plane k), k+1/2 (k, k+1: plane k+1)
+        const double pkm_im = il ? P(k - 1, j, i - 1) : 0.0, pkm_ip = ih ? P(k - 1, j, i + 1) : 0.0;
+        const double pkp_im = il ? P(k + 1, j, i - 1) : 0.0, pkp_ip = ih ? P(k + 1, j, i + 1) : 0.0;
+        if (il) cr.edge(__ldg(x.Xrp + pk + row + i), pkm_im, pkm, pim, pc, true, true);
+        if (ih) cr.edge(__ldg(x.Xrp + pk + row + i + 1), pkm, pkm_ip, pc, pip, false, true);
+        if (il) cr.edge(__ldg(x.Xrp + pk + plane + row + i), pim, pc, pkp_im, pkp, true, false);
+        if (ih) cr.edge(__ldg(x.Xrp + pk + plane + row + i + 1), pc, pip, pkp, pkp_ip, false, false);
+        // theta-phi edges of column i: a = theta, b = phi
+        const double pkm_jm = jl ? P(k - 1, j - 1, i) : 0.0, pkm_jp = jh ? P(k - 1, j + 1, i) : 0.0;
+        const double pkp_jm = jl ? P(k + 1, j - 1, i) : 0.0, pkp_jp = jh ? P(k + 1, j + 1, i) : 0.0;
+        if (jl) cr.edge(__ldg(x.Xtp + pk + row + i), pkm_jm, pkm, pjm, pc, true, true);
+        if (jh) cr.edge(__ldg(x.Xtp + pk + row + nr + i), pkm, pkm_jp, pc, pjp, false, true);
+        if (jl) cr.edge(__ldg(x.Xtp + pk + plane + row + i), pjm, pc, pkp_jm, pkp, true, false);
+        if (jh) cr.edge(__ldg(x.Xtp + pk + plane + row + nr + i), pc, pjp, pkp, pkp_jp, false, false);
+        const double q = __dadd_rn(y7, cr.s);
+        y[c] = q;
+        if (WITH_DOT) dot[0].add(pc, q);
+    }
+    if (WITH_DOT) {
+        Acc<EXACT> out[1];
+        if (reduce_last<EXACT, kThreads, 1>(dot, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total,
+                                            out)) {
+            if (threadIdx.x == 0) {
+                a.sc->red1[0] = out[0].p;
+                a.sc->red1[1] = out[0].s;
+                if (a.p2p_ll) ll_push_pairs(a, a.sc->red1, 1);   // to every rank (peer communicator)
+            }
+        }
+    }
+}
+
+inline unsigned grid_aniso(uint32_t n) {
+    uint64_t g = (n + kThreads - 1) / kThreads;
+    if (g < 1) g = 1;
+    if (g > (uint64_t)(148 * kAnisoBlocks)) g = 148 * kAnisoBlocks;
+    return (unsigned)g;
+}
+
+inline unsigned grid_setup(uint32_t n) {
+    uint64_t g = (n + kThreads - 1) / kThreads;
+    if (g < 1) g = 1;
+    if (g > (uint64_t)kRedBlocks) g = kRedBlocks;
+    return (unsigned)g;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl_aniso(bool pdl, void (*kern)(KArgs...), unsigned grid, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+}  // namespace
+
+void launch_aniso_edges(const Dims &d, const DevArrays &a, const AnisoArrays &x, const double *krt, const double *krp,
+                        const double *ktp, cudaStream_t st) {
+    k_aniso_edges<<<grid_setup(d.n), kThreads, 0, st>>>(d, a, x, krt, krp, ktp);
+}
+
+void launch_aniso_diag(const Dims &d, const DevArrays &a, const AnisoArrays &x, cudaStream_t st) {
+    k_aniso_diag<<<grid_setup(d.n), kThreads, 0, st>>>(d, a, x);
+}
+
+unsigned aniso_stencil_blocks(const Dims &d, StencilPart part) {
+    const Range rg = make_range(d, part);
+    return rg.vend ? grid_aniso(rg.vend) : 0u;
+}
+
+void launch_aniso_matvec(const Dims &d, const DevArrays &a, const AnisoArrays &x, double *y, StencilPart part,
+                         bool with_dot, bool loop, unsigned red_slot0, unsigned red_total, bool exact, cudaStream_t st) {
+    const Range rg = make_range(d, part);
+    if (rg.vend == 0) return;
+    const unsigned g = grid_aniso(rg.vend);
+    const bool pdl = d.pdl != 0;
+#define AN(W, L, E) launch_pdl_aniso(pdl, k_aniso_flat<W, L, E>, g, st, d, a, x, y, rg, red_slot0, red_total)
+    if (exact) {
+        if (with_dot) {
+            if (loop) AN(true, true, true);
+            else AN(true, false, true);
+        } else AN(false, false, true);
+    } else {
+        if (with_dot) {
+            if (loop) AN(true, true, false);
+            else AN(true, false, false);
+        } else AN(false, false, false);
+    }
+#undef AN
+}
+
+}  // namespace maspcg

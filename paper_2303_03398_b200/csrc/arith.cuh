@@ -17,6 +17,12 @@
 
 namespace maspcg {
 
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void two_sum(double a, double b, double &x, double &y) {
     x = __dadd_rn(a, b);
     const double z = __dsub_rn(x, a);
@@ -137,12 +143,12 @@ __device__ __forceinline__ bool reduce_last(Acc<EXACT> (&v)[N], double *partials
             partials[(2 * k) * kPartialSlots + slot] = v[k].p;
             partials[(2 * k + 1) * kPartialSlots + slot] = v[k].s;
         }
-        __threadfence();
-        am_last = atomicAdd(ticket, 1u) == total - 1;
+        // release (this thread's partial stores) + acquire (every earlier block's, through the RMW chain
+        // of the ticket) in one atomic; the block barrier then orders the last block's loads after it
+        am_last = atom_add_acq_rel_gpu(ticket, 1u) == total - 1;
     }
     __syncthreads();
     if (!am_last) return false;
-    __threadfence();
     Acc<EXACT> acc[N];
 #pragma unroll
     for (int k = 0; k < N; ++k)

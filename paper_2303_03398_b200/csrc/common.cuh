@@ -118,6 +118,12 @@ struct Dims {
     float l2_frac;
 };
 
+// A launch range over local cells: v in [0, vend), cell c = v + off0 (+ off1 once v >= split), so one
+// kernel covers the interior planes or the two boundary planes of a slab.
+struct Range {
+    uint32_t vend, off0, split, off1;
+};
+
 // Array classes of Dims::l2_mask and their residency codes.
 enum : int { L2A_D = 0, L2A_P, L2A_R, L2A_X, L2A_Q, L2A_T, kL2Arrays };
 enum : uint32_t { L2_NORMAL = 0u, L2_KEEP = 1u, L2_KEEP_FRAC = 2u, L2_FIRST = 3u };

@@ -24,57 +24,17 @@
 #include "kernels.cuh"
 #include "arith.cuh"
 #include "p2p_ll.cuh"
+#include "loopdev.cuh"
 
 namespace maspcg {
 
 namespace {
-
-// Programmatic dependent launch (PDL): the loop kernels are launched with programmatic stream
-// serialisation, so the next kernel's blocks are scheduled onto SMs as this kernel's blocks retire
-// (hiding the launch latency and the reduction tail); griddepcontrol.wait then blocks until the
-// previous grid has completed and its memory is visible, before any dependent data is read.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void st_release_sys64(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-// peer mode: after a p-update that stored its boundary planes into the neighbours' halos, release them
-__device__ __forceinline__ void release_p_halo(const DevArrays &a) {
-    __threadfence_system();
-    const unsigned long long e = a.p2p->epoch[P2P_HALO] + 1;
-    a.p2p->epoch[P2P_HALO] = e;
-    st_release_sys64(a.peer_flag_hi, e);
-    st_release_sys64(a.peer_flag_lo, e);
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-// peer mode, loop stencil: wait until both neighbours have released this iteration's halo planes (stored
-// by their p-updates); every block waits before its first load, so no halo line is cached in L1 early
-__device__ __forceinline__ void acquire_p_halo(const DevArrays &a) {
-    if (threadIdx.x == 0) {
-        const unsigned long long e = *(volatile unsigned long long *)&a.p2p->epoch[P2P_HALO];
-        while (ld_acquire_sys64(&a.p2p->flags[P2P_FROM_LEFT][0]) < e) __nanosleep(32);
-        while (ld_acquire_sys64(&a.p2p->flags[P2P_FROM_RIGHT][0]) < e) __nanosleep(32);
-    }
-    __syncthreads();
-}
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 constexpr int kMinBlocks = kRedBlocks / 148;   // 8 resident blocks of 256 threads per SM (<= 32 registers)
 constexpr int kVecBlocks = 4;                   // vector kernels: 4 blocks of 256 threads per SM (<= 64 registers)
 constexpr int kMvBlocks = 5;                    // the vector stencil: 5 blocks per SM (<= 51 registers)
 static_assert(kPartialSlots >= 2 * kRedBlocks && kPartialSlots >= 2 * 148 * kMvBlocks,
               "a split stencil (interior + boundary launches) must fit the Dot2 partial slots");
-
-__device__ __forceinline__ void decompose(const Dims &d, uint32_t c, int &i, int &j, int &k) {
-    uint32_t row = d.div_r.div(c);
-    i = (int)(c - row * (uint32_t)d.nr);
-    uint32_t kk = d.div_t.div(row);
-    j = (int)(row - kk * (uint32_t)d.nt);
-    k = (int)kk;
-}
 
 // Write a freshly computed p value of local cell c (plane k) into the padded
 // p array and, on a single rank, into the periodic halo copies.
@@ -216,10 +176,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_fill_p(Dims d, DevArra
 // WITH_DOT: block partials of p.y -> last block writes sc->red1 (Dot2 pair).
 // LOOP: returns at entry once sc->done is set.
 // Sum order = the oracle's: r_lo, r_hi, theta_lo, theta_hi, phi_lo, phi_hi, then D p - sum.
-struct Range {
-    uint32_t vend, off0, split, off1;
-};
-
 template <bool WITH_DOT, bool LOOP, bool EXACT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_matvec_flat(Dims d, DevArrays a, double *__restrict__ y,
                                                                       Range rg, unsigned red_slot0,
@@ -451,13 +407,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArr
     __shared__ bool am_last;
     peer_st = __syncthreads_or(peer_st);   // only blocks that stored into a peer pay the system-scope fence
     if (threadIdx.x == 0) {
-        if (peer_st) __threadfence_system();
-        else __threadfence();
-        am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
+        if (peer_st) fence_acq_rel_sys();
+        am_last = atom_add_acq_rel_gpu(&sc->ticket[2], 1u) == total - 1;
     }
     __syncthreads();
     if (am_last && threadIdx.x == 0) {
-        __threadfence();
         if (a.peer_p_lo && !last) release_p_halo(a);
         const int it = sc->iter + 1;
         sc->iter = it;
@@ -487,56 +441,16 @@ __device__ __forceinline__ void st2(double *p, double a, double b) {
     *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
 
-// ---- L2 residency (Dims::l2_mask).  On a small slab (P = 4, 8) the loop's most-reused arrays fit the
-// 126 MB L2: loads and stores of a kept class carry an evict_last policy so they survive the streaming
-// of the others between kernels, and their HBM bytes drop out of the iteration -- the "super" scaling
-// of PAPER.md:277 (§V-C).  Policies are built per kernel entry (createpolicy, no memory access).
-__device__ __forceinline__ uint64_t l2_policy(const Dims &d, int cls) {
-    const uint32_t m = (d.l2_mask >> (2 * cls)) & 3u;
-    uint64_t pol;
-    if (m == L2_KEEP) asm("createpolicy.fractional.L2::evict_last.b64 %0, 0f3F800000;" : "=l"(pol));
-    else if (m == L2_KEEP_FRAC)
-        asm("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(d.l2_frac));
-    else if (m == L2_FIRST) asm("createpolicy.fractional.L2::evict_first.b64 %0, 0f3F800000;" : "=l"(pol));
-    else asm("createpolicy.fractional.L2::evict_normal.b64 %0, 0f3F800000;" : "=l"(pol));
-    return pol;
-}
-// read-only for the kernel's lifetime (non-coherent path)
-__device__ __forceinline__ double2 ld2h(const double *p, uint64_t pol) {
-    double2 v;
-    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ double ld1h(const double *p, uint64_t pol) {
-    double v;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
-// written by this kernel (coherent path; ordered against the stores by `volatile`)
-__device__ __forceinline__ double2 ld2rwh(const double *p, uint64_t pol) {
-    double2 v;
-    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol)
-                 : "memory");
-    return v;
-}
-// peer-written halo planes: stored over NVLink by a neighbour while this kernel may
-// already run, acquired by thread 0 + a block barrier -- read through L2 (ld.global.cg), never .nc
-__device__ __forceinline__ double2 ld2coh(const double *p) {
-    return __ldcg(reinterpret_cast<const double2 *>(p));
-}
-__device__ __forceinline__ void st2h(double *p, double a, double b, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(a), "d"(b), "l"(pol)
-                 : "memory");
-}
-
 template <bool WITH_DOT, bool LOOP, bool EXACT, bool MV2>
 __global__ void __launch_bounds__(kThreads, kMvBlocks) k_matvec_vec2(Dims d, DevArrays a, double *__restrict__ y,
                                                                       Range rg, unsigned red_slot0,
                                                                       unsigned red_total) {
     pdl_wait();
     pdl_trigger();
+    // peer mode: done is checked before the halo acquire (a finished solve releases no halo)
+    const bool pw = LOOP && a.peer_wait;
     if (LOOP && *(volatile int *)&a.sc->done) return;
-    if (LOOP && a.peer_wait) acquire_p_halo(a);
+    if (pw) acquire_p_halo(a);
     using A = Ar<EXACT>;
     const double *__restrict__ p = a.p;
     const double *__restrict__ Tr = a.Tr;
@@ -640,6 +554,20 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
     pdl_trigger();
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
+    double *__restrict__ r = a.r;
+    const uint64_t pol_r = l2_policy(d, L2A_R), pol_q = l2_policy(d, L2A_Q), pol_d = l2_policy(d, L2A_D);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = d.n >> 1;
+    uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    auto cell = [&](uint32_t ww) { return 2u * (rev ? npair - 1 - ww : ww); };
+    // The first trip's loads are issued BEFORE the scalars (done, p.q, rho): they do not depend on them,
+    // so their latency overlaps the scalar reads at kernel entry instead of following them.
+    const double2 z2 = make_double2(0.0, 0.0);
+    const bool two = UP2 && w + stride < npair, one = w < npair;
+    const uint32_t f0 = cell(one ? w : 0u), f1 = cell(two ? w + stride : 0u);
+    double2 rv0 = z2, qv0 = z2, dv0 = z2, rv1 = z2, qv1 = z2, dv1 = z2;
+    if (one) rv0 = ld2rwh(r + f0, pol_r), qv0 = ld2h(a.q + f0, pol_q), dv0 = ld2h(a.D + f0, pol_d);
+    if (two) rv1 = ld2rwh(r + f1, pol_r), qv1 = ld2h(a.q + f1, pol_q), dv1 = ld2h(a.D + f1, pol_d);
     if (*(volatile int *)&sc->done) return;
     const double pi = pair_value<EXACT>(a, sc->red1, 0, 1);
     if (!(pi > 0.0) || !isfinite(pi)) {
@@ -650,11 +578,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
         return;
     }
     const double alpha = __ddiv_rn(sc->rho, pi);
-    double *__restrict__ r = a.r;
-    const uint64_t pol_r = l2_policy(d, L2A_R), pol_q = l2_policy(d, L2A_Q), pol_d = l2_policy(d, L2A_D);
     Acc<EXACT> acc[2];
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t npair = d.n >> 1;
     auto body = [&](uint32_t c, double2 rv, double2 qv, double2 dv) {
         const double r0 = A::ymax(rv.x, alpha, qv.x), r1 = A::ymax(rv.y, alpha, qv.y);
         st2h(r + c, r0, r1, pol_r);
@@ -664,18 +588,26 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_update_vec2(Dims d, De
         acc[1].add(r0, r0);
         acc[1].add(r1, r1);
     };
-    uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (UP2) {   // two pairs per trip, loads first; the same per-thread order of the sums
-        for (; w + stride < npair; w += 2 * stride) {
-            const uint32_t c0 = 2u * (rev ? npair - 1 - w : w), c1 = 2u * (rev ? npair - 1 - (w + stride) : w + stride);
-            const double2 rv0 = ld2rwh(r + c0, pol_r), qv0 = ld2h(a.q + c0, pol_q), dv0 = ld2h(a.D + c0, pol_d);
-            const double2 rv1 = ld2rwh(r + c1, pol_r), qv1 = ld2h(a.q + c1, pol_q), dv1 = ld2h(a.D + c1, pol_d);
-            body(c0, rv0, qv0, dv0);
-            body(c1, rv1, qv1, dv1);
+    // the same per-thread order of the sums as a plain grid-stride loop (two pairs per trip, then one)
+    if (two) {
+        body(f0, rv0, qv0, dv0);
+        body(f1, rv1, qv1, dv1);
+        w += 2 * stride;
+        if (UP2) {
+            for (; w + stride < npair; w += 2 * stride) {
+                const uint32_t c0 = cell(w), c1 = cell(w + stride);
+                const double2 ra = ld2rwh(r + c0, pol_r), qa = ld2h(a.q + c0, pol_q), da = ld2h(a.D + c0, pol_d);
+                const double2 rb = ld2rwh(r + c1, pol_r), qb = ld2h(a.q + c1, pol_q), db = ld2h(a.D + c1, pol_d);
+                body(c0, ra, qa, da);
+                body(c1, rb, qb, db);
+            }
         }
+    } else if (one) {
+        body(f0, rv0, qv0, dv0);
+        w += stride;
     }
     for (; w < npair; w += stride) {
-        const uint32_t c = 2u * (rev ? npair - 1 - w : w);
+        const uint32_t c = cell(w);
         body(c, ld2rwh(r + c, pol_r), ld2h(a.q + c, pol_q), ld2h(a.D + c, pol_d));
     }
     Acc<EXACT> out[2];
@@ -698,6 +630,22 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
     pdl_trigger();
     using A = Ar<EXACT>;
     Scalars *sc = a.sc;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = d.n >> 1;
+    double *__restrict__ p = a.p;
+    const uint64_t pol_p = l2_policy(d, L2A_P), pol_x = l2_policy(d, L2A_X), pol_r = l2_policy(d, L2A_R);
+    const uint64_t pol_d = l2_policy(d, L2A_D);
+    // the first pair's four loads before the scalars (see k_update_vec2); r and D are read even in the
+    // last iteration, where p is not updated (harmless)
+    const double2 z2 = make_double2(0.0, 0.0);
+    uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool pre = !PU2 && v < npair;
+    double2 po_f = z2, xv_f = z2, rv_f = z2, dv_f = z2;
+    if (pre) {
+        const uint32_t c = 2u * v;
+        po_f = ld2rwh(p + (size_t)c + d.plane, pol_p), xv_f = ld2rwh(x + c, pol_x);
+        rv_f = ld2h(a.r + c, pol_r), dv_f = ld2h(a.D + c, pol_d);
+    }
     if (*(volatile int *)&sc->done) return;
     const double rz = pair_value<EXACT>(a, sc->red2, 0, 2);
     const double rr = pair_value<EXACT>(a, sc->red2, 1, 2);
@@ -708,11 +656,6 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
     const double alpha = sc->alpha;
     const double beta = last ? 0.0 : __ddiv_rn(rz, sc->rho);
     int peer_st = 0;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t npair = d.n >> 1;
-    double *__restrict__ p = a.p;
-    const uint64_t pol_p = l2_policy(d, L2A_P), pol_x = l2_policy(d, L2A_X), pol_r = l2_policy(d, L2A_R);
-    const uint64_t pol_d = l2_policy(d, L2A_D);
     auto store = [&](uint32_t c, double2 po, double2 xv, double2 rv, double2 dv) {
         st2h(x + c, A::axpy(alpha, po.x, xv.x), A::axpy(alpha, po.y, xv.y), pol_x);
         if (!last) {
@@ -728,8 +671,10 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
             }
         }
     };
-    const double2 z2 = make_double2(0.0, 0.0);
-    uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pre) {
+        store(2u * v, po_f, xv_f, rv_f, dv_f);
+        v += stride;
+    }
     if (PU2) {
         // two pairs per thread and trip: all eight 16-byte loads issued before the first store
         for (; v + stride < npair; v += 2 * stride) {
@@ -751,13 +696,11 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
     __shared__ bool am_last;
     peer_st = __syncthreads_or(peer_st);   // only blocks that stored into a peer pay the system-scope fence
     if (threadIdx.x == 0) {
-        if (peer_st) __threadfence_system();
-        else __threadfence();
-        am_last = atomicAdd(&sc->ticket[2], 1u) == total - 1;
+        if (peer_st) fence_acq_rel_sys();
+        am_last = atom_add_acq_rel_gpu(&sc->ticket[2], 1u) == total - 1;
     }
     __syncthreads();
     if (am_last && threadIdx.x == 0) {
-        __threadfence();
         if (a.peer_p_lo && !last) release_p_halo(a);
         const int it = sc->iter + 1;
         sc->iter = it;
@@ -938,7 +881,7 @@ void launch_fill_p(const Dims &d, const DevArrays &a, const double *x, cudaStrea
     k_fill_p<<<grid_for(d.n), kThreads, 0, st>>>(d, a, x);
 }
 
-static Range make_range(const Dims &d, StencilPart part) {
+Range make_range(const Dims &d, StencilPart part) {
     Range rg{};
     const uint32_t pl = d.plane;
     switch (part) {

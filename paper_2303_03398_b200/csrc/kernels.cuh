@@ -18,6 +18,8 @@ void launch_face_coeffs(const Dims &d, const double *f, const double *f_hi, cons
 void launch_finalize_D(const Dims &d, const DevArrays &a, int bc_in, int bc_out, cudaStream_t st);
 void launch_fill_p(const Dims &d, const DevArrays &a, const double *x, cudaStream_t st);
 
+// The cells of `part` of the local slab as a launch range.
+Range make_range(const Dims &d, StencilPart part);
 // Number of blocks launch_matvec uses for `part` (0: nothing to do).
 unsigned stencil_blocks(const Dims &d, StencilPart part, const double *y);
 // y = A p over `part` of the slab.  with_dot: partial p.y into partial slots

@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "fused.cuh"
 #include "kernels.cuh"
+#include "aniso.cuh"
 #include "persist.cuh"
 #include "vv.cuh"
 #include "wave.cuh"
@@ -81,6 +82,9 @@ struct maspcg_ctx {
                          // (MASPCG_OPT_FUSE_HALO)
     int l2_keep = 1;            // MASPCG_OPT_L2_KEEP: L2 residency plan of the three-kernel loop (plan_l2)
     size_t l2_bytes = 0;        // L2 capacity of the device
+    size_t l2_persist_max = 0;  // cudaDevAttrMaxPersistingL2CacheSize
+    size_t l2_persist_set = 0;  // the persisting set-aside this context requested (0: none)
+    size_t l2_plan_bytes = 0;   // bytes the current plan keeps
     uint32_t g_l2mask = 0;      // the plan the cached graphs were captured with
     float g_l2frac = 1.f;
     unsigned persist_grid = 0;   // path 5: co-resident grid of the persistent kernel
@@ -106,6 +110,14 @@ struct maspcg_ctx {
     Dims dv{};
     bool vv_coef_set = false, vv_bc_set = false, vv_dirty = true;
     int vmode = 0;
+
+    // field-aligned anisotropic conduction (NEXT-4, R33, aniso.cu): its own workspace and 1-D edge metric
+    std::vector<double> an_gr, an_qr, an_gt, an_cs, an_gts;
+    void *an_ws = nullptr;
+    size_t an_ws_bytes = 0;
+    AnisoArrays xa{};
+    bool an_on = false;              // the cross terms are set: solve / apply use the 19-point operator
+    bool an_metric_dirty = true;
 };
 
 #define SET_ERR(ctx, code, ...)                                              \
@@ -251,7 +263,8 @@ bool use_persist(const maspcg_ctx *c, const void *x) {
 int graph_key(const maspcg_ctx *c) {
     return (use_fused(c) ? 1 : 0) | (exact_arith(c) ? 2 : 0) | (c->use_tma ? 4 : 0) | (c->d.vec_ok ? 8 : 0) |
            (use_wave(c) ? 32 : 0) | (c->d.pdl ? 64 : 0) | (c->vmode ? 128 : 0) | (use_cg1(c) ? 256 : 0) |
-           (c->a.peer_p_lo ? 512 : 0) | (c->a.gather_ranks ? 1024 : 0) | (c->a.p2p_ll ? 2048 : 0);
+           (c->a.peer_p_lo ? 512 : 0) | (c->a.gather_ranks ? 1024 : 0) | (c->a.p2p_ll ? 2048 : 0) |
+           (c->an_on ? (1 << 14) : 0);
 }
 
 // Global value of `npairs` Dot2 (p, s) pairs: all-gather the ranks' pairs and combine them in rank
@@ -270,6 +283,29 @@ maspcg_status allreduce_dot2(maspcg_ctx *c, double *pairs, int npairs, cudaStrea
 }
 
 // ------------------------------------------------------------ vector viscosity (NEXT-2, vv.cu)
+// Workspace of the field-aligned operator (NEXT-4).  base == nullptr: only computes the size.
+size_t aniso_layout(const maspcg_ctx *c, char *base, AnisoArrays *out) {
+    const size_t n = (size_t)c->nloc * c->nt * c->nr, plane = (size_t)c->nt * c->nr;
+    size_t off = 0;
+    auto take = [&](size_t count) -> double * {
+        double *p = base ? (double *)(base + off) : nullptr;
+        off = align_up(off + 8 * count, 256);
+        return p;
+    };
+    AnisoArrays t{};
+    t.Xrt = take(n);
+    t.Xrp = take(n + plane);
+    t.Xtp = take(n + plane);
+    t.D7 = take(n);
+    t.gr = take(c->nr);
+    t.qr = take(c->nr);
+    t.gt = take(c->nt);
+    t.cs = take(c->nt);
+    t.gts = take(c->nt);
+    if (out) *out = t;
+    return off;
+}
+
 size_t vv_layout(const maspcg_ctx *c, char *base, VVArrays *out) {
     const size_t nr = c->nr, nt = c->nt, nloc = c->nloc, pl1 = nt * nr;
     size_t off = 0;
@@ -409,16 +445,24 @@ maspcg_status vv_stencil(maspcg_ctx *c, double *y, bool with_dot, bool loop, cud
 // the caller's stream; joins before the boundary planes.
 cudaError_t record_timing(maspcg_ctx *c, int kern, int which, int it, cudaStream_t st);
 
+// The operator's stencil over `part`: the 7-point kernels, or the 19-point field-aligned one (NEXT-4).
+unsigned op_blocks(const maspcg_ctx *c, StencilPart part, const double *y) {
+    return c->an_on ? aniso_stencil_blocks(c->d, part) : stencil_blocks(c->d, part, y);
+}
+void op_matvec(const maspcg_ctx *c, const Dims &d, double *y, StencilPart part, bool with_dot, bool loop,
+               unsigned slot0, unsigned total, cudaStream_t st) {
+    if (c->an_on) launch_aniso_matvec(d, c->a, c->xa, y, part, with_dot, loop, slot0, total, exact_arith(c), st);
+    else launch_matvec(d, c->a, y, part, with_dot, loop, slot0, total, exact_arith(c), st);
+}
+
 maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool loop, cudaStream_t st, int tslot = -1) {
     if (c->vmode) return vv_stencil(c, y, with_dot, loop, st);
     if (!c->comm) {
-        launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
-                      stencil_blocks(c->d, StencilPart::Full, y), exact_arith(c), st);
+        op_matvec(c, c->d, y, StencilPart::Full, with_dot, loop, 0, op_blocks(c, StencilPart::Full, y), st);
         return MASPCG_OK;
     }
     if (loop && c->a.peer_wait) {   // the stencil acquires the pushed halo planes itself
-        launch_matvec(c->d, c->a, y, StencilPart::Full, with_dot, loop, 0,
-                      stencil_blocks(c->d, StencilPart::Full, y), exact_arith(c), st);
+        op_matvec(c, c->d, y, StencilPart::Full, with_dot, loop, 0, op_blocks(c, StencilPart::Full, y), st);
         return MASPCG_OK;
     }
     CK(c, cudaEventRecord(c->ev_p, st));
@@ -430,17 +474,18 @@ maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool lo
         RET_IF(halo_padded(c, c->a.p, c->comm_stream));
     if (tslot >= 0) CK(c, record_timing(c, 5, 1, tslot, c->comm_stream));
     CK(c, cudaEventRecord(c->ev_halo, c->comm_stream));
-    const unsigned gi = stencil_blocks(c->d, StencilPart::Interior, y);
-    const unsigned gb = stencil_blocks(c->d, StencilPart::Boundary, y);
-    // The interior launch without programmatic dependent launch (MASPCG_INTERIOR_PDL=0, default): with PDL
-    // its blocks become resident while the previous p-update still runs and hold every SM slot, so the
-    // exchange kernel on the comm stream cannot start until the interior stencil retires.
-    static const int ipdl = getenv("MASPCG_INTERIOR_PDL") ? atoi(getenv("MASPCG_INTERIOR_PDL")) : 0;
+    const unsigned gi = op_blocks(c, StencilPart::Interior, y);
+    const unsigned gb = op_blocks(c, StencilPart::Boundary, y);
+    // MASPCG_INTERIOR_PDL=0 launches the interior planes without programmatic dependent launch (its blocks
+    // then do not occupy the SMs while the p-update still runs, leaving room for the exchange kernel):
+    // measured slower on the P = 8 slab of c3 with the one-rank NCCL communicator (92.6 vs 91.4 us), so
+    // PDL stays on.
+    static const int ipdl = getenv("MASPCG_INTERIOR_PDL") ? atoi(getenv("MASPCG_INTERIOR_PDL")) : 1;
     Dims di = c->d;
     if (!ipdl) di.pdl = 0;
-    launch_matvec(di, c->a, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, exact_arith(c), st);
+    op_matvec(c, di, y, StencilPart::Interior, with_dot, loop, 0, gi + gb, st);
     CK(c, cudaStreamWaitEvent(st, c->ev_halo, 0));
-    launch_matvec(c->d, c->a, y, StencilPart::Boundary, with_dot, loop, gi, gi + gb, exact_arith(c), st);
+    op_matvec(c, c->d, y, StencilPart::Boundary, with_dot, loop, gi, gi + gb, st);
     return MASPCG_OK;
 }
 
@@ -452,6 +497,7 @@ maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
         SET_ERR(c, MASPCG_E_SINGULAR, "shift is zero everywhere and no r boundary is Dirichlet: A is singular");
     launch_finalize_D(c->d, c->a, c->bc_in, c->bc_out, st);
     CK(c, cudaGetLastError());
+    if (c->an_on) launch_aniso_diag(c->d, c->a, c->xa, st);   // D7 kept for the stencil, D = Jacobi diagonal
     if (c->comm) RET_IF(halo_planes(c, c->a.D, c->a.dh, st));   // D of the neighbours' boundary planes
     c->D_dirty = false;
     return MASPCG_OK;
@@ -751,33 +797,50 @@ int l2_ranges(const maspcg_ctx *c, const double *x, L2Range out[8]) {
 void plan_l2(maspcg_ctx *c, const double *x) {
     c->d.l2_mask = 0u;
     c->d.l2_frac = 1.f;
-    if (!c->l2_keep || c->vmode || use_fused(c) || use_cg1(c) || use_wave(c) || use_persist(c, x)) return;
+    c->l2_plan_bytes = 0;
+    if (!c->l2_keep || c->vmode || c->an_on || use_fused(c) || use_cg1(c) || use_wave(c) || use_persist(c, x)) return;
     if (!c->d.vec_ok || (c->nr % 2) || ((uintptr_t)x & 15)) return;   // the 16-byte kernels carry the hints
-    if (const char *e = getenv("MASPCG_L2_MASK")) {
+    const double n8 = 8.0 * c->d.n, pl8 = 8.0 * c->d.plane;
+    if (const char *e = getenv("MASPCG_L2_MASK")) {   // explicit plan (A/B runs)
         c->d.l2_mask = (uint32_t)strtoul(e, nullptr, 0);
         if (const char *f = getenv("MASPCG_L2_FRAC")) c->d.l2_frac = (float)atof(f);
+        c->l2_plan_bytes = c->l2_persist_max;
         return;
     }
     double budget = 0.75;
     if (const char *e = getenv("MASPCG_L2_BUDGET")) budget = atof(e);
-    const double n8 = 8.0 * c->d.n, pl8 = 8.0 * c->d.plane;
+    double cap = budget * (double)c->l2_bytes;
+    // evict_last lines are retained only inside the persisting set-aside of the L2
+    // (cudaLimitPersistingL2CacheSize); the plan cannot keep more than the device allows there
+    if (c->l2_persist_max && cap > (double)c->l2_persist_max) cap = (double)c->l2_persist_max;
+    // Whole classes only, greedily: a partly kept class (fractional policy) and a set-aside larger than the
+    // kept bytes both measured slower than no plan (the set-aside shrinks the L2 left to the streams).
     const struct {
         int cls;
         double bytes;
-    } order[] = {{L2A_D, n8}, {L2A_P, n8 + 2 * pl8}, {L2A_R, n8}, {L2A_X, n8}, {L2A_Q, n8}, {L2A_T, 3 * n8 + pl8}};
-    double left = budget * (double)c->l2_bytes;
+    } order[] = {{L2A_D, n8}, {L2A_P, n8 + 2 * pl8}, {L2A_R, n8}, {L2A_X, n8}, {L2A_Q, n8}};
+    double kept = 0.0;
     for (const auto &o : order) {
-        if (o.bytes <= left) {
-            c->d.l2_mask |= L2_KEEP << (2 * o.cls);
-            left -= o.bytes;
-            continue;
-        }
-        if (left >= 0.05 * o.bytes) {
-            c->d.l2_mask |= L2_KEEP_FRAC << (2 * o.cls);
-            c->d.l2_frac = (float)(left / o.bytes);
-        }
-        break;
+        if (kept + o.bytes > cap) break;
+        c->d.l2_mask |= L2_KEEP << (2 * o.cls);
+        kept += o.bytes;
     }
+    c->l2_plan_bytes = (size_t)kept;
+    if (getenv("MASPCG_L2_VERBOSE"))
+        fprintf(stderr, "maspcg l2 plan: mask 0x%x kept %.1f MB (L2 %.1f MB, persisting max %.1f MB)\n",
+                c->d.l2_mask, kept / 1e6, c->l2_bytes / 1e6, c->l2_persist_max / 1e6);
+}
+
+// The persisting set-aside for a plan: exactly its kept bytes (device-wide limit; released at destroy).
+void l2_setaside(maspcg_ctx *c) {
+    if (!c->d.l2_mask) return;
+    const char *e = getenv("MASPCG_L2_PERSIST");
+    if (e && !atoi(e)) return;
+    size_t want = c->l2_plan_bytes;
+    if (c->l2_persist_max && want > c->l2_persist_max) want = c->l2_persist_max;
+    if (!want || c->l2_persist_set == want) return;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) c->l2_persist_set = want;
+    else cudaGetLastError();
 }
 
 maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol, int maxit, double *hist,
@@ -789,6 +852,8 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     if (maxit < 0) SET_ERR(c, MASPCG_E_INVALID, "maxit must be >= 0");
     if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
     RET_IF(c->vmode ? ensure_vv(c, st) : ensure_D(c, st));
+    if (c->an_on && !c->vmode && (use_fused(c) || use_cg1(c) || use_wave(c) || use_persist(c, x)))
+        SET_ERR(c, MASPCG_E_INVALID, "the field-aligned operator runs on the three-kernel path (MASPCG_OPT_PATH 0 or 1)");
     const bool fused = use_fused(c);
     if (fused && c->ptab)
         SET_ERR(c, MASPCG_E_INVALID, "the fused path (2) is not available with the peer-memory communicator");
@@ -857,6 +922,7 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
     CK(c, cudaGetLastError());
     long long launched = 4 + (c->comm ? 1 : 0);
     plan_l2(c, x);
+    l2_setaside(c);
 
     // PCG loop: chunks of `chunk` iterations, one speculative chunk in flight.
     CK(c, cudaMemcpyAsync(c->snap[0], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
@@ -1067,9 +1133,11 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     c->d.vec_ok = 1;
     c->d.pdl = 1;
     {
-        int l2 = 0;
+        int l2 = 0, pmax = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, cuda_device);
+        cudaDeviceGetAttribute(&pmax, cudaDevAttrMaxPersistingL2CacheSize, cuda_device);
         c->l2_bytes = (size_t)(l2 > 0 ? l2 : 0);
+        c->l2_persist_max = (size_t)(pmax > 0 ? pmax : 0);
     }
     c->fused_bj = fused_bj(nr, nt);   // 0: nr too large for one register batch per thread -> three kernels
     if (c->fused_bj > 0) {
@@ -1142,6 +1210,10 @@ maspcg_status maspcg_destroy(maspcg_ctx *c) {
         if (c->snap[b]) cudaFreeHost(c->snap[b]);
     }
     if (c->vflags_host) cudaFreeHost(c->vflags_host);
+    if (c->l2_persist_set) {   // release the persisting L2 set-aside this context requested
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    }
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     delete c;
@@ -1207,6 +1279,21 @@ maspcg_status maspcg_set_grid(maspcg_ctx *c, const double *rf, const double *tf,
     hpg[np - 1] = (pc[0] + kTwoPi) - pc[np - 1];
     c->dp_loc.assign(dpg.begin() + c->k0, dpg.begin() + c->k0 + c->nloc);
     c->hp_loc.assign(hpg.begin() + c->k0, hpg.begin() + c->k0 + c->nloc);
+
+    // field-aligned conduction edge metric (NEXT-4, R33): the expressions of reading R33
+    c->an_gr.assign(nr, 0.0);
+    c->an_qr.assign(nr, 0.0);
+    c->an_gt.assign(nt, 0.0);
+    c->an_cs.assign(nt, 0.0);
+    c->an_gts.assign(nt, 0.0);
+    for (int i = 1; i < nr; ++i) c->an_gr[i] = (rc[i] * rc[i] + rc[i] * rc[i - 1] + rc[i - 1] * rc[i - 1]) / (3.0 * rf[i]);
+    for (int i = 0; i < nr; ++i) c->an_qr[i] = c->R3[i] / (rc[i] * rc[i]);
+    for (int j = 1; j < nt; ++j) {
+        c->an_gt[j] = 2.0 * std::sin(0.5 * (tc[j - 1] + tc[j])) * std::sin(0.5 * c->ht[j]) / c->ht[j];
+        c->an_gts[j] = c->an_gt[j] / c->sinf[j];
+    }
+    for (int j = 0; j < nt; ++j) c->an_cs[j] = 2.0 * std::sin(0.5 * c->dt[j]);
+    c->an_metric_dirty = true;
 
     // vector-viscosity metric (NEXT-2, R27): the expressions of the vector oracle's grid
     c->vv_grid_ok = (tf[0] == 0.0 && std::fabs(tf[nt] - kPi) <= 1e-12 && np >= 2) ? 1 : 0;
@@ -1475,6 +1562,7 @@ maspcg_status maspcg_sts_step(maspcg_ctx *c, double *u, double tau, int stages, 
     if (!c) return MASPCG_E_INVALID;
     if (!u) SET_ERR(c, MASPCG_E_INVALID, "u must be non-NULL");
     if (stages < 2 || stages > 4096) SET_ERR(c, MASPCG_E_INVALID, "stages must be in [2, 4096]");
+    if (c->an_on) SET_ERR(c, MASPCG_E_INVALID, "super-time-stepping uses the 7-point operator (aniso set)");
     if (!(tau > 0.0) || !std::isfinite(tau)) SET_ERR(c, MASPCG_E_INVALID, "tau must be finite and > 0");
     if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
     RET_IF(bind_device(c));
@@ -1512,6 +1600,7 @@ maspcg_status maspcg_sts_step(maspcg_ctx *c, double *u, double tau, int stages, 
 
 maspcg_status maspcg_sts_dt_limit(maspcg_ctx *c, double *dt_fe, void *stream) {
     if (!c || !dt_fe) return MASPCG_E_INVALID;
+    if (c->an_on) SET_ERR(c, MASPCG_E_INVALID, "super-time-stepping uses the 7-point operator (aniso set)");
     if (!c->ws) SET_ERR(c, MASPCG_E_STATE, "no workspace");
     RET_IF(bind_device(c));
     cudaStream_t st = (cudaStream_t)stream;
@@ -1721,6 +1810,89 @@ maspcg_status maspcg_peer_import(maspcg_ctx *c, int region, int rank, const void
     if (c->ptab->mapping[region][rank]) peer_close(c->ptab->mapping[region][rank]);
     c->ptab->mapping[region][rank] = map;
     c->ptab->base[region][rank] = base;
+    return MASPCG_OK;
+}
+
+// ---------------------------------------------------------------- field-aligned conduction (NEXT-4)
+size_t maspcg_aniso_workspace_bytes(const maspcg_ctx *c) { return c ? aniso_layout(c, nullptr, nullptr) : 0; }
+
+maspcg_status maspcg_aniso_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!dev_ptr || ((uintptr_t)dev_ptr & 255)) SET_ERR(c, MASPCG_E_INVALID, "workspace must be 256-byte aligned");
+    const size_t need = aniso_layout(c, nullptr, nullptr);
+    if (bytes < need) SET_ERR(c, MASPCG_E_NOMEM, "aniso workspace too small: %zu < %zu bytes", bytes, need);
+    RET_IF(bind_device(c));
+    c->an_ws = dev_ptr;
+    c->an_ws_bytes = bytes;
+    aniso_layout(c, (char *)dev_ptr, &c->xa);
+    c->an_on = false;
+    c->an_metric_dirty = true;
+    c->D_dirty = true;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_set_aniso_coefficients(maspcg_ctx *c, const double *krt, const double *krp, const double *ktp,
+                                            void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!krt && !krp && !ktp) {   // back to the 7-point operator
+        c->an_on = false;
+        c->D_dirty = true;
+        return MASPCG_OK;
+    }
+    if (!krt || !krp || !ktp) SET_ERR(c, MASPCG_E_INVALID, "krt, krp, ktp must all be given (or all NULL)");
+    if (!c->grid_set || !c->ws || !c->an_ws)
+        SET_ERR(c, MASPCG_E_STATE, "set_grid, set_workspace and aniso_set_workspace must precede set_aniso_coefficients");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_metric(c, st));
+    if (c->an_metric_dirty) {
+        auto up = [&](double *dst, const std::vector<double> &v) {
+            return cudaMemcpyAsync(dst, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, st);
+        };
+        CK(c, up(c->xa.gr, c->an_gr));
+        CK(c, up(c->xa.qr, c->an_qr));
+        CK(c, up(c->xa.gt, c->an_gt));
+        CK(c, up(c->xa.cs, c->an_cs));
+        CK(c, up(c->xa.gts, c->an_gts));
+    }
+    CK(c, cudaMemsetAsync(&c->a.sc->vinvalid, 0, sizeof(int), st));
+    launch_aniso_edges(c->d, c->a, c->xa, krt, krp, ktp, st);
+    CK(c, cudaGetLastError());
+    const size_t pl = c->d.plane, last = (size_t)c->nloc * pl;
+    if (!c->comm) {   // face (np-1)+1/2 is the lower phi face of plane 0 (periodic, R9)
+        CK(c, cudaMemcpyAsync(c->xa.Xrp, c->xa.Xrp + last, 8 * pl, cudaMemcpyDeviceToDevice, st));
+        CK(c, cudaMemcpyAsync(c->xa.Xtp, c->xa.Xtp + last, 8 * pl, cudaMemcpyDeviceToDevice, st));
+    } else {   // the face below plane 0 is the last face of the left neighbour's slab
+        COMM(c, c->comm->shift_right(c->xa.Xrp + last, c->xa.Xrp, pl, st, c->err));
+        COMM(c, c->comm->shift_right(c->xa.Xtp + last, c->xa.Xtp, pl, st, c->err));
+        COMM(c, c->comm->allreduce_max(&c->a.sc->vinvalid, 1, st, c->err));
+    }
+    CK(c, cudaMemcpyAsync(c->vflags_host, &c->a.sc->vinvalid, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));   // host metric vectors may change with the next set_grid
+    c->an_metric_dirty = false;
+    c->stats.kernel_launches += 1;
+    c->D_dirty = true;
+    if (c->vflags_host[0]) {
+        c->an_on = false;
+        SET_ERR(c, MASPCG_E_INVALID, "an edge coefficient is non-finite");
+    }
+    c->an_on = true;
+    return MASPCG_OK;
+}
+
+maspcg_status maspcg_aniso_get_operator(maspcg_ctx *c, double *Xrt, double *Xrp, double *Xtp, double *D7,
+                                        void *stream) {
+    if (!c) return MASPCG_E_INVALID;
+    if (!c->an_on) SET_ERR(c, MASPCG_E_STATE, "no field-aligned coefficients set");
+    RET_IF(bind_device(c));
+    cudaStream_t st = (cudaStream_t)stream;
+    RET_IF(ensure_D(c, st));
+    const size_t n = (size_t)c->nloc * c->nt * c->nr, pl = (size_t)c->nt * c->nr;
+    if (Xrt) CK(c, cudaMemcpyAsync(Xrt, c->xa.Xrt, 8 * n, cudaMemcpyDefault, st));
+    if (Xrp) CK(c, cudaMemcpyAsync(Xrp, c->xa.Xrp + pl, 8 * n, cudaMemcpyDefault, st));
+    if (Xtp) CK(c, cudaMemcpyAsync(Xtp, c->xa.Xtp + pl, 8 * n, cudaMemcpyDefault, st));
+    if (D7) CK(c, cudaMemcpyAsync(D7, c->xa.D7, 8 * n, cudaMemcpyDefault, st));
+    CK(c, cudaStreamSynchronize(st));
     return MASPCG_OK;
 }
 

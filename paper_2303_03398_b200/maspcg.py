@@ -94,6 +94,10 @@ SIGNATURES = {
     "maspcg_vv_apply": ([_V, _V, _V, _V], _I),
     "maspcg_vv_solve": ([_V, _V, _V, _D, _I, _V, ctypes.POINTER(Info), _V], _I),
     "maspcg_vv_get_diag": ([_V, _V, _V], _I),
+    "maspcg_aniso_workspace_bytes": ([_V], _SZ),
+    "maspcg_aniso_set_workspace": ([_V, _V, _SZ], _I),
+    "maspcg_set_aniso_coefficients": ([_V, _V, _V, _V, _V], _I),
+    "maspcg_aniso_get_operator": ([_V, _V, _V, _V, _V, _V], _I),
     "maspcg_create_peer": ([_I, _I, _I, _I, _I, _V, _I, ctypes.POINTER(_V)], _I),
     "maspcg_peer_export": ([_V, _I, _V], _I),
     "maspcg_peer_import": ([_V, _I, _I, _V], _I),
@@ -333,6 +337,29 @@ class Solver:
                                                 _stream(stream)))
         return Tr, Tt, Tp, D
 
+    # ---------------------------------------------------------------- field-aligned conduction (NEXT-4)
+    def aniso_enable(self):
+        """Allocate and attach the cross terms' workspace (maspcg_aniso_workspace_bytes / _set_workspace)."""
+        import torch
+        if getattr(self, "aniso_workspace", None) is not None:
+            return
+        nbytes = self._L.maspcg_aniso_workspace_bytes(self.ctx)
+        self.aniso_workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        base = self.aniso_workspace.data_ptr()
+        self._check(self._L.maspcg_aniso_set_workspace(self.ctx, base + (-base) % 256, nbytes))
+
+    def set_aniso_coefficients(self, krt, krp, ktp, stream=None):
+        """maspcg_set_aniso_coefficients: edge cross coefficients kappa_par b_a b_b (device tensors
+        [nloc][nt+1][nr+1], [nloc][nt][nr+1], [nloc][nt+1][nr]); all None: back to the 7-point operator."""
+        self.aniso_enable()
+        self._check(self._L.maspcg_set_aniso_coefficients(self.ctx, _ptr(krt), _ptr(krp), _ptr(ktp), _stream(stream)))
+
+    def aniso_get_operator(self, stream=None):
+        """maspcg_aniso_get_operator: (Xrt, Xrp, Xtp, D7) in the library layout [nloc][nt][nr] (host copies)."""
+        out = [np.empty(self.local_shape) for _ in range(4)]
+        self._check(self._L.maspcg_aniso_get_operator(self.ctx, *(_ptr(a) for a in out), _stream(stream)))
+        return tuple(out)
+
     # ---------------------------------------------------------------- vector viscosity (NEXT-2)
     @property
     def vv_local_shape(self):
@@ -426,4 +453,6 @@ def solver_for_problem(prob, *, group=None, device=None, chunk=16, stream=None, 
     S.set_bc_r(prob.bc_in, T(prob.g_in), prob.bc_out, T(prob.g_out), stream) if (
         prob.g_in is not None or prob.g_out is not None) else S.set_bc_r(prob.bc_in, None, prob.bc_out, None,
                                                                            stream)
+    if getattr(prob, "krt", None) is not None:   # field-aligned conduction (inputs.AnisoProblem)
+        S.set_aniso_coefficients(T(prob.krt), T(prob.krp), T(prob.ktp), stream)
     return S
