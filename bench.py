@@ -104,6 +104,9 @@ CONFIG_INFO = {
     "c3": ("configs[2]", "coronal-relaxation-shaped viscosity solve"),
     "c4": ("configs[3]", "weak-scaling per-GPU slab, high-contrast thermal-conduction coefficients"),
     "c5": ("configs[4]", "repeated warm-started implicit solves of a time loop (paper-sized grid)"),
+    "c1a": ("configs[0] grid", "field-aligned thermal conduction (SURVEY 8(f) NEXT-4), 19-point operator"),
+    "c2a": ("configs[1] grid", "field-aligned thermal conduction (SURVEY 8(f) NEXT-4), 19-point operator"),
+    "c3a": ("configs[2] grid", "field-aligned thermal conduction (SURVEY 8(f) NEXT-4), 19-point operator"),
 }
 
 
@@ -234,7 +237,11 @@ def oracle_sample(prob, iters: int, openmp: bool = False):
     import oracle
     oracle.use_openmp(openmp)
     t0 = time.perf_counter()
-    op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
+    if getattr(prob, "krt", None) is not None:   # field-aligned conduction (NEXT-4)
+        op = oracle.AnisoOperator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in,
+                                  prob.bc_out, prob.krt, prob.krp, prob.ktp)
+    else:
+        op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
     b = op.rhs(prob.f, prob.g_in, prob.g_out)
     t1 = time.perf_counter()
     op.pcg(b, prob.x0, 0.0, 0)
@@ -444,10 +451,17 @@ def run_reference(args):
     oracle.build(openmp=True)
     oracle.use_openmp(True)
     shape = tuple(int(v) for v in args.shape.split(",")) if args.shape else None
-    prob = inputs.make_problem(args.config, shape=shape)
+    aniso = args.operator == "aniso"
+    if aniso:
+        args.config = args.config if args.config in inputs.ANISO_CONFIGS else "c3a"
+        prob = inputs.make_aniso_problem(args.config, shape=shape)
+        op = oracle.AnisoOperator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in,
+                                  prob.bc_out, prob.krt, prob.krp, prob.ktp)
+    else:
+        prob = inputs.make_problem(args.config, shape=shape)
+        op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
     tol = 0.0 if args.maxit else prob.tol
     maxit = args.maxit if args.maxit else prob.maxit
-    op = oracle.Operator(prob.rf, prob.tf, prob.pf, prob.kr, prob.kt, prob.kp, prob.s, prob.bc_in, prob.bc_out)
     b = op.rhs(prob.f, prob.g_in, prob.g_out)
     m = args.ref_iters
     for _ in range(args.warmup):
@@ -549,9 +563,10 @@ def main():
     ap.add_argument("--vec", type=int, default=1, help="three-kernel path: 1 16-byte vector kernels (nr even), 0 scalar")
     ap.add_argument("--arith", type=int, default=0, help="0 oracle-identical (Dot2, no FMA), 1 fast (FMA)")
     ap.add_argument("--tma", type=int, default=0, help="fused pass A: 1 TMA-staged (nr even), 0 register batches")
-    ap.add_argument("--operator", default="scalar", choices=["scalar", "vv"],
+    ap.add_argument("--operator", default="scalar", choices=["scalar", "vv", "aniso"],
                     help="scalar: the 7-point parabolic solve (default); vv: the staggered vector viscosity "
-                         "(NEXT-2) on the c3 grid (config c3v)")
+                         "(NEXT-2) on the c3 grid (config c3v); aniso: field-aligned thermal conduction "
+                         "(NEXT-4, the 19-point operator) on the c3 grid (config c3a)")
     args = ap.parse_args()
     self_launch(args)
     protect_stdout()
@@ -575,18 +590,25 @@ def main():
     dev = torch.device(f"cuda:{local}")
 
     # ---- synthetic input of this rank's slab (decomposition-independent generator)
-    nr, nt, np_ = inputs.CONFIGS[args.config]
+    aniso = args.operator == "aniso"
+    if aniso and args.config not in inputs.ANISO_CONFIGS:
+        args.config = "c3a"
+    nr, nt, np_ = (inputs.ANISO_CONFIGS if aniso else inputs.CONFIGS)[args.config]
     shape = tuple(int(v) for v in args.shape.split(",")) if args.shape else None
     if shape:
         nr, nt, np_ = shape
     if args.config == "c4" and not shape:
         np_ *= world
     k0, nloc = inputs.slab_extent(np_, rank, world)
-    prob = inputs.make_problem(args.config, k0, nloc, nranks=world, shape=shape)
+    if aniso:
+        prob = inputs.make_aniso_problem(args.config, k0, nloc, shape=shape)
+    else:
+        prob = inputs.make_problem(args.config, k0, nloc, nranks=world, shape=shape)
     tol = 0.0 if args.maxit else prob.tol
     maxit = args.maxit if args.maxit else prob.maxit
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     kr, kt, kp, s, f, x0 = (T(a) for a in (prob.kr, prob.kt, prob.kp, prob.s, prob.f, prob.x0))
+    krt, krp, ktp = (T(a) for a in (prob.krt, prob.krp, prob.ktp)) if aniso else (None, None, None)
 
     rho_cells = None
     if args.from_fields:
@@ -616,6 +638,8 @@ def main():
             S.set_coefficients_from_fields(rho_cells, 1e-3, 2, maspcg.MEAN_ARITHMETIC, rho_cells, 1.0 / 1e-2)
         else:
             S.set_coefficients(kr, kt, kp, s)                         # a2
+        if aniso:
+            S.set_aniso_coefficients(krt, krp, ktp)                   # field-aligned cross terms (NEXT-4)
         S.set_bc_r(prob.bc_in, None, prob.bc_out, None)
         if warm:
             # the caller's time loop (not the solver path): step 0 solves with the c3-like f from x0;
@@ -668,7 +692,10 @@ def main():
 
     # ---- roofline of the dominant kernel (the stencil pass), CUDA events on the launching stream
     peak, peak_src = peaks()
-    path = PATHS[stats["path"]]
+    path = dict(PATHS[stats["path"]])
+    if aniso:   # the 19-point field-aligned stencil: p, T_r, T_theta, T_phi, D7, Xrt, Xrp, Xtp, q
+        path.update({"name": "three kernels, field-aligned 19-point operator",
+                     "stencil": ("aniso stencil + p.q (k_aniso_flat)", 72), "iter": 152})
     st_name, st_bpc = path["stencil"]
     mv_ms = stats["matvec_ms"] / max(stats["matvec_launches"], 1)
     achieved = st_bpc * ncell_local / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
@@ -717,9 +744,15 @@ def main():
         h2d = sum(a.nbytes for a in (hkr, hkt, hkp, hs, hf, hx0))
         d2h = hx.nbytes
 
+        if aniso:
+            hx3 = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (prob.krt, prob.krp, prob.ktp)]
+            h2d += sum(t.numel() * 8 for t in hx3)
+
         def step_host():
             S.set_grid(prob.rf, prob.tf, prob.pf)
             S.set_coefficients(hkr, hkt, hkp, hs)                    # maspcg_set_coefficients_host
+            if aniso:   # pinned host -> device, then maspcg_set_aniso_coefficients
+                S.set_aniso_coefficients(*(t.to(dev, non_blocking=True) for t in hx3))
             S.set_bc_r(prob.bc_in, None, prob.bc_out, None)
             hx[...] = hx0
             st, info, hist = S.solve(hf, hx, tol, maxit)              # maspcg_solve_host
@@ -761,8 +794,9 @@ def main():
     # ---- CPU baseline: the oracle as it stands on this box's host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_block(inputs.make_problem(args.config, shape=shape), args.config, args.ref_iters,
-                                 4 * args.ref_iters)
+        full = (inputs.make_aniso_problem(args.config, shape=shape) if aniso
+                else inputs.make_problem(args.config, shape=shape))
+        cpu = cpu_baseline_block(full, args.config, args.ref_iters, 4 * args.ref_iters)
 
     if rank == 0:
         par_note = ((" (one-rank peer-memory communicator)" if use_peer else " (one-rank NCCL communicator)")

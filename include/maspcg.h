@@ -142,11 +142,12 @@ typedef enum {
     MASPCG_OPT_L2_KEEP = 10,     /* three-kernel path (nr even): L2 residency of the loop's arrays.  1 (default,
                                     auto): when the local slab is small enough (P = 4, 8 of c3), the arrays with the
                                     most accesses per iteration and byte -- D (3 reads), p and r (3 accesses each),
-                                    then x, q and the face coefficients -- are loaded and stored with an L2
-                                    evict_last policy, greedily up to 3/4 of the L2 (the last one partially, by a
-                                    fractional policy); their lines are returned to the normal priority after the
-                                    solve.  The "super" scaling of PAPER.md:277 (§V-C).  0: plain loads and stores.
-                                    Arithmetic and results are unaffected. */
+                                    then x and q -- are loaded and stored with an L2 evict_last policy, whole
+                                    classes greedily up to 0.45 of the L2, inside a persisting set-aside of exactly
+                                    their size (cudaLimitPersistingL2CacheSize, a device-wide limit this context
+                                    sets and releases at destroy); their lines are returned to the normal priority
+                                    after the solve.  The "super" scaling of PAPER.md:277 (§V-C).  0: plain loads
+                                    and stores.  Arithmetic and results are unaffected. */
     MASPCG_OPT_PATH = 4         /* iteration path: 0 = auto (default, = 1), 1 = three streaming kernels (stencil+p.q,
                                     r-update+Jacobi+dots, deferred x-update+p-update; 128 B/cell), 2 = fused two passes
                                     (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell),
@@ -219,9 +220,14 @@ MASPCG_API maspcg_status maspcg_set_workspace(maspcg_ctx *ctx, void *dev_ptr, si
  *   kp    [nloc][nt][nr]    phi-face k+1/2 of each local plane k
  *   shift [nloc][nt][nr]    s >= 0 (e.g. rho/dt for backward Euler, R5)
  * Assembles the face transmissibilities T and s*V in library memory and
- * fetches the phi-face below the slab from the previous rank.  Returns
- * E_INVALID (agreed across ranks) if any value is negative or non-finite.
- * Synchronises `cuda_stream` (the validation result is read back). */
+ * fetches the phi-face below the slab from the previous rank.  A negative or
+ * non-finite value gives E_INVALID (agreed across ranks), reported by the
+ * NEXT call that uses the operator (solve, apply, get_operator, sts_*): the
+ * validation result travels to pinned host memory behind the assembly, so
+ * this call does not wait for the device (no host synchronisation per
+ * coefficient change, e.g. per time step).  Calls on one context must be
+ * ordered on one stream.  The _host variant copies the caller's buffers,
+ * waits for the copies and reports E_INVALID itself. */
 MASPCG_API maspcg_status maspcg_set_coefficients(maspcg_ctx *ctx, const double *kr,
                                                  const double *kt, const double *kp,
                                                  const double *shift, void *cuda_stream);

@@ -13,6 +13,8 @@
 // Xrt, Xrp, Xtp (24), y (8) = 72 B/cell of algorithmic traffic per apply.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "aniso.cuh"
 #include "arith.cuh"
 #include "common.cuh"
@@ -24,6 +26,7 @@ namespace maspcg {
 namespace {
 
 constexpr int kAnisoBlocks = 4;   // resident blocks of 256 threads per SM (<= 64 registers)
+
 
 // ---------------------------------------------------------------- edge weights (setup)
 __global__ void __launch_bounds__(kThreads) k_aniso_edges(Dims d, DevArrays a, AnisoArrays x,
@@ -194,11 +197,198 @@ __global__ void __launch_bounds__(kThreads, kAnisoBlocks) k_aniso_flat(Dims d, D
     }
 }
 
+// ---------------------------------------------------------------- operator apply, two cells per thread (nr even)
+// The pair (i0, i0 + 1), i0 even: every stream is a 16-byte load, the pair's shared neighbours and the
+// r-theta / r-phi edge between its two cells (face i0 + 1) are loaded and differenced once.  Each cell's
+// cross terms are accumulated in the R33 edge order, with the same operations as the one-cell kernel, so
+// the results are that kernel's (and the oracle's) bit for bit.
+struct Row4 {   // p of one row at the pair's columns i0 - 1 (m, if i0 > 0), i0, i0 + 1, i0 + 2 (q, if i0 + 2 < nr)
+    double m, c0, c1, q;
+};
+
+__device__ __forceinline__ double2 ldv2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
+__device__ __forceinline__ double2 ldv2c(const double *p, bool coherent) {
+    return coherent ? __ldcg(reinterpret_cast<const double2 *>(p)) : __ldg(reinterpret_cast<const double2 *>(p));
+}
+
+template <bool EXACT>
+__device__ __forceinline__ void xterm(double &s, double X, double da, double db, bool sa_plus, bool sb_plus) {
+    const double v = __dadd_rn(sa_plus ? db : -db, sb_plus ? da : -da);
+    s = EXACT ? __dadd_rn(s, __dmul_rn(X, v)) : fma(X, v, s);
+}
+// da (the two a-differences) and db (the two b-differences) of the 2x2 block u00 (lo a, lo b), u10 (hi a,
+// lo b), u01 (lo a, hi b), u11 (hi a, hi b)
+__device__ __forceinline__ void diffs(double u00, double u10, double u01, double u11, double &da, double &db) {
+    da = __dadd_rn(__dsub_rn(u10, u00), __dsub_rn(u11, u01));
+    db = __dadd_rn(__dsub_rn(u01, u00), __dsub_rn(u11, u10));
+}
+
+template <bool WITH_DOT, bool LOOP, bool EXACT, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays a, AnisoArrays x,
+                                                            double *__restrict__ y, Range rg, unsigned red_slot0,
+                                                            unsigned red_total) {
+    pdl_wait();
+    pdl_trigger();
+    if (LOOP && *(volatile int *)&a.sc->done) return;
+    if (LOOP && a.peer_wait) acquire_p_halo(a);
+    const bool coh = LOOP && a.peer_wait;
+    using A = Ar<EXACT>;
+    const int nr = d.nr, nt = d.nt, nloc = d.nloc;
+    const size_t plane = d.plane;
+    Acc<EXACT> dot[1];
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = rg.vend >> 1;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < npair; v += stride) {
+        const uint32_t v2 = 2u * v;
+        const uint32_t c = v2 + rg.off0 + (v2 >= rg.split ? rg.off1 : 0u);
+        int i0, j, k;
+        decompose(d, c, i0, j, k);
+        const bool il = i0 > 0, ih = i0 + 2 < nr, jl = j > 0, jh = j < nt - 1;
+        const double *pk = a.p + plane + c;   // padded p at (plane k, row j, column i0)
+        const bool cm = coh && k == 0, cp = coh && k == nloc - 1;   // halo planes written by the neighbours
+        auto row4 = [&](const double *q, bool coherent) {
+            Row4 r;
+            const double2 v = ldv2c(q, coherent);
+            r.c0 = v.x, r.c1 = v.y;
+            r.m = il ? (coherent ? __ldcg(q - 1) : __ldg(q - 1)) : 0.0;
+            r.q = ih ? (coherent ? __ldcg(q + 2) : __ldg(q + 2)) : 0.0;
+            return r;
+        };
+        const double2 z2 = make_double2(0.0, 0.0);
+        const Row4 Rj = row4(pk, false);
+        const Row4 Rjm = jl ? row4(pk - nr, false) : Row4{0.0, 0.0, 0.0, 0.0};
+        const Row4 Rjp = jh ? row4(pk + nr, false) : Row4{0.0, 0.0, 0.0, 0.0};
+        const Row4 Mj = row4(pk - plane, cm);
+        const Row4 Pj = row4(pk + plane, cp);
+        const double2 Mjm = jl ? ldv2c(pk - plane - nr, cm) : z2, Mjp = jh ? ldv2c(pk - plane + nr, cm) : z2;
+        const double2 Pjm = jl ? ldv2c(pk + plane - nr, cp) : z2, Pjp = jh ? ldv2c(pk + plane + nr, cp) : z2;
+        // ---- the 7-point part, the oracle's order per cell
+        const double2 tr = ldv2(a.Tr + c);
+        const double tr2 = ih ? __ldg(a.Tr + c + 2) : 0.0;
+        const double2 ttl = ldv2(a.Tt + c), tth = jh ? ldv2(a.Tt + c + nr) : z2;
+        const double2 tpl = ldv2(a.Tp + c), tph = ldv2(a.Tp + c + plane);
+        const double2 d7 = ldv2(x.D7 + c);
+        double s0 = 0.0, s1 = 0.0;
+        if (il) s0 = A::acc(s0, tr.x, Rj.m);
+        s0 = A::acc(s0, tr.y, Rj.c1);
+        if (jl) s0 = A::acc(s0, ttl.x, Rjm.c0);
+        if (jh) s0 = A::acc(s0, tth.x, Rjp.c0);
+        s0 = A::acc(s0, tpl.x, Mj.c0);
+        s0 = A::acc(s0, tph.x, Pj.c0);
+        const double y70 = A::diag_minus(d7.x, Rj.c0, s0);
+        s1 = A::acc(s1, tr.y, Rj.c0);
+        if (ih) s1 = A::acc(s1, tr2, Rj.q);
+        if (jl) s1 = A::acc(s1, ttl.y, Rjm.c1);
+        if (jh) s1 = A::acc(s1, tth.y, Rjp.c1);
+        s1 = A::acc(s1, tpl.y, Mj.c1);
+        s1 = A::acc(s1, tph.y, Pj.c1);
+        const double y71 = A::diag_minus(d7.y, Rj.c1, s1);
+        // ---- cross terms: x0 for cell i0, x1 for cell i0 + 1, each in the R33 edge order
+        double x0 = 0.0, x1 = 0.0, da, db;
+        const size_t e = c;   // (k, j, i0) in the [nloc][nt][nr] edge arrays
+        // r-theta edges of plane k: je = j (rows j-1, j) and je = j + 1 (rows j, j+1); ie = i0, i0+1, i0+2
+        if (jl) {
+            const double2 X = ldv2(x.Xrt + e);
+            const double X2 = ih ? __ldg(x.Xrt + e + 2) : 0.0;
+            if (il) { diffs(Rjm.m, Rjm.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
+            diffs(Rjm.c0, Rjm.c1, Rj.c0, Rj.c1, da, db);
+            xterm<EXACT>(x0, X.y, da, db, false, true);
+            xterm<EXACT>(x1, X.y, da, db, true, true);
+            if (ih) { diffs(Rjm.c1, Rjm.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
+        }
+        if (jh) {
+            const double2 X = ldv2(x.Xrt + e + nr);
+            const double X2 = ih ? __ldg(x.Xrt + e + nr + 2) : 0.0;
+            if (il) { diffs(Rj.m, Rj.c0, Rjp.m, Rjp.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
+            diffs(Rj.c0, Rj.c1, Rjp.c0, Rjp.c1, da, db);
+            xterm<EXACT>(x0, X.y, da, db, false, false);
+            xterm<EXACT>(x1, X.y, da, db, true, false);
+            if (ih) { diffs(Rj.c1, Rj.q, Rjp.c1, Rjp.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
+        }
+        // r-phi edges of row j: face k-1/2 (planes k-1, k; Xrp plane k) then k+1/2 (planes k, k+1; plane k+1)
+        {
+            const double2 X = ldv2(x.Xrp + e);
+            const double X2 = ih ? __ldg(x.Xrp + e + 2) : 0.0;
+            if (il) { diffs(Mj.m, Mj.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
+            diffs(Mj.c0, Mj.c1, Rj.c0, Rj.c1, da, db);
+            xterm<EXACT>(x0, X.y, da, db, false, true);
+            xterm<EXACT>(x1, X.y, da, db, true, true);
+            if (ih) { diffs(Mj.c1, Mj.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
+        }
+        {
+            const double2 X = ldv2(x.Xrp + e + plane);
+            const double X2 = ih ? __ldg(x.Xrp + e + plane + 2) : 0.0;
+            if (il) { diffs(Rj.m, Rj.c0, Pj.m, Pj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
+            diffs(Rj.c0, Rj.c1, Pj.c0, Pj.c1, da, db);
+            xterm<EXACT>(x0, X.y, da, db, false, false);
+            xterm<EXACT>(x1, X.y, da, db, true, false);
+            if (ih) { diffs(Rj.c1, Rj.q, Pj.c1, Pj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
+        }
+        // theta-phi edges of each cell's column: (j, lo), (j+1, lo), (j, hi), (j+1, hi)
+        {
+            const double2 Xjl = jl ? ldv2(x.Xtp + e) : z2, Xjpl = jh ? ldv2(x.Xtp + e + nr) : z2;
+            const double2 Xjh = jl ? ldv2(x.Xtp + e + plane) : z2, Xjph = jh ? ldv2(x.Xtp + e + plane + nr) : z2;
+            if (jl) {
+                diffs(Mjm.x, Mj.c0, Rjm.c0, Rj.c0, da, db); xterm<EXACT>(x0, Xjl.x, da, db, true, true);
+                diffs(Mjm.y, Mj.c1, Rjm.c1, Rj.c1, da, db); xterm<EXACT>(x1, Xjl.y, da, db, true, true);
+            }
+            if (jh) {
+                diffs(Mj.c0, Mjp.x, Rj.c0, Rjp.c0, da, db); xterm<EXACT>(x0, Xjpl.x, da, db, false, true);
+                diffs(Mj.c1, Mjp.y, Rj.c1, Rjp.c1, da, db); xterm<EXACT>(x1, Xjpl.y, da, db, false, true);
+            }
+            if (jl) {
+                diffs(Rjm.c0, Rj.c0, Pjm.x, Pj.c0, da, db); xterm<EXACT>(x0, Xjh.x, da, db, true, false);
+                diffs(Rjm.c1, Rj.c1, Pjm.y, Pj.c1, da, db); xterm<EXACT>(x1, Xjh.y, da, db, true, false);
+            }
+            if (jh) {
+                diffs(Rj.c0, Rjp.c0, Pj.c0, Pjp.x, da, db); xterm<EXACT>(x0, Xjph.x, da, db, false, false);
+                diffs(Rj.c1, Rjp.c1, Pj.c1, Pjp.y, da, db); xterm<EXACT>(x1, Xjph.y, da, db, false, false);
+            }
+        }
+        const double q0 = __dadd_rn(y70, x0), q1 = __dadd_rn(y71, x1);
+        *reinterpret_cast<double2 *>(y + c) = make_double2(q0, q1);
+        if (WITH_DOT) {
+            dot[0].add(Rj.c0, q0);
+            dot[0].add(Rj.c1, q1);
+        }
+    }
+    if (WITH_DOT) {
+        Acc<EXACT> out[1];
+        if (reduce_last<EXACT, kThreads, 1>(dot, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total,
+                                            out)) {
+            if (threadIdx.x == 0) {
+                a.sc->red1[0] = out[0].p;
+                a.sc->red1[1] = out[0].s;
+                if (a.p2p_ll) ll_push_pairs(a, a.sc->red1, 1);   // to every rank (peer communicator)
+            }
+        }
+    }
+}
+
 inline unsigned grid_aniso(uint32_t n) {
     uint64_t g = (n + kThreads - 1) / kThreads;
     if (g < 1) g = 1;
     if (g > (uint64_t)(148 * kAnisoBlocks)) g = 148 * kAnisoBlocks;
     return (unsigned)g;
+}
+
+// blocks per SM of the pair kernel: 2 (default, 128 registers, no spills) or 3 (MASPCG_ANISO_BLOCKS=3:
+// 85 registers with spills)
+inline int aniso2_blocks() {
+    static const int b = getenv("MASPCG_ANISO_BLOCKS") ? atoi(getenv("MASPCG_ANISO_BLOCKS")) : 2;
+    return b == 3 ? 3 : 2;
+}
+
+inline unsigned grid_aniso2(uint32_t n) {   // two cells per thread, a resident grid
+    uint64_t g = (n / 2 + kThreads - 1) / kThreads;
+    if (g < 1) g = 1;
+    if (g > (uint64_t)(148 * aniso2_blocks())) g = 148 * aniso2_blocks();
+    return (unsigned)g;
+}
+
+// the pair kernel: nr even (pairs never straddle a row) and y 16-byte aligned (MASPCG_OPT_VEC)
+inline bool aniso_vec2(const Dims &d, const double *y) {
+    return d.vec_ok && (d.nr % 2 == 0) && (((uintptr_t)y & 15) == 0);
 }
 
 inline unsigned grid_setup(uint32_t n) {
@@ -233,18 +423,26 @@ void launch_aniso_diag(const Dims &d, const DevArrays &a, const AnisoArrays &x, 
     k_aniso_diag<<<grid_setup(d.n), kThreads, 0, st>>>(d, a, x);
 }
 
-unsigned aniso_stencil_blocks(const Dims &d, StencilPart part) {
+unsigned aniso_stencil_blocks(const Dims &d, StencilPart part, const double *y) {
     const Range rg = make_range(d, part);
-    return rg.vend ? grid_aniso(rg.vend) : 0u;
+    if (!rg.vend) return 0u;
+    return aniso_vec2(d, y) ? grid_aniso2(rg.vend) : grid_aniso(rg.vend);
 }
 
 void launch_aniso_matvec(const Dims &d, const DevArrays &a, const AnisoArrays &x, double *y, StencilPart part,
                          bool with_dot, bool loop, unsigned red_slot0, unsigned red_total, bool exact, cudaStream_t st) {
     const Range rg = make_range(d, part);
     if (rg.vend == 0) return;
-    const unsigned g = grid_aniso(rg.vend);
+    const bool vec = aniso_vec2(d, y);
+    const unsigned g = vec ? grid_aniso2(rg.vend) : grid_aniso(rg.vend);
     const bool pdl = d.pdl != 0;
-#define AN(W, L, E) launch_pdl_aniso(pdl, k_aniso_flat<W, L, E>, g, st, d, a, x, y, rg, red_slot0, red_total)
+#define AN(W, L, E)                                                                                      \
+    do {                                                                                                 \
+        if (vec && aniso2_blocks() == 3)                                                                 \
+            launch_pdl_aniso(pdl, k_aniso_vec2<W, L, E, 3>, g, st, d, a, x, y, rg, red_slot0, red_total);   \
+        else if (vec) launch_pdl_aniso(pdl, k_aniso_vec2<W, L, E, 2>, g, st, d, a, x, y, rg, red_slot0, red_total); \
+        else launch_pdl_aniso(pdl, k_aniso_flat<W, L, E>, g, st, d, a, x, y, rg, red_slot0, red_total);     \
+    } while (0)
     if (exact) {
         if (with_dot) {
             if (loop) AN(true, true, true);

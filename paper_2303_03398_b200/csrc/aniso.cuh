@@ -33,6 +33,6 @@ void launch_aniso_diag(const Dims &d, const DevArrays &a, const AnisoArrays &x, 
 // y = A p over `part` of the slab (as launch_matvec), optional Dot2 partial of p.y
 void launch_aniso_matvec(const Dims &d, const DevArrays &a, const AnisoArrays &x, double *y, StencilPart part,
                          bool with_dot, bool loop, unsigned red_slot0, unsigned red_total, bool exact, cudaStream_t st);
-unsigned aniso_stencil_blocks(const Dims &d, StencilPart part);
+unsigned aniso_stencil_blocks(const Dims &d, StencilPart part, const double *y);
 
 }  // namespace maspcg

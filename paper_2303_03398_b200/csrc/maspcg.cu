@@ -69,7 +69,9 @@ struct maspcg_ctx {
     cudaStream_t cap_stream = nullptr;   // graphs are captured here (the caller's may be the legacy stream)
     cudaEvent_t ev_p = nullptr, ev_halo = nullptr, ev_chunk[2] = {nullptr, nullptr};
     Scalars *snap[2] = {nullptr, nullptr};
-    int *vflags_host = nullptr;
+    int *vflags_host = nullptr;      // [0..1] synchronous checks; [2..3] set_coefficients (deferred, ev_valid)
+    cudaEvent_t ev_valid = nullptr;  // recorded after set_coefficients copied its validation flags
+    bool valid_pending = false;      // those flags are not read yet (settle_validation)
 
     // graph cache (one captured chunk of `chunk` iterations)
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // one captured chunk per timing-event set
@@ -447,7 +449,7 @@ cudaError_t record_timing(maspcg_ctx *c, int kern, int which, int it, cudaStream
 
 // The operator's stencil over `part`: the 7-point kernels, or the 19-point field-aligned one (NEXT-4).
 unsigned op_blocks(const maspcg_ctx *c, StencilPart part, const double *y) {
-    return c->an_on ? aniso_stencil_blocks(c->d, part) : stencil_blocks(c->d, part, y);
+    return c->an_on ? aniso_stencil_blocks(c->d, part, y) : stencil_blocks(c->d, part, y);
 }
 void op_matvec(const maspcg_ctx *c, const Dims &d, double *y, StencilPart part, bool with_dot, bool loop,
                unsigned slot0, unsigned total, cudaStream_t st) {
@@ -489,7 +491,22 @@ maspcg_status stencil_with_halo(maspcg_ctx *c, double *y, bool with_dot, bool lo
     return MASPCG_OK;
 }
 
+// The deferred result of the last set_coefficients: E_INVALID (reported by the first call that uses the
+// operator) for a negative or non-finite coefficient; the shift-present flag for the singularity check.
+maspcg_status settle_validation(maspcg_ctx *c) {
+    if (!c->valid_pending) return MASPCG_OK;
+    CK(c, cudaEventSynchronize(c->ev_valid));
+    c->valid_pending = false;
+    if (c->vflags_host[2]) {
+        c->coef_set = false;
+        SET_ERR(c, MASPCG_E_INVALID, "a diffusion coefficient or the shift is negative or non-finite");
+    }
+    c->any_shift = c->vflags_host[3];
+    return MASPCG_OK;
+}
+
 maspcg_status ensure_D(maspcg_ctx *c, cudaStream_t st) {
+    RET_IF(settle_validation(c));
     if (!c->coef_set || !c->bc_set)
         SET_ERR(c, MASPCG_E_STATE, "set_coefficients and set_bc_r must precede solve/apply");
     if (!c->D_dirty) return MASPCG_OK;
@@ -807,7 +824,10 @@ void plan_l2(maspcg_ctx *c, const double *x) {
         c->l2_plan_bytes = c->l2_persist_max;
         return;
     }
-    double budget = 0.75;
+    // 0.45 of the L2: on the P = 8 slab of c3 keeping D and p (54.7 MB) measured 74.3 us per iteration,
+    // D, p and r (81.7 MB, the whole persisting maximum of 82.9 MB) 78.7 and no plan 81.9; on the P = 4
+    // slab D alone (54 MB) 143.0 against 150.6 (profiles/r02/l2_residency_plans.txt)
+    double budget = 0.45;
     if (const char *e = getenv("MASPCG_L2_BUDGET")) budget = atof(e);
     double cap = budget * (double)c->l2_bytes;
     // evict_last lines are retained only inside the persisting set-aside of the L2
@@ -1098,6 +1118,7 @@ static maspcg_status create_impl(int nr, int nt, int np, int rank, int nranks, c
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->snap[0], sizeof(Scalars));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->snap[1], sizeof(Scalars));
     if (e == cudaSuccess) e = cudaMallocHost((void **)&c->vflags_host, 4 * sizeof(int));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_valid, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         g_create_error = std::string("CUDA initialisation failed: ") + cudaGetErrorString(e);
         maspcg_destroy(c);
@@ -1210,6 +1231,7 @@ maspcg_status maspcg_destroy(maspcg_ctx *c) {
         if (c->snap[b]) cudaFreeHost(c->snap[b]);
     }
     if (c->vflags_host) cudaFreeHost(c->vflags_host);
+    if (c->ev_valid) cudaEventDestroy(c->ev_valid);
     if (c->l2_persist_set) {   // release the persisting L2 set-aside this context requested
         cudaCtxResetPersistingL2Cache();
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
@@ -1410,15 +1432,14 @@ maspcg_status maspcg_set_coefficients(maspcg_ctx *c, const double *kr, const dou
         COMM(c, c->comm->shift_right(c->a.Tp + (size_t)c->nloc * pl, c->a.Tp, pl, st, c->err));
         COMM(c, c->comm->allreduce_max(&c->a.sc->vinvalid, 2, st, c->err));
     }
-    CK(c, cudaMemcpyAsync(c->vflags_host, &c->a.sc->vinvalid, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(c, cudaStreamSynchronize(st));
+    // The validation flags (agreed across ranks above) travel to pinned host memory behind the assembly; they
+    // are read by the next call that uses the operator (settle_validation), so the host does not wait here
+    // for the assembly -- no host synchronisation per coefficient change (e.g. every time step).
+    CK(c, cudaMemcpyAsync(c->vflags_host + 2, &c->a.sc->vinvalid, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaEventRecord(c->ev_valid, st));
+    c->valid_pending = true;
     c->stats.kernel_launches += 1;
     c->D_dirty = true;
-    if (c->vflags_host[0]) {
-        c->coef_set = false;
-        SET_ERR(c, MASPCG_E_INVALID, "a diffusion coefficient or the shift is negative or non-finite");
-    }
-    c->any_shift = c->vflags_host[1];
     c->coef_set = true;
     return MASPCG_OK;
 }
@@ -1462,7 +1483,8 @@ maspcg_status maspcg_set_coefficients_host(maspcg_ctx *c, const double *kr, cons
     CK(c, cudaMemcpyAsync(c->a.skt, kt, 8 * (size_t)c->nloc * (c->nt + 1) * c->nr, cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->a.skp, kp, 8 * n, cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->a.ss, shift, 8 * n, cudaMemcpyHostToDevice, st));
-    return maspcg_set_coefficients(c, c->a.skr, c->a.skt, c->a.skp, c->a.ss, stream);
+    RET_IF(maspcg_set_coefficients(c, c->a.skr, c->a.skt, c->a.skp, c->a.ss, stream));
+    return settle_validation(c);   // host buffers: returns after the copies, with the validation result
 }
 
 static maspcg_status set_bc_common(maspcg_ctx *c, maspcg_bc inner, const double *gi, maspcg_bc outer,

@@ -460,3 +460,22 @@ def random_aniso_problem(nr: int, nt: int, np_: int, seed: int, *, bc_in=BC_DIRI
     kr, kt, kp, krt, krp, ktp = aniso_coefficients(rough, kperp, b_field, p.rf, p.tf, p.pf, k0, nloc)
     return AnisoProblem(f"arand{seed}", nr, nt, np_, k0, nloc, p.rf, p.tf, p.pf, kr, kt, kp, p.s, p.f, p.x0,
                         p.bc_in, p.bc_out, p.g_in, p.g_out, p.tol, p.maxit, krt, krp, ktp)
+
+
+def isolated_pair_problem(nr: int = 8, nt: int = 6, np_: int = 8, seed: int = 31) -> Problem:
+    """A singular connected component the global E_SINGULAR check cannot see: the two
+    phi-neighbour cells (k = 2, 3) at (j = 2, i = 3) have kappa = 0 on their 10 outer faces and s = 0, all
+    other cells s > 0; the rhs is zero except an equal value on the pair (uniform phi faces give the pair
+    equal volumes).  Then p_0 is constant on the pair and A p_0 = 0 exactly: p.Ap = 0 in iteration 1."""
+    p = random_problem(nr, nt, np_, seed, bc_in=BC_NEUMANN0, bc_out=BC_NEUMANN0)
+    i, j, k = 3, 2, 2
+    kr, kt, kp, s = p.kr.copy(), p.kt.copy(), p.kp.copy(), p.s.copy()
+    for kk in (k, k + 1):
+        kr[kk, j, i] = kr[kk, j, i + 1] = 0.0
+        kt[kk, j, i] = kt[kk, j + 1, i] = 0.0
+        s[kk, j, i] = 0.0
+    kp[k - 1, j, i] = kp[k + 1, j, i] = 0.0     # the pair's outer phi faces; kp[k] (between them) stays > 0
+    f = np.zeros_like(p.f)
+    f[k, j, i] = f[k + 1, j, i] = 1.0
+    return Problem("isolated-pair", nr, nt, np_, 0, np_, p.rf, p.tf, p.pf, kr, kt, kp, s, f, p.x0,
+                   BC_NEUMANN0, BC_NEUMANN0, None, None, 1e-10, 100)

@@ -1,0 +1,53 @@
+"""Full-size solves against golden fixtures written by the CPU oracle alone (-m gpu).
+
+tests/golden/{c3,c5}_full_solve.json come from tools/make_golden.py, which calls only oracle/ and the
+seeded generators: the complete residual history of the oracle's solve of BASELINE.json configs[2] (c3,
+150 x 300 x 600, 830 iterations to 1e-10) and of step 0 of configs[4] (c5, 200 x 300 x 600), its
+iteration count, ||x||^2 and x at a fixed sample of 4,096 cells.  The GPU solves the same generated
+problem in the bench's launch configuration (three-kernel path, CUDA graphs, chunk 16) and must
+reproduce every history entry, the count and the sampled solution bit for bit (R24).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2303_03398_b200 import inputs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def M():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("-m gpu tests need a CUDA device")
+    from paper_2303_03398_b200 import build, maspcg
+    build.build()
+    return maspcg
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_full_size_solve_matches_oracle_golden(M, name):
+    import torch
+    path = os.path.join(HERE, "golden", f"{name}_full_solve.json")
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: run tools/make_golden.py {name}")
+    g = json.load(open(path))
+    p = inputs.make_problem(name)
+    assert [p.nr, p.nt, p.np] == g["shape"]
+    S = M.solver_for_problem(p, chunk=16)
+    x = torch.from_numpy(p.x0).cuda()
+    st, info, hist = S.solve(torch.from_numpy(p.f).cuda(), x, p.tol, p.maxit)
+    torch.cuda.synchronize()
+    xs = x.cpu().numpy().ravel()
+    S.close()
+    assert st == g["status"] == 0
+    assert info["iters"] == g["iters"]
+    assert info["bnorm"] == g["bnorm"]
+    assert np.array_equal(hist, np.array(g["hist"])), np.abs(hist - np.array(g["hist"])).max()
+    idx = np.array(g["x_sample_index"], dtype=np.int64)
+    assert np.array_equal(xs[idx], np.array(g["x_sample"]))
+    assert float(np.dot(xs, xs)) == g["x_norm2"]

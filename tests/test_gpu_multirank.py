@@ -162,8 +162,9 @@ def test_multirank_errors_agree(M):
         if r == 1:
             kr[0, 1, 2] = -3.0
         T = lambda a: torch.from_numpy(a).cuda()
-        try:
+        try:   # the validation is reported by the first call that uses the operator (deferred, no host sync)
             S.set_coefficients(T(kr), T(p.kt), T(p.kp), T(p.s))
+            S.get_operator()
             return M.OK
         except M.MaspcgError as e:
             return e.status

@@ -277,8 +277,12 @@ def test_error_paths(torch_cuda, M):
     assert st == M.OK
     kr = p.kr.copy()
     kr[1, 2, 3] = -1.0
-    with pytest.raises(M.MaspcgError) as e:
+    with pytest.raises(M.MaspcgError) as e:   # reported by the next call that uses the operator (deferred)
         S.set_coefficients(dev(torch, kr), dev(torch, p.kt), dev(torch, p.kp), dev(torch, p.s))
+        S.solve(dev(torch, p.f), x, 1e-10, 5)
+    assert e.value.status == M.E_INVALID
+    with pytest.raises(M.MaspcgError) as e:   # host entry point: reported by the call itself
+        S.set_coefficients(kr, p.kt, p.kp, p.s)
     assert e.value.status == M.E_INVALID
     bad = p.pf.copy()
     bad[-1] = 6.0
@@ -398,6 +402,7 @@ def test_coefficients_from_fields_bitwise(torch_cuda, M, oracle_mod, mean, half_
         assert np.array_equal(g, o)
     with pytest.raises(M.MaspcgError) as e:          # T^(5/2) of a negative temperature -> NaN
         S.set_coefficients_from_fields(dev(torch, -T), 1.0, 5, mean, None, 1.0)
+        S.get_operator()                              # (reported by the next use of the operator)
     assert e.value.status == M.E_INVALID
 
 

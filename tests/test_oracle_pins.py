@@ -555,3 +555,18 @@ def test_openmp_build_gives_identical_iterates(oracle_mod):
         oracle_mod.use_openmp(False)
     assert a["iters"] == b["iters"] == 130
     assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["hist"], b["hist"])
+
+
+def test_breakdown_from_an_isolated_singular_pair(oracle_mod):
+    """a kappa = 0-isolated pair of cells with s = 0 and no Dirichlet face is a singular
+    component the global check cannot see.  With the rhs on the pair only (equal values), z_0 = r_0 / D is
+    constant on the pair, A z_0 = 0 exactly (the pair's row is D p - T p with D = T), so p.Ap = 0 in the
+    first iteration: E_BREAKDOWN with iters 0 and a finite hist[0] (not a setup failure)."""
+    p = inputs.isolated_pair_problem()
+    op = oracle_mod.Operator(p.rf, p.tf, p.pf, p.kr, p.kt, p.kp, p.s, p.bc_in, p.bc_out)
+    b = op.rhs(p.f)
+    z0 = b / op.D
+    assert np.count_nonzero(z0) == 2 and z0[2, 2, 3] == z0[3, 2, 3]
+    assert not op.apply(z0).any()
+    st, x, iters, hist, bn, rn = op.pcg(b, np.zeros(op.shape), 1e-10, 50)
+    assert st == oracle_mod.E_BREAKDOWN and iters == 0 and np.isfinite(hist[0]) and hist[0] > 0

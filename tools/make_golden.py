@@ -1,0 +1,58 @@
+#!/usr/bin/env python
+"""Golden fixtures of the full-size solves, written by the CPU ORACLE ONLY (oracle/ + the seeded input
+generators; nothing from the CUDA path).  Used by tests/test_gpu_golden.py to compare the GPU's full-size
+solves element by element: the whole residual history, the iteration count, ||x|| and x at a fixed sample
+of cells (every cell is not stored: 216 MB).
+
+    python tools/make_golden.py c3      # BASELINE.json configs[2], 150 x 300 x 600, tol 1e-10
+    python tools/make_golden.py c5      # configs[4] step 0 (cold solve), 200 x 300 x 600
+
+Runs the oracle's -fopenmp build (identical values to the plain build,
+tests/test_oracle_pins.py::test_openmp_build_gives_identical_iterates).
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_2303_03398_b200 import inputs  # noqa: E402
+
+NSAMPLE = 4096
+
+
+def sample_index(n, seed=12345):
+    """Fixed cell sample: splitmix64 of 0..NSAMPLE-1 modulo n (sorted, unique)."""
+    idx = inputs.splitmix64(np.arange(NSAMPLE, dtype=np.uint64) + np.uint64(seed)) % np.uint64(n)
+    return np.unique(idx.astype(np.int64))
+
+
+def main(name):
+    oracle.use_openmp(True)
+    p = inputs.make_problem(name)
+    t0 = time.time()
+    o = oracle.solve_problem(p)
+    dt = time.time() - t0
+    x = o["x"].ravel()
+    idx = sample_index(x.size)
+    out = {
+        "source": f"tools/make_golden.py {name}: oracle/masoracle.c (-fopenmp build) masoracle_pcg on "
+                  f"inputs.make_problem('{name}') (BASELINE.json {name}), tol {p.tol}",
+        "config": name, "shape": [p.nr, p.nt, p.np], "status": int(o["status"]), "iters": int(o["iters"]),
+        "bnorm": o["bnorm"], "hist": [float(v) for v in o["hist"]],
+        "x_norm2": float(np.dot(x, x)), "x_sample_index": idx.tolist(), "x_sample": [float(v) for v in x[idx]],
+        "oracle_seconds": dt,
+    }
+    path = os.path.join(ROOT, "tests", "golden", f"{name}_full_solve.json")
+    with open(path, "w") as f:
+        json.dump(out, f)
+    print(path, o["status"], o["iters"], f"{dt:.0f} s")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "c3")
