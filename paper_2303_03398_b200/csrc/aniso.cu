@@ -246,26 +246,28 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
         const bool il = i0 > 0, ih = i0 + 2 < nr, jl = j > 0, jh = j < nt - 1;
         const double *pk = a.p + plane + c;   // padded p at (plane k, row j, column i0)
         const bool cm = coh && k == 0, cp = coh && k == nloc - 1;   // halo planes written by the neighbours
+        // Every load is unconditional (branch-free, so the compiler can issue them all ahead of their uses):
+        // a neighbour that does not exist is replaced by an in-range address whose value is never used.
+        const size_t om = il ? 1 : 0, oq = ih ? 2 : 1, ojm = jl ? nr : 0, ojp = jh ? nr : 0;
         auto row4 = [&](const double *q, bool coherent) {
             Row4 r;
             const double2 v = ldv2c(q, coherent);
             r.c0 = v.x, r.c1 = v.y;
-            r.m = il ? (coherent ? __ldcg(q - 1) : __ldg(q - 1)) : 0.0;
-            r.q = ih ? (coherent ? __ldcg(q + 2) : __ldg(q + 2)) : 0.0;
+            r.m = coherent ? __ldcg(q - om) : __ldg(q - om);
+            r.q = coherent ? __ldcg(q + oq) : __ldg(q + oq);
             return r;
         };
-        const double2 z2 = make_double2(0.0, 0.0);
         const Row4 Rj = row4(pk, false);
-        const Row4 Rjm = jl ? row4(pk - nr, false) : Row4{0.0, 0.0, 0.0, 0.0};
-        const Row4 Rjp = jh ? row4(pk + nr, false) : Row4{0.0, 0.0, 0.0, 0.0};
+        const Row4 Rjm = row4(pk - ojm, false);
+        const Row4 Rjp = row4(pk + ojp, false);
         const Row4 Mj = row4(pk - plane, cm);
         const Row4 Pj = row4(pk + plane, cp);
-        const double2 Mjm = jl ? ldv2c(pk - plane - nr, cm) : z2, Mjp = jh ? ldv2c(pk - plane + nr, cm) : z2;
-        const double2 Pjm = jl ? ldv2c(pk + plane - nr, cp) : z2, Pjp = jh ? ldv2c(pk + plane + nr, cp) : z2;
+        const double2 Mjm = ldv2c(pk - plane - ojm, cm), Mjp = ldv2c(pk - plane + ojp, cm);
+        const double2 Pjm = ldv2c(pk + plane - ojm, cp), Pjp = ldv2c(pk + plane + ojp, cp);
         // ---- the 7-point part, the oracle's order per cell
         const double2 tr = ldv2(a.Tr + c);
-        const double tr2 = ih ? __ldg(a.Tr + c + 2) : 0.0;
-        const double2 ttl = ldv2(a.Tt + c), tth = jh ? ldv2(a.Tt + c + nr) : z2;
+        const double tr2 = __ldg(a.Tr + c + oq);
+        const double2 ttl = ldv2(a.Tt + c), tth = ldv2(a.Tt + c + ojp);
         const double2 tpl = ldv2(a.Tp + c), tph = ldv2(a.Tp + c + plane);
         const double2 d7 = ldv2(x.D7 + c);
         double s0 = 0.0, s1 = 0.0;
@@ -287,9 +289,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
         double x0 = 0.0, x1 = 0.0, da, db;
         const size_t e = c;   // (k, j, i0) in the [nloc][nt][nr] edge arrays
         // r-theta edges of plane k: je = j (rows j-1, j) and je = j + 1 (rows j, j+1); ie = i0, i0+1, i0+2
+        const double2 Xt0 = ldv2(x.Xrt + e), Xt1 = ldv2(x.Xrt + e + ojp);
+        const double Xt0q = __ldg(x.Xrt + e + oq), Xt1q = __ldg(x.Xrt + e + ojp + oq);
+        const double2 Xp0 = ldv2(x.Xrp + e), Xp1 = ldv2(x.Xrp + e + plane);
+        const double Xp0q = __ldg(x.Xrp + e + oq), Xp1q = __ldg(x.Xrp + e + plane + oq);
+        const double2 Xjl = ldv2(x.Xtp + e), Xjpl = ldv2(x.Xtp + e + ojp);
+        const double2 Xjh = ldv2(x.Xtp + e + plane), Xjph = ldv2(x.Xtp + e + plane + ojp);
         if (jl) {
-            const double2 X = ldv2(x.Xrt + e);
-            const double X2 = ih ? __ldg(x.Xrt + e + 2) : 0.0;
+            const double2 X = Xt0;
+            const double X2 = Xt0q;
             if (il) { diffs(Rjm.m, Rjm.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
             diffs(Rjm.c0, Rjm.c1, Rj.c0, Rj.c1, da, db);
             xterm<EXACT>(x0, X.y, da, db, false, true);
@@ -297,8 +305,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
             if (ih) { diffs(Rjm.c1, Rjm.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
         }
         if (jh) {
-            const double2 X = ldv2(x.Xrt + e + nr);
-            const double X2 = ih ? __ldg(x.Xrt + e + nr + 2) : 0.0;
+            const double2 X = Xt1;
+            const double X2 = Xt1q;
             if (il) { diffs(Rj.m, Rj.c0, Rjp.m, Rjp.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
             diffs(Rj.c0, Rj.c1, Rjp.c0, Rjp.c1, da, db);
             xterm<EXACT>(x0, X.y, da, db, false, false);
@@ -307,8 +315,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
         }
         // r-phi edges of row j: face k-1/2 (planes k-1, k; Xrp plane k) then k+1/2 (planes k, k+1; plane k+1)
         {
-            const double2 X = ldv2(x.Xrp + e);
-            const double X2 = ih ? __ldg(x.Xrp + e + 2) : 0.0;
+            const double2 X = Xp0;
+            const double X2 = Xp0q;
             if (il) { diffs(Mj.m, Mj.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
             diffs(Mj.c0, Mj.c1, Rj.c0, Rj.c1, da, db);
             xterm<EXACT>(x0, X.y, da, db, false, true);
@@ -316,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
             if (ih) { diffs(Mj.c1, Mj.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
         }
         {
-            const double2 X = ldv2(x.Xrp + e + plane);
-            const double X2 = ih ? __ldg(x.Xrp + e + plane + 2) : 0.0;
+            const double2 X = Xp1;
+            const double X2 = Xp1q;
             if (il) { diffs(Rj.m, Rj.c0, Pj.m, Pj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
             diffs(Rj.c0, Rj.c1, Pj.c0, Pj.c1, da, db);
             xterm<EXACT>(x0, X.y, da, db, false, false);
@@ -326,8 +334,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
         }
         // theta-phi edges of each cell's column: (j, lo), (j+1, lo), (j, hi), (j+1, hi)
         {
-            const double2 Xjl = jl ? ldv2(x.Xtp + e) : z2, Xjpl = jh ? ldv2(x.Xtp + e + nr) : z2;
-            const double2 Xjh = jl ? ldv2(x.Xtp + e + plane) : z2, Xjph = jh ? ldv2(x.Xtp + e + plane + nr) : z2;
             if (jl) {
                 diffs(Mjm.x, Mj.c0, Rjm.c0, Rj.c0, da, db); xterm<EXACT>(x0, Xjl.x, da, db, true, true);
                 diffs(Mjm.y, Mj.c1, Rjm.c1, Rj.c1, da, db); xterm<EXACT>(x1, Xjl.y, da, db, true, true);

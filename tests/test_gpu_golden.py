@@ -3,11 +3,13 @@
 tests/golden/{c3,c5}_full_solve.json come from tools/make_golden.py, which calls only oracle/ and the
 seeded generators: the complete residual history of the oracle's solve of BASELINE.json configs[2] (c3,
 150 x 300 x 600, 830 iterations to 1e-10) and of step 0 of configs[4] (c5, 200 x 300 x 600), its
-iteration count, ||x||^2 and x at a fixed sample of 4,096 cells.  The GPU solves the same generated
+iteration count, the SHA-256 of the whole solution, ||x||^2 (fsum) and x at a fixed sample of 4,096 cells.  The GPU solves the same generated
 problem in the bench's launch configuration (three-kernel path, CUDA graphs, chunk 16) and must
 reproduce every history entry, the count and the sampled solution bit for bit (R24).
 """
+import hashlib
 import json
+import math
 import os
 
 import numpy as np
@@ -50,4 +52,6 @@ def test_full_size_solve_matches_oracle_golden(M, name):
     assert np.array_equal(hist, np.array(g["hist"])), np.abs(hist - np.array(g["hist"])).max()
     idx = np.array(g["x_sample_index"], dtype=np.int64)
     assert np.array_equal(xs[idx], np.array(g["x_sample"]))
-    assert float(np.dot(xs, xs)) == g["x_norm2"]
+    assert math.fsum(xs * xs) == g["x_norm2_fsum"]
+    # every cell of the solution, bit for bit
+    assert hashlib.sha256(np.ascontiguousarray(xs, dtype="<f8").tobytes()).hexdigest() == g["x_sha256"]

@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Golden fixtures of the full-size solves, written by the CPU ORACLE ONLY (oracle/ + the seeded input
 generators; nothing from the CUDA path).  Used by tests/test_gpu_golden.py to compare the GPU's full-size
-solves element by element: the whole residual history, the iteration count, ||x|| and x at a fixed sample
-of cells (every cell is not stored: 216 MB).
+solves element by element: the whole residual history, the iteration count, the SHA-256 of the whole
+solution x (every cell, bit for bit, without storing 216 MB), ||x||^2 (math.fsum, deterministic) and x at a
+fixed sample of cells.
 
     python tools/make_golden.py c3      # BASELINE.json configs[2], 150 x 300 x 600, tol 1e-10
     python tools/make_golden.py c5      # configs[4] step 0 (cold solve), 200 x 300 x 600
@@ -10,7 +11,9 @@ of cells (every cell is not stored: 216 MB).
 Runs the oracle's -fopenmp build (identical values to the plain build,
 tests/test_oracle_pins.py::test_openmp_build_gives_identical_iterates).
 """
+import hashlib
 import json
+import math
 import os
 import sys
 import time
@@ -45,7 +48,8 @@ def main(name):
                   f"inputs.make_problem('{name}') (BASELINE.json {name}), tol {p.tol}",
         "config": name, "shape": [p.nr, p.nt, p.np], "status": int(o["status"]), "iters": int(o["iters"]),
         "bnorm": o["bnorm"], "hist": [float(v) for v in o["hist"]],
-        "x_norm2": float(np.dot(x, x)), "x_sample_index": idx.tolist(), "x_sample": [float(v) for v in x[idx]],
+        "x_sha256": hashlib.sha256(np.ascontiguousarray(x, dtype="<f8").tobytes()).hexdigest(),
+        "x_norm2_fsum": math.fsum(x * x), "x_sample_index": idx.tolist(), "x_sample": [float(v) for v in x[idx]],
         "oracle_seconds": dt,
     }
     path = os.path.join(ROOT, "tests", "golden", f"{name}_full_solve.json")
