@@ -328,9 +328,6 @@ def run_vv(args):
 
     for _ in range(args.warmup):
         step()
-    if warm:   # the timed steps are the time loop from its start: step 0 cold, steps 1.. warm-started
-        x.copy_(x0)
-        nstep[0] = 0
     S.set_option(maspcg.OPT_TIMING, args.kernel_timing)
     S.reset_stats()
     if world > 1:
@@ -425,6 +422,7 @@ def run_vv(args):
                        "parallelism": f"phi-slab x{world}", "iters_per_solve": iters / args.steps,
                        "chunk": args.chunk, "l2": "no flush: working set ~4 GB >> 126 MB L2",
                        "step": "vv_set_coefficients + vv_set_bc_r + vv_solve to tol"},
+            "step_ms": step_stats(step_ms),
             "cell_updates_per_s": nr * nt * np_ * value,
             "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),

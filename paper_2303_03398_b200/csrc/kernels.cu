@@ -441,7 +441,10 @@ __device__ __forceinline__ void st2(double *p, double a, double b) {
     *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
 
-template <bool WITH_DOT, bool LOOP, bool EXACT, bool MV2>
+// HINT: the loads and stores carry the L2 residency policies of Dims::l2_mask and the peer-written halo
+// planes are read coherently (loop stencil with an L2 plan or the peer communicator); without it the plain
+// __ldg path (the policy registers and the per-load selection cost ~9 % on the P = 1 stencil).
+template <bool WITH_DOT, bool LOOP, bool EXACT, bool MV2, bool HINT>
 __global__ void __launch_bounds__(kThreads, kMvBlocks) k_matvec_vec2(Dims d, DevArrays a, double *__restrict__ y,
                                                                       Range rg, unsigned red_slot0,
                                                                       unsigned red_total) {
@@ -469,11 +472,14 @@ __global__ void __launch_bounds__(kThreads, kMvBlocks) k_matvec_vec2(Dims d, Dev
         uint32_t c;
         bool jlo, jhi, ilo, ihi;
     };
-    const uint64_t pol_p = l2_policy(d, L2A_P), pol_t = l2_policy(d, L2A_T), pol_d = l2_policy(d, L2A_D);
-    const uint64_t pol_q = l2_policy(d, L2A_Q);
+    uint64_t pol_p = 0, pol_t = 0, pol_d = 0, pol_q = 0;
+    if (HINT) {
+        pol_p = l2_policy(d, L2A_P), pol_t = l2_policy(d, L2A_T), pol_d = l2_policy(d, L2A_D);
+        pol_q = l2_policy(d, L2A_Q);
+    }
     // peer mode: the halo planes k = -1 and k = nloc were stored by the neighbours during this kernel's
     // lifetime (acquired above), so they are read coherently
-    const bool coh = LOOP && a.peer_wait;
+    const bool coh = HINT && LOOP && a.peer_wait;
     auto load = [&](uint32_t v) {
         PairIn q;
         const uint32_t v2 = 2u * v;
@@ -481,6 +487,27 @@ __global__ void __launch_bounds__(kThreads, kMvBlocks) k_matvec_vec2(Dims d, Dev
         int i, j, k;
         decompose(d, q.c, i, j, k);
         const size_t cp = (size_t)q.c + plane;
+        if (!HINT) {   // plain read-only loads
+            q.pc = __ldg(reinterpret_cast<const double2 *>(p + cp));
+            q.trv = __ldg(reinterpret_cast<const double2 *>(Tr + q.c));
+            q.ttl = __ldg(reinterpret_cast<const double2 *>(Tt + q.c));
+            q.tpl = __ldg(reinterpret_cast<const double2 *>(Tp + q.c));
+            q.tph = __ldg(reinterpret_cast<const double2 *>(Tp + q.c + plane));
+            q.pkm = __ldg(reinterpret_cast<const double2 *>(p + cp - plane));
+            q.pkp = __ldg(reinterpret_cast<const double2 *>(p + cp + plane));
+            q.dv = __ldg(reinterpret_cast<const double2 *>(D + q.c));
+            q.jlo = j > 0, q.jhi = j < nt - 1, q.ilo = i > 0, q.ihi = i + 2 < nr;
+            q.ptm = make_double2(0.0, 0.0), q.ptp = q.ptm, q.tth = q.ptm;
+            if (q.jlo) q.ptm = __ldg(reinterpret_cast<const double2 *>(p + cp - nr));
+            if (q.jhi) {
+                q.ptp = __ldg(reinterpret_cast<const double2 *>(p + cp + nr));
+                q.tth = __ldg(reinterpret_cast<const double2 *>(Tt + q.c + nr));
+            }
+            q.pm = q.ilo ? __ldg(p + cp - 1) : 0.0;
+            q.pp2 = q.ihi ? __ldg(p + cp + 2) : 0.0;
+            q.tr2 = q.ihi ? __ldg(Tr + q.c + 2) : 0.0;
+            return q;
+        }
         q.pc = ld2h(p + cp, pol_p);
         q.trv = ld2h(Tr + q.c, pol_t);
         q.ttl = ld2h(Tt + q.c, pol_t);
@@ -520,7 +547,8 @@ __global__ void __launch_bounds__(kThreads, kMvBlocks) k_matvec_vec2(Dims d, Dev
         s = A::acc(s, q.tpl.y, q.pkm.y);
         s = A::acc(s, q.tph.y, q.pkp.y);
         const double q1 = A::diag_minus(q.dv.y, q.pc.y, s);
-        st2h(y + q.c, q0, q1, pol_q);
+        if (HINT) st2h(y + q.c, q0, q1, pol_q);
+        else st2(y + q.c, q0, q1);
         if (WITH_DOT) {
             dot[0].add(q.pc.x, q0);
             dot[0].add(q.pc.y, q1);
@@ -911,10 +939,13 @@ void launch_matvec(const Dims &d, const DevArrays &a, double *y, StencilPart par
     const unsigned g = vec ? grid_mv2(rg.vend) : grid_for(rg.vend);
     // MASPCG_MATVEC2=1: two pairs per trip -- measured slower (5.98 vs 6.07 TB/s live: 64 registers, spills)
     static const int mv2 = getenv("MASPCG_MATVEC2") ? atoi(getenv("MASPCG_MATVEC2")) : 0;
+    // the policy / coherent-halo variant only where it is needed (an L2 plan or peer-written halos)
+    const bool hint = loop && (d.l2_mask != 0u || a.peer_wait != 0);
 #define MV(W, L, E)                                                                             \
     do {                                                                                        \
-        if (vec && mv2) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E, true>, g, st, d, a, y, rg, red_slot0, red_total); \
-        else if (vec) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E, false>, g, st, d, a, y, rg, red_slot0, red_total); \
+        if (vec && mv2) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E, true, false>, g, st, d, a, y, rg, red_slot0, red_total); \
+        else if (vec && L && hint) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E, false, true>, g, st, d, a, y, rg, red_slot0, red_total); \
+        else if (vec) launch_pdl(d.pdl != 0, k_matvec_vec2<W, L, E, false, false>, g, st, d, a, y, rg, red_slot0, red_total); \
         else k_matvec_flat<W, L, E><<<g, kThreads, 0, st>>>(d, a, y, rg, red_slot0, red_total);     \
     } while (0)
     if (exact) {

@@ -815,7 +815,11 @@ void plan_l2(maspcg_ctx *c, const double *x) {
     c->d.l2_mask = 0u;
     c->d.l2_frac = 1.f;
     c->l2_plan_bytes = 0;
-    if (!c->l2_keep || c->vmode || c->an_on || use_fused(c) || use_cg1(c) || use_wave(c) || use_persist(c, x)) return;
+    if (c->vmode) {   // the vector operator: the term rings of its chunked matvec (set at vv_set_workspace)
+        c->l2_plan_bytes = (c->l2_keep && c->vd.ring) ? vv_ring_bytes(c->vd, c->vd.ring) : 0;
+        return;
+    }
+    if (!c->l2_keep || c->an_on || use_fused(c) || use_cg1(c) || use_wave(c) || use_persist(c, x)) return;
     if (!c->d.vec_ok || (c->nr % 2) || ((uintptr_t)x & 15)) return;   // the 16-byte kernels carry the hints
     const double n8 = 8.0 * c->d.n, pl8 = 8.0 * c->d.plane;
     if (const char *e = getenv("MASPCG_L2_MASK")) {   // explicit plan (A/B runs)
@@ -853,7 +857,7 @@ void plan_l2(maspcg_ctx *c, const double *x) {
 
 // The persisting set-aside for a plan: exactly its kept bytes (device-wide limit; released at destroy).
 void l2_setaside(maspcg_ctx *c) {
-    if (!c->d.l2_mask) return;
+    if (!c->d.l2_mask && !c->l2_plan_bytes) return;
     const char *e = getenv("MASPCG_L2_PERSIST");
     if (e && !atoi(e)) return;
     size_t want = c->l2_plan_bytes;
@@ -1002,6 +1006,11 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
         launched += m;
         c->d.l2_mask = 0u;
         c->d.l2_frac = 1.f;
+    }
+    if (c->vmode && c->l2_plan_bytes) {   // the vector operator's term rings
+        const size_t rb = vv_ring_bytes(c->vd, c->vd.ring) / 4;
+        for (double *t : {c->va.E, c->va.TR, c->va.TT, c->va.TP}) launch_l2_demote(t, rb, st);
+        launched += 4;
     }
     c->a.peer_p_lo = c->a.peer_p_hi = nullptr;   // only the loop's p-updates store into the neighbours
     c->a.peer_flag_lo = c->a.peer_flag_hi = nullptr;
@@ -1702,6 +1711,16 @@ maspcg_status maspcg_vv_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes
     v.ncell = (uint32_t)((size_t)c->nloc * v.plane1);
     v.div_r = make_fastdiv((uint32_t)c->nr);
     v.div_t = make_fastdiv((uint32_t)c->nt);
+    v.kb = 0;
+    v.ke = c->nloc;
+    v.chunk = 0;
+    v.nchunks = 1;
+    // chunked matvec with L2-resident term rings (vv.cu): 0.45 of the L2, within the persisting maximum
+    {
+        double cap = c->l2_keep ? 0.45 * (double)c->l2_bytes : 0.0;
+        if (c->l2_persist_max && cap > (double)c->l2_persist_max) cap = (double)c->l2_persist_max;
+        v.ring = vv_ring_planes(v, (size_t)cap);
+    }
     c->vv_coef_set = c->vv_bc_set = false;
     c->vv_dirty = true;
     RET_IF(peer_register(c, 1, (char *)dev_ptr, need));

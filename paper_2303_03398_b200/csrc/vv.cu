@@ -49,6 +49,31 @@ __device__ __forceinline__ size_t UC(const VVDims &v, int k, int j, int i) {
     return (size_t)k * v.plane1 + (size_t)j * v.nr + i;
 }
 __device__ __forceinline__ size_t GW(const VVDims &v, int k, int c, int j) { return ((size_t)(k + 1) * 3 + c) * v.nt + j; }
+// term plane slot of plane k (-1 .. nloc): the full padded array, or the ring of the chunked matvec
+__device__ __forceinline__ uint32_t tslot(const VVDims &v, int k) {
+    const uint32_t kk = (uint32_t)(k + 1);
+    return v.ring ? kk % v.ring : kk;
+}
+// L2 policy of the term rings: evict_last (kept in the persisting set-aside) in ring mode, else normal
+__device__ __forceinline__ uint64_t term_policy(const VVDims &v) {
+    uint64_t pol;
+    if (v.ring) asm("createpolicy.fractional.L2::evict_last.b64 %0, 0f3F800000;" : "=l"(pol));
+    else asm("createpolicy.fractional.L2::evict_normal.b64 %0, 0f3F800000;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void S2T(double *p, double x, double y, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(x), "d"(y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double2 L2T(const double *p, uint64_t pol) {
+    double2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double L1T(const double *p, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
 
 // ------------------------------------------------------------ face geometry (R27; oracle A_r .. L_p)
 struct Geo {
@@ -512,17 +537,21 @@ __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1
 
 template <bool WALL>
 __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays a, DevArrays base, int loop) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // programmatic dependent launch (chunked matvec)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (loop && *(volatile int *)&base.sc->done) return;
     extern __shared__ double2 stg[];   // [2][kStg][kVVThreads]
     const Field<WALL> F{v, a, a.p, Geo{a}};
     const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t npair = (v.ncell + 2 * v.plane1) >> 1;   // planes -1 .. nloc
+    const uint32_t npair = ((uint32_t)(v.ke - v.kb + 2) * v.plane1) >> 1;   // planes kb-1 .. ke
+    const uint32_t c0 = (uint32_t)v.kb * v.plane1;
+    const uint64_t polT = term_policy(v);
     const int nr = v.nr, nt = v.nt;
     auto slot = [&](int stage, int s) -> double2 * { return stg + ((size_t)stage * kStg + s) * kVVThreads + threadIdx.x; };
     auto issue = [&](uint32_t t, int stage) {
         if (t < npair) {
             int i0, j, k;
-            cell_of(v, 2 * t, i0, j, k);
+            cell_of(v, 2 * t + c0, i0, j, k);
             k -= 1;
             const int km = k > -1 ? k - 1 : -1, kp = k < v.nloc ? k + 1 : v.nloc;
             const int jp = j < nt - 1 ? j + 1 : j, kw = k < 0 ? 0 : (k > v.nloc - 1 ? v.nloc - 1 : k);
@@ -554,9 +583,10 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays 
         cp_wait1();        // this thread's copies of stage st have landed
         __syncwarp(act);   // ... and the other lanes' (r2, pm1, tm1 come from the neighbouring lanes' slots)
         int i0, j, k;
-        cell_of(v, 2 * t, i0, j, k);
+        cell_of(v, 2 * t + c0, i0, j, k);
         k -= 1;
         const size_t pc = PC(v, k, j, i0);
+        const size_t pt = (size_t)tslot(v, k) * v.plane1 + (size_t)j * nr + i0;   // term slot
         const bool last = (i0 + 2 == nr);
         const double2 R = *slot(st, 0), T = *slot(st, 1), Pp = *slot(st, 2), Tj1 = *slot(st, 3), Pk1 = *slot(st, 4);
         const double2 Rm = *slot(st, 5), Tkm = *slot(st, 6), wt = *slot(st, 7), wr = *slot(st, 8), wp = *slot(st, 9);
@@ -570,16 +600,16 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays 
         const double tm1 = i0 == 0 ? 0.0 : (dn_in ? slot(st, 1)[-1].y : __ldg(a.p + PV(v, k, 1, j, i0 - 1)));
         const double vr0 = (i0 == 0) ? F.gi(k, 0, j) : R.x;          // v_r on r-face i0 (wall at 0)
         const double vr2 = last ? F.go(k, 0, j) : r2;
-        if (k <= v.nloc - 1) {
+        if (k <= v.ke - 1) {   // (ke <= nloc)
             const double e0 = F.ediv_w(i0, j, k, vr0, R.y, T.x, Tj1.x, Pp.x, Pk1.x, wcv.x);
             const double e1 = F.ediv_w(i0 + 1, j, k, R.y, vr2, T.y, Tj1.y, Pp.y, Pk1.y, wcv.y);
-            S2(a.E + pc, e0, e1);
+            S2T(a.E + pt, e0, e1, polT);
         }
-        if (k >= 0) {
+        if (k >= v.kb) {       // (kb >= 0)
             const double vrm0 = (i0 == 0) ? F.gi(k - 1, 0, j) : Rm.x;
             const double dn0 = (i0 == 0) ? F.gi(k, 2, j) : pm1;
-            S2(a.TT + pc, mul(wt.x, F.Gt_v(i0, j, k, vr0, vrm0, Pp.x, dn0)),
-               mul(wt.y, F.Gt_v(i0 + 1, j, k, R.y, Rm.y, Pp.y, Pp.x)));
+            S2T(a.TT + pt, mul(wt.x, F.Gt_v(i0, j, k, vr0, vrm0, Pp.x, dn0)),
+                mul(wt.y, F.Gt_v(i0 + 1, j, k, R.y, Rm.y, Pp.y, Pp.x)), polT);
             double tr0 = 0.0, tr1 = 0.0, tp0 = 0.0, tp1 = 0.0;
             if (j >= 1) {
                 tr0 = mul(wr.x, F.Gr_v(i0, j, k, Pp.x, Pjm.x, T.x, Tkm.x));
@@ -591,8 +621,8 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays 
                     tp1 = mul(wp.y, F.Gp_v(i0 + 1, j, T.y, T.x, R.y, Rjm.y));
                 }
             }
-            S2(a.TR + pc, tr0, tr1);
-            S2(a.TP + pc, tp0, tp1);
+            S2T(a.TR + pt, tr0, tr1, polT);
+            S2T(a.TP + pt, tp0, tp1, polT);
             if (last) {
                 const size_t w = (size_t)(k + 1) * nt + j;
                 a.TTO[w] = mul(__ldg(a.WtO + w), F.Gt_v(nr, j, k, F.go(k, 0, j), F.go(k - 1, 0, j), F.go(k, 2, j), Pp.y));
@@ -609,6 +639,8 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_terms3(VVDims v, VVArrays 
 template <bool WITH_DOT, bool LOOP, bool EXACT>
 __global__ void __launch_bounds__(kVVThreads, 2) k_vv_rows2(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
                                                          unsigned total) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (LOOP && *(volatile int *)&base.sc->done) return;
     const Geo g{a};
     const double *__restrict__ E = a.E;
@@ -616,33 +648,40 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_rows2(VVDims v, VVArrays a
     const uint32_t pl = v.plane1;
     Acc<EXACT> dot[1];
     const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t npair = v.ncell >> 1;
+    const uint32_t npair = ((uint32_t)(v.ke - v.kb) * v.plane1) >> 1;   // planes kb .. ke-1
+    const uint32_t c0 = (uint32_t)v.kb * v.plane1;
+    const uint64_t polT = term_policy(v);
     // (staging these streams with cp.async as in k_vv_terms3 measured slower here: 643 vs 513 us)
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += stride) {
         int i0, j, k;
-        cell_of(v, 2 * t, i0, j, k);
-        const size_t pc = PC(v, k, j, i0);
+        cell_of(v, 2 * t + c0, i0, j, k);
+        // term slots of planes k, k - 1, k + 1 (rings wrap)
+        const uint32_t s0 = tslot(v, k);
+        const uint32_t sm_ = v.ring ? (s0 == 0 ? v.ring - 1 : s0 - 1) : s0 - 1;
+        const uint32_t sp_ = v.ring ? (s0 + 1 == v.ring ? 0 : s0 + 1) : s0 + 1;
+        const size_t in = (size_t)j * nr + i0;
+        const size_t pc = (size_t)s0 * pl + in, pcm = (size_t)sm_ * pl + in, pcp = (size_t)sp_ * pl + in;
         const bool last = (i0 + 2 == nr);
-        const double2 e = L2(E + pc);
+        const double2 e = L2T(E + pc, polT);
         const double2 pr = L2(a.p + PV(v, k, 0, j, i0));
         const double2 pt = L2(a.p + PV(v, k, 1, j, i0));
         const double2 pp = L2(a.p + PV(v, k, 2, j, i0));
-        const double2 tt = L2(a.TT + pc);
-        const double2 tr = L2(a.TR + pc);
-        const double2 tp = L2(a.TP + pc);
+        const double2 tt = L2T(a.TT + pc, polT);
+        const double2 tr = L2T(a.TR + pc, polT);
+        const double2 tp = L2T(a.TP + pc, polT);
         const double2 sm0 = L2(a.sM + UV(v, k, 0, j, i0));
         const double2 sm1 = L2(a.sM + UV(v, k, 1, j, i0));
         const double2 sm2 = L2(a.sM + UV(v, k, 2, j, i0));
-        const double2 tt1 = L2(a.TT + pc + pl);
-        const double tt2 = last ? __ldg(a.TTO + (size_t)(k + 1) * nt + j) : __ldg(a.TT + pc + 2);
-        const double tp2 = last ? __ldg(a.TPO + (size_t)(k + 1) * nt + j) : __ldg(a.TP + pc + 2);
-        // the remaining streams up front (addresses inside the padded arrays; unused values discarded)
-        const double em1 = __ldg(E + pc - 1);
-        const double2 tpj = L2(a.TP + pc + nr);
-        const double2 ej = L2(E + pc - nr);
-        const double2 ek = L2(E + pc - pl);
-        const double2 tr1 = L2(a.TR + pc + pl);
-        const double2 trj = L2(a.TR + pc + nr);
+        const double2 tt1 = L2T(a.TT + pcp, polT);
+        const double tt2 = last ? __ldg(a.TTO + (size_t)(k + 1) * nt + j) : L1T(a.TT + pc + 2, polT);
+        const double tp2 = last ? __ldg(a.TPO + (size_t)(k + 1) * nt + j) : L1T(a.TP + pc + 2, polT);
+        // the remaining streams up front (addresses clamped inside the arrays; unused values discarded)
+        const double em1 = L1T(E + pc - (i0 > 0 ? 1 : 0), polT);
+        const double2 tpj = L2T(a.TP + pc + (j + 1 < nt ? nr : 0), polT);
+        const double2 ej = L2T(E + pc - (j > 0 ? nr : 0), polT);
+        const double2 ek = L2T(E + pcm, polT);
+        const double2 tr1 = L2T(a.TR + pcp, polT);
+        const double2 trj = L2T(a.TR + pc + (j + 1 < nt ? nr : 0), polT);
         // r-faces i0 (i0 >= 1) and i0 + 1
         double yr0 = 0.0, yr1;
         {
@@ -726,8 +765,27 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_rows2(VVDims v, VVArrays a
         Acc<EXACT> out[1];
         if (reduce_last<EXACT, kVVThreads, 1>(dot, base.partials, &base.sc->ticket[0], blockIdx.x, total, out)) {
             if (threadIdx.x == 0) {
-                base.sc->red1[0] = out[0].p;
-                base.sc->red1[1] = out[0].s;
+                if (v.nchunks <= 1) {
+                    base.sc->red1[0] = out[0].p;
+                    base.sc->red1[1] = out[0].s;
+                } else {
+                    // chunked matvec: this chunk's pair into slot `chunk` of the fourth partial row; the last
+                    // chunk combines all chunk pairs in chunk order (the earlier launches have completed)
+                    double *cp = base.partials + 6 * kPartialSlots;
+                    cp[v.chunk] = out[0].p;
+                    cp[kPartialSlots + v.chunk] = out[0].s;
+                    if (v.chunk == v.nchunks - 1) {
+                        Acc<EXACT> acc;
+                        for (int q = 0; q < v.nchunks; ++q) {
+                            Acc<EXACT> o;
+                            o.p = cp[q];
+                            o.s = cp[kPartialSlots + q];
+                            acc.add(o);
+                        }
+                        base.sc->red1[0] = acc.p;
+                        base.sc->red1[1] = acc.s;
+                    }
+                }
             }
         }
     }
@@ -1190,8 +1248,92 @@ bool launch_fused(const VVDims &v, const VVArrays &a, const DevArrays &base, dou
     return true;
 }
 
-void launch_vv_matvec(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
+uint32_t vv_ring_planes(const VVDims &v, size_t bytes) {
+    const char *e = getenv("MASPCG_VV_CHUNK");
+    if (e && !atoi(e)) return 0;
+    if (v.nr % 2) return 0;
+    if (e && atoi(e) > 2) {   // explicit ring planes (tests, A/B runs): chunks of ring - 2 planes
+        const uint32_t r = (uint32_t)atoi(e);
+        return (int)r - 2 < v.nloc ? r : 0;
+    }
+    const size_t per_plane = 4 * (size_t)v.plane1 * sizeof(double);
+    const uint32_t ring = (uint32_t)(bytes / per_plane);
+    if (ring < 8 || (int)ring - 2 >= v.nloc / 2) return 0;   // the chunks would be too thin, or <= 2 of them
+    return ring;
+}
+
+size_t vv_ring_bytes(const VVDims &v, uint32_t ring) { return 4 * (size_t)v.plane1 * ring * sizeof(double); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl_vv(void (*kern)(KArgs...), unsigned grid, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kVVThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// The chunked matvec: for chunks of K = ring - 2 planes, the terms of planes [kb - 1, ke] then the rows of
+// [kb, ke); the two recomputed boundary planes per chunk cost 2/K of phase 1.
+void launch_vv_chunked(const VVDims &v0, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
+                       bool exact, cudaStream_t st) {
+    const int K = (int)v0.ring - 2;
+    const int nch = (v0.nloc + K - 1) / K;
+    const size_t sm = sizeof(double2) * 2 * kStg * kVVThreads;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_vv_terms3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        VVDims v = v0;
+        v.kb = ch * K;
+        v.ke = v.kb + K < v0.nloc ? v.kb + K : v0.nloc;
+        v.chunk = ch;
+        v.nchunks = nch;
+        const uint32_t n1 = (uint32_t)(v.ke - v.kb + 2) * v.plane1;
+        // every launch with programmatic dependent launch: the next chunk's blocks are resident while the
+        // previous kernel drains (each kernel waits on griddepcontrol.wait before touching memory)
+        launch_pdl_vv(k_vv_terms3<false>, resident_grid(k_vv_terms3<false>, n1 / 2, sm), sm, st, v, a, base,
+                      loop ? 1 : 0);
+        const uint32_t n2 = (uint32_t)(v.ke - v.kb) * v.plane1;
+#define VRC(W, L, E)                                                                      \
+    do {                                                                                  \
+        const unsigned g = resident_grid(k_vv_rows2<W, L, E>, n2 / 2);                     \
+        launch_pdl_vv(k_vv_rows2<W, L, E>, g, 0, st, v, a, base, y, g);                    \
+    } while (0)
+        if (!with_dot) VRC(false, false, true);
+        else if (exact) {
+            if (loop) VRC(true, true, true);
+            else VRC(true, false, true);
+        } else {
+            if (loop) VRC(true, true, false);
+            else VRC(true, false, false);
+        }
+#undef VRC
+    }
+}
+
+void launch_vv_matvec(const VVDims &vin, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
                       bool wall, bool exact, cudaStream_t st) {
+    const bool pair0 = (vin.nr % 2 == 0) && (((uintptr_t)y & 15) == 0);
+    if (pair0 && !wall && vin.ring && vv_staged()) {   // chunked: the terms of a chunk stay in the L2 rings
+        launch_vv_chunked(vin, a, base, y, with_dot, loop, exact, st);
+        return;
+    }
+    // one pass over the whole slab with full-size term arrays (also the wall-data operator of the setup)
+    VVDims v = vin;
+    v.kb = 0;
+    v.ke = vin.nloc;
+    v.ring = 0;
+    v.chunk = 0;
+    v.nchunks = 1;
     if (!wall) {
         bool done;
         if (!with_dot) done = launch_fused<false, false, true>(v, a, base, y, st);
@@ -1201,7 +1343,7 @@ void launch_vv_matvec(const VVDims &v, const VVArrays &a, const DevArrays &base,
                          : launch_fused<true, false, false>(v, a, base, y, st);
         if (done) return;
     }
-    const bool pair = (v.nr % 2 == 0) && (((uintptr_t)y & 15) == 0);
+    const bool pair = pair0;
     const uint32_t nt1 = v.ncell + 2 * v.plane1;
     if (pair && vv_staged()) {
         const size_t sm = sizeof(double2) * 2 * kStg * kVVThreads;

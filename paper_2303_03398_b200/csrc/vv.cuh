@@ -23,6 +23,12 @@ struct VVDims {
     uint32_t ncell;         // nloc * nt * nr
     FastDiv div_r, div_t;
     int wall_in, wall_out;  // 0 no-slip, 1 free-slip
+    // chunked matvec (the pair kernels, homogeneous operator): the rows of planes [kb, ke) from the terms of
+    // planes [kb - 1, ke], which live in rings of `ring` planes (slot (k + 1) % ring) kept in the L2
+    // (evict_last inside a persisting set-aside); ring == 0: full-size term arrays, one chunk [0, nloc)
+    int kb, ke;
+    uint32_t ring;
+    int chunk, nchunks;     // the rows' Dot2: per-chunk pairs, combined by the last chunk's last block
 };
 
 struct VVArrays {
@@ -74,6 +80,10 @@ void launch_vv_diag(const VVDims &v, const VVArrays &a, cudaStream_t st);
 // partial p.y -> sc->red1 via the last block; loop: early exit when sc->done.
 void launch_vv_matvec(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
                       bool wall, bool exact, cudaStream_t st);
+// Planes per term ring of the chunked matvec for an L2 budget of `bytes` (0: the chunked form is off --
+// MASPCG_VV_CHUNK=0, odd nr, or a slab of at most two chunks), and the ring's bytes (4 term arrays).
+uint32_t vv_ring_planes(const VVDims &v, size_t bytes);
+size_t vv_ring_bytes(const VVDims &v, uint32_t ring);
 // b = M f - bw; r = b - q; z = r / D; p = z (padded, periodic copies when periodic_local);
 // Dot2 partials r.z, r.r, b.b -> sc->red3.
 void launch_vv_setup_residual(const VVDims &v, const VVArrays &a, const DevArrays &base, const Dims &dv,
