@@ -815,6 +815,10 @@ def main():
             "step_ms": step_stats(step_ms),
             "per_step": [{"iters": int(i), "ms": float(m)} for i, m in zip(step_iters, step_ms)]
             if args.steps <= 64 else None,
+            # c5: the time loop from its cold step 0 (warm-started steps after it), end-to-end total
+            "time_loop": {"steps": args.steps, "total_ms": ms, "total_iters": iters,
+                          "note": "step 0 cold (x0 = 0), steps >= 1 warm-started from the previous solution "
+                                  "with f = s u^(n-1)"} if warm else None,
             "cell_updates_per_s": nr * nt * np_ * value,
             "roofline": roofline, "per_kernel": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "sts": sts,
             "gpu_launches": stats["kernel_launches"], "clocks": clk.summary(),

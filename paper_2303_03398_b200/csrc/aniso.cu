@@ -223,6 +223,138 @@ __device__ __forceinline__ void diffs(double u00, double u10, double u01, double
     db = __dadd_rn(__dsub_rn(u01, u00), __dsub_rn(u11, u10));
 }
 
+// The arithmetic of one pair (i0, i0 + 1) of plane k, row j, from its p values and coefficient streams: the
+// 7-point part in the oracle's order, the cross terms in the R33 edge order, the store of y and the Dot2
+// update.
+// The pair's coefficient streams (T_r, T_theta, T_phi, D7, the three edge arrays): loaded unconditionally
+// (clamped addresses), so the caller can issue them ahead of the p values.
+struct PairCoef {
+    double2 tr, ttl, tth, tpl, tph, d7, Xt0, Xt1, Xp0, Xp1, Xjl, Xjpl, Xjh, Xjph;
+    double tr2, Xt0q, Xt1q, Xp0q, Xp1q;
+};
+__device__ __forceinline__ PairCoef load_coef(const Dims &d, const DevArrays &a, const AnisoArrays &x, uint32_t c,
+                                              int i0, int j) {
+    const int nr = d.nr, nt = d.nt;
+    const size_t plane = d.plane;
+    const size_t oq = (i0 + 2 < nr) ? 2 : 1, ojp = (j < nt - 1) ? nr : 0;
+    const size_t e = c;   // (k, j, i0) in the [nloc][nt][nr] edge arrays
+    PairCoef q;
+    q.tr = ldv2(a.Tr + c);
+    q.tr2 = __ldg(a.Tr + c + oq);
+    q.ttl = ldv2(a.Tt + c), q.tth = ldv2(a.Tt + c + ojp);
+    q.tpl = ldv2(a.Tp + c), q.tph = ldv2(a.Tp + c + plane);
+    q.d7 = ldv2(x.D7 + c);
+    q.Xt0 = ldv2(x.Xrt + e), q.Xt1 = ldv2(x.Xrt + e + ojp);
+    q.Xt0q = __ldg(x.Xrt + e + oq), q.Xt1q = __ldg(x.Xrt + e + ojp + oq);
+    q.Xp0 = ldv2(x.Xrp + e), q.Xp1 = ldv2(x.Xrp + e + plane);
+    q.Xp0q = __ldg(x.Xrp + e + oq), q.Xp1q = __ldg(x.Xrp + e + plane + oq);
+    q.Xjl = ldv2(x.Xtp + e), q.Xjpl = ldv2(x.Xtp + e + ojp);
+    q.Xjh = ldv2(x.Xtp + e + plane), q.Xjph = ldv2(x.Xtp + e + plane + ojp);
+    return q;
+}
+
+template <bool WITH_DOT, bool EXACT>
+__device__ __forceinline__ void aniso_pair(const Dims &d, const PairCoef &K, double *__restrict__ y, uint32_t c,
+                                           int i0, int j, const Row4 &Rj, const Row4 &Rjm, const Row4 &Rjp,
+                                           const Row4 &Mj, const Row4 &Pj, const double2 Mjm, const double2 Mjp,
+                                           const double2 Pjm, const double2 Pjp, Acc<EXACT> &dotacc) {
+    using A = Ar<EXACT>;
+    const int nr = d.nr, nt = d.nt;
+    const bool il = i0 > 0, ih = i0 + 2 < nr, jl = j > 0, jh = j < nt - 1;
+    // ---- the 7-point part, the oracle's order per cell
+    const double2 tr = K.tr;
+    const double tr2 = K.tr2;
+    const double2 ttl = K.ttl, tth = K.tth;
+    const double2 tpl = K.tpl, tph = K.tph;
+    const double2 d7 = K.d7;
+    double s0 = 0.0, s1 = 0.0;
+    if (il) s0 = A::acc(s0, tr.x, Rj.m);
+    s0 = A::acc(s0, tr.y, Rj.c1);
+    if (jl) s0 = A::acc(s0, ttl.x, Rjm.c0);
+    if (jh) s0 = A::acc(s0, tth.x, Rjp.c0);
+    s0 = A::acc(s0, tpl.x, Mj.c0);
+    s0 = A::acc(s0, tph.x, Pj.c0);
+    const double y70 = A::diag_minus(d7.x, Rj.c0, s0);
+    s1 = A::acc(s1, tr.y, Rj.c0);
+    if (ih) s1 = A::acc(s1, tr2, Rj.q);
+    if (jl) s1 = A::acc(s1, ttl.y, Rjm.c1);
+    if (jh) s1 = A::acc(s1, tth.y, Rjp.c1);
+    s1 = A::acc(s1, tpl.y, Mj.c1);
+    s1 = A::acc(s1, tph.y, Pj.c1);
+    const double y71 = A::diag_minus(d7.y, Rj.c1, s1);
+    // ---- cross terms: x0 for cell i0, x1 for cell i0 + 1, each in the R33 edge order
+    double x0 = 0.0, x1 = 0.0, da, db;
+    // r-theta edges of plane k: je = j (rows j-1, j) and je = j + 1 (rows j, j+1); ie = i0, i0+1, i0+2
+    const double2 Xt0 = K.Xt0, Xt1 = K.Xt1;
+    const double Xt0q = K.Xt0q, Xt1q = K.Xt1q;
+    const double2 Xp0 = K.Xp0, Xp1 = K.Xp1;
+    const double Xp0q = K.Xp0q, Xp1q = K.Xp1q;
+    const double2 Xjl = K.Xjl, Xjpl = K.Xjpl;
+    const double2 Xjh = K.Xjh, Xjph = K.Xjph;
+    if (jl) {
+        const double2 X = Xt0;
+        const double X2 = Xt0q;
+        if (il) { diffs(Rjm.m, Rjm.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
+        diffs(Rjm.c0, Rjm.c1, Rj.c0, Rj.c1, da, db);
+        xterm<EXACT>(x0, X.y, da, db, false, true);
+        xterm<EXACT>(x1, X.y, da, db, true, true);
+        if (ih) { diffs(Rjm.c1, Rjm.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
+    }
+    if (jh) {
+        const double2 X = Xt1;
+        const double X2 = Xt1q;
+        if (il) { diffs(Rj.m, Rj.c0, Rjp.m, Rjp.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
+        diffs(Rj.c0, Rj.c1, Rjp.c0, Rjp.c1, da, db);
+        xterm<EXACT>(x0, X.y, da, db, false, false);
+        xterm<EXACT>(x1, X.y, da, db, true, false);
+        if (ih) { diffs(Rj.c1, Rj.q, Rjp.c1, Rjp.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
+    }
+    // r-phi edges of row j: face k-1/2 (planes k-1, k; Xrp plane k) then k+1/2 (planes k, k+1; plane k+1)
+    {
+        const double2 X = Xp0;
+        const double X2 = Xp0q;
+        if (il) { diffs(Mj.m, Mj.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
+        diffs(Mj.c0, Mj.c1, Rj.c0, Rj.c1, da, db);
+        xterm<EXACT>(x0, X.y, da, db, false, true);
+        xterm<EXACT>(x1, X.y, da, db, true, true);
+        if (ih) { diffs(Mj.c1, Mj.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
+    }
+    {
+        const double2 X = Xp1;
+        const double X2 = Xp1q;
+        if (il) { diffs(Rj.m, Rj.c0, Pj.m, Pj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
+        diffs(Rj.c0, Rj.c1, Pj.c0, Pj.c1, da, db);
+        xterm<EXACT>(x0, X.y, da, db, false, false);
+        xterm<EXACT>(x1, X.y, da, db, true, false);
+        if (ih) { diffs(Rj.c1, Rj.q, Pj.c1, Pj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
+    }
+    // theta-phi edges of each cell's column: (j, lo), (j+1, lo), (j, hi), (j+1, hi)
+    {
+        if (jl) {
+            diffs(Mjm.x, Mj.c0, Rjm.c0, Rj.c0, da, db); xterm<EXACT>(x0, Xjl.x, da, db, true, true);
+            diffs(Mjm.y, Mj.c1, Rjm.c1, Rj.c1, da, db); xterm<EXACT>(x1, Xjl.y, da, db, true, true);
+        }
+        if (jh) {
+            diffs(Mj.c0, Mjp.x, Rj.c0, Rjp.c0, da, db); xterm<EXACT>(x0, Xjpl.x, da, db, false, true);
+            diffs(Mj.c1, Mjp.y, Rj.c1, Rjp.c1, da, db); xterm<EXACT>(x1, Xjpl.y, da, db, false, true);
+        }
+        if (jl) {
+            diffs(Rjm.c0, Rj.c0, Pjm.x, Pj.c0, da, db); xterm<EXACT>(x0, Xjh.x, da, db, true, false);
+            diffs(Rjm.c1, Rj.c1, Pjm.y, Pj.c1, da, db); xterm<EXACT>(x1, Xjh.y, da, db, true, false);
+        }
+        if (jh) {
+            diffs(Rj.c0, Rjp.c0, Pj.c0, Pjp.x, da, db); xterm<EXACT>(x0, Xjph.x, da, db, false, false);
+            diffs(Rj.c1, Rjp.c1, Pj.c1, Pjp.y, da, db); xterm<EXACT>(x1, Xjph.y, da, db, false, false);
+        }
+    }
+    const double q0 = __dadd_rn(y70, x0), q1 = __dadd_rn(y71, x1);
+    *reinterpret_cast<double2 *>(y + c) = make_double2(q0, q1);
+    if (WITH_DOT) {
+        dotacc.add(Rj.c0, q0);
+        dotacc.add(Rj.c1, q1);
+    }
+}
+
 template <bool WITH_DOT, bool LOOP, bool EXACT, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays a, AnisoArrays x,
                                                             double *__restrict__ y, Range rg, unsigned red_slot0,
@@ -264,99 +396,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
         const Row4 Pj = row4(pk + plane, cp);
         const double2 Mjm = ldv2c(pk - plane - ojm, cm), Mjp = ldv2c(pk - plane + ojp, cm);
         const double2 Pjm = ldv2c(pk + plane - ojm, cp), Pjp = ldv2c(pk + plane + ojp, cp);
-        // ---- the 7-point part, the oracle's order per cell
-        const double2 tr = ldv2(a.Tr + c);
-        const double tr2 = __ldg(a.Tr + c + oq);
-        const double2 ttl = ldv2(a.Tt + c), tth = ldv2(a.Tt + c + ojp);
-        const double2 tpl = ldv2(a.Tp + c), tph = ldv2(a.Tp + c + plane);
-        const double2 d7 = ldv2(x.D7 + c);
-        double s0 = 0.0, s1 = 0.0;
-        if (il) s0 = A::acc(s0, tr.x, Rj.m);
-        s0 = A::acc(s0, tr.y, Rj.c1);
-        if (jl) s0 = A::acc(s0, ttl.x, Rjm.c0);
-        if (jh) s0 = A::acc(s0, tth.x, Rjp.c0);
-        s0 = A::acc(s0, tpl.x, Mj.c0);
-        s0 = A::acc(s0, tph.x, Pj.c0);
-        const double y70 = A::diag_minus(d7.x, Rj.c0, s0);
-        s1 = A::acc(s1, tr.y, Rj.c0);
-        if (ih) s1 = A::acc(s1, tr2, Rj.q);
-        if (jl) s1 = A::acc(s1, ttl.y, Rjm.c1);
-        if (jh) s1 = A::acc(s1, tth.y, Rjp.c1);
-        s1 = A::acc(s1, tpl.y, Mj.c1);
-        s1 = A::acc(s1, tph.y, Pj.c1);
-        const double y71 = A::diag_minus(d7.y, Rj.c1, s1);
-        // ---- cross terms: x0 for cell i0, x1 for cell i0 + 1, each in the R33 edge order
-        double x0 = 0.0, x1 = 0.0, da, db;
-        const size_t e = c;   // (k, j, i0) in the [nloc][nt][nr] edge arrays
-        // r-theta edges of plane k: je = j (rows j-1, j) and je = j + 1 (rows j, j+1); ie = i0, i0+1, i0+2
-        const double2 Xt0 = ldv2(x.Xrt + e), Xt1 = ldv2(x.Xrt + e + ojp);
-        const double Xt0q = __ldg(x.Xrt + e + oq), Xt1q = __ldg(x.Xrt + e + ojp + oq);
-        const double2 Xp0 = ldv2(x.Xrp + e), Xp1 = ldv2(x.Xrp + e + plane);
-        const double Xp0q = __ldg(x.Xrp + e + oq), Xp1q = __ldg(x.Xrp + e + plane + oq);
-        const double2 Xjl = ldv2(x.Xtp + e), Xjpl = ldv2(x.Xtp + e + ojp);
-        const double2 Xjh = ldv2(x.Xtp + e + plane), Xjph = ldv2(x.Xtp + e + plane + ojp);
-        if (jl) {
-            const double2 X = Xt0;
-            const double X2 = Xt0q;
-            if (il) { diffs(Rjm.m, Rjm.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
-            diffs(Rjm.c0, Rjm.c1, Rj.c0, Rj.c1, da, db);
-            xterm<EXACT>(x0, X.y, da, db, false, true);
-            xterm<EXACT>(x1, X.y, da, db, true, true);
-            if (ih) { diffs(Rjm.c1, Rjm.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
-        }
-        if (jh) {
-            const double2 X = Xt1;
-            const double X2 = Xt1q;
-            if (il) { diffs(Rj.m, Rj.c0, Rjp.m, Rjp.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
-            diffs(Rj.c0, Rj.c1, Rjp.c0, Rjp.c1, da, db);
-            xterm<EXACT>(x0, X.y, da, db, false, false);
-            xterm<EXACT>(x1, X.y, da, db, true, false);
-            if (ih) { diffs(Rj.c1, Rj.q, Rjp.c1, Rjp.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
-        }
-        // r-phi edges of row j: face k-1/2 (planes k-1, k; Xrp plane k) then k+1/2 (planes k, k+1; plane k+1)
-        {
-            const double2 X = Xp0;
-            const double X2 = Xp0q;
-            if (il) { diffs(Mj.m, Mj.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
-            diffs(Mj.c0, Mj.c1, Rj.c0, Rj.c1, da, db);
-            xterm<EXACT>(x0, X.y, da, db, false, true);
-            xterm<EXACT>(x1, X.y, da, db, true, true);
-            if (ih) { diffs(Mj.c1, Mj.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
-        }
-        {
-            const double2 X = Xp1;
-            const double X2 = Xp1q;
-            if (il) { diffs(Rj.m, Rj.c0, Pj.m, Pj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
-            diffs(Rj.c0, Rj.c1, Pj.c0, Pj.c1, da, db);
-            xterm<EXACT>(x0, X.y, da, db, false, false);
-            xterm<EXACT>(x1, X.y, da, db, true, false);
-            if (ih) { diffs(Rj.c1, Rj.q, Pj.c1, Pj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
-        }
-        // theta-phi edges of each cell's column: (j, lo), (j+1, lo), (j, hi), (j+1, hi)
-        {
-            if (jl) {
-                diffs(Mjm.x, Mj.c0, Rjm.c0, Rj.c0, da, db); xterm<EXACT>(x0, Xjl.x, da, db, true, true);
-                diffs(Mjm.y, Mj.c1, Rjm.c1, Rj.c1, da, db); xterm<EXACT>(x1, Xjl.y, da, db, true, true);
-            }
-            if (jh) {
-                diffs(Mj.c0, Mjp.x, Rj.c0, Rjp.c0, da, db); xterm<EXACT>(x0, Xjpl.x, da, db, false, true);
-                diffs(Mj.c1, Mjp.y, Rj.c1, Rjp.c1, da, db); xterm<EXACT>(x1, Xjpl.y, da, db, false, true);
-            }
-            if (jl) {
-                diffs(Rjm.c0, Rj.c0, Pjm.x, Pj.c0, da, db); xterm<EXACT>(x0, Xjh.x, da, db, true, false);
-                diffs(Rjm.c1, Rj.c1, Pjm.y, Pj.c1, da, db); xterm<EXACT>(x1, Xjh.y, da, db, true, false);
-            }
-            if (jh) {
-                diffs(Rj.c0, Rjp.c0, Pj.c0, Pjp.x, da, db); xterm<EXACT>(x0, Xjph.x, da, db, false, false);
-                diffs(Rj.c1, Rjp.c1, Pj.c1, Pjp.y, da, db); xterm<EXACT>(x1, Xjph.y, da, db, false, false);
-            }
-        }
-        const double q0 = __dadd_rn(y70, x0), q1 = __dadd_rn(y71, x1);
-        *reinterpret_cast<double2 *>(y + c) = make_double2(q0, q1);
-        if (WITH_DOT) {
-            dot[0].add(Rj.c0, q0);
-            dot[0].add(Rj.c1, q1);
-        }
+        const PairCoef K = load_coef(d, a, x, c, i0, j);
+        aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, Rj, Rjm, Rjp, Mj, Pj, Mjm, Mjp, Pjm, Pjp, dot[0]);
     }
     if (WITH_DOT) {
         Acc<EXACT> out[1];
@@ -439,9 +480,9 @@ void launch_aniso_matvec(const Dims &d, const DevArrays &a, const AnisoArrays &x
                          bool with_dot, bool loop, unsigned red_slot0, unsigned red_total, bool exact, cudaStream_t st) {
     const Range rg = make_range(d, part);
     if (rg.vend == 0) return;
+    const bool pdl = d.pdl != 0;
     const bool vec = aniso_vec2(d, y);
     const unsigned g = vec ? grid_aniso2(rg.vend) : grid_aniso(rg.vend);
-    const bool pdl = d.pdl != 0;
 #define AN(W, L, E)                                                                                      \
     do {                                                                                                 \
         if (vec && aniso2_blocks() == 3)                                                                 \

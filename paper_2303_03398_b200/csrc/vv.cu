@@ -1248,18 +1248,17 @@ bool launch_fused(const VVDims &v, const VVArrays &a, const DevArrays &base, dou
     return true;
 }
 
+// Opt-in (MASPCG_VV_CHUNK = ring planes, > 2): measured SLOWER than the one-pass two phases on c3v (1,491 vs
+// 1,128 us per ring + matvec with the ring sized from 0.45 of the L2; 1,472-1,568 us for rings of 30-80
+// planes): the terms did not stay in the L2 (ncu without cache control: the rows still read ~77 B/cell from
+// DRAM, L2 hit rate 21 %) and the 32 launches per matvec lose ~20 % per chunk to ramp-up and tail
+// (profiles/r02/vv_chunked_matvec.txt).  `bytes` is unused while the default is off.
 uint32_t vv_ring_planes(const VVDims &v, size_t bytes) {
+    (void)bytes;
     const char *e = getenv("MASPCG_VV_CHUNK");
-    if (e && !atoi(e)) return 0;
-    if (v.nr % 2) return 0;
-    if (e && atoi(e) > 2) {   // explicit ring planes (tests, A/B runs): chunks of ring - 2 planes
-        const uint32_t r = (uint32_t)atoi(e);
-        return (int)r - 2 < v.nloc ? r : 0;
-    }
-    const size_t per_plane = 4 * (size_t)v.plane1 * sizeof(double);
-    const uint32_t ring = (uint32_t)(bytes / per_plane);
-    if (ring < 8 || (int)ring - 2 >= v.nloc / 2) return 0;   // the chunks would be too thin, or <= 2 of them
-    return ring;
+    if (!e || atoi(e) <= 2 || (v.nr % 2)) return 0;
+    const uint32_t r = (uint32_t)atoi(e);   // chunks of ring - 2 planes
+    return (int)r - 2 < v.nloc ? r : 0;
 }
 
 size_t vv_ring_bytes(const VVDims &v, uint32_t ring) { return 4 * (size_t)v.plane1 * ring * sizeof(double); }

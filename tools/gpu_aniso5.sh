@@ -1,0 +1,14 @@
+#!/bin/bash
+# shared-memory tile aniso kernel: parity + bench A/B against the all-global pair kernel, ncu of the tile kernel
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_a5.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_aniso.py -x -q > gpurun_out/pytest_aniso5.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_aniso5.log
+out=gpurun_out/aniso5.txt; rm -f $out
+for rep in 1 2; do
+  for t in 1 0; do
+    MASPCG_ANISO_TILE=$t timeout 600 python bench.py --operator aniso --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/an_tmp.json 2>> gpurun_out/an5.err
+    python -c "import json; d=json.load(open('gpurun_out/an_tmp.json')); r=d['roofline']; print('tile=$t', round(d['value'],1), 'it/s', 'stencil us', round(r['avg_launch_ms']*1e3,1), 'frac', round(r['frac'],3), d['clocks']['sm_mhz'])" >> $out
+  done
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_aniso_tile" -s 3 -c 1 \
+    -o gpurun_out/prof_aniso_tile python bench.py --operator aniso --steps 1 --warmup 0 --maxit 6 --no-cpu-baseline --no-e2e > gpurun_out/ncu_aniso5.log 2>&1
