@@ -190,3 +190,58 @@ def test_peer_single_rank_c3_full_size(M, oracle_mod):
     p.tol, p.maxit = 0.0, 20
     st, info, hist, x = solve(M, p, 1, 1, fuse_halo=2)
     assert info["iters"] == 20 and np.array_equal(hist, o["hist"]) and np.array_equal(x, o["x"])
+
+
+def _stress_worker(rank, world, port, out_dir):
+    """Many peer-mode iterations with random per-rank delays: a host sleep and a GPU spin kernel of random
+    length before every solve, so the ranks' stencils start at different times and the halo acquire / the
+    coherent halo loads (DESIGN 9; ld.global.cg after ld.acquire.sys) are exercised under skew."""
+    import sys
+    import time
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2303_03398_b200 import maspcg
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    rng = np.random.default_rng(1000 + rank)
+    out = {}
+    try:
+        for name, fn in [("rand", lambda k0, n: inputs.random_problem(12, 10, 8, 41, k0=k0 or 0, nloc=n)),
+                         ("aniso", lambda k0, n: inputs.random_aniso_problem(12, 10, 8, 42, k0=k0 or 0, nloc=n))]:
+            k0, nloc = inputs.slab_extent(8, rank, world)
+            p = fn(k0, nloc)
+            S = maspcg.solver_for_problem(p, comm="peer")
+            S.set_option(maspcg.OPT_FUSE_HALO, 2)     # the stencil blocks acquire the halo flags themselves
+            for rep in range(6):
+                time.sleep(float(rng.uniform(0.0, 0.03)))
+                torch.cuda._sleep(int(rng.integers(0, 2_000_000)))   # a GPU-side delay on this rank's stream
+                x = T(p.x0)
+                st, info, hist = S.solve(T(p.f), x, 0.0, 300)
+                torch.cuda.synchronize()
+                out[(name, rep)] = (st, info["iters"], hist, x.cpu().numpy())
+            dist.barrier()
+            S.close()
+        np.save(os.path.join(out_dir, f"stress{rank}.npy"), out, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_stress_random_delays(tmp_path, oracle_mod, world):
+    """world processes, 300 iterations x 6 solves each of the 7-point and the field-aligned operators with
+    random host and GPU delays per rank before every solve: every solve equals the oracle's 300 iterates
+    bit for bit on every rank."""
+    import torch.multiprocessing as mp
+    mp.spawn(_stress_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    res = [np.load(tmp_path / f"stress{r}.npy", allow_pickle=True).item() for r in range(world)]
+    ref = {"rand": oracle_mod.solve_problem(inputs.random_problem(12, 10, 8, 41), tol=0.0, maxit=300),
+           "aniso": oracle_mod.solve_aniso_problem(inputs.random_aniso_problem(12, 10, 8, 42), tol=0.0, maxit=300)}
+    for name, o in ref.items():
+        for rep in range(6):
+            for r in res:
+                st, it, hist, _ = r[(name, rep)]
+                assert st == o["status"] and it == o["iters"] == 300 and np.array_equal(hist, o["hist"]), (name, rep)
+            x = np.concatenate([r[(name, rep)][3] for r in res], axis=0)
+            assert np.array_equal(x, o["x"]), (name, rep)
