@@ -11,6 +11,10 @@
 // cell's 12 edges, in the fixed R33 order, of Xq (s_a db + s_b da), da and db the sums of the edge's
 // two a- and b-differences.  Bandwidth: p (8, neighbours from L1/L2), T_r, T_theta, T_phi, D7 (32),
 // Xrt, Xrp, Xtp (24), y (8) = 72 B/cell of algorithmic traffic per apply.
+//
+// Kernels: k_aniso_tma (default: p rows staged by 1-D bulk copies into double-buffered shared-memory tiles),
+// k_aniso_vec2 (two cells per thread from global memory; the split boundary launch of a multi-rank stencil),
+// k_aniso_flat (one cell per thread, odd nr), k_aniso_edges / k_aniso_diag (setup).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -253,11 +257,19 @@ __device__ __forceinline__ PairCoef load_coef(const Dims &d, const DevArrays &a,
     return q;
 }
 
-template <bool WITH_DOT, bool EXACT>
+// Access to a pair's p values (the arithmetic below is written against these accessors).
+__device__ __forceinline__ double g_m(const Row4 &r) { return r.m; }
+__device__ __forceinline__ double g_c0(const Row4 &r) { return r.c0; }
+__device__ __forceinline__ double g_c1(const Row4 &r) { return r.c1; }
+__device__ __forceinline__ double g_q(const Row4 &r) { return r.q; }
+__device__ __forceinline__ double g_x(const double2 &v) { return v.x; }
+__device__ __forceinline__ double g_y(const double2 &v) { return v.y; }
+
+template <bool WITH_DOT, bool EXACT, typename R4, typename R2>
 __device__ __forceinline__ void aniso_pair(const Dims &d, const PairCoef &K, double *__restrict__ y, uint32_t c,
-                                           int i0, int j, const Row4 &Rj, const Row4 &Rjm, const Row4 &Rjp,
-                                           const Row4 &Mj, const Row4 &Pj, const double2 Mjm, const double2 Mjp,
-                                           const double2 Pjm, const double2 Pjp, Acc<EXACT> &dotacc) {
+                                           int i0, int j, const R4 &Rj, const R4 &Rjm, const R4 &Rjp,
+                                           const R4 &Mj, const R4 &Pj, const R2 &Mjm, const R2 &Mjp,
+                                           const R2 &Pjm, const R2 &Pjp, Acc<EXACT> &dotacc) {
     using A = Ar<EXACT>;
     const int nr = d.nr, nt = d.nt;
     const bool il = i0 > 0, ih = i0 + 2 < nr, jl = j > 0, jh = j < nt - 1;
@@ -268,20 +280,20 @@ __device__ __forceinline__ void aniso_pair(const Dims &d, const PairCoef &K, dou
     const double2 tpl = K.tpl, tph = K.tph;
     const double2 d7 = K.d7;
     double s0 = 0.0, s1 = 0.0;
-    if (il) s0 = A::acc(s0, tr.x, Rj.m);
-    s0 = A::acc(s0, tr.y, Rj.c1);
-    if (jl) s0 = A::acc(s0, ttl.x, Rjm.c0);
-    if (jh) s0 = A::acc(s0, tth.x, Rjp.c0);
-    s0 = A::acc(s0, tpl.x, Mj.c0);
-    s0 = A::acc(s0, tph.x, Pj.c0);
-    const double y70 = A::diag_minus(d7.x, Rj.c0, s0);
-    s1 = A::acc(s1, tr.y, Rj.c0);
-    if (ih) s1 = A::acc(s1, tr2, Rj.q);
-    if (jl) s1 = A::acc(s1, ttl.y, Rjm.c1);
-    if (jh) s1 = A::acc(s1, tth.y, Rjp.c1);
-    s1 = A::acc(s1, tpl.y, Mj.c1);
-    s1 = A::acc(s1, tph.y, Pj.c1);
-    const double y71 = A::diag_minus(d7.y, Rj.c1, s1);
+    if (il) s0 = A::acc(s0, tr.x, g_m(Rj));
+    s0 = A::acc(s0, tr.y, g_c1(Rj));
+    if (jl) s0 = A::acc(s0, ttl.x, g_c0(Rjm));
+    if (jh) s0 = A::acc(s0, tth.x, g_c0(Rjp));
+    s0 = A::acc(s0, tpl.x, g_c0(Mj));
+    s0 = A::acc(s0, tph.x, g_c0(Pj));
+    const double y70 = A::diag_minus(d7.x, g_c0(Rj), s0);
+    s1 = A::acc(s1, tr.y, g_c0(Rj));
+    if (ih) s1 = A::acc(s1, tr2, g_q(Rj));
+    if (jl) s1 = A::acc(s1, ttl.y, g_c1(Rjm));
+    if (jh) s1 = A::acc(s1, tth.y, g_c1(Rjp));
+    s1 = A::acc(s1, tpl.y, g_c1(Mj));
+    s1 = A::acc(s1, tph.y, g_c1(Pj));
+    const double y71 = A::diag_minus(d7.y, g_c1(Rj), s1);
     // ---- cross terms: x0 for cell i0, x1 for cell i0 + 1, each in the R33 edge order
     double x0 = 0.0, x1 = 0.0, da, db;
     // r-theta edges of plane k: je = j (rows j-1, j) and je = j + 1 (rows j, j+1); ie = i0, i0+1, i0+2
@@ -294,64 +306,64 @@ __device__ __forceinline__ void aniso_pair(const Dims &d, const PairCoef &K, dou
     if (jl) {
         const double2 X = Xt0;
         const double X2 = Xt0q;
-        if (il) { diffs(Rjm.m, Rjm.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
-        diffs(Rjm.c0, Rjm.c1, Rj.c0, Rj.c1, da, db);
+        if (il) { diffs(g_m(Rjm), g_c0(Rjm), g_m(Rj), g_c0(Rj), da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
+        diffs(g_c0(Rjm), g_c1(Rjm), g_c0(Rj), g_c1(Rj), da, db);
         xterm<EXACT>(x0, X.y, da, db, false, true);
         xterm<EXACT>(x1, X.y, da, db, true, true);
-        if (ih) { diffs(Rjm.c1, Rjm.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
+        if (ih) { diffs(g_c1(Rjm), g_q(Rjm), g_c1(Rj), g_q(Rj), da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
     }
     if (jh) {
         const double2 X = Xt1;
         const double X2 = Xt1q;
-        if (il) { diffs(Rj.m, Rj.c0, Rjp.m, Rjp.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
-        diffs(Rj.c0, Rj.c1, Rjp.c0, Rjp.c1, da, db);
+        if (il) { diffs(g_m(Rj), g_c0(Rj), g_m(Rjp), g_c0(Rjp), da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
+        diffs(g_c0(Rj), g_c1(Rj), g_c0(Rjp), g_c1(Rjp), da, db);
         xterm<EXACT>(x0, X.y, da, db, false, false);
         xterm<EXACT>(x1, X.y, da, db, true, false);
-        if (ih) { diffs(Rj.c1, Rj.q, Rjp.c1, Rjp.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
+        if (ih) { diffs(g_c1(Rj), g_q(Rj), g_c1(Rjp), g_q(Rjp), da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
     }
     // r-phi edges of row j: face k-1/2 (planes k-1, k; Xrp plane k) then k+1/2 (planes k, k+1; plane k+1)
     {
         const double2 X = Xp0;
         const double X2 = Xp0q;
-        if (il) { diffs(Mj.m, Mj.c0, Rj.m, Rj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
-        diffs(Mj.c0, Mj.c1, Rj.c0, Rj.c1, da, db);
+        if (il) { diffs(g_m(Mj), g_c0(Mj), g_m(Rj), g_c0(Rj), da, db); xterm<EXACT>(x0, X.x, da, db, true, true); }
+        diffs(g_c0(Mj), g_c1(Mj), g_c0(Rj), g_c1(Rj), da, db);
         xterm<EXACT>(x0, X.y, da, db, false, true);
         xterm<EXACT>(x1, X.y, da, db, true, true);
-        if (ih) { diffs(Mj.c1, Mj.q, Rj.c1, Rj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
+        if (ih) { diffs(g_c1(Mj), g_q(Mj), g_c1(Rj), g_q(Rj), da, db); xterm<EXACT>(x1, X2, da, db, false, true); }
     }
     {
         const double2 X = Xp1;
         const double X2 = Xp1q;
-        if (il) { diffs(Rj.m, Rj.c0, Pj.m, Pj.c0, da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
-        diffs(Rj.c0, Rj.c1, Pj.c0, Pj.c1, da, db);
+        if (il) { diffs(g_m(Rj), g_c0(Rj), g_m(Pj), g_c0(Pj), da, db); xterm<EXACT>(x0, X.x, da, db, true, false); }
+        diffs(g_c0(Rj), g_c1(Rj), g_c0(Pj), g_c1(Pj), da, db);
         xterm<EXACT>(x0, X.y, da, db, false, false);
         xterm<EXACT>(x1, X.y, da, db, true, false);
-        if (ih) { diffs(Rj.c1, Rj.q, Pj.c1, Pj.q, da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
+        if (ih) { diffs(g_c1(Rj), g_q(Rj), g_c1(Pj), g_q(Pj), da, db); xterm<EXACT>(x1, X2, da, db, false, false); }
     }
     // theta-phi edges of each cell's column: (j, lo), (j+1, lo), (j, hi), (j+1, hi)
     {
         if (jl) {
-            diffs(Mjm.x, Mj.c0, Rjm.c0, Rj.c0, da, db); xterm<EXACT>(x0, Xjl.x, da, db, true, true);
-            diffs(Mjm.y, Mj.c1, Rjm.c1, Rj.c1, da, db); xterm<EXACT>(x1, Xjl.y, da, db, true, true);
+            diffs(g_x(Mjm), g_c0(Mj), g_c0(Rjm), g_c0(Rj), da, db); xterm<EXACT>(x0, Xjl.x, da, db, true, true);
+            diffs(g_y(Mjm), g_c1(Mj), g_c1(Rjm), g_c1(Rj), da, db); xterm<EXACT>(x1, Xjl.y, da, db, true, true);
         }
         if (jh) {
-            diffs(Mj.c0, Mjp.x, Rj.c0, Rjp.c0, da, db); xterm<EXACT>(x0, Xjpl.x, da, db, false, true);
-            diffs(Mj.c1, Mjp.y, Rj.c1, Rjp.c1, da, db); xterm<EXACT>(x1, Xjpl.y, da, db, false, true);
+            diffs(g_c0(Mj), g_x(Mjp), g_c0(Rj), g_c0(Rjp), da, db); xterm<EXACT>(x0, Xjpl.x, da, db, false, true);
+            diffs(g_c1(Mj), g_y(Mjp), g_c1(Rj), g_c1(Rjp), da, db); xterm<EXACT>(x1, Xjpl.y, da, db, false, true);
         }
         if (jl) {
-            diffs(Rjm.c0, Rj.c0, Pjm.x, Pj.c0, da, db); xterm<EXACT>(x0, Xjh.x, da, db, true, false);
-            diffs(Rjm.c1, Rj.c1, Pjm.y, Pj.c1, da, db); xterm<EXACT>(x1, Xjh.y, da, db, true, false);
+            diffs(g_c0(Rjm), g_c0(Rj), g_x(Pjm), g_c0(Pj), da, db); xterm<EXACT>(x0, Xjh.x, da, db, true, false);
+            diffs(g_c1(Rjm), g_c1(Rj), g_y(Pjm), g_c1(Pj), da, db); xterm<EXACT>(x1, Xjh.y, da, db, true, false);
         }
         if (jh) {
-            diffs(Rj.c0, Rjp.c0, Pj.c0, Pjp.x, da, db); xterm<EXACT>(x0, Xjph.x, da, db, false, false);
-            diffs(Rj.c1, Rjp.c1, Pj.c1, Pjp.y, da, db); xterm<EXACT>(x1, Xjph.y, da, db, false, false);
+            diffs(g_c0(Rj), g_c0(Rjp), g_c0(Pj), g_x(Pjp), da, db); xterm<EXACT>(x0, Xjph.x, da, db, false, false);
+            diffs(g_c1(Rj), g_c1(Rjp), g_c1(Pj), g_y(Pjp), da, db); xterm<EXACT>(x1, Xjph.y, da, db, false, false);
         }
     }
     const double q0 = __dadd_rn(y70, x0), q1 = __dadd_rn(y71, x1);
     *reinterpret_cast<double2 *>(y + c) = make_double2(q0, q1);
     if (WITH_DOT) {
-        dotacc.add(Rj.c0, q0);
-        dotacc.add(Rj.c1, q1);
+        dotacc.add(g_c0(Rj), q0);
+        dotacc.add(g_c1(Rj), q1);
     }
 }
 
@@ -412,6 +424,156 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_vec2(Dims d, DevArrays
     }
 }
 
+// ---------------------------------------------------------------- operator apply, TMA-staged tiles
+// A block walks 256-pair chunks (512 consecutive cells: a few rows of one or two planes).  The p rows a chunk
+// needs -- rows R0 - 1 .. R1 + 1 of planes k - 1, k, k + 1, three contiguous ranges of the padded p -- are
+// brought into shared memory by three 1-D bulk copies (cp.async.bulk, the Tensor Memory Accelerator) issued
+// by one thread and counted on an mbarrier, double-buffered: the copies of chunk n + 1 are in flight while
+// chunk n is computed.  No per-element staging arithmetic, no global p loads in the compute; the coefficient
+// streams are loaded per thread as in the pair kernel.
+constexpr int kTilePairs = kThreads;
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init1(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+// p + off as one explicit 64-bit add (a bulk-copy source address; see fused.cu for the ptxas 12.9 issue)
+__device__ __forceinline__ const double *gaddr64(const double *p, size_t off) {
+    const double *r;
+    asm("add.s64 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(off * sizeof(double)));
+    return r;
+}
+
+template <bool WITH_DOT, bool LOOP, bool EXACT, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_aniso_tma(Dims d, DevArrays a, AnisoArrays x, double *__restrict__ y,
+                                                           Range rg, unsigned red_slot0, unsigned red_total,
+                                                           int maxrows) {
+    extern __shared__ __align__(128) double tiles[];   // [2 stages][3 planes][maxrows][nr]
+    __shared__ __align__(8) uint64_t bars[2];
+    pdl_wait();
+    pdl_trigger();
+    if (LOOP && *(volatile int *)&a.sc->done) return;
+    if (LOOP && a.peer_wait) acquire_p_halo(a);   // before any copy of a (peer-written) halo plane
+    const int nr = d.nr, nt = d.nt;
+    const int rows_pad = (d.nloc + 2) * nt;         // rows of the padded p
+    const uint32_t npair = rg.vend >> 1;            // a range without a split (full slab or interior planes)
+    const uint32_t nch = (npair + kTilePairs - 1) / kTilePairs;
+    const size_t stage = (size_t)3 * maxrows * nr;
+    const double *const gp = a.p;
+    if (threadIdx.x == 0) {
+        mbar_init1(&bars[0]);
+        mbar_init1(&bars[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // the staged rows of chunk ch: Ra = R0 - 1 .. R1 + 1 (slab rows k nt + j)
+    auto rows_of = [&](uint32_t ch, int &Ra, int &nrows) {
+        const uint32_t v0 = ch * kTilePairs;
+        const uint32_t v1 = v0 + kTilePairs < npair ? v0 + kTilePairs : npair;
+        const int R0 = (int)d.div_r.div(2u * v0 + rg.off0);
+        const int R1 = (int)d.div_r.div(2u * (v1 - 1) + 1u + rg.off0);
+        Ra = R0 - 1;
+        nrows = R1 - R0 + 3;
+    };
+    auto issue = [&](uint32_t ch, int st) {   // thread 0: three bulk copies into stage st
+        int Ra, nrows;
+        rows_of(ch, Ra, nrows);
+        uint32_t bytes = 0;
+        int lo[3], n[3];
+        for (int pl = 0; pl < 3; ++pl) {
+            int r0 = Ra + nt + (pl - 1) * nt, r1 = r0 + nrows;   // padded rows [r0, r1)
+            lo[pl] = r0 < 0 ? -r0 : 0;                           // rows outside the padded array are never read
+            r0 = r0 < 0 ? 0 : r0;
+            r1 = r1 > rows_pad ? rows_pad : r1;
+            n[pl] = r1 - r0;
+            bytes += (uint32_t)(n[pl] * nr * sizeof(double));
+        }
+        mbar_expect(&bars[st], bytes);
+        for (int pl = 0; pl < 3; ++pl) {
+            const int r0 = Ra + nt + (pl - 1) * nt + lo[pl];
+            double *dst = tiles + (size_t)st * stage + ((size_t)pl * maxrows + lo[pl]) * nr;
+            bulk_copy(dst, gaddr64(gp, (size_t)r0 * nr), (uint32_t)(n[pl] * nr * sizeof(double)), &bars[st]);
+        }
+    };
+    Acc<EXACT> dot[1];
+    uint32_t use[2] = {0u, 0u};
+    const uint32_t first = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (first < nch) issue(first, 0);
+        if (first + gridDim.x < nch) issue(first + gridDim.x, 1);
+    }
+    int it = 0;
+    for (uint32_t ch = first; ch < nch; ch += gridDim.x, ++it) {
+        const int st = it & 1;
+        const uint32_t v0 = ch * kTilePairs;
+        const uint32_t v1 = v0 + kTilePairs < npair ? v0 + kTilePairs : npair;
+        const uint32_t v = v0 + threadIdx.x;
+        const bool mine = v < v1;
+        const uint32_t c = 2u * (mine ? v : v0) + rg.off0;
+        int i0, j, k;
+        decompose(d, c, i0, j, k);
+        int Ra, nrows;
+        rows_of(ch, Ra, nrows);
+        mbar_wait_parity(&bars[st], use[st] & 1u);
+        ++use[st];
+        if (mine) {
+            // (loading the coefficients before the wait, or reading the tile lazily at each use, measured
+            // slower: 625 vs 580-588 us per launch on c3a -- more registers live across the wait)
+            const PairCoef K = load_coef(d, a, x, c, i0, j);
+            const double *tb = tiles + (size_t)st * stage;
+            const int lr = k * nt + j - Ra;   // 1 .. nrows - 2
+            const int im = i0 > 0 ? i0 - 1 : i0, iq = i0 + 2 < nr ? i0 + 2 : i0 + 1;
+            auto T = [&](int pl, int dr) -> const double * { return tb + ((size_t)pl * maxrows + lr + dr) * nr; };
+            auto row4 = [&](const double *r) {
+                const double2 v2 = *reinterpret_cast<const double2 *>(r + i0);
+                return Row4{r[im], v2.x, v2.y, r[iq]};
+            };
+            auto pr2 = [&](const double *r) { return *reinterpret_cast<const double2 *>(r + i0); };
+            aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, row4(T(1, 0)), row4(T(1, -1)), row4(T(1, 1)),
+                                        row4(T(0, 0)), row4(T(2, 0)), pr2(T(0, -1)), pr2(T(0, 1)), pr2(T(2, -1)),
+                                        pr2(T(2, 1)), dot[0]);
+        }
+        __syncthreads();   // every thread is done with stage st
+        if (threadIdx.x == 0 && ch + 2 * gridDim.x < nch) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(ch + 2 * gridDim.x, st);
+        }
+    }
+    if (WITH_DOT) {
+        Acc<EXACT> out[1];
+        if (reduce_last<EXACT, kThreads, 1>(dot, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total,
+                                            out)) {
+            if (threadIdx.x == 0) {
+                a.sc->red1[0] = out[0].p;
+                a.sc->red1[1] = out[0].s;
+                if (a.p2p_ll) ll_push_pairs(a, a.sc->red1, 1);   // to every rank (peer communicator)
+            }
+        }
+    }
+}
+
+inline int tile_rows(int nr) { return (2 * kTilePairs + nr - 1) / nr + 3; }
+inline size_t tile_smem(int nr) { return sizeof(double) * 2 * 3 * (size_t)tile_rows(nr) * nr; }
+
 inline unsigned grid_aniso(uint32_t n) {
     uint64_t g = (n + kThreads - 1) / kThreads;
     if (g < 1) g = 1;
@@ -446,6 +608,22 @@ inline unsigned grid_setup(uint32_t n) {
 }
 
 template <typename... KArgs, typename... Args>
+void launch_pdl_aniso_smem(bool pdl, void (*kern)(KArgs...), unsigned grid, size_t smem, cudaStream_t st,
+                           Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
 void launch_pdl_aniso(bool pdl, void (*kern)(KArgs...), unsigned grid, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -470,9 +648,31 @@ void launch_aniso_diag(const Dims &d, const DevArrays &a, const AnisoArrays &x, 
     k_aniso_diag<<<grid_setup(d.n), kThreads, 0, st>>>(d, a, x);
 }
 
+// the TMA tile kernel: pair layout and a range without a split (MASPCG_ANISO_TMA=0 selects the all-global
+// pair kernel for comparisons)
+inline bool aniso_tma(const Dims &d, const double *y, const Range &rg) {
+    static const int on = getenv("MASPCG_ANISO_TMA") ? atoi(getenv("MASPCG_ANISO_TMA")) : 1;
+    return on && aniso_vec2(d, y) && rg.split == 0xffffffffu;
+}
+
+// resident blocks per SM of the TMA kernel: 2 (default, 128 registers) or MASPCG_ANISO_TMA_BLOCKS = 3 (80
+// registers with spills; measured slower, 669 vs 625 us)
+inline int tma_blocks() {
+    static const int b = getenv("MASPCG_ANISO_TMA_BLOCKS") ? atoi(getenv("MASPCG_ANISO_TMA_BLOCKS")) : 2;
+    return b == 3 ? 3 : 2;
+}
+
+inline unsigned grid_tma(uint32_t n) {   // n cells: 256-pair chunks, a resident grid
+    uint64_t g = ((uint64_t)n / 2 + kTilePairs - 1) / kTilePairs;
+    if (g < 1) g = 1;
+    if (g > (uint64_t)(148 * tma_blocks())) g = 148 * tma_blocks();
+    return (unsigned)g;
+}
+
 unsigned aniso_stencil_blocks(const Dims &d, StencilPart part, const double *y) {
     const Range rg = make_range(d, part);
     if (!rg.vend) return 0u;
+    if (aniso_tma(d, y, rg)) return grid_tma(rg.vend);
     return aniso_vec2(d, y) ? grid_aniso2(rg.vend) : grid_aniso(rg.vend);
 }
 
@@ -481,6 +681,34 @@ void launch_aniso_matvec(const Dims &d, const DevArrays &a, const AnisoArrays &x
     const Range rg = make_range(d, part);
     if (rg.vend == 0) return;
     const bool pdl = d.pdl != 0;
+    if (aniso_tma(d, y, rg)) {
+        const unsigned g = grid_tma(rg.vend);
+        const size_t sm = tile_smem(d.nr);
+        const int mr = tile_rows(d.nr);
+#define TM(W, L, E)                                                                                           \
+    do {                                                                                                      \
+        if (tma_blocks() == 2) {                                                                              \
+            cudaFuncSetAttribute(k_aniso_tma<W, L, E, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+            launch_pdl_aniso_smem(pdl, k_aniso_tma<W, L, E, 2>, g, sm, st, d, a, x, y, rg, red_slot0, red_total, mr); \
+        } else {                                                                                              \
+            cudaFuncSetAttribute(k_aniso_tma<W, L, E, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+            launch_pdl_aniso_smem(pdl, k_aniso_tma<W, L, E, 3>, g, sm, st, d, a, x, y, rg, red_slot0, red_total, mr); \
+        }                                                                                                     \
+    } while (0)
+        if (exact) {
+            if (with_dot) {
+                if (loop) TM(true, true, true);
+                else TM(true, false, true);
+            } else TM(false, false, true);
+        } else {
+            if (with_dot) {
+                if (loop) TM(true, true, false);
+                else TM(true, false, false);
+            } else TM(false, false, false);
+        }
+#undef TM
+        return;
+    }
     const bool vec = aniso_vec2(d, y);
     const unsigned g = vec ? grid_aniso2(rg.vend) : grid_aniso(rg.vend);
 #define AN(W, L, E)                                                                                      \

@@ -101,6 +101,65 @@ __global__ void __launch_bounds__(kThreads) k_assemble(Dims d, DevArrays a, cons
 // D = sV + Tr_lo + Tr_hi + Tt_lo + Tt_hi + Tp_lo + Tp_hi  (R7, R10)
 // ---------------------------------------------------------------- coefficients from fields (NEXT-1)
 // kappa_c = kappa0 f_c^(m/2) as ((kappa0 f) f ...) sqrt(f) -- the same product as the oracle (R25).
+// The same assembly, two r-neighbour cells per thread (nr even): 16-byte loads of kt, kp, s and 16-byte
+// stores of T_r, T_theta, T_phi, sV; each cell's products and divisions in the order of k_assemble.
+__global__ void __launch_bounds__(kThreads) k_assemble_vec2(Dims d, DevArrays a, const double *__restrict__ kr,
+                                                            const double *__restrict__ kt,
+                                                            const double *__restrict__ kp,
+                                                            const double *__restrict__ s) {
+    int bad = 0, pos = 0;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t npair = d.n >> 1;
+    const int nr = d.nr, nt = d.nt;
+    auto fin = [](double v) { return !(v >= 0.0) | !isfinite(v); };
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < npair; v += stride) {
+        const uint32_t c = 2u * v;
+        int i, j, k;
+        decompose(d, c, i, j, k);
+        const uint32_t row = (uint32_t)k * nt + j;
+        const size_t rb = (size_t)row * (nr + 1) + i;
+        const size_t tb = ((size_t)k * (nt + 1) + j) * nr + i;
+        const double kr0 = __ldg(kr + rb), kr1 = __ldg(kr + rb + 1);
+        const double2 ktv = __ldg(reinterpret_cast<const double2 *>(kt + tb));
+        const double2 kpv = __ldg(reinterpret_cast<const double2 *>(kp + c));
+        const double2 sv = __ldg(reinterpret_cast<const double2 *>(s + c));
+        const double dpk = a.dp[k], Cj = a.C[j];
+        bad |= fin(kr0) | fin(kr1) | fin(ktv.x) | fin(ktv.y) | fin(kpv.x) | fin(kpv.y) | fin(sv.x) | fin(sv.y);
+        pos |= (sv.x > 0.0) | (sv.y > 0.0);
+        const double tr0 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(kr0, a.rf2[i]), Cj), dpk), a.hr[i]);
+        const double tr1 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(kr1, a.rf2[i + 1]), Cj), dpk), a.hr[i + 1]);
+        *reinterpret_cast<double2 *>(a.Tr + c) = make_double2(tr0, tr1);
+        if (i + 2 == nr) {
+            const double kro = __ldg(kr + rb + 2);
+            bad |= fin(kro);
+            a.TrB[row] = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(kro, a.rf2[nr]), Cj), dpk), a.hr[nr]);
+        }
+        double tt0 = 0.0, tt1 = 0.0;
+        if (j != 0) {
+            const double sf = a.sinf[j], htj = a.ht[j];
+            tt0 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(ktv.x, sf), a.dr[i]), dpk), htj);
+            tt1 = __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(ktv.y, sf), a.dr[i + 1]), dpk), htj);
+        }
+        *reinterpret_cast<double2 *>(a.Tt + c) = make_double2(tt0, tt1);
+        if (j == nt - 1) {
+            const double2 kte = __ldg(reinterpret_cast<const double2 *>(kt + tb + nr));
+            bad |= fin(kte.x) | fin(kte.y);
+        }
+        const double dtj = a.dt[j], den = __dmul_rn(a.sinc[j], a.hp[k]);
+        const double tp0 = __ddiv_rn(__dmul_rn(__dmul_rn(kpv.x, a.dr[i]), dtj), den);
+        const double tp1 = __ddiv_rn(__dmul_rn(__dmul_rn(kpv.y, a.dr[i + 1]), dtj), den);
+        *reinterpret_cast<double2 *>(a.Tp + (size_t)c + d.plane) = make_double2(tp0, tp1);
+        const double V0 = __dmul_rn(__dmul_rn(a.R3[i], Cj), dpk), V1 = __dmul_rn(__dmul_rn(a.R3[i + 1], Cj), dpk);
+        *reinterpret_cast<double2 *>(a.sV + c) = make_double2(__dmul_rn(sv.x, V0), __dmul_rn(sv.y, V1));
+    }
+    bad = __syncthreads_or(bad);
+    pos = __syncthreads_or(pos);
+    if (threadIdx.x == 0) {
+        if (bad) atomicOr(&a.sc->vinvalid, 1);
+        if (pos) atomicOr(&a.sc->vshift, 1);
+    }
+}
+
 __device__ __forceinline__ double kappa_of(double kappa0, int half_power, double f) {
     double v = kappa0;
     for (int m = 0; m < half_power / 2; ++m) v = __dmul_rn(v, f);
@@ -891,7 +950,9 @@ inline unsigned grid_for(uint32_t n) {
 // ---------------------------------------------------------------- launchers
 void launch_assemble(const Dims &d, const DevArrays &a, const double *kr, const double *kt, const double *kp,
                      const double *s, cudaStream_t st) {
-    k_assemble<<<grid_for(d.n), kThreads, 0, st>>>(d, a, kr, kt, kp, s);
+    const bool al = ((((uintptr_t)kt | (uintptr_t)kp | (uintptr_t)s) & 15) == 0);
+    if (d.vec_ok && (d.nr % 2 == 0) && al) k_assemble_vec2<<<grid_for(d.n / 2), kThreads, 0, st>>>(d, a, kr, kt, kp, s);
+    else k_assemble<<<grid_for(d.n), kThreads, 0, st>>>(d, a, kr, kt, kp, s);
 }
 
 void launch_face_coeffs(const Dims &d, const double *f, const double *f_hi, const double *rho, double kappa0,

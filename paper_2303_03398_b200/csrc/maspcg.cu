@@ -1904,8 +1904,17 @@ maspcg_status maspcg_set_aniso_coefficients(maspcg_ctx *c, const double *krt, co
         CK(c, cudaMemcpyAsync(c->xa.Xrp, c->xa.Xrp + last, 8 * pl, cudaMemcpyDeviceToDevice, st));
         CK(c, cudaMemcpyAsync(c->xa.Xtp, c->xa.Xtp + last, 8 * pl, cudaMemcpyDeviceToDevice, st));
     } else {   // the face below plane 0 is the last face of the left neighbour's slab
-        COMM(c, c->comm->shift_right(c->xa.Xrp + last, c->xa.Xrp, pl, st, c->err));
-        COMM(c, c->comm->shift_right(c->xa.Xtp + last, c->xa.Xtp, pl, st, c->err));
+        // staged through halo scratch of the main workspace (rh, dh: [2][plane] each, rebuilt before any use
+        // that needs them), the region every communicator -- also the peer one, whose exchanges store into
+        // registered workspaces only -- can address; two buffers, so the second exchange cannot overwrite
+        // the first one's received plane before it is copied out
+        double *scratch[2] = {c->a.rh, c->a.dh};
+        double *edges[2] = {c->xa.Xrp, c->xa.Xtp};
+        for (int q = 0; q < 2; ++q)
+            CK(c, cudaMemcpyAsync(scratch[q], edges[q] + last, 8 * pl, cudaMemcpyDeviceToDevice, st));
+        for (int q = 0; q < 2; ++q) COMM(c, c->comm->shift_right(scratch[q], scratch[q] + pl, pl, st, c->err));
+        for (int q = 0; q < 2; ++q)
+            CK(c, cudaMemcpyAsync(edges[q], scratch[q] + pl, 8 * pl, cudaMemcpyDeviceToDevice, st));
         COMM(c, c->comm->allreduce_max(&c->a.sc->vinvalid, 1, st, c->err));
     }
     CK(c, cudaMemcpyAsync(c->vflags_host, &c->a.sc->vinvalid, sizeof(int), cudaMemcpyDeviceToHost, st));

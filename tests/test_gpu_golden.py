@@ -2,7 +2,8 @@
 
 tests/golden/{c3,c5}_full_solve.json come from tools/make_golden.py, which calls only oracle/ and the
 seeded generators: the complete residual history of the oracle's solve of BASELINE.json configs[2] (c3,
-150 x 300 x 600, 830 iterations to 1e-10) and of step 0 of configs[4] (c5, 200 x 300 x 600), its
+150 x 300 x 600, 830 iterations to 1e-10), of step 0 of configs[4] (c5, 200 x 300 x 600) and of the first
+40 (tol = 0) iterations of configs[3]'s one-GPU slab (c4, 400 x 400 x 800, 128 M cells), its
 iteration count, the SHA-256 of the whole solution, ||x||^2 (fsum) and x at a fixed sample of 4,096 cells.  The GPU solves the same generated
 problem in the bench's launch configuration (three-kernel path, CUDA graphs, chunk 16) and must
 reproduce every history entry, the count and the sampled solution bit for bit (R24).
@@ -31,7 +32,7 @@ def M():
     return maspcg
 
 
-@pytest.mark.parametrize("name", ["c3", "c5"])
+@pytest.mark.parametrize("name", ["c3", "c5", "c4"])
 def test_full_size_solve_matches_oracle_golden(M, name):
     import torch
     path = os.path.join(HERE, "golden", f"{name}_full_solve.json")
@@ -42,11 +43,11 @@ def test_full_size_solve_matches_oracle_golden(M, name):
     assert [p.nr, p.nt, p.np] == g["shape"]
     S = M.solver_for_problem(p, chunk=16)
     x = torch.from_numpy(p.x0).cuda()
-    st, info, hist = S.solve(torch.from_numpy(p.f).cuda(), x, p.tol, p.maxit)
+    st, info, hist = S.solve(torch.from_numpy(p.f).cuda(), x, p.tol, g.get("maxit", p.maxit))
     torch.cuda.synchronize()
     xs = x.cpu().numpy().ravel()
     S.close()
-    assert st == g["status"] == 0
+    assert st == g["status"] and st >= 0
     assert info["iters"] == g["iters"]
     assert info["bnorm"] == g["bnorm"]
     assert np.array_equal(hist, np.array(g["hist"])), np.abs(hist - np.array(g["hist"])).max()
