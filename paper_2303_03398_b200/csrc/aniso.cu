@@ -543,14 +543,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_tma(Dims d, DevArrays 
             const int lr = k * nt + j - Ra;   // 1 .. nrows - 2
             const int im = i0 > 0 ? i0 - 1 : i0, iq = i0 + 2 < nr ? i0 + 2 : i0 + 1;
             auto T = [&](int pl, int dr) -> const double * { return tb + ((size_t)pl * maxrows + lr + dr) * nr; };
-            auto row4 = [&](const double *r) {
-                const double2 v2 = *reinterpret_cast<const double2 *>(r + i0);
-                return Row4{r[im], v2.x, v2.y, r[iq]};
-            };
-            auto pr2 = [&](const double *r) { return *reinterpret_cast<const double2 *>(r + i0); };
-            aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, row4(T(1, 0)), row4(T(1, -1)), row4(T(1, 1)),
-                                        row4(T(0, 0)), row4(T(2, 0)), pr2(T(0, -1)), pr2(T(0, 1)), pr2(T(2, -1)),
-                                        pr2(T(2, 1)), dot[0]);
+            {
+                auto row4 = [&](const double *r) {
+                    const double2 v2 = *reinterpret_cast<const double2 *>(r + i0);
+                    return Row4{r[im], v2.x, v2.y, r[iq]};
+                };
+                auto pr2 = [&](const double *r) { return *reinterpret_cast<const double2 *>(r + i0); };
+                aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, row4(T(1, 0)), row4(T(1, -1)), row4(T(1, 1)),
+                                            row4(T(0, 0)), row4(T(2, 0)), pr2(T(0, -1)), pr2(T(0, 1)),
+                                            pr2(T(2, -1)), pr2(T(2, 1)), dot[0]);
+            }
         }
         __syncthreads();   // every thread is done with stage st
         if (threadIdx.x == 0 && ch + 2 * gridDim.x < nch) {
@@ -656,7 +658,8 @@ inline bool aniso_tma(const Dims &d, const double *y, const Range &rg) {
 }
 
 // resident blocks per SM of the TMA kernel: 2 (default, 128 registers) or MASPCG_ANISO_TMA_BLOCKS = 3 (80
-// registers with spills; measured slower, 669 vs 625 us)
+// registers with spills; measured slower, 882-897 vs 575-584 us; reading the tile lazily at each use instead
+// of copying a pair's p values to registers measured 615 us at 2 blocks, 734 at 3 -- removed)
 inline int tma_blocks() {
     static const int b = getenv("MASPCG_ANISO_TMA_BLOCKS") ? atoi(getenv("MASPCG_ANISO_TMA_BLOCKS")) : 2;
     return b == 3 ? 3 : 2;
@@ -687,13 +690,13 @@ void launch_aniso_matvec(const Dims &d, const DevArrays &a, const AnisoArrays &x
         const int mr = tile_rows(d.nr);
 #define TM(W, L, E)                                                                                           \
     do {                                                                                                      \
-        if (tma_blocks() == 2) {                                                                              \
+        if (tma_blocks() == 2) {                                                                      \
             cudaFuncSetAttribute(k_aniso_tma<W, L, E, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
             launch_pdl_aniso_smem(pdl, k_aniso_tma<W, L, E, 2>, g, sm, st, d, a, x, y, rg, red_slot0, red_total, mr); \
-        } else {                                                                                              \
+        } else {                                                                                             \
             cudaFuncSetAttribute(k_aniso_tma<W, L, E, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
             launch_pdl_aniso_smem(pdl, k_aniso_tma<W, L, E, 3>, g, sm, st, d, a, x, y, rg, red_slot0, red_total, mr); \
-        }                                                                                                     \
+        }                                                                                                    \
     } while (0)
         if (exact) {
             if (with_dot) {
