@@ -555,6 +555,9 @@ def main():
     ap.add_argument("--kernel-timing", type=int, default=2,
                     help="CUDA events around the hot kernels in the timed region: 2 sampled (the middle slot of "
                          "every graph chunk), 3 sampled (slot 0), 1 every iteration, 0 none")
+    ap.add_argument("--device-loop", type=int, default=1,
+                    help="1 (default): the whole PCG loop as one CUDA-graph launch with a conditional WHILE node "
+                         "(MASPCG_OPT_DEVICE_LOOP; used when kernel timing is off); 0: host chunk loop")
     ap.add_argument("--l2-keep", type=int, default=1,
                     help="1 (default): L2 residency of the loop's most-reused arrays when the slab is small "
                          "(MASPCG_OPT_L2_KEEP auto); 0: off")
@@ -622,6 +625,7 @@ def main():
     S.set_option(maspcg.OPT_PDL, args.pdl)
     S.set_option(maspcg.OPT_FUSE_HALO, args.fuse_halo)
     S.set_option(maspcg.OPT_L2_KEEP, args.l2_keep)
+    S.set_option(maspcg.OPT_DEVICE_LOOP, args.device_loop)
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
 
@@ -811,7 +815,9 @@ def main():
                              "set_bc_r + solve to tol") if args.from_fields else
                             "set_grid + set_coefficients + set_bc_r + solve to tol",
                     "arith": "oracle-identical (no FMA, Dot2 dots)" if args.arith == 0 else "fast (FMA, plain sums)",
-                    "l2_keep": "auto (MASPCG_OPT_L2_KEEP)" if args.l2_keep else "off"},
+                    "l2_keep": "auto (MASPCG_OPT_L2_KEEP)" if args.l2_keep else "off",
+                    "loop": "device (conditional WHILE graph)" if (args.device_loop and not args.kernel_timing)
+                    else "host chunks (kernel timing events need the host loop)" if args.device_loop else "host chunks"},
             "step_ms": step_stats(step_ms),
             "per_step": [{"iters": int(i), "ms": float(m)} for i, m in zip(step_iters, step_ms)]
             if args.steps <= 64 else None,

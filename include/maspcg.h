@@ -148,6 +148,14 @@ typedef enum {
                                     sets and releases at destroy); their lines are returned to the normal priority
                                     after the solve.  The "super" scaling of PAPER.md:277 (§V-C).  0: plain loads
                                     and stores.  Arithmetic and results are unaffected. */
+    MASPCG_OPT_DEVICE_LOOP = 11, /* 1 (default): the whole PCG loop is ONE CUDA-graph launch -- a conditional WHILE
+                                    node whose body is a chunk of iterations followed by a kernel that sets the
+                                    condition to "not done"; the history is kept on the device.
+                                    Used when eligible: three-kernel path, graphs on, timing off, maxit <= 65536, one
+                                    rank or the peer communicator with MASPCG_OPT_FUSE_HALO 2; otherwise (and with 0)
+                                    the host loop, one snapshot per chunk with a speculative chunk in flight.
+                                    Measured: c3 542.6 vs 543.2 us per iteration, P = 8 slab 73.1 vs 73.4 (one rank)
+                                    and 84.4-84.6 vs 85.7-86.4 (one-rank peer). */
     MASPCG_OPT_PATH = 4         /* iteration path: 0 = auto (default, = 1), 1 = three streaming kernels (stencil+p.q,
                                     r-update+Jacobi+dots, deferred x-update+p-update; 128 B/cell), 2 = fused two passes
                                     (p- and x-update folded into a phi-marching tiled stencil + r update; 112 B/cell),

@@ -29,6 +29,7 @@ constexpr int kPartialSlots = 2560;     // per-block Dot2 partial slots of one r
                                         // boundary stencil grids together (2 x kRedBlocks for the scalar kernels)
 constexpr int kThreads = 256;           // threads per block of the streaming kernels
 constexpr int kMaxRanks = 16;           // all-gather scratch of the Dot2 all-reduce
+constexpr int kDevHist = 65536;         // device residual history of the conditional-graph solve loop
 
 // Division by a runtime constant for 0 <= n < 2^31 (round-up multiplier
 // method): q = (n * m) >> p with p = 31 + ceil(log2 d), m = ceil(2^p / d).
@@ -192,6 +193,8 @@ struct DevArrays {
     double *peer_stage[kP2PMaxRanks];   // rank r's P2PArea::stage, mapped into this process
     int gather_ranks;   // > 0: the loop's dot products arrive all-gathered (gather[rank][pairs]) and the
                         // consuming kernel combines them in rank order itself (no combine kernel)
+    double *hist_dev;   // [kDevHist] ||r_k|| at slot k - 1 (device loop, MASPCG_OPT_DEVICE_LOOP), written when
+    int hist_dev_on;    // hist_dev_on is set
     double *partials;   // [8][kPartialSlots]  Dot2 (p, s) partials of up to 4 sums
     double *gather;     // [kMaxRanks][8]   all-gather scratch of the Dot2 all-reduce
     Scalars *sc;

@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_pupdate(Dims d, DevArr
         sc->iter = it;
         sc->rn = rn;
         sc->hist_ring[(it - 1) % chunk] = rn;
+        if (a.hist_dev_on) a.hist_dev[it - 1] = rn;   // the device loop's full history
         if (conv) {
             sc->status = ST_OK;
             sc->done = 1;
@@ -793,6 +794,7 @@ __global__ void __launch_bounds__(kThreads, kVecBlocks) k_pupdate_vec2(Dims d, D
         sc->iter = it;
         sc->rn = rn;
         sc->hist_ring[(it - 1) % chunk] = rn;
+        if (a.hist_dev_on) a.hist_dev[it - 1] = rn;   // the device loop's full history
         if (conv) {
             sc->status = ST_OK;
             sc->done = 1;
@@ -1120,6 +1122,16 @@ unsigned launch_sts_gershgorin(const Dims &d, const DevArrays &a, double *out, c
     const unsigned g = grid_for(d.n);
     k_sts_gershgorin<<<g, kThreads, 0, st>>>(d, a, out);
     return g;
+}
+
+// The device loop (conditional WHILE node of a CUDA graph): run the body (a chunk of iterations) again
+// while the solve is not done.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const Scalars *sc) {
+    cudaGraphSetConditional(h, (*(volatile const int *)&sc->done) ? 0u : 1u);
+}
+
+void launch_loop_cond(cudaGraphConditionalHandle h, const Scalars *sc, cudaStream_t st) {
+    k_loop_cond<<<1, 1, 0, st>>>(h, sc);
 }
 
 // Return the lines of [p, p + bytes) to the normal eviction priority (after a solve that kept them).

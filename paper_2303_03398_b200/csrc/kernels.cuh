@@ -45,6 +45,8 @@ void launch_sts_stage(const Dims &d, const DevArrays &a, const double *yj1p, con
 // per-block maxima of the Gershgorin bound of lambda_max(V^-1 K) into out[0..blocks); returns blocks
 unsigned launch_sts_gershgorin(const Dims &d, const DevArrays &a, double *out, cudaStream_t st);
 void launch_zero_x_if(const Dims &d, const DevArrays &a, double *x, cudaStream_t st);
+// inside the body of a conditional WHILE node: set the condition to "not done"
+void launch_loop_cond(cudaGraphConditionalHandle h, const Scalars *sc, cudaStream_t st);
 // applypriority L2::evict_normal over the 128-byte lines of [p, p + bytes) (undoes an L2_KEEP policy)
 void launch_l2_demote(const void *p, size_t bytes, cudaStream_t st);
 

@@ -77,6 +77,14 @@ struct maspcg_ctx {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};   // one captured chunk per timing-event set
     const void *g_x = nullptr;
     int g_chunk = 0, g_variant = -1;
+    // the device loop (MASPCG_OPT_DEVICE_LOOP): one graph whose conditional WHILE node repeats a chunk until done
+    int device_loop = 1;   // MASPCG_OPT_DEVICE_LOOP (used whenever eligible: graphs on, timing off, ...)
+    cudaGraphExec_t lexec = nullptr;
+    const void *l_x = nullptr;
+    int l_chunk = 0, l_variant = -1;
+    uint32_t l_l2mask = 0;
+    float l_l2frac = 1.f;
+    double *hist_host = nullptr;     // pinned [kDevHist]: the device history of a device-loop solve
 
     // options
     int chunk = 16, use_graphs = 1, timing = 0, path_opt = 0, arith = 0;
@@ -163,6 +171,7 @@ size_t layout(const maspcg_ctx *c, char *base, DevArrays *a) {
     t.partials = (double *)take(sizeof(double) * 8 * kPartialSlots);
     t.p2p = (P2PArea *)take(sizeof(P2PArea));
     t.gather = (double *)take(sizeof(double) * 8 * kMaxRanks);
+    t.hist_dev = (double *)take(sizeof(double) * kDevHist);
     t.P[0] = (double *)take(8 * n);
     t.P[1] = (double *)take(8 * n);
     t.rh = (double *)take(8 * 2 * plane);
@@ -739,6 +748,72 @@ maspcg_status enqueue_chunk(maspcg_ctx *c, double *x, cudaStream_t st, int set) 
     return MASPCG_OK;
 }
 
+// The whole PCG loop as ONE graph launch (MASPCG_OPT_DEVICE_LOOP; SURVEY 8(f) NEXT-3 "conditional-graph
+// device loop"): a conditional WHILE node whose body is a chunk of iterations followed by k_loop_cond,
+// which sets the condition to "not done".  No host round trip until the solve ends.
+bool device_loop_ok(const maspcg_ctx *c, const void *x, int maxit) {
+    if (!c->device_loop || !c->use_graphs || c->timing || maxit > kDevHist) return false;
+    if (use_fused(c) || use_cg1(c) || use_wave(c) || use_persist(c, x)) return false;
+    if (!c->comm) return true;
+    // exchanges that are kernels only: the peer communicator with the halo acquired by the stencil
+    return !c->vmode && c->comm->has_pair_allreduce() && c->fuse_halo == 2;
+}
+
+maspcg_status enqueue_device_loop(maspcg_ctx *c, double *x, cudaStream_t st) {
+    const int key = graph_key(c);
+    if (!c->lexec || c->l_x != x || c->l_chunk != c->chunk || c->l_variant != key || c->l_l2mask != c->d.l2_mask ||
+        c->l_l2frac != c->d.l2_frac) {
+        if (c->lexec) {
+            cudaGraphExecDestroy(c->lexec);
+            c->lexec = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        CK(c, cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault);
+        cudaGraphNode_t node;
+        cudaGraphNodeParams cp{};
+        if (e == cudaSuccess) {
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+        }
+        if (e != cudaSuccess) {
+            cudaGraphDestroy(g);
+            CK(c, e);
+        }
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaStream_t cs = c->cap_stream;
+        e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) {
+            cudaGraphDestroy(g);
+            CK(c, e);
+        }
+        maspcg_status s = MASPCG_OK;
+        for (int it = 0; it < c->chunk && s == MASPCG_OK; ++it) s = enqueue_any(c, x, cs, it);
+        if (s == MASPCG_OK) launch_loop_cond(h, c->a.sc, cs);
+        cudaGraph_t out = nullptr;
+        e = cudaStreamEndCapture(cs, &out);
+        if (s != MASPCG_OK || e != cudaSuccess) {
+            cudaGraphDestroy(g);
+            RET_IF(s);
+            CK(c, e);
+        }
+        e = cudaGraphInstantiate(&c->lexec, g, 0);
+        cudaGraphDestroy(g);
+        CK(c, e);
+        c->l_x = x;
+        c->l_chunk = c->chunk;
+        c->l_variant = key;
+        c->l_l2mask = c->d.l2_mask;
+        c->l_l2frac = c->d.l2_frac;
+    }
+    CK(c, cudaGraphLaunch(c->lexec, st));
+    return MASPCG_OK;
+}
+
 void accumulate_timing(maspcg_ctx *c, int set, int iters_in_chunk) {
     const size_t base = (size_t)set * 12 * c->chunk;
     const bool comm = c->comm && !use_fused(c) && !use_cg1(c) && !use_wave(c);   // events of enqueue_iteration
@@ -968,6 +1043,26 @@ maspcg_status solve_impl(maspcg_ctx *c, const double *rhs, double *x, double tol
         launched += use_persist(c, x) ? 1 : (long long)c->chunk * kernels_per_iteration(c);
         return MASPCG_OK;
     };
+    if (!done && device_loop_ok(c, x, maxit)) {   // the whole loop in one graph launch
+        if (!c->hist_host) CK(c, cudaMallocHost((void **)&c->hist_host, sizeof(double) * kDevHist));
+        c->a.hist_dev_on = 1;
+        maspcg_status ls = enqueue_device_loop(c, x, st);
+        c->a.hist_dev_on = 0;
+        RET_IF(ls);
+        CK(c, cudaMemcpyAsync(c->snap[0], c->a.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, st));
+        CK(c, cudaMemcpyAsync(c->hist_host, c->a.hist_dev, sizeof(double) * (size_t)maxit, cudaMemcpyDeviceToHost, st));
+        CK(c, cudaEventRecord(c->ev_chunk[0], st));
+        CK(c, cudaEventSynchronize(c->ev_chunk[0]));
+        const Scalars &s = *c->snap[0];
+        if (hist)
+            for (int k = 1; k <= s.iter; ++k) hist[k] = c->hist_host[k - 1];
+        iters = s.iter;
+        status = s.status;
+        rn = s.rn;
+        done = true;
+        const long long bodies = (iters + c->chunk - 1) / c->chunk > 0 ? (iters + c->chunk - 1) / c->chunk : 1;
+        launched += bodies * (c->chunk * kernels_per_iteration(c) + 1);
+    }
     if (!done) {
         RET_IF(issue(cur));
         while (true) {
@@ -1223,6 +1318,9 @@ maspcg_status maspcg_destroy(maspcg_ctx *c) {
     for (int b = 0; b < 2; ++b)
         if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
     c->gexec[0] = c->gexec[1] = nullptr;
+    if (c->lexec) cudaGraphExecDestroy(c->lexec);
+    c->lexec = nullptr;
+    if (c->hist_host) cudaFreeHost(c->hist_host);
     delete c->comm;
     if (c->ptab) {
         for (int g = 0; g < kP2PRegions; ++g)
@@ -1417,6 +1515,10 @@ maspcg_status maspcg_set_workspace(maspcg_ctx *c, void *dev_ptr, size_t bytes) {
             cudaGraphExecDestroy(c->gexec[b]);
             c->gexec[b] = nullptr;
         }
+    }
+    if (c->lexec) {
+        cudaGraphExecDestroy(c->lexec);
+        c->lexec = nullptr;
     }
     return MASPCG_OK;
 }
@@ -1975,6 +2077,7 @@ maspcg_status maspcg_set_option(maspcg_ctx *c, maspcg_option opt, long long v) {
             break;
         case MASPCG_OPT_FUSE_HALO: c->fuse_halo = v < 0 ? 0 : (v > 2 ? 2 : v); break;
         case MASPCG_OPT_L2_KEEP: c->l2_keep = v ? 1 : 0; break;
+        case MASPCG_OPT_DEVICE_LOOP: c->device_loop = v ? 1 : 0; break;
         case MASPCG_OPT_PATH:
             if (v < 0 || v > 5)
                 SET_ERR(c, MASPCG_E_INVALID, "path must be 0 (auto), 1 (three kernels), 2 (fused), 3 (wave), 4 (single "

@@ -31,6 +31,7 @@ MEAN_ARITHMETIC, MEAN_HARMONIC = 0, 1
 OPT_CHUNK, OPT_USE_GRAPHS, OPT_TIMING, OPT_PATH, OPT_ARITH, OPT_TMA, OPT_VEC, OPT_PDL = 1, 2, 3, 4, 5, 6, 7, 8
 OPT_FUSE_HALO = 9
 OPT_L2_KEEP = 10
+OPT_DEVICE_LOOP = 11
 ARITH_EXACT, ARITH_FAST = 0, 1
 PATH_AUTO, PATH_THREE_KERNELS, PATH_FUSED = 0, 1, 2
 

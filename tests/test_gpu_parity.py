@@ -481,3 +481,32 @@ def test_sts_c3_full_size_bitwise(torch_cuda, M, oracle_mod):
     uo = op.rkl2_step(u0, p.s, tau, 10, p.g_in, p.g_out)
     assert np.array_equal(ug.cpu().numpy(), uo)
     S.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "rand"])
+@pytest.mark.parametrize("chunk", [16, 5])
+def test_device_loop_bitwise(torch_cuda, M, oracle_mod, name, chunk):
+    """MASPCG_OPT_DEVICE_LOOP: the whole PCG loop as one CUDA-graph launch (a conditional WHILE node over a
+    chunk of iterations) gives the oracle's iterates, count and history bit for bit."""
+    p = inputs.random_problem(14, 9, 10, 17) if name == "rand" else inputs.make_problem(name)
+    o = oracle_mod.solve_problem(p)
+    g = gpu_solve(torch_cuda, M, p, chunk=chunk, opts={M.OPT_DEVICE_LOOP: 1})
+    assert_solve_parity(g, o)
+    g[4].close()
+
+
+def test_device_loop_edge_cases(torch_cuda, M, oracle_mod):
+    """Device loop: tol = 0 runs exactly maxit iterations (also when maxit is not a multiple of the chunk);
+    a converged x0 returns at once."""
+    torch = torch_cuda
+    p = inputs.make_problem("c1")
+    for maxit in (7, 33):
+        o = oracle_mod.solve_problem(p, tol=0.0, maxit=maxit)
+        g = gpu_solve(torch, M, p, tol=0.0, maxit=maxit, opts={M.OPT_DEVICE_LOOP: 1})
+        assert g[0] == M.NOT_CONVERGED and g[1]["iters"] == maxit
+        assert_solve_parity(g, o)
+        g[4].close()
+    o = oracle_mod.solve_problem(p)
+    g = gpu_solve(torch, M, p, x0=o["x"], tol=1e-6, opts={M.OPT_DEVICE_LOOP: 1})
+    assert g[0] == M.OK and g[1]["iters"] == 0
+    g[4].close()
