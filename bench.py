@@ -313,6 +313,8 @@ def run_vv(args):
     S = maspcg.Solver(nr, nt, np_, prob.rf, prob.tf, prob.pf, device=local, chunk=args.chunk,
                       force_comm=args.force_comm)
     S.set_option(maspcg.OPT_ARITH, args.arith)
+    S.set_option(maspcg.OPT_PDL, args.pdl)
+    S.set_option(maspcg.OPT_DEVICE_LOOP, args.device_loop)
     S.vv_enable()
     x = torch.empty_like(x0)
     stream = torch.cuda.current_stream()
