@@ -1341,6 +1341,8 @@ void launch_vv_matvec(const VVDims &vin, const VVArrays &a, const DevArrays &bas
         else done = loop ? launch_fused<true, true, false>(v, a, base, y, st)
                          : launch_fused<true, false, false>(v, a, base, y, st);
         if (done) return;
+        // default: the plane-marching operator with TMA-staged planes (vv_march.cu)
+        if (launch_vv_march(v, a, base, y, with_dot, loop, exact, st)) return;
     }
     const bool pair = pair0;
     const uint32_t nt1 = v.ncell + 2 * v.plane1;

@@ -80,6 +80,10 @@ void launch_vv_diag(const VVDims &v, const VVArrays &a, cudaStream_t st);
 // partial p.y -> sc->red1 via the last block; loop: early exit when sc->done.
 void launch_vv_matvec(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
                       bool wall, bool exact, cudaStream_t st);
+// The same (homogeneous operator, nr even) as ONE plane-marching kernel with TMA-staged input planes
+// (vv_march.cu); false when not applicable (odd nr, unaligned y, MASPCG_VV_MARCH=0) -- nothing launched.
+bool launch_vv_march(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
+                     bool exact, cudaStream_t st);
 // Planes per term ring of the chunked matvec for an L2 budget of `bytes` (0: the chunked form is off --
 // MASPCG_VV_CHUNK=0, odd nr, or a slab of at most two chunks), and the ring's bytes (4 term arrays).
 uint32_t vv_ring_planes(const VVDims &v, size_t bytes);

@@ -309,3 +309,70 @@ def test_vv_chunked_multirank_exact(M, oracle_mod, monkeypatch):
     for st, info, hist, *_ in res:
         assert st == o["status"] == 0 and info["iters"] == o["iters"] and np.array_equal(hist, o["hist"])
     assert np.array_equal(np.concatenate([r[3] for r in res], axis=0), o["x"])
+
+
+# ------------------------------------------------------------------ the plane-marching TMA operator (vv_march.cu)
+@pytest.mark.parametrize("tj,grid", [(None, None), (1, None), (3, 5), (2, 1)])
+@pytest.mark.parametrize("shape,walls", [((8, 4, 2), (0, 1)), ((16, 16, 32), (1, 0)), ((20, 30, 48), (0, 1)),
+                                         ((2, 5, 3), (0, 0)), ((6, 9, 7), (1, 1))])
+def test_vv_march_operator_exact(M, oracle_mod, monkeypatch, tj, grid, shape, walls):
+    """The default operator for even nr: one plane-marching kernel per matvec whose p planes and coefficient
+    rows arrive by bulk copies (vv_march.cu).  Apply and whole solves identical to the oracle; forced small
+    tiles (ragged last tile, halo rows at both ends) and forced small grids (several tile/plane segments per
+    block, the rings carried across segments)."""
+    import torch
+    if tj:
+        monkeypatch.setenv("MASPCG_VV_MARCH_TJ", str(tj))
+    if grid:
+        monkeypatch.setenv("MASPCG_VV_MARCH_GRID", str(grid))
+    p = inputs.make_vv_problem("rand", shape=shape, seed=41 + sum(shape), wall_in=walls[0], wall_out=walls[1])
+    op = oracle_op(oracle_mod, p)
+    S = gpu_solver(M, p)
+    x = np.stack([inputs.white_noise(61 + c, p.nr, p.nt, 0, p.np) for c in range(3)], axis=1)
+    y = S.vv_apply(dev(x))
+    torch.cuda.synchronize()
+    S.close()
+    assert np.array_equal(y.cpu().numpy(), op.apply(x))
+    o = oracle_mod.vv_solve_problem(p)
+    st, info, hist, xs, _, _ = gpu_vv_solve(M, p)
+    assert st == o["status"] == 0 and info["iters"] == o["iters"]
+    assert np.array_equal(hist, o["hist"]) and np.array_equal(xs, o["x"])
+
+
+@pytest.mark.parametrize("shape", [(16, 16, 32), (20, 30, 48)])
+def test_vv_two_phase_operator_exact(M, oracle_mod, monkeypatch, shape):
+    """MASPCG_VV_MARCH=0: the two-phase kernels (terms, then rows) stay bit-identical too."""
+    import torch
+    monkeypatch.setenv("MASPCG_VV_MARCH", "0")
+    p = inputs.make_vv_problem("rand", shape=shape, seed=5 + sum(shape), wall_in=0, wall_out=1)
+    op = oracle_op(oracle_mod, p)
+    S = gpu_solver(M, p)
+    x = np.stack([inputs.white_noise(71 + c, p.nr, p.nt, 0, p.np) for c in range(3)], axis=1)
+    y = S.vv_apply(dev(x))
+    torch.cuda.synchronize()
+    S.close()
+    assert np.array_equal(y.cpu().numpy(), op.apply(x))
+    o = oracle_mod.vv_solve_problem(p)
+    st, info, hist, xs, _, _ = gpu_vv_solve(M, p)
+    assert st == o["status"] == 0 and info["iters"] == o["iters"]
+    assert np.array_equal(hist, o["hist"]) and np.array_equal(xs, o["x"])
+
+
+@pytest.mark.parametrize("P,shape", [(2, (10, 8, 16)), (4, (8, 13, 8)), (3, (4, 7, 9))])
+def test_vv_march_multirank_exact(M, oracle_mod, monkeypatch, P, shape):
+    """The marching operator on phi-slabs (halo planes of p from the loopback exchange), forced small tiles
+    and grids: iterates and history equal the global oracle's on every rank."""
+    monkeypatch.setenv("MASPCG_VV_MARCH_TJ", "3")
+    monkeypatch.setenv("MASPCG_VV_MARCH_GRID", "4")
+    full = inputs.make_vv_problem("rand", shape=shape, seed=50 + P, wall_in=0, wall_out=1)
+    o = oracle_mod.vv_solve_problem(full)
+
+    def fn(r, group):
+        k0, nloc = inputs.slab_extent(full.np, r, P)
+        p = inputs.make_vv_problem("rand", k0, nloc, shape=shape, seed=50 + P, wall_in=0, wall_out=1)
+        return gpu_vv_solve(M, p, loopback=(group, r))
+
+    res = run_ranks(M, P, fn)
+    for st, info, hist, *_ in res:
+        assert st == o["status"] == 0 and info["iters"] == o["iters"] and np.array_equal(hist, o["hist"])
+    assert np.array_equal(np.concatenate([r[3] for r in res], axis=0), o["x"])
