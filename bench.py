@@ -372,7 +372,8 @@ def run_vv(args):
     gb = lambda k: VV_BYTES[k] * ncl / (avg(k) * 1e-3) / 1e9 if avg(k) > 0 else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
-                "kernel": "vv pole-ring sums + vector stencil + p.q (k_vv_ring + k_vv_matvec)",
+                "kernel": "vv pole-ring sums + vector stencil + p.q (k_vv_ring + k_vv_march, the plane-marching TMA operator; "
+                          "MASPCG_VV_MARCH=0: the two-phase k_vv_terms3 + k_vv_rows2)",
                 "algorithmic_bytes_per_launch": VV_BYTES["matvec"] * ncl, "avg_launch_ms": mv_ms,
                 "peak_source": peak_src, "share_of_step": avg("matvec") * iters / ms if ms > 0 else None,
                 "timed_launches": stats["matvec_launches"]}
