@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevAr
     if (dbg & 32) return;
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t pbar[3], cbar[2];   // p ring, coefficient ring
+    __shared__ double2 cst[3][kMT];                       // per-thread metric products (see below)
     const int nr = v.nr, nt = v.nt, nh = nr >> 1, tj = L.tj, RL = nr + 2, TR2 = tj + 2;
     double *const pring = sm;
     double *const cring = pring + 3 * (size_t)L.pslot;
@@ -138,30 +139,29 @@ __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevAr
         const int j = j0 - 1 + lr;
         const bool act = role != 0 && j >= 0 && j < nt;
         // ---- the r-pair's metric products for row j (phi-independent; Geo's association)
-        double arC0 = 0, arC1 = 0, arC2 = 0, atS0 = 0, atS1 = 0, atU0 = 0, atU1 = 0, ap0 = 0, ap1 = 0;
-        double lt0 = 0, lt1 = 0, lt2 = 0, lpc0 = 0, lpc1 = 0, lpc2 = 0, lpm0 = 0, lpm1 = 0, hr0 = 0, hr1 = 0;
+        // ((atU0, atU1), (lpm0, lpm1), (arC2, lt0), one use each per step, live in shared memory: registers bind)
+        double arC0 = 0, arC1 = 0, atS0 = 0, atS1 = 0, ap0 = 0, ap1 = 0;
+        double lt1 = 0, lt2 = 0, lpc0 = 0, lpc1 = 0, lpc2 = 0, hr0 = 0, hr1 = 0;
         if (act) {
             const double Cj = a.C[j], sfj = a.sinf[j], sfu = a.sinf[j + 1], dtj = a.dt[j], htj = a.ht[j], scj = a.sinc[j];
             const double scm = j >= 1 ? a.sinc[j - 1] : 0.0;
             const double d0 = a.dR2[i0], d1 = a.dR2[i0 + 1];
             arC0 = mul(a.rf2[i0], Cj);
             arC1 = mul(a.rf2[i0 + 1], Cj);
-            arC2 = mul(a.rf2[i0 + 2], Cj);
+            const double arC2 = mul(a.rf2[i0 + 2], Cj);
             atS0 = mul(sfj, d0);
             atS1 = mul(sfj, d1);
-            atU0 = mul(sfu, d0);
-            atU1 = mul(sfu, d1);
+            cst[0][t] = make_double2(mul(sfu, d0), mul(sfu, d1));   // atU0, atU1
             ap0 = mul(d0, dtj);
             ap1 = mul(d1, dtj);
             const double c0 = a.rce[i0], c1 = a.rce[i0 + 1], c2 = a.rce[i0 + 2];
-            lt0 = mul(c0, htj);
+            cst[2][t] = make_double2(arC2, mul(c0, htj));            // arC2, lt0
             lt1 = mul(c1, htj);
             lt2 = mul(c2, htj);
             lpc0 = mul(c0, scj);
             lpc1 = mul(c1, scj);
             lpc2 = mul(c2, scj);
-            lpm0 = mul(c1, scm);
-            lpm1 = mul(c2, scm);
+            cst[1][t] = make_double2(mul(c1, scm), mul(c2, scm));   // lpm0, lpm1
             hr0 = a.hr[i0];
             hr1 = a.hr[i0 + 1];
         }
@@ -251,11 +251,12 @@ __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevAr
                     const double2 Tj1 = ld2(PT(P0, 1, lr + 1) + i0), Pk1 = ld2(PT(P1, 2, lr) + i0);
                     const double vr2 = last ? 0.0 : PT(P0, 0, lr)[i0 + 2];
                     const double2 wc = ld2(Cw + (size_t)lr * nr + i0);
-                    const double A0 = mul(arC0, dps), A1 = mul(arC1, dps), A2 = mul(arC2, dps);
+                    const double2 aU = cst[0][t];
+                    const double A0 = mul(arC0, dps), A1 = mul(arC1, dps), A2 = mul(cst[2][t].x, dps);
                     {
                         const double fr_lo = mul(A0, vr0), fr_hi = mul(A1, R.y);
                         const double ft_lo = (j == 0) ? 0.0 : mul(mul(atS0, dps), T.x);
-                        const double ft_hi = (j == nt - 1) ? 0.0 : mul(mul(atU0, dps), Tj1.x);
+                        const double ft_hi = (j == nt - 1) ? 0.0 : mul(mul(aU.x, dps), Tj1.x);
                         const double fp_lo = mul(ap0, Pp.x), fp_hi = mul(ap0, Pk1.x);
                         double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
                         d = add(d, sub(fp_hi, fp_lo));
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevAr
                     {
                         const double fr_lo = mul(A1, R.y), fr_hi = mul(A2, vr2);
                         const double ft_lo = (j == 0) ? 0.0 : mul(mul(atS1, dps), T.y);
-                        const double ft_hi = (j == nt - 1) ? 0.0 : mul(mul(atU1, dps), Tj1.y);
+                        const double ft_hi = (j == nt - 1) ? 0.0 : mul(mul(aU.y, dps), Tj1.y);
                         const double fp_lo = mul(ap1, Pp.y), fp_hi = mul(ap1, Pk1.y);
                         double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
                         d = add(d, sub(fp_hi, fp_lo));
@@ -301,14 +302,14 @@ __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevAr
                         }
                     }
                     if (j >= 1) {
-                        const double2 Pjm = ld2(PT(P0, 2, lr - 1) + i0);
+                        const double2 Pjm = ld2(PT(P0, 2, lr - 1) + i0), lpm = cst[1][t];
                         const double2 wr = ld2(Cr + co);
                         {
-                            const double gp_a = mul(Lp1, Pp.x), gp_b = mul(mul(lpm0, hm), Pjm.x);
+                            const double gp_a = mul(Lp1, Pp.x), gp_b = mul(mul(lpm.x, hm), Pjm.x);
                             tr0 = mul(wr.x, sub(sub(gp_a, gp_b), sub(mul(lt1, T.x), mul(lt1, Tm.x))));
                         }
                         {
-                            const double gp_a = mul(Lp2, Pp.y), gp_b = mul(mul(lpm1, hm), Pjm.y);
+                            const double gp_a = mul(Lp2, Pp.y), gp_b = mul(mul(lpm.y, hm), Pjm.y);
                             tr1 = mul(wr.y, sub(sub(gp_a, gp_b), sub(mul(lt2, T.y), mul(lt2, Tm.y))));
                         }
                     }
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevAr
                             const double2 wp = ld2(Cp + co);
                             {
                                 const double vrjm = i0 == 0 ? 0.0 : Rjm.x;
-                                const double gt_a = mul(lt1, T.x), gt_b = mul(lt0, tm1);
+                                const double gt_a = mul(lt1, T.x), gt_b = mul(cst[2][t].y, tm1);
                                 const double gr_a = mul(hr0, vr0), gr_b = mul(hr0, vrjm);
                                 tp0 = mul(wp.x, sub(sub(gt_a, gt_b), sub(gr_a, gr_b)));
                             }
@@ -470,7 +471,7 @@ bool vv_march_layout(const VVDims &v, MarchLayout &L) {
         L.cslot = (3u * (tj + 1) + 4u * tj) * v.nr;
         L.nphi = 2u * (v.nloc + 2);
         L.tbuf = 4u * (tj + 2) * (v.nr + 2);
-        if (march_smem_bytes(L) <= 225u * 1024u) break;
+        if (march_smem_bytes(L) <= 202u * 1024u + 512u) break;   // (+ 24.4 KB static: 227 KB per block)
     }
     if (tj < 1) return false;
     L.njt = (v.nt + tj - 1) / tj;
