@@ -9,6 +9,8 @@ fixed sample of cells.
     python tools/make_golden.py c5      # configs[4] step 0 (cold solve), 200 x 300 x 600
     python tools/make_golden.py c4      # configs[3] one-GPU slab 400 x 400 x 800, the first 40 of its
                                         # tol = 0 iterations (the bench runs 500)
+    python tools/make_golden.py c3v     # the staggered vector viscosity on the c3 grid (bench.py --operator
+                                        # vv), 81 M unknowns, tol 1e-10 (oracle/masoracle_vv.c, single thread)
 
 Runs the oracle's -fopenmp build (identical values to the plain build,
 tests/test_oracle_pins.py::test_openmp_build_gives_identical_iterates).
@@ -39,16 +41,19 @@ def sample_index(n, seed=12345):
 
 def main(name):
     oracle.use_openmp(True)
-    p = inputs.make_problem(name)
+    vv = name in inputs.VV_CONFIGS
+    p = inputs.make_vv_problem(name) if vv else inputs.make_problem(name)
     maxit = 40 if name == "c4" else p.maxit
     t0 = time.time()
-    o = oracle.solve_problem(p, maxit=maxit)
+    o = oracle.vv_solve_problem(p, maxit=maxit) if vv else oracle.solve_problem(p, maxit=maxit)
     dt = time.time() - t0
     x = o["x"].ravel()
     idx = sample_index(x.size)
     out = {
-        "source": f"tools/make_golden.py {name}: oracle/masoracle.c (-fopenmp build) masoracle_pcg on "
-                  f"inputs.make_problem('{name}') (BASELINE.json {name}), tol {p.tol}, maxit {maxit}",
+        "source": (f"tools/make_golden.py {name}: oracle/masoracle_vv.c vector-viscosity PCG on "
+                   f"inputs.make_vv_problem('{name}'), tol {p.tol}, maxit {maxit}") if vv else
+                  (f"tools/make_golden.py {name}: oracle/masoracle.c (-fopenmp build) masoracle_pcg on "
+                   f"inputs.make_problem('{name}') (BASELINE.json {name}), tol {p.tol}, maxit {maxit}"),
         "maxit": maxit,
         "config": name, "shape": [p.nr, p.nt, p.np], "status": int(o["status"]), "iters": int(o["iters"]),
         "bnorm": o["bnorm"], "hist": [float(v) for v in o["hist"]],
