@@ -573,6 +573,176 @@ __global__ void __launch_bounds__(kThreads, MINB) k_aniso_tma(Dims d, DevArrays 
     }
 }
 
+// ---------------------------------------------------------------- operator apply, plane-marching (default)
+// The same arithmetic (aniso_pair) with every operand staged by the Tensor Memory Accelerator: a block owns a
+// theta-tile of tj rows x all nr radii and marches through a run of phi-planes.  Per plane it receives, by 1-D bulk
+// copies counted on mbarriers, the p tile of plane s + 2 (rows j0 - 1 .. j0 + tj) into a 4-slot ring (planes
+// s - 1, s, s + 1 read, s + 2 in flight) and the coefficient rows of step s + 1 into a 3-slot ring: T_r, T_theta,
+// D7, X_rt of plane s + 1 and T_phi, X_rphi, X_thetaphi of the face above it (the face below is the previous
+// step's); the threads read their pair's operands from shared memory (no global loads, no per-element index
+// arithmetic), one block barrier per plane.  The pair kernels hold ~40 coefficient values in registers across a
+// global-memory latency (latency-bound at 2 blocks per SM); here the bulk copies carry the memory parallelism.
+constexpr int kAM = 512;   // threads per block (one block per SM)
+
+struct AnisoMarch {
+    int tj, njt;
+    int k0, nk;           // planes [k0, k0 + nk) of the slab (Full: 0, nloc; Interior: 1, nloc - 2)
+    uint32_t pslot;       // (tj + 2) rows of nr
+    uint32_t cslot;       // (7 tj + 3) rows of nr: Tr [tj], Tt [tj+1], D7 [tj], Xrt [tj+1], Tp+ [tj], Xrp+ [tj], Xtp+ [tj+1]
+    uint32_t units;       // njt * nk
+};
+inline size_t am_smem(const AnisoMarch &M) { return sizeof(double) * (4 * (size_t)M.pslot + 3 * (size_t)M.cslot); }
+
+template <bool WITH_DOT, bool LOOP, bool EXACT>
+__global__ void __launch_bounds__(kAM, 1) k_aniso_march(Dims d, DevArrays a, AnisoArrays x, double *__restrict__ y,
+                                                       AnisoMarch M, unsigned red_slot0, unsigned red_total) {
+    extern __shared__ __align__(128) double amsm[];
+    __shared__ __align__(8) uint64_t pbar[4], cbar[3];
+    pdl_wait();
+    pdl_trigger();
+    if (LOOP && *(volatile int *)&a.sc->done) return;
+    if (LOOP && a.peer_wait) acquire_p_halo(a);   // before any copy of a (peer-written) halo plane
+    const int nr = d.nr, nt = d.nt, nh = nr >> 1, tj = M.tj;
+    const size_t plane = d.plane;
+    double *const pring = amsm;
+    double *const cring = pring + 4 * (size_t)M.pslot;
+    const uint32_t oTt = (uint32_t)tj * nr, oD7 = (uint32_t)(2 * tj + 1) * nr, oXrt = (uint32_t)(3 * tj + 1) * nr;
+    const uint32_t oTp = (uint32_t)(4 * tj + 2) * nr, oXrp = (uint32_t)(5 * tj + 2) * nr, oXtp = (uint32_t)(6 * tj + 2) * nr;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q) mbar_init1(&pbar[q]);
+        for (int q = 0; q < 3; ++q) mbar_init1(&cbar[q]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    const bool member = t < tj * nh;
+    const int lr = member ? t / nh : 0;
+    const int i0 = member ? 2 * (t - lr * nh) : 0;
+    const bool il = i0 > 0, ih = i0 + 2 < nr;
+    const int om = il ? 1 : 0, oq = ih ? 2 : 1;
+    Acc<EXACT> dot[1];
+    const uint64_t u0 = (uint64_t)blockIdx.x * M.units / gridDim.x, u1 = (uint64_t)(blockIdx.x + 1) * M.units / gridDim.x;
+    uint32_t pidx = 0, cidx = 0;   // running issue counts of the rings
+    for (uint64_t u = u0; u < u1;) {
+        const int jt = (int)(u / (uint32_t)M.nk);
+        const int kb = M.k0 + (int)(u - (uint64_t)jt * M.nk);
+        const int kend = M.k0 + M.nk;
+        const int ke = (int)((uint64_t)kb + (u1 - u) < (uint64_t)kend ? kb + (u1 - u) : kend);
+        u += (uint64_t)(ke - kb);
+        const int j0 = jt * tj, j = j0 + lr;
+        const bool act = member && j < nt;
+        const bool jl = j > 0, jh = j < nt - 1;
+        const int jlo = j0 - 1 > 0 ? j0 - 1 : 0;
+        const int jhi1 = j0 + tj < nt - 1 ? j0 + tj : nt - 1;          // rows .. j0 + tj
+        const int jhi0 = j0 + tj - 1 < nt - 1 ? j0 + tj - 1 : nt - 1;  // rows .. j0 + tj - 1
+        // p plane k (-1 .. nloc) into ring slot idx % 4: rows jlo .. jhi1 to tile rows from j0 - 1
+        auto issue_p = [&](int k, uint32_t idx) {
+            const uint32_t q = idx & 3u, bytes = (uint32_t)(jhi1 - jlo + 1) * nr * 8u;
+            mbar_expect(&pbar[q], bytes);
+            bulk_copy(pring + (size_t)q * M.pslot + (size_t)(jlo - (j0 - 1)) * nr,
+                      gaddr64(a.p, (size_t)(k + 1) * plane + (size_t)jlo * nr), bytes, &pbar[q]);
+        };
+        // coefficient stage of plane s (s = kb - 1: only the face above it, i.e. the faces of plane kb)
+        auto issue_c = [&](int s, uint32_t idx) {
+            const uint32_t q = idx % 3u;
+            double *cs = cring + (size_t)q * M.cslot;
+            const uint32_t b0 = (uint32_t)(jhi0 - j0 + 1) * nr * 8u, b1 = (uint32_t)(jhi1 - j0 + 1) * nr * 8u;
+            const bool full = s >= kb;
+            mbar_expect(&cbar[q], (full ? 2 * b0 + 2 * b1 : 0u) + 2 * b0 + b1);
+            const size_t ps = (size_t)s * plane + (size_t)j0 * nr, pu = ps + plane;   // plane s, the face above
+            if (full) {
+                bulk_copy(cs, gaddr64(a.Tr, ps), b0, &cbar[q]);
+                bulk_copy(cs + oTt, gaddr64(a.Tt, ps), b1, &cbar[q]);
+                bulk_copy(cs + oD7, gaddr64(x.D7, ps), b0, &cbar[q]);
+                bulk_copy(cs + oXrt, gaddr64(x.Xrt, ps), b1, &cbar[q]);
+            }
+            bulk_copy(cs + oTp, gaddr64(a.Tp, pu), b0, &cbar[q]);
+            bulk_copy(cs + oXrp, gaddr64(x.Xrp, pu), b0, &cbar[q]);
+            bulk_copy(cs + oXtp, gaddr64(x.Xtp, pu), b1, &cbar[q]);
+        };
+        // ring index of p plane k: pb + k - (kb - 1) (planes kb - 1 .. ke); of stage s: cb + s - (kb - 1) (kb - 1 .. ke - 1)
+        const uint32_t pb = pidx, cb = cidx;
+        pidx += (uint32_t)(ke - kb + 2);
+        cidx += (uint32_t)(ke - kb + 1);
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_p(kb - 1, pb);
+            issue_p(kb, pb + 1);
+            issue_p(kb + 1, pb + 2);
+            issue_c(kb - 1, cb);
+            issue_c(kb, cb + 1);
+        }
+        {   // the first step's older operands: planes kb - 1, kb and the faces of plane kb
+            const uint32_t i1 = pb, i2 = pb + 1;
+            mbar_wait_parity(&pbar[i1 & 3u], (i1 >> 2) & 1u);
+            mbar_wait_parity(&pbar[i2 & 3u], (i2 >> 2) & 1u);
+            mbar_wait_parity(&cbar[cb % 3u], (cb / 3u) & 1u);
+        }
+        for (int s = kb; s < ke; ++s) {
+            const uint32_t q = (uint32_t)(s - (kb - 1));
+            if (threadIdx.x == 0) {   // into the slots of plane s - 2 and stage s - 2 (free: barrier of step s - 1)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (s + 2 <= ke) issue_p(s + 2, pb + q + 2);
+                if (s + 1 <= ke - 1) issue_c(s + 1, cb + q + 1);
+            }
+            const uint32_t ip = pb + q + 1, ic = cb + q;   // plane s + 1, stage s
+            mbar_wait_parity(&pbar[ip & 3u], (ip >> 2) & 1u);
+            mbar_wait_parity(&cbar[ic % 3u], (ic / 3u) & 1u);
+            if (act) {
+                const double *Pm = pring + (size_t)((ip - 2) & 3u) * M.pslot;   // plane s - 1
+                const double *P0 = pring + (size_t)((ip - 1) & 3u) * M.pslot;   // plane s
+                const double *P1 = pring + (size_t)(ip & 3u) * M.pslot;         // plane s + 1
+                const double *C = cring + (size_t)(ic % 3u) * M.cslot;           // stage s
+                const double *Cb = cring + (size_t)((ic + 2) % 3u) * M.cslot;    // stage s - 1: the faces of plane s
+                const int r = lr + 1;                                            // tile row of j
+                const int rm = jl ? r - 1 : r, rp = jh ? r + 1 : r;
+                auto row4 = [&](const double *P, int rr) {
+                    const double *w = P + (size_t)rr * nr + i0;
+                    const double2 v2 = *reinterpret_cast<const double2 *>(w);
+                    return Row4{w[-om], v2.x, v2.y, w[oq]};
+                };
+                auto pr2 = [&](const double *P, int rr) { return *reinterpret_cast<const double2 *>(P + (size_t)rr * nr + i0); };
+                const uint32_t o0 = (uint32_t)lr * nr + i0, o1 = (uint32_t)(jh ? lr + 1 : lr) * nr + i0;
+                auto c2 = [&](const double *base, uint32_t off) { return *reinterpret_cast<const double2 *>(base + off); };
+                PairCoef K;
+                K.tr = c2(C, o0);
+                K.tr2 = C[o0 + oq];
+                K.ttl = c2(C + oTt, o0);
+                K.tth = c2(C + oTt, o1);
+                K.tpl = c2(Cb + oTp, o0);
+                K.tph = c2(C + oTp, o0);
+                K.d7 = c2(C + oD7, o0);
+                K.Xt0 = c2(C + oXrt, o0);
+                K.Xt1 = c2(C + oXrt, o1);
+                K.Xt0q = C[oXrt + o0 + oq];
+                K.Xt1q = C[oXrt + o1 + oq];
+                K.Xp0 = c2(Cb + oXrp, o0);
+                K.Xp1 = c2(C + oXrp, o0);
+                K.Xp0q = Cb[oXrp + o0 + oq];
+                K.Xp1q = C[oXrp + o0 + oq];
+                K.Xjl = c2(Cb + oXtp, o0);
+                K.Xjpl = c2(Cb + oXtp, o1);
+                K.Xjh = c2(C + oXtp, o0);
+                K.Xjph = c2(C + oXtp, o1);
+                const uint32_t c = (uint32_t)((size_t)s * plane + (size_t)j * nr + i0);
+                aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, row4(P0, r), row4(P0, rm), row4(P0, rp), row4(Pm, r),
+                                            row4(P1, r), pr2(Pm, rm), pr2(Pm, rp), pr2(P1, rm), pr2(P1, rp), dot[0]);
+            }
+            __syncthreads();
+        }
+    }
+    if (WITH_DOT) {
+        Acc<EXACT> out[1];
+        if (reduce_last<EXACT, kAM, 1>(dot, a.partials, &a.sc->ticket[0], red_slot0 + blockIdx.x, red_total, out)) {
+            if (threadIdx.x == 0) {
+                a.sc->red1[0] = out[0].p;
+                a.sc->red1[1] = out[0].s;
+                if (a.p2p_ll) ll_push_pairs(a, a.sc->red1, 1);   // to every rank (peer communicator)
+            }
+        }
+    }
+}
+
 inline int tile_rows(int nr) { return (2 * kTilePairs + nr - 1) / nr + 3; }
 inline size_t tile_smem(int nr) { return sizeof(double) * 2 * 3 * (size_t)tile_rows(nr) * nr; }
 
@@ -672,9 +842,47 @@ inline unsigned grid_tma(uint32_t n) {   // n cells: 256-pair chunks, a resident
     return (unsigned)g;
 }
 
+// the plane-marching kernel (default; MASPCG_ANISO_MARCH=0 disables it, MASPCG_ANISO_MARCH_TJ / _GRID force
+// smaller tiles / grids for the tests): the pair layout, the full slab or its interior planes
+inline bool aniso_march(const Dims &d, const double *y, StencilPart part, AnisoMarch &M) {
+    const char *e = getenv("MASPCG_ANISO_MARCH");
+    if ((e && e[0] == '0') || !aniso_vec2(d, y) || part == StencilPart::Boundary) return false;
+    M.k0 = part == StencilPart::Full ? 0 : 1;
+    M.nk = part == StencilPart::Full ? d.nloc : d.nloc - 2;
+    if (M.nk < 1 || d.nr < 2) return false;
+    int tj = kAM / (d.nr / 2);
+    if (tj > d.nt) tj = d.nt;
+    const char *f = getenv("MASPCG_ANISO_MARCH_TJ");
+    if (f && atoi(f) > 0 && atoi(f) < tj) tj = atoi(f);
+    for (; tj >= 1; --tj) {
+        M.tj = tj;
+        M.pslot = (uint32_t)(tj + 2) * d.nr;
+        M.cslot = (uint32_t)(7 * tj + 3) * d.nr;
+        if (am_smem(M) <= 220u * 1024u) break;
+    }
+    if (tj < 1) return false;
+    M.njt = (d.nt + tj - 1) / tj;
+    M.units = (uint32_t)M.njt * (uint32_t)M.nk;
+    return true;
+}
+
+inline unsigned grid_march(const AnisoMarch &M) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t g = (uint32_t)sms;
+    const char *f = getenv("MASPCG_ANISO_MARCH_GRID");
+    if (f && atoi(f) > 0) g = (uint32_t)atoi(f);
+    if (g > M.units) g = M.units;
+    if (g > (uint32_t)kRedBlocks) g = kRedBlocks;
+    return g < 1 ? 1u : g;
+}
+
 unsigned aniso_stencil_blocks(const Dims &d, StencilPart part, const double *y) {
     const Range rg = make_range(d, part);
     if (!rg.vend) return 0u;
+    AnisoMarch M;
+    if (aniso_march(d, y, part, M)) return grid_march(M);
     if (aniso_tma(d, y, rg)) return grid_tma(rg.vend);
     return aniso_vec2(d, y) ? grid_aniso2(rg.vend) : grid_aniso(rg.vend);
 }
@@ -684,6 +892,39 @@ void launch_aniso_matvec(const Dims &d, const DevArrays &a, const AnisoArrays &x
     const Range rg = make_range(d, part);
     if (rg.vend == 0) return;
     const bool pdl = d.pdl != 0;
+    AnisoMarch M;
+    if (aniso_march(d, y, part, M)) {
+        const unsigned g = grid_march(M);
+        const size_t sm = am_smem(M);
+#define AM(W, L, E)                                                                                           \
+    do {                                                                                                      \
+        cudaFuncSetAttribute(k_aniso_march<W, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
+        cudaLaunchConfig_t cfg{};                                                                             \
+        cfg.gridDim = dim3(g);                                                                                \
+        cfg.blockDim = dim3(kAM);                                                                             \
+        cfg.dynamicSmemBytes = sm;                                                                            \
+        cfg.stream = st;                                                                                      \
+        cudaLaunchAttribute attr[1];                                                                          \
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                      \
+        attr[0].val.programmaticStreamSerializationAllowed = 1;                                               \
+        cfg.attrs = attr;                                                                                     \
+        cfg.numAttrs = pdl ? 1 : 0;                                                                           \
+        cudaLaunchKernelEx(&cfg, k_aniso_march<W, L, E>, d, a, x, y, M, red_slot0, red_total);                \
+    } while (0)
+        if (exact) {
+            if (with_dot) {
+                if (loop) AM(true, true, true);
+                else AM(true, false, true);
+            } else AM(false, false, true);
+        } else {
+            if (with_dot) {
+                if (loop) AM(true, true, false);
+                else AM(true, false, false);
+            } else AM(false, false, false);
+        }
+#undef AM
+        return;
+    }
     if (aniso_tma(d, y, rg)) {
         const unsigned g = grid_tma(rg.vend);
         const size_t sm = tile_smem(d.nr);

@@ -791,309 +791,6 @@ __global__ void __launch_bounds__(kVVThreads, 2) k_vv_rows2(VVDims v, VVArrays a
     }
 }
 
-// ------------------------------------------------------------ plane-marching fused operator (homogeneous)
-// One block owns tj theta-rows (all radii, nr even: 16-byte pairs) of a run of phi-planes and marches
-// through them: at step s it forms the terms e(s), tau_theta(s+1), tau_r(s+1), tau_phi(s) of its rows
-// (plus one halo row on each side) into shared-memory rings and, in the same pass, the three rows of
-// plane s-1 from the terms of steps s-1 and s-2 -- one barrier per plane, and the terms never touch
-// HBM: 104 B/cell (p, wc, W_r, W_theta, W_phi, sM / q) instead of the 184 of the two phases.  The
-// metric factors come from shared-memory copies of the 1-D arrays (per-row theta factors, per-step
-// phi factors), each product formed as Geo forms it, so the rows are the two-phase kernels' bit for bit.
-//   rings: e 3 planes, tau_theta 3, tau_r 3, tau_phi 2; (tj + 2) rows of nr + 2 values (slot nr = the
-//   outer-wall edge of the last radial cell)
-constexpr int kFusedSlots = 11;
-inline size_t fused_ring(int nr, int tj) { return (size_t)kFusedSlots * (tj + 2) * (nr + 2); }
-inline size_t fused_smem(int nr, int tj) {
-    return sizeof(double) * (fused_ring(nr, tj) + 4 * (size_t)(nr + 2) + 6 * (size_t)(tj + 3));
-}
-
-struct FGeo {            // shared-memory metric factors of a block
-    const double *rf2, *dR2, *rce, *hr;             // radial: nr+1, nr, nr+2, nr+1
-    const double *C, *sinf, *dt, *ht, *sinc;        // theta rows j0-1 .. j0+tj+1 (index g = j - j0 + 1)
-    __device__ __forceinline__ double A_r(int i, int g, double dpk) const { return mul(mul(rf2[i], C[g]), dpk); }
-    __device__ __forceinline__ double A_t(int i, int g, double dpk) const { return mul(mul(sinf[g], dR2[i]), dpk); }
-    __device__ __forceinline__ double A_p(int i, int g) const { return mul(dR2[i], dt[g]); }
-    __device__ __forceinline__ double L_t(int e, int g) const { return mul(rce[e], ht[g]); }
-    __device__ __forceinline__ double L_p(int e, int g, double hmk) const { return mul(mul(rce[e], sinc[g]), hmk); }
-};
-
-template <bool WITH_DOT, bool LOOP, bool EXACT>
-__global__ void __launch_bounds__(kVVThreads, 2) k_vv_fused(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
-                                                         int tj, int njt, int kchunk, FastDiv divh, unsigned total) {
-    if (LOOP && *(volatile int *)&base.sc->done) return;
-    extern __shared__ double fsm[];
-    const int nr = v.nr, nt = v.nt, RL = nr + 2, nh = nr >> 1;
-    const size_t tile = (size_t)(tj + 2) * RL;
-    double *sE = fsm, *sTT = sE + 3 * tile, *sTR = sTT + 3 * tile, *sTP = sTR + 3 * tile;
-    double *geo = sTP + 2 * tile;
-    const int jt = (int)(blockIdx.x % (unsigned)njt), kc = (int)(blockIdx.x / (unsigned)njt);
-    const int j0 = jt * tj, kb = kc * kchunk;
-    const int ke = kb + kchunk < v.nloc ? kb + kchunk : v.nloc;
-    FGeo G;
-    {
-        double *q = geo;
-        double *rf2 = q; q += nr + 2;
-        double *dR2 = q; q += nr + 2;
-        double *rce = q; q += nr + 2;
-        double *hr = q; q += nr + 2;
-        double *C = q; q += tj + 3;
-        double *sinf = q; q += tj + 3;
-        double *dt = q; q += tj + 3;
-        double *ht = q; q += tj + 3;
-        double *sinc = q;
-        for (int i = threadIdx.x; i < nr + 2; i += kVVThreads) {
-            rf2[i] = i <= nr ? a.rf2[i] : 0.0;
-            dR2[i] = i < nr ? a.dR2[i] : 0.0;
-            rce[i] = a.rce[i];
-            hr[i] = i <= nr ? a.hr[i] : 0.0;
-        }
-        for (int g = threadIdx.x; g < tj + 3; g += kVVThreads) {
-            const int j = j0 - 1 + g;
-            const bool in = j >= 0 && j < nt;
-            C[g] = in ? a.C[j] : 0.0;
-            dt[g] = in ? a.dt[j] : 0.0;
-            sinc[g] = in ? a.sinc[j] : 0.0;
-            sinf[g] = (j >= 0 && j <= nt) ? a.sinf[j] : 0.0;
-            ht[g] = (j >= 0 && j <= nt) ? a.ht[j] : 0.0;
-        }
-        G = FGeo{rf2, dR2, rce, hr, C, sinf, dt, ht, sinc};
-        __syncthreads();
-    }
-    const double *__restrict__ P = a.p;
-    const int nterm = (tj + 2) * nh, nrowc = tj * nh;
-    Acc<EXACT> dot[1];
-    if (kb < v.nloc) {
-        for (int s = kb - 1; s <= ke; ++s) {
-            const bool do_terms = s <= ke - 1, do_rows = s - 1 >= kb;
-            const int nw = (do_terms ? nterm : 0) + (do_rows ? nrowc : 0);
-            const int e3 = (s + 3) % 3, n3 = (s + 4) % 3;    // ring slots of planes s and s + 1 (s >= -1)
-            const double dps = a.dpp[s + 1], hm1 = a.hmp[s + 2];
-            for (int w = threadIdx.x; w < nw; w += kVVThreads) {
-                if (do_terms && w < nterm) {
-                    const int lr = (int)divh.div((uint32_t)w), i0 = 2 * (w - lr * nh), j = j0 - 1 + lr;
-                    if (j < 0 || j >= nt) continue;
-                    const int g = lr;   // geometry row of j
-                    const bool last = (i0 + 2 == nr);
-                    const size_t o = (size_t)lr * RL + i0;
-                    const int jp = j < nt - 1 ? j + 1 : j, jm = j > 0 ? j - 1 : 0;
-                    // plane s
-                    const double2 R = L2(P + PV(v, s, 0, j, i0)), T = L2(P + PV(v, s, 1, j, i0));
-                    const double2 Pp = L2(P + PV(v, s, 2, j, i0));
-                    // plane s + 1
-                    const double2 R1 = L2(P + PV(v, s + 1, 0, j, i0)), T1 = L2(P + PV(v, s + 1, 1, j, i0));
-                    const double2 P1 = L2(P + PV(v, s + 1, 2, j, i0)), P1jm = L2(P + PV(v, s + 1, 2, jm, i0));
-                    const double pm1 = __ldg(P + PV(v, s + 1, 2, j, i0 > 0 ? i0 - 1 : 0));
-                    const size_t pc1 = PC(v, s + 1, j, i0);
-                    const double2 wt = L2(a.Wt + pc1), wr = L2(a.Wr + pc1);
-                    if (lr <= tj) {   // e(s) of rows j0-1 .. j0+tj-1
-                        const double2 Tj1 = L2(P + PV(v, s, 1, jp, i0)), wc = L2(a.wc + PC(v, s, j, i0));
-                        const double r2 = last ? 0.0 : __ldg(P + PV(v, s, 0, j, i0 + 2));
-                        const double vr0 = (i0 == 0) ? 0.0 : R.x;
-                        double ev[2];
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int i = i0 + h;
-                            const double vrl = h ? R.y : vr0, vrh = h ? r2 : R.y;
-                            const double vtl = h ? T.y : T.x, vth = h ? Tj1.y : Tj1.x;
-                            const double vpl = h ? Pp.y : Pp.x, vph = h ? P1.y : P1.x;
-                            const double fr_lo = mul(G.A_r(i, g, dps), vrl);
-                            const double fr_hi = mul(G.A_r(i + 1, g, dps), vrh);
-                            const double ft_lo = (j == 0) ? 0.0 : mul(G.A_t(i, g, dps), vtl);
-                            const double ft_hi = (j == nt - 1) ? 0.0 : mul(G.A_t(i, g + 1, dps), vth);
-                            const double ap = G.A_p(i, g);
-                            const double fp_lo = mul(ap, vpl), fp_hi = mul(ap, vph);
-                            double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
-                            d = add(d, sub(fp_hi, fp_lo));
-                            ev[h] = mul(h ? wc.y : wc.x, d);
-                        }
-                        *reinterpret_cast<double2 *>(sE + e3 * tile + o) = make_double2(ev[0], ev[1]);
-                    }
-                    if (lr >= 1) {
-                        // tau_theta(s+1), rows j0 .. j0+tj-1: theta-edges at r-faces i0, i0+1 (and nr)
-                        if (lr <= tj) {
-                            double tv[2];
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                const int e = i0 + h;
-                                const double vrk = h ? R1.y : (i0 == 0 ? 0.0 : R1.x);
-                                const double vrkm = h ? R.y : (i0 == 0 ? 0.0 : R.x);
-                                const double up = h ? P1.y : P1.x;
-                                const double dn = h ? P1.x : (i0 == 0 ? 0.0 : pm1);
-                                const double gr_a = mul(G.hr[e], vrk), gr_b = mul(G.hr[e], vrkm);
-                                const double gp_a = mul(G.L_p(e + 1, g, hm1), up), gp_b = mul(G.L_p(e, g, hm1), dn);
-                                tv[h] = mul(h ? wt.y : wt.x, sub(sub(gr_a, gr_b), sub(gp_a, gp_b)));
-                            }
-                            *reinterpret_cast<double2 *>(sTT + n3 * tile + o) = make_double2(tv[0], tv[1]);
-                            if (last) {
-                                const double gp_b = mul(G.L_p(nr, g, hm1), P1.y);
-                                const double gt = sub(sub(mul(G.hr[nr], 0.0), mul(G.hr[nr], 0.0)),
-                                                      sub(mul(G.L_p(nr + 1, g, hm1), 0.0), gp_b));
-                                sTT[n3 * tile + o + 2] = mul(__ldg(a.WtO + (size_t)(s + 2) * nt + j), gt);
-                            }
-                        }
-                        // tau_r(s+1), rows j0 .. j0+tj
-                        double r0 = 0.0, r1 = 0.0;
-                        if (j >= 1) {
-#pragma unroll
-                            for (int h = 0; h < 2; ++h) {
-                                const int i = i0 + h;
-                                const double vpj = h ? P1.y : P1.x, vpjm = h ? P1jm.y : P1jm.x;
-                                const double vtk = h ? T1.y : T1.x, vtkm = h ? T.y : T.x;
-                                const double gp_a = mul(G.L_p(i + 1, g, hm1), vpj);
-                                const double gp_b = mul(G.L_p(i + 1, g - 1, hm1), vpjm);
-                                const double lt = G.L_t(i + 1, g);
-                                const double t = mul(h ? wr.y : wr.x, sub(sub(gp_a, gp_b), sub(mul(lt, vtk), mul(lt, vtkm))));
-                                if (h) r1 = t; else r0 = t;
-                            }
-                        }
-                        *reinterpret_cast<double2 *>(sTR + n3 * tile + o) = make_double2(r0, r1);
-                        // tau_phi(s), rows j0 .. j0+tj
-                        if (s >= kb) {
-                            double *tp = sTP + (size_t)((s + 2) & 1) * tile + o;
-                            double t0 = 0.0, t1 = 0.0;
-                            if (j >= 1) {
-                                const double2 Rjm = L2(P + PV(v, s, 0, jm, i0));
-                                const double tm1 = __ldg(P + PV(v, s, 1, j, i0 > 0 ? i0 - 1 : 0));
-                                const double2 wp = L2(a.Wp + UC(v, s, j, i0));
-#pragma unroll
-                                for (int h = 0; h < 2; ++h) {
-                                    const int e = i0 + h;
-                                    const double up = h ? T.y : T.x;
-                                    const double dn = h ? T.x : (i0 == 0 ? 0.0 : tm1);
-                                    const double vrj = h ? R.y : (i0 == 0 ? 0.0 : R.x);
-                                    const double vrjm = h ? Rjm.y : (i0 == 0 ? 0.0 : Rjm.x);
-                                    const double gt_a = mul(G.L_t(e + 1, g), up), gt_b = mul(G.L_t(e, g), dn);
-                                    const double gr_a = mul(G.hr[e], vrj), gr_b = mul(G.hr[e], vrjm);
-                                    const double t = mul(h ? wp.y : wp.x, sub(sub(gt_a, gt_b), sub(gr_a, gr_b)));
-                                    if (h) t1 = t; else t0 = t;
-                                }
-                                if (last) {
-                                    const double gt = sub(sub(mul(G.L_t(nr + 1, g), 0.0), mul(G.L_t(nr, g), T.y)),
-                                                          sub(mul(G.hr[nr], 0.0), mul(G.hr[nr], 0.0)));
-                                    tp[2] = mul(__ldg(a.WpO + (size_t)s * nt + j), gt);
-                                }
-                            } else if (last) {
-                                tp[2] = 0.0;
-                            }
-                            *reinterpret_cast<double2 *>(tp) = make_double2(t0, t1);
-                        }
-                    }
-                } else {
-                    // the rows of plane k = s - 1 from the terms of steps k and k - 1
-                    const int w2 = do_terms ? w - nterm : w;
-                    const int lr0 = (int)divh.div((uint32_t)w2), i0 = 2 * (w2 - lr0 * nh), lr = lr0 + 1, j = j0 + lr0;
-                    if (j >= nt) continue;
-                    const int g = lr, k = s - 1;
-                    const double dpk = a.dpp[k + 1], hmk = a.hmp[k + 1];
-                    const size_t o = (size_t)lr * RL + i0;
-                    const double *E0 = sE + (size_t)((k + 3) % 3) * tile + o;
-                    const double *Em = sE + (size_t)((k + 2) % 3) * tile + o;
-                    const double *TT0 = sTT + (size_t)((k + 3) % 3) * tile + o;
-                    const double *TT1 = sTT + (size_t)((k + 4) % 3) * tile + o;
-                    const double *TR0 = sTR + (size_t)((k + 3) % 3) * tile + o;
-                    const double *TR1 = sTR + (size_t)((k + 4) % 3) * tile + o;
-                    const double *TP0 = sTP + (size_t)((k + 2) & 1) * tile + o;
-                    const double2 pr = L2(P + PV(v, k, 0, j, i0)), pt = L2(P + PV(v, k, 1, j, i0));
-                    const double2 pp = L2(P + PV(v, k, 2, j, i0));
-                    const double2 sm0 = L2(a.sM + UV(v, k, 0, j, i0)), sm1 = L2(a.sM + UV(v, k, 1, j, i0));
-                    const double2 sm2 = L2(a.sM + UV(v, k, 2, j, i0));
-                    const double2 e = *reinterpret_cast<const double2 *>(E0);
-                    const double2 tt = *reinterpret_cast<const double2 *>(TT0);
-                    const double2 tp = *reinterpret_cast<const double2 *>(TP0);
-                    const double2 tr = *reinterpret_cast<const double2 *>(TR0);
-                    const double2 tt1 = *reinterpret_cast<const double2 *>(TT1);
-                    const double tt2 = TT0[2], tp2 = TP0[2];
-                    double yr0 = 0.0, yr1;
-                    {
-                        if (i0 >= 1) {
-                            yr0 = mul(sm0.x, pr.x);
-                            yr0 = add(yr0, mul(G.A_r(i0, g, dpk), sub(E0[-1], e.x)));
-                            double cc = sub(tt.x, tt1.x);
-                            if (j >= 1) cc = sub(cc, tp.x);
-                            if (j + 1 <= nt - 1) cc = add(cc, TP0[RL]);
-                            yr0 = add(yr0, mul(G.hr[i0], cc));
-                        }
-                        yr1 = mul(sm0.y, pr.y);
-                        yr1 = add(yr1, mul(G.A_r(i0 + 1, g, dpk), sub(e.x, e.y)));
-                        double cc = sub(tt.y, tt1.y);
-                        if (j >= 1) cc = sub(cc, tp.y);
-                        if (j + 1 <= nt - 1) cc = add(cc, TP0[RL + 1]);
-                        yr1 = add(yr1, mul(G.hr[i0 + 1], cc));
-                    }
-                    double yt0 = 0.0, yt1 = 0.0;
-                    if (j >= 1) {
-                        const double2 ej = *reinterpret_cast<const double2 *>(E0 - RL);
-                        const double2 tr1 = *reinterpret_cast<const double2 *>(TR1);
-                        yt0 = mul(sm1.x, pt.x);
-                        yt0 = add(yt0, mul(G.A_t(i0, g, dpk), sub(ej.x, e.x)));
-                        double cc = sub(tr1.x, tr.x);
-                        cc = add(cc, tp.x);
-                        cc = sub(cc, tp.y);
-                        yt0 = add(yt0, mul(G.L_t(i0 + 1, g), cc));
-                        yt1 = mul(sm1.y, pt.y);
-                        yt1 = add(yt1, mul(G.A_t(i0 + 1, g, dpk), sub(ej.y, e.y)));
-                        cc = sub(tr1.y, tr.y);
-                        cc = add(cc, tp.y);
-                        cc = sub(cc, tp2);
-                        yt1 = add(yt1, mul(G.L_t(i0 + 2, g), cc));
-                    }
-                    double yp0, yp1;
-                    {
-                        const double2 ek = *reinterpret_cast<const double2 *>(Em);
-                        double2 lo, hi;
-                        if (j == 0) {
-                            lo.x = mul(__ldg(a.WN + i0), add(__ldg(a.ring + 2 * i0), __ldg(a.ring + 2 * i0 + 1)));
-                            lo.y = mul(__ldg(a.WN + i0 + 1), add(__ldg(a.ring + 2 * i0 + 2), __ldg(a.ring + 2 * i0 + 3)));
-                        } else {
-                            lo = tr;
-                        }
-                        if (j == nt - 1) {
-                            const double *rs = a.ring + 2 * (nr + i0);
-                            hi.x = mul(__ldg(a.WS + i0), -add(__ldg(rs), __ldg(rs + 1)));
-                            hi.y = mul(__ldg(a.WS + i0 + 1), -add(__ldg(rs + 2), __ldg(rs + 3)));
-                        } else {
-                            hi = *reinterpret_cast<const double2 *>(TR0 + RL);
-                        }
-                        yp0 = mul(sm2.x, pp.x);
-                        yp0 = add(yp0, mul(G.A_p(i0, g), sub(ek.x, e.x)));
-                        double cc = sub(lo.x, hi.x);
-                        cc = sub(cc, tt.x);
-                        cc = add(cc, tt.y);
-                        yp0 = add(yp0, mul(G.L_p(i0 + 1, g, hmk), cc));
-                        yp1 = mul(sm2.y, pp.y);
-                        yp1 = add(yp1, mul(G.A_p(i0 + 1, g), sub(ek.y, e.y)));
-                        cc = sub(lo.y, hi.y);
-                        cc = sub(cc, tt.y);
-                        cc = add(cc, tt2);
-                        yp1 = add(yp1, mul(G.L_p(i0 + 2, g, hmk), cc));
-                    }
-                    S2(y + UV(v, k, 0, j, i0), yr0, yr1);
-                    S2(y + UV(v, k, 1, j, i0), yt0, yt1);
-                    S2(y + UV(v, k, 2, j, i0), yp0, yp1);
-                    if (WITH_DOT) {
-                        dot[0].add(pr.x, yr0);
-                        dot[0].add(pt.x, yt0);
-                        dot[0].add(pp.x, yp0);
-                        dot[0].add(pr.y, yr1);
-                        dot[0].add(pt.y, yt1);
-                        dot[0].add(pp.y, yp1);
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    if (WITH_DOT) {
-        Acc<EXACT> out[1];
-        if (reduce_last<EXACT, kVVThreads, 1>(dot, base.partials, &base.sc->ticket[0], blockIdx.x, total, out)) {
-            if (threadIdx.x == 0) {
-                base.sc->red1[0] = out[0].p;
-                base.sc->red1[1] = out[0].s;
-            }
-        }
-    }
-}
-
 // ------------------------------------------------------------ setup of a solve (the oracle's rhs + PCG start)
 template <bool EXACT>
 __global__ void __launch_bounds__(kVVThreads) k_vv_setup_residual(VVDims v, VVArrays a, DevArrays base, Dims dv,
@@ -1212,42 +909,6 @@ void launch_vv_diag(const VVDims &v, const VVArrays &a, cudaStream_t st) {
     k_vv_diag<<<vv_grid(v.ncell), kVVThreads, 0, st>>>(v, a);
 }
 
-// MASPCG_VV_TJ = n > 0 selects the plane-marching fused operator with n theta-rows per block (read at
-// every launch); unset or 0: the two-phase kernels, which measured faster
-inline int vv_fused_tj(int nr) {
-    const char *e = getenv("MASPCG_VV_TJ");
-    int tj = e ? atoi(e) : 0;
-    while (tj > 0 && fused_smem(nr, tj) > 200 * 1024) --tj;
-    return tj;
-}
-
-template <bool W, bool L, bool E>
-bool launch_fused(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, cudaStream_t st) {
-    const int tj = vv_fused_tj(v.nr);
-    if (tj < 1 || (v.nr % 2) != 0 || ((uintptr_t)y & 15) != 0) return false;
-    const int njt = (v.nt + tj - 1) / tj;
-    if (njt > kRedBlocks) return false;
-    const size_t sm = fused_smem(v.nr, tj);
-    // queried at every launch (host-side only; no shared state between contexts of different shapes)
-    int dev = 0, per_sm = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_vv_fused<W, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);   // the cap
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vv_fused<W, L, E>, kVVThreads, sm);
-    if (per_sm < 1) per_sm = 1;
-    int target = sms * per_sm;
-    if (target > kRedBlocks) target = kRedBlocks;
-    int nkc = target / njt;   // one resident wave: a partial second wave would double the time
-    if (nkc > v.nloc) nkc = v.nloc;
-    if (nkc * njt > kRedBlocks) nkc = kRedBlocks / njt;
-    if (nkc < 1) nkc = 1;
-    const int kchunk = (v.nloc + nkc - 1) / nkc;
-    nkc = (v.nloc + kchunk - 1) / kchunk;
-    const unsigned g = (unsigned)(njt * nkc);
-    k_vv_fused<W, L, E><<<g, kVVThreads, sm, st>>>(v, a, base, y, tj, njt, kchunk, make_fastdiv((uint32_t)(v.nr / 2)), g);
-    return true;
-}
-
 // Opt-in (MASPCG_VV_CHUNK = ring planes, > 2): measured SLOWER than the one-pass two phases on c3v (1,491 vs
 // 1,128 us per ring + matvec with the ring sized from 0.45 of the L2; 1,472-1,568 us for rings of 30-80
 // planes): the terms did not stay in the L2 (ncu without cache control: the rows still read ~77 B/cell from
@@ -1333,17 +994,8 @@ void launch_vv_matvec(const VVDims &vin, const VVArrays &a, const DevArrays &bas
     v.ring = 0;
     v.chunk = 0;
     v.nchunks = 1;
-    if (!wall) {
-        bool done;
-        if (!with_dot) done = launch_fused<false, false, true>(v, a, base, y, st);
-        else if (exact) done = loop ? launch_fused<true, true, true>(v, a, base, y, st)
-                                    : launch_fused<true, false, true>(v, a, base, y, st);
-        else done = loop ? launch_fused<true, true, false>(v, a, base, y, st)
-                         : launch_fused<true, false, false>(v, a, base, y, st);
-        if (done) return;
-        // default: the plane-marching operator with TMA-staged planes (vv_march.cu)
-        if (launch_vv_march(v, a, base, y, with_dot, loop, exact, st)) return;
-    }
+    // default for the homogeneous operator: the plane-marching kernel with TMA-staged planes (vv_march.cu)
+    if (!wall && launch_vv_march(v, a, base, y, with_dot, loop, exact, st)) return;
     const bool pair = pair0;
     const uint32_t nt1 = v.ncell + 2 * v.plane1;
     if (pair && vv_staged()) {

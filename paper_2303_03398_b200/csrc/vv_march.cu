@@ -96,9 +96,13 @@ inline size_t march_smem_bytes(const MarchLayout &L) {
 
 namespace {
 
-template <bool WITH_DOT, bool LOOP, bool EXACT>
+// PROBE: the timing-probe build (tools/vv_march_probe.py), whose `dbg` bits switch parts off -- 1 arithmetic,
+// 2 bulk copies, 4 block barrier, 8 rows, 16 terms, 32 everything; its results are wrong.  The product build
+// (PROBE = false) compiles the switches out.
+template <bool WITH_DOT, bool LOOP, bool EXACT, bool PROBE>
 __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevArrays base, double *__restrict__ y,
-                                                    MarchLayout L, unsigned total, int dbg) {
+                                                    MarchLayout L, unsigned total, int dbg_) {
+    const int dbg = PROBE ? dbg_ : 0;
     if (LOOP && *(volatile int *)&base.sc->done) return;
     if (dbg & 32) return;
     extern __shared__ __align__(128) double sm[];
@@ -479,11 +483,11 @@ bool vv_march_layout(const VVDims &v, MarchLayout &L) {
     return true;
 }
 
-template <bool W, bool LP, bool E>
+template <bool W, bool LP, bool E, bool PR>
 static void launch_march(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, const MarchLayout &L,
                          cudaStream_t st) {
     const size_t sm = march_smem_bytes(L);
-    cudaFuncSetAttribute(k_vv_march<W, LP, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_vv_march<W, LP, E, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -493,8 +497,8 @@ static void launch_march(const VVDims &v, const VVArrays &a, const DevArrays &ba
     if (g > L.units) g = L.units;
     if (g > (uint32_t)kRedBlocks) g = kRedBlocks;
     if (g < 1) g = 1;
-    const char *d = getenv("MASPCG_VV_MARCH_DEBUG");   // (timing probes only: 1 copies only, 2 arithmetic only)
-    k_vv_march<W, LP, E><<<g, kMT, sm, st>>>(v, a, base, y, L, g, d ? atoi(d) : 0);
+    const char *d = getenv("MASPCG_VV_MARCH_DEBUG");   // (timing probes only, see k_vv_march)
+    k_vv_march<W, LP, E, PR><<<g, kMT, sm, st>>>(v, a, base, y, L, g, d ? atoi(d) : 0);
 }
 
 bool launch_vv_march(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
@@ -502,13 +506,18 @@ bool launch_vv_march(const VVDims &v, const VVArrays &a, const DevArrays &base, 
     if (!vv_march_enabled() || ((uintptr_t)y & 15) != 0) return false;
     MarchLayout L;
     if (!vv_march_layout(v, L)) return false;
-    if (!with_dot) launch_march<false, false, true>(v, a, base, y, L, st);
+    const char *d = getenv("MASPCG_VV_MARCH_DEBUG");
+    if (d && atoi(d) != 0) {   // the timing probe (apply only)
+        launch_march<false, false, true, true>(v, a, base, y, L, st);
+        return true;
+    }
+    if (!with_dot) launch_march<false, false, true, false>(v, a, base, y, L, st);
     else if (exact) {
-        if (loop) launch_march<true, true, true>(v, a, base, y, L, st);
-        else launch_march<true, false, true>(v, a, base, y, L, st);
+        if (loop) launch_march<true, true, true, false>(v, a, base, y, L, st);
+        else launch_march<true, false, true, false>(v, a, base, y, L, st);
     } else {
-        if (loop) launch_march<true, true, false>(v, a, base, y, L, st);
-        else launch_march<true, false, false>(v, a, base, y, L, st);
+        if (loop) launch_march<true, true, false, false>(v, a, base, y, L, st);
+        else launch_march<true, false, false, false>(v, a, base, y, L, st);
     }
     return true;
 }

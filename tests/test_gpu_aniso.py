@@ -228,3 +228,62 @@ def test_full_c3a_fixed_iterations_bitwise(M, oracle_mod):
     g = gpu_solve(M, p, tol=0.0, maxit=12)
     assert g[0] == o["status"] == M.NOT_CONVERGED
     assert_bitwise(g, o)
+
+
+# ------------------------------------------------------------------ the plane-marching TMA operator (default)
+@pytest.mark.parametrize("tj,grid", [(None, None), (1, None), (3, 5), (2, 1)])
+@pytest.mark.parametrize("shape,bc", [((12, 6, 2), (0, 1)), ((64, 16, 8), (1, 0)), ((10, 9, 8), (0, 0)),
+                                      ((2, 5, 3), (0, 1)), ((20, 13, 11), (1, 0))])
+def test_march_operator_and_solve_bitwise(M, oracle_mod, monkeypatch, tj, grid, shape, bc):
+    """The default stencil for even nr: one plane-marching kernel whose p planes and coefficient rows arrive by
+    bulk copies (k_aniso_march).  y = A x and whole solves bit-identical to the oracle; forced small tiles (ragged
+    last tile) and grids (several (tile, plane) segments per block, the rings carried across segments)."""
+    if tj:
+        monkeypatch.setenv("MASPCG_ANISO_MARCH_TJ", str(tj))
+    if grid:
+        monkeypatch.setenv("MASPCG_ANISO_MARCH_GRID", str(grid))
+    p = inputs.random_aniso_problem(*shape, 5 * sum(shape) + bc[0], bc_in=bc[0], bc_out=bc[1])
+    o = oracle_op(oracle_mod, p)
+    S = M.solver_for_problem(p)
+    x = inputs.white_noise(93, p.nr, p.nt, 0, p.np)
+    y = S.apply(dev(x)).cpu().numpy()
+    S.close()
+    assert np.array_equal(y, o.apply(x)), np.abs(y - o.apply(x)).max()
+    assert_bitwise(gpu_solve(M, p), oracle_mod.solve_aniso_problem(p))
+
+
+@pytest.mark.parametrize("march", ["0", "1"])
+def test_march_and_pair_kernels_c2a(M, oracle_mod, monkeypatch, march):
+    """c2a with the marching kernel and with the previous TMA pair kernel (MASPCG_ANISO_MARCH=0): both the
+    oracle's iterates bit for bit."""
+    monkeypatch.setenv("MASPCG_ANISO_MARCH", march)
+    p = inputs.make_aniso_problem("c2a")
+    assert_bitwise(gpu_solve(M, p), oracle_mod.solve_aniso_problem(p))
+
+
+def test_march_multirank_bitwise(M, oracle_mod, monkeypatch):
+    """The marching kernel on the interior planes of 3 loopback slabs (the boundary planes by the pair kernel),
+    forced small tiles and grids: every rank returns the global oracle's iterates."""
+    import torch
+    monkeypatch.setenv("MASPCG_ANISO_MARCH_TJ", "3")
+    monkeypatch.setenv("MASPCG_ANISO_MARCH_GRID", "4")
+    P = 3
+    fn = lambda k0, n: inputs.random_aniso_problem(10, 7, 12, 21, bc_in=0, bc_out=1, k0=k0 or 0, nloc=n)
+    full = fn(None, None)
+    o = oracle_mod.solve_aniso_problem(full)
+
+    def rank(r, group):
+        k0, nloc = inputs.slab_extent(full.np, r, P)
+        p = fn(k0, nloc)
+        S = M.solver_for_problem(p, loopback=(group, r))
+        xr = dev(p.x0)
+        st, info, hist = S.solve(dev(p.f), xr, p.tol, p.maxit, raise_on_error=False)
+        torch.cuda.current_stream().synchronize()
+        res = (st, info["iters"], hist, xr.cpu().numpy())
+        S.close()
+        return res
+
+    out = run_ranks(M, P, rank)
+    for st, it, hist, _ in out:
+        assert st == o["status"] and it == o["iters"] and np.array_equal(hist, o["hist"])
+    assert np.array_equal(np.concatenate([r[3] for r in out], axis=0), o["x"])

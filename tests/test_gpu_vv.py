@@ -124,27 +124,6 @@ def test_vv_c3v_full_size_operator_bitwise(M, oracle_mod):
         S.close()
 
 
-@pytest.mark.parametrize("tj", [1, 3, 6])
-@pytest.mark.parametrize("shape,walls", [((8, 4, 2), (0, 1)), ((16, 16, 32), (1, 0)), ((20, 30, 48), (0, 1))])
-def test_vv_fused_operator_exact(M, oracle_mod, monkeypatch, tj, shape, walls):
-    """The opt-in plane-marching fused operator (MASPCG_VV_TJ = theta-rows per block, even nr): apply
-    and a whole solve identical to the oracle, like the default two-phase kernels."""
-    import torch
-    monkeypatch.setenv("MASPCG_VV_TJ", str(tj))
-    p = inputs.make_vv_problem("rand", shape=shape, seed=11 + tj, wall_in=walls[0], wall_out=walls[1])
-    op = oracle_op(oracle_mod, p)
-    S = gpu_solver(M, p)
-    x = np.stack([inputs.white_noise(91 + c, p.nr, p.nt, 0, p.np) for c in range(3)], axis=1)
-    y = S.vv_apply(dev(x))
-    torch.cuda.synchronize()
-    S.close()
-    assert np.array_equal(y.cpu().numpy(), op.apply(x))
-    o = oracle_mod.vv_solve_problem(p)
-    st, info, hist, xs, _, _ = gpu_vv_solve(M, p)
-    assert st == o["status"] == 0 and info["iters"] == o["iters"]
-    assert np.array_equal(hist, o["hist"]) and np.array_equal(xs, o["x"])
-
-
 @pytest.mark.parametrize("chunk,graphs", [(1, 1), (7, 1), (16, 0)])
 def test_vv_loop_modes_identical(M, oracle_mod, chunk, graphs):
     p = inputs.make_vv_problem("rand", shape=(9, 8, 10), seed=4)
@@ -243,14 +222,10 @@ def run_ranks(M, P, fn):
 
 
 @pytest.mark.parametrize("P,shape,walls", [(2, (7, 6, 8), (0, 1)), (3, (5, 9, 6), (0, 0)), (4, (8, 5, 8), (1, 1)),
-                                           (4, (16, 16, 4), (0, 1)), (3, (8, 6, 9), "fused")])
+                                           (4, (16, 16, 4), (0, 1)), (3, (8, 6, 9), (0, 1))])
 def test_vv_multirank_exact(M, oracle_mod, monkeypatch, P, shape, walls):
     """phi-slabs on P loopback ranks: the diagonal of each slab, the iterates and the history equal the
-    global oracle's bit for bit (nloc = 1 included), identical on every rank; "fused": the opt-in
-    plane-marching operator (MASPCG_VV_TJ) on the slabs."""
-    if walls == "fused":
-        monkeypatch.setenv("MASPCG_VV_TJ", "2")
-        walls = (0, 1)
+    global oracle's bit for bit (nloc = 1 included), identical on every rank (even nr: the marching operator)."""
     full = inputs.make_vv_problem("rand", shape=shape, seed=P, wall_in=walls[0], wall_out=walls[1])
     o = oracle_mod.vv_solve_problem(full)
     op = o["op"]
