@@ -678,6 +678,12 @@ __global__ void __launch_bounds__(kAM, 1) k_aniso_march(Dims d, DevArrays a, Ani
             mbar_wait_parity(&pbar[i2 & 3u], (i2 >> 2) & 1u);
             mbar_wait_parity(&cbar[cb % 3u], (cb / 3u) & 1u);
         }
+        // the own row's p of planes s - 1 and s, carried from step to step (plane s + 1 is the only new row4)
+        Row4 Mj{0.0, 0.0, 0.0, 0.0}, Rj{0.0, 0.0, 0.0, 0.0};
+        // and the coefficients of the face below plane s (the previous step's face above): T_phi, X_rphi, X_thetaphi
+        double2 cTp = make_double2(0.0, 0.0), cXp = cTp, cXj = cTp, cXjp = cTp;
+        double cXpq = 0.0;
+        double2 Mjm2 = make_double2(0.0, 0.0), Mjp2 = Mjm2;   // plane s - 1, rows j -+ 1 (the previous step's)
         for (int s = kb; s < ke; ++s) {
             const uint32_t q = (uint32_t)(s - (kb - 1));
             if (threadIdx.x == 0) {   // into the slots of plane s - 2 and stage s - 2 (free: barrier of step s - 1)
@@ -709,24 +715,47 @@ __global__ void __launch_bounds__(kAM, 1) k_aniso_march(Dims d, DevArrays a, Ani
                 K.tr2 = C[o0 + oq];
                 K.ttl = c2(C + oTt, o0);
                 K.tth = c2(C + oTt, o1);
-                K.tpl = c2(Cb + oTp, o0);
+                if (s == kb) {
+                    cTp = c2(Cb + oTp, o0);
+                    cXp = c2(Cb + oXrp, o0);
+                    cXpq = Cb[oXrp + o0 + oq];
+                    cXj = c2(Cb + oXtp, o0);
+                    cXjp = c2(Cb + oXtp, o1);
+                }
+                K.tpl = cTp;
                 K.tph = c2(C + oTp, o0);
                 K.d7 = c2(C + oD7, o0);
                 K.Xt0 = c2(C + oXrt, o0);
                 K.Xt1 = c2(C + oXrt, o1);
                 K.Xt0q = C[oXrt + o0 + oq];
                 K.Xt1q = C[oXrt + o1 + oq];
-                K.Xp0 = c2(Cb + oXrp, o0);
+                K.Xp0 = cXp;
                 K.Xp1 = c2(C + oXrp, o0);
-                K.Xp0q = Cb[oXrp + o0 + oq];
+                K.Xp0q = cXpq;
                 K.Xp1q = C[oXrp + o0 + oq];
-                K.Xjl = c2(Cb + oXtp, o0);
-                K.Xjpl = c2(Cb + oXtp, o1);
+                K.Xjl = cXj;
+                K.Xjpl = cXjp;
                 K.Xjh = c2(C + oXtp, o0);
                 K.Xjph = c2(C + oXtp, o1);
                 const uint32_t c = (uint32_t)((size_t)s * plane + (size_t)j * nr + i0);
-                aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, row4(P0, r), row4(P0, rm), row4(P0, rp), row4(Pm, r),
-                                            row4(P1, r), pr2(Pm, rm), pr2(Pm, rp), pr2(P1, rm), pr2(P1, rp), dot[0]);
+                if (s == kb) {
+                    Mj = row4(Pm, r);
+                    Rj = row4(P0, r);
+                    Mjm2 = pr2(Pm, rm);
+                    Mjp2 = pr2(Pm, rp);
+                }
+                const Row4 Pj = row4(P1, r), Rjm = row4(P0, rm), Rjp = row4(P0, rp);
+                aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, Rj, Rjm, Rjp, Mj, Pj, Mjm2, Mjp2, pr2(P1, rm),
+                                            pr2(P1, rp), dot[0]);
+                Mjm2 = make_double2(Rjm.c0, Rjm.c1);
+                Mjp2 = make_double2(Rjp.c0, Rjp.c1);
+                Mj = Rj;
+                Rj = Pj;
+                cTp = K.tph;
+                cXp = K.Xp1;
+                cXpq = K.Xp1q;
+                cXj = K.Xjh;
+                cXjp = K.Xjph;
             }
             __syncthreads();
         }
