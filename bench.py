@@ -217,10 +217,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def ncu_traffic_per_launch(path_id: int):
+def ncu_traffic_per_launch(path_id, name=None):
     """dram__bytes_read.sum + dram__bytes_write.sum of the stencil kernel from the committed
-    `ncu --set full` summary of that path (profiles/ncu_stencil_path{1,2}.json), or None."""
-    path = os.path.join(ROOT, "profiles", f"ncu_stencil_path{path_id}.json")
+    `ncu --set full` summary of that path (profiles/ncu_stencil_path{1,2}.json, or profiles/<name>.json), or None."""
+    path = os.path.join(ROOT, "profiles", f"{name}.json" if name else f"ncu_stencil_path{path_id}.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -700,11 +700,12 @@ def main():
     path = dict(PATHS[stats["path"]])
     if aniso:   # the 19-point field-aligned stencil: p, T_r, T_theta, T_phi, D7, Xrt, Xrp, Xtp, q
         path.update({"name": "three kernels, field-aligned 19-point operator",
-                     "stencil": ("aniso stencil + p.q (k_aniso_flat)", 72), "iter": 152})
+                     "stencil": ("aniso stencil + p.q (k_aniso_march, the plane-marching TMA stencil; "
+                                 "MASPCG_ANISO_MARCH=0: k_aniso_tma)", 72), "iter": 152})
     st_name, st_bpc = path["stencil"]
     mv_ms = stats["matvec_ms"] / max(stats["matvec_launches"], 1)
     achieved = st_bpc * ncell_local / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
-    traffic, traffic_src = ncu_traffic_per_launch(stats["path"])
+    traffic, traffic_src = ncu_traffic_per_launch(stats["path"], "ncu_aniso_stencil" if aniso else None)
     # sampled timing: average per launch over the timed launches, times the launches of the run
     avg = lambda k: stats[k + "_ms"] / stats[k + "_launches"] if stats[k + "_launches"] else 0.0
     kern_ms = (avg("matvec") + avg("update") + avg("pupdate")) * iters
