@@ -39,6 +39,9 @@ __device__ __forceinline__ void acquire_p_halo(const DevArrays &a) {
         const unsigned long long e = *(volatile unsigned long long *)&a.p2p->epoch[P2P_HALO];
         while (ld_acquire_sys64(&a.p2p->flags[P2P_FROM_LEFT][0]) < e) __nanosleep(32);
         while (ld_acquire_sys64(&a.p2p->flags[P2P_FROM_RIGHT][0]) < e) __nanosleep(32);
+        // the halo planes may next be read by bulk copies (the async proxy) of the TMA-staged stencils: order
+        // the acquired generic-proxy writes before them
+        asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
 }
