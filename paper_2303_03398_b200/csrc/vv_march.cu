@@ -13,10 +13,11 @@
 //    tau_phi = W Gamma of the cell's lower edges) and the three rows of plane s - 1.
 //  * thread = one r-pair (i0, i0 + 1) of one tile row, FIXED for the whole segment, so the products of the
 //    1-D metric factors that do not depend on phi (rf2[i] C[j], sinf[j] dR2[i], dR2[i] dt[j], rce[e] ht[j],
-//    rce[e] sinc[j]) are formed once into registers; per plane only the phi factors dp(k), hm(k) multiply
-//    in -- each product associated exactly as vv.cu's Geo forms it, so every term and row is bit-identical
-//    to the oracle's.  Rows j0 - 1 (lower halo: e only) and j0 + tj (upper halo: tau_r, tau_phi only) are
-//    computed by extra threads of the block.
+//    rce[e] sinc[j]) are formed once (13 in registers, the six used once per step in a per-thread shared
+//    table: the kernel then fits 128 registers without spills); per plane only the phi factors dp(k), hm(k)
+//    (a shared table of the slab's planes) multiply in -- each product associated exactly as vv.cu's Geo forms
+//    it, so every term and row is bit-identical to the oracle's.  Rows j0 - 1 (lower halo: e only) and j0 + tj
+//    (upper halo: tau_r, tau_phi only) are computed by extra threads of the block.
 //  * inputs: the p tile of a plane (3 components x rows j0-1 .. j0+tj, one contiguous range per component)
 //    in a 3-slot ring (plane s + 2 in flight while planes s, s + 1 are read) and the coefficient rows of a
 //    step (wc, W_r, W_theta, W_phi of plane s, sM of plane s - 1) in a 2-slot ring -- every one a 1-D bulk
@@ -24,8 +25,10 @@
 //    slot's mbarrier.  No per-element staging arithmetic; the memory-level parallelism comes from the bulk
 //    copies, not from resident warps.
 //  * terms: the neighbours' e, tau (i - 1, i + 1, j - 1, j + 1 of the same plane) through a double-buffered
-//    shared tile [tj + 2][nr + 2] per term (slot nr: the outer-wall edge of the last radial cell); the
-//    cell's own terms of planes s - 1, s carried by the step order.  One block barrier per plane.
+//    shared tile [tj + 2][nr + 2] per term (slot nr: the outer-wall edge of the last radial cell); the own p of
+//    plane s - 1 and tau_theta(s), tau_r(s) in registers, e(s - 2) read before e(s) overwrites it.  One block
+//    barrier per plane (a hardware barrier: waiting warps issue nothing -- mbarrier-based split barriers with
+//    spinning or sleeping waiters measured slower).
 //  * Dot2 partial of p.q per thread, combined by the last block (reduce_last) as every matvec kernel.
 // Homogeneous operator only (the loop's; the wall-data operator of the setup uses the two phases), nr even.
 #include <cuda_runtime.h>
