@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "arith.cuh"
 #include "common.cuh"
@@ -218,231 +219,239 @@ __global__ void __launch_bounds__(kMT, 1) k_vv_march(VVDims v, VVArrays a, DevAr
             issue_c(kb - 1, cb);
         }
         double2 Rm = make_double2(0.0, 0.0), Tm = Rm, Pm = Rm;   // own p of plane s - 1
-        for (int s = kb - 1; s <= ke; ++s) {
-            const int q = s - (kb - 1);
-            if (t == 0 && !(dbg & 2)) {   // into the slots of plane s - 1 and step s - 1 (free: the barrier of step s - 1)
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                if (s + 2 <= ke) issue_p(s + 2, pb + (uint32_t)q + 2);
-                if (s + 1 <= ke) issue_c(s + 1, cb + (uint32_t)q + 1);
-            }
-            const bool e_on = s <= ke - 1;
-            // the outer-wall edge weights of this step (last pair only), loaded ahead of the waits
-            double wto = 0.0, wpo = 0.0;
-            if (act && last && s >= kb) {
-                if (role == 2) wto = __ldg(a.WtO + (size_t)(s + 1) * nt + j);
-                if (e_on && j >= 1) wpo = __ldg(a.WpO + (size_t)s * nt + j);
-            }
-            const uint32_t ps = pb + (uint32_t)q, ps1 = ps + 1, cs_ = cb + (uint32_t)q;
-            const double *P0 = pring + (size_t)(ps % 3) * L.pslot;    // plane s
-            const double *P1 = pring + (size_t)(ps1 % 3) * L.pslot;   // plane s + 1
-            const double *Cw = cring + (size_t)(cs_ & 1) * L.cslot;
-            const double *Cr = Cw + (size_t)(tj + 1) * nr, *Cp = Cr + (size_t)(tj + 1) * nr, *Ct = Cp + (size_t)(tj + 1) * nr;
-            const double *Cs = Ct + (size_t)tj * nr;
-            double *TBn = tb0 + (size_t)(s & 1) * L.tbuf;         // terms of plane s (still e of plane s - 2)
-            const double *TBo = tb0 + (size_t)((s - 1) & 1) * L.tbuf;   // terms of plane s - 1
-            const size_t TA = (size_t)TR2 * RL;                    // one term array
-            if (!(dbg & 2)) {
-                mbar_wait(&pbar[ps % 3], (ps / 3) & 1u);
-                if (e_on) mbar_wait(&pbar[ps1 % 3], (ps1 / 3) & 1u);
-                mbar_wait(&cbar[cs_ & 1], (cs_ >> 1) & 1u);
-            }
-            if (act && !(dbg & 1)) {
-                const double dps = phi[2 * (s + 1)], hms = phi[2 * (s + 1) + 1];
-                auto PT = [&](const double *P, int c, int r) { return P + ((size_t)c * TR2 + r) * nr; };
-                const double2 R = ld2(PT(P0, 0, lr) + i0), T = ld2(PT(P0, 1, lr) + i0), Pp = ld2(PT(P0, 2, lr) + i0);
-                const double vr0 = i0 == 0 ? 0.0 : R.x;
-                const size_t o = (size_t)lr * RL + i0;
-                // -- e(s): rows j0 - 1 .. j0 + tj - 1 (stored after the rows have read e(s - 2) from the same slot)
-                double e0 = 0.0, e1 = 0.0;
-                if (role <= 2 && e_on && !(dbg & 16)) {
-                    const double2 Tj1 = ld2(PT(P0, 1, lr + 1) + i0), Pk1 = ld2(PT(P1, 2, lr) + i0);
-                    const double vr2 = last ? 0.0 : PT(P0, 0, lr)[i0 + 2];
-                    const double2 wc = ld2(Cw + (size_t)lr * nr + i0);
-                    const double2 aU = cst[0][t];
-                    const double A0 = mul(arC0, dps), A1 = mul(arC1, dps), A2 = mul(cst[2][t].x, dps);
-                    {
-                        const double fr_lo = mul(A0, vr0), fr_hi = mul(A1, R.y);
-                        const double ft_lo = (j == 0) ? 0.0 : mul(mul(atS0, dps), T.x);
-                        const double ft_hi = (j == nt - 1) ? 0.0 : mul(mul(aU.x, dps), Tj1.x);
-                        const double fp_lo = mul(ap0, Pp.x), fp_hi = mul(ap0, Pk1.x);
-                        double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
-                        d = add(d, sub(fp_hi, fp_lo));
-                        e0 = mul(wc.x, d);
-                    }
-                    {
-                        const double fr_lo = mul(A1, R.y), fr_hi = mul(A2, vr2);
-                        const double ft_lo = (j == 0) ? 0.0 : mul(mul(atS1, dps), T.y);
-                        const double ft_hi = (j == nt - 1) ? 0.0 : mul(mul(aU.y, dps), Tj1.y);
-                        const double fp_lo = mul(ap1, Pp.y), fp_hi = mul(ap1, Pk1.y);
-                        double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
-                        d = add(d, sub(fp_hi, fp_lo));
-                        e1 = mul(wc.y, d);
-                    }
+        // The step loop, specialised for interior tiles (every row of the tile and its halo rows strictly between
+        // the poles: no pole / boundary-row predicates) and generic for the first and last tiles
+        auto march = [&](auto interior) {
+            constexpr bool IN = decltype(interior)::value;
+            const bool ACT = IN ? member : act;
+            for (int s = kb - 1; s <= ke; ++s) {
+                const int q = s - (kb - 1);
+                if (t == 0 && !(dbg & 2)) {   // into the slots of plane s - 1 and step s - 1 (free: the barrier of step s - 1)
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (s + 2 <= ke) issue_p(s + 2, pb + (uint32_t)q + 2);
+                    if (s + 1 <= ke) issue_c(s + 1, cb + (uint32_t)q + 1);
                 }
-                // -- tau_theta(s) (own rows), tau_r(s) (own + upper halo), tau_phi(s) (own + upper halo)
-                double tt0 = 0.0, tt1 = 0.0, tr0 = 0.0, tr1 = 0.0;
-                if (role >= 2 && s >= kb && !(dbg & 16)) {
-                    const double hm = hms;
-                    const double Lp0 = mul(lpc0, hm), Lp1 = mul(lpc1, hm), Lp2 = mul(lpc2, hm);
-                    const size_t co = (size_t)(lr - 1) * nr + i0;
-                    if (role == 2) {
-                        const double pm1 = i0 == 0 ? 0.0 : PT(P0, 2, lr)[i0 - 1];
-                        const double2 wt = ld2(Ct + co);
+                const bool e_on = s <= ke - 1;
+                // the outer-wall edge weights of this step (last pair only), loaded ahead of the waits
+                double wto = 0.0, wpo = 0.0;
+                if (ACT && last && s >= kb) {
+                    if (role == 2) wto = __ldg(a.WtO + (size_t)(s + 1) * nt + j);
+                    if (e_on && (IN || j >= 1)) wpo = __ldg(a.WpO + (size_t)s * nt + j);
+                }
+                const uint32_t ps = pb + (uint32_t)q, ps1 = ps + 1, cs_ = cb + (uint32_t)q;
+                const double *P0 = pring + (size_t)(ps % 3) * L.pslot;    // plane s
+                const double *P1 = pring + (size_t)(ps1 % 3) * L.pslot;   // plane s + 1
+                const double *Cw = cring + (size_t)(cs_ & 1) * L.cslot;
+                const double *Cr = Cw + (size_t)(tj + 1) * nr, *Cp = Cr + (size_t)(tj + 1) * nr, *Ct = Cp + (size_t)(tj + 1) * nr;
+                const double *Cs = Ct + (size_t)tj * nr;
+                double *TBn = tb0 + (size_t)(s & 1) * L.tbuf;         // terms of plane s (still e of plane s - 2)
+                const double *TBo = tb0 + (size_t)((s - 1) & 1) * L.tbuf;   // terms of plane s - 1
+                const size_t TA = (size_t)TR2 * RL;                    // one term array
+                if (!(dbg & 2)) {
+                    mbar_wait(&pbar[ps % 3], (ps / 3) & 1u);
+                    if (e_on) mbar_wait(&pbar[ps1 % 3], (ps1 / 3) & 1u);
+                    mbar_wait(&cbar[cs_ & 1], (cs_ >> 1) & 1u);
+                }
+                if (ACT && !(dbg & 1)) {
+                    const double dps = phi[2 * (s + 1)], hms = phi[2 * (s + 1) + 1];
+                    auto PT = [&](const double *P, int c, int r) { return P + ((size_t)c * TR2 + r) * nr; };
+                    const double2 R = ld2(PT(P0, 0, lr) + i0), T = ld2(PT(P0, 1, lr) + i0), Pp = ld2(PT(P0, 2, lr) + i0);
+                    const double vr0 = i0 == 0 ? 0.0 : R.x;
+                    const size_t o = (size_t)lr * RL + i0;
+                    // -- e(s): rows j0 - 1 .. j0 + tj - 1 (stored after the rows have read e(s - 2) from the same slot)
+                    double e0 = 0.0, e1 = 0.0;
+                    if (role <= 2 && e_on && !(dbg & 16)) {
+                        const double2 Tj1 = ld2(PT(P0, 1, lr + 1) + i0), Pk1 = ld2(PT(P1, 2, lr) + i0);
+                        const double vr2 = last ? 0.0 : PT(P0, 0, lr)[i0 + 2];
+                        const double2 wc = ld2(Cw + (size_t)lr * nr + i0);
+                        const double2 aU = cst[0][t];
+                        const double A0 = mul(arC0, dps), A1 = mul(arC1, dps), A2 = mul(cst[2][t].x, dps);
                         {
-                            const double vrkm = i0 == 0 ? 0.0 : Rm.x;
-                            const double gr_a = mul(hr0, vr0), gr_b = mul(hr0, vrkm);
-                            const double gp_a = mul(Lp1, Pp.x), gp_b = mul(Lp0, pm1);
-                            tt0 = mul(wt.x, sub(sub(gr_a, gr_b), sub(gp_a, gp_b)));
+                            const double fr_lo = mul(A0, vr0), fr_hi = mul(A1, R.y);
+                            const double ft_lo = (!IN && j == 0) ? 0.0 : mul(mul(atS0, dps), T.x);
+                            const double ft_hi = (!IN && j == nt - 1) ? 0.0 : mul(mul(aU.x, dps), Tj1.x);
+                            const double fp_lo = mul(ap0, Pp.x), fp_hi = mul(ap0, Pk1.x);
+                            double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
+                            d = add(d, sub(fp_hi, fp_lo));
+                            e0 = mul(wc.x, d);
                         }
                         {
-                            const double gr_a = mul(hr1, R.y), gr_b = mul(hr1, Rm.y);
-                            const double gp_a = mul(Lp2, Pp.y), gp_b = mul(Lp1, Pp.x);
-                            tt1 = mul(wt.y, sub(sub(gr_a, gr_b), sub(gp_a, gp_b)));
-                        }
-                        double *TT = TBn + TA + o;
-                        st2(TT, tt0, tt1);
-                        if (last) {   // the outer-wall theta-edge (r-face nr): Gt(nr) with zero wall data
-                            const double hrn = a.hr[nr];
-                            const double Lpn1 = mul(mul(a.rce[nr + 1], a.sinc[j]), hm);
-                            const double gt = sub(sub(mul(hrn, 0.0), mul(hrn, 0.0)), sub(mul(Lpn1, 0.0), mul(Lp2, Pp.y)));
-                            TT[2] = mul(wto, gt);
+                            const double fr_lo = mul(A1, R.y), fr_hi = mul(A2, vr2);
+                            const double ft_lo = (!IN && j == 0) ? 0.0 : mul(mul(atS1, dps), T.y);
+                            const double ft_hi = (!IN && j == nt - 1) ? 0.0 : mul(mul(aU.y, dps), Tj1.y);
+                            const double fp_lo = mul(ap1, Pp.y), fp_hi = mul(ap1, Pk1.y);
+                            double d = add(sub(fr_hi, fr_lo), sub(ft_hi, ft_lo));
+                            d = add(d, sub(fp_hi, fp_lo));
+                            e1 = mul(wc.y, d);
                         }
                     }
-                    if (j >= 1) {
-                        const double2 Pjm = ld2(PT(P0, 2, lr - 1) + i0), lpm = cst[1][t];
-                        const double2 wr = ld2(Cr + co);
-                        {
-                            const double gp_a = mul(Lp1, Pp.x), gp_b = mul(mul(lpm.x, hm), Pjm.x);
-                            tr0 = mul(wr.x, sub(sub(gp_a, gp_b), sub(mul(lt1, T.x), mul(lt1, Tm.x))));
-                        }
-                        {
-                            const double gp_a = mul(Lp2, Pp.y), gp_b = mul(mul(lpm.y, hm), Pjm.y);
-                            tr1 = mul(wr.y, sub(sub(gp_a, gp_b), sub(mul(lt2, T.y), mul(lt2, Tm.y))));
-                        }
-                    }
-                    st2(TBn + 2 * TA + o, tr0, tr1);
-                    if (e_on) {   // tau_phi(s), planes kb .. ke - 1
-                        double tp0 = 0.0, tp1 = 0.0, tpw = 0.0;
-                        if (j >= 1) {
-                            const double2 Rjm = ld2(PT(P0, 0, lr - 1) + i0);
-                            const double tm1 = i0 == 0 ? 0.0 : PT(P0, 1, lr)[i0 - 1];
-                            const double2 wp = ld2(Cp + co);
+                    // -- tau_theta(s) (own rows), tau_r(s) (own + upper halo), tau_phi(s) (own + upper halo)
+                    double tt0 = 0.0, tt1 = 0.0, tr0 = 0.0, tr1 = 0.0;
+                    if (role >= 2 && s >= kb && !(dbg & 16)) {
+                        const double hm = hms;
+                        const double Lp0 = mul(lpc0, hm), Lp1 = mul(lpc1, hm), Lp2 = mul(lpc2, hm);
+                        const size_t co = (size_t)(lr - 1) * nr + i0;
+                        if (role == 2) {
+                            const double pm1 = i0 == 0 ? 0.0 : PT(P0, 2, lr)[i0 - 1];
+                            const double2 wt = ld2(Ct + co);
                             {
-                                const double vrjm = i0 == 0 ? 0.0 : Rjm.x;
-                                const double gt_a = mul(lt1, T.x), gt_b = mul(cst[2][t].y, tm1);
-                                const double gr_a = mul(hr0, vr0), gr_b = mul(hr0, vrjm);
-                                tp0 = mul(wp.x, sub(sub(gt_a, gt_b), sub(gr_a, gr_b)));
+                                const double vrkm = i0 == 0 ? 0.0 : Rm.x;
+                                const double gr_a = mul(hr0, vr0), gr_b = mul(hr0, vrkm);
+                                const double gp_a = mul(Lp1, Pp.x), gp_b = mul(Lp0, pm1);
+                                tt0 = mul(wt.x, sub(sub(gr_a, gr_b), sub(gp_a, gp_b)));
                             }
                             {
-                                const double gt_a = mul(lt2, T.y), gt_b = mul(lt1, T.x);
-                                const double gr_a = mul(hr1, R.y), gr_b = mul(hr1, Rjm.y);
-                                tp1 = mul(wp.y, sub(sub(gt_a, gt_b), sub(gr_a, gr_b)));
+                                const double gr_a = mul(hr1, R.y), gr_b = mul(hr1, Rm.y);
+                                const double gp_a = mul(Lp2, Pp.y), gp_b = mul(Lp1, Pp.x);
+                                tt1 = mul(wt.y, sub(sub(gr_a, gr_b), sub(gp_a, gp_b)));
                             }
-                            if (last) {   // the outer-wall phi-edge: Gp(nr) with zero wall data
+                            double *TT = TBn + TA + o;
+                            st2(TT, tt0, tt1);
+                            if (last) {   // the outer-wall theta-edge (r-face nr): Gt(nr) with zero wall data
                                 const double hrn = a.hr[nr];
-                                const double Ltn1 = mul(a.rce[nr + 1], a.ht[j]);
-                                const double gt = sub(sub(mul(Ltn1, 0.0), mul(lt2, T.y)), sub(mul(hrn, 0.0), mul(hrn, 0.0)));
-                                tpw = mul(wpo, gt);
+                                const double Lpn1 = mul(mul(a.rce[nr + 1], a.sinc[j]), hm);
+                                const double gt = sub(sub(mul(hrn, 0.0), mul(hrn, 0.0)), sub(mul(Lpn1, 0.0), mul(Lp2, Pp.y)));
+                                TT[2] = mul(wto, gt);
                             }
                         }
-                        double *TP = TBn + 3 * TA + o;
-                        st2(TP, tp0, tp1);
-                        if (last) TP[2] = tpw;
+                        if (IN || j >= 1) {
+                            const double2 Pjm = ld2(PT(P0, 2, lr - 1) + i0), lpm = cst[1][t];
+                            const double2 wr = ld2(Cr + co);
+                            {
+                                const double gp_a = mul(Lp1, Pp.x), gp_b = mul(mul(lpm.x, hm), Pjm.x);
+                                tr0 = mul(wr.x, sub(sub(gp_a, gp_b), sub(mul(lt1, T.x), mul(lt1, Tm.x))));
+                            }
+                            {
+                                const double gp_a = mul(Lp2, Pp.y), gp_b = mul(mul(lpm.y, hm), Pjm.y);
+                                tr1 = mul(wr.y, sub(sub(gp_a, gp_b), sub(mul(lt2, T.y), mul(lt2, Tm.y))));
+                            }
+                        }
+                        st2(TBn + 2 * TA + o, tr0, tr1);
+                        if (e_on) {   // tau_phi(s), planes kb .. ke - 1
+                            double tp0 = 0.0, tp1 = 0.0, tpw = 0.0;
+                            if (IN || j >= 1) {
+                                const double2 Rjm = ld2(PT(P0, 0, lr - 1) + i0);
+                                const double tm1 = i0 == 0 ? 0.0 : PT(P0, 1, lr)[i0 - 1];
+                                const double2 wp = ld2(Cp + co);
+                                {
+                                    const double vrjm = i0 == 0 ? 0.0 : Rjm.x;
+                                    const double gt_a = mul(lt1, T.x), gt_b = mul(cst[2][t].y, tm1);
+                                    const double gr_a = mul(hr0, vr0), gr_b = mul(hr0, vrjm);
+                                    tp0 = mul(wp.x, sub(sub(gt_a, gt_b), sub(gr_a, gr_b)));
+                                }
+                                {
+                                    const double gt_a = mul(lt2, T.y), gt_b = mul(lt1, T.x);
+                                    const double gr_a = mul(hr1, R.y), gr_b = mul(hr1, Rjm.y);
+                                    tp1 = mul(wp.y, sub(sub(gt_a, gt_b), sub(gr_a, gr_b)));
+                                }
+                                if (last) {   // the outer-wall phi-edge: Gp(nr) with zero wall data
+                                    const double hrn = a.hr[nr];
+                                    const double Ltn1 = mul(a.rce[nr + 1], a.ht[j]);
+                                    const double gt = sub(sub(mul(Ltn1, 0.0), mul(lt2, T.y)), sub(mul(hrn, 0.0), mul(hrn, 0.0)));
+                                    tpw = mul(wpo, gt);
+                                }
+                            }
+                            double *TP = TBn + 3 * TA + o;
+                            st2(TP, tp0, tp1);
+                            if (last) TP[2] = tpw;
+                        }
                     }
+                    // -- the rows of plane k = s - 1 (own rows)
+                    if (role == 2 && s - 1 >= kb && !(dbg & 8)) {
+                        const int k = s - 1;
+                        const double dpk = phi[2 * (k + 1)], hmk = phi[2 * (k + 1) + 1];
+                        const double *Eo = TBo + o, *TTo = TBo + TA + o, *TRo = TBo + 2 * TA + o, *TPo = TBo + 3 * TA + o;
+                        const double2 e = ld2(Eo), tt = ld2(TTo), tr = ld2(TRo), tp = ld2(TPo);
+                        const double2 ek = ld2(TBn + o);   // own e(k - 1): written at step s - 2, not yet overwritten
+                        const double tt2 = TTo[2], tp2 = TPo[2];
+                        const size_t so = (size_t)(lr - 1) * nr + i0;
+                        const double2 sm0 = ld2(Cs + so), sm1 = ld2(Cs + (size_t)tj * nr + so), sm2 = ld2(Cs + 2 * (size_t)tj * nr + so);
+                        double yr0 = 0.0, yr1;
+                        {
+                            const double2 tpj = (IN || j + 1 <= nt - 1) ? ld2(TPo + RL) : make_double2(0.0, 0.0);
+                            if (i0 >= 1) {
+                                yr0 = mul(sm0.x, Rm.x);
+                                yr0 = add(yr0, mul(mul(arC0, dpk), sub(Eo[-1], e.x)));
+                                double cc = sub(tt.x, tt0);
+                                if (IN || j >= 1) cc = sub(cc, tp.x);
+                                if (IN || j + 1 <= nt - 1) cc = add(cc, tpj.x);
+                                yr0 = add(yr0, mul(hr0, cc));
+                            }
+                            yr1 = mul(sm0.y, Rm.y);
+                            yr1 = add(yr1, mul(mul(arC1, dpk), sub(e.x, e.y)));
+                            double cc = sub(tt.y, tt1);
+                            if (IN || j >= 1) cc = sub(cc, tp.y);
+                            if (IN || j + 1 <= nt - 1) cc = add(cc, tpj.y);
+                            yr1 = add(yr1, mul(hr1, cc));
+                        }
+                        double yt0 = 0.0, yt1 = 0.0;
+                        if (IN || j >= 1) {
+                            const double2 ej = ld2(Eo - RL);
+                            yt0 = mul(sm1.x, Tm.x);
+                            yt0 = add(yt0, mul(mul(atS0, dpk), sub(ej.x, e.x)));
+                            double cc = sub(tr0, tr.x);
+                            cc = add(cc, tp.x);
+                            cc = sub(cc, tp.y);
+                            yt0 = add(yt0, mul(lt1, cc));
+                            yt1 = mul(sm1.y, Tm.y);
+                            yt1 = add(yt1, mul(mul(atS1, dpk), sub(ej.y, e.y)));
+                            cc = sub(tr1, tr.y);
+                            cc = add(cc, tp.y);
+                            cc = sub(cc, tp2);
+                            yt1 = add(yt1, mul(lt2, cc));
+                        }
+                        double yp0, yp1;
+                        {
+                            double2 lo, hi;
+                            if (!IN && j == 0) {
+                                lo.x = mul(__ldg(a.WN + i0), add(__ldg(a.ring + 2 * i0), __ldg(a.ring + 2 * i0 + 1)));
+                                lo.y = mul(__ldg(a.WN + i0 + 1), add(__ldg(a.ring + 2 * i0 + 2), __ldg(a.ring + 2 * i0 + 3)));
+                            } else {
+                                lo = tr;
+                            }
+                            if (!IN && j == nt - 1) {
+                                const double *rs = a.ring + 2 * (nr + i0);
+                                hi.x = mul(__ldg(a.WS + i0), -add(__ldg(rs), __ldg(rs + 1)));
+                                hi.y = mul(__ldg(a.WS + i0 + 1), -add(__ldg(rs + 2), __ldg(rs + 3)));
+                            } else {
+                                hi = ld2(TRo + RL);
+                            }
+                            yp0 = mul(sm2.x, Pm.x);
+                            yp0 = add(yp0, mul(ap0, sub(ek.x, e.x)));
+                            double cc = sub(lo.x, hi.x);
+                            cc = sub(cc, tt.x);
+                            cc = add(cc, tt.y);
+                            yp0 = add(yp0, mul(mul(lpc1, hmk), cc));
+                            yp1 = mul(sm2.y, Pm.y);
+                            yp1 = add(yp1, mul(ap1, sub(ek.y, e.y)));
+                            cc = sub(lo.y, hi.y);
+                            cc = sub(cc, tt.y);
+                            cc = add(cc, tt2);
+                            yp1 = add(yp1, mul(mul(lpc2, hmk), cc));
+                        }
+                        const size_t yo = ((size_t)k * 3) * v.plane1 + (size_t)j * nr + i0;
+                        st2(y + yo, yr0, yr1);
+                        st2(y + yo + v.plane1, yt0, yt1);
+                        st2(y + yo + 2 * (size_t)v.plane1, yp0, yp1);
+                        if (WITH_DOT) {
+                            dot[0].add(Rm.x, yr0);
+                            dot[0].add(Tm.x, yt0);
+                            dot[0].add(Pm.x, yp0);
+                            dot[0].add(Rm.y, yr1);
+                            dot[0].add(Tm.y, yt1);
+                            dot[0].add(Pm.y, yp1);
+                        }
+                    }
+                    if (role <= 2 && e_on) st2(TBn + o, e0, e1);
+                    Rm = R;
+                    Tm = T;
+                    Pm = Pp;
                 }
-                // -- the rows of plane k = s - 1 (own rows)
-                if (role == 2 && s - 1 >= kb && !(dbg & 8)) {
-                    const int k = s - 1;
-                    const double dpk = phi[2 * (k + 1)], hmk = phi[2 * (k + 1) + 1];
-                    const double *Eo = TBo + o, *TTo = TBo + TA + o, *TRo = TBo + 2 * TA + o, *TPo = TBo + 3 * TA + o;
-                    const double2 e = ld2(Eo), tt = ld2(TTo), tr = ld2(TRo), tp = ld2(TPo);
-                    const double2 ek = ld2(TBn + o);   // own e(k - 1): written at step s - 2, not yet overwritten
-                    const double tt2 = TTo[2], tp2 = TPo[2];
-                    const size_t so = (size_t)(lr - 1) * nr + i0;
-                    const double2 sm0 = ld2(Cs + so), sm1 = ld2(Cs + (size_t)tj * nr + so), sm2 = ld2(Cs + 2 * (size_t)tj * nr + so);
-                    double yr0 = 0.0, yr1;
-                    {
-                        const double2 tpj = (j + 1 <= nt - 1) ? ld2(TPo + RL) : make_double2(0.0, 0.0);
-                        if (i0 >= 1) {
-                            yr0 = mul(sm0.x, Rm.x);
-                            yr0 = add(yr0, mul(mul(arC0, dpk), sub(Eo[-1], e.x)));
-                            double cc = sub(tt.x, tt0);
-                            if (j >= 1) cc = sub(cc, tp.x);
-                            if (j + 1 <= nt - 1) cc = add(cc, tpj.x);
-                            yr0 = add(yr0, mul(hr0, cc));
-                        }
-                        yr1 = mul(sm0.y, Rm.y);
-                        yr1 = add(yr1, mul(mul(arC1, dpk), sub(e.x, e.y)));
-                        double cc = sub(tt.y, tt1);
-                        if (j >= 1) cc = sub(cc, tp.y);
-                        if (j + 1 <= nt - 1) cc = add(cc, tpj.y);
-                        yr1 = add(yr1, mul(hr1, cc));
-                    }
-                    double yt0 = 0.0, yt1 = 0.0;
-                    if (j >= 1) {
-                        const double2 ej = ld2(Eo - RL);
-                        yt0 = mul(sm1.x, Tm.x);
-                        yt0 = add(yt0, mul(mul(atS0, dpk), sub(ej.x, e.x)));
-                        double cc = sub(tr0, tr.x);
-                        cc = add(cc, tp.x);
-                        cc = sub(cc, tp.y);
-                        yt0 = add(yt0, mul(lt1, cc));
-                        yt1 = mul(sm1.y, Tm.y);
-                        yt1 = add(yt1, mul(mul(atS1, dpk), sub(ej.y, e.y)));
-                        cc = sub(tr1, tr.y);
-                        cc = add(cc, tp.y);
-                        cc = sub(cc, tp2);
-                        yt1 = add(yt1, mul(lt2, cc));
-                    }
-                    double yp0, yp1;
-                    {
-                        double2 lo, hi;
-                        if (j == 0) {
-                            lo.x = mul(__ldg(a.WN + i0), add(__ldg(a.ring + 2 * i0), __ldg(a.ring + 2 * i0 + 1)));
-                            lo.y = mul(__ldg(a.WN + i0 + 1), add(__ldg(a.ring + 2 * i0 + 2), __ldg(a.ring + 2 * i0 + 3)));
-                        } else {
-                            lo = tr;
-                        }
-                        if (j == nt - 1) {
-                            const double *rs = a.ring + 2 * (nr + i0);
-                            hi.x = mul(__ldg(a.WS + i0), -add(__ldg(rs), __ldg(rs + 1)));
-                            hi.y = mul(__ldg(a.WS + i0 + 1), -add(__ldg(rs + 2), __ldg(rs + 3)));
-                        } else {
-                            hi = ld2(TRo + RL);
-                        }
-                        yp0 = mul(sm2.x, Pm.x);
-                        yp0 = add(yp0, mul(ap0, sub(ek.x, e.x)));
-                        double cc = sub(lo.x, hi.x);
-                        cc = sub(cc, tt.x);
-                        cc = add(cc, tt.y);
-                        yp0 = add(yp0, mul(mul(lpc1, hmk), cc));
-                        yp1 = mul(sm2.y, Pm.y);
-                        yp1 = add(yp1, mul(ap1, sub(ek.y, e.y)));
-                        cc = sub(lo.y, hi.y);
-                        cc = sub(cc, tt.y);
-                        cc = add(cc, tt2);
-                        yp1 = add(yp1, mul(mul(lpc2, hmk), cc));
-                    }
-                    const size_t yo = ((size_t)k * 3) * v.plane1 + (size_t)j * nr + i0;
-                    st2(y + yo, yr0, yr1);
-                    st2(y + yo + v.plane1, yt0, yt1);
-                    st2(y + yo + 2 * (size_t)v.plane1, yp0, yp1);
-                    if (WITH_DOT) {
-                        dot[0].add(Rm.x, yr0);
-                        dot[0].add(Tm.x, yt0);
-                        dot[0].add(Pm.x, yp0);
-                        dot[0].add(Rm.y, yr1);
-                        dot[0].add(Tm.y, yt1);
-                        dot[0].add(Pm.y, yp1);
-                    }
-                }
-                if (role <= 2 && e_on) st2(TBn + o, e0, e1);
-                Rm = R;
-                Tm = T;
-                Pm = Pp;
+                if (!(dbg & 4)) __syncthreads();
             }
-            if (!(dbg & 4)) __syncthreads();
-        }
+        };
+        if (j0 - 1 >= 1 && j0 + tj <= nt - 2) march(std::true_type{});
+        else march(std::false_type{});
         __syncthreads();   // segment end: every slot and term buffer free
     }
     if (WITH_DOT) {

@@ -11,6 +11,8 @@ fixed sample of cells.
                                         # tol = 0 iterations (the bench runs 500)
     python tools/make_golden.py c3v     # the staggered vector viscosity on the c3 grid (bench.py --operator
                                         # vv), 81 M unknowns, tol 1e-10 (oracle/masoracle_vv.c, single thread)
+    python tools/make_golden.py c3a     # field-aligned conduction on the c3 grid (bench.py --operator aniso),
+                                        # tol 1e-10 (oracle/masoracle.c -fopenmp)
 
 Runs the oracle's -fopenmp build (identical values to the plain build,
 tests/test_oracle_pins.py::test_openmp_build_gives_identical_iterates).
@@ -42,16 +44,24 @@ def sample_index(n, seed=12345):
 def main(name):
     oracle.use_openmp(True)
     vv = name in inputs.VV_CONFIGS
-    p = inputs.make_vv_problem(name) if vv else inputs.make_problem(name)
+    an = name in inputs.ANISO_CONFIGS
+    p = inputs.make_vv_problem(name) if vv else (inputs.make_aniso_problem(name) if an else inputs.make_problem(name))
     maxit = 40 if name == "c4" else p.maxit
     t0 = time.time()
-    o = oracle.vv_solve_problem(p, maxit=maxit) if vv else oracle.solve_problem(p, maxit=maxit)
+    if vv:
+        o = oracle.vv_solve_problem(p, maxit=maxit)
+    elif an:
+        o = oracle.solve_aniso_problem(p, maxit=maxit)
+    else:
+        o = oracle.solve_problem(p, maxit=maxit)
     dt = time.time() - t0
     x = o["x"].ravel()
     idx = sample_index(x.size)
     out = {
         "source": (f"tools/make_golden.py {name}: oracle/masoracle_vv.c vector-viscosity PCG on "
                    f"inputs.make_vv_problem('{name}'), tol {p.tol}, maxit {maxit}") if vv else
+                  (f"tools/make_golden.py {name}: oracle/masoracle.c (-fopenmp build) field-aligned PCG on "
+                   f"inputs.make_aniso_problem('{name}'), tol {p.tol}, maxit {maxit}") if an else
                   (f"tools/make_golden.py {name}: oracle/masoracle.c (-fopenmp build) masoracle_pcg on "
                    f"inputs.make_problem('{name}') (BASELINE.json {name}), tol {p.tol}, maxit {maxit}"),
         "maxit": maxit,
