@@ -287,3 +287,15 @@ def test_march_multirank_bitwise(M, oracle_mod, monkeypatch):
     for st, it, hist, _ in out:
         assert st == o["status"] and it == o["iters"] and np.array_equal(hist, o["hist"])
     assert np.array_equal(np.concatenate([r[3] for r in out], axis=0), o["x"])
+
+
+@pytest.mark.parametrize("name", ["c1a", "c2a"])
+def test_march_fast_arithmetic_tolerance_contract(M, oracle_mod, name):
+    """MASPCG_OPT_ARITH = 1 through the marching stencil: the tolerance contract (solution relative L2 <= 1e-10,
+    iterations +-1)."""
+    p = inputs.make_aniso_problem(name)
+    o = oracle_mod.solve_aniso_problem(p)
+    st, info, hist, x = gpu_solve(M, p, opts={M.OPT_ARITH: M.ARITH_FAST})
+    assert st == o["status"] == 0
+    assert abs(info["iters"] - o["iters"]) <= 1
+    assert np.linalg.norm(x - o["x"]) <= 1e-10 * np.linalg.norm(o["x"])

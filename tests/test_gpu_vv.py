@@ -351,3 +351,15 @@ def test_vv_march_multirank_exact(M, oracle_mod, monkeypatch, P, shape):
     for st, info, hist, *_ in res:
         assert st == o["status"] == 0 and info["iters"] == o["iters"] and np.array_equal(hist, o["hist"])
     assert np.array_equal(np.concatenate([r[3] for r in res], axis=0), o["x"])
+
+
+@pytest.mark.parametrize("name,shape", [("c2v", None), ("rand", (16, 16, 32))])
+def test_vv_fast_arithmetic_tolerance_contract(M, oracle_mod, name, shape):
+    """MASPCG_OPT_ARITH = 1 (FMA-contracted updates, plain dot sums) through the marching operator: the tolerance
+    contract of BASELINE.json (solution relative L2 <= 1e-10 against the oracle, iterations +-1)."""
+    p = inputs.make_vv_problem(name, shape=shape, seed=3) if shape else inputs.make_vv_problem(name)
+    o = oracle_mod.vv_solve_problem(p)
+    st, info, hist, x, _, _ = gpu_vv_solve(M, p, opts={M.OPT_ARITH: M.ARITH_FAST})
+    assert st == o["status"] == 0
+    assert abs(info["iters"] - o["iters"]) <= 1
+    assert np.linalg.norm(x - o["x"]) <= 1e-10 * np.linalg.norm(o["x"])
