@@ -649,7 +649,8 @@ __global__ void __launch_bounds__(kAM, 1) k_aniso_march(Dims d, DevArrays a, Ani
             const uint32_t b0 = (uint32_t)(jhi0 - j0 + 1) * nr * 8u, b1 = (uint32_t)(jhi1 - j0 + 1) * nr * 8u;
             const bool full = s >= kb;
             mbar_expect(&cbar[q], (full ? 2 * b0 + 2 * b1 : 0u) + 2 * b0 + b1);
-            const size_t ps = (size_t)s * plane + (size_t)j0 * nr, pu = ps + plane;   // plane s, the face above
+            const size_t pu = (size_t)(s + 1) * plane + (size_t)j0 * nr;         // the face above plane s
+            const size_t ps = full ? pu - plane : 0;                              // plane s (s >= kb >= 0)
             if (full) {
                 bulk_copy(cs, gaddr64(a.Tr, ps), b0, &cbar[q]);
                 bulk_copy(cs + oTt, gaddr64(a.Tt, ps), b1, &cbar[q]);
