@@ -510,7 +510,7 @@ static void launch_march(const VVDims &v, const VVArrays &a, const DevArrays &ba
     if (g > (uint32_t)kRedBlocks) g = kRedBlocks;
     if (g < 1) g = 1;
     const char *d = getenv("MASPCG_VV_MARCH_DEBUG");   // (timing probes only, see k_vv_march)
-    k_vv_march<W, LP, E, PR><<<g, kMT, sm, st>>>(v, a, base, y, L, g, d ? atoi(d) : 0);
+    k_vv_march<W, LP, E, PR><<<g, kMT, sm, st>>>(v, a, base, y, L, g, PR && d ? (atoi(d) & 0xff) : 0);
 }
 
 bool launch_vv_march(const VVDims &v, const VVArrays &a, const DevArrays &base, double *y, bool with_dot, bool loop,
@@ -519,7 +519,9 @@ bool launch_vv_march(const VVDims &v, const VVArrays &a, const DevArrays &base, 
     MarchLayout L;
     if (!vv_march_layout(v, L)) return false;
     const char *d = getenv("MASPCG_VV_MARCH_DEBUG");
-    if (d && atoi(d) != 0) {   // the timing probe (apply only)
+    // the timing probe (tools/vv_march_probe.py sets the switch bits plus 0x100): never a loop matvec, and only with
+    // the 0x100 marker, so a stray value cannot change a solve
+    if (d && (atoi(d) & 0x100) && !with_dot && !loop) {
         launch_march<false, false, true, true>(v, a, base, y, L, st);
         return true;
     }

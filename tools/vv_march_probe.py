@@ -30,7 +30,9 @@ for extra in sys.argv[2:]:
     variants.append((extra, {k: v}))
 for name, env in variants:
     old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
+    # the library honours the switch bits only with the 0x100 probe marker (vv_march.cu)
+    os.environ.update({k: (str(int(v) | 0x100) if k == "MASPCG_VV_MARCH_DEBUG" and v != "0" else v)
+                       for k, v in env.items()})
     for _ in range(3):
         S.vv_apply(x, y)
     torch.cuda.synchronize()
