@@ -122,3 +122,78 @@ def test_aniso_full_size_solve_matches_oracle_golden(M, name):
     assert np.array_equal(xs[idx], np.array(g["x_sample"]))
     assert math.fsum(xs * xs) == g["x_norm2_fsum"]
     assert hashlib.sha256(np.ascontiguousarray(xs, dtype="<f8").tobytes()).hexdigest() == g["x_sha256"]
+
+
+# ------------------------------------------------------------------ the 8-GPU decomposition at full size (loopback)
+def _run_loopback(M, P, fn):
+    """P ranks in one process on cuda:0 (the loopback communicator: the library's halo exchanges and rank-ordered
+    reductions, without NCCL), one host thread each."""
+    import threading
+
+    import torch
+    group = M.LoopbackGroup(P)
+    out, errs = [None] * P, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                out[r] = fn(r, group)
+            st.synchronize()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=800)
+    assert not any(t.is_alive() for t in th), "a rank hung"
+    group.close()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def _check_slabs_against_golden(g, res):
+    xs = np.concatenate([r[3].reshape(r[3].shape[0], -1) for r in res], axis=0).ravel()
+    for st, iters, hist, _ in res:
+        assert st == g["status"] and iters == g["iters"]
+        assert np.array_equal(hist, np.array(g["hist"]))
+    assert hashlib.sha256(np.ascontiguousarray(xs, dtype="<f8").tobytes()).hexdigest() == g["x_sha256"]
+
+
+@pytest.mark.timeout(1500)
+@pytest.mark.parametrize("name", ["c3", "c3v"])
+def test_full_size_8_slabs_match_golden(M, name):
+    """The bench workloads split into the 8 phi-slabs of the 8-GPU strong-scaling run (75 planes each), on 8 loopback
+    ranks: every rank's history and the concatenated solution equal the single-rank oracle golden bit for bit (c3:
+    830 iterations, the scalar operator; c3v: 841, the vector operator with its pole-ring sums all-gathered)."""
+    import torch
+    g = json.load(open(os.path.join(HERE, "golden", f"{name}_full_solve.json")))
+    P = 8
+    vv = name.endswith("v")
+    np_ = inputs.VV_CONFIGS[name][2] if vv else g["shape"][2]
+
+    def fn(r, group):
+        dev = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        if vv:
+            k0, nloc = inputs.slab_extent(np_, r, P)
+            p = inputs.make_vv_problem(name, k0, nloc)
+            S = M.Solver(p.nr, p.nt, p.np, p.rf, p.tf, p.pf, chunk=16, loopback=(group, r))
+            S.vv_set_coefficients(dev(p.nu), dev(p.s))
+            S.vv_set_bc_r(p.wall_in, dev(p.g_in), p.wall_out, dev(p.g_out))
+            x = dev(p.x0)
+            st, info, hist = S.vv_solve(dev(p.f), x, p.tol, p.maxit, raise_on_error=False)
+        else:
+            p = inputs.make_problem(name, *inputs.slab_extent(np_, r, P))
+            S = M.solver_for_problem(p, chunk=16, loopback=(group, r))
+            x = dev(p.x0)
+            st, info, hist = S.solve(dev(p.f), x, p.tol, p.maxit, raise_on_error=False)
+        torch.cuda.current_stream().synchronize()
+        res = (st, info["iters"], hist, x.cpu().numpy())
+        S.close()
+        return res
+
+    _check_slabs_against_golden(g, _run_loopback(M, P, fn))
