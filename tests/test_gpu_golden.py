@@ -165,11 +165,12 @@ def _check_slabs_against_golden(g, res):
 
 
 @pytest.mark.timeout(1500)
-@pytest.mark.parametrize("name", ["c3", "c3v"])
+@pytest.mark.parametrize("name", ["c3", "c3v", "c3a"])
 def test_full_size_8_slabs_match_golden(M, name):
     """The bench workloads split into the 8 phi-slabs of the 8-GPU strong-scaling run (75 planes each), on 8 loopback
     ranks: every rank's history and the concatenated solution equal the single-rank oracle golden bit for bit (c3:
-    830 iterations, the scalar operator; c3v: 841, the vector operator with its pole-ring sums all-gathered)."""
+    830 iterations, the scalar operator; c3v: 841, the vector operator with its pole-ring sums all-gathered; c3a:
+    1,028, the field-aligned operator with the edge planes below each slab from the left rank)."""
     import torch
     g = json.load(open(os.path.join(HERE, "golden", f"{name}_full_solve.json")))
     P = 8
@@ -187,7 +188,8 @@ def test_full_size_8_slabs_match_golden(M, name):
             x = dev(p.x0)
             st, info, hist = S.vv_solve(dev(p.f), x, p.tol, p.maxit, raise_on_error=False)
         else:
-            p = inputs.make_problem(name, *inputs.slab_extent(np_, r, P))
+            mk = inputs.make_aniso_problem if name.endswith("a") else inputs.make_problem
+            p = mk(name, *inputs.slab_extent(np_, r, P))
             S = M.solver_for_problem(p, chunk=16, loopback=(group, r))
             x = dev(p.x0)
             st, info, hist = S.solve(dev(p.f), x, p.tol, p.maxit, raise_on_error=False)
