@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "aniso.cuh"
 #include "arith.cuh"
@@ -265,14 +266,15 @@ __device__ __forceinline__ double g_q(const Row4 &r) { return r.q; }
 __device__ __forceinline__ double g_x(const double2 &v) { return v.x; }
 __device__ __forceinline__ double g_y(const double2 &v) { return v.y; }
 
-template <bool WITH_DOT, bool EXACT, typename R4, typename R2>
+template <bool WITH_DOT, bool EXACT, bool JIN = false, typename R4, typename R2>
 __device__ __forceinline__ void aniso_pair(const Dims &d, const PairCoef &K, double *__restrict__ y, uint32_t c,
                                            int i0, int j, const R4 &Rj, const R4 &Rjm, const R4 &Rjp,
                                            const R4 &Mj, const R4 &Pj, const R2 &Mjm, const R2 &Mjp,
                                            const R2 &Pjm, const R2 &Pjp, Acc<EXACT> &dotacc) {
     using A = Ar<EXACT>;
     const int nr = d.nr, nt = d.nt;
-    const bool il = i0 > 0, ih = i0 + 2 < nr, jl = j > 0, jh = j < nt - 1;
+    // JIN: the caller guarantees 0 < j < nt - 1 (a tile strictly between the poles)
+    const bool il = i0 > 0, ih = i0 + 2 < nr, jl = JIN || j > 0, jh = JIN || j < nt - 1;
     // ---- the 7-point part, the oracle's order per cell
     const double2 tr = K.tr;
     const double tr2 = K.tr2;
@@ -685,81 +687,88 @@ __global__ void __launch_bounds__(kAM, 1) k_aniso_march(Dims d, DevArrays a, Ani
         double2 cTp = make_double2(0.0, 0.0), cXp = cTp, cXj = cTp, cXjp = cTp;
         double cXpq = 0.0;
         double2 Mjm2 = make_double2(0.0, 0.0), Mjp2 = Mjm2;   // plane s - 1, rows j -+ 1 (the previous step's)
-        for (int s = kb; s < ke; ++s) {
-            const uint32_t q = (uint32_t)(s - (kb - 1));
-            if (threadIdx.x == 0) {   // into the slots of plane s - 2 and stage s - 2 (free: barrier of step s - 1)
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                if (s + 2 <= ke) issue_p(s + 2, pb + q + 2);
-                if (s + 1 <= ke - 1) issue_c(s + 1, cb + q + 1);
-            }
-            const uint32_t ip = pb + q + 1, ic = cb + q;   // plane s + 1, stage s
-            mbar_wait_parity(&pbar[ip & 3u], (ip >> 2) & 1u);
-            mbar_wait_parity(&cbar[ic % 3u], (ic / 3u) & 1u);
-            if (act) {
-                const double *Pm = pring + (size_t)((ip - 2) & 3u) * M.pslot;   // plane s - 1
-                const double *P0 = pring + (size_t)((ip - 1) & 3u) * M.pslot;   // plane s
-                const double *P1 = pring + (size_t)(ip & 3u) * M.pslot;         // plane s + 1
-                const double *C = cring + (size_t)(ic % 3u) * M.cslot;           // stage s
-                const double *Cb = cring + (size_t)((ic + 2) % 3u) * M.cslot;    // stage s - 1: the faces of plane s
-                const int r = lr + 1;                                            // tile row of j
-                const int rm = jl ? r - 1 : r, rp = jh ? r + 1 : r;
-                auto row4 = [&](const double *P, int rr) {
-                    const double *w = P + (size_t)rr * nr + i0;
-                    const double2 v2 = *reinterpret_cast<const double2 *>(w);
-                    return Row4{w[-om], v2.x, v2.y, w[oq]};
-                };
-                auto pr2 = [&](const double *P, int rr) { return *reinterpret_cast<const double2 *>(P + (size_t)rr * nr + i0); };
-                const uint32_t o0 = (uint32_t)lr * nr + i0, o1 = (uint32_t)(jh ? lr + 1 : lr) * nr + i0;
-                auto c2 = [&](const double *base, uint32_t off) { return *reinterpret_cast<const double2 *>(base + off); };
-                PairCoef K;
-                K.tr = c2(C, o0);
-                K.tr2 = C[o0 + oq];
-                K.ttl = c2(C + oTt, o0);
-                K.tth = c2(C + oTt, o1);
-                if (s == kb) {
-                    cTp = c2(Cb + oTp, o0);
-                    cXp = c2(Cb + oXrp, o0);
-                    cXpq = Cb[oXrp + o0 + oq];
-                    cXj = c2(Cb + oXtp, o0);
-                    cXjp = c2(Cb + oXtp, o1);
+        // the step loop, compiled for interior tiles (every row strictly between the poles: no j-boundary
+        // predicates in aniso_pair) and generic for the first and last tiles
+        auto march = [&](auto interior) {
+            constexpr bool JIN = decltype(interior)::value;
+            for (int s = kb; s < ke; ++s) {
+                const uint32_t q = (uint32_t)(s - (kb - 1));
+                if (threadIdx.x == 0) {   // into the slots of plane s - 2 and stage s - 2 (free: barrier of step s - 1)
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (s + 2 <= ke) issue_p(s + 2, pb + q + 2);
+                    if (s + 1 <= ke - 1) issue_c(s + 1, cb + q + 1);
                 }
-                K.tpl = cTp;
-                K.tph = c2(C + oTp, o0);
-                K.d7 = c2(C + oD7, o0);
-                K.Xt0 = c2(C + oXrt, o0);
-                K.Xt1 = c2(C + oXrt, o1);
-                K.Xt0q = C[oXrt + o0 + oq];
-                K.Xt1q = C[oXrt + o1 + oq];
-                K.Xp0 = cXp;
-                K.Xp1 = c2(C + oXrp, o0);
-                K.Xp0q = cXpq;
-                K.Xp1q = C[oXrp + o0 + oq];
-                K.Xjl = cXj;
-                K.Xjpl = cXjp;
-                K.Xjh = c2(C + oXtp, o0);
-                K.Xjph = c2(C + oXtp, o1);
-                const uint32_t c = (uint32_t)((size_t)s * plane + (size_t)j * nr + i0);
-                if (s == kb) {
-                    Mj = row4(Pm, r);
-                    Rj = row4(P0, r);
-                    Mjm2 = pr2(Pm, rm);
-                    Mjp2 = pr2(Pm, rp);
+                const uint32_t ip = pb + q + 1, ic = cb + q;   // plane s + 1, stage s
+                mbar_wait_parity(&pbar[ip & 3u], (ip >> 2) & 1u);
+                mbar_wait_parity(&cbar[ic % 3u], (ic / 3u) & 1u);
+                if (act) {
+                    const double *Pm = pring + (size_t)((ip - 2) & 3u) * M.pslot;   // plane s - 1
+                    const double *P0 = pring + (size_t)((ip - 1) & 3u) * M.pslot;   // plane s
+                    const double *P1 = pring + (size_t)(ip & 3u) * M.pslot;         // plane s + 1
+                    const double *C = cring + (size_t)(ic % 3u) * M.cslot;           // stage s
+                    const double *Cb = cring + (size_t)((ic + 2) % 3u) * M.cslot;    // stage s - 1: the faces of plane s
+                    const int r = lr + 1;                                            // tile row of j
+                    const int rm = (JIN || jl) ? r - 1 : r, rp = (JIN || jh) ? r + 1 : r;
+                    auto row4 = [&](const double *P, int rr) {
+                        const double *w = P + (size_t)rr * nr + i0;
+                        const double2 v2 = *reinterpret_cast<const double2 *>(w);
+                        return Row4{w[-om], v2.x, v2.y, w[oq]};
+                    };
+                    auto pr2 = [&](const double *P, int rr) { return *reinterpret_cast<const double2 *>(P + (size_t)rr * nr + i0); };
+                    const uint32_t o0 = (uint32_t)lr * nr + i0, o1 = (uint32_t)((JIN || jh) ? lr + 1 : lr) * nr + i0;
+                    auto c2 = [&](const double *base, uint32_t off) { return *reinterpret_cast<const double2 *>(base + off); };
+                    PairCoef K;
+                    K.tr = c2(C, o0);
+                    K.tr2 = C[o0 + oq];
+                    K.ttl = c2(C + oTt, o0);
+                    K.tth = c2(C + oTt, o1);
+                    if (s == kb) {
+                        cTp = c2(Cb + oTp, o0);
+                        cXp = c2(Cb + oXrp, o0);
+                        cXpq = Cb[oXrp + o0 + oq];
+                        cXj = c2(Cb + oXtp, o0);
+                        cXjp = c2(Cb + oXtp, o1);
+                    }
+                    K.tpl = cTp;
+                    K.tph = c2(C + oTp, o0);
+                    K.d7 = c2(C + oD7, o0);
+                    K.Xt0 = c2(C + oXrt, o0);
+                    K.Xt1 = c2(C + oXrt, o1);
+                    K.Xt0q = C[oXrt + o0 + oq];
+                    K.Xt1q = C[oXrt + o1 + oq];
+                    K.Xp0 = cXp;
+                    K.Xp1 = c2(C + oXrp, o0);
+                    K.Xp0q = cXpq;
+                    K.Xp1q = C[oXrp + o0 + oq];
+                    K.Xjl = cXj;
+                    K.Xjpl = cXjp;
+                    K.Xjh = c2(C + oXtp, o0);
+                    K.Xjph = c2(C + oXtp, o1);
+                    const uint32_t c = (uint32_t)((size_t)s * plane + (size_t)j * nr + i0);
+                    if (s == kb) {
+                        Mj = row4(Pm, r);
+                        Rj = row4(P0, r);
+                        Mjm2 = pr2(Pm, rm);
+                        Mjp2 = pr2(Pm, rp);
+                    }
+                    const Row4 Pj = row4(P1, r), Rjm = row4(P0, rm), Rjp = row4(P0, rp);
+                    aniso_pair<WITH_DOT, EXACT, JIN>(d, K, y, c, i0, j, Rj, Rjm, Rjp, Mj, Pj, Mjm2, Mjp2, pr2(P1, rm),
+                                                pr2(P1, rp), dot[0]);
+                    Mjm2 = make_double2(Rjm.c0, Rjm.c1);
+                    Mjp2 = make_double2(Rjp.c0, Rjp.c1);
+                    Mj = Rj;
+                    Rj = Pj;
+                    cTp = K.tph;
+                    cXp = K.Xp1;
+                    cXpq = K.Xp1q;
+                    cXj = K.Xjh;
+                    cXjp = K.Xjph;
                 }
-                const Row4 Pj = row4(P1, r), Rjm = row4(P0, rm), Rjp = row4(P0, rp);
-                aniso_pair<WITH_DOT, EXACT>(d, K, y, c, i0, j, Rj, Rjm, Rjp, Mj, Pj, Mjm2, Mjp2, pr2(P1, rm),
-                                            pr2(P1, rp), dot[0]);
-                Mjm2 = make_double2(Rjm.c0, Rjm.c1);
-                Mjp2 = make_double2(Rjp.c0, Rjp.c1);
-                Mj = Rj;
-                Rj = Pj;
-                cTp = K.tph;
-                cXp = K.Xp1;
-                cXpq = K.Xp1q;
-                cXj = K.Xjh;
-                cXjp = K.Xjph;
+                __syncthreads();
             }
-            __syncthreads();
-        }
+        };
+        if (j0 >= 1 && j0 + tj <= nt - 1) march(std::true_type{});
+        else march(std::false_type{});
     }
     if (WITH_DOT) {
         Acc<EXACT> out[1];
